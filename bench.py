@@ -1,0 +1,403 @@
+#!/usr/bin/env python
+"""bench.py — MSPipe node-memory stage on B200: events/s + roofline.
+
+A *step* is one batch through the whole hot path (A1-A7):
+sample_batch + memory_fetch (prep of batch t+k) and memory_update +
+memory_writeback (commit of batch t), captured once per step as a CUDA graph
+and replayed.  Inputs are resident in HBM; L2 is flushed (a 256 MiB write)
+between timed steps, outside the timed events.  Default workload: the
+Wikipedia-shaped stream (BASELINE.json configs[1]) at its build staleness k=1.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config wiki] [--impl mspipe|reference]
+
+N > 1 (torchrun): each rank runs an independent replica of the stage on its
+own copy of the stream (the sharded-memory exchange is not in
+this build), value = events of all ranks / max-over-ranks time.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "memory-stage events/sec"
+UNIT = "events/s"
+FLUSH_BYTES = 256 << 20
+FP32_FMA_LANES_PER_SM = 128  # B200 SM: 4 SMSPs x 32 FP32 lanes (B200_PROFILING.md / guide unit counts)
+
+
+def _peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return dict(hbm_gbs=float(d.get("hbm_gbs", 6650.0)), bf16_tflops=float(d.get("bf16_tflops", 1590.0)),
+                    bf16_tflops_sustained=float(d.get("bf16_tflops_sustained", 1400.0)), source="measured")
+    return dict(hbm_gbs=6650.0, bf16_tflops=1590.0, bf16_tflops_sustained=1400.0, source="fallback")
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.path = os.path.join(ROOT, "gpurun_out", f"clocks_{os.getpid()}.csv")
+
+    def __enter__(self):
+        try:
+            os.makedirs(os.path.dirname(self.path), exist_ok=True)
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}",
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "100"], stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.f.close()
+
+    def summary(self):
+        if self.proc is None:
+            return None
+        rows = []
+        with open(self.path) as f:
+            for line in f:
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) >= 7:
+                    try:
+                        rows.append((float(parts[0]), float(parts[1]), parts[3:7]))
+                    except ValueError:
+                        pass
+        if not rows:
+            return None
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for _, _, r in rows for i, v in enumerate(r) if v.lower() == "active"})
+        return {"sm_mhz": statistics.median(r[0] for r in rows), "sm_max_mhz": max(r[1] for r in rows),
+                "reasons": reasons, "samples": len(rows)}
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def _unique_counts(src, dst, B):
+    """U per batch (host arithmetic on the inputs, for the algorithmic-bytes model)."""
+    out = []
+    for j0 in range(0, len(src), B):
+        out.append(len(np.unique(np.concatenate([src[j0:j0 + B], dst[j0:j0 + B]]))))
+    return np.array(out)
+
+
+def algorithmic(cfg, stage_cfg, U):
+    """Bytes (or FLOPs) each op must move per batch."""
+    B, F, M, He = cfg.batch, cfg.fanout, cfg.mem_dim, cfg.edge_dim
+    Dm = 2 * M + He
+    Dx = Dm + cfg.time_dim
+    stride = (Dm + 3) // 4 * 4
+    R = 3 * B
+    n_sub = R * (F + 1)
+    sample = R * (4 + 8 + 16 + F * 16 + F * 20 + 4 + (F + 1) * 4)
+    row = 4 * M + 8
+    fetch = n_sub * (4 + 2 * row) + (n_sub * 2 * (4 * stride + 8) if stage_cfg.fetch_mail else 0)
+    upd_bytes = 2 * B * 8 + U * (2 * 4 * M + 8 + 8 + 4 * He + 4 * M + 8 + 4 * stride + 8)
+    upd_flops = U * 2 * 3 * M * (Dx + M)
+    wb = U * (4 + 2 * (4 * M + 8 + 4 * stride))
+    return dict(sample=sample, fetch=fetch, update=upd_bytes, update_flops=upd_flops, writeback=wb)
+
+
+def run_mspipe(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2402_15113_b200 import MemoryStage, StageConfig, _C, build_tcsr, gamma_quantile
+    from synth import make_workload
+
+    ws, rank, local = _dist()
+    if ws > 1:
+        dist.init_process_group("nccl")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    w = make_workload(args.config, seed=args.seed)
+    cfg = w["cfg"]
+    k = cfg.staleness_k if args.k is None else args.k
+    mit = None
+    if cfg.mitigation and not args.no_mitigation:
+        mit = dict(lam=cfg.lam, gamma=gamma_quantile(cfg.num_nodes, w["src"], w["dst"], w["ts"], cfg.quantile_p),
+                   n_sim=cfg.n_sim)
+    sc = StageConfig(cfg.num_nodes, cfg.mem_dim, cfg.edge_dim, cfg.time_dim, cfg.fanout, cfg.batch, k,
+                     schedule=args.schedule, mitigation=mit, fetch_mail=args.fetch_mail)
+    g = build_tcsr(cfg.num_nodes, w["src"], w["dst"], w["ts"], dev)
+    nb = -(-len(w["src"]) // cfg.batch)
+    U_host = _unique_counts(w["src"], w["dst"], cfg.batch)
+    flush = torch.empty(FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
+
+    def make_stage(staged):
+        st = MemoryStage(sc, w["params"], g, dev)
+        if staged:
+            st.bind_host(w["src"], w["dst"], w["ts"], w["neg"], w["ef"])
+        else:
+            t = {kk: torch.from_numpy(w[kk]).to(dev) for kk in ("src", "dst", "ts", "neg", "ef")}
+            st.bind_resident(t["src"], t["dst"], t["ts"], t["neg"], t["ef"])
+        return st
+
+    def capture(st, timing):
+        s = torch.cuda.Stream(device=dev)
+        st.timing = {} if timing else None
+        graphs, marks = [], []
+        with torch.cuda.stream(s):
+            for ops in st.step_ops():
+                gr = torch.cuda.CUDAGraph()
+                before = {kk: len(v) for kk, v in (st.timing or {}).items()}
+                with torch.cuda.graph(gr, stream=s):
+                    st.run_ops(ops)
+                graphs.append(gr)
+                marks.append({kk: (before.get(kk, 0), len(v)) for kk, v in (st.timing or {}).items()})
+        st.memory.reset()
+        return graphs, marks, s
+
+    def timed_run(st, graphs, marks, s, W, K, profile=False):
+        """W warm-up + K timed steps (wrapping over epochs); returns per-step ms and per-op ms."""
+        step_ms, op_ms = [], {}
+        pending = []
+        total = W + K
+        with torch.cuda.stream(s):
+            for n in range(total):
+                t = n % nb
+                if t == 0 and n > 0:
+                    torch.cuda.synchronize()
+                    _collect(pending, step_ms, op_ms, st, marks)
+                    st.memory.reset()
+                if not profile:
+                    flush.fill_(float(n))
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record(s)
+                graphs[t].replay()
+                e1.record(s)
+                if n >= W:
+                    pending.append((t, e0, e1))
+            torch.cuda.synchronize()
+        _collect(pending, step_ms, op_ms, st, marks)
+        return step_ms, op_ms
+
+    def _collect(pending, step_ms, op_ms, st, marks):
+        for t, e0, e1 in pending:
+            step_ms.append(e0.elapsed_time(e1))
+            if st.timing:
+                for name in ("sample", "fetch", "update", "writeback"):
+                    a, b = marks[t].get(name, (0, 0))
+                    ends = st.timing.get(name + "_end", [])
+                    for q in range(a, b):
+                        op_ms.setdefault(name, []).append(st.timing[name][q].elapsed_time(ends[q]))
+        pending.clear()
+
+    W, K = args.warmup, args.steps
+    # ---- device-resident run (the `value`) ---------------------------------
+    st = make_stage(False)
+    graphs, marks, s = capture(st, timing=True)
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        step_ms, op_ms = timed_run(st, graphs, marks, s, W, K, profile=args.profile)
+    _C.check(s)
+    tot_ms = float(sum(step_ms))
+    if ws > 1:
+        tt = torch.tensor([tot_ms], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        tot_ms = float(tt.item())
+        dist.barrier()
+    timed_batches = [(W + q) % nb for q in range(K)]
+    events = sum(min(cfg.batch, len(w["src"]) - b * cfg.batch) for b in timed_batches)
+    value = ws * events / (tot_ms / 1e3)
+    del graphs
+    # ---- roofline of the dominant op ---------------------------------------
+    peaks = _peaks()
+    mean_U = float(np.mean(U_host[timed_batches]))
+    alg = algorithmic(cfg, sc, mean_U)
+    op_mean = {kk: float(np.mean(v)) for kk, v in op_ms.items() if v}
+    dom = max(op_mean, key=op_mean.get) if op_mean else "update"
+    clocks = clk.summary()
+    if dom == "update":
+        sm_clock = 1965.0
+        peak_alu = 148 * FP32_FMA_LANES_PER_SM * 2 * sm_clock * 1e6 / 1e12
+        ach = alg["update_flops"] / (op_mean[dom] / 1e3) / 1e12
+        roof = {"kernel": "k_gru_simt (+k_dedup) via mspipe_memory_update", "bound": "alu", "achieved": ach,
+                "peak": peak_alu, "unit": "TFLOP/s", "frac": ach / peak_alu,
+                "peak_source": "148 SMs x 128 FP32 lanes x 2 x 1965 MHz (guide unit counts, max clock)"}
+    else:
+        ach = alg[dom] / (op_mean[dom] / 1e3) / 1e9
+        roof = {"kernel": dom, "bound": "hbm", "achieved": ach, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                "frac": ach / peaks["hbm_gbs"], "peak_source": peaks["source"]}
+    roof["traffic"] = _ncu_traffic(args.config, dom)
+    roof["op_ms_mean"] = op_mean
+    roof["op_share"] = {kk: v / sum(op_mean.values()) for kk, v in op_mean.items()} if op_mean else None
+    roof["alg_bytes_per_launch"] = {kk: alg[kk] for kk in ("sample", "fetch", "update", "writeback")}
+    roof["gru_flops_per_launch"] = alg["update_flops"]
+    out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": K, "warmup": W,
+           "ms_per_step": tot_ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+           "dtype": "f32", "data": "synthetic",
+           "config": {"workload": args.config, "events": int(len(w["src"])), "num_nodes": cfg.num_nodes,
+                      "batch": cfg.batch, "staleness_k": k, "schedule": args.schedule, "fanout": cfg.fanout,
+                      "mem_dim": cfg.mem_dim, "edge_dim": cfg.edge_dim, "time_dim": cfg.time_dim,
+                      "mitigation": bool(mit), "fetch_mail": args.fetch_mail, "gru": "fp32-simt",
+                      "l2": "flushed (256 MiB write) between timed steps, outside the timed events",
+                      "parallelism": "single" if ws == 1 else f"replicas{ws}"},
+           "roofline": roof, "gpu_launches": _launches(st.step_ops(), timed_batches, bool(mit)), "clocks": clocks}
+    if args.profile:
+        if rank == 0:
+            print(json.dumps(out))
+        return
+    # ---- e2e: host buffers through the same C-ABI calls ---------------------
+    st2 = make_stage(True)
+    graphs2, marks2, s2 = capture(st2, timing=False)
+    if ws > 1:
+        dist.barrier()
+    step2, _ = timed_run(st2, graphs2, marks2, s2, W, K)
+    _C.check(s2)
+    tot2 = float(sum(step2))
+    if ws > 1:
+        tt = torch.tensor([tot2], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        tot2 = float(tt.item())
+    out["e2e"] = {"value": ws * events / (tot2 / 1e3), "unit": UNIT,
+                  "h2d_bytes_per_step": st2.h2d_bytes_per_batch(), "d2h_bytes_per_step": st2.d2h_bytes_per_batch(),
+                  "ms_per_step": tot2 / K}
+    del graphs2
+    # ---- CPU oracle beside it (rank 0, N = 1 only) ---------------------------
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        out["cpu_baseline"] = cpu_baseline(w, cfg, k, args.schedule, mit, args.cpu_events)
+    if rank == 0:
+        print(json.dumps(out))
+    if ws > 1:
+        dist.destroy_process_group()
+
+
+def _launches(steps, timed_batches, mit):
+    """Kernels of this library per timed step: prep = sampler + gather (+ mitigation),
+    commit = dedup + GRU + write-back."""
+    per = {"prep": 2 + (1 if mit else 0), "commit": 3}
+    return int(sum(per[op] for t in timed_batches for op, _ in steps[t]))
+
+
+def _ncu_traffic(config, dom):
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as f:
+        d = json.load(f)
+    return d.get(config, {}).get(dom)
+
+
+def cpu_baseline(w, cfg, k, schedule, mit, n_events):
+    import oracle
+    threads = len(os.sched_getaffinity(0))
+    oracle.set_threads(threads)
+    E = min(n_events, len(w["src"]))
+    sl = slice(0, E)
+    t0 = time.perf_counter()
+    oracle.run_stream(cfg.num_nodes, w["src"][sl], w["dst"][sl], w["ts"][sl], w["ef"][sl], w["params"], cfg.batch,
+                      k, schedule, mitigation=mit, fanout=cfg.fanout, neg=w["neg"][sl])
+    dt = time.perf_counter() - t0
+    return {"value": E / dt, "unit": UNIT, "cores": threads, "kind": "oracle",
+            "sample": f"first {E} events ({-(-E // cfg.batch)} batches) of the same stream, full per-batch path "
+                      f"(sampler, subgraph gather, dedup, {'mitigation, ' if mit else ''}message, f64 GRU, commit), "
+                      f"{dt:.1f} s"}
+
+
+def run_reference(args):
+    """The base contract's reference arm = the CPU oracle, as it stands."""
+    ws, rank, _ = _dist()
+    if rank != 0:
+        return
+    import oracle
+    from paper_2402_15113_b200.graph import gamma_quantile
+    from synth import make_workload
+    w = make_workload(args.config, seed=args.seed)
+    cfg = w["cfg"]
+    k = cfg.staleness_k if args.k is None else args.k
+    mit = None
+    if cfg.mitigation and not args.no_mitigation:
+        mit = dict(lam=cfg.lam, gamma=gamma_quantile(cfg.num_nodes, w["src"], w["dst"], w["ts"], cfg.quantile_p),
+                   n_sim=cfg.n_sim)
+    threads = len(os.sched_getaffinity(0))
+    oracle.set_threads(threads)
+    W, K = args.warmup, args.steps
+    nb = -(-len(w["src"]) // cfg.batch)
+    W = min(W, nb - 1)
+    K = min(K, nb - W)
+    E_w = min(W * cfg.batch, len(w["src"]))
+    E_t = min((W + K) * cfg.batch, len(w["src"]))
+
+    def timed(E):
+        sl = slice(0, E)
+        t0 = time.perf_counter()
+        oracle.run_stream(cfg.num_nodes, w["src"][sl], w["dst"][sl], w["ts"][sl], w["ef"][sl], w["params"],
+                          cfg.batch, k, args.schedule, mitigation=mit, fanout=cfg.fanout, neg=w["neg"][sl])
+        return time.perf_counter() - t0
+
+    t_w = timed(E_w) if E_w > 0 else 0.0
+    t_all = timed(E_t)
+    dt = max(t_all - t_w, 1e-9)
+    value = (E_t - E_w) / dt
+    out = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": K,
+           "warmup": W, "ms_per_step": 1e3 * dt / K, "higher_is_better": True, "scaling": "weak",
+           "vs_baseline": None, "dtype": "f64-accumulate/f32-state", "data": "synthetic",
+           "config": {"workload": args.config, "batch": cfg.batch, "staleness_k": k, "schedule": args.schedule,
+                      "fanout": cfg.fanout, "mem_dim": cfg.mem_dim, "edge_dim": cfg.edge_dim,
+                      "mitigation": bool(mit), "parallelism": "host cores"},
+           "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle",
+                            "sample": f"batches {W + 1}..{W + K} of the stream (after {W} untimed), full per-batch path"},
+           "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="mspipe", choices=["mspipe", "reference"])
+    ap.add_argument("--config", default="wiki")
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--k", type=int, default=None)
+    ap.add_argument("--schedule", default="exact", choices=["exact", "grouped"])
+    ap.add_argument("--fetch-mail", action="store_true")
+    ap.add_argument("--no-mitigation", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-events", type=int, default=157_474)
+    ap.add_argument("--profile", action="store_true", help="short run for ncu: no flush/e2e/cpu")
+    args = ap.parse_args()
+    if args.warmup < 3 and not args.profile:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_mspipe(args)
+
+
+if __name__ == "__main__":
+    main()

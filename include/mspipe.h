@@ -1,0 +1,243 @@
+/*
+ * mspipe.h — C ABI of the B200 (sm_100a) node-memory stage of MSPipe
+ * (arXiv 2402.15113).  Implemented by paper_2402_15113_b200/libmspipe.so.
+ *
+ * "P:Lnnn" cites /root/reference/PAPER.md line nnn, "S:Lnnn" SPEC.md, "Gnn"
+ * a reading of the paper listed in DESIGN.md §3.
+ *
+ * The per-batch stage (one "iteration" i, 1-based) is, in stream order:
+ *   mspipe_sample_batch / mspipe_sample_recent   A1  recent-𝒩 sampler
+ *   mspipe_memory_fetch                          A3  snapshot fetch (+A4 mitigation)
+ *   mspipe_memory_update                         A2+A5+A6 dedup, message, GRU
+ *   mspipe_memory_writeback                      A7  last-writer-wins commit
+ *
+ * Conventions (all entry points):
+ *  - Array pointers are DEVICE pointers (cudaMalloc / torch CUDA tensors) on
+ *    the current CUDA device unless marked [host].  The caller owns every
+ *    array; the library never frees caller memory.
+ *  - Every compute call is asynchronous on `stream` (a cudaStream_t passed as
+ *    void*; NULL = legacy default stream) and never synchronises the host.
+ *    Only *_create / *_destroy allocate or free (their own handle state).
+ *  - Host-checkable precondition failures return a negative status at once
+ *    and set mspipe_last_error().  Errors found on the device (an id outside
+ *    [0, num_nodes), ...) set a sticky device flag reported by
+ *    mspipe_check().  Nothing throws or aborts across the ABI.
+ *  - Node ids and event ids are int32; timestamps are float64 ("ticks");
+ *    memory and mail values are float32.  Row-major layouts throughout.
+ *  - Determinism: every output is a pure function of the inputs and of the
+ *    stream order of the calls (no dependence on atomic arrival order).
+ *  - One host thread per handle at a time.
+ */
+#ifndef MSPIPE_H_
+#define MSPIPE_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MSPIPE_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define MSPIPE_API __attribute__((visibility("default")))
+#else
+#define MSPIPE_API
+#endif
+
+typedef int32_t mspipe_status;
+enum {
+  MSPIPE_OK = 0,
+  MSPIPE_EINVAL = -1,      /* null pointer, negative size, bad dims / fanout / lambda */
+  MSPIPE_ERANGE = -2,      /* an id outside [0, num_nodes) (device-detected; via mspipe_check) */
+  MSPIPE_ESTALE = -3,      /* fetch would violate i-1-k <= committed <= i-1 */
+  MSPIPE_EORDER = -4,      /* commit_version != committed + 1 */
+  MSPIPE_EUNSUPPORTED = -5,/* valid request this build does not implement (reported, never faked) */
+  MSPIPE_ECUDA = -6,       /* a CUDA runtime error; text in mspipe_last_error() */
+  MSPIPE_ENCCL = -7        /* an NCCL error (world > 1) */
+};
+
+/* Device-flag bits reported by mspipe_check (OR-ed). */
+enum { MSPIPE_DEVERR_RANGE = 1, MSPIPE_DEVERR_CAPACITY = 2 };
+
+MSPIPE_API int32_t mspipe_abi_version(void);                  /* [host] == MSPIPE_ABI_VERSION */
+MSPIPE_API const char* mspipe_last_error(void);               /* [host] thread-local text of the last non-OK status */
+/* Synchronises `stream`, then returns MSPIPE_ERANGE if any kernel of this
+ * library raised the device flag since the last check (clearing it), else OK
+ * (or ECUDA on a pending CUDA error). */
+MSPIPE_API mspipe_status mspipe_check(void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Temporal CSR ("T-CSR"): per node, its incident events in stream order, so
+ * ts is non-decreasing inside a row and ties keep eid order.  A self-loop
+ * contributes one entry.  Read-only, caller-owned, device memory.
+ *   indptr [num_nodes+1] int64, nbr/eid [nnz] int32 (other endpoint, event id),
+ *   ts [nnz] float64.
+ * ------------------------------------------------------------------------- */
+typedef struct {
+  int64_t num_nodes, nnz;
+  const int64_t* indptr;
+  const int32_t* nbr;
+  const int32_t* eid;
+  const double* ts;
+} mspipe_tcsr;
+
+/* A1 — recent-𝒩 temporal neighbour sampler.  "We sampled the 10 most recent
+ * 1-hop neighbors", run on the GPU per local batch;
+ * S:L98-L106.  For root r with query time t_q it returns the
+ * min(fanout, #incident events with ts < t_q) most recent events, newest
+ * first (G15: strict <, ties by larger eid first).
+ *   roots [num_roots] int32, query_ts [num_roots] float64.
+ *   out_nbr/out_eid [num_roots, fanout] int32 (-1 pad), out_ts [.., fanout]
+ *   float64 (0 pad), out_dt [.., fanout] float32 = (float)(t_q - ts) (0 pad),
+ *   out_cnt [num_roots] int32.  out_sub_ids (nullable) [num_roots, fanout+1]
+ *   int32: the subgraph node list, column 0 = the root, then the neighbours
+ *   (-1 pad) — the MFG layout of 3B(𝒩+1) nodes per batch.
+ * Roots outside [0, num_nodes) yield an empty row and raise MSPIPE_DEVERR_RANGE. */
+MSPIPE_API mspipe_status mspipe_sample_recent(const mspipe_tcsr* g, const int32_t* roots,
+                                   const double* query_ts, int64_t num_roots, int32_t fanout,
+                                   int32_t* out_nbr, int32_t* out_eid, double* out_ts,
+                                   float* out_dt, int32_t* out_cnt, int32_t* out_sub_ids,
+                                   void* stream);
+
+/* A1 in batch form: the 3B roots of one batch are [src_0..src_{B-1},
+ * dst_0.., neg_0..] ("three nodes per sample ... source, destination and
+ * neg_sample"), each queried at its event's time ts_a.  Same outputs
+ * as mspipe_sample_recent with num_roots = 3 * num_events. */
+MSPIPE_API mspipe_status mspipe_sample_batch(const mspipe_tcsr* g, const int32_t* src, const int32_t* dst,
+                                  const int32_t* neg, const double* ts, int64_t num_events,
+                                  int32_t fanout, int32_t* out_nbr, int32_t* out_eid,
+                                  double* out_ts, float* out_dt, int32_t* out_cnt,
+                                  int32_t* out_sub_ids, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Node-memory state.  Tables are caller-owned device arrays:
+ *   mem [num_nodes, mem_dim] f32, mem_ts [num_nodes] f64,
+ *   mail [num_nodes, mail_stride] f32 (the first Dm = 2*mem_dim + edge_dim
+ *   columns are used, padding columns are copied verbatim), mail_ts [num_nodes] f64.
+ * mem_dim % 4 == 0 and mail_stride % 4 == 0 (16-byte row vectors).
+ * staleness_k is the build staleness k (= paper k - 1, G8): a fetch for
+ * iteration i is legal iff  i-1-k <= committed <= i-1  (Eq. 2, P:L196-L204;
+ * Alg. 1 gate "while i - i_upd > k_i: wait").
+ * world == 1 only in this build (world > 1 returns MSPIPE_EUNSUPPORTED).
+ * create allocates O(num_nodes) int32 scratch + an error flag on the current
+ * device; destroy frees them.
+ * ------------------------------------------------------------------------- */
+typedef struct mspipe_memory mspipe_memory;
+
+MSPIPE_API mspipe_status mspipe_memory_create(mspipe_memory** out, int64_t num_nodes, int32_t mem_dim,
+                                   int32_t edge_dim, int32_t staleness_k, float* mem,
+                                   double* mem_ts, float* mail, double* mail_ts,
+                                   int64_t mail_stride, int32_t rank, int32_t world,
+                                   const void* nccl_unique_id /* [host] 128 B, NULL iff world==1 */);
+MSPIPE_API mspipe_status mspipe_memory_destroy(mspipe_memory* st);
+MSPIPE_API int64_t mspipe_memory_committed(const mspipe_memory* st); /* [host] last enqueued commit version */
+/* [host] restart an epoch: committed := 0 (the caller re-zeroes the tables, G17). */
+MSPIPE_API mspipe_status mspipe_memory_reset(mspipe_memory* st);
+
+/* A4 — similarity-based staleness mitigation (MSPipe-S), applied "in the
+ * memory fetching stage".  Targets are the 2B update endpoints
+ * of the batch in root layout [src_0..src_{B-1}, dst_0..dst_{B-1}], target a
+ * queried at t* = ts[a mod B].  For target w (snapshot state S):
+ *   eligible iff t* - S.mem_ts[w] > gamma (G11);
+ *   N1 = distinct ids of sample(w, t*) minus w; every distinct u of
+ *   sample(x, t*) minus w, x in N1, scores c(u) += 1 ("count their common
+ *   neighbors", G9); active iff S.mem_ts[u] > S.mem_ts[w] and
+ *   t* - S.mem_ts[u] < gamma; Omega = first n_sim active u by
+ *   (c desc, S.mem_ts[u] desc, u asc) (G10);
+ *   out_h[w] = lambda*S.mem[w] + (1-lambda)*mean_{u in Omega} S.mem[u], or
+ *   S.mem[w] when not eligible or Omega is empty.
+ * out_h [2B, mem_dim] f32 (the GRU hidden input, G13); out_omega nullable
+ * [2B, n_sim] int32 (-1 pad); out_elig nullable [2B] uint8.
+ * 1 <= fanout <= 32, 0 <= n_sim <= 16, lambda in [0, 1]. */
+typedef struct {
+  float lambda;
+  double gamma;
+  int32_t n_sim;
+  int32_t fanout;
+  const mspipe_tcsr* g;
+  const int32_t* src;
+  const int32_t* dst;
+  const double* ts;
+  int64_t num_events;
+  float* out_h;
+  int32_t* out_omega;
+  uint8_t* out_elig;
+} mspipe_mitigation;
+
+/* A3 — fetch under the staleness bound.  Copies rows of the state as of the
+ * stream point of the call (which, by the ordering contract above, is the
+ * state after commits 1..committed) for `ids` into dense outputs:
+ *   out_mem [n, mem_dim], out_mem_ts [n]; out_mail [n, mail_stride] and
+ *   out_mail_ts [n] are optional (NULL = not fetched).  id -1 gives a zero
+ *   row and ts 0 (padding of the sampler's subgraph list).
+ * Then runs the optional mitigation on the same state.  *out_version [host]
+ * receives v(i) = committed.  Returns MSPIPE_ESTALE (and enqueues nothing) if
+ * the staleness gate fails. */
+MSPIPE_API mspipe_status mspipe_memory_fetch(mspipe_memory* st, int64_t iteration, const int32_t* ids,
+                                  int64_t n, float* out_mem, double* out_mem_ts, float* out_mail,
+                                  double* out_mail_ts, const mspipe_mitigation* mit,
+                                  int64_t* out_version, void* stream);
+
+/* GRU memory updater parameters, torch.nn.GRUCell layout, gates (r, z, n)
+ * (G5): w_ih [3M, Dx], w_hh [3M, M], b_ih [3M], b_hh [3M], time encoder
+ * enc_q = cos(fmaf(time_w[q], dt, time_b[q])) (G2), q < time_dim.
+ * Dx = 2M + edge_dim + time_dim.  create packs the weights once into the
+ * kernel layout (device memory owned by the handle). */
+enum { MSPIPE_FP32_SIMT = 0, MSPIPE_FP32_3XTF32 = 1, MSPIPE_BF16 = 2 };
+typedef struct mspipe_gru mspipe_gru;
+MSPIPE_API mspipe_status mspipe_gru_create(mspipe_gru** out, int32_t mem_dim, int32_t edge_dim,
+                                int32_t time_dim, int32_t precision, const float* w_ih,
+                                const float* w_hh, const float* b_ih, const float* b_hh,
+                                const float* time_w, const float* time_b, void* stream);
+MSPIPE_API mspipe_status mspipe_gru_destroy(mspipe_gru* p);
+
+/* A2 + A5 + A6 — one batch of num_events events (global eids are the
+ * caller's business; edge_feat holds this batch's rows [num_events, edge_dim]).
+ *   Pairs: event a gives p = 2a (node src_a, other dst_a) and p = 2a+1 (node
+ *   dst_a, other src_a); win(w) = max{p : node_p = w} (last event wins,
+ *   S:L186; G6); negatives are never written (G7).  U winners in win order:
+ *   out_nodes [<=2B] int32, out_winner [<=2B] int32 (pair index),
+ *   *out_num_unique (device int32) = U.
+ *   Snapshot rows in root layout: row r in [0, 2B) is [src_0..src_{B-1},
+ *   dst_0..dst_{B-1}][r] and lives at snap_mem + r*snap_step*mem_dim,
+ *   snap_mem_ts + r*snap_step (snap_step = fanout+1 when the rows come from a
+ *   subgraph fetch of mspipe_sample_*'s out_sub_ids, 1 for a dense fetch).
+ *   snap_h (nullable) [2B, mem_dim]: mitigated hidden input per row.
+ *   For winner w with pair p (event a, other o, t* = ts_a):
+ *     dt = (float)(t* - S.mem_ts[w]) (Δt, G4);
+ *     x = [S.mem[w] ‖ S.mem[o] ‖ edge_feat[a] ‖ cos(fmaf(ω, dt, φ))] (G1-G3);
+ *     h' = GRUCell(x, h) with h = snap_h or S.mem[w].
+ *   out_mem [<=2B, mem_dim] = h', out_ts [<=2B] = t*, out_mail
+ *   [<=2B, mail_stride] = x[0:Dm] (G14), all in winner order. */
+MSPIPE_API mspipe_status mspipe_memory_update(mspipe_memory* st, const mspipe_gru* gru, const int32_t* src,
+                                   const int32_t* dst, const double* ts, int64_t num_events,
+                                   const float* edge_feat, const float* snap_mem,
+                                   const double* snap_mem_ts, int64_t snap_step,
+                                   const float* snap_h, int32_t* out_nodes, int32_t* out_winner,
+                                   int32_t* out_num_unique, float* out_mem, double* out_ts,
+                                   float* out_mail, void* stream);
+
+/* A7 — last-writer-wins write-back, committing version `commit_version`
+ * (must equal committed + 1, else MSPIPE_EORDER): for u < *num_unique,
+ *   mem[nodes[u]] = new_mem[u], mem_ts[nodes[u]] = new_ts[u],
+ *   mail[nodes[u]] = new_mail[u] (mail_stride row), mail_ts[nodes[u]] = new_ts[u]
+ * ("written back to the node memory storage"; i_upd <- i,
+ * P:L855).  nodes must be unique (as produced by mspipe_memory_update);
+ * max_n bounds *num_unique (grid sizing). */
+MSPIPE_API mspipe_status mspipe_memory_writeback(mspipe_memory* st, int64_t commit_version,
+                                      const int32_t* nodes, const int32_t* num_unique,
+                                      int64_t max_n, const float* new_mem, const double* new_ts,
+                                      const float* new_mail, void* stream);
+
+/* Utility (timing): record `event` (a cudaEvent_t) on `stream` with
+ * cudaEventRecordExternal, so that under stream capture it becomes an
+ * event-record node of the graph and can still be used for elapsed-time
+ * measurement of the captured kernels. */
+MSPIPE_API mspipe_status mspipe_util_event_record(void* event, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MSPIPE_H_ */

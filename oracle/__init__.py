@@ -53,7 +53,7 @@ def lib():
         L.orc_snapshot_version.argtypes = [i64, i32, i32]
         L.orc_snapshot_version.restype = i64
         L.orc_run_stream.argtypes = [i64, i64, P, P, P, P, i32, i32, i32, P, P, P, P, P, P, i64,
-                                     i32, i32, i32, f32, f64, i32, i32, P, P, P, P, i64, P]
+                                     i32, i32, i32, f32, f64, i32, i32, P, P, P, P, i64, P, P, i32]
         L.orc_run_stream.restype = i64
         L.orc_delta_t_population.argtypes = [i64, i64, P, P, P, P]
         L.orc_delta_t_population.restype = i64
@@ -191,8 +191,11 @@ def new_state(num_nodes, mem_dim, edge_dim):
 
 
 def run_stream(num_nodes, src, dst, ts, ef, params, batch, k, schedule="exact", mitigation=None,
-               fanout=10, state=None, max_batches=-1):
-    """C.2 O1-O8 over the stream; returns (final state, per-batch versions)."""
+               fanout=10, state=None, max_batches=-1, neg=None):
+    """C.2 O1-O8 over the stream; returns (final state, per-batch versions).
+    With `neg`, every batch also runs A1 on its 3B roots and gathers the
+    snapshot rows of the subgraph (the whole per-batch path, for timing)."""
+    negc = None if neg is None else _c(neg, np.int32)
     src, dst, ts = _c(src, np.int32), _c(dst, np.int32), _c(ts, np.float64)
     ef = _c(ef, np.float32)
     He = ef.shape[1]
@@ -211,7 +214,8 @@ def run_stream(num_nodes, src, dst, ts, ef, params, batch, k, schedule="exact", 
         _p(pr["w_hh"]), _p(pr["b_ih"]), _p(pr["b_hh"]), _p(pr["time_w"]), _p(pr["time_b"]), batch,
         k, 1 if schedule == "grouped" else 0, 1 if mit else 0, float(mit["lam"]) if mit else 1.0,
         float(mit["gamma"]) if mit else 0.0, int(mit["n_sim"]) if mit else 5, fanout,
-        _p(st["mem"]), _p(st["mem_ts"]), _p(st["mail"]), _p(st["mail_ts"]), max_batches, _p(vers))
+        _p(st["mem"]), _p(st["mem_ts"]), _p(st["mail"]), _p(st["mail_ts"]), max_batches, _p(vers),
+        _p(negc), 0 if negc is None else 1)
     if r < 0:
         raise ValueError(f"orc_run_stream rc={r}")
     return st, vers[:r]

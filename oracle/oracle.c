@@ -451,12 +451,32 @@ int64_t orc_run_stream(int64_t N, int64_t E, const int32_t* src, const int32_t* 
                        const float* b_hh, const float* time_w, const float* time_b, int64_t B,
                        int32_t k, int32_t schedule, int32_t mit_on, float lambda, double gamma,
                        int32_t n_sim, int32_t fanout, float* mem, double* mem_ts, float* mail,
-                       double* mail_ts, int64_t max_batches, int64_t* out_versions) {
+                       double* mail_ts, int64_t max_batches, int64_t* out_versions,
+                       const int32_t* neg, int32_t subgraph) {
   if (B < 1 || k < 0 || M < 1) return ORC_EINVAL;
+  if (subgraph && !neg) return ORC_EINVAL;
   const int32_t Dm = 2 * M + He;
   int64_t nb = (E + B - 1) / B;
   if (max_batches >= 0 && max_batches < nb) nb = max_batches;
-  orc_graph* g = mit_on ? orc_graph_create(N, E, src, dst, ts) : NULL;
+  orc_graph* g = (mit_on || subgraph) ? orc_graph_create(N, E, src, dst, ts) : NULL;
+  /* optional A1 + A3s: sample the 3B roots [src, dst, neg] at their event
+   * times and copy the snapshot rows of the 3B(𝒩+1) subgraph nodes (P:L818,
+   * P:L1153) — not needed for the state, done so the timed CPU baseline runs
+   * every step of the per-batch path. */
+  int64_t R3 = 3 * B;
+  int32_t* sroots = NULL; double* sq = NULL; int32_t *snbr = NULL, *seid = NULL, *scnt = NULL;
+  double* sts = NULL; float* sdt = NULL; float* smem = NULL; double* smts = NULL;
+  if (subgraph) {
+    sroots = (int32_t*)malloc(sizeof(int32_t) * R3);
+    sq = (double*)malloc(sizeof(double) * R3);
+    snbr = (int32_t*)malloc(sizeof(int32_t) * R3 * fanout);
+    seid = (int32_t*)malloc(sizeof(int32_t) * R3 * fanout);
+    sts = (double*)malloc(sizeof(double) * R3 * fanout);
+    sdt = (float*)malloc(sizeof(float) * R3 * fanout);
+    scnt = (int32_t*)malloc(sizeof(int32_t) * R3);
+    smem = (float*)malloc(sizeof(float) * R3 * (fanout + 1) * M);
+    smts = (double*)malloc(sizeof(double) * R3 * (fanout + 1));
+  }
   int32_t R = k + 1;
   size_t szm = sizeof(float) * (size_t)N * M, szt = sizeof(double) * (size_t)N;
   float** rmem = (float**)malloc(sizeof(float*) * R);
@@ -477,6 +497,31 @@ int64_t orc_run_stream(int64_t N, int64_t E, const int32_t* src, const int32_t* 
     if (out_versions) out_versions[i - 1] = v;
     int64_t j0 = (i - 1) * B;
     int64_t nb_ev = (j0 + B <= E) ? B : E - j0;
+    if (subgraph) {
+      const float* Sm = rmem[v % R];
+      const double* St = rts[v % R];
+      for (int64_t a = 0; a < nb_ev; ++a) {
+        sroots[a] = src[j0 + a];
+        sroots[nb_ev + a] = dst[j0 + a];
+        sroots[2 * nb_ev + a] = neg[j0 + a];
+        sq[a] = sq[nb_ev + a] = sq[2 * nb_ev + a] = ts[j0 + a];
+      }
+      orc_sample(g, 3 * nb_ev, sroots, sq, fanout, snbr, seid, sts, sdt, scnt);
+#pragma omp parallel for schedule(static)
+      for (int64_t r = 0; r < 3 * nb_ev; ++r) {
+        for (int32_t c = 0; c <= fanout; ++c) {
+          int32_t id = (c == 0) ? sroots[r] : snbr[r * fanout + c - 1];
+          float* dstrow = smem + (r * (fanout + 1) + c) * M;
+          if (id >= 0) {
+            memcpy(dstrow, Sm + (int64_t)id * M, sizeof(float) * M);
+            smts[r * (fanout + 1) + c] = St[id];
+          } else {
+            memset(dstrow, 0, sizeof(float) * M);
+            smts[r * (fanout + 1) + c] = 0.0;
+          }
+        }
+      }
+    }
     int64_t U = orc_memory_update(N, nb_ev, src + j0, dst + j0, ts + j0, ef + j0 * He, M, He,
                                   Dt, w_ih, w_hh, b_ih, b_hh, time_w, time_b, rmem[v % R],
                                   rts[v % R], mit_on, g, lambda, gamma, n_sim, fanout, nodes,
@@ -502,6 +547,9 @@ int64_t orc_run_stream(int64_t N, int64_t E, const int32_t* src, const int32_t* 
   free(nmem);
   free(nts);
   free(nmail);
+  if (subgraph) {
+    free(sroots); free(sq); free(snbr); free(seid); free(sts); free(sdt); free(scnt); free(smem); free(smts);
+  }
   orc_graph_free(g);
   return nb;
 }

@@ -1,0 +1,242 @@
+"""Thin ctypes binding of include/mspipe.h (libmspipe.so).  Argument marshalling
+only: every step of the stage runs in the library's sm_100a kernels.  There
+is no CPU fallback — a missing library or a non-CUDA tensor raises.
+
+Names mirror the C entry points without the ``mspipe_`` prefix.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libmspipe.so")
+
+OK, EINVAL, ERANGE, ESTALE, EORDER, EUNSUPPORTED, ECUDA, ENCCL = 0, -1, -2, -3, -4, -5, -6, -7
+FP32_SIMT, FP32_3XTF32, BF16 = 0, 1, 2
+ABI_VERSION = 1
+
+P = C.c_void_p
+i32, i64, f32, f64 = C.c_int32, C.c_int64, C.c_float, C.c_double
+
+EXPORTS = ("mspipe_abi_version", "mspipe_last_error", "mspipe_check", "mspipe_sample_recent",
+           "mspipe_sample_batch", "mspipe_memory_create", "mspipe_memory_destroy",
+           "mspipe_memory_committed", "mspipe_memory_reset", "mspipe_memory_fetch",
+           "mspipe_gru_create", "mspipe_gru_destroy", "mspipe_memory_update",
+           "mspipe_memory_writeback", "mspipe_util_event_record")
+
+
+class MspipeError(RuntimeError):
+    def __init__(self, status, where, text):
+        super().__init__(f"{where}: status {status}: {text}")
+        self.status = status
+
+
+class Tcsr(C.Structure):
+    _fields_ = [("num_nodes", i64), ("nnz", i64), ("indptr", P), ("nbr", P), ("eid", P), ("ts", P)]
+
+
+class Mitigation(C.Structure):
+    _fields_ = [("lam", f32), ("gamma", f64), ("n_sim", i32), ("fanout", i32), ("g", C.POINTER(Tcsr)),
+                ("src", P), ("dst", P), ("ts", P), ("num_events", i64), ("out_h", P), ("out_omega", P),
+                ("out_elig", P)]
+
+
+_lib = None
+
+
+def lib():
+    """Load libmspipe.so (built by paper_2402_15113_b200.build.build())."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; g.build()'` "
+                               "(nvcc, sm_100a). There is no CPU fallback.")
+        L = C.CDLL(LIB_PATH)
+        L.mspipe_abi_version.restype = i32
+        L.mspipe_last_error.restype = C.c_char_p
+        L.mspipe_check.argtypes = [P]
+        L.mspipe_sample_recent.argtypes = [C.POINTER(Tcsr), P, P, i64, i32, P, P, P, P, P, P, P]
+        L.mspipe_sample_batch.argtypes = [C.POINTER(Tcsr), P, P, P, P, i64, i32, P, P, P, P, P, P, P]
+        L.mspipe_memory_create.argtypes = [C.POINTER(P), i64, i32, i32, i32, P, P, P, P, i64, i32, i32, P]
+        L.mspipe_memory_destroy.argtypes = [P]
+        L.mspipe_memory_committed.argtypes = [P]
+        L.mspipe_memory_committed.restype = i64
+        L.mspipe_memory_reset.argtypes = [P]
+        L.mspipe_memory_fetch.argtypes = [P, i64, P, i64, P, P, P, P, C.POINTER(Mitigation),
+                                          C.POINTER(i64), P]
+        L.mspipe_gru_create.argtypes = [C.POINTER(P), i32, i32, i32, i32, P, P, P, P, P, P, P]
+        L.mspipe_gru_destroy.argtypes = [P]
+        L.mspipe_memory_update.argtypes = [P, P, P, P, P, i64, P, P, P, i64, P, P, P, P, P, P, P, P]
+        L.mspipe_memory_writeback.argtypes = [P, i64, P, P, i64, P, P, P, P]
+        L.mspipe_util_event_record.argtypes = [P, P]
+        if L.mspipe_abi_version() != ABI_VERSION:
+            raise RuntimeError(f"libmspipe ABI {L.mspipe_abi_version()} != binding {ABI_VERSION}")
+        _lib = L
+    return _lib
+
+
+def _ck(status, where):
+    if status != OK:
+        raise MspipeError(status, where, lib().mspipe_last_error().decode(errors="replace"))
+
+
+def ptr(t):
+    """Device pointer of a CUDA tensor (None -> NULL).  Refuses host tensors."""
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise ValueError("libmspipe takes CUDA tensors (no CPU fallback)")
+    if not t.is_contiguous():
+        raise ValueError("libmspipe takes contiguous tensors")
+    return C.c_void_p(t.data_ptr())
+
+
+def stream_ptr(stream=None):
+    s = torch.cuda.current_stream() if stream is None else stream
+    return C.c_void_p(s.cuda_stream)
+
+
+def check(stream=None):
+    _ck(lib().mspipe_check(stream_ptr(stream)), "mspipe_check")
+
+
+def last_error() -> str:
+    return lib().mspipe_last_error().decode(errors="replace")
+
+
+def event_record(event: torch.cuda.Event, stream=None):
+    """Record a timing event so that it is also captured as a graph node."""
+    _ck(lib().mspipe_util_event_record(C.c_void_p(event.cuda_event), stream_ptr(stream)), "event_record")
+
+
+def sample_recent(g: "TcsrHandle", roots, query_ts, fanout, out, stream=None):
+    _ck(lib().mspipe_sample_recent(C.byref(g.c), ptr(roots), ptr(query_ts), roots.numel(), fanout,
+                                   ptr(out["nbr"]), ptr(out["eid"]), ptr(out["ts"]), ptr(out["dt"]),
+                                   ptr(out["cnt"]), ptr(out.get("sub")), stream_ptr(stream)), "mspipe_sample_recent")
+    return out
+
+
+def sample_batch(g: "TcsrHandle", src, dst, neg, ts, fanout, out, stream=None):
+    _ck(lib().mspipe_sample_batch(C.byref(g.c), ptr(src), ptr(dst), ptr(neg), ptr(ts), src.numel(), fanout,
+                                  ptr(out["nbr"]), ptr(out["eid"]), ptr(out["ts"]), ptr(out["dt"]),
+                                  ptr(out["cnt"]), ptr(out.get("sub")), stream_ptr(stream)), "mspipe_sample_batch")
+    return out
+
+
+def alloc_sample(num_roots, fanout, device, sub=True):
+    d = dict(nbr=torch.empty((num_roots, fanout), dtype=torch.int32, device=device),
+             eid=torch.empty((num_roots, fanout), dtype=torch.int32, device=device),
+             ts=torch.empty((num_roots, fanout), dtype=torch.float64, device=device),
+             dt=torch.empty((num_roots, fanout), dtype=torch.float32, device=device),
+             cnt=torch.empty((num_roots,), dtype=torch.int32, device=device))
+    if sub:
+        d["sub"] = torch.empty((num_roots, fanout + 1), dtype=torch.int32, device=device)
+    return d
+
+
+class TcsrHandle:
+    """Device-resident T-CSR (caller-owned tensors + the C struct pointing at them)."""
+
+    def __init__(self, num_nodes, indptr, nbr, eid, ts):
+        self.indptr, self.nbr, self.eid, self.ts = indptr, nbr, eid, ts
+        self.c = Tcsr(int(num_nodes), int(nbr.numel()), ptr(indptr), ptr(nbr), ptr(eid), ptr(ts))
+
+
+class GruHandle:
+    def __init__(self, mem_dim, edge_dim, time_dim, params: dict, device, precision=FP32_SIMT, stream=None):
+        self.dims = (mem_dim, edge_dim, time_dim)
+        self.w = {k: torch.as_tensor(v, dtype=torch.float32).contiguous().to(device) for k, v in params.items()}
+        h = C.c_void_p()
+        _ck(lib().mspipe_gru_create(C.byref(h), mem_dim, edge_dim, time_dim, precision, ptr(self.w["w_ih"]),
+                                    ptr(self.w["w_hh"]), ptr(self.w["b_ih"]), ptr(self.w["b_hh"]),
+                                    ptr(self.w["time_w"]), ptr(self.w["time_b"]), stream_ptr(stream)),
+            "mspipe_gru_create")
+        self.h = h
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.mspipe_gru_destroy(self.h)
+            self.h = None
+
+
+def mail_stride_for(mem_dim, edge_dim):
+    Dm = 2 * mem_dim + edge_dim
+    return (Dm + 3) // 4 * 4
+
+
+class MemoryHandle:
+    """mspipe_memory over caller-owned (here: this object's) state tables."""
+
+    def __init__(self, num_nodes, mem_dim, edge_dim, staleness_k, device, rank=0, world=1, nccl_id=None):
+        self.num_nodes, self.mem_dim, self.edge_dim, self.k = num_nodes, mem_dim, edge_dim, staleness_k
+        self.mail_stride = mail_stride_for(mem_dim, edge_dim)
+        self.mem = torch.zeros((num_nodes, mem_dim), dtype=torch.float32, device=device)
+        self.mem_ts = torch.zeros((num_nodes,), dtype=torch.float64, device=device)
+        self.mail = torch.zeros((num_nodes, self.mail_stride), dtype=torch.float32, device=device)
+        self.mail_ts = torch.zeros((num_nodes,), dtype=torch.float64, device=device)
+        h = C.c_void_p()
+        _ck(lib().mspipe_memory_create(C.byref(h), num_nodes, mem_dim, edge_dim, staleness_k, ptr(self.mem),
+                                       ptr(self.mem_ts), ptr(self.mail), ptr(self.mail_ts), self.mail_stride,
+                                       rank, world, nccl_id), "mspipe_memory_create")
+        self.h = h
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.mspipe_memory_destroy(self.h)
+            self.h = None
+
+    @property
+    def committed(self):
+        return int(lib().mspipe_memory_committed(self.h))
+
+    def reset(self, zero_tables=True):
+        """New epoch: committed := 0; tables back to S_0 = 0 (G17)."""
+        if zero_tables:
+            for t in (self.mem, self.mem_ts, self.mail, self.mail_ts):
+                t.zero_()
+        _ck(lib().mspipe_memory_reset(self.h), "mspipe_memory_reset")
+
+
+def memory_fetch(st: MemoryHandle, iteration, ids, out_mem, out_mem_ts, out_mail=None, out_mail_ts=None,
+                 mitigation: Mitigation | None = None, stream=None) -> int:
+    v = i64(-1)
+    _ck(lib().mspipe_memory_fetch(st.h, int(iteration), ptr(ids), ids.numel(), ptr(out_mem), ptr(out_mem_ts),
+                                  ptr(out_mail), ptr(out_mail_ts),
+                                  C.byref(mitigation) if mitigation is not None else None, C.byref(v),
+                                  stream_ptr(stream)), "mspipe_memory_fetch")
+    return int(v.value)
+
+
+def make_mitigation(g: TcsrHandle, lam, gamma, n_sim, fanout, src, dst, ts, out_h, out_omega=None, out_elig=None):
+    m = Mitigation(float(lam), float(gamma), int(n_sim), int(fanout), C.pointer(g.c), ptr(src), ptr(dst), ptr(ts),
+                   src.numel(), ptr(out_h), ptr(out_omega), ptr(out_elig))
+    m._keep = (g, src, dst, ts, out_h, out_omega, out_elig)
+    return m
+
+
+def memory_update(st: MemoryHandle, gru: GruHandle, src, dst, ts, edge_feat, snap_mem, snap_mem_ts, snap_step,
+                  out, snap_h=None, stream=None):
+    _ck(lib().mspipe_memory_update(st.h, gru.h, ptr(src), ptr(dst), ptr(ts), src.numel(), ptr(edge_feat),
+                                   ptr(snap_mem), ptr(snap_mem_ts), int(snap_step), ptr(snap_h), ptr(out["nodes"]),
+                                   ptr(out["winner"]), ptr(out["num"]), ptr(out["mem"]), ptr(out["ts"]),
+                                   ptr(out["mail"]), stream_ptr(stream)), "mspipe_memory_update")
+    return out
+
+
+def alloc_update(num_events, mem_dim, mail_stride, device):
+    n = 2 * num_events
+    return dict(nodes=torch.empty((n,), dtype=torch.int32, device=device),
+                winner=torch.empty((n,), dtype=torch.int32, device=device),
+                num=torch.zeros((1,), dtype=torch.int32, device=device),
+                mem=torch.empty((n, mem_dim), dtype=torch.float32, device=device),
+                ts=torch.empty((n,), dtype=torch.float64, device=device),
+                mail=torch.empty((n, mail_stride), dtype=torch.float32, device=device))
+
+
+def memory_writeback(st: MemoryHandle, commit_version, upd, stream=None):
+    _ck(lib().mspipe_memory_writeback(st.h, int(commit_version), ptr(upd["nodes"]), ptr(upd["num"]),
+                                      upd["nodes"].numel(), ptr(upd["mem"]), ptr(upd["ts"]), ptr(upd["mail"]),
+                                      stream_ptr(stream)), "mspipe_memory_writeback")

@@ -1,0 +1,288 @@
+// api.cu — the extern "C" entry points of include/mspipe.h: argument checks,
+// handle state, the staleness gate, and dispatch to the kernels.
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include "internal.cuh"
+
+namespace mspipe {
+
+__device__ int g_dev_err = 0;
+
+static thread_local char t_last_error[512] = "";
+
+mspipe_status fail(mspipe_status s, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(t_last_error, sizeof(t_last_error), fmt, ap);
+  va_end(ap);
+  return s;
+}
+
+mspipe_status cuda_status(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return MSPIPE_OK;
+  return fail(MSPIPE_ECUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+static mspipe_status after_launch(const char* what) {
+  return cuda_status(cudaGetLastError(), what);
+}
+
+static bool tcsr_ok(const mspipe_tcsr* g) {
+  return g && g->num_nodes >= 0 && g->nnz >= 0 && g->indptr && (g->nnz == 0 || (g->nbr && g->eid && g->ts));
+}
+
+}  // namespace mspipe
+
+using namespace mspipe;
+
+extern "C" {
+
+int32_t mspipe_abi_version(void) { return MSPIPE_ABI_VERSION; }
+
+const char* mspipe_last_error(void) { return t_last_error; }
+
+mspipe_status mspipe_check(void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return cuda_status(e, "mspipe_check: stream");
+  int h = 0;
+  e = cudaMemcpyFromSymbol(&h, g_dev_err, sizeof(int));
+  if (e != cudaSuccess) return cuda_status(e, "mspipe_check: flag read");
+  if (h != 0) {
+    int z = 0;
+    cudaMemcpyToSymbol(g_dev_err, &z, sizeof(int));
+    return fail(MSPIPE_ERANGE, "device error flag 0x%x (1=id out of range, 2=capacity)", h);
+  }
+  return MSPIPE_OK;
+}
+
+mspipe_status mspipe_sample_recent(const mspipe_tcsr* g, const int32_t* roots,
+                                   const double* query_ts, int64_t num_roots, int32_t fanout,
+                                   int32_t* out_nbr, int32_t* out_eid, double* out_ts,
+                                   float* out_dt, int32_t* out_cnt, int32_t* out_sub_ids,
+                                   void* stream) {
+  if (!tcsr_ok(g)) return fail(MSPIPE_EINVAL, "sample_recent: bad T-CSR");
+  if (num_roots < 0 || fanout < 1 || fanout > 64) return fail(MSPIPE_EINVAL, "sample_recent: num_roots=%lld fanout=%d", (long long)num_roots, fanout);
+  if (num_roots == 0) return MSPIPE_OK;
+  if (!roots || !query_ts || !out_nbr || !out_eid || !out_ts || !out_dt || !out_cnt)
+    return fail(MSPIPE_EINVAL, "sample_recent: null output/input");
+  launch_sample(to_tcsr(g), roots, query_ts, nullptr, nullptr, nullptr, nullptr, 0, num_roots,
+                fanout, out_nbr, out_eid, out_ts, out_dt, out_cnt, out_sub_ids, (cudaStream_t)stream);
+  return after_launch("sample_recent");
+}
+
+mspipe_status mspipe_sample_batch(const mspipe_tcsr* g, const int32_t* src, const int32_t* dst,
+                                  const int32_t* neg, const double* ts, int64_t num_events,
+                                  int32_t fanout, int32_t* out_nbr, int32_t* out_eid,
+                                  double* out_ts, float* out_dt, int32_t* out_cnt,
+                                  int32_t* out_sub_ids, void* stream) {
+  if (!tcsr_ok(g)) return fail(MSPIPE_EINVAL, "sample_batch: bad T-CSR");
+  if (num_events < 0 || fanout < 1 || fanout > 64) return fail(MSPIPE_EINVAL, "sample_batch: num_events=%lld fanout=%d", (long long)num_events, fanout);
+  if (num_events == 0) return MSPIPE_OK;
+  if (!src || !dst || !neg || !ts || !out_nbr || !out_eid || !out_ts || !out_dt || !out_cnt)
+    return fail(MSPIPE_EINVAL, "sample_batch: null output/input");
+  launch_sample(to_tcsr(g), nullptr, nullptr, src, dst, neg, ts, num_events, 3 * num_events, fanout,
+                out_nbr, out_eid, out_ts, out_dt, out_cnt, out_sub_ids, (cudaStream_t)stream);
+  return after_launch("sample_batch");
+}
+
+mspipe_status mspipe_memory_create(mspipe_memory** out, int64_t num_nodes, int32_t mem_dim,
+                                   int32_t edge_dim, int32_t staleness_k, float* mem,
+                                   double* mem_ts, float* mail, double* mail_ts,
+                                   int64_t mail_stride, int32_t rank, int32_t world,
+                                   const void* nccl_unique_id) {
+  if (!out) return fail(MSPIPE_EINVAL, "memory_create: out is NULL");
+  *out = nullptr;
+  if (num_nodes < 1 || num_nodes > INT32_MAX || mem_dim < 4 || mem_dim % 4 || edge_dim < 0 || staleness_k < 0)
+    return fail(MSPIPE_EINVAL, "memory_create: num_nodes=%lld mem_dim=%d (multiple of 4) edge_dim=%d k=%d",
+                (long long)num_nodes, mem_dim, edge_dim, staleness_k);
+  int32_t Dm = 2 * mem_dim + edge_dim;
+  if (mail_stride < Dm || mail_stride % 4) return fail(MSPIPE_EINVAL, "memory_create: mail_stride=%lld must be >= %d and a multiple of 4", (long long)mail_stride, Dm);
+  if (!mem || !mem_ts || !mail || !mail_ts) return fail(MSPIPE_EINVAL, "memory_create: null table");
+  if (world != 1 || rank != 0)
+    return fail(MSPIPE_EUNSUPPORTED, "memory_create: world=%d: sharded memory is not in this build", world);
+  (void)nccl_unique_id;
+  (void)num_sms();  // cache the SM count now: later calls may run under stream capture
+  mspipe_memory* st = new mspipe_memory();
+  st->num_nodes = num_nodes;
+  st->mem_dim = mem_dim;
+  st->edge_dim = edge_dim;
+  st->mail_dim = Dm;
+  st->k = staleness_k;
+  st->mem = mem;
+  st->mem_ts = mem_ts;
+  st->mail = mail;
+  st->mail_ts = mail_ts;
+  st->mail_stride = mail_stride;
+  st->rank = rank;
+  st->world = world;
+  st->committed = 0;
+  cudaGetDevice(&st->device);
+  cudaError_t e = cudaMalloc(&st->scratch, sizeof(int32_t) * (size_t)num_nodes);
+  if (e == cudaSuccess) e = cudaMemset(st->scratch, 0xFF, sizeof(int32_t) * (size_t)num_nodes);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) {
+    if (st->scratch) cudaFree(st->scratch);
+    delete st;
+    return cuda_status(e, "memory_create: scratch");
+  }
+  *out = st;
+  return MSPIPE_OK;
+}
+
+mspipe_status mspipe_memory_destroy(mspipe_memory* st) {
+  if (!st) return MSPIPE_OK;
+  if (st->scratch) cudaFree(st->scratch);
+  delete st;
+  return MSPIPE_OK;
+}
+
+int64_t mspipe_memory_committed(const mspipe_memory* st) { return st ? st->committed : -1; }
+
+mspipe_status mspipe_memory_reset(mspipe_memory* st) {
+  if (!st) return fail(MSPIPE_EINVAL, "memory_reset: NULL handle");
+  st->committed = 0;
+  return MSPIPE_OK;
+}
+
+mspipe_status mspipe_memory_fetch(mspipe_memory* st, int64_t iteration, const int32_t* ids,
+                                  int64_t n, float* out_mem, double* out_mem_ts, float* out_mail,
+                                  double* out_mail_ts, const mspipe_mitigation* mit,
+                                  int64_t* out_version, void* stream) {
+  if (!st) return fail(MSPIPE_EINVAL, "memory_fetch: NULL handle");
+  if (iteration < 1 || n < 0) return fail(MSPIPE_EINVAL, "memory_fetch: iteration=%lld n=%lld", (long long)iteration, (long long)n);
+  // Staleness gate, Eq. (2) / Alg. 1 L8-L11: i-1-k <= committed <= i-1.
+  if (st->committed < iteration - 1 - st->k || st->committed > iteration - 1)
+    return fail(MSPIPE_ESTALE, "memory_fetch: iteration %lld with committed=%lld violates k=%d",
+                (long long)iteration, (long long)st->committed, st->k);
+  if (n > 0 && (!ids || !out_mem || !out_mem_ts)) return fail(MSPIPE_EINVAL, "memory_fetch: null ids/outputs");
+  if ((out_mail == nullptr) != (out_mail_ts == nullptr)) return fail(MSPIPE_EINVAL, "memory_fetch: out_mail and out_mail_ts go together");
+  if (mit) {
+    if (!tcsr_ok(mit->g) || !mit->src || !mit->dst || !mit->ts || !mit->out_h || mit->num_events < 0)
+      return fail(MSPIPE_EINVAL, "memory_fetch: bad mitigation arguments");
+    if (!(mit->lambda >= 0.f && mit->lambda <= 1.f) || mit->n_sim < 0 || mit->n_sim > 16 || mit->fanout < 1 || mit->fanout > 16)
+      return fail(MSPIPE_EINVAL, "memory_fetch: lambda=%g n_sim=%d fanout=%d (fanout<=16, n_sim<=16)", mit->lambda, mit->n_sim, mit->fanout);
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  if (n > 0)
+    launch_fetch(ids, n, st->num_nodes, st->mem, st->mem_ts, st->mem_dim, out_mail ? st->mail : nullptr,
+                 st->mail_ts, st->mail_stride, out_mem, out_mem_ts, out_mail, out_mail_ts, s);
+  if (mit && mit->num_events > 0)
+    launch_mitigate(to_tcsr(mit->g), mit->src, mit->dst, mit->ts, mit->num_events, st->mem, st->mem_ts,
+                    st->mem_dim, mit->lambda, mit->gamma, mit->n_sim, mit->fanout, mit->out_h,
+                    mit->out_omega, mit->out_elig, s);
+  if (out_version) *out_version = st->committed;
+  return after_launch("memory_fetch");
+}
+
+mspipe_status mspipe_gru_create(mspipe_gru** out, int32_t mem_dim, int32_t edge_dim,
+                                int32_t time_dim, int32_t precision, const float* w_ih,
+                                const float* w_hh, const float* b_ih, const float* b_hh,
+                                const float* time_w, const float* time_b, void* stream) {
+  if (!out) return fail(MSPIPE_EINVAL, "gru_create: out is NULL");
+  *out = nullptr;
+  if (mem_dim < 4 || mem_dim % 4 || edge_dim < 0 || time_dim < 0)
+    return fail(MSPIPE_EINVAL, "gru_create: mem_dim=%d edge_dim=%d time_dim=%d", mem_dim, edge_dim, time_dim);
+  if (!w_ih || !w_hh || !b_ih || !b_hh || (time_dim > 0 && (!time_w || !time_b)))
+    return fail(MSPIPE_EINVAL, "gru_create: null weight");
+  if (precision != MSPIPE_FP32_SIMT)
+    return fail(MSPIPE_EUNSUPPORTED, "gru_create: precision %d not in this build", precision);
+  mspipe_gru* p = new mspipe_gru();
+  GruDesc& d = p->d;
+  d.M = mem_dim;
+  d.He = edge_dim;
+  d.Dt = time_dim;
+  d.Dm = 2 * mem_dim + edge_dim;
+  d.Dx = d.Dm + time_dim;
+  d.K = d.Dx + mem_dim;
+  d.Kpad = (d.K + 31) / 32 * 32;
+  d.Npad = (mem_dim + 31) / 32 * 128;
+  p->precision = precision;
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e = cudaMalloc(&p->wpack, sizeof(float) * (size_t)d.Kpad * d.Npad);
+  if (e == cudaSuccess) e = cudaMalloc(&p->bias, sizeof(float) * (size_t)d.Npad);
+  if (e == cudaSuccess) e = cudaMalloc(&p->time_w, sizeof(float) * (size_t)(time_dim > 0 ? time_dim : 1));
+  if (e == cudaSuccess) e = cudaMalloc(&p->time_b, sizeof(float) * (size_t)(time_dim > 0 ? time_dim : 1));
+  if (e == cudaSuccess && time_dim > 0) e = cudaMemcpyAsync(p->time_w, time_w, sizeof(float) * time_dim, cudaMemcpyDeviceToDevice, s);
+  if (e == cudaSuccess && time_dim > 0) e = cudaMemcpyAsync(p->time_b, time_b, sizeof(float) * time_dim, cudaMemcpyDeviceToDevice, s);
+  if (e != cudaSuccess) {
+    mspipe_gru_destroy(p);
+    return cuda_status(e, "gru_create: alloc");
+  }
+  d.wpack = p->wpack;
+  d.bias = p->bias;
+  d.time_w = p->time_w;
+  d.time_b = p->time_b;
+  launch_gru_pack(w_ih, w_hh, b_ih, b_hh, d, p->wpack, p->bias, s);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    mspipe_gru_destroy(p);
+    return cuda_status(e, "gru_create: pack");
+  }
+  *out = p;
+  return MSPIPE_OK;
+}
+
+mspipe_status mspipe_gru_destroy(mspipe_gru* p) {
+  if (!p) return MSPIPE_OK;
+  cudaFree(p->wpack);
+  cudaFree(p->bias);
+  cudaFree(p->time_w);
+  cudaFree(p->time_b);
+  delete p;
+  return MSPIPE_OK;
+}
+
+mspipe_status mspipe_memory_update(mspipe_memory* st, const mspipe_gru* gru, const int32_t* src,
+                                   const int32_t* dst, const double* ts, int64_t num_events,
+                                   const float* edge_feat, const float* snap_mem,
+                                   const double* snap_mem_ts, int64_t snap_step,
+                                   const float* snap_h, int32_t* out_nodes, int32_t* out_winner,
+                                   int32_t* out_num_unique, float* out_mem, double* out_ts,
+                                   float* out_mail, void* stream) {
+  if (!st || !gru) return fail(MSPIPE_EINVAL, "memory_update: NULL handle");
+  if (gru->d.M != st->mem_dim || gru->d.He != st->edge_dim)
+    return fail(MSPIPE_EINVAL, "memory_update: GRU dims (M=%d He=%d) != memory dims (M=%d He=%d)", gru->d.M, gru->d.He, st->mem_dim, st->edge_dim);
+  if (num_events < 0 || num_events > 16384 || snap_step < 1)
+    return fail(MSPIPE_EINVAL, "memory_update: num_events=%lld (<= 16384) snap_step=%lld", (long long)num_events, (long long)snap_step);
+  if (!out_num_unique) return fail(MSPIPE_EINVAL, "memory_update: null out_num_unique");
+  cudaStream_t s = (cudaStream_t)stream;
+  if (num_events == 0) {
+    return cuda_status(cudaMemsetAsync(out_num_unique, 0, sizeof(int32_t), s), "memory_update");
+  }
+  if (!src || !dst || !ts || (st->edge_dim > 0 && !edge_feat) || !snap_mem || !snap_mem_ts || !out_nodes ||
+      !out_winner || !out_mem || !out_ts || !out_mail)
+    return fail(MSPIPE_EINVAL, "memory_update: null input/output");
+  launch_dedup(src, dst, num_events, st->scratch, st->num_nodes, out_nodes, out_winner, out_num_unique, s);
+  launch_gru_simt(gru->d, src, dst, ts, num_events, edge_feat, snap_mem, snap_mem_ts, snap_step, snap_h,
+                  out_nodes, out_winner, out_num_unique, out_mem, out_ts, out_mail, st->mail_stride, s);
+  return after_launch("memory_update");
+}
+
+mspipe_status mspipe_memory_writeback(mspipe_memory* st, int64_t commit_version,
+                                      const int32_t* nodes, const int32_t* num_unique,
+                                      int64_t max_n, const float* new_mem, const double* new_ts,
+                                      const float* new_mail, void* stream) {
+  if (!st) return fail(MSPIPE_EINVAL, "memory_writeback: NULL handle");
+  if (commit_version != st->committed + 1)
+    return fail(MSPIPE_EORDER, "memory_writeback: commit_version=%lld but committed=%lld", (long long)commit_version, (long long)st->committed);
+  if (max_n < 0) return fail(MSPIPE_EINVAL, "memory_writeback: max_n=%lld", (long long)max_n);
+  if (max_n > 0 && (!nodes || !num_unique || !new_mem || !new_ts || !new_mail))
+    return fail(MSPIPE_EINVAL, "memory_writeback: null input");
+  if (max_n > 0)
+    launch_writeback(nodes, num_unique, max_n, new_mem, new_ts, new_mail, st->mem_dim, st->mail_stride,
+                     st->mem, st->mem_ts, st->mail, st->mail_ts, st->num_nodes, (cudaStream_t)stream);
+  mspipe_status rc = after_launch("memory_writeback");
+  if (rc == MSPIPE_OK) st->committed = commit_version;  // i_upd <- i (Alg. 1 L16)
+  return rc;
+}
+
+mspipe_status mspipe_util_event_record(void* event, void* stream) {
+  if (!event) return fail(MSPIPE_EINVAL, "util_event_record: NULL event");
+  return cuda_status(cudaEventRecordWithFlags((cudaEvent_t)event, (cudaStream_t)stream, cudaEventRecordExternal),
+                     "util_event_record");
+}
+
+}  // extern "C"

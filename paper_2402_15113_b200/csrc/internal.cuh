@@ -1,0 +1,106 @@
+// internal.cuh — shared declarations of libmspipe (not part of the ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "mspipe.h"
+
+namespace mspipe {
+
+__host__ __device__ __forceinline__ int64_t min64(int64_t a, int64_t b) { return a < b ? a : b; }
+
+// Sticky device error flag (one per device, lives in this module).
+extern __device__ int g_dev_err;
+
+__device__ __forceinline__ void raise_dev(int bits) { atomicOr(&g_dev_err, bits); }
+
+mspipe_status fail(mspipe_status s, const char* fmt, ...);
+mspipe_status cuda_status(cudaError_t e, const char* what);
+
+inline int num_sms() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+struct Tcsr {
+  int64_t num_nodes, nnz;
+  const int64_t* indptr;
+  const int32_t* nbr;
+  const int32_t* eid;
+  const double* ts;
+};
+
+inline Tcsr to_tcsr(const mspipe_tcsr* g) {
+  return Tcsr{g->num_nodes, g->nnz, g->indptr, g->nbr, g->eid, g->ts};
+}
+
+// ---- kernels' host-side launchers (one .cu each) -------------------------
+// sampler.cu
+void launch_sample(const Tcsr& g, const int32_t* roots, const double* qts, const int32_t* src,
+                   const int32_t* dst, const int32_t* neg, const double* ev_ts, int64_t num_events,
+                   int64_t num_roots, int32_t fanout, int32_t* out_nbr, int32_t* out_eid,
+                   double* out_ts, float* out_dt, int32_t* out_cnt, int32_t* out_sub,
+                   cudaStream_t s);
+// memory.cu
+void launch_fetch(const int32_t* ids, int64_t n, int64_t num_nodes, const float* mem,
+                  const double* mem_ts, int32_t mem_dim, const float* mail, const double* mail_ts,
+                  int64_t mail_stride, float* out_mem, double* out_mem_ts, float* out_mail,
+                  double* out_mail_ts, cudaStream_t s);
+void launch_mitigate(const Tcsr& g, const int32_t* src, const int32_t* dst, const double* ts,
+                     int64_t num_events, const float* mem, const double* mem_ts, int32_t mem_dim,
+                     float lambda, double gamma, int32_t n_sim, int32_t fanout, float* out_h,
+                     int32_t* out_omega, uint8_t* out_elig, cudaStream_t s);
+void launch_dedup(const int32_t* src, const int32_t* dst, int64_t num_events, int32_t* scratch,
+                  int64_t num_nodes, int32_t* out_nodes, int32_t* out_winner, int32_t* out_num,
+                  cudaStream_t s);
+void launch_writeback(const int32_t* nodes, const int32_t* num, int64_t max_n,
+                      const float* new_mem, const double* new_ts, const float* new_mail,
+                      int32_t mem_dim, int64_t mail_stride, float* mem, double* mem_ts,
+                      float* mail, double* mail_ts, int64_t num_nodes, cudaStream_t s);
+// gru_simt.cu
+struct GruDesc {
+  int32_t M, He, Dt, Dm, Dx, K, Kpad, Npad;
+  const float* wpack;   // [Kpad, Npad]
+  const float* bias;    // [Npad]
+  const float* time_w;  // [Dt]
+  const float* time_b;  // [Dt]
+};
+void launch_gru_pack(const float* w_ih, const float* w_hh, const float* b_ih, const float* b_hh,
+                     const GruDesc& d, float* wpack, float* bias, cudaStream_t s);
+void launch_gru_simt(const GruDesc& d, const int32_t* src, const int32_t* dst, const double* ts,
+                     int64_t num_events, const float* edge_feat, const float* snap_mem,
+                     const double* snap_mem_ts, int64_t snap_step, const float* snap_h,
+                     const int32_t* nodes, const int32_t* winner, const int32_t* num_unique,
+                     float* out_mem, double* out_ts, float* out_mail, int64_t mail_stride,
+                     cudaStream_t s);
+
+}  // namespace mspipe
+
+struct mspipe_memory {
+  int64_t num_nodes;
+  int32_t mem_dim, edge_dim, mail_dim, k;
+  float* mem;
+  double* mem_ts;
+  float* mail;
+  double* mail_ts;
+  int64_t mail_stride;
+  int32_t rank, world;
+  int64_t committed;
+  int32_t* scratch;  // [num_nodes] int32, -1 between calls (self-cleaning)
+  int device;
+};
+
+struct mspipe_gru {
+  mspipe::GruDesc d;
+  int32_t precision;
+  float* wpack;
+  float* bias;
+  float* time_w;
+  float* time_b;
+};

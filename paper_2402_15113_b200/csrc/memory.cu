@@ -1,0 +1,368 @@
+// memory.cu — A3 snapshot fetch, A4 mitigation, A2 dedup, A7 write-back.
+#include "internal.cuh"
+
+namespace mspipe {
+
+static inline unsigned grid_for(int64_t work_items, int threads, int per_sm) {
+  int64_t b = (work_items + threads - 1) / threads;
+  const int64_t cap = (int64_t)num_sms() * per_sm;
+  if (b > cap) b = cap;
+  if (b < 1) b = 1;
+  return (unsigned)b;
+}
+
+// ---------------------------------------------------------------------------
+// A3 — gather rows of the state tables into dense snapshot buffers
+// ("fetches the required ... node memory vectors"; Eq. 2 reads
+// s~^(i-k)).  One thread moves one 16-byte vector; consecutive
+// threads walk a row's vectors, so both the table reads (one 400 B / 1.5 KB
+// row per id) and the dense writes are contiguous per warp.  id -1 = pad.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_fetch_gather(
+    const int32_t* __restrict__ ids, int64_t n, int64_t N, const float4* __restrict__ mem,
+    const double* __restrict__ mem_ts, int32_t Qm, const float4* __restrict__ mail,
+    const double* __restrict__ mail_ts, int32_t Qa, float4* __restrict__ out_mem,
+    double* __restrict__ out_mem_ts, float4* __restrict__ out_mail,
+    double* __restrict__ out_mail_ts) {
+  const int32_t Q = Qm + Qa;
+  const int64_t total = n * Q;
+  const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = t / Q;
+    const int32_t c = (int32_t)(t - row * Q);
+    const int32_t id = __ldg(ids + row);
+    const bool ok = id >= 0 && id < N;
+    if (!ok && id != -1 && c == 0) raise_dev(MSPIPE_DEVERR_RANGE);
+    if (c < Qm) {
+      out_mem[row * Qm + c] = ok ? __ldg(mem + (int64_t)id * Qm + c) : z;
+      if (c == 0) out_mem_ts[row] = ok ? __ldg(mem_ts + id) : 0.0;
+    } else {
+      const int32_t cc = c - Qm;
+      out_mail[row * Qa + cc] = ok ? __ldg(mail + (int64_t)id * Qa + cc) : z;
+      if (cc == 0) out_mail_ts[row] = ok ? __ldg(mail_ts + id) : 0.0;
+    }
+  }
+}
+
+void launch_fetch(const int32_t* ids, int64_t n, int64_t num_nodes, const float* mem,
+                  const double* mem_ts, int32_t mem_dim, const float* mail, const double* mail_ts,
+                  int64_t mail_stride, float* out_mem, double* out_mem_ts, float* out_mail,
+                  double* out_mail_ts, cudaStream_t s) {
+  const int32_t Qm = mem_dim / 4;
+  const int32_t Qa = mail ? (int32_t)(mail_stride / 4) : 0;
+  const int threads = 256;
+  k_fetch_gather<<<grid_for(n * (Qm + Qa), threads, 16), threads, 0, s>>>(
+      ids, n, num_nodes, (const float4*)mem, mem_ts, Qm, (const float4*)mail, mail_ts, Qa,
+      (float4*)out_mem, out_mem_ts, (float4*)out_mail, out_mail_ts);
+}
+
+// ---------------------------------------------------------------------------
+// A4 — MSPipe-S similarity-based mitigation, one warp per
+// target.  Eligibility is one compare; only eligible targets (the Δt tail,
+// ~1-p of rows) walk the 2-hop neighbourhood.  Every decision uses
+// only ids and timestamps, so eligibility and Ω are bit-exact; the blend is
+// f32.
+// ---------------------------------------------------------------------------
+constexpr int kMitMaxF = 16;
+constexpr int kMitMaxC = kMitMaxF * kMitMaxF;
+constexpr int kMitWarps = 4;
+
+struct MitWarpSmem {
+  int32_t cand[kMitMaxC];
+  int32_t kid[kMitMaxC];
+  int32_t kc[kMitMaxC];
+  double kmts[kMitMaxC];
+  int32_t omega[kMitMaxF];
+};
+
+__device__ __forceinline__ int64_t lower_bound_ts(const Tcsr& g, int32_t v, double t,
+                                                  int64_t* beg_out) {
+  const int64_t beg = __ldg(g.indptr + v);
+  int64_t lo = beg, hi = __ldg(g.indptr + v + 1);
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (__ldg(g.ts + mid) < t) lo = mid + 1;
+    else hi = mid;
+  }
+  *beg_out = beg;
+  return lo;
+}
+
+__global__ void __launch_bounds__(32 * kMitWarps) k_mitigate(
+    Tcsr g, const int32_t* __restrict__ src, const int32_t* __restrict__ dst,
+    const double* __restrict__ ts, int64_t B, const float* __restrict__ mem,
+    const double* __restrict__ mem_ts, int32_t M, float lambda, double gamma, int32_t n_sim,
+    int32_t F, float* __restrict__ out_h, int32_t* __restrict__ out_omega,
+    uint8_t* __restrict__ out_elig) {
+  __shared__ MitWarpSmem sm_all[kMitWarps];
+  const int lane = threadIdx.x & 31;
+  MitWarpSmem& sm = sm_all[threadIdx.x >> 5];
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int32_t Q = M / 4;
+  const float4* mem4 = (const float4*)mem;
+  float4* h4 = (float4*)out_h;
+  for (int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < 2 * B; t += nwarps) {
+    const int64_t a = t < B ? t : t - B;
+    const int32_t w = t < B ? __ldg(src + a) : __ldg(dst + a);
+    const double tstar = __ldg(ts + a);
+    const bool wok = w >= 0 && w < g.num_nodes;
+    if (!wok && lane == 0) raise_dev(MSPIPE_DEVERR_RANGE);
+    const double mtw = wok ? __ldg(mem_ts + w) : 0.0;
+    const bool elig = wok && (tstar - mtw) > gamma;  // G11: strictly longer than γ
+    int32_t nk = 0;
+    if (elig) {
+      // N1 = distinct ids of sample(w, t*) \ {w}
+      int64_t begw;
+      const int64_t endw = lower_bound_ts(g, w, tstar, &begw);
+      const int32_t cntw = (int32_t)min64(endw - begw, (int64_t)F);
+      int32_t x = (lane < cntw) ? __ldg(g.nbr + (endw - 1 - lane)) : -1;
+      if (x == w) x = -1;
+      const unsigned grp = __match_any_sync(0xffffffffu, x);
+      const bool keep = x >= 0 && lane == __ffs(grp) - 1;
+      // candidates: lane l < F owns slots [l*F, (l+1)*F) with the distinct ids of sample(x_l, t*) \ {w}
+      if (lane < F) {
+        int32_t nl = 0;
+        if (keep) {
+          int64_t begx;
+          const int64_t endx = lower_bound_ts(g, x, tstar, &begx);
+          const int32_t cx = (int32_t)min64(endx - begx, (int64_t)F);
+          for (int32_t i = 0; i < cx; ++i) {
+            const int32_t u = __ldg(g.nbr + (endx - 1 - i));
+            if (u == w) continue;
+            bool dup = false;
+            for (int32_t j = 0; j < nl; ++j) dup |= (sm.cand[lane * F + j] == u);
+            if (!dup) sm.cand[lane * F + nl++] = u;
+          }
+        }
+        for (int32_t j = nl; j < F; ++j) sm.cand[lane * F + j] = -1;
+      }
+      __syncwarp();
+      // c(u) = #lists containing u; keep first occurrence of each active u
+      const int32_t FF = F * F;
+      for (int32_t e0 = 0; e0 < FF; e0 += 32) {
+        const int32_t e = e0 + lane;
+        const int32_t u = e < FF ? sm.cand[e] : -1;
+        bool take = false;
+        int32_t c = 0;
+        double mu = 0.0;
+        if (u >= 0) {
+          bool first = true;
+          for (int32_t e2 = 0; e2 < FF; ++e2) {
+            const int32_t u2 = sm.cand[e2];
+            if (u2 == u) {
+              ++c;
+              if (e2 < e) first = false;
+            }
+          }
+          if (first) {
+            mu = __ldg(mem_ts + u);
+            take = mu > mtw && (tstar - mu) < gamma;  // active: fresher than w and Δt < γ
+          }
+        }
+        const unsigned bal = __ballot_sync(0xffffffffu, take);
+        if (take) {
+          const int32_t pos = nk + __popc(bal & ((1u << lane) - 1u));
+          sm.kid[pos] = u;
+          sm.kc[pos] = c;
+          sm.kmts[pos] = mu;
+        }
+        nk += __popc(bal);
+      }
+      __syncwarp();
+      // rank by (c desc, mem_ts desc, id asc); the first n_sim form Ω
+      for (int32_t i = lane; i < nk; i += 32) {
+        const int32_t ui = sm.kid[i], ci = sm.kc[i];
+        const double mi = sm.kmts[i];
+        int32_t rank = 0;
+        for (int32_t j = 0; j < nk; ++j) {
+          const int32_t cj = sm.kc[j];
+          const double mj = sm.kmts[j];
+          const int32_t uj = sm.kid[j];
+          rank += (cj > ci) || (cj == ci && (mj > mi || (mj == mi && uj < ui)));
+        }
+        if (rank < n_sim) sm.omega[rank] = ui;
+      }
+      __syncwarp();
+    }
+    const int32_t k = min(nk, n_sim);
+    if (out_omega && lane < n_sim) out_omega[t * n_sim + lane] = lane < k ? sm.omega[lane] : -1;
+    if (out_elig && lane == 0) out_elig[t] = elig ? 1 : 0;
+    for (int32_t q = lane; q < Q; q += 32) {
+      float4 sw = wok ? __ldg(mem4 + (int64_t)w * Q + q) : make_float4(0.f, 0.f, 0.f, 0.f);
+      if (k > 0) {
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int32_t s2 = 0; s2 < k; ++s2) {
+          const float4 v = __ldg(mem4 + (int64_t)sm.omega[s2] * Q + q);
+          acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+        }
+        const float inv = (float)k;
+        const float l1 = 1.0f - lambda;
+        sw.x = lambda * sw.x + l1 * (acc.x / inv);
+        sw.y = lambda * sw.y + l1 * (acc.y / inv);
+        sw.z = lambda * sw.z + l1 * (acc.z / inv);
+        sw.w = lambda * sw.w + l1 * (acc.w / inv);
+      }
+      h4[t * Q + q] = sw;
+    }
+    __syncwarp();
+  }
+}
+
+void launch_mitigate(const Tcsr& g, const int32_t* src, const int32_t* dst, const double* ts,
+                     int64_t num_events, const float* mem, const double* mem_ts, int32_t mem_dim,
+                     float lambda, double gamma, int32_t n_sim, int32_t fanout, float* out_h,
+                     int32_t* out_omega, uint8_t* out_elig, cudaStream_t s) {
+  const int threads = 32 * kMitWarps;
+  k_mitigate<<<grid_for(2 * num_events * 32, threads, 16), threads, 0, s>>>(
+      g, src, dst, ts, num_events, mem, mem_ts, mem_dim, lambda, gamma, n_sim, fanout, out_h,
+      out_omega, out_elig);
+}
+
+// ---------------------------------------------------------------------------
+// A2 — deterministic most-recent dedup in one CTA.  Pair p = 2a + role has
+// node src_a (role 0) / dst_a (role 1); the winner of node w is max{p} (the
+// most recent message, G6).  Phase 1: warp-aggregated atomicMax of p into
+// scratch[node] (__match_any_sync groups equal nodes so a hot node costs one
+// atomic per warp; max is order-independent).  Phase 2: a pair wins iff
+// scratch[node_p] == p; a block scan over contiguous chunks compacts the
+// winners in p order.  Phase 3: winners restore scratch[node] = -1.
+// ---------------------------------------------------------------------------
+constexpr int kDedupThreads = 1024;
+
+__global__ void __launch_bounds__(kDedupThreads) k_dedup(
+    const int32_t* __restrict__ src, const int32_t* __restrict__ dst, int64_t B,
+    int32_t* __restrict__ scratch, int64_t N, int32_t* __restrict__ out_nodes,
+    int32_t* __restrict__ out_winner, int32_t* __restrict__ out_num) {
+  __shared__ int32_t warp_tot[kDedupThreads / 32];
+  __shared__ int32_t total_s;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int64_t P = 2 * B;
+  const int64_t Pr = (P + kDedupThreads - 1) / kDedupThreads * kDedupThreads;
+  for (int64_t p = tid; p < Pr; p += kDedupThreads) {
+    int32_t node = -1;
+    if (p < P) {
+      node = (p & 1) ? __ldg(dst + (p >> 1)) : __ldg(src + (p >> 1));
+      if (node < 0 || node >= N) {
+        raise_dev(MSPIPE_DEVERR_RANGE);
+        node = -1;
+      }
+    }
+    const unsigned grp = __match_any_sync(0xffffffffu, node);
+    const int leader = 31 - __clz(grp);  // highest lane = largest p of the group
+    if (node >= 0 && lane == leader) atomicMax(scratch + node, (int32_t)p);
+  }
+  __threadfence();
+  __syncthreads();
+  // contiguous chunk per thread: [tid*C, tid*C + C)
+  const int64_t C = (P + kDedupThreads - 1) / kDedupThreads;  // <= 32 (B <= 16384)
+  const int64_t p0 = tid * C;
+  uint32_t flags = 0;
+  int32_t cnt = 0;
+  for (int64_t i = 0; i < C; ++i) {
+    const int64_t p = p0 + i;
+    if (p >= P) break;
+    const int32_t node = (p & 1) ? __ldg(dst + (p >> 1)) : __ldg(src + (p >> 1));
+    if (node < 0 || node >= N) continue;
+    if (__ldcg(scratch + node) == (int32_t)p) {
+      flags |= 1u << i;
+      ++cnt;
+    }
+  }
+  // block exclusive scan of cnt
+  int32_t incl = cnt;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const int32_t y = __shfl_up_sync(0xffffffffu, incl, d);
+    if (lane >= d) incl += y;
+  }
+  if (lane == 31) warp_tot[wid] = incl;
+  __syncthreads();
+  if (wid == 0) {
+    int32_t v = warp_tot[lane];
+    int32_t vi = v;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int32_t y = __shfl_up_sync(0xffffffffu, vi, d);
+      if (lane >= d) vi += y;
+    }
+    warp_tot[lane] = vi - v;  // exclusive prefix of warp totals
+    if (lane == 31) total_s = vi;
+  }
+  __syncthreads();
+  int32_t off = warp_tot[wid] + incl - cnt;
+  for (int64_t i = 0; i < C; ++i) {
+    if (flags & (1u << i)) {
+      const int64_t p = p0 + i;
+      out_nodes[off] = (p & 1) ? __ldg(dst + (p >> 1)) : __ldg(src + (p >> 1));
+      out_winner[off] = (int32_t)p;
+      ++off;
+    }
+  }
+  __syncthreads();  // all scratch reads are done before the reset
+  for (int64_t i = 0; i < C; ++i) {
+    if (flags & (1u << i)) {
+      const int64_t p = p0 + i;
+      const int32_t node = (p & 1) ? __ldg(dst + (p >> 1)) : __ldg(src + (p >> 1));
+      scratch[node] = -1;
+    }
+  }
+  if (tid == 0) *out_num = total_s;
+}
+
+void launch_dedup(const int32_t* src, const int32_t* dst, int64_t num_events, int32_t* scratch,
+                  int64_t num_nodes, int32_t* out_nodes, int32_t* out_winner, int32_t* out_num,
+                  cudaStream_t s) {
+  k_dedup<<<1, kDedupThreads, 0, s>>>(src, dst, num_events, scratch, num_nodes, out_nodes,
+                                      out_winner, out_num);
+}
+
+// ---------------------------------------------------------------------------
+// A7 — write-back of U unique rows (commit of version i, P:L154, P:L820,
+// P:L854-L855).  Rows are unique within a batch, so the scatter is a plain
+// 16-byte-vector copy per thread; U is read on the device.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_writeback(
+    const int32_t* __restrict__ nodes, const int32_t* __restrict__ num, int64_t max_n,
+    const float4* __restrict__ new_mem, const double* __restrict__ new_ts,
+    const float4* __restrict__ new_mail, int32_t Qm, int32_t Qa, float4* __restrict__ mem,
+    double* __restrict__ mem_ts, float4* __restrict__ mail, double* __restrict__ mail_ts,
+    int64_t N) {
+  const int64_t U = min64((int64_t)__ldg(num), max_n);
+  const int32_t Q = Qm + Qa;
+  const int64_t total = U * Q;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = t / Q;
+    const int32_t c = (int32_t)(t - row * Q);
+    const int32_t node = __ldg(nodes + row);
+    if (node < 0 || node >= N) {
+      if (c == 0) raise_dev(MSPIPE_DEVERR_RANGE);
+      continue;
+    }
+    if (c < Qm) {
+      mem[(int64_t)node * Qm + c] = __ldg(new_mem + row * Qm + c);
+      if (c == 0) {
+        const double t1 = __ldg(new_ts + row);
+        mem_ts[node] = t1;
+        mail_ts[node] = t1;
+      }
+    } else {
+      const int32_t cc = c - Qm;
+      mail[(int64_t)node * Qa + cc] = __ldg(new_mail + row * Qa + cc);
+    }
+  }
+}
+
+void launch_writeback(const int32_t* nodes, const int32_t* num, int64_t max_n,
+                      const float* new_mem, const double* new_ts, const float* new_mail,
+                      int32_t mem_dim, int64_t mail_stride, float* mem, double* mem_ts,
+                      float* mail, double* mail_ts, int64_t num_nodes, cudaStream_t s) {
+  const int32_t Qm = mem_dim / 4, Qa = (int32_t)(mail_stride / 4);
+  const int threads = 256;
+  k_writeback<<<grid_for(max_n * (Qm + Qa), threads, 16), threads, 0, s>>>(
+      nodes, num, max_n, (const float4*)new_mem, new_ts, (const float4*)new_mail, Qm, Qa,
+      (float4*)mem, mem_ts, (float4*)mail, mail_ts, num_nodes);
+}
+
+}  // namespace mspipe

@@ -1,0 +1,231 @@
+"""The per-batch node-memory stage as a stream-ordered schedule of ABI calls.
+
+For batch (iteration) i, 1-based:
+    prep(i)   = mspipe_sample_batch(i) -> subgraph ids, then mspipe_memory_fetch(i)
+                (snapshot rows of the 3B(𝒩+1) subgraph nodes, P:L818, P:L1153;
+                optional MSPipe-S mitigation of the 2B update targets)
+    commit(i) = mspipe_memory_update(i) (dedup + message + GRU) then
+                mspipe_memory_writeback(i)  (i_upd <- i)
+
+The staleness bound becomes an ORDER on one stream (no host waits): with the
+exact schedule prep(i) is enqueued right after commit(i-1-k), so it reads
+version v(i) = i-1-k (Eq. 2; the gate of Alg. 1 L8-L11 is the
+check inside mspipe_memory_fetch).  k+1 snapshot slots hold the prepared
+batches in flight — the paper's "K additional subgraphs" (P:L557,
+P:L1171-L1175).  The grouped schedule fetches k+1 batches after one commit.
+
+A *step* (bench.py) is one batch: its ops are [prep(t+k), commit(t)].  Steps
+are captured once into CUDA graphs and replayed (µs-scale batches are
+launch-bound otherwise).
+"""
+from __future__ import annotations
+
+import dataclasses
+
+import torch
+
+from . import _C
+
+
+@dataclasses.dataclass
+class StageConfig:
+    num_nodes: int
+    mem_dim: int
+    edge_dim: int
+    time_dim: int
+    fanout: int
+    batch: int
+    k: int
+    schedule: str = "exact"        # "exact" | "grouped"
+    mitigation: dict | None = None  # dict(lam, gamma, n_sim) or None
+    fetch_mail: bool = False        # also fetch mail rows of the subgraph nodes
+    precision: int = _C.FP32_SIMT
+
+
+def schedule_ops(nb: int, k: int, schedule: str = "exact"):
+    """Stream order of prep/commit ops for batches 1..nb."""
+    ops = []
+    if schedule == "exact":
+        for i in range(1, min(k, nb) + 1):
+            ops.append(("prep", i))
+        for t in range(1, nb + 1):
+            if t + k <= nb:
+                ops.append(("prep", t + k))
+            ops.append(("commit", t))
+    elif schedule == "grouped":
+        for g0 in range(1, nb + 1, k + 1):
+            grp = list(range(g0, min(g0 + k, nb) + 1))
+            ops += [("prep", i) for i in grp]
+            ops += [("commit", i) for i in grp]
+    else:
+        raise ValueError(schedule)
+    return ops
+
+
+def snapshot_versions(nb: int, k: int, schedule: str = "exact"):
+    """v(i) the schedule reads (for checks): committed count at prep(i)."""
+    v, committed = {}, 0
+    for op, i in schedule_ops(nb, k, schedule):
+        if op == "prep":
+            v[i] = committed
+        else:
+            committed = i
+    return [v[i] for i in range(1, nb + 1)]
+
+
+class _Slot:
+    def __init__(self, cfg: StageConfig, mail_stride: int, device, staged: bool):
+        B, F, M = cfg.batch, cfg.fanout, cfg.mem_dim
+        self.samp = _C.alloc_sample(3 * B, F, device, sub=True)
+        n = 3 * B * (F + 1)
+        self.mem = torch.empty((n, M), dtype=torch.float32, device=device)
+        self.mem_ts = torch.empty((n,), dtype=torch.float64, device=device)
+        self.mail = torch.empty((n, mail_stride), dtype=torch.float32, device=device) if cfg.fetch_mail else None
+        self.mail_ts = torch.empty((n,), dtype=torch.float64, device=device) if cfg.fetch_mail else None
+        self.h = torch.empty((2 * B, M), dtype=torch.float32, device=device) if cfg.mitigation else None
+        self.omega = (torch.empty((2 * B, cfg.mitigation["n_sim"]), dtype=torch.int32, device=device)
+                      if cfg.mitigation else None)
+        self.elig = torch.empty((2 * B,), dtype=torch.uint8, device=device) if cfg.mitigation else None
+        self.version = -1
+        if staged:
+            self.inp = dict(src=torch.empty(B, dtype=torch.int32, device=device),
+                            dst=torch.empty(B, dtype=torch.int32, device=device),
+                            neg=torch.empty(B, dtype=torch.int32, device=device),
+                            ts=torch.empty(B, dtype=torch.float64, device=device),
+                            ef=torch.empty((B, cfg.edge_dim), dtype=torch.float32, device=device))
+
+
+class MemoryStage:
+    """Drives libmspipe over an event stream.  Inputs are either resident in
+    HBM (``bind_resident``) or staged per batch from pinned host memory
+    (``bind_host``: the H2D copy of the batch happens inside prep(i))."""
+
+    def __init__(self, cfg: StageConfig, params: dict, tcsr: _C.TcsrHandle, device="cuda"):
+        self.cfg = cfg
+        self.device = torch.device(device)
+        self.tcsr = tcsr
+        self.memory = _C.MemoryHandle(cfg.num_nodes, cfg.mem_dim, cfg.edge_dim, cfg.k, self.device)
+        self.gru = _C.GruHandle(cfg.mem_dim, cfg.edge_dim, cfg.time_dim, params, self.device, cfg.precision)
+        self.upd = _C.alloc_update(cfg.batch, cfg.mem_dim, self.memory.mail_stride, self.device)
+        self.staged = False
+        self.slots = None
+        self.timing = None  # optional dict name -> list of (start, end) events per op
+        self.versions = {}
+
+    # -- inputs ---------------------------------------------------------------
+    def bind_resident(self, src, dst, ts, neg, ef):
+        self.E = src.numel()
+        self.res = dict(src=src, dst=dst, ts=ts, neg=neg, ef=ef)
+        self.staged = False
+        self.slots = [_Slot(self.cfg, self.memory.mail_stride, self.device, False) for _ in range(self.cfg.k + 1)]
+
+    def bind_host(self, src, dst, ts, neg, ef):
+        """Host arrays are pinned; each prep copies its batch H2D (e2e path)."""
+        self.E = int(src.shape[0])
+        self.host = {k: torch.as_tensor(v).pin_memory() for k, v in
+                     dict(src=src, dst=dst, ts=ts, neg=neg, ef=ef).items()}
+        self.staged = True
+        self.slots = [_Slot(self.cfg, self.memory.mail_stride, self.device, True) for _ in range(self.cfg.k + 1)]
+        self.out_host = dict(nodes=torch.empty(2 * self.cfg.batch, dtype=torch.int32).pin_memory(),
+                             num=torch.empty(1, dtype=torch.int32).pin_memory(),
+                             mem=torch.empty((2 * self.cfg.batch, self.cfg.mem_dim), dtype=torch.float32).pin_memory())
+
+    @property
+    def num_batches(self):
+        return -(-self.E // self.cfg.batch)
+
+    def _range(self, i):
+        B = self.cfg.batch
+        j0 = (i - 1) * B
+        return j0, min(j0 + B, self.E)
+
+    def inputs(self, i):
+        j0, j1 = self._range(i)
+        if not self.staged:
+            return {k: v[j0:j1] for k, v in self.res.items()}
+        n = j1 - j0
+        return {k: v[:n] for k, v in self.slots[(i - 1) % (self.cfg.k + 1)].inp.items()}
+
+    # -- ops ------------------------------------------------------------------
+    def _slot(self, i):
+        return self.slots[(i - 1) % (self.cfg.k + 1)]
+
+    def _ev(self, name):
+        if self.timing is None:
+            return None
+        e = torch.cuda.Event(enable_timing=True)
+        _C.event_record(e)
+        self.timing.setdefault(name, []).append(e)
+        return e
+
+    def prep(self, i):
+        cfg, sl = self.cfg, self._slot(i)
+        if self.staged:
+            j0, j1 = self._range(i)
+            n = j1 - j0
+            for key in ("src", "dst", "neg", "ts", "ef"):
+                sl.inp[key][:n].copy_(self.host[key][j0:j1], non_blocking=True)
+        x = self.inputs(i)
+        n = x["src"].numel()
+        samp = {k: v[: 3 * n] for k, v in sl.samp.items()}
+        self._ev("sample")
+        _C.sample_batch(self.tcsr, x["src"], x["dst"], x["neg"], x["ts"], cfg.fanout, samp)
+        self._ev("sample_end")
+        ids = samp["sub"].reshape(-1)
+        m = ids.numel()
+        mit = None
+        if cfg.mitigation:
+            mit = _C.make_mitigation(self.tcsr, cfg.mitigation["lam"], cfg.mitigation["gamma"],
+                                     cfg.mitigation["n_sim"], cfg.fanout, x["src"], x["dst"], x["ts"],
+                                     sl.h[: 2 * n], sl.omega[: 2 * n], sl.elig[: 2 * n])
+        self._ev("fetch")
+        sl.version = _C.memory_fetch(self.memory, i, ids, sl.mem[:m], sl.mem_ts[:m],
+                                     sl.mail[:m] if sl.mail is not None else None,
+                                     sl.mail_ts[:m] if sl.mail_ts is not None else None, mit)
+        self._ev("fetch_end")
+        self.versions[i] = sl.version
+
+    def commit(self, i):
+        cfg, sl = self.cfg, self._slot(i)
+        x = self.inputs(i)
+        n = x["src"].numel()
+        upd = {k: (v if k == "num" else v[: 2 * n]) for k, v in self.upd.items()}
+        self._ev("update")
+        _C.memory_update(self.memory, self.gru, x["src"], x["dst"], x["ts"], x["ef"], sl.mem, sl.mem_ts,
+                         cfg.fanout + 1, upd, snap_h=sl.h[: 2 * n] if sl.h is not None else None)
+        self._ev("update_end")
+        self._ev("writeback")
+        _C.memory_writeback(self.memory, i, upd)
+        self._ev("writeback_end")
+        if self.staged:
+            self.out_host["num"].copy_(self.upd["num"], non_blocking=True)
+            self.out_host["nodes"].copy_(self.upd["nodes"], non_blocking=True)
+            self.out_host["mem"].copy_(self.upd["mem"], non_blocking=True)
+
+    def run_ops(self, ops):
+        for op, i in ops:
+            (self.prep if op == "prep" else self.commit)(i)
+
+    def run(self, nb=None):
+        """Eager: all batches (or the first nb) in schedule order."""
+        nb = self.num_batches if nb is None else nb
+        self.run_ops(schedule_ops(nb, self.cfg.k, self.cfg.schedule))
+
+    def step_ops(self, nb=None):
+        """Ops grouped per step (one commit per step; prologue preps in step 0)."""
+        nb = self.num_batches if nb is None else nb
+        steps, cur = [], []
+        for op in schedule_ops(nb, self.cfg.k, self.cfg.schedule):
+            cur.append(op)
+            if op[0] == "commit":
+                steps.append(cur)
+                cur = []
+        return steps
+
+    def h2d_bytes_per_batch(self):
+        B = self.cfg.batch
+        return B * (4 + 4 + 4 + 8 + 4 * self.cfg.edge_dim)
+
+    def d2h_bytes_per_batch(self):
+        B = self.cfg.batch
+        return 4 + 2 * B * 4 + 2 * B * self.cfg.mem_dim * 4

@@ -1,0 +1,357 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the
+same seeded inputs.  Bit-exact for ids, counts, winners, timestamps, Ω,
+eligibility and copied rows; values within the north-star tolerance
+|g - o| <= 1e-4 |o| + 1e-6 (fp32, teacher-forced).  Expected values come
+from oracle/ only."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from paper_2402_15113_b200 import MemoryStage, StageConfig, _C, build_tcsr
+from synth import CONFIGS, edge_features, gru_params, make_events, make_workload
+
+pytestmark = pytest.mark.gpu
+
+RTOL, ATOL = 1e-4, 1e-6
+
+
+@pytest.fixture(scope="module")
+def dev():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    d = torch.device("cuda:0")
+    torch.cuda.set_device(d)
+    return d
+
+
+def _close(g, o, rtol=RTOL, atol=ATOL):
+    g = np.asarray(g, np.float64)
+    o = np.asarray(o, np.float64)
+    bad = np.abs(g - o) > rtol * np.abs(o) + atol
+    return not bad.any(), float(np.abs(g - o).max(initial=0.0))
+
+
+def _t(a, dev):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+
+
+# ------------------------------------------------------------------ A1 sampler
+@pytest.mark.parametrize("name,E", [("tiny", None), ("wiki", None), ("lastfm", 300_000), ("reddit", 200_000)])
+def test_sampler_batch_bit_exact(dev, name, E):
+    cfg = CONFIGS[name]
+    src, dst, ts, neg = make_events(cfg, 0, E)
+    g = build_tcsr(cfg.num_nodes, src, dst, ts, dev)
+    og = oracle.Graph(cfg.num_nodes, src, dst, ts)
+    B, F = cfg.batch, cfg.fanout
+    nb = -(-len(src) // B)
+    rng = np.random.default_rng(1)
+    picks = sorted(set([1, 2, nb] + rng.integers(1, nb + 1, 12).tolist()))
+    for i in picks:
+        j0, j1 = (i - 1) * B, min(i * B, len(src))
+        n = j1 - j0
+        out = _C.alloc_sample(3 * n, F, dev)
+        _C.sample_batch(g, _t(src[j0:j1], dev), _t(dst[j0:j1], dev), _t(neg[j0:j1], dev), _t(ts[j0:j1], dev), F, out)
+        roots = np.concatenate([src[j0:j1], dst[j0:j1], neg[j0:j1]])
+        qts = np.concatenate([ts[j0:j1]] * 3)
+        ref = og.sample(roots, qts, F)
+        for key in ("nbr", "eid", "ts", "dt", "cnt"):
+            assert np.array_equal(out[key].cpu().numpy(), ref[key]), (i, key)
+        sub = out["sub"].cpu().numpy()
+        assert np.array_equal(sub[:, 0], roots)
+        assert np.array_equal(sub[:, 1:], ref["nbr"])
+    _C.check()
+
+
+@pytest.mark.parametrize("fanout", [1, 3, 10, 17, 64])
+def test_sampler_recent_arbitrary_queries(dev, fanout):
+    cfg = CONFIGS["lastfm"]
+    src, dst, ts, _ = make_events(cfg, 2, 100_000)
+    g = build_tcsr(cfg.num_nodes, src, dst, ts, dev)
+    rng = np.random.default_rng(fanout)
+    n = 5003  # ragged tail over 32-root warps
+    roots = rng.integers(0, cfg.num_nodes, n).astype(np.int32)
+    qts = ts[rng.integers(0, len(ts), n)] + rng.integers(-1, 2, n)
+    qts[:5] = [0.0, -1.0, ts[-1] + 10, ts[0], ts[len(ts) // 2]]
+    out = _C.alloc_sample(n, fanout, dev)
+    _C.sample_recent(g, _t(roots, dev), _t(qts, dev), fanout, out)
+    ref = oracle.sample_brute(src, dst, ts, roots[:300], qts[:300], fanout)  # the definition
+    ref2 = oracle.Graph(cfg.num_nodes, src, dst, ts).sample(roots, qts, fanout)
+    for key in ("nbr", "eid", "ts", "dt", "cnt"):
+        got = out[key].cpu().numpy()
+        assert np.array_equal(got[:300], ref[key]), key
+        assert np.array_equal(got, ref2[key]), key
+    _C.check()
+
+
+def test_sampler_edge_cases(dev):
+    src = np.array([0, 1, 2, 2], np.int32)
+    dst = np.array([1, 1, 2, 0], np.int32)  # self-loops (1,1), (2,2)
+    ts = np.array([1.0, 2.0, 2.0, 3.0])
+    g = build_tcsr(5, src, dst, ts, dev)
+    empty = _C.alloc_sample(0, 4, dev)
+    _C.sample_recent(g, torch.empty(0, dtype=torch.int32, device=dev), torch.empty(0, dtype=torch.float64, device=dev), 4, empty)
+    roots = np.array([1, 2, 4, 0], np.int32)
+    qts = np.array([5.0, 5.0, 5.0, 1.0])
+    out = _C.alloc_sample(4, 4, dev)
+    _C.sample_recent(g, _t(roots, dev), _t(qts, dev), 4, out)
+    ref = oracle.sample_brute(src, dst, ts, roots, qts, 4)
+    for key in ("nbr", "eid", "ts", "dt", "cnt"):
+        assert np.array_equal(out[key].cpu().numpy(), ref[key]), key
+    assert out["cnt"].cpu().tolist() == [2, 2, 0, 0]  # self-loop once; isolated node; strict ts < t_q
+    _C.check()
+    bad = _C.alloc_sample(1, 4, dev)
+    _C.sample_recent(g, _t(np.array([7], np.int32), dev), _t(np.array([1.0]), dev), 4, bad)
+    with pytest.raises(_C.MspipeError) as e:
+        _C.check()
+    assert e.value.status == _C.ERANGE
+    assert bad["cnt"].item() == 0
+
+
+# ------------------------------------------------------------------ A2-A6 teacher-forced
+def _random_state(num_nodes, M, src, dst, ts, j0, seed):
+    """Seeded synthetic snapshot: random memory rows; mem_ts = time of each
+    node's last event before the batch (0 if none), as a real trajectory has."""
+    rng = np.random.default_rng(seed)
+    mem = rng.uniform(-1, 1, (num_nodes, M)).astype(np.float32)
+    mem_ts = np.zeros(num_nodes)
+    mem_ts[src[:j0]] = ts[:j0]  # numpy fancy assignment keeps the last write
+    last_dst = np.zeros(num_nodes)
+    last_dst[dst[:j0]] = ts[:j0]
+    return mem, np.maximum(mem_ts, last_dst)
+
+
+def _teacher_forced(dev, name, i, mitigation=None, seed=0, E=None):
+    cfg = CONFIGS[name]
+    src, dst, ts, neg = make_events(cfg, seed, E)
+    B, F, M = cfg.batch, cfg.fanout, cfg.mem_dim
+    j0, j1 = (i - 1) * B, min(i * B, len(src))
+    ef = edge_features(seed, j0, j1 - j0, cfg.edge_dim)
+    params = gru_params(M, cfg.mail_dim, cfg.time_dim)
+    mem, mem_ts = _random_state(cfg.num_nodes, M, src, dst, ts, j0, seed + i)
+    g = build_tcsr(cfg.num_nodes, src, dst, ts, dev)
+    sc = StageConfig(cfg.num_nodes, M, cfg.edge_dim, cfg.time_dim, F, B, 0, mitigation=mitigation)
+    st = MemoryStage(sc, params, g, dev)
+    st.memory.mem.copy_(_t(mem, dev))
+    st.memory.mem_ts.copy_(_t(mem_ts, dev))
+    x = {k: _t(v[j0:j1], dev) for k, v in dict(src=src, dst=dst, ts=ts, neg=neg).items()}
+    x["ef"] = _t(ef, dev)
+    st.bind_resident(x["src"], x["dst"], x["ts"], x["neg"], x["ef"])
+    st.prep(1)
+    sl = st.slots[0]
+    n = j1 - j0
+    upd = {k: (v if k == "num" else v[: 2 * n]) for k, v in st.upd.items()}
+    _C.memory_update(st.memory, st.gru, x["src"], x["dst"], x["ts"], x["ef"], sl.mem, sl.mem_ts, F + 1, upd,
+                     snap_h=sl.h[: 2 * n] if sl.h is not None else None)
+    torch.cuda.synchronize()
+    _C.check()
+    og = oracle.Graph(cfg.num_nodes, src, dst, ts) if mitigation else None
+    ref = oracle.memory_update(cfg.num_nodes, src[j0:j1], dst[j0:j1], ts[j0:j1], ef, params, mem, mem_ts,
+                               mitigation=mitigation, graph=og, fanout=F)
+    return st, sl, upd, ref, (src[j0:j1], dst[j0:j1], ts[j0:j1], neg[j0:j1]), (mem, mem_ts)
+
+
+@pytest.mark.parametrize("name,i,E", [("tiny", 1, None), ("tiny", 50, None), ("wiki", 137, None),
+                                      ("lastfm", 400, 300_000), ("gdelt", 3, 20_000)])
+def test_update_teacher_forced(dev, name, i, E):
+    st, sl, upd, ref, ev, (mem, mem_ts) = _teacher_forced(dev, name, i, E=E)
+    U = int(upd["num"].item())
+    assert U == len(ref["nodes"])
+    assert np.array_equal(upd["nodes"][:U].cpu().numpy(), ref["nodes"])
+    assert np.array_equal(upd["winner"][:U].cpu().numpy(), ref["winner"])
+    assert np.array_equal(upd["ts"][:U].cpu().numpy(), ref["ts"])
+    Dm = ref["mail"].shape[1]
+    mail = upd["mail"][:U].cpu().numpy()
+    assert np.array_equal(mail[:, :Dm], ref["mail"])  # copies of snapshot rows + ef
+    assert (mail[:, Dm:] == 0).all()
+    ok, err = _close(upd["mem"][:U].cpu().numpy(), ref["mem"])
+    assert ok, f"GRU mismatch max abs {err}"
+    # A3 fetch: copied rows are the state rows of the subgraph ids (pads zero)
+    ids = sl.samp["sub"][: 3 * len(ev[0])].reshape(-1).cpu().numpy()
+    got = sl.mem[: len(ids)].cpu().numpy()
+    gts = sl.mem_ts[: len(ids)].cpu().numpy()
+    valid = ids >= 0
+    assert np.array_equal(got[valid], mem[ids[valid]]) and (got[~valid] == 0).all()
+    assert np.array_equal(gts[valid], mem_ts[ids[valid]]) and (gts[~valid] == 0).all()
+
+
+@pytest.mark.parametrize("name,i,E,p", [("tiny", 30, None, 0.5), ("reddit", 200, 150_000, 0.8),
+                                        ("wiki", 100, None, 0.8), ("lastfm", 90, 100_000, 0.9)])
+def test_mitigation_teacher_forced(dev, name, i, E, p):
+    cfg = CONFIGS[name]
+    gamma = oracle.gamma(cfg.num_nodes, *make_events(cfg, 0, E)[:3], p)
+    mit = dict(lam=0.95, gamma=gamma, n_sim=5)
+    st, sl, upd, ref, ev, (mem, mem_ts) = _teacher_forced(dev, name, i, mitigation=mit, E=E)
+    U = int(upd["num"].item())
+    n = len(ev[0])
+    win = ref["winner"]
+    rows = np.where(win % 2 == 0, win // 2, n + win // 2)  # root-layout row of each winner
+    elig = sl.elig[: 2 * n].cpu().numpy().astype(bool)[rows]
+    omega = sl.omega[: 2 * n].cpu().numpy()[rows]
+    h = sl.h[: 2 * n].cpu().numpy()[rows]
+    assert np.array_equal(elig, ref["elig"])
+    assert elig.sum() >= 3, "test should exercise eligible targets"
+    assert np.array_equal(omega, ref["omega"])
+    assert (ref["omega"][:, 0] >= 0).sum() >= 1, "test should exercise a non-empty Omega"
+    ok, err = _close(h, ref["h"])
+    assert ok, err
+    ok, err = _close(upd["mem"][:U].cpu().numpy(), ref["mem"])
+    assert ok, err
+    # all 2B target rows against the oracle's mitigation on explicit targets
+    og = oracle.Graph(CONFIGS[name].num_nodes, *make_events(CONFIGS[name], 0, E)[:3])
+    ids = np.concatenate([ev[0], ev[1]])
+    allref = og.mitigate(ids, np.concatenate([ev[2], ev[2]]), mem, mem_ts, 0.95, gamma, 5, CONFIGS[name].fanout)
+    assert np.array_equal(sl.elig[: 2 * n].cpu().numpy().astype(bool), allref["elig"])
+    assert np.array_equal(sl.omega[: 2 * n].cpu().numpy(), allref["omega"])
+    ok, err = _close(sl.h[: 2 * n].cpu().numpy(), allref["h"])
+    assert ok, err
+
+
+def test_mitigation_lambda_one_is_identity(dev):
+    mit = dict(lam=1.0, gamma=1.0, n_sim=5)
+    st, sl, upd, ref, ev, (mem, _) = _teacher_forced(dev, "tiny", 30, mitigation=mit)
+    n = len(ev[0])
+    ids = np.concatenate([ev[0], ev[1]])
+    assert np.array_equal(sl.h[: 2 * n].cpu().numpy(), mem[ids])
+
+
+# ------------------------------------------------------------------ whole streams
+def _stream(dev, name, k, schedule="exact", mitigation=None, E=None, seed=0):
+    w = make_workload(name, seed=seed, num_events=E)
+    cfg = w["cfg"]
+    sc = StageConfig(cfg.num_nodes, cfg.mem_dim, cfg.edge_dim, cfg.time_dim, cfg.fanout, cfg.batch, k,
+                     schedule=schedule, mitigation=mitigation, fetch_mail=True)
+    g = build_tcsr(cfg.num_nodes, w["src"], w["dst"], w["ts"], dev)
+    st = MemoryStage(sc, w["params"], g, dev)
+    t = {kk: _t(w[kk], dev) for kk in ("src", "dst", "ts", "neg", "ef")}
+    st.bind_resident(t["src"], t["dst"], t["ts"], t["neg"], t["ef"])
+    st.run()
+    torch.cuda.synchronize()
+    _C.check()
+    ref, vers = oracle.run_stream(cfg.num_nodes, w["src"], w["dst"], w["ts"], w["ef"], w["params"], cfg.batch, k,
+                                  schedule, mitigation=mitigation, fanout=cfg.fanout)
+    return st, ref, vers, cfg
+
+
+@pytest.mark.parametrize("name,k,schedule,E", [("tiny", 0, "exact", None), ("tiny", 1, "exact", None),
+                                               ("tiny", 2, "grouped", None), ("wiki", 1, "exact", None),
+                                               ("lastfm", 2, "exact", 120_000)])
+def test_stream_free_running(dev, name, k, schedule, E):
+    st, ref, vers, cfg = _stream(dev, name, k, schedule, E=E)
+    assert [st.versions[i] for i in range(1, len(vers) + 1)] == vers.tolist()
+    assert np.array_equal(st.memory.mem_ts.cpu().numpy(), ref["mem_ts"])
+    assert np.array_equal(st.memory.mail_ts.cpu().numpy(), ref["mail_ts"])
+    g = st.memory.mem.cpu().numpy().astype(np.float64)
+    o = ref["mem"].astype(np.float64)
+    rel = np.linalg.norm(g - o, axis=1) / np.maximum(np.linalg.norm(o, axis=1), 1e-3)
+    print(f"{name} k={k} {schedule}: free-running row-rel max {rel.max():.3g} p99 {np.quantile(rel, 0.99):.3g}")
+    assert rel.max() <= 1e-4
+    Dm = cfg.mail_dim
+    ok, err = _close(st.memory.mail.cpu().numpy()[:, :Dm], ref["mail"], rtol=1e-4, atol=1e-5)
+    assert ok, err
+
+
+def test_stream_mitigation_reddit_shaped(dev):
+    cfg = CONFIGS["reddit"]
+    E = 60_000
+    src, dst, ts, _ = make_events(cfg, 0, E)
+    gamma = oracle.gamma(cfg.num_nodes, src, dst, ts, 0.99)
+    mit = dict(lam=0.95, gamma=gamma, n_sim=5)
+    st, ref, vers, cfg = _stream(dev, "reddit", 2, mitigation=mit, E=E)
+    assert np.array_equal(st.memory.mem_ts.cpu().numpy(), ref["mem_ts"])
+    g = st.memory.mem.cpu().numpy().astype(np.float64)
+    o = ref["mem"].astype(np.float64)
+    rel = np.linalg.norm(g - o, axis=1) / np.maximum(np.linalg.norm(o, axis=1), 1e-3)
+    print(f"reddit k=2 MSPipe-S: free-running row-rel max {rel.max():.3g}")
+    assert rel.max() <= 1e-4
+
+
+def test_bias_only_closed_form_on_gpu(dev):
+    """P4 on the GPU path: W = 0, b_in = c => mem[w] = tanh(c)(1 - 2^-m_w),
+    m_w from the integer replay of the same schedule (independent of the oracle)."""
+    cfg = CONFIGS["tiny"]
+    E, B, k = 4000, 200, 2
+    src, dst, ts, neg = make_events(cfg, 5, E)
+    M, He, Dt, c = cfg.mem_dim, cfg.edge_dim, cfg.time_dim, 0.9
+    p = dict(w_ih=np.zeros((3 * M, 2 * M + He + Dt), np.float32), w_hh=np.zeros((3 * M, M), np.float32),
+             b_ih=np.zeros(3 * M, np.float32), b_hh=np.zeros(3 * M, np.float32),
+             time_w=np.ones(Dt, np.float32), time_b=np.zeros(Dt, np.float32))
+    p["b_ih"][2 * M:] = c
+    g = build_tcsr(cfg.num_nodes, src, dst, ts, dev)
+    st = MemoryStage(StageConfig(cfg.num_nodes, M, He, Dt, 10, B, k), p, g, dev)
+    ef = edge_features(5, 0, E, He)
+    st.bind_resident(*(_t(a, dev) for a in (src, dst, ts, neg, ef)))
+    st.run()
+    hist = [np.zeros(cfg.num_nodes, np.int64)]
+    for i in range(1, E // B + 1):
+        snap = hist[max(0, i - 1 - k)]
+        live = hist[-1].copy()
+        for a in range((i - 1) * B, i * B):
+            for w in (src[a], dst[a]):
+                live[w] = snap[w] + 1
+        hist.append(live)
+    want = np.tanh(c) * (1.0 - 2.0 ** (-hist[-1].astype(np.float64)))
+    ok, err = _close(st.memory.mem.cpu().numpy(), np.broadcast_to(want[:, None], (cfg.num_nodes, M)))
+    assert ok, err
+
+
+# ------------------------------------------------------------------ ABI contract
+def test_abi_staleness_and_order_errors(dev):
+    cfg = CONFIGS["tiny"]
+    src, dst, ts, neg = make_events(cfg, 0, 1000)
+    g = build_tcsr(cfg.num_nodes, src, dst, ts, dev)
+    st = MemoryStage(StageConfig(cfg.num_nodes, 100, 172, 100, 10, 200, 1), gru_params(100, 372, 100), g, dev)
+    ids = torch.zeros(4, dtype=torch.int32, device=dev)
+    om = torch.empty((4, 100), device=dev)
+    ots = torch.empty(4, dtype=torch.float64, device=dev)
+    assert _C.memory_fetch(st.memory, 1, ids, om, ots) == 0
+    assert _C.memory_fetch(st.memory, 2, ids, om, ots) == 0  # k = 1: version 0 is fresh enough for i = 2
+    with pytest.raises(_C.MspipeError) as e:
+        _C.memory_fetch(st.memory, 3, ids, om, ots)  # needs committed >= 1
+    assert e.value.status == _C.ESTALE
+    upd = _C.alloc_update(200, 100, st.memory.mail_stride, dev)
+    with pytest.raises(_C.MspipeError) as e:
+        _C.memory_writeback(st.memory, 2, upd)
+    assert e.value.status == _C.EORDER
+    _C.memory_writeback(st.memory, 1, upd)  # num = 0 rows
+    assert st.memory.committed == 1
+    with pytest.raises(_C.MspipeError) as e:
+        _C.memory_fetch(st.memory, 1, ids, om, ots)  # would read a version newer than i - 1
+    assert e.value.status == _C.ESTALE
+
+
+def test_cuda_graph_replay_equals_eager(dev):
+    w = make_workload("tiny", seed=3, num_events=3000)
+    cfg = w["cfg"]
+    outs = []
+    for use_graph in (False, True):
+        sc = StageConfig(cfg.num_nodes, cfg.mem_dim, cfg.edge_dim, cfg.time_dim, cfg.fanout, cfg.batch, 1)
+        g = build_tcsr(cfg.num_nodes, w["src"], w["dst"], w["ts"], dev)
+        st = MemoryStage(sc, w["params"], g, dev)
+        t = {kk: _t(w[kk], dev) for kk in ("src", "dst", "ts", "neg", "ef")}
+        st.bind_resident(t["src"], t["dst"], t["ts"], t["neg"], t["ef"])
+        if use_graph:
+            steps = st.step_ops()
+            s = torch.cuda.Stream()
+            graphs = []
+            with torch.cuda.stream(s):
+                for ops in steps:
+                    gr = torch.cuda.CUDAGraph()
+                    with torch.cuda.graph(gr, stream=s):
+                        st.run_ops(ops)
+                    graphs.append(gr)
+            st.memory.reset()
+            for gr in graphs:
+                gr.replay()
+        else:
+            st.run()
+        torch.cuda.synchronize()
+        outs.append((st.memory.mem.cpu().numpy(), st.memory.mem_ts.cpu().numpy()))
+    assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
+
+
+def test_determinism_two_runs_bitwise(dev):
+    a = _stream(dev, "lastfm", 1, E=30_000)[0].memory
+    b = _stream(dev, "lastfm", 1, E=30_000)[0].memory
+    for key in ("mem", "mem_ts", "mail", "mail_ts"):
+        assert torch.equal(getattr(a, key), getattr(b, key)), key
