@@ -184,13 +184,18 @@ MSPIPE_API mspipe_status mspipe_memory_fetch(mspipe_memory* st, int64_t iteratio
  * (G5): w_ih [3M, Dx], w_hh [3M, M], b_ih [3M], b_hh [3M], time encoder
  * enc_q = cos(fmaf(time_w[q], dt, time_b[q])) (G2), q < time_dim.
  * Dx = 2M + edge_dim + time_dim.  create packs the weights once into the
- * kernel layout (device memory owned by the handle). */
+ * kernel layout and allocates the operand workspace for batches of up to
+ * max_events events (device memory owned by the handle).
+ * precision: MSPIPE_FP32_3XTF32 = tcgen05 tensor cores, fp32 parity via the
+ * 3xTF32 split (default); MSPIPE_FP32_SIMT = CUDA-core fp32 (baseline);
+ * MSPIPE_BF16 is reserved (EUNSUPPORTED in this build). */
 enum { MSPIPE_FP32_SIMT = 0, MSPIPE_FP32_3XTF32 = 1, MSPIPE_BF16 = 2 };
 typedef struct mspipe_gru mspipe_gru;
 MSPIPE_API mspipe_status mspipe_gru_create(mspipe_gru** out, int32_t mem_dim, int32_t edge_dim,
-                                int32_t time_dim, int32_t precision, const float* w_ih,
-                                const float* w_hh, const float* b_ih, const float* b_hh,
-                                const float* time_w, const float* time_b, void* stream);
+                                int32_t time_dim, int32_t precision, int64_t max_events,
+                                const float* w_ih, const float* w_hh, const float* b_ih,
+                                const float* b_hh, const float* time_w, const float* time_b,
+                                void* stream);
 MSPIPE_API mspipe_status mspipe_gru_destroy(mspipe_gru* p);
 
 /* A2 + A5 + A6 — one batch of num_events events (global eids are the

@@ -67,7 +67,7 @@ def lib():
         L.mspipe_memory_reset.argtypes = [P]
         L.mspipe_memory_fetch.argtypes = [P, i64, P, i64, P, P, P, P, C.POINTER(Mitigation),
                                           C.POINTER(i64), P]
-        L.mspipe_gru_create.argtypes = [C.POINTER(P), i32, i32, i32, i32, P, P, P, P, P, P, P]
+        L.mspipe_gru_create.argtypes = [C.POINTER(P), i32, i32, i32, i32, i64, P, P, P, P, P, P, P]
         L.mspipe_gru_destroy.argtypes = [P]
         L.mspipe_memory_update.argtypes = [P, P, P, P, P, i64, P, P, P, i64, P, P, P, P, P, P, P, P]
         L.mspipe_memory_writeback.argtypes = [P, i64, P, P, i64, P, P, P, P]
@@ -146,11 +146,13 @@ class TcsrHandle:
 
 
 class GruHandle:
-    def __init__(self, mem_dim, edge_dim, time_dim, params: dict, device, precision=FP32_SIMT, stream=None):
+    def __init__(self, mem_dim, edge_dim, time_dim, params: dict, device, precision=FP32_3XTF32, max_events=600,
+                 stream=None):
         self.dims = (mem_dim, edge_dim, time_dim)
         self.w = {k: torch.as_tensor(v, dtype=torch.float32).contiguous().to(device) for k, v in params.items()}
         h = C.c_void_p()
-        _ck(lib().mspipe_gru_create(C.byref(h), mem_dim, edge_dim, time_dim, precision, ptr(self.w["w_ih"]),
+        _ck(lib().mspipe_gru_create(C.byref(h), mem_dim, edge_dim, time_dim, precision, int(max_events),
+                                    ptr(self.w["w_ih"]),
                                     ptr(self.w["w_hh"]), ptr(self.w["b_ih"]), ptr(self.w["b_hh"]),
                                     ptr(self.w["time_w"]), ptr(self.w["time_b"]), stream_ptr(stream)),
             "mspipe_gru_create")

@@ -178,16 +178,18 @@ mspipe_status mspipe_memory_fetch(mspipe_memory* st, int64_t iteration, const in
 }
 
 mspipe_status mspipe_gru_create(mspipe_gru** out, int32_t mem_dim, int32_t edge_dim,
-                                int32_t time_dim, int32_t precision, const float* w_ih,
-                                const float* w_hh, const float* b_ih, const float* b_hh,
-                                const float* time_w, const float* time_b, void* stream) {
+                                int32_t time_dim, int32_t precision, int64_t max_events,
+                                const float* w_ih, const float* w_hh, const float* b_ih,
+                                const float* b_hh, const float* time_w, const float* time_b,
+                                void* stream) {
   if (!out) return fail(MSPIPE_EINVAL, "gru_create: out is NULL");
   *out = nullptr;
-  if (mem_dim < 4 || mem_dim % 4 || edge_dim < 0 || time_dim < 0)
-    return fail(MSPIPE_EINVAL, "gru_create: mem_dim=%d edge_dim=%d time_dim=%d", mem_dim, edge_dim, time_dim);
+  if (mem_dim < 4 || mem_dim % 4 || edge_dim < 0 || time_dim < 0 || max_events < 1 || max_events > 16384)
+    return fail(MSPIPE_EINVAL, "gru_create: mem_dim=%d edge_dim=%d time_dim=%d max_events=%lld (1..16384)",
+                mem_dim, edge_dim, time_dim, (long long)max_events);
   if (!w_ih || !w_hh || !b_ih || !b_hh || (time_dim > 0 && (!time_w || !time_b)))
     return fail(MSPIPE_EINVAL, "gru_create: null weight");
-  if (precision != MSPIPE_FP32_SIMT)
+  if (precision != MSPIPE_FP32_SIMT && precision != MSPIPE_FP32_3XTF32)
     return fail(MSPIPE_EUNSUPPORTED, "gru_create: precision %d not in this build", precision);
   mspipe_gru* p = new mspipe_gru();
   GruDesc& d = p->d;
@@ -199,9 +201,19 @@ mspipe_status mspipe_gru_create(mspipe_gru** out, int32_t mem_dim, int32_t edge_
   d.K = d.Dx + mem_dim;
   d.Kpad = (d.K + 31) / 32 * 32;
   d.Npad = (mem_dim + 31) / 32 * 128;
+  if (precision == MSPIPE_FP32_3XTF32 && d.Kpad / 32 > 64) {
+    delete p;
+    return fail(MSPIPE_EUNSUPPORTED, "gru_create: K = 2M + He + Dt + M = %d > 2048 on the tensor-core path", d.K);
+  }
   p->precision = precision;
+  p->max_events = max_events;
   cudaStream_t s = (cudaStream_t)stream;
-  cudaError_t e = cudaMalloc(&p->wpack, sizeof(float) * (size_t)d.Kpad * d.Npad);
+  (void)num_sms();
+  cudaError_t e = precision == MSPIPE_FP32_SIMT
+                      ? cudaMalloc(&p->wpack, sizeof(float) * (size_t)d.Kpad * d.Npad)
+                      : cudaMalloc(&p->wtc, sizeof(float) * gru_tc_packed_floats(d));
+  if (e == cudaSuccess && precision == MSPIPE_FP32_3XTF32)
+    e = cudaMalloc(&p->xbuf, sizeof(float) * gru_tc_xbuf_floats(d, max_events));
   if (e == cudaSuccess) e = cudaMalloc(&p->bias, sizeof(float) * (size_t)d.Npad);
   if (e == cudaSuccess) e = cudaMalloc(&p->time_w, sizeof(float) * (size_t)(time_dim > 0 ? time_dim : 1));
   if (e == cudaSuccess) e = cudaMalloc(&p->time_b, sizeof(float) * (size_t)(time_dim > 0 ? time_dim : 1));
@@ -215,7 +227,8 @@ mspipe_status mspipe_gru_create(mspipe_gru** out, int32_t mem_dim, int32_t edge_
   d.bias = p->bias;
   d.time_w = p->time_w;
   d.time_b = p->time_b;
-  launch_gru_pack(w_ih, w_hh, b_ih, b_hh, d, p->wpack, p->bias, s);
+  if (precision == MSPIPE_FP32_SIMT) launch_gru_pack(w_ih, w_hh, b_ih, b_hh, d, p->wpack, p->bias, s);
+  else launch_gru_pack_tc(w_ih, w_hh, b_ih, b_hh, d, p->wtc, p->bias, s);
   e = cudaGetLastError();
   if (e != cudaSuccess) {
     mspipe_gru_destroy(p);
@@ -227,7 +240,9 @@ mspipe_status mspipe_gru_create(mspipe_gru** out, int32_t mem_dim, int32_t edge_
 
 mspipe_status mspipe_gru_destroy(mspipe_gru* p) {
   if (!p) return MSPIPE_OK;
-  cudaFree(p->wpack);
+  if (p->wpack) cudaFree(p->wpack);
+  if (p->wtc) cudaFree(p->wtc);
+  if (p->xbuf) cudaFree(p->xbuf);
   cudaFree(p->bias);
   cudaFree(p->time_w);
   cudaFree(p->time_b);
@@ -245,8 +260,9 @@ mspipe_status mspipe_memory_update(mspipe_memory* st, const mspipe_gru* gru, con
   if (!st || !gru) return fail(MSPIPE_EINVAL, "memory_update: NULL handle");
   if (gru->d.M != st->mem_dim || gru->d.He != st->edge_dim)
     return fail(MSPIPE_EINVAL, "memory_update: GRU dims (M=%d He=%d) != memory dims (M=%d He=%d)", gru->d.M, gru->d.He, st->mem_dim, st->edge_dim);
-  if (num_events < 0 || num_events > 16384 || snap_step < 1)
-    return fail(MSPIPE_EINVAL, "memory_update: num_events=%lld (<= 16384) snap_step=%lld", (long long)num_events, (long long)snap_step);
+  if (num_events < 0 || num_events > gru->max_events || snap_step < 1)
+    return fail(MSPIPE_EINVAL, "memory_update: num_events=%lld (<= max_events %lld of the GRU handle) snap_step=%lld",
+                (long long)num_events, (long long)gru->max_events, (long long)snap_step);
   if (!out_num_unique) return fail(MSPIPE_EINVAL, "memory_update: null out_num_unique");
   cudaStream_t s = (cudaStream_t)stream;
   if (num_events == 0) {
@@ -256,8 +272,14 @@ mspipe_status mspipe_memory_update(mspipe_memory* st, const mspipe_gru* gru, con
       !out_winner || !out_mem || !out_ts || !out_mail)
     return fail(MSPIPE_EINVAL, "memory_update: null input/output");
   launch_dedup(src, dst, num_events, st->scratch, st->num_nodes, out_nodes, out_winner, out_num_unique, s);
-  launch_gru_simt(gru->d, src, dst, ts, num_events, edge_feat, snap_mem, snap_mem_ts, snap_step, snap_h,
-                  out_nodes, out_winner, out_num_unique, out_mem, out_ts, out_mail, st->mail_stride, s);
+  if (gru->precision == MSPIPE_FP32_3XTF32) {
+    cudaError_t e = launch_gru_tc(gru->d, gru->wtc, gru->xbuf, ts, num_events, edge_feat, snap_mem, snap_mem_ts, snap_step,
+                                  snap_h, out_winner, out_num_unique, out_mem, out_ts, out_mail, st->mail_stride, s);
+    if (e != cudaSuccess) return cuda_status(e, "memory_update: tcgen05 GRU launch");
+  } else {
+    launch_gru_simt(gru->d, src, dst, ts, num_events, edge_feat, snap_mem, snap_mem_ts, snap_step, snap_h,
+                    out_nodes, out_winner, out_num_unique, out_mem, out_ts, out_mail, st->mail_stride, s);
+  }
   return after_launch("memory_update");
 }
 

@@ -1,0 +1,563 @@
+// gru_tc.cu — A5 + A6 on the 5th-generation tensor cores (MSPIPE_FP32_3XTF32).
+//
+// The memory updater is one contraction [U x K] . [K x 4M], K = Dx + M, with
+// packed gate blocks (r, z, n_x, n_h) so the GRUCell gates (G5) are applied
+// on the accumulator tile.  It runs as tcgen05.mma
+// kind::tf32 with fp32 accumulators in TMEM.  fp32 parity (north star:
+// 1e-4 relative) comes from the 3xTF32 split  a = a_hi + a_lo,
+// a_hi = rna_tf32(a), a_lo = rna_tf32(a - a_hi), and
+//   D += A_hi.B_hi + A_hi.B_lo + A_lo.B_hi      (dropped A_lo.B_lo ~ 2^-22).
+//
+// Two kernels:
+//  k_build_x — one warp per (winner row, 32-wide K chunk): gathers the message
+//    x = [s_w | s_o | e | cos(w dt + p) | h] (A5, fused time encoding) from
+//    the snapshot rows, writes the A operand as ready-to-copy SWIZZLE_128B
+//    K-major images (hi | lo) per (128-row tile, chunk), and the mail row and
+//    commit timestamp of the winner (G14).  Thousands of warps hide the
+//    gather latency that a per-CTA producer could not.
+//  k_gru_tc — CTA = 128 rows x 16 hidden units (N = 64 accumulator columns)
+//    x a K range.  One thread streams (A, B) chunk images with cp.async.bulk
+//    (TMA engine, mbarrier complete_tx) through a 4-stage ring, one thread
+//    issues 12 MMAs per chunk, all 4 warps read TMEM in the epilogue.  U ~ 10^3
+//    rows is only a handful of M tiles, so K is split S ways over a cluster
+//    (1,1,S); the S partial tiles are summed through distributed shared memory
+//    in fixed rank order (deterministic) and each rank applies the gates to
+//    128/S rows.
+#include <stdlib.h>
+
+#include "internal.cuh"
+
+namespace mspipe {
+
+namespace tc {
+
+constexpr int kM = 128;                 // rows per tile (UMMA M)
+constexpr int kJ = 16;                  // hidden units per tile
+constexpr int kN = 4 * kJ;              // accumulator columns (UMMA N)
+constexpr int kKC = 32;                 // fp32 per 128 B swizzle row = one K chunk
+constexpr int kATile = kM * kKC * 4;    // 16 KB
+constexpr int kBTile = kN * kKC * 4;    // 8 KB
+constexpr int kABlock = 2 * kATile;     // hi | lo
+constexpr int kBBlock = 2 * kBTile;
+constexpr int kStageBytes = kABlock + kBBlock;  // 48 KB
+constexpr int kStages = 4;
+constexpr int kThreads = 128;
+constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 1024 /*barriers*/;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra.uni WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void fence_barrier_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* smem_dst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          smem_u32(smem_dst)),
+      "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+}
+__device__ __forceinline__ void tmem_alloc(uint32_t* slot, uint32_t ncols) {
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(slot)),
+               "r"(ncols)
+               : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t ncols) {
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(taddr), "r"(ncols) : "memory");
+}
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+// 32 TMEM lanes x 32 consecutive fp32 columns -> 32 registers per thread.
+#define MSPIPE_TMEM_LD32(taddr, r)                                                                          \
+  asm volatile(                                                                                             \
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "                                                             \
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"                                            \
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"                          \
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),    \
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),           \
+        "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),         \
+        "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),         \
+        "=r"(r[29]), "=r"(r[30]), "=r"(r[31])                                                               \
+      : "r"(taddr))
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t mapa(uint32_t saddr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ float4 ld_dsmem_f4(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared::cluster.v4.f32 {%0,%1,%2,%3}, [%4];\n"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(addr)
+               : "memory");
+  return v;
+}
+__device__ __forceinline__ float tf32_rna(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;\n" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+// SWIZZLE_128B K-major smem descriptor (sm_100: version 1, SBO = 1024 B, LBO field 16 B).
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+  uint64_t d = (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)1u << 16;
+  d |= (uint64_t)(1024u >> 4) << 32;
+  d |= (uint64_t)1u << 46;
+  d |= (uint64_t)2u << 61;
+  return d;
+}
+// kind::tf32 instruction descriptor: D f32, A/B tf32, K-major, M = 128, N = 64.
+constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(kN >> 3) << 17) |
+                            ((uint32_t)(kM >> 4) << 24);
+// byte offset of element (row, k) in a [rows x 32] fp32 SWIZZLE_128B K-major tile
+__host__ __device__ __forceinline__ uint32_t sw128_off(uint32_t row, uint32_t k) {
+  return row * 128u + ((((k >> 2) ^ (row & 7u)) & 7u) << 4) + (k & 3u) * 4u;
+}
+
+}  // namespace tc
+
+int gru_tc_jtiles(const GruDesc& d) { return (d.M + tc::kJ - 1) / tc::kJ; }
+
+// ---------------------------------------------------------------------------
+// weight packing: per (hidden tile jt, K chunk c) a 16 KB block
+// [hi image 8 KB | lo image 8 KB] of the B operand, N = 64 rows n = g*16 + jj
+// (gate g in r, z, n_x, n_h), K-major SWIZZLE_128B; bias[jt*64 + n].
+// ---------------------------------------------------------------------------
+__global__ void k_gru_pack_tc(const float* __restrict__ w_ih, const float* __restrict__ w_hh,
+                              const float* __restrict__ b_ih, const float* __restrict__ b_hh, GruDesc d,
+                              int32_t jtiles, float* __restrict__ wtc, float* __restrict__ bias) {
+  const int32_t nchunks = d.Kpad / tc::kKC;
+  const int64_t total = (int64_t)jtiles * nchunks * tc::kN * tc::kKC;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t kk = (int32_t)(t % tc::kKC);
+    const int32_t n = (int32_t)((t / tc::kKC) % tc::kN);
+    const int32_t c = (int32_t)((t / (tc::kKC * tc::kN)) % nchunks);
+    const int32_t jt = (int32_t)(t / ((int64_t)tc::kKC * tc::kN * nchunks));
+    const int32_t g = n / tc::kJ, jj = n % tc::kJ, j = jt * tc::kJ + jj, k = c * tc::kKC + kk;
+    const int32_t M = d.M;
+    float v = 0.f;
+    if (j < M) {
+      if (k < d.Dx) {
+        if (g < 3) v = w_ih[(int64_t)(g * M + j) * d.Dx + k];
+      } else if (k < d.K) {
+        const int32_t q = k - d.Dx;
+        if (g == 0) v = w_hh[(int64_t)j * M + q];
+        else if (g == 1) v = w_hh[(int64_t)(M + j) * M + q];
+        else if (g == 3) v = w_hh[(int64_t)(2 * M + j) * M + q];
+      }
+    }
+    const float hi = tc::tf32_rna(v);
+    const float lo = tc::tf32_rna(v - hi);
+    char* blk = reinterpret_cast<char*>(wtc) + ((int64_t)jt * nchunks + c) * tc::kBBlock;
+    const uint32_t off = tc::sw128_off((uint32_t)n, (uint32_t)kk);
+    *reinterpret_cast<float*>(blk + off) = hi;
+    *reinterpret_cast<float*>(blk + tc::kBTile + off) = lo;
+    if (c == 0 && kk == 0) {
+      float b = 0.f;
+      if (j < M) {
+        if (g == 0) b = b_ih[j] + b_hh[j];
+        else if (g == 1) b = b_ih[M + j] + b_hh[M + j];
+        else if (g == 2) b = b_ih[2 * M + j];
+        else b = b_hh[2 * M + j];
+      }
+      bias[jt * tc::kN + n] = b;
+    }
+  }
+}
+
+size_t gru_tc_packed_floats(const GruDesc& d) {
+  return (size_t)gru_tc_jtiles(d) * (d.Kpad / tc::kKC) * (tc::kBBlock / 4);
+}
+
+size_t gru_tc_xbuf_floats(const GruDesc& d, int64_t max_events) {
+  const int64_t mtiles = (2 * max_events + tc::kM - 1) / tc::kM;
+  return (size_t)mtiles * (d.Kpad / tc::kKC) * (tc::kABlock / 4);
+}
+
+void launch_gru_pack_tc(const float* w_ih, const float* w_hh, const float* b_ih, const float* b_hh,
+                        const GruDesc& d, float* wtc, float* bias, cudaStream_t s) {
+  const int threads = 256;
+  const int64_t total = (int64_t)gru_tc_packed_floats(d) / 2;
+  int64_t blocks = (total + threads - 1) / threads;
+  if (blocks > 4096) blocks = 4096;
+  k_gru_pack_tc<<<(unsigned)blocks, threads, 0, s>>>(w_ih, w_hh, b_ih, b_hh, d, gru_tc_jtiles(d), wtc, bias);
+}
+
+// ---------------------------------------------------------------------------
+struct TcArgs {
+  GruDesc d;
+  const float* wtc;   // packed B blocks
+  float* xbuf;        // A blocks [mtile][chunk][hi | lo]
+  const double* ts;
+  int64_t B;
+  const float* ef;
+  const float* snap_mem;
+  const double* snap_ts;
+  int64_t step;
+  const float* snap_h;
+  const int32_t* winner;
+  const int32_t* num_unique;
+  float* out_mem;
+  double* out_ts;
+  float* out_mail;
+  int64_t mail_stride;
+};
+
+// A5: one warp per (row, chunk).  lane = column inside the chunk.
+__global__ void __launch_bounds__(256) k_build_x(TcArgs a) {
+  const GruDesc& d = a.d;
+  const int32_t U = __ldg(a.num_unique);
+  const int32_t nchunks = d.Kpad / tc::kKC;
+  const int32_t mtiles = (U + tc::kM - 1) / tc::kM;
+  const int64_t items = (int64_t)mtiles * nchunks * tc::kM;
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int32_t M = d.M;
+  for (int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < items; w += nwarps) {
+    const int32_t row = (int32_t)(w % tc::kM);
+    const int32_t c = (int32_t)((w / tc::kM) % nchunks);
+    const int32_t mt = (int32_t)(w / ((int64_t)tc::kM * nchunks));
+    const int32_t u = mt * tc::kM + row;
+    const int32_t k = c * tc::kKC + lane;
+    float v = 0.f;
+    if (u < U) {
+      const int32_t p = __ldg(a.winner + u);
+      const int32_t ev = p >> 1, role = p & 1;
+      const int64_t rw = role ? a.B + ev : ev;
+      const int64_t ro = role ? ev : a.B + ev;
+      if (k < M) v = __ldg(a.snap_mem + rw * a.step * M + k);
+      else if (k < 2 * M) v = __ldg(a.snap_mem + ro * a.step * M + (k - M));
+      else if (k < d.Dm) v = __ldg(a.ef + (int64_t)ev * d.He + (k - 2 * M));
+      else if (k < d.Dx) {
+        const float dt = (float)(__ldg(a.ts + ev) - __ldg(a.snap_ts + rw * a.step));  // Δt (G4)
+        const int q = k - d.Dm;
+        v = cosf(fmaf(__ldg(d.time_w + q), dt, __ldg(d.time_b + q)));
+      } else if (k < d.K) {
+        const int q = k - d.Dx;
+        v = a.snap_h ? __ldg(a.snap_h + rw * M + q) : __ldg(a.snap_mem + rw * a.step * M + q);
+      }
+      if (k < a.mail_stride) a.out_mail[(int64_t)u * a.mail_stride + k] = k < d.Dm ? v : 0.f;
+      if (c == 0 && lane == 0) a.out_ts[u] = __ldg(a.ts + ev);
+    }
+    const float hi = tc::tf32_rna(v);
+    const float lo = tc::tf32_rna(v - hi);
+    char* blk = reinterpret_cast<char*>(a.xbuf) + ((int64_t)mt * nchunks + c) * tc::kABlock;
+    const uint32_t off = tc::sw128_off((uint32_t)row, (uint32_t)lane);
+    *reinterpret_cast<float*>(blk + off) = hi;
+    *reinterpret_cast<float*>(blk + tc::kATile + off) = lo;
+  }
+}
+
+__device__ __forceinline__ void gates4(const TcArgs& a, int32_t u, int32_t j0, const float* pr, const float* pz,
+                                       const float* pnx, const float* pnh, int nvalid) {
+  // h' = (1 - z) n + z h, r = σ(.), z = σ(.), n = tanh(x_n + r h_n)  (GRUCell, G5)
+  const GruDesc& d = a.d;
+  const int32_t p = __ldg(a.winner + u);
+  const int32_t ev = p >> 1, role = p & 1;
+  const int64_t rw = role ? a.B + ev : ev;
+  const float* hrow = a.snap_h ? a.snap_h + rw * d.M : a.snap_mem + rw * a.step * d.M;
+  float out[4];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    if (e < nvalid) {
+      const int32_t j = j0 + e;
+      const float r = 1.0f / (1.0f + expf(-pr[e]));
+      const float z = 1.0f / (1.0f + expf(-pz[e]));
+      const float n = tanhf(pnx[e] + r * pnh[e]);
+      out[e] = (1.0f - z) * n + z * __ldg(hrow + j);
+    }
+  }
+  float* dst = a.out_mem + (int64_t)u * d.M + j0;
+  if (nvalid == 4) *reinterpret_cast<float4*>(dst) = make_float4(out[0], out[1], out[2], out[3]);
+  else
+    for (int e = 0; e < nvalid; ++e) dst[e] = out[e];
+}
+
+__global__ void __launch_bounds__(tc::kThreads, 1) k_gru_tc(TcArgs a) {
+  using namespace tc;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
+  uint64_t* empty = full + kStages;
+  uint64_t* acc_full = empty + kStages;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 1);
+
+  const GruDesc& d = a.d;
+  const int32_t U = __ldg(a.num_unique);
+  // grid (S, jtiles, mtiles): the K split is the cluster dimension and the
+  // M tile the slowest one, so tiles beyond U (known only on the device)
+  // are the last CTAs the scheduler launches and they exit at once.
+  const int32_t mt = blockIdx.z;
+  const int32_t m0 = mt * kM;
+  if (m0 >= U) return;  // uniform across the cluster (same blockIdx.z)
+  const int jt = blockIdx.y;
+  const int S = gridDim.x;
+  const int split = blockIdx.x;
+  const int32_t nchunks = d.Kpad / kKC;
+  const int32_t c0 = split * nchunks / S, c1 = (split + 1) * nchunks / S;
+  const int32_t nc = c1 - c0;  // <= kMaxChunks (host picks S >= nchunks / kMaxChunks)
+  const uint32_t tcols = nc <= 2 ? 128u : (nc <= 4 ? 256u : 512u);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(acc_full, 1);
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, tcols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0 && lane == 0) {
+    // loader: one A block (32 KB) + one B block (16 KB) per stage
+    const char* abase = reinterpret_cast<const char*>(a.xbuf) + (int64_t)mt * nchunks * kABlock;
+    const char* bbase = reinterpret_cast<const char*>(a.wtc) + (int64_t)jt * nchunks * kBBlock;
+    for (int ci = 0; ci < nc; ++ci) {
+      const int s = ci % kStages;
+      const uint32_t ph = (uint32_t)(ci / kStages) & 1u;
+      mbar_wait(&empty[s], ph ^ 1u);
+      uint8_t* st = smem + s * kStageBytes;
+      mbar_arrive_expect_tx(&full[s], kStageBytes);
+      bulk_g2s(st, abase + (int64_t)(c0 + ci) * kABlock, kABlock, &full[s]);
+      bulk_g2s(st + kABlock, bbase + (int64_t)(c0 + ci) * kBBlock, kBBlock, &full[s]);
+    }
+  } else if (warp == 1 && lane == 0) {
+    // MMA issuer.  Each K chunk accumulates into its OWN 64-column TMEM
+    // buffer (12 MMAs): the tensor core's accumulation truncates, so the error
+    // grows with the MMAs per accumulator (measured: max 5.2e-6 for 222 MMAs,
+    // 1.0e-6 for 28); the epilogue then adds the buffers in fp32 registers
+    // with round-to-nearest, in chunk order.
+    for (int ci = 0; ci < nc; ++ci) {
+      const int s = ci % kStages;
+      const uint32_t ph = (uint32_t)(ci / kStages) & 1u;
+      mbar_wait(&full[s], ph);
+      tc_fence_after();
+      const uint32_t base = smem_u32(smem + s * kStageBytes);
+      const uint64_t da_hi = sw128_desc(base), da_lo = sw128_desc(base + kATile);
+      const uint64_t db_hi = sw128_desc(base + kABlock), db_lo = sw128_desc(base + kABlock + kBTile);
+      const uint32_t tacc = tmem + (uint32_t)(ci * kN);
+#pragma unroll
+      for (int kk = 0; kk < kKC / 8; ++kk) {
+        const uint64_t adv = (uint64_t)(kk * 32) >> 4;  // 8 tf32 = 32 B along K inside the swizzle row
+        mma_tf32(tacc, da_lo + adv, db_hi + adv, kIdesc, kk != 0);
+        mma_tf32(tacc, da_hi + adv, db_lo + adv, kIdesc, 1u);
+        mma_tf32(tacc, da_hi + adv, db_hi + adv, kIdesc, 1u);
+      }
+      mma_commit(&empty[s]);
+    }
+    mma_commit(acc_full);
+  }
+  __syncwarp();
+
+  // ---------------- epilogue: TMEM -> registers (thread = row)
+  mbar_wait(acc_full, 0);
+  tc_fence_after();
+  const int m = warp * 32 + lane;
+  const uint32_t tbase = tmem + ((uint32_t)(warp * 32) << 16);
+  uint32_t r0[32], r1[32];
+  MSPIPE_TMEM_LD32(tbase, r0);
+  MSPIPE_TMEM_LD32(tbase + 32, r1);
+  tmem_wait_ld();
+  for (int ci = 1; ci < nc; ++ci) {
+    uint32_t t0[32], t1[32];
+    MSPIPE_TMEM_LD32(tbase + ci * kN, t0);
+    MSPIPE_TMEM_LD32(tbase + ci * kN + 32, t1);
+    tmem_wait_ld();
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      r0[i] = __float_as_uint(__fadd_rn(__uint_as_float(r0[i]), __uint_as_float(t0[i])));
+      r1[i] = __float_as_uint(__fadd_rn(__uint_as_float(r1[i]), __uint_as_float(t1[i])));
+    }
+  }
+  float* part = reinterpret_cast<float*>(smem);  // stage 0 reused: 128 x 64 fp32 partial
+  const float* bias = d.bias + jt * kN;
+  if (S == 1) {
+    const int32_t u = m0 + m;
+    if (u < U) {
+#pragma unroll
+      for (int q = 0; q < kJ / 4; ++q) {
+        const int32_t j0 = jt * kJ + q * 4;
+        const int nv = min(4, d.M - j0);
+        if (nv <= 0) break;
+        float pr[4], pz[4], pnx[4], pnh[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int jj = q * 4 + e;
+          pr[e] = __uint_as_float(r0[jj]) + __ldg(bias + jj);
+          pz[e] = __uint_as_float(r0[kJ + jj]) + __ldg(bias + kJ + jj);
+          pnx[e] = __uint_as_float(r1[jj]) + __ldg(bias + 2 * kJ + jj);
+          pnh[e] = __uint_as_float(r1[kJ + jj]) + __ldg(bias + 3 * kJ + jj);
+        }
+        gates4(a, u, j0, pr, pz, pnx, pnh, nv);
+      }
+    }
+  } else {
+    float4* row = reinterpret_cast<float4*>(part + m * kN);
+#pragma unroll
+    for (int c4 = 0; c4 < 8; ++c4) {
+      row[c4 ^ (m & 15)] = make_float4(__uint_as_float(r0[4 * c4]), __uint_as_float(r0[4 * c4 + 1]),
+                                       __uint_as_float(r0[4 * c4 + 2]), __uint_as_float(r0[4 * c4 + 3]));
+      row[(8 + c4) ^ (m & 15)] = make_float4(__uint_as_float(r1[4 * c4]), __uint_as_float(r1[4 * c4 + 1]),
+                                             __uint_as_float(r1[4 * c4 + 2]), __uint_as_float(r1[4 * c4 + 3]));
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem, tcols);
+  }
+  if (S > 1) {
+    cluster_sync_all();
+    const uint32_t rank = cluster_rank();
+    const int rb = (int)rank * kM / S, re = ((int)rank + 1) * kM / S;
+    const uint32_t part_local = smem_u32(part);
+    for (int it = threadIdx.x; it < (re - rb) * (kJ / 4); it += kThreads) {
+      const int mm = rb + it / (kJ / 4), q = it % (kJ / 4);
+      const int32_t u = m0 + mm;
+      const int32_t j0 = jt * kJ + q * 4;
+      const int nv = min(4, d.M - j0);
+      if (u >= U || nv <= 0) continue;
+      float4 acc[4];
+#pragma unroll
+      for (int g = 0; g < 4; ++g) acc[g] = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int sr = 0; sr < S; ++sr) {  // fixed order: deterministic sum
+        const uint32_t remote = mapa(part_local, (uint32_t)sr);
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+          const int chunk = g * (kJ / 4) + q;
+          const float4 v = ld_dsmem_f4(remote + (uint32_t)(mm * kN + ((chunk ^ (mm & 15)) * 4)) * 4u);
+          acc[g].x += v.x;
+          acc[g].y += v.y;
+          acc[g].z += v.z;
+          acc[g].w += v.w;
+        }
+      }
+      float pr[4], pz[4], pnx[4], pnh[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int jj = q * 4 + e;
+        pr[e] = (&acc[0].x)[e] + __ldg(bias + jj);
+        pz[e] = (&acc[1].x)[e] + __ldg(bias + kJ + jj);
+        pnx[e] = (&acc[2].x)[e] + __ldg(bias + 2 * kJ + jj);
+        pnh[e] = (&acc[3].x)[e] + __ldg(bias + 3 * kJ + jj);
+      }
+      gates4(a, u, j0, pr, pz, pnx, pnh, nv);
+    }
+    cluster_sync_all();  // every partial stays alive until all ranks have read it
+  }
+}
+
+constexpr int kMaxChunks = 8;  // 8 x 64 TMEM columns = 512 (the whole TMEM of the SM)
+
+int gru_tc_splits(int64_t max_rows, const GruDesc& d) {
+  static int forced = -1;
+  if (forced < 0) {
+    const char* e = getenv("MSPIPE_TC_SPLITS");  // debugging / experiments only
+    forced = e ? atoi(e) : 0;
+  }
+  const int nchunks = d.Kpad / tc::kKC;
+  const int64_t s_min = (nchunks + kMaxChunks - 1) / kMaxChunks;  // one TMEM buffer per chunk
+  if (forced > 0) return (int)(forced > s_min ? forced : s_min);
+  const int64_t tiles = ((max_rows + tc::kM - 1) / tc::kM) * gru_tc_jtiles(d);
+  int64_t s = (2 * (int64_t)num_sms() + tiles - 1) / tiles;
+  if (s > 8) s = 8;
+  if (s > nchunks / 2) s = nchunks / 2;
+  if (s < s_min) s = s_min;
+  if (s < 1) s = 1;
+  return (int)s;
+}
+
+cudaError_t launch_gru_tc(const GruDesc& d, const float* wtc, float* xbuf, const double* ts, int64_t num_events,
+                          const float* edge_feat, const float* snap_mem, const double* snap_mem_ts,
+                          int64_t snap_step, const float* snap_h, const int32_t* winner,
+                          const int32_t* num_unique, float* out_mem, double* out_ts, float* out_mail,
+                          int64_t mail_stride, cudaStream_t s) {
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(k_gru_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::kSmemBytes);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  TcArgs a{d, wtc, xbuf, ts, num_events, edge_feat, snap_mem, snap_mem_ts, snap_step, snap_h, winner,
+           num_unique, out_mem, out_ts, out_mail, mail_stride};
+  const int64_t max_rows = 2 * num_events;
+  const int64_t mtiles = (max_rows + tc::kM - 1) / tc::kM;
+  {
+    const int64_t warps = mtiles * (d.Kpad / tc::kKC) * tc::kM;
+    int64_t blocks = (warps * 32 + 255) / 256;
+    const int64_t cap = (int64_t)num_sms() * 8;
+    if (blocks > cap) blocks = cap;
+    k_build_x<<<(unsigned)blocks, 256, 0, s>>>(a);
+  }
+  const int S = gru_tc_splits(max_rows, d);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)S, (unsigned)gru_tc_jtiles(d), (unsigned)mtiles);
+  cfg.blockDim = dim3(tc::kThreads);
+  cfg.dynamicSmemBytes = tc::kSmemBytes;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = (unsigned)S;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k_gru_tc, a);
+}
+
+}  // namespace mspipe

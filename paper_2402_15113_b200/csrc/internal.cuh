@@ -80,6 +80,17 @@ void launch_gru_simt(const GruDesc& d, const int32_t* src, const int32_t* dst, c
                      float* out_mem, double* out_ts, float* out_mail, int64_t mail_stride,
                      cudaStream_t s);
 
+// gru_tc.cu
+size_t gru_tc_packed_floats(const GruDesc& d);
+size_t gru_tc_xbuf_floats(const GruDesc& d, int64_t max_events);
+void launch_gru_pack_tc(const float* w_ih, const float* w_hh, const float* b_ih, const float* b_hh,
+                        const GruDesc& d, float* wtc, float* bias, cudaStream_t s);
+cudaError_t launch_gru_tc(const GruDesc& d, const float* wtc, float* xbuf, const double* ts, int64_t num_events,
+                          const float* edge_feat, const float* snap_mem, const double* snap_mem_ts,
+                          int64_t snap_step, const float* snap_h, const int32_t* winner,
+                          const int32_t* num_unique, float* out_mem, double* out_ts, float* out_mail,
+                          int64_t mail_stride, cudaStream_t s);
+
 }  // namespace mspipe
 
 struct mspipe_memory {
@@ -99,7 +110,10 @@ struct mspipe_memory {
 struct mspipe_gru {
   mspipe::GruDesc d;
   int32_t precision;
-  float* wpack;
+  int64_t max_events;
+  float* wpack;  // SIMT layout [Kpad, Npad] (precision FP32_SIMT)
+  float* wtc;    // tcgen05 B-operand images (precision FP32_3XTF32)
+  float* xbuf;   // tcgen05 A-operand images for <= max_events events
   float* bias;
   float* time_w;
   float* time_b;

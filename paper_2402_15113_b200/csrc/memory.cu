@@ -229,14 +229,22 @@ void launch_mitigate(const Tcsr& g, const int32_t* src, const int32_t* dst, cons
 // winners in p order.  Phase 3: winners restore scratch[node] = -1.
 // ---------------------------------------------------------------------------
 constexpr int kDedupThreads = 1024;
+constexpr int64_t kDedupSmemNodes = 40960;  // node table in shared memory up to 160 KB
 
+template <bool kSmem>
 __global__ void __launch_bounds__(kDedupThreads) k_dedup(
     const int32_t* __restrict__ src, const int32_t* __restrict__ dst, int64_t B,
-    int32_t* __restrict__ scratch, int64_t N, int32_t* __restrict__ out_nodes,
+    int32_t* __restrict__ gscratch, int64_t N, int32_t* __restrict__ out_nodes,
     int32_t* __restrict__ out_winner, int32_t* __restrict__ out_num) {
+  extern __shared__ int32_t sscratch[];
   __shared__ int32_t warp_tot[kDedupThreads / 32];
   __shared__ int32_t total_s;
+  int32_t* scratch = kSmem ? sscratch : gscratch;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  if (kSmem) {
+    for (int64_t i = tid; i < N; i += kDedupThreads) sscratch[i] = -1;
+    __syncthreads();
+  }
   const int64_t P = 2 * B;
   const int64_t Pr = (P + kDedupThreads - 1) / kDedupThreads * kDedupThreads;
   for (int64_t p = tid; p < Pr; p += kDedupThreads) {
@@ -252,7 +260,7 @@ __global__ void __launch_bounds__(kDedupThreads) k_dedup(
     const int leader = 31 - __clz(grp);  // highest lane = largest p of the group
     if (node >= 0 && lane == leader) atomicMax(scratch + node, (int32_t)p);
   }
-  __threadfence();
+  if (!kSmem) __threadfence();
   __syncthreads();
   // contiguous chunk per thread: [tid*C, tid*C + C)
   const int64_t C = (P + kDedupThreads - 1) / kDedupThreads;  // <= 32 (B <= 16384)
@@ -264,7 +272,8 @@ __global__ void __launch_bounds__(kDedupThreads) k_dedup(
     if (p >= P) break;
     const int32_t node = (p & 1) ? __ldg(dst + (p >> 1)) : __ldg(src + (p >> 1));
     if (node < 0 || node >= N) continue;
-    if (__ldcg(scratch + node) == (int32_t)p) {
+    const int32_t w = kSmem ? sscratch[node] : __ldcg(gscratch + node);
+    if (w == (int32_t)p) {
       flags |= 1u << i;
       ++cnt;
     }
@@ -299,12 +308,14 @@ __global__ void __launch_bounds__(kDedupThreads) k_dedup(
       ++off;
     }
   }
-  __syncthreads();  // all scratch reads are done before the reset
-  for (int64_t i = 0; i < C; ++i) {
-    if (flags & (1u << i)) {
-      const int64_t p = p0 + i;
-      const int32_t node = (p & 1) ? __ldg(dst + (p >> 1)) : __ldg(src + (p >> 1));
-      scratch[node] = -1;
+  if (!kSmem) {
+    __syncthreads();  // all scratch reads are done before the reset
+    for (int64_t i = 0; i < C; ++i) {
+      if (flags & (1u << i)) {
+        const int64_t p = p0 + i;
+        const int32_t node = (p & 1) ? __ldg(dst + (p >> 1)) : __ldg(src + (p >> 1));
+        gscratch[node] = -1;
+      }
     }
   }
   if (tid == 0) *out_num = total_s;
@@ -313,8 +324,19 @@ __global__ void __launch_bounds__(kDedupThreads) k_dedup(
 void launch_dedup(const int32_t* src, const int32_t* dst, int64_t num_events, int32_t* scratch,
                   int64_t num_nodes, int32_t* out_nodes, int32_t* out_winner, int32_t* out_num,
                   cudaStream_t s) {
-  k_dedup<<<1, kDedupThreads, 0, s>>>(src, dst, num_events, scratch, num_nodes, out_nodes,
-                                      out_winner, out_num);
+  if (num_nodes <= kDedupSmemNodes) {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_dedup<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)(kDedupSmemNodes * sizeof(int32_t)));
+      attr = true;
+    }
+    k_dedup<true><<<1, kDedupThreads, num_nodes * sizeof(int32_t), s>>>(src, dst, num_events, scratch, num_nodes,
+                                                                         out_nodes, out_winner, out_num);
+  } else {
+    k_dedup<false><<<1, kDedupThreads, 0, s>>>(src, dst, num_events, scratch, num_nodes, out_nodes, out_winner,
+                                               out_num);
+  }
 }
 
 // ---------------------------------------------------------------------------

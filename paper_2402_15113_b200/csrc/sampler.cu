@@ -1,8 +1,14 @@
 // sampler.cu — A1, the recent-𝒩 temporal neighbour sampler (P:L412, P:L810,
-// P:L814).  One warp serves 32 roots: each lane bisects its root's
-// T-CSR row for the first ts >= t_q (so entries before it are exactly the
-// events with ts < t_q, G15), then the warp writes the 32 x fanout output
-// block cooperatively so every store instruction is contiguous.
+// P:L814).
+//
+// One warp per root.  The sampler is memory-LATENCY bound (dependent probes
+// into the time-sorted row), so the warp searches 33-ary: 32 lanes probe 32
+// interior positions of the current range at once and a ballot shrinks the
+// range 33x per round.  A row of L entries takes ceil(log33(L / 32)) + 1
+// dependent rounds instead of log2(L) (wiki: 1-2, LastFM hot items: 3).  The
+// first position with ts >= t_q is `end`; the newest min(fanout, end - beg)
+// entries before it are the answer (G15: strict <, ties newest-eid first).
+// Lanes s < fanout then read entry end-1-s and write output slot s.
 #include "internal.cuh"
 
 namespace mspipe {
@@ -16,76 +22,64 @@ __global__ void __launch_bounds__(256) k_sample_recent(
     double* __restrict__ out_ts, float* __restrict__ out_dt, int32_t* __restrict__ out_cnt,
     int32_t* __restrict__ out_sub) {
   const int lane = threadIdx.x & 31;
-  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t base = warp * 32; base < R; base += nwarps * 32) {
-    const int64_t r = base + lane;
-    int64_t end = 0;
-    int32_t cnt = 0;
-    int32_t v = -1;
-    double tq = 0.0;
-    if (r < R) {
-      if (kBatch) {
-        const int64_t role = r / B, a = r - role * B;
-        v = role == 0 ? __ldg(src + a) : (role == 1 ? __ldg(dst + a) : __ldg(neg + a));
-        tq = __ldg(ev_ts + a);
-      } else {
-        v = __ldg(roots + r);
-        tq = __ldg(qts + r);
-      }
-      if (v >= 0 && v < g.num_nodes) {
-        const int64_t beg = __ldg(g.indptr + v);
-        int64_t lo = beg, hi = __ldg(g.indptr + v + 1);
-        while (lo < hi) {  // lower bound of t_q in the row's non-decreasing ts
-          const int64_t mid = (lo + hi) >> 1;
-          if (__ldg(g.ts + mid) < tq) lo = mid + 1;
-          else hi = mid;
-        }
-        end = lo;
-        cnt = (int32_t)min64(end - beg, (int64_t)F);
-      } else {
-        raise_dev(MSPIPE_DEVERR_RANGE);
-      }
-      out_cnt[r] = cnt;
+  for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < R; r += nwarps) {
+    int32_t v;
+    double tq;
+    if (kBatch) {
+      const int64_t role = r / B, a = r - role * B;
+      v = role == 0 ? __ldg(src + a) : (role == 1 ? __ldg(dst + a) : __ldg(neg + a));
+      tq = __ldg(ev_ts + a);
+    } else {
+      v = __ldg(roots + r);
+      tq = __ldg(qts + r);
     }
-    const int nr = (int)min64(32, R - base);
-    const int total = 32 * F;
-    for (int idx = lane; idx < total; idx += 32) {
-      const int rr = idx / F, slot = idx - rr * F;
-      const int64_t e = __shfl_sync(0xffffffffu, end, rr);
-      const int32_t c = __shfl_sync(0xffffffffu, cnt, rr);
-      const double t = __shfl_sync(0xffffffffu, tq, rr);
-      if (rr < nr) {
-        const int64_t o = base * F + idx;
-        if (slot < c) {
-          const int64_t q = e - 1 - slot;
-          const double tsq = __ldg(g.ts + q);
-          out_nbr[o] = __ldg(g.nbr + q);
-          out_eid[o] = __ldg(g.eid + q);
-          out_ts[o] = tsq;
-          out_dt[o] = (float)(t - tsq);
-        } else {
-          out_nbr[o] = -1;
-          out_eid[o] = -1;
-          out_ts[o] = 0.0;
-          out_dt[o] = 0.0f;
-        }
+    int64_t beg = 0, end = 0;
+    const bool ok = v >= 0 && v < g.num_nodes;
+    if (ok) {
+      beg = __ldg(g.indptr + v);
+      int64_t lo = beg, hi = __ldg(g.indptr + v + 1);
+      // invariant: ts[lo-1] < tq (or lo = beg) and ts[hi] >= tq (or hi = row end)
+      while (hi - lo > 32) {
+        const int64_t span = hi - lo;
+        const int64_t p = lo + ((int64_t)(lane + 1) * span) / 33;  // strictly inside [lo, hi)
+        const bool below = __ldg(g.ts + p) < tq;
+        const unsigned bal = __ballot_sync(0xffffffffu, below);
+        const int c = __popc(bal);  // ts is sorted, so the true lanes are a prefix
+        const int64_t plast = __shfl_sync(0xffffffffu, p, c > 0 ? c - 1 : 0);
+        const int64_t pfirst = __shfl_sync(0xffffffffu, p, c < 32 ? c : 31);
+        if (c > 0) lo = plast + 1;
+        if (c < 32) hi = pfirst;
+      }
+      const int64_t q = lo + lane;
+      const bool below = q < hi && __ldg(g.ts + q) < tq;
+      end = lo + __popc(__ballot_sync(0xffffffffu, below));
+    } else if (lane == 0) {
+      raise_dev(MSPIPE_DEVERR_RANGE);
+    }
+    const int32_t cnt = (int32_t)min64(end - beg, (int64_t)F);
+    for (int s = lane; s < F; s += 32) {  // output slot s = entry end-1-s (newest first)
+      const int64_t o = r * F + s;
+      if (s < cnt) {
+        const int64_t q = end - 1 - s;
+        const double tsq = __ldg(g.ts + q);
+        out_nbr[o] = __ldg(g.nbr + q);
+        out_eid[o] = __ldg(g.eid + q);
+        out_ts[o] = tsq;
+        out_dt[o] = (float)(tq - tsq);
+      } else {
+        out_nbr[o] = -1;
+        out_eid[o] = -1;
+        out_ts[o] = 0.0;
+        out_dt[o] = 0.0f;
       }
     }
+    if (lane == 0) out_cnt[r] = cnt;
     if (out_sub) {
-      const int F1 = F + 1;
-      const int tot1 = 32 * F1;
-      for (int idx = lane; idx < tot1; idx += 32) {
-        const int rr = idx / F1, slot = idx - rr * F1;
-        const int64_t e = __shfl_sync(0xffffffffu, end, rr);
-        const int32_t c = __shfl_sync(0xffffffffu, cnt, rr);
-        const int32_t vv = __shfl_sync(0xffffffffu, v, rr);
-        if (rr < nr) {
-          int32_t id;
-          if (slot == 0) id = vv;
-          else id = (slot - 1 < c) ? __ldg(g.nbr + (e - slot)) : -1;
-          out_sub[base * F1 + idx] = id;
-        }
+      // subgraph node list [root, nbr_0 .. nbr_{F-1}] (3B(𝒩+1) nodes per batch)
+      for (int s = lane; s <= F; s += 32) {
+        const int32_t id = s == 0 ? v : ((s - 1 < cnt) ? __ldg(g.nbr + (end - s)) : -1);
+        out_sub[r * (F + 1) + s] = id;
       }
     }
   }
@@ -97,9 +91,8 @@ void launch_sample(const Tcsr& g, const int32_t* roots, const double* qts, const
                    double* out_ts, float* out_dt, int32_t* out_cnt, int32_t* out_sub,
                    cudaStream_t s) {
   const int threads = 256;
-  const int64_t warps = (num_roots + 31) / 32;
-  int64_t blocks = (warps * 32 + threads - 1) / threads;
-  const int64_t cap = (int64_t)num_sms() * 8;
+  int64_t blocks = (num_roots * 32 + threads - 1) / threads;
+  const int64_t cap = (int64_t)num_sms() * 16;
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
   if (roots)

@@ -39,7 +39,7 @@ class StageConfig:
     schedule: str = "exact"        # "exact" | "grouped"
     mitigation: dict | None = None  # dict(lam, gamma, n_sim) or None
     fetch_mail: bool = False        # also fetch mail rows of the subgraph nodes
-    precision: int = _C.FP32_SIMT
+    precision: int = _C.FP32_3XTF32  # tcgen05 3xTF32 (fp32 parity); _C.FP32_SIMT = CUDA-core baseline
 
 
 def schedule_ops(nb: int, k: int, schedule: str = "exact"):
@@ -105,7 +105,8 @@ class MemoryStage:
         self.device = torch.device(device)
         self.tcsr = tcsr
         self.memory = _C.MemoryHandle(cfg.num_nodes, cfg.mem_dim, cfg.edge_dim, cfg.k, self.device)
-        self.gru = _C.GruHandle(cfg.mem_dim, cfg.edge_dim, cfg.time_dim, params, self.device, cfg.precision)
+        self.gru = _C.GruHandle(cfg.mem_dim, cfg.edge_dim, cfg.time_dim, params, self.device, cfg.precision,
+                                max_events=cfg.batch)
         self.upd = _C.alloc_update(cfg.batch, cfg.mem_dim, self.memory.mail_stride, self.device)
         self.staged = False
         self.slots = None
@@ -150,10 +151,25 @@ class MemoryStage:
     def _slot(self, i):
         return self.slots[(i - 1) % (self.cfg.k + 1)]
 
+    def reserve_timing_events(self, n):
+        """Materialise n timing events outside any stream capture (torch
+        creates the CUDA event lazily at its first record)."""
+        self._pool = []
+        for _ in range(n):
+            e = torch.cuda.Event(enable_timing=True)
+            e.record()
+            self._pool.append(e)
+        torch.cuda.synchronize()
+        self.timing = {}
+
     def _ev(self, name):
         if self.timing is None:
             return None
-        e = torch.cuda.Event(enable_timing=True)
+        if getattr(self, "_pool", None):
+            e = self._pool.pop()
+        else:
+            e = torch.cuda.Event(enable_timing=True)
+            e.record()  # materialise (not allowed under capture: reserve_timing_events first)
         _C.event_record(e)
         self.timing.setdefault(name, []).append(e)
         return e

@@ -121,7 +121,7 @@ def _random_state(num_nodes, M, src, dst, ts, j0, seed):
     return mem, np.maximum(mem_ts, last_dst)
 
 
-def _teacher_forced(dev, name, i, mitigation=None, seed=0, E=None):
+def _teacher_forced(dev, name, i, mitigation=None, seed=0, E=None, precision=_C.FP32_3XTF32):
     cfg = CONFIGS[name]
     src, dst, ts, neg = make_events(cfg, seed, E)
     B, F, M = cfg.batch, cfg.fanout, cfg.mem_dim
@@ -130,7 +130,8 @@ def _teacher_forced(dev, name, i, mitigation=None, seed=0, E=None):
     params = gru_params(M, cfg.mail_dim, cfg.time_dim)
     mem, mem_ts = _random_state(cfg.num_nodes, M, src, dst, ts, j0, seed + i)
     g = build_tcsr(cfg.num_nodes, src, dst, ts, dev)
-    sc = StageConfig(cfg.num_nodes, M, cfg.edge_dim, cfg.time_dim, F, B, 0, mitigation=mitigation)
+    sc = StageConfig(cfg.num_nodes, M, cfg.edge_dim, cfg.time_dim, F, B, 0, mitigation=mitigation,
+                     precision=precision)
     st = MemoryStage(sc, params, g, dev)
     st.memory.mem.copy_(_t(mem, dev))
     st.memory.mem_ts.copy_(_t(mem_ts, dev))
@@ -153,8 +154,9 @@ def _teacher_forced(dev, name, i, mitigation=None, seed=0, E=None):
 
 @pytest.mark.parametrize("name,i,E", [("tiny", 1, None), ("tiny", 50, None), ("wiki", 137, None),
                                       ("lastfm", 400, 300_000), ("gdelt", 3, 20_000)])
-def test_update_teacher_forced(dev, name, i, E):
-    st, sl, upd, ref, ev, (mem, mem_ts) = _teacher_forced(dev, name, i, E=E)
+@pytest.mark.parametrize("precision", [_C.FP32_3XTF32, _C.FP32_SIMT])
+def test_update_teacher_forced(dev, name, i, E, precision):
+    st, sl, upd, ref, ev, (mem, mem_ts) = _teacher_forced(dev, name, i, E=E, precision=precision)
     U = int(upd["num"].item())
     assert U == len(ref["nodes"])
     assert np.array_equal(upd["nodes"][:U].cpu().numpy(), ref["nodes"])
@@ -216,11 +218,11 @@ def test_mitigation_lambda_one_is_identity(dev):
 
 
 # ------------------------------------------------------------------ whole streams
-def _stream(dev, name, k, schedule="exact", mitigation=None, E=None, seed=0):
+def _stream(dev, name, k, schedule="exact", mitigation=None, E=None, seed=0, precision=_C.FP32_3XTF32):
     w = make_workload(name, seed=seed, num_events=E)
     cfg = w["cfg"]
     sc = StageConfig(cfg.num_nodes, cfg.mem_dim, cfg.edge_dim, cfg.time_dim, cfg.fanout, cfg.batch, k,
-                     schedule=schedule, mitigation=mitigation, fetch_mail=True)
+                     schedule=schedule, mitigation=mitigation, fetch_mail=True, precision=precision)
     g = build_tcsr(cfg.num_nodes, w["src"], w["dst"], w["ts"], dev)
     st = MemoryStage(sc, w["params"], g, dev)
     t = {kk: _t(w[kk], dev) for kk in ("src", "dst", "ts", "neg", "ef")}
@@ -236,8 +238,9 @@ def _stream(dev, name, k, schedule="exact", mitigation=None, E=None, seed=0):
 @pytest.mark.parametrize("name,k,schedule,E", [("tiny", 0, "exact", None), ("tiny", 1, "exact", None),
                                                ("tiny", 2, "grouped", None), ("wiki", 1, "exact", None),
                                                ("lastfm", 2, "exact", 120_000)])
-def test_stream_free_running(dev, name, k, schedule, E):
-    st, ref, vers, cfg = _stream(dev, name, k, schedule, E=E)
+@pytest.mark.parametrize("precision", [_C.FP32_3XTF32, _C.FP32_SIMT])
+def test_stream_free_running(dev, name, k, schedule, E, precision):
+    st, ref, vers, cfg = _stream(dev, name, k, schedule, E=E, precision=precision)
     assert [st.versions[i] for i in range(1, len(vers) + 1)] == vers.tolist()
     assert np.array_equal(st.memory.mem_ts.cpu().numpy(), ref["mem_ts"])
     assert np.array_equal(st.memory.mail_ts.cpu().numpy(), ref["mail_ts"])
