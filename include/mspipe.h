@@ -7,8 +7,9 @@
  *
  * The per-batch stage (one "iteration" i, 1-based) is, in stream order:
  *   mspipe_sample_batch / mspipe_sample_recent   A1  recent-𝒩 sampler
+ *   mspipe_memory_dedup                          A2  most-recent-message winners
  *   mspipe_memory_fetch                          A3  snapshot fetch (+A4 mitigation)
- *   mspipe_memory_update                         A2+A5+A6 dedup, message, GRU
+ *   mspipe_memory_update                         A5+A6 message, time encoding, GRU
  *   mspipe_memory_writeback                      A7  last-writer-wins commit
  *
  * Conventions (all entry points):
@@ -198,13 +199,23 @@ MSPIPE_API mspipe_status mspipe_gru_create(mspipe_gru** out, int32_t mem_dim, in
                                 void* stream);
 MSPIPE_API mspipe_status mspipe_gru_destroy(mspipe_gru* p);
 
-/* A2 + A5 + A6 — one batch of num_events events (global eids are the
- * caller's business; edge_feat holds this batch's rows [num_events, edge_dim]).
- *   Pairs: event a gives p = 2a (node src_a, other dst_a) and p = 2a+1 (node
- *   dst_a, other src_a); win(w) = max{p : node_p = w} (last event wins,
- *   S:L186; G6); negatives are never written (G7).  U winners in win order:
+/* A2 — pair expansion and most-recent-message aggregation of one batch.
+ *   Event a gives p = 2a (node src_a, other dst_a) and p = 2a+1 (node dst_a,
+ *   other src_a); win(w) = max{p : node_p = w} (the message "generated by the
+ *   graph event related to v", last event wins; G6);
+ *   negatives are never written (G7).  U winners in win order:
  *   out_nodes [<=2B] int32, out_winner [<=2B] int32 (pair index),
- *   *out_num_unique (device int32) = U.
+ *   *out_num_unique (device int32) = U.  Integer only, bit-exact,
+ *   independent of the memory state, so it may run ahead with the sampler.
+ *   num_events <= 16384. */
+MSPIPE_API mspipe_status mspipe_memory_dedup(mspipe_memory* st, const int32_t* src, const int32_t* dst,
+                                  int64_t num_events, int32_t* out_nodes, int32_t* out_winner,
+                                  int32_t* out_num_unique, void* stream);
+
+/* A5 + A6 — message build and GRU update of the U winners of one batch of
+ * num_events events (winner / num_unique from mspipe_memory_dedup; global
+ * eids are the caller's business; edge_feat holds this batch's rows
+ * [num_events, edge_dim]).
  *   Snapshot rows in root layout: row r in [0, 2B) is [src_0..src_{B-1},
  *   dst_0..dst_{B-1}][r] and lives at snap_mem + r*snap_step*mem_dim,
  *   snap_mem_ts + r*snap_step (snap_step = fanout+1 when the rows come from a
@@ -220,8 +231,8 @@ MSPIPE_API mspipe_status mspipe_memory_update(mspipe_memory* st, const mspipe_gr
                                    const int32_t* dst, const double* ts, int64_t num_events,
                                    const float* edge_feat, const float* snap_mem,
                                    const double* snap_mem_ts, int64_t snap_step,
-                                   const float* snap_h, int32_t* out_nodes, int32_t* out_winner,
-                                   int32_t* out_num_unique, float* out_mem, double* out_ts,
+                                   const float* snap_h, const int32_t* winner,
+                                   const int32_t* num_unique, float* out_mem, double* out_ts,
                                    float* out_mail, void* stream);
 
 /* A7 — last-writer-wins write-back, committing version `commit_version`

@@ -12,7 +12,7 @@ import os
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libmspipe.so")
+LIB_PATH = os.environ.get("MSPIPE_LIB") or os.path.join(_HERE, "libmspipe.so")  # override: debug builds only
 
 OK, EINVAL, ERANGE, ESTALE, EORDER, EUNSUPPORTED, ECUDA, ENCCL = 0, -1, -2, -3, -4, -5, -6, -7
 FP32_SIMT, FP32_3XTF32, BF16 = 0, 1, 2
@@ -24,7 +24,7 @@ i32, i64, f32, f64 = C.c_int32, C.c_int64, C.c_float, C.c_double
 EXPORTS = ("mspipe_abi_version", "mspipe_last_error", "mspipe_check", "mspipe_sample_recent",
            "mspipe_sample_batch", "mspipe_memory_create", "mspipe_memory_destroy",
            "mspipe_memory_committed", "mspipe_memory_reset", "mspipe_memory_fetch",
-           "mspipe_gru_create", "mspipe_gru_destroy", "mspipe_memory_update",
+           "mspipe_memory_dedup", "mspipe_gru_create", "mspipe_gru_destroy", "mspipe_memory_update",
            "mspipe_memory_writeback", "mspipe_util_event_record")
 
 
@@ -69,7 +69,8 @@ def lib():
                                           C.POINTER(i64), P]
         L.mspipe_gru_create.argtypes = [C.POINTER(P), i32, i32, i32, i32, i64, P, P, P, P, P, P, P]
         L.mspipe_gru_destroy.argtypes = [P]
-        L.mspipe_memory_update.argtypes = [P, P, P, P, P, i64, P, P, P, i64, P, P, P, P, P, P, P, P]
+        L.mspipe_memory_dedup.argtypes = [P, P, P, i64, P, P, P, P]
+        L.mspipe_memory_update.argtypes = [P, P, P, P, P, i64, P, P, P, i64, P, P, P, P, P, P, P]
         L.mspipe_memory_writeback.argtypes = [P, i64, P, P, i64, P, P, P, P]
         L.mspipe_util_event_record.argtypes = [P, P]
         if L.mspipe_abi_version() != ABI_VERSION:
@@ -219,20 +220,34 @@ def make_mitigation(g: TcsrHandle, lam, gamma, n_sim, fanout, src, dst, ts, out_
     return m
 
 
+def memory_dedup(st: MemoryHandle, src, dst, out, stream=None):
+    """A2: fills out["nodes"], out["winner"], out["num"] (device U)."""
+    _ck(lib().mspipe_memory_dedup(st.h, ptr(src), ptr(dst), src.numel(), ptr(out["nodes"]), ptr(out["winner"]),
+                                  ptr(out["num"]), stream_ptr(stream)), "mspipe_memory_dedup")
+    return out
+
+
 def memory_update(st: MemoryHandle, gru: GruHandle, src, dst, ts, edge_feat, snap_mem, snap_mem_ts, snap_step,
                   out, snap_h=None, stream=None):
+    """A5+A6: reads out["winner"], out["num"] (from memory_dedup); fills out["mem"], out["ts"], out["mail"]."""
     _ck(lib().mspipe_memory_update(st.h, gru.h, ptr(src), ptr(dst), ptr(ts), src.numel(), ptr(edge_feat),
-                                   ptr(snap_mem), ptr(snap_mem_ts), int(snap_step), ptr(snap_h), ptr(out["nodes"]),
+                                   ptr(snap_mem), ptr(snap_mem_ts), int(snap_step), ptr(snap_h),
                                    ptr(out["winner"]), ptr(out["num"]), ptr(out["mem"]), ptr(out["ts"]),
                                    ptr(out["mail"]), stream_ptr(stream)), "mspipe_memory_update")
     return out
 
 
-def alloc_update(num_events, mem_dim, mail_stride, device):
+def alloc_dedup(num_events, device):
     n = 2 * num_events
     return dict(nodes=torch.empty((n,), dtype=torch.int32, device=device),
                 winner=torch.empty((n,), dtype=torch.int32, device=device),
-                num=torch.zeros((1,), dtype=torch.int32, device=device),
+                num=torch.zeros((1,), dtype=torch.int32, device=device))
+
+
+def alloc_update(num_events, mem_dim, mail_stride, device):
+    """Dedup outputs + GRU outputs in one dict (the layout memory_writeback reads)."""
+    n = 2 * num_events
+    return dict(**alloc_dedup(num_events, device),
                 mem=torch.empty((n, mem_dim), dtype=torch.float32, device=device),
                 ts=torch.empty((n,), dtype=torch.float64, device=device),
                 mail=torch.empty((n, mail_stride), dtype=torch.float32, device=device))

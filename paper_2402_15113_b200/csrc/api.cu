@@ -250,12 +250,26 @@ mspipe_status mspipe_gru_destroy(mspipe_gru* p) {
   return MSPIPE_OK;
 }
 
+mspipe_status mspipe_memory_dedup(mspipe_memory* st, const int32_t* src, const int32_t* dst,
+                                  int64_t num_events, int32_t* out_nodes, int32_t* out_winner,
+                                  int32_t* out_num_unique, void* stream) {
+  if (!st) return fail(MSPIPE_EINVAL, "memory_dedup: NULL handle");
+  if (num_events < 0 || num_events > 16384)
+    return fail(MSPIPE_EINVAL, "memory_dedup: num_events=%lld (0..16384)", (long long)num_events);
+  if (!out_num_unique) return fail(MSPIPE_EINVAL, "memory_dedup: null out_num_unique");
+  cudaStream_t s = (cudaStream_t)stream;
+  if (num_events == 0) return cuda_status(cudaMemsetAsync(out_num_unique, 0, sizeof(int32_t), s), "memory_dedup");
+  if (!src || !dst || !out_nodes || !out_winner) return fail(MSPIPE_EINVAL, "memory_dedup: null input/output");
+  launch_dedup(src, dst, num_events, st->scratch, st->num_nodes, out_nodes, out_winner, out_num_unique, s);
+  return after_launch("memory_dedup");
+}
+
 mspipe_status mspipe_memory_update(mspipe_memory* st, const mspipe_gru* gru, const int32_t* src,
                                    const int32_t* dst, const double* ts, int64_t num_events,
                                    const float* edge_feat, const float* snap_mem,
                                    const double* snap_mem_ts, int64_t snap_step,
-                                   const float* snap_h, int32_t* out_nodes, int32_t* out_winner,
-                                   int32_t* out_num_unique, float* out_mem, double* out_ts,
+                                   const float* snap_h, const int32_t* winner,
+                                   const int32_t* num_unique, float* out_mem, double* out_ts,
                                    float* out_mail, void* stream) {
   if (!st || !gru) return fail(MSPIPE_EINVAL, "memory_update: NULL handle");
   if (gru->d.M != st->mem_dim || gru->d.He != st->edge_dim)
@@ -263,15 +277,14 @@ mspipe_status mspipe_memory_update(mspipe_memory* st, const mspipe_gru* gru, con
   if (num_events < 0 || num_events > gru->max_events || snap_step < 1)
     return fail(MSPIPE_EINVAL, "memory_update: num_events=%lld (<= max_events %lld of the GRU handle) snap_step=%lld",
                 (long long)num_events, (long long)gru->max_events, (long long)snap_step);
-  if (!out_num_unique) return fail(MSPIPE_EINVAL, "memory_update: null out_num_unique");
   cudaStream_t s = (cudaStream_t)stream;
-  if (num_events == 0) {
-    return cuda_status(cudaMemsetAsync(out_num_unique, 0, sizeof(int32_t), s), "memory_update");
-  }
-  if (!src || !dst || !ts || (st->edge_dim > 0 && !edge_feat) || !snap_mem || !snap_mem_ts || !out_nodes ||
-      !out_winner || !out_mem || !out_ts || !out_mail)
+  if (num_events == 0) return MSPIPE_OK;
+  if (!src || !dst || !ts || (st->edge_dim > 0 && !edge_feat) || !snap_mem || !snap_mem_ts || !winner ||
+      !num_unique || !out_mem || !out_ts || !out_mail)
     return fail(MSPIPE_EINVAL, "memory_update: null input/output");
-  launch_dedup(src, dst, num_events, st->scratch, st->num_nodes, out_nodes, out_winner, out_num_unique, s);
+  int32_t* out_winner = const_cast<int32_t*>(winner);
+  int32_t* out_num_unique = const_cast<int32_t*>(num_unique);
+  int32_t* out_nodes = nullptr;
   if (gru->precision == MSPIPE_FP32_3XTF32) {
     cudaError_t e = launch_gru_tc(gru->d, gru->wtc, gru->xbuf, ts, num_events, edge_feat, snap_mem, snap_mem_ts, snap_step,
                                   snap_h, out_winner, out_num_unique, out_mem, out_ts, out_mail, st->mail_stride, s);

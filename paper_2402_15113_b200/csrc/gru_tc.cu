@@ -40,9 +40,11 @@ constexpr int kBTile = kN * kKC * 4;    // 8 KB
 constexpr int kABlock = 2 * kATile;     // hi | lo
 constexpr int kBBlock = 2 * kBTile;
 constexpr int kStageBytes = kABlock + kBBlock;  // 48 KB
-constexpr int kStages = 4;
+constexpr int kStages = 3;
 constexpr int kThreads = 128;
-constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 1024 /*barriers*/;
+constexpr int kHBufBytes = kM * kJ * 4;   // h rows of the tile's hidden units (prefetched)
+constexpr int kRecvBytes = kM * kN * 4;   // K-split partials received from the cluster (S x 128/S rows)
+constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 1024 /*barriers*/ + kHBufBytes + kRecvBytes;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -132,12 +134,23 @@ __device__ __forceinline__ uint32_t mapa(uint32_t saddr, uint32_t rank) {
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(saddr), "r"(rank));
   return r;
 }
+// generic address of the same shared-memory location in CTA `rank` of the cluster
+__device__ __forceinline__ const void* mapa_generic(const void* p, uint32_t rank) {
+  uint64_t r;
+  asm volatile("mapa.u64 %0, %1, %2;\n" : "=l"(r) : "l"(reinterpret_cast<uint64_t>(p)), "r"(rank));
+  return reinterpret_cast<const void*>(r);
+}
+__device__ __forceinline__ void st_dsmem_f4(uint32_t addr, float x, float y, float z, float w) {
+  asm volatile("st.shared::cluster.v4.f32 [%0], {%1,%2,%3,%4};\n" ::"r"(addr), "f"(x), "f"(y), "f"(z), "f"(w)
+               : "memory");
+}
+// Not volatile and no memory clobber so the compiler may batch these loads;
+// they stay after the cluster barrier through their address dependence on mapa.
 __device__ __forceinline__ float4 ld_dsmem_f4(uint32_t addr) {
   float4 v;
-  asm volatile("ld.shared::cluster.v4.f32 {%0,%1,%2,%3}, [%4];\n"
-               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
-               : "r"(addr)
-               : "memory");
+  asm("ld.shared::cluster.v4.f32 {%0,%1,%2,%3}, [%4];\n"
+      : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+      : "r"(addr));
   return v;
 }
 __device__ __forceinline__ float tf32_rna(float x) {
@@ -163,6 +176,22 @@ __host__ __device__ __forceinline__ uint32_t sw128_off(uint32_t row, uint32_t k)
 }
 
 }  // namespace tc
+
+#ifdef MSPIPE_PHASES
+__device__ unsigned long long g_phase[8192][10];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define PHASE_T(i)                                                                           \
+  g_phase[(blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x][i] = gtimer()
+#define PHASE(i) \
+  if (threadIdx.x == 0) PHASE_T(i)
+#else
+#define PHASE_T(i)
+#define PHASE(i)
+#endif
 
 int gru_tc_jtiles(const GruDesc& d) { return (d.M + tc::kJ - 1) / tc::kJ; }
 
@@ -297,29 +326,19 @@ __global__ void __launch_bounds__(256) k_build_x(TcArgs a) {
   }
 }
 
-__device__ __forceinline__ void gates4(const TcArgs& a, int32_t u, int32_t j0, const float* pr, const float* pz,
-                                       const float* pnx, const float* pnh, int nvalid) {
-  // h' = (1 - z) n + z h, r = σ(.), z = σ(.), n = tanh(x_n + r h_n)  (GRUCell, G5)
-  const GruDesc& d = a.d;
-  const int32_t p = __ldg(a.winner + u);
-  const int32_t ev = p >> 1, role = p & 1;
-  const int64_t rw = role ? a.B + ev : ev;
-  const float* hrow = a.snap_h ? a.snap_h + rw * d.M : a.snap_mem + rw * a.step * d.M;
+// GRUCell gates (G5): r = σ(.), z = σ(.), n = tanh(x_n + r h_n), h' = (1 - z) n + z h.
+__device__ __forceinline__ float4 gates4(const float* pr, const float* pz, const float* pnx, const float* pnh,
+                                         float4 h) {
+  const float* hv = &h.x;
   float out[4];
 #pragma unroll
   for (int e = 0; e < 4; ++e) {
-    if (e < nvalid) {
-      const int32_t j = j0 + e;
-      const float r = 1.0f / (1.0f + expf(-pr[e]));
-      const float z = 1.0f / (1.0f + expf(-pz[e]));
-      const float n = tanhf(pnx[e] + r * pnh[e]);
-      out[e] = (1.0f - z) * n + z * __ldg(hrow + j);
-    }
+    const float r = 1.0f / (1.0f + expf(-pr[e]));
+    const float z = 1.0f / (1.0f + expf(-pz[e]));
+    const float n = tanhf(pnx[e] + r * pnh[e]);
+    out[e] = (1.0f - z) * n + z * hv[e];
   }
-  float* dst = a.out_mem + (int64_t)u * d.M + j0;
-  if (nvalid == 4) *reinterpret_cast<float4*>(dst) = make_float4(out[0], out[1], out[2], out[3]);
-  else
-    for (int e = 0; e < nvalid; ++e) dst[e] = out[e];
+  return make_float4(out[0], out[1], out[2], out[3]);
 }
 
 __global__ void __launch_bounds__(tc::kThreads, 1) k_gru_tc(TcArgs a) {
@@ -330,8 +349,11 @@ __global__ void __launch_bounds__(tc::kThreads, 1) k_gru_tc(TcArgs a) {
   uint64_t* empty = full + kStages;
   uint64_t* acc_full = empty + kStages;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 1);
+  float4* hbuf = reinterpret_cast<float4*>(smem + kStages * kStageBytes + 1024);  // [128 rows][kJ/4]
+  float4* recv = reinterpret_cast<float4*>(smem + kStages * kStageBytes + 1024 + kHBufBytes);
 
   const GruDesc& d = a.d;
+  PHASE(9);
   const int32_t U = __ldg(a.num_unique);
   // grid (S, jtiles, mtiles): the K split is the cluster dimension and the
   // M tile the slowest one, so tiles beyond U (known only on the device)
@@ -357,6 +379,7 @@ __global__ void __launch_bounds__(tc::kThreads, 1) k_gru_tc(TcArgs a) {
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc(tmem_slot, tcols);
+  PHASE(0);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -400,11 +423,30 @@ __global__ void __launch_bounds__(tc::kThreads, 1) k_gru_tc(TcArgs a) {
       mma_commit(&empty[s]);
     }
     mma_commit(acc_full);
+    PHASE_T(2);
+  } else if (warp >= 2) {
+    // idle warps: prefetch h (the GRU hidden input: snap_h or the snapshot
+    // row, G13) of the rows this CTA will finalise, 4 hidden units per item
+    const int rank = S > 1 ? (int)cluster_rank() : 0;
+    const int rb = rank * kM / S, re = (rank + 1) * kM / S;
+    for (int it = threadIdx.x - 64; it < (re - rb) * (kJ / 4); it += 64) {
+      const int mm = rb + it / (kJ / 4), q = it % (kJ / 4);
+      const int32_t u = m0 + mm, j0 = jt * kJ + q * 4;
+      float4 hv = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (u < U && j0 < d.M) {  // M % 4 == 0: a quad is all valid or all padding
+        const int32_t p = __ldg(a.winner + u);
+        const int64_t rw = (p & 1) ? a.B + (p >> 1) : (p >> 1);
+        const float* hrow = a.snap_h ? a.snap_h + rw * d.M : a.snap_mem + rw * a.step * d.M;
+        hv = __ldg(reinterpret_cast<const float4*>(hrow + j0));
+      }
+      hbuf[mm * (kJ / 4) + q] = hv;
+    }
   }
   __syncwarp();
 
   // ---------------- epilogue: TMEM -> registers (thread = row)
   mbar_wait(acc_full, 0);
+  PHASE(3);
   tc_fence_after();
   const int m = warp * 32 + lane;
   const uint32_t tbase = tmem + ((uint32_t)(warp * 32) << 16);
@@ -423,16 +465,38 @@ __global__ void __launch_bounds__(tc::kThreads, 1) k_gru_tc(TcArgs a) {
       r1[i] = __float_as_uint(__fadd_rn(__uint_as_float(r1[i]), __uint_as_float(t1[i])));
     }
   }
-  float* part = reinterpret_cast<float*>(smem);  // stage 0 reused: 128 x 64 fp32 partial
+  PHASE(4);
   const float* bias = d.bias + jt * kN;
+  if (S > 1) {
+    // push this CTA's partial row m into the receive buffer of the rank that
+    // finalises it: recv[src_rank][m - rb(owner)][16 x float4], float4 index
+    // XOR-swizzled by the row so the owner's reads are conflict-free.
+    // Fire-and-forget remote stores instead of latency-bound remote loads.
+    const int R = kM / S;
+    const int owner = m / R, lm = m % R;
+    const uint32_t dst = mapa(smem_u32(recv) + (uint32_t)((cluster_rank() * R + lm) * (kN / 4)) * 16u, (uint32_t)owner);
+#pragma unroll
+    for (int c4 = 0; c4 < 8; ++c4) {
+      st_dsmem_f4(dst + 16u * (uint32_t)(c4 ^ (lm & 15)), __uint_as_float(r0[4 * c4]), __uint_as_float(r0[4 * c4 + 1]),
+                  __uint_as_float(r0[4 * c4 + 2]), __uint_as_float(r0[4 * c4 + 3]));
+      st_dsmem_f4(dst + 16u * (uint32_t)((8 + c4) ^ (lm & 15)), __uint_as_float(r1[4 * c4]),
+                  __uint_as_float(r1[4 * c4 + 1]), __uint_as_float(r1[4 * c4 + 2]), __uint_as_float(r1[4 * c4 + 3]));
+    }
+  }
+  tc_fence_before();
+  __syncthreads();  // hbuf complete
+  PHASE(5);
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem, tcols);
+  }
   if (S == 1) {
     const int32_t u = m0 + m;
     if (u < U) {
 #pragma unroll
       for (int q = 0; q < kJ / 4; ++q) {
         const int32_t j0 = jt * kJ + q * 4;
-        const int nv = min(4, d.M - j0);
-        if (nv <= 0) break;
+        if (j0 >= d.M) break;
         float pr[4], pz[4], pnx[4], pnh[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
@@ -442,51 +506,34 @@ __global__ void __launch_bounds__(tc::kThreads, 1) k_gru_tc(TcArgs a) {
           pnx[e] = __uint_as_float(r1[jj]) + __ldg(bias + 2 * kJ + jj);
           pnh[e] = __uint_as_float(r1[kJ + jj]) + __ldg(bias + 3 * kJ + jj);
         }
-        gates4(a, u, j0, pr, pz, pnx, pnh, nv);
+        *reinterpret_cast<float4*>(a.out_mem + (int64_t)u * d.M + j0) =
+            gates4(pr, pz, pnx, pnh, hbuf[m * (kJ / 4) + q]);
       }
     }
   } else {
-    float4* row = reinterpret_cast<float4*>(part + m * kN);
-#pragma unroll
-    for (int c4 = 0; c4 < 8; ++c4) {
-      row[c4 ^ (m & 15)] = make_float4(__uint_as_float(r0[4 * c4]), __uint_as_float(r0[4 * c4 + 1]),
-                                       __uint_as_float(r0[4 * c4 + 2]), __uint_as_float(r0[4 * c4 + 3]));
-      row[(8 + c4) ^ (m & 15)] = make_float4(__uint_as_float(r1[4 * c4]), __uint_as_float(r1[4 * c4 + 1]),
-                                             __uint_as_float(r1[4 * c4 + 2]), __uint_as_float(r1[4 * c4 + 3]));
-    }
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 2) {
-    tc_fence_after();
-    tmem_dealloc(tmem, tcols);
-  }
-  if (S > 1) {
-    cluster_sync_all();
-    const uint32_t rank = cluster_rank();
-    const int rb = (int)rank * kM / S, re = ((int)rank + 1) * kM / S;
-    const uint32_t part_local = smem_u32(part);
-    for (int it = threadIdx.x; it < (re - rb) * (kJ / 4); it += kThreads) {
-      const int mm = rb + it / (kJ / 4), q = it % (kJ / 4);
+    cluster_sync_all();  // all pushes into recv are visible; nobody writes recv afterwards
+    PHASE(6);
+    const int R = kM / S;
+    const int rb = (int)cluster_rank() * R;
+    for (int it = threadIdx.x; it < R * (kJ / 4); it += kThreads) {
+      const int lm = it / (kJ / 4), q = it % (kJ / 4);
+      const int mm = rb + lm;
       const int32_t u = m0 + mm;
       const int32_t j0 = jt * kJ + q * 4;
-      const int nv = min(4, d.M - j0);
-      if (u >= U || nv <= 0) continue;
+      if (u >= U || j0 >= d.M) continue;
       float4 acc[4];
 #pragma unroll
-      for (int g = 0; g < 4; ++g) acc[g] = make_float4(0.f, 0.f, 0.f, 0.f);
-      for (int sr = 0; sr < S; ++sr) {  // fixed order: deterministic sum
-        const uint32_t remote = mapa(part_local, (uint32_t)sr);
+      for (int g = 0; g < 4; ++g) acc[g] = recv[(0 * R + lm) * (kN / 4) + ((g * (kJ / 4) + q) ^ (lm & 15))];
+      for (int sr = 1; sr < S; ++sr)  // fixed rank order: deterministic sum
 #pragma unroll
         for (int g = 0; g < 4; ++g) {
-          const int chunk = g * (kJ / 4) + q;
-          const float4 v = ld_dsmem_f4(remote + (uint32_t)(mm * kN + ((chunk ^ (mm & 15)) * 4)) * 4u);
+          const float4 v = recv[(sr * R + lm) * (kN / 4) + ((g * (kJ / 4) + q) ^ (lm & 15))];
           acc[g].x += v.x;
           acc[g].y += v.y;
           acc[g].z += v.z;
           acc[g].w += v.w;
         }
-      }
+      if (it == threadIdx.x) PHASE(7);
       float pr[4], pz[4], pnx[4], pnh[4];
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
@@ -496,29 +543,30 @@ __global__ void __launch_bounds__(tc::kThreads, 1) k_gru_tc(TcArgs a) {
         pnx[e] = (&acc[2].x)[e] + __ldg(bias + 2 * kJ + jj);
         pnh[e] = (&acc[3].x)[e] + __ldg(bias + 3 * kJ + jj);
       }
-      gates4(a, u, j0, pr, pz, pnx, pnh, nv);
+      *reinterpret_cast<float4*>(a.out_mem + (int64_t)u * d.M + j0) =
+          gates4(pr, pz, pnx, pnh, hbuf[mm * (kJ / 4) + q]);
     }
-    cluster_sync_all();  // every partial stays alive until all ranks have read it
+    PHASE(8);
   }
 }
 
 constexpr int kMaxChunks = 8;  // 8 x 64 TMEM columns = 512 (the whole TMEM of the SM)
 
 int gru_tc_splits(int64_t max_rows, const GruDesc& d) {
+  // K-split = cluster size.  Powers of two pack the GPCs (measured: 5-CTA
+  // clusters of 1-CTA-per-SM blocks spill into a second wave, 4 do not).
   static int forced = -1;
   if (forced < 0) {
     const char* e = getenv("MSPIPE_TC_SPLITS");  // debugging / experiments only
     forced = e ? atoi(e) : 0;
   }
   const int nchunks = d.Kpad / tc::kKC;
-  const int64_t s_min = (nchunks + kMaxChunks - 1) / kMaxChunks;  // one TMEM buffer per chunk
+  int64_t s_min = (nchunks + kMaxChunks - 1) / kMaxChunks;  // one TMEM buffer per chunk
   if (forced > 0) return (int)(forced > s_min ? forced : s_min);
   const int64_t tiles = ((max_rows + tc::kM - 1) / tc::kM) * gru_tc_jtiles(d);
-  int64_t s = (2 * (int64_t)num_sms() + tiles - 1) / tiles;
-  if (s > 8) s = 8;
-  if (s > nchunks / 2) s = nchunks / 2;
-  if (s < s_min) s = s_min;
-  if (s < 1) s = 1;
+  int64_t s = 1;
+  while (s < 8 && tiles * s * 2 <= 2 * (int64_t)num_sms() && s * 2 <= nchunks / 2) s *= 2;
+  while (s < s_min) s *= 2;
   return (int)s;
 }
 
@@ -561,3 +609,9 @@ cudaError_t launch_gru_tc(const GruDesc& d, const float* wtc, float* xbuf, const
 }
 
 }  // namespace mspipe
+
+#ifdef MSPIPE_PHASES
+extern "C" __attribute__((visibility("default"))) int mspipe_debug_phases(void* host, int n) {
+  return (int)cudaMemcpyFromSymbol(host, mspipe::g_phase, sizeof(unsigned long long) * 10 * n);
+}
+#endif

@@ -14,33 +14,55 @@ static inline unsigned grid_for(int64_t work_items, int threads, int per_sm) {
 // ---------------------------------------------------------------------------
 // A3 — gather rows of the state tables into dense snapshot buffers
 // ("fetches the required ... node memory vectors"; Eq. 2 reads
-// s~^(i-k)).  One thread moves one 16-byte vector; consecutive
-// threads walk a row's vectors, so both the table reads (one 400 B / 1.5 KB
-// row per id) and the dense writes are contiguous per warp.  id -1 = pad.
+// s~^(i-k)).  A warp moves kRows rows per step: it first loads
+// the kRows ids, then issues every 16-byte row-vector load of those rows, then
+// the stores, so kRows x (row / 512 B) requests are in flight per warp and no
+// per-element index arithmetic (division) is needed.  Each row read is one
+// contiguous 400 B (mem) / 1.5 KB (mail) segment and each write is dense.
+// id -1 = pad (zero row, ts 0).
 // ---------------------------------------------------------------------------
+constexpr int kFetchRows = 4;
+
 __global__ void __launch_bounds__(256) k_fetch_gather(
     const int32_t* __restrict__ ids, int64_t n, int64_t N, const float4* __restrict__ mem,
     const double* __restrict__ mem_ts, int32_t Qm, const float4* __restrict__ mail,
     const double* __restrict__ mail_ts, int32_t Qa, float4* __restrict__ out_mem,
     double* __restrict__ out_mem_ts, float4* __restrict__ out_mail,
     double* __restrict__ out_mail_ts) {
-  const int32_t Q = Qm + Qa;
-  const int64_t total = n * Q;
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
-  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
-       t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t row = t / Q;
-    const int32_t c = (int32_t)(t - row * Q);
-    const int32_t id = __ldg(ids + row);
-    const bool ok = id >= 0 && id < N;
-    if (!ok && id != -1 && c == 0) raise_dev(MSPIPE_DEVERR_RANGE);
-    if (c < Qm) {
-      out_mem[row * Qm + c] = ok ? __ldg(mem + (int64_t)id * Qm + c) : z;
-      if (c == 0) out_mem_ts[row] = ok ? __ldg(mem_ts + id) : 0.0;
-    } else {
-      const int32_t cc = c - Qm;
-      out_mail[row * Qa + cc] = ok ? __ldg(mail + (int64_t)id * Qa + cc) : z;
-      if (cc == 0) out_mail_ts[row] = ok ? __ldg(mail_ts + id) : 0.0;
+  for (int64_t base = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * kFetchRows; base < n;
+       base += nwarps * kFetchRows) {
+    int32_t id[kFetchRows];
+#pragma unroll
+    for (int r = 0; r < kFetchRows; ++r) {
+      id[r] = base + r < n ? __ldg(ids + base + r) : -1;
+      if (lane == 0 && (id[r] < -1 || id[r] >= N)) raise_dev(MSPIPE_DEVERR_RANGE);
+      if (id[r] >= N) id[r] = -1;
+    }
+    for (int32_t c = lane; c < Qm; c += 32) {
+      float4 v[kFetchRows];
+#pragma unroll
+      for (int r = 0; r < kFetchRows; ++r) v[r] = id[r] >= 0 ? __ldg(mem + (int64_t)id[r] * Qm + c) : z;
+#pragma unroll
+      for (int r = 0; r < kFetchRows; ++r)
+        if (base + r < n) out_mem[(base + r) * Qm + c] = v[r];
+    }
+    if (lane < kFetchRows && base + lane < n) {
+      int32_t my = id[0];
+#pragma unroll
+      for (int r = 1; r < kFetchRows; ++r) my = lane == r ? id[r] : my;
+      out_mem_ts[base + lane] = my >= 0 ? __ldg(mem_ts + my) : 0.0;
+      if (out_mail_ts) out_mail_ts[base + lane] = my >= 0 ? __ldg(mail_ts + my) : 0.0;
+    }
+    for (int32_t c = lane; c < Qa; c += 32) {
+      float4 v[kFetchRows];
+#pragma unroll
+      for (int r = 0; r < kFetchRows; ++r) v[r] = id[r] >= 0 ? __ldg(mail + (int64_t)id[r] * Qa + c) : z;
+#pragma unroll
+      for (int r = 0; r < kFetchRows; ++r)
+        if (base + r < n) out_mail[(base + r) * Qa + c] = v[r];
     }
   }
 }
@@ -52,7 +74,7 @@ void launch_fetch(const int32_t* ids, int64_t n, int64_t num_nodes, const float*
   const int32_t Qm = mem_dim / 4;
   const int32_t Qa = mail ? (int32_t)(mail_stride / 4) : 0;
   const int threads = 256;
-  k_fetch_gather<<<grid_for(n * (Qm + Qa), threads, 16), threads, 0, s>>>(
+  k_fetch_gather<<<grid_for((n + kFetchRows - 1) / kFetchRows * 32, threads, 8), threads, 0, s>>>(
       ids, n, num_nodes, (const float4*)mem, mem_ts, Qm, (const float4*)mail, mail_ts, Qa,
       (float4*)out_mem, out_mem_ts, (float4*)out_mail, out_mail_ts);
 }
@@ -342,7 +364,8 @@ void launch_dedup(const int32_t* src, const int32_t* dst, int64_t num_events, in
 // ---------------------------------------------------------------------------
 // A7 — write-back of U unique rows (commit of version i, P:L154, P:L820,
 // P:L854-L855).  Rows are unique within a batch, so the scatter is a plain
-// 16-byte-vector copy per thread; U is read on the device.
+// copy; a warp moves kFetchRows rows per step (loads of all rows first, then
+// the stores).  U is read on the device.
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) k_writeback(
     const int32_t* __restrict__ nodes, const int32_t* __restrict__ num, int64_t max_n,
@@ -351,27 +374,46 @@ __global__ void __launch_bounds__(256) k_writeback(
     double* __restrict__ mem_ts, float4* __restrict__ mail, double* __restrict__ mail_ts,
     int64_t N) {
   const int64_t U = min64((int64_t)__ldg(num), max_n);
-  const int32_t Q = Qm + Qa;
-  const int64_t total = U * Q;
-  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
-       t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t row = t / Q;
-    const int32_t c = (int32_t)(t - row * Q);
-    const int32_t node = __ldg(nodes + row);
-    if (node < 0 || node >= N) {
-      if (c == 0) raise_dev(MSPIPE_DEVERR_RANGE);
-      continue;
-    }
-    if (c < Qm) {
-      mem[(int64_t)node * Qm + c] = __ldg(new_mem + row * Qm + c);
-      if (c == 0) {
-        const double t1 = __ldg(new_ts + row);
-        mem_ts[node] = t1;
-        mail_ts[node] = t1;
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t base = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * kFetchRows; base < U;
+       base += nwarps * kFetchRows) {
+    int32_t node[kFetchRows];
+#pragma unroll
+    for (int r = 0; r < kFetchRows; ++r) {
+      node[r] = base + r < U ? __ldg(nodes + base + r) : -1;
+      if (base + r < U && (node[r] < 0 || node[r] >= N)) {
+        if (lane == 0) raise_dev(MSPIPE_DEVERR_RANGE);
+        node[r] = -1;
       }
-    } else {
-      const int32_t cc = c - Qm;
-      mail[(int64_t)node * Qa + cc] = __ldg(new_mail + row * Qa + cc);
+    }
+    for (int32_t c = lane; c < Qm; c += 32) {
+      float4 v[kFetchRows];
+#pragma unroll
+      for (int r = 0; r < kFetchRows; ++r)
+        if (node[r] >= 0) v[r] = __ldg(new_mem + (base + r) * Qm + c);
+#pragma unroll
+      for (int r = 0; r < kFetchRows; ++r)
+        if (node[r] >= 0) mem[(int64_t)node[r] * Qm + c] = v[r];
+    }
+    for (int32_t c = lane; c < Qa; c += 32) {
+      float4 v[kFetchRows];
+#pragma unroll
+      for (int r = 0; r < kFetchRows; ++r)
+        if (node[r] >= 0) v[r] = __ldg(new_mail + (base + r) * Qa + c);
+#pragma unroll
+      for (int r = 0; r < kFetchRows; ++r)
+        if (node[r] >= 0) mail[(int64_t)node[r] * Qa + c] = v[r];
+    }
+    if (lane < kFetchRows) {
+      int32_t my = node[0];
+#pragma unroll
+      for (int r = 1; r < kFetchRows; ++r) my = lane == r ? node[r] : my;
+      if (my >= 0) {
+        const double t1 = __ldg(new_ts + base + lane);
+        mem_ts[my] = t1;
+        mail_ts[my] = t1;
+      }
     }
   }
 }
@@ -382,7 +424,7 @@ void launch_writeback(const int32_t* nodes, const int32_t* num, int64_t max_n,
                       float* mail, double* mail_ts, int64_t num_nodes, cudaStream_t s) {
   const int32_t Qm = mem_dim / 4, Qa = (int32_t)(mail_stride / 4);
   const int threads = 256;
-  k_writeback<<<grid_for(max_n * (Qm + Qa), threads, 16), threads, 0, s>>>(
+  k_writeback<<<grid_for((max_n + kFetchRows - 1) / kFetchRows * 32, threads, 8), threads, 0, s>>>(
       nodes, num, max_n, (const float4*)new_mem, new_ts, (const float4*)new_mail, Qm, Qa,
       (float4*)mem, mem_ts, (float4*)mail, mail_ts, num_nodes);
 }

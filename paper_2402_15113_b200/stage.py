@@ -86,6 +86,7 @@ class _Slot:
         self.omega = (torch.empty((2 * B, cfg.mitigation["n_sim"]), dtype=torch.int32, device=device)
                       if cfg.mitigation else None)
         self.elig = torch.empty((2 * B,), dtype=torch.uint8, device=device) if cfg.mitigation else None
+        self.dd = _C.alloc_dedup(B, device)
         self.version = -1
         if staged:
             self.inp = dict(src=torch.empty(B, dtype=torch.int32, device=device),
@@ -175,6 +176,7 @@ class MemoryStage:
         return e
 
     def prep(self, i):
+        """A1 sampler, A2 dedup, A3 fetch (+A4 mitigation) of batch i into its slot."""
         cfg, sl = self.cfg, self._slot(i)
         if self.staged:
             j0, j1 = self._range(i)
@@ -187,6 +189,9 @@ class MemoryStage:
         self._ev("sample")
         _C.sample_batch(self.tcsr, x["src"], x["dst"], x["neg"], x["ts"], cfg.fanout, samp)
         self._ev("sample_end")
+        self._ev("dedup")
+        _C.memory_dedup(self.memory, x["src"], x["dst"], sl.dd)
+        self._ev("dedup_end")
         ids = samp["sub"].reshape(-1)
         m = ids.numel()
         mit = None
@@ -201,31 +206,81 @@ class MemoryStage:
         self._ev("fetch_end")
         self.versions[i] = sl.version
 
-    def commit(self, i):
+    def _upd(self, i):
+        n = self.inputs(i)["src"].numel()
+        sl = self._slot(i)
+        upd = {k: v[: 2 * n] for k, v in self.upd.items() if k not in ("nodes", "winner", "num")}
+        upd.update(nodes=sl.dd["nodes"][: 2 * n], winner=sl.dd["winner"][: 2 * n], num=sl.dd["num"])
+        return upd
+
+    def update(self, i):
+        """A5+A6 of batch i from its slot (touches no state table)."""
         cfg, sl = self.cfg, self._slot(i)
         x = self.inputs(i)
         n = x["src"].numel()
-        upd = {k: (v if k == "num" else v[: 2 * n]) for k, v in self.upd.items()}
         self._ev("update")
         _C.memory_update(self.memory, self.gru, x["src"], x["dst"], x["ts"], x["ef"], sl.mem, sl.mem_ts,
-                         cfg.fanout + 1, upd, snap_h=sl.h[: 2 * n] if sl.h is not None else None)
+                         cfg.fanout + 1, self._upd(i), snap_h=sl.h[: 2 * n] if sl.h is not None else None)
         self._ev("update_end")
+
+    def writeback(self, i):
+        """A7: commit version i."""
+        upd = self._upd(i)
         self._ev("writeback")
         _C.memory_writeback(self.memory, i, upd)
         self._ev("writeback_end")
         if self.staged:
-            self.out_host["num"].copy_(self.upd["num"], non_blocking=True)
-            self.out_host["nodes"].copy_(self.upd["nodes"], non_blocking=True)
-            self.out_host["mem"].copy_(self.upd["mem"], non_blocking=True)
+            n2 = upd["nodes"].numel()
+            self.out_host["num"].copy_(upd["num"], non_blocking=True)
+            self.out_host["nodes"][:n2].copy_(upd["nodes"], non_blocking=True)
+            self.out_host["mem"][:n2].copy_(upd["mem"], non_blocking=True)
 
-    def run_ops(self, ops):
+    def commit(self, i):
+        self.update(i)
+        self.writeback(i)
+
+    def run_ops(self, ops, overlap=None):
+        """Enqueue ops in order.  With overlap (default when k >= 1), preps of
+        batches not committed in this op group go to a side stream: they only
+        read the T-CSR and (fetch) the state tables, and the tables change
+        only in writeback, so prep(t+k) runs concurrently with update(t); the
+        side stream is joined before the first writeback of the group, which
+        keeps fetch(t+k) between writeback(t-1) and writeback(t) — the exact
+        staleness order of Eq. 2 — while overlapping the two halves of the
+        iteration (the paper's pipelining, moved onto the GPU)."""
+        overlap = (self.cfg.k >= 1) if overlap is None else overlap
+        if not overlap:
+            for op, i in ops:
+                (self.prep if op == "prep" else self.commit)(i)
+            return
+        main = torch.cuda.current_stream()
+        if getattr(self, "side", None) is None or self.side.device != main.device:
+            self.side = torch.cuda.Stream(device=main.device)
+        commits = {i for op, i in ops if op == "commit"}
+        forked = joined = False
         for op, i in ops:
-            (self.prep if op == "prep" else self.commit)(i)
+            if op == "prep" and i not in commits:
+                if not forked:
+                    self.side.wait_stream(main)
+                    forked = True
+                with torch.cuda.stream(self.side):
+                    self.prep(i)
+            elif op == "prep":
+                self.prep(i)
+            else:
+                self.update(i)
+                if forked and not joined:
+                    main.wait_stream(self.side)
+                    joined = True
+                self.writeback(i)
+        if forked and not joined:
+            main.wait_stream(self.side)
 
     def run(self, nb=None):
-        """Eager: all batches (or the first nb) in schedule order."""
+        """All batches (or the first nb) in schedule order, one step at a time."""
         nb = self.num_batches if nb is None else nb
-        self.run_ops(schedule_ops(nb, self.cfg.k, self.cfg.schedule))
+        for ops in self.step_ops(nb):
+            self.run_ops(ops)
 
     def step_ops(self, nb=None):
         """Ops grouped per step (one commit per step; prologue preps in step 0)."""

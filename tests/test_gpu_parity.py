@@ -141,7 +141,7 @@ def _teacher_forced(dev, name, i, mitigation=None, seed=0, E=None, precision=_C.
     st.prep(1)
     sl = st.slots[0]
     n = j1 - j0
-    upd = {k: (v if k == "num" else v[: 2 * n]) for k, v in st.upd.items()}
+    upd = st._upd(1)  # winners from prep's mspipe_memory_dedup + the update outputs
     _C.memory_update(st.memory, st.gru, x["src"], x["dst"], x["ts"], x["ef"], sl.mem, sl.mem_ts, F + 1, upd,
                      snap_h=sl.h[: 2 * n] if sl.h is not None else None)
     torch.cuda.synchronize()
@@ -358,3 +358,22 @@ def test_determinism_two_runs_bitwise(dev):
     b = _stream(dev, "lastfm", 1, E=30_000)[0].memory
     for key in ("mem", "mem_ts", "mail", "mail_ts"):
         assert torch.equal(getattr(a, key), getattr(b, key)), key
+
+
+def test_two_stream_overlap_equals_serial(dev):
+    """prep(t+k) on a side stream overlapping update(t) gives bitwise the same state."""
+    w = make_workload("lastfm", seed=4, num_events=24_000)
+    cfg = w["cfg"]
+    outs = []
+    for overlap in (False, True):
+        sc = StageConfig(cfg.num_nodes, cfg.mem_dim, cfg.edge_dim, cfg.time_dim, cfg.fanout, cfg.batch, 2)
+        g = build_tcsr(cfg.num_nodes, w["src"], w["dst"], w["ts"], dev)
+        st = MemoryStage(sc, w["params"], g, dev)
+        t = {kk: _t(w[kk], dev) for kk in ("src", "dst", "ts", "neg", "ef")}
+        st.bind_resident(t["src"], t["dst"], t["ts"], t["neg"], t["ef"])
+        for ops in st.step_ops():
+            st.run_ops(ops, overlap=overlap)
+        torch.cuda.synchronize()
+        outs.append([getattr(st.memory, k).cpu().numpy() for k in ("mem", "mem_ts", "mail", "mail_ts")])
+    for a, b in zip(*outs):
+        assert np.array_equal(a, b)
