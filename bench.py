@@ -210,11 +210,14 @@ def run_mspipe(args):
         for t, e0, e1 in pending:
             step_ms.append(e0.elapsed_time(e1))
             if st.timing:
-                for name in ("sample", "fetch", "update", "writeback"):
+                for name in ("sample", "dedup", "fetch", "update", "writeback"):
                     a, b = marks[t].get(name, (0, 0))
                     ends = st.timing.get(name + "_end", [])
                     for q in range(a, b):
                         op_ms.setdefault(name, []).append(st.timing[name][q].elapsed_time(ends[q]))
+                        # offsets inside the step (diagnostic timeline)
+                        op_ms.setdefault(name + "@start", []).append(e0.elapsed_time(st.timing[name][q]))
+                        op_ms.setdefault(name + "@end", []).append(e0.elapsed_time(ends[q]))
         pending.clear()
 
     W, K = args.warmup, args.steps
@@ -241,7 +244,8 @@ def run_mspipe(args):
     peaks = _peaks()
     mean_U = float(np.mean(U_host[timed_batches]))
     alg = algorithmic(cfg, sc, mean_U)
-    op_mean = {kk: float(np.mean(v)) for kk, v in op_ms.items() if v}
+    op_mean = {kk: float(np.mean(v)) for kk, v in op_ms.items() if v and "@" not in kk}
+    timeline = {kk: float(np.mean(v)) for kk, v in op_ms.items() if v and "@" in kk}
     dom = max(op_mean, key=op_mean.get) if op_mean else "update"
     clocks = clk.summary()
     if dom == "update" and args.gru == "tc":
@@ -266,6 +270,7 @@ def run_mspipe(args):
     roof["traffic"] = _ncu_traffic(args.config, dom)
     roof["op_ms_mean"] = op_mean
     roof["op_share"] = {kk: v / sum(op_mean.values()) for kk, v in op_mean.items()} if op_mean else None
+    roof["step_timeline_ms"] = dict(sorted(timeline.items(), key=lambda kv: kv[1]))
     roof["alg_bytes_per_launch"] = {kk: alg[kk] for kk in ("sample", "fetch", "update", "writeback")}
     roof["gru_flops_per_launch"] = alg["update_flops"]
     out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": K, "warmup": W,
