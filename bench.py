@@ -125,7 +125,11 @@ def algorithmic(cfg, stage_cfg, U):
     upd_bytes = 2 * B * 8 + U * (2 * 4 * M + 8 + 8 + 4 * He + 4 * M + 8 + 4 * stride + 8)
     upd_flops = U * 2 * 3 * M * (Dx + M)
     wb = U * (4 + 2 * (4 * M + 8 + 4 * stride))
-    return dict(sample=sample, fetch=fetch, update=upd_bytes, update_flops=upd_flops, writeback=wb)
+    dedup = 2 * B * 8
+    # fused ops: prep = A1 + A2 + A3 in one launch; build = the A5 half of update (its bytes); the
+    # apply half (A6) keeps the name "update" and its FLOPs
+    return dict(sample=sample, dedup=dedup, fetch=fetch, prep=sample + dedup + fetch, build=upd_bytes,
+                update=upd_bytes, update_flops=upd_flops, writeback=wb)
 
 
 def run_mspipe(args):
@@ -193,7 +197,7 @@ def run_mspipe(args):
                     torch.cuda.synchronize()
                     _collect(pending, step_ms, op_ms, st, marks)
                     st.memory.reset()
-                if not profile:
+                if not profile and args.l2 == "flush":
                     flush.fill_(float(n))
                 e0 = torch.cuda.Event(enable_timing=True)
                 e1 = torch.cuda.Event(enable_timing=True)
@@ -210,7 +214,7 @@ def run_mspipe(args):
         for t, e0, e1 in pending:
             step_ms.append(e0.elapsed_time(e1))
             if st.timing:
-                for name in ("sample", "dedup", "fetch", "update", "writeback"):
+                for name in ("prep", "build", "sample", "dedup", "fetch", "update", "writeback"):
                     a, b = marks[t].get(name, (0, 0))
                     ends = st.timing.get(name + "_end", [])
                     for q in range(a, b):
@@ -222,14 +226,23 @@ def run_mspipe(args):
 
     W, K = args.warmup, args.steps
     # ---- device-resident run (the `value`) ---------------------------------
+    # The timed graphs carry no per-op event nodes (each one is an extra graph
+    # node on the critical path); the per-op breakdown for the roofline comes
+    # from a second, instrumented replay of the same steps right after.
     st = make_stage(False)
-    graphs, marks, s = capture(st, timing=True)
+    graphs, marks, s = capture(st, timing=False)
     if ws > 1:
         dist.barrier()
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
-        step_ms, op_ms = timed_run(st, graphs, marks, s, W, K, profile=args.profile)
+        step_ms, _ = timed_run(st, graphs, marks, s, W, K, profile=args.profile)
     _C.check(s)
+    del graphs
+    st_i = make_stage(False)
+    graphs_i, marks_i, s_i = capture(st_i, timing=True)
+    step_ms_instr, op_ms = timed_run(st_i, graphs_i, marks_i, s_i, W, K, profile=args.profile)
+    _C.check(s_i)
+    del graphs_i
     tot_ms = float(sum(step_ms))
     if ws > 1:
         tt = torch.tensor([tot_ms], device=dev)
@@ -239,7 +252,6 @@ def run_mspipe(args):
     timed_batches = [(W + q) % nb for q in range(K)]
     events = sum(min(cfg.batch, len(w["src"]) - b * cfg.batch) for b in timed_batches)
     value = ws * events / (tot_ms / 1e3)
-    del graphs
     # ---- roofline of the dominant op ---------------------------------------
     peaks = _peaks()
     mean_U = float(np.mean(U_host[timed_batches]))
@@ -271,7 +283,8 @@ def run_mspipe(args):
     roof["op_ms_mean"] = op_mean
     roof["op_share"] = {kk: v / sum(op_mean.values()) for kk, v in op_mean.items()} if op_mean else None
     roof["step_timeline_ms"] = dict(sorted(timeline.items(), key=lambda kv: kv[1]))
-    roof["alg_bytes_per_launch"] = {kk: alg[kk] for kk in ("sample", "fetch", "update", "writeback")}
+    roof["instrumented_ms_per_step"] = float(np.mean(step_ms_instr)) if step_ms_instr else None
+    roof["alg_bytes_per_launch"] = {kk: alg[kk] for kk in op_mean if kk in alg}
     roof["gru_flops_per_launch"] = alg["update_flops"]
     out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": K, "warmup": W,
            "ms_per_step": tot_ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
@@ -280,9 +293,10 @@ def run_mspipe(args):
                       "batch": cfg.batch, "staleness_k": k, "schedule": args.schedule, "fanout": cfg.fanout,
                       "mem_dim": cfg.mem_dim, "edge_dim": cfg.edge_dim, "time_dim": cfg.time_dim,
                       "mitigation": bool(mit), "fetch_mail": args.fetch_mail, "gru": "fp32-3xtf32-tcgen05" if args.gru == "tc" else "fp32-simt",
-                      "l2": "flushed (256 MiB write) between timed steps, outside the timed events",
+                      "l2": ("flushed (256 MiB write) between timed steps, outside the timed events"
+                             if args.l2 == "flush" else "warm: steps back to back, state tables L2-resident"),
                       "parallelism": "single" if ws == 1 else f"replicas{ws}"},
-           "roofline": roof, "gpu_launches": _launches(st.step_ops(), timed_batches, bool(mit)), "clocks": clocks}
+           "roofline": roof, "gpu_launches": _launches(st.step_ops(), timed_batches, bool(mit), st.fused), "clocks": clocks}
     if args.profile:
         if rank == 0:
             print(json.dumps(out))
@@ -312,10 +326,11 @@ def run_mspipe(args):
         dist.destroy_process_group()
 
 
-def _launches(steps, timed_batches, mit):
-    """Kernels of this library per timed step: prep = sampler + gather (+ mitigation),
-    commit = dedup + GRU + write-back."""
-    per = {"prep": 2 + (1 if mit else 0), "commit": 3}
+def _launches(steps, timed_batches, mit, fused):
+    """Kernels of this library per timed step.  fused: prep = k_prep + k_build_x
+    (+ k_mitigate), commit = k_gru_tc + k_writeback; otherwise prep = sampler +
+    dedup + gather (+ mitigation), commit = build + GEMM (or SIMT GRU) + write-back."""
+    per = {"prep": (2 if fused else 3) + (1 if mit else 0), "commit": 2 if fused else 3}
     return int(sum(per[op] for t in timed_batches for op, _ in steps[t]))
 
 
@@ -405,6 +420,8 @@ def main():
     ap.add_argument("--gru", default="tc", choices=["tc", "simt"])
     ap.add_argument("--no-mitigation", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--l2", default="flush", choices=["flush", "warm"],
+                    help="flush: 256 MiB write between timed steps (default); warm: back-to-back steps")
     ap.add_argument("--cpu-events", type=int, default=157_474)
     ap.add_argument("--profile", action="store_true", help="short run for ncu: no flush/e2e/cpu")
     args = ap.parse_args()

@@ -247,6 +247,45 @@ MSPIPE_API mspipe_status mspipe_memory_writeback(mspipe_memory* st, int64_t comm
                                       int64_t max_n, const float* new_mem, const double* new_ts,
                                       const float* new_mail, void* stream);
 
+/* ---------------------------------------------------------------------------
+ * Fused forms of the same steps (same results, fewer launches).
+ * ------------------------------------------------------------------------- */
+
+/* A1 + A2 + A3 (+ A4) of batch `iteration` in one launch (plus one for the
+ * mitigation when `mit` is given): exactly mspipe_sample_batch, then
+ * mspipe_memory_dedup, then mspipe_memory_fetch(ids = out_sub_ids,
+ * n = 3B(𝒩+1)) with the same arguments and outputs as those calls.  The same
+ * staleness gate applies.  fanout <= 31; num_events <= 8192. */
+MSPIPE_API mspipe_status mspipe_memory_prep(mspipe_memory* st, const mspipe_tcsr* g, int64_t iteration,
+                                 const int32_t* src, const int32_t* dst, const int32_t* neg,
+                                 const double* ts, int64_t num_events, int32_t fanout,
+                                 int32_t* out_nbr, int32_t* out_eid, double* out_ts, float* out_dt,
+                                 int32_t* out_cnt, int32_t* out_sub_ids, int32_t* out_nodes,
+                                 int32_t* out_winner, int32_t* out_num_unique, float* out_mem,
+                                 double* out_mem_ts, float* out_mail, double* out_mail_ts,
+                                 const mspipe_mitigation* mit, int64_t* out_version, void* stream);
+
+/* mspipe_memory_update split in its two halves (precision MSPIPE_FP32_3XTF32
+ * only), so the message build of a later batch can run ahead of the GRU of the
+ * current one.  `workspace` (device, caller-owned, >= mspipe_gru_workspace_size
+ * bytes) carries the tensor-core A-operand images from the build to the apply
+ * of the SAME batch.
+ *   mspipe_message_build (A5): out_ts [<=2B], out_mail [<=2B, mail_stride]
+ *     exactly as mspipe_memory_update;
+ *   mspipe_gru_apply (A6): out_mem [<=2B, mem_dim] exactly as
+ *     mspipe_memory_update. */
+MSPIPE_API size_t mspipe_gru_workspace_size(const mspipe_gru* gru, int64_t num_events);
+MSPIPE_API mspipe_status mspipe_message_build(const mspipe_gru* gru, const double* ts, int64_t num_events,
+                                   const float* edge_feat, const float* snap_mem,
+                                   const double* snap_mem_ts, int64_t snap_step,
+                                   const float* snap_h, const int32_t* winner,
+                                   const int32_t* num_unique, double* out_ts, float* out_mail,
+                                   int64_t mail_stride, void* workspace, size_t ws_bytes, void* stream);
+MSPIPE_API mspipe_status mspipe_gru_apply(const mspipe_gru* gru, int64_t num_events, const float* snap_mem,
+                               int64_t snap_step, const float* snap_h, const int32_t* winner,
+                               const int32_t* num_unique, float* out_mem, const void* workspace,
+                               size_t ws_bytes, void* stream);
+
 /* Utility (timing): record `event` (a cudaEvent_t) on `stream` with
  * cudaEventRecordExternal, so that under stream capture it becomes an
  * event-record node of the graph and can still be used for elapsed-time

@@ -25,7 +25,8 @@ EXPORTS = ("mspipe_abi_version", "mspipe_last_error", "mspipe_check", "mspipe_sa
            "mspipe_sample_batch", "mspipe_memory_create", "mspipe_memory_destroy",
            "mspipe_memory_committed", "mspipe_memory_reset", "mspipe_memory_fetch",
            "mspipe_memory_dedup", "mspipe_gru_create", "mspipe_gru_destroy", "mspipe_memory_update",
-           "mspipe_memory_writeback", "mspipe_util_event_record")
+           "mspipe_memory_writeback", "mspipe_memory_prep", "mspipe_gru_workspace_size",
+           "mspipe_message_build", "mspipe_gru_apply", "mspipe_util_event_record")
 
 
 class MspipeError(RuntimeError):
@@ -73,6 +74,12 @@ def lib():
         L.mspipe_memory_update.argtypes = [P, P, P, P, P, i64, P, P, P, i64, P, P, P, P, P, P, P]
         L.mspipe_memory_writeback.argtypes = [P, i64, P, P, i64, P, P, P, P]
         L.mspipe_util_event_record.argtypes = [P, P]
+        L.mspipe_memory_prep.argtypes = [P, C.POINTER(Tcsr), i64, P, P, P, P, i64, i32, P, P, P, P, P, P, P, P, P, P,
+                                         P, P, P, C.POINTER(Mitigation), C.POINTER(i64), P]
+        L.mspipe_gru_workspace_size.argtypes = [P, i64]
+        L.mspipe_gru_workspace_size.restype = C.c_size_t
+        L.mspipe_message_build.argtypes = [P, P, i64, P, P, P, i64, P, P, P, P, P, i64, P, C.c_size_t, P]
+        L.mspipe_gru_apply.argtypes = [P, i64, P, i64, P, P, P, P, P, C.c_size_t, P]
         if L.mspipe_abi_version() != ABI_VERSION:
             raise RuntimeError(f"libmspipe ABI {L.mspipe_abi_version()} != binding {ABI_VERSION}")
         _lib = L
@@ -235,6 +242,40 @@ def memory_update(st: MemoryHandle, gru: GruHandle, src, dst, ts, edge_feat, sna
                                    ptr(out["winner"]), ptr(out["num"]), ptr(out["mem"]), ptr(out["ts"]),
                                    ptr(out["mail"]), stream_ptr(stream)), "mspipe_memory_update")
     return out
+
+
+def memory_prep(st: MemoryHandle, g: TcsrHandle, iteration, src, dst, neg, ts, fanout, samp, dd, out_mem, out_mem_ts,
+                out_mail=None, out_mail_ts=None, mitigation: Mitigation | None = None, stream=None) -> int:
+    """A1+A2+A3(+A4) fused: fills samp (alloc_sample), dd (alloc_dedup) and the fetched rows."""
+    v = i64(-1)
+    _ck(lib().mspipe_memory_prep(st.h, C.byref(g.c), int(iteration), ptr(src), ptr(dst), ptr(neg), ptr(ts),
+                                 src.numel(), fanout, ptr(samp["nbr"]), ptr(samp["eid"]), ptr(samp["ts"]),
+                                 ptr(samp["dt"]), ptr(samp["cnt"]), ptr(samp["sub"]), ptr(dd["nodes"]),
+                                 ptr(dd["winner"]), ptr(dd["num"]), ptr(out_mem), ptr(out_mem_ts), ptr(out_mail),
+                                 ptr(out_mail_ts), C.byref(mitigation) if mitigation is not None else None,
+                                 C.byref(v), stream_ptr(stream)), "mspipe_memory_prep")
+    return int(v.value)
+
+
+def gru_workspace_size(gru: GruHandle, num_events) -> int:
+    return int(lib().mspipe_gru_workspace_size(gru.h, int(num_events)))
+
+
+def message_build(gru: GruHandle, ts, edge_feat, snap_mem, snap_mem_ts, snap_step, winner, num, out_ts, out_mail,
+                  workspace, snap_h=None, stream=None):
+    """A5: message + time encoding -> tensor-core operand images (workspace), mail rows, commit ts."""
+    _ck(lib().mspipe_message_build(gru.h, ptr(ts), ts.numel(), ptr(edge_feat), ptr(snap_mem), ptr(snap_mem_ts),
+                                   int(snap_step), ptr(snap_h), ptr(winner), ptr(num), ptr(out_ts), ptr(out_mail),
+                                   out_mail.shape[1], ptr(workspace), workspace.numel() * workspace.element_size(),
+                                   stream_ptr(stream)), "mspipe_message_build")
+
+
+def gru_apply(gru: GruHandle, num_events, snap_mem, snap_step, winner, num, out_mem, workspace, snap_h=None,
+              stream=None):
+    """A6: the GRU contraction + gates from the operand images of message_build."""
+    _ck(lib().mspipe_gru_apply(gru.h, int(num_events), ptr(snap_mem), int(snap_step), ptr(snap_h), ptr(winner),
+                               ptr(num), ptr(out_mem), ptr(workspace), workspace.numel() * workspace.element_size(),
+                               stream_ptr(stream)), "mspipe_gru_apply")
 
 
 def alloc_dedup(num_events, device):

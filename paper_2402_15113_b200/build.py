@@ -10,7 +10,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libmspipe.so")
-SOURCES = ["api.cu", "sampler.cu", "memory.cu", "gru_simt.cu", "gru_tc.cu"]
+SOURCES = ["api.cu", "sampler.cu", "memory.cu", "prep.cu", "gru_simt.cu", "gru_tc.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-rdc=true", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC,-fvisibility=hidden", "--expt-relaxed-constexpr",

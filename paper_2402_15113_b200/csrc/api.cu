@@ -1,6 +1,7 @@
 // api.cu — the extern "C" entry points of include/mspipe.h: argument checks,
 // handle state, the staleness gate, and dispatch to the kernels.
 #include <stdarg.h>
+#include <stdlib.h>
 #include <stdio.h>
 #include <string.h>
 
@@ -23,6 +24,16 @@ mspipe_status fail(mspipe_status s, const char* fmt, ...) {
 mspipe_status cuda_status(cudaError_t e, const char* what) {
   if (e == cudaSuccess) return MSPIPE_OK;
   return fail(MSPIPE_ECUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+bool pdl_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    // measured on the wiki step (32.6 us without vs 35.0 us with): off by default
+    const char* e = getenv("MSPIPE_PDL");
+    on = (e && e[0] == '1') ? 1 : 0;
+  }
+  return on != 0;
 }
 
 static mspipe_status after_launch(const char* what) {
@@ -312,6 +323,98 @@ mspipe_status mspipe_memory_writeback(mspipe_memory* st, int64_t commit_version,
   mspipe_status rc = after_launch("memory_writeback");
   if (rc == MSPIPE_OK) st->committed = commit_version;  // i_upd <- i (Alg. 1 L16)
   return rc;
+}
+
+mspipe_status mspipe_memory_prep(mspipe_memory* st, const mspipe_tcsr* g, int64_t iteration,
+                                 const int32_t* src, const int32_t* dst, const int32_t* neg,
+                                 const double* ts, int64_t num_events, int32_t fanout,
+                                 int32_t* out_nbr, int32_t* out_eid, double* out_ts, float* out_dt,
+                                 int32_t* out_cnt, int32_t* out_sub_ids, int32_t* out_nodes,
+                                 int32_t* out_winner, int32_t* out_num_unique, float* out_mem,
+                                 double* out_mem_ts, float* out_mail, double* out_mail_ts,
+                                 const mspipe_mitigation* mit, int64_t* out_version, void* stream) {
+  if (!st) return fail(MSPIPE_EINVAL, "memory_prep: NULL handle");
+  if (!tcsr_ok(g) || g->num_nodes != st->num_nodes) return fail(MSPIPE_EINVAL, "memory_prep: bad T-CSR");
+  if (iteration < 1 || num_events < 0 || num_events > 8192 || fanout < 1 || fanout > 31)
+    return fail(MSPIPE_EINVAL, "memory_prep: iteration=%lld num_events=%lld (<= 8192) fanout=%d (<= 31)",
+                (long long)iteration, (long long)num_events, fanout);
+  if (st->committed < iteration - 1 - st->k || st->committed > iteration - 1)
+    return fail(MSPIPE_ESTALE, "memory_prep: iteration %lld with committed=%lld violates k=%d",
+                (long long)iteration, (long long)st->committed, st->k);
+  if ((out_mail == nullptr) != (out_mail_ts == nullptr)) return fail(MSPIPE_EINVAL, "memory_prep: out_mail and out_mail_ts go together");
+  cudaStream_t s = (cudaStream_t)stream;
+  if (num_events > 0) {
+    if (!src || !dst || !neg || !ts || !out_nbr || !out_eid || !out_ts || !out_dt || !out_cnt || !out_sub_ids ||
+        !out_nodes || !out_winner || !out_num_unique || !out_mem || !out_mem_ts)
+      return fail(MSPIPE_EINVAL, "memory_prep: null input/output");
+    cudaError_t e = launch_prep(to_tcsr(g), src, dst, neg, ts, num_events, fanout, out_nbr, out_eid, out_ts, out_dt,
+                                out_cnt, out_sub_ids, st->scratch, out_nodes, out_winner, out_num_unique, st->mem,
+                                st->mem_ts, st->mem_dim, st->mail, st->mail_ts, st->mail_stride, out_mem,
+                                out_mem_ts, out_mail, out_mail_ts, s);
+    if (e != cudaSuccess) return cuda_status(e, "memory_prep: launch");
+  } else if (out_num_unique) {
+    cudaError_t e = cudaMemsetAsync(out_num_unique, 0, sizeof(int32_t), s);
+    if (e != cudaSuccess) return cuda_status(e, "memory_prep");
+  }
+  if (mit && mit->num_events > 0) {
+    if (!tcsr_ok(mit->g) || !mit->src || !mit->dst || !mit->ts || !mit->out_h)
+      return fail(MSPIPE_EINVAL, "memory_prep: bad mitigation arguments");
+    if (!(mit->lambda >= 0.f && mit->lambda <= 1.f) || mit->n_sim < 0 || mit->n_sim > 16 || mit->fanout < 1 || mit->fanout > 16)
+      return fail(MSPIPE_EINVAL, "memory_prep: lambda=%g n_sim=%d fanout=%d", mit->lambda, mit->n_sim, mit->fanout);
+    launch_mitigate(to_tcsr(mit->g), mit->src, mit->dst, mit->ts, mit->num_events, st->mem, st->mem_ts, st->mem_dim,
+                    mit->lambda, mit->gamma, mit->n_sim, mit->fanout, mit->out_h, mit->out_omega, mit->out_elig, s);
+  }
+  if (out_version) *out_version = st->committed;
+  return after_launch("memory_prep");
+}
+
+size_t mspipe_gru_workspace_size(const mspipe_gru* gru, int64_t num_events) {
+  if (!gru || gru->precision != MSPIPE_FP32_3XTF32 || num_events < 0) return 0;
+  return sizeof(float) * gru_tc_xbuf_floats(gru->d, num_events);
+}
+
+mspipe_status mspipe_message_build(const mspipe_gru* gru, const double* ts, int64_t num_events,
+                                   const float* edge_feat, const float* snap_mem,
+                                   const double* snap_mem_ts, int64_t snap_step,
+                                   const float* snap_h, const int32_t* winner,
+                                   const int32_t* num_unique, double* out_ts, float* out_mail,
+                                   int64_t mail_stride, void* workspace, size_t ws_bytes, void* stream) {
+  if (!gru) return fail(MSPIPE_EINVAL, "message_build: NULL handle");
+  if (gru->precision != MSPIPE_FP32_3XTF32)
+    return fail(MSPIPE_EUNSUPPORTED, "message_build: only for precision MSPIPE_FP32_3XTF32 (use mspipe_memory_update)");
+  if (num_events < 0 || num_events > gru->max_events || snap_step < 1 || mail_stride < gru->d.Dm || mail_stride % 4)
+    return fail(MSPIPE_EINVAL, "message_build: num_events=%lld snap_step=%lld mail_stride=%lld", (long long)num_events,
+                (long long)snap_step, (long long)mail_stride);
+  if (num_events == 0) return MSPIPE_OK;
+  if (ws_bytes < mspipe_gru_workspace_size(gru, num_events) || !workspace)
+    return fail(MSPIPE_EINVAL, "message_build: workspace of %zu bytes < %zu", ws_bytes, mspipe_gru_workspace_size(gru, num_events));
+  if (!ts || (gru->d.He > 0 && !edge_feat) || !snap_mem || !snap_mem_ts || !winner || !num_unique || !out_ts || !out_mail)
+    return fail(MSPIPE_EINVAL, "message_build: null input/output");
+  cudaError_t e = launch_gru_tc(gru->d, gru->wtc, (float*)workspace, ts, num_events, edge_feat, snap_mem, snap_mem_ts,
+                                snap_step, snap_h, winner, num_unique, nullptr, out_ts, out_mail, mail_stride,
+                                (cudaStream_t)stream, kGruBuild);
+  if (e != cudaSuccess) return cuda_status(e, "message_build: launch");
+  return after_launch("message_build");
+}
+
+mspipe_status mspipe_gru_apply(const mspipe_gru* gru, int64_t num_events, const float* snap_mem,
+                               int64_t snap_step, const float* snap_h, const int32_t* winner,
+                               const int32_t* num_unique, float* out_mem, const void* workspace,
+                               size_t ws_bytes, void* stream) {
+  if (!gru) return fail(MSPIPE_EINVAL, "gru_apply: NULL handle");
+  if (gru->precision != MSPIPE_FP32_3XTF32)
+    return fail(MSPIPE_EUNSUPPORTED, "gru_apply: only for precision MSPIPE_FP32_3XTF32 (use mspipe_memory_update)");
+  if (num_events < 0 || num_events > gru->max_events || snap_step < 1)
+    return fail(MSPIPE_EINVAL, "gru_apply: num_events=%lld snap_step=%lld", (long long)num_events, (long long)snap_step);
+  if (num_events == 0) return MSPIPE_OK;
+  if (ws_bytes < mspipe_gru_workspace_size(gru, num_events) || !workspace)
+    return fail(MSPIPE_EINVAL, "gru_apply: workspace of %zu bytes too small", ws_bytes);
+  if (!snap_mem || !winner || !num_unique || !out_mem) return fail(MSPIPE_EINVAL, "gru_apply: null input/output");
+  cudaError_t e = launch_gru_tc(gru->d, gru->wtc, (float*)workspace, nullptr, num_events, nullptr, snap_mem, nullptr,
+                                snap_step, snap_h, winner, num_unique, out_mem, nullptr, nullptr, 0,
+                                (cudaStream_t)stream, kGruGemm);
+  if (e != cudaSuccess) return cuda_status(e, "gru_apply: launch");
+  return after_launch("gru_apply");
 }
 
 mspipe_status mspipe_util_event_record(void* event, void* stream) {

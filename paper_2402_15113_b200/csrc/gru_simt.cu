@@ -117,6 +117,7 @@ __global__ void __launch_bounds__(kThreads) k_gru_simt(
   __shared__ __align__(16) float As[2][kMT][kKC + 4];
   __shared__ __align__(16) float Bs[2][kKC][kNT];
   __shared__ RowInfo ri;
+  pdl_begin();
   const int32_t U = __ldg(num_unique);
   const int32_t m0 = blockIdx.x * kMT;
   if (m0 >= U) return;
@@ -251,8 +252,8 @@ void launch_gru_simt(const GruDesc& d, const int32_t* src, const int32_t* dst, c
   GruArgs a{d, ts, num_events, edge_feat, snap_mem, snap_mem_ts, snap_step, snap_h};
   const int64_t max_rows = 2 * num_events;
   dim3 grid((unsigned)((max_rows + kMT - 1) / kMT), (unsigned)(d.Npad / kNT));
-  k_gru_simt<<<grid, kThreads, 0, s>>>(a, src, dst, winner, num_unique, out_mem, out_ts, out_mail,
-                                       mail_stride);
+  launch_k(k_gru_simt, grid, dim3(kThreads), 0, s, 1, a, src, dst, winner, num_unique, out_mem, out_ts, out_mail,
+           mail_stride);
 }
 
 }  // namespace mspipe

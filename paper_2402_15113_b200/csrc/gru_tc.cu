@@ -283,6 +283,7 @@ struct TcArgs {
 
 // A5: one warp per (row, chunk).  lane = column inside the chunk.
 __global__ void __launch_bounds__(256) k_build_x(TcArgs a) {
+  pdl_begin();
   const GruDesc& d = a.d;
   const int32_t U = __ldg(a.num_unique);
   const int32_t nchunks = d.Kpad / tc::kKC;
@@ -354,6 +355,7 @@ __global__ void __launch_bounds__(tc::kThreads, 1) k_gru_tc(TcArgs a) {
 
   const GruDesc& d = a.d;
   PHASE(9);
+  pdl_begin();
   const int32_t U = __ldg(a.num_unique);
   // grid (S, jtiles, mtiles): the K split is the cluster dimension and the
   // M tile the slowest one, so tiles beyond U (known only on the device)
@@ -574,7 +576,7 @@ cudaError_t launch_gru_tc(const GruDesc& d, const float* wtc, float* xbuf, const
                           const float* edge_feat, const float* snap_mem, const double* snap_mem_ts,
                           int64_t snap_step, const float* snap_h, const int32_t* winner,
                           const int32_t* num_unique, float* out_mem, double* out_ts, float* out_mail,
-                          int64_t mail_stride, cudaStream_t s) {
+                          int64_t mail_stride, cudaStream_t s, int parts) {
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(k_gru_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::kSmemBytes);
@@ -585,27 +587,18 @@ cudaError_t launch_gru_tc(const GruDesc& d, const float* wtc, float* xbuf, const
            num_unique, out_mem, out_ts, out_mail, mail_stride};
   const int64_t max_rows = 2 * num_events;
   const int64_t mtiles = (max_rows + tc::kM - 1) / tc::kM;
-  {
+  if (parts & kGruBuild) {
     const int64_t warps = mtiles * (d.Kpad / tc::kKC) * tc::kM;
     int64_t blocks = (warps * 32 + 255) / 256;
     const int64_t cap = (int64_t)num_sms() * 8;
     if (blocks > cap) blocks = cap;
-    k_build_x<<<(unsigned)blocks, 256, 0, s>>>(a);
+    cudaError_t e = launch_k(k_build_x, dim3((unsigned)blocks), dim3(256), 0, s, 1, a);
+    if (e != cudaSuccess) return e;
   }
+  if (!(parts & kGruGemm)) return cudaSuccess;
   const int S = gru_tc_splits(max_rows, d);
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)S, (unsigned)gru_tc_jtiles(d), (unsigned)mtiles);
-  cfg.blockDim = dim3(tc::kThreads);
-  cfg.dynamicSmemBytes = tc::kSmemBytes;
-  cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = (unsigned)S;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, k_gru_tc, a);
+  return launch_k(k_gru_tc, dim3((unsigned)S, (unsigned)gru_tc_jtiles(d), (unsigned)mtiles), dim3(tc::kThreads),
+                  tc::kSmemBytes, s, (unsigned)S, a);
 }
 
 }  // namespace mspipe

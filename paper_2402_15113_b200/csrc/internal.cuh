@@ -3,6 +3,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <utility>
+
 #include "mspipe.h"
 
 namespace mspipe {
@@ -28,6 +30,47 @@ inline int num_sms() {
   return n;
 }
 
+// ---- Programmatic Dependent Launch --------------------------------------
+// Every kernel of the library starts with pdl_begin(): it lets the next
+// kernel of the stream be launched at once (its launch latency overlaps this
+// kernel) and then waits until the previous kernel of the stream has
+// completed with its memory visible, before any global memory access.  No-ops
+// when a kernel is launched without the programmatic-serialization attribute.
+__device__ __forceinline__ void pdl_begin() {
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+}
+
+bool pdl_enabled();  // env MSPIPE_PDL=0 disables (A/B experiments)
+
+// cudaLaunchKernelEx with the PDL attribute (+ an optional (cx,1,1) cluster).
+template <typename... KArgs, typename... Args>
+cudaError_t launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                     unsigned cluster_x, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[2];
+  unsigned n = 0;
+  if (pdl_enabled()) {
+    attr[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[n].val.programmaticStreamSerializationAllowed = 1;
+    ++n;
+  }
+  if (cluster_x > 1) {
+    attr[n].id = cudaLaunchAttributeClusterDimension;
+    attr[n].val.clusterDim.x = cluster_x;
+    attr[n].val.clusterDim.y = 1;
+    attr[n].val.clusterDim.z = 1;
+    ++n;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = n;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+
 struct Tcsr {
   int64_t num_nodes, nnz;
   const int64_t* indptr;
@@ -35,6 +78,38 @@ struct Tcsr {
   const int32_t* eid;
   const double* ts;
 };
+
+// A1 core, executed by a whole warp for one root v at query time tq: returns
+// `end`, the first row position with ts >= tq (the entries [beg, end) are the
+// incident events with ts < tq, G15), and *beg = row start.  33-ary search:
+// 32 lanes probe 32 interior positions of [lo, hi) per round and a ballot
+// (ts is sorted, so the true lanes are a prefix) shrinks the range 33x; a row
+// of L entries costs ceil(log33(L/32)) + 1 dependent rounds instead of log2(L).
+// An id outside [0, N) gives an empty row and raises MSPIPE_DEVERR_RANGE.
+__device__ __forceinline__ int64_t warp_recent_end(const Tcsr& g, int32_t v, double tq, int lane,
+                                                   int64_t* beg_out) {
+  if (v < 0 || v >= g.num_nodes) {
+    if (lane == 0) raise_dev(MSPIPE_DEVERR_RANGE);
+    *beg_out = 0;
+    return 0;
+  }
+  const int64_t beg = __ldg(g.indptr + v);
+  int64_t lo = beg, hi = __ldg(g.indptr + v + 1);
+  while (hi - lo > 32) {
+    const int64_t span = hi - lo;
+    const int64_t p = lo + ((int64_t)(lane + 1) * span) / 33;  // strictly inside [lo, hi)
+    const bool below = __ldg(g.ts + p) < tq;
+    const int c = __popc(__ballot_sync(0xffffffffu, below));
+    const int64_t plast = __shfl_sync(0xffffffffu, p, c > 0 ? c - 1 : 0);
+    const int64_t pfirst = __shfl_sync(0xffffffffu, p, c < 32 ? c : 31);
+    if (c > 0) lo = plast + 1;
+    if (c < 32) hi = pfirst;
+  }
+  const int64_t q = lo + lane;
+  const bool below = q < hi && __ldg(g.ts + q) < tq;
+  *beg_out = beg;
+  return lo + __popc(__ballot_sync(0xffffffffu, below));
+}
 
 inline Tcsr to_tcsr(const mspipe_tcsr* g) {
   return Tcsr{g->num_nodes, g->nnz, g->indptr, g->nbr, g->eid, g->ts};
@@ -85,11 +160,20 @@ size_t gru_tc_packed_floats(const GruDesc& d);
 size_t gru_tc_xbuf_floats(const GruDesc& d, int64_t max_events);
 void launch_gru_pack_tc(const float* w_ih, const float* w_hh, const float* b_ih, const float* b_hh,
                         const GruDesc& d, float* wtc, float* bias, cudaStream_t s);
+enum { kGruBuild = 1, kGruGemm = 2 };
 cudaError_t launch_gru_tc(const GruDesc& d, const float* wtc, float* xbuf, const double* ts, int64_t num_events,
                           const float* edge_feat, const float* snap_mem, const double* snap_mem_ts,
                           int64_t snap_step, const float* snap_h, const int32_t* winner,
                           const int32_t* num_unique, float* out_mem, double* out_ts, float* out_mail,
-                          int64_t mail_stride, cudaStream_t s);
+                          int64_t mail_stride, cudaStream_t s, int parts = kGruBuild | kGruGemm);
+// prep.cu
+cudaError_t launch_prep(const Tcsr& g, const int32_t* src, const int32_t* dst, const int32_t* neg,
+                        const double* ts, int64_t num_events, int32_t fanout, int32_t* out_nbr,
+                        int32_t* out_eid, double* out_ts, float* out_dt, int32_t* out_cnt, int32_t* out_sub,
+                        int32_t* scratch, int32_t* out_nodes, int32_t* out_winner, int32_t* out_num,
+                        const float* mem, const double* mem_ts, int32_t mem_dim, const float* mail,
+                        const double* mail_ts, int64_t mail_stride, float* out_mem, double* out_mem_ts,
+                        float* out_mail, double* out_mail_ts, cudaStream_t s);
 
 }  // namespace mspipe
 

@@ -1,4 +1,5 @@
 // memory.cu — A3 snapshot fetch, A4 mitigation, A2 dedup, A7 write-back.
+#include "dedup.cuh"
 #include "internal.cuh"
 
 namespace mspipe {
@@ -29,6 +30,7 @@ __global__ void __launch_bounds__(256) k_fetch_gather(
     const double* __restrict__ mail_ts, int32_t Qa, float4* __restrict__ out_mem,
     double* __restrict__ out_mem_ts, float4* __restrict__ out_mail,
     double* __restrict__ out_mail_ts) {
+  pdl_begin();
   const int lane = threadIdx.x & 31;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -74,9 +76,9 @@ void launch_fetch(const int32_t* ids, int64_t n, int64_t num_nodes, const float*
   const int32_t Qm = mem_dim / 4;
   const int32_t Qa = mail ? (int32_t)(mail_stride / 4) : 0;
   const int threads = 256;
-  k_fetch_gather<<<grid_for((n + kFetchRows - 1) / kFetchRows * 32, threads, 8), threads, 0, s>>>(
-      ids, n, num_nodes, (const float4*)mem, mem_ts, Qm, (const float4*)mail, mail_ts, Qa,
-      (float4*)out_mem, out_mem_ts, (float4*)out_mail, out_mail_ts);
+  launch_k(k_fetch_gather, dim3(grid_for((n + kFetchRows - 1) / kFetchRows * 32, threads, 8)), dim3(threads), 0, s,
+           1, ids, n, num_nodes, (const float4*)mem, mem_ts, Qm, (const float4*)mail, mail_ts, Qa, (float4*)out_mem,
+           out_mem_ts, (float4*)out_mail, out_mail_ts);
 }
 
 // ---------------------------------------------------------------------------
@@ -117,6 +119,7 @@ __global__ void __launch_bounds__(32 * kMitWarps) k_mitigate(
     const double* __restrict__ mem_ts, int32_t M, float lambda, double gamma, int32_t n_sim,
     int32_t F, float* __restrict__ out_h, int32_t* __restrict__ out_omega,
     uint8_t* __restrict__ out_elig) {
+  pdl_begin();
   __shared__ MitWarpSmem sm_all[kMitWarps];
   const int lane = threadIdx.x & 31;
   MitWarpSmem& sm = sm_all[threadIdx.x >> 5];
@@ -236,9 +239,8 @@ void launch_mitigate(const Tcsr& g, const int32_t* src, const int32_t* dst, cons
                      float lambda, double gamma, int32_t n_sim, int32_t fanout, float* out_h,
                      int32_t* out_omega, uint8_t* out_elig, cudaStream_t s) {
   const int threads = 32 * kMitWarps;
-  k_mitigate<<<grid_for(2 * num_events * 32, threads, 16), threads, 0, s>>>(
-      g, src, dst, ts, num_events, mem, mem_ts, mem_dim, lambda, gamma, n_sim, fanout, out_h,
-      out_omega, out_elig);
+  launch_k(k_mitigate, dim3(grid_for(2 * num_events * 32, threads, 16)), dim3(threads), 0, s, 1, g, src, dst, ts,
+           num_events, mem, mem_ts, mem_dim, lambda, gamma, n_sim, fanout, out_h, out_omega, out_elig);
 }
 
 // ---------------------------------------------------------------------------
@@ -251,96 +253,15 @@ void launch_mitigate(const Tcsr& g, const int32_t* src, const int32_t* dst, cons
 // winners in p order.  Phase 3: winners restore scratch[node] = -1.
 // ---------------------------------------------------------------------------
 constexpr int kDedupThreads = 1024;
-constexpr int64_t kDedupSmemNodes = 40960;  // node table in shared memory up to 160 KB
 
 template <bool kSmem>
 __global__ void __launch_bounds__(kDedupThreads) k_dedup(
     const int32_t* __restrict__ src, const int32_t* __restrict__ dst, int64_t B,
     int32_t* __restrict__ gscratch, int64_t N, int32_t* __restrict__ out_nodes,
     int32_t* __restrict__ out_winner, int32_t* __restrict__ out_num) {
+  pdl_begin();
   extern __shared__ int32_t sscratch[];
-  __shared__ int32_t warp_tot[kDedupThreads / 32];
-  __shared__ int32_t total_s;
-  int32_t* scratch = kSmem ? sscratch : gscratch;
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  if (kSmem) {
-    for (int64_t i = tid; i < N; i += kDedupThreads) sscratch[i] = -1;
-    __syncthreads();
-  }
-  const int64_t P = 2 * B;
-  const int64_t Pr = (P + kDedupThreads - 1) / kDedupThreads * kDedupThreads;
-  for (int64_t p = tid; p < Pr; p += kDedupThreads) {
-    int32_t node = -1;
-    if (p < P) {
-      node = (p & 1) ? __ldg(dst + (p >> 1)) : __ldg(src + (p >> 1));
-      if (node < 0 || node >= N) {
-        raise_dev(MSPIPE_DEVERR_RANGE);
-        node = -1;
-      }
-    }
-    const unsigned grp = __match_any_sync(0xffffffffu, node);
-    const int leader = 31 - __clz(grp);  // highest lane = largest p of the group
-    if (node >= 0 && lane == leader) atomicMax(scratch + node, (int32_t)p);
-  }
-  if (!kSmem) __threadfence();
-  __syncthreads();
-  // contiguous chunk per thread: [tid*C, tid*C + C)
-  const int64_t C = (P + kDedupThreads - 1) / kDedupThreads;  // <= 32 (B <= 16384)
-  const int64_t p0 = tid * C;
-  uint32_t flags = 0;
-  int32_t cnt = 0;
-  for (int64_t i = 0; i < C; ++i) {
-    const int64_t p = p0 + i;
-    if (p >= P) break;
-    const int32_t node = (p & 1) ? __ldg(dst + (p >> 1)) : __ldg(src + (p >> 1));
-    if (node < 0 || node >= N) continue;
-    const int32_t w = kSmem ? sscratch[node] : __ldcg(gscratch + node);
-    if (w == (int32_t)p) {
-      flags |= 1u << i;
-      ++cnt;
-    }
-  }
-  // block exclusive scan of cnt
-  int32_t incl = cnt;
-#pragma unroll
-  for (int d = 1; d < 32; d <<= 1) {
-    const int32_t y = __shfl_up_sync(0xffffffffu, incl, d);
-    if (lane >= d) incl += y;
-  }
-  if (lane == 31) warp_tot[wid] = incl;
-  __syncthreads();
-  if (wid == 0) {
-    int32_t v = warp_tot[lane];
-    int32_t vi = v;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const int32_t y = __shfl_up_sync(0xffffffffu, vi, d);
-      if (lane >= d) vi += y;
-    }
-    warp_tot[lane] = vi - v;  // exclusive prefix of warp totals
-    if (lane == 31) total_s = vi;
-  }
-  __syncthreads();
-  int32_t off = warp_tot[wid] + incl - cnt;
-  for (int64_t i = 0; i < C; ++i) {
-    if (flags & (1u << i)) {
-      const int64_t p = p0 + i;
-      out_nodes[off] = (p & 1) ? __ldg(dst + (p >> 1)) : __ldg(src + (p >> 1));
-      out_winner[off] = (int32_t)p;
-      ++off;
-    }
-  }
-  if (!kSmem) {
-    __syncthreads();  // all scratch reads are done before the reset
-    for (int64_t i = 0; i < C; ++i) {
-      if (flags & (1u << i)) {
-        const int64_t p = p0 + i;
-        const int32_t node = (p & 1) ? __ldg(dst + (p >> 1)) : __ldg(src + (p >> 1));
-        gscratch[node] = -1;
-      }
-    }
-  }
-  if (tid == 0) *out_num = total_s;
+  block_dedup<kDedupThreads, kSmem>(src, dst, B, gscratch, sscratch, N, out_nodes, out_winner, out_num);
 }
 
 void launch_dedup(const int32_t* src, const int32_t* dst, int64_t num_events, int32_t* scratch,
@@ -353,11 +274,11 @@ void launch_dedup(const int32_t* src, const int32_t* dst, int64_t num_events, in
                            (int)(kDedupSmemNodes * sizeof(int32_t)));
       attr = true;
     }
-    k_dedup<true><<<1, kDedupThreads, num_nodes * sizeof(int32_t), s>>>(src, dst, num_events, scratch, num_nodes,
-                                                                         out_nodes, out_winner, out_num);
+    launch_k(k_dedup<true>, dim3(1), dim3(kDedupThreads), num_nodes * sizeof(int32_t), s, 1, src, dst, num_events,
+             scratch, num_nodes, out_nodes, out_winner, out_num);
   } else {
-    k_dedup<false><<<1, kDedupThreads, 0, s>>>(src, dst, num_events, scratch, num_nodes, out_nodes, out_winner,
-                                               out_num);
+    launch_k(k_dedup<false>, dim3(1), dim3(kDedupThreads), 0, s, 1, src, dst, num_events, scratch, num_nodes,
+             out_nodes, out_winner, out_num);
   }
 }
 
@@ -373,6 +294,7 @@ __global__ void __launch_bounds__(256) k_writeback(
     const float4* __restrict__ new_mail, int32_t Qm, int32_t Qa, float4* __restrict__ mem,
     double* __restrict__ mem_ts, float4* __restrict__ mail, double* __restrict__ mail_ts,
     int64_t N) {
+  pdl_begin();
   const int64_t U = min64((int64_t)__ldg(num), max_n);
   const int lane = threadIdx.x & 31;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -424,9 +346,9 @@ void launch_writeback(const int32_t* nodes, const int32_t* num, int64_t max_n,
                       float* mail, double* mail_ts, int64_t num_nodes, cudaStream_t s) {
   const int32_t Qm = mem_dim / 4, Qa = (int32_t)(mail_stride / 4);
   const int threads = 256;
-  k_writeback<<<grid_for((max_n + kFetchRows - 1) / kFetchRows * 32, threads, 8), threads, 0, s>>>(
-      nodes, num, max_n, (const float4*)new_mem, new_ts, (const float4*)new_mail, Qm, Qa,
-      (float4*)mem, mem_ts, (float4*)mail, mail_ts, num_nodes);
+  launch_k(k_writeback, dim3(grid_for((max_n + kFetchRows - 1) / kFetchRows * 32, threads, 8)), dim3(threads), 0, s,
+           1, nodes, num, max_n, (const float4*)new_mem, new_ts, (const float4*)new_mail, Qm, Qa, (float4*)mem,
+           mem_ts, (float4*)mail, mail_ts, num_nodes);
 }
 
 }  // namespace mspipe

@@ -1,0 +1,156 @@
+// prep.cu — A1 + A2 + A3 of one batch in ONE launch (mspipe_memory_prep).
+//
+// The per-batch prep is three latency-bound steps whose separate launches
+// cost more than their work.  k_prep fuses them:
+//   block 0       : A2, the block dedup of the 2B pairs (dedup.cuh);
+//   blocks 1..    : one warp per root of the batch ([src | dst | neg]):
+//                   A1 (warp_recent_end: 33-ary search of the T-CSR row) and,
+//                   with the subgraph ids still in registers, A3: the warp
+//                   gathers the 𝒩+1 state rows of its subgraph (root first)
+//                   straight into the dense snapshot buffers.
+// Reading the tables here is the "fetch": the stage orders this launch between
+// write-back(i-1-k) and write-back(i-k) (Eq. 2).
+#include "dedup.cuh"
+#include "internal.cuh"
+
+namespace mspipe {
+
+constexpr int kPrepThreads = 512;
+constexpr int kPrepWarps = kPrepThreads / 32;
+
+struct PrepArgs {
+  Tcsr g;
+  const int32_t* src;
+  const int32_t* dst;
+  const int32_t* neg;
+  const double* ts;
+  int64_t B;
+  int32_t F;
+  int32_t* out_nbr;
+  int32_t* out_eid;
+  double* out_ts;
+  float* out_dt;
+  int32_t* out_cnt;
+  int32_t* out_sub;
+  int32_t* gscratch;
+  int32_t* out_nodes;
+  int32_t* out_winner;
+  int32_t* out_num;
+  const float4* mem;
+  const double* mem_ts;
+  int32_t Qm;
+  const float4* mail;
+  const double* mail_ts;
+  int32_t Qa;
+  float4* out_mem;
+  double* out_mem_ts;
+  float4* out_mail;
+  double* out_mail_ts;
+};
+
+// copy `nrows` table rows (ids held by lanes 0..nrows-1, -1 = zero row) of Q
+// float4 each into dst rows base..base+nrows-1; 4 loads in flight per lane.
+__device__ __forceinline__ void warp_gather_rows(const float4* __restrict__ tab, int32_t Q, int32_t my_id,
+                                                 int nrows, float4* __restrict__ dst, int64_t dst_row0,
+                                                 int lane) {
+  const int total = nrows * Q;
+  const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int base = 0; base < total; base += 32 * 4) {
+    float4 v[4];
+    int idx[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      idx[u] = base + u * 32 + lane;
+      const int s = idx[u] < total ? idx[u] / Q : 0;
+      const int32_t id = __shfl_sync(0xffffffffu, my_id, s);
+      const int c = idx[u] - s * Q;
+      v[u] = (idx[u] < total && id >= 0) ? __ldg(tab + (int64_t)id * Q + c) : z;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (idx[u] < total) dst[dst_row0 * Q + idx[u]] = v[u];
+  }
+}
+
+template <bool kSmem>
+__global__ void __launch_bounds__(kPrepThreads) k_prep(PrepArgs a) {
+  extern __shared__ int32_t sscratch[];
+  pdl_begin();
+  if (blockIdx.x == 0) {
+    block_dedup<kPrepThreads, kSmem>(a.src, a.dst, a.B, a.gscratch, sscratch, a.g.num_nodes, a.out_nodes,
+                                     a.out_winner, a.out_num);
+    return;
+  }
+  const int lane = threadIdx.x & 31;
+  const int64_t R = 3 * a.B;
+  const int F = a.F, F1 = a.F + 1;
+  const int64_t nwarps = (int64_t)(gridDim.x - 1) * kPrepWarps;
+  for (int64_t r = (int64_t)(blockIdx.x - 1) * kPrepWarps + (threadIdx.x >> 5); r < R; r += nwarps) {
+    const int64_t role = r / a.B, ev = r - role * a.B;
+    const int32_t v = role == 0 ? __ldg(a.src + ev) : (role == 1 ? __ldg(a.dst + ev) : __ldg(a.neg + ev));
+    const double tq = __ldg(a.ts + ev);
+    int64_t beg;
+    const int64_t end = warp_recent_end(a.g, v, tq, lane, &beg);
+    const int32_t cnt = (int32_t)min64(end - beg, (int64_t)F);
+    // A1 outputs; lane s < F = slot s (newest first); lane s in [1, F] also holds subgraph id s
+    int32_t id = lane == 0 ? v : -1;
+    if (lane < F) {
+      const int64_t o = r * F + lane;
+      if (lane < cnt) {
+        const int64_t q = end - 1 - lane;
+        const double tsq = __ldg(a.g.ts + q);
+        a.out_nbr[o] = __ldg(a.g.nbr + q);
+        a.out_eid[o] = __ldg(a.g.eid + q);
+        a.out_ts[o] = tsq;
+        a.out_dt[o] = (float)(tq - tsq);
+      } else {
+        a.out_nbr[o] = -1;
+        a.out_eid[o] = -1;
+        a.out_ts[o] = 0.0;
+        a.out_dt[o] = 0.0f;
+      }
+    }
+    if (lane >= 1 && lane <= F && lane - 1 < cnt) id = __ldg(a.g.nbr + (end - lane));
+    if (lane == 0) a.out_cnt[r] = cnt;
+    if (lane <= F) a.out_sub[r * F1 + lane] = id;
+    // A3: the subgraph's snapshot rows (pads and out-of-range ids give zero rows)
+    const int32_t gid = (id >= 0 && id < a.g.num_nodes) ? id : -1;
+    if (lane <= F) {
+      a.out_mem_ts[r * F1 + lane] = gid >= 0 ? __ldg(a.mem_ts + gid) : 0.0;
+      if (a.out_mail_ts) a.out_mail_ts[r * F1 + lane] = gid >= 0 ? __ldg(a.mail_ts + gid) : 0.0;
+    }
+    warp_gather_rows(a.mem, a.Qm, gid, F1, a.out_mem, r * F1, lane);
+    if (a.Qa > 0) warp_gather_rows(a.mail, a.Qa, gid, F1, a.out_mail, r * F1, lane);
+  }
+}
+
+cudaError_t launch_prep(const Tcsr& g, const int32_t* src, const int32_t* dst, const int32_t* neg,
+                        const double* ts, int64_t num_events, int32_t fanout, int32_t* out_nbr,
+                        int32_t* out_eid, double* out_ts, float* out_dt, int32_t* out_cnt, int32_t* out_sub,
+                        int32_t* scratch, int32_t* out_nodes, int32_t* out_winner, int32_t* out_num,
+                        const float* mem, const double* mem_ts, int32_t mem_dim, const float* mail,
+                        const double* mail_ts, int64_t mail_stride, float* out_mem, double* out_mem_ts,
+                        float* out_mail, double* out_mail_ts, cudaStream_t s) {
+  PrepArgs a{g, src, dst, neg, ts, num_events, fanout, out_nbr, out_eid, out_ts, out_dt, out_cnt, out_sub,
+             scratch, out_nodes, out_winner, out_num, (const float4*)mem, mem_ts, mem_dim / 4,
+             (const float4*)mail, mail_ts, out_mail ? (int32_t)(mail_stride / 4) : 0, (float4*)out_mem, out_mem_ts,
+             (float4*)out_mail, out_mail ? out_mail_ts : nullptr};
+  int64_t blocks = (3 * num_events + kPrepWarps - 1) / kPrepWarps;
+  const int64_t cap = (int64_t)num_sms() * 4;
+  if (blocks > cap) blocks = cap;
+  blocks += 1;  // block 0: dedup
+  if (g.num_nodes <= kDedupSmemNodes) {
+    static bool attr = false;
+    if (!attr) {
+      cudaError_t e = cudaFuncSetAttribute(k_prep<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)(kDedupSmemNodes * sizeof(int32_t)));
+      if (e != cudaSuccess) return e;
+      attr = true;
+    }
+    return launch_k(k_prep<true>, dim3((unsigned)blocks), dim3(kPrepThreads), g.num_nodes * sizeof(int32_t), s, 1,
+                    a);
+  }
+  return launch_k(k_prep<false>, dim3((unsigned)blocks), dim3(kPrepThreads), 0, s, 1, a);
+}
+
+}  // namespace mspipe

@@ -21,6 +21,7 @@ __global__ void __launch_bounds__(256) k_sample_recent(
     int32_t F, int32_t* __restrict__ out_nbr, int32_t* __restrict__ out_eid,
     double* __restrict__ out_ts, float* __restrict__ out_dt, int32_t* __restrict__ out_cnt,
     int32_t* __restrict__ out_sub) {
+  pdl_begin();
   const int lane = threadIdx.x & 31;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < R; r += nwarps) {
@@ -34,29 +35,8 @@ __global__ void __launch_bounds__(256) k_sample_recent(
       v = __ldg(roots + r);
       tq = __ldg(qts + r);
     }
-    int64_t beg = 0, end = 0;
-    const bool ok = v >= 0 && v < g.num_nodes;
-    if (ok) {
-      beg = __ldg(g.indptr + v);
-      int64_t lo = beg, hi = __ldg(g.indptr + v + 1);
-      // invariant: ts[lo-1] < tq (or lo = beg) and ts[hi] >= tq (or hi = row end)
-      while (hi - lo > 32) {
-        const int64_t span = hi - lo;
-        const int64_t p = lo + ((int64_t)(lane + 1) * span) / 33;  // strictly inside [lo, hi)
-        const bool below = __ldg(g.ts + p) < tq;
-        const unsigned bal = __ballot_sync(0xffffffffu, below);
-        const int c = __popc(bal);  // ts is sorted, so the true lanes are a prefix
-        const int64_t plast = __shfl_sync(0xffffffffu, p, c > 0 ? c - 1 : 0);
-        const int64_t pfirst = __shfl_sync(0xffffffffu, p, c < 32 ? c : 31);
-        if (c > 0) lo = plast + 1;
-        if (c < 32) hi = pfirst;
-      }
-      const int64_t q = lo + lane;
-      const bool below = q < hi && __ldg(g.ts + q) < tq;
-      end = lo + __popc(__ballot_sync(0xffffffffu, below));
-    } else if (lane == 0) {
-      raise_dev(MSPIPE_DEVERR_RANGE);
-    }
+    int64_t beg = 0;
+    const int64_t end = warp_recent_end(g, v, tq, lane, &beg);
     const int32_t cnt = (int32_t)min64(end - beg, (int64_t)F);
     for (int s = lane; s < F; s += 32) {  // output slot s = entry end-1-s (newest first)
       const int64_t o = r * F + s;
@@ -95,14 +75,14 @@ void launch_sample(const Tcsr& g, const int32_t* roots, const double* qts, const
   const int64_t cap = (int64_t)num_sms() * 16;
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
+  const int32_t* np = nullptr;
+  const double* nd = nullptr;
   if (roots)
-    k_sample_recent<false><<<(unsigned)blocks, threads, 0, s>>>(g, roots, qts, nullptr, nullptr, nullptr, nullptr, 1,
-                                                                 num_roots, fanout, out_nbr, out_eid, out_ts, out_dt,
-                                                                 out_cnt, out_sub);
+    launch_k(k_sample_recent<false>, dim3((unsigned)blocks), dim3(threads), 0, s, 1, g, roots, qts, np, np, np, nd,
+             (int64_t)1, num_roots, fanout, out_nbr, out_eid, out_ts, out_dt, out_cnt, out_sub);
   else
-    k_sample_recent<true><<<(unsigned)blocks, threads, 0, s>>>(g, nullptr, nullptr, src, dst, neg, ev_ts, num_events,
-                                                                num_roots, fanout, out_nbr, out_eid, out_ts, out_dt,
-                                                                out_cnt, out_sub);
+    launch_k(k_sample_recent<true>, dim3((unsigned)blocks), dim3(threads), 0, s, 1, g, np, nd, src, dst, neg, ev_ts,
+             num_events, num_roots, fanout, out_nbr, out_eid, out_ts, out_dt, out_cnt, out_sub);
 }
 
 }  // namespace mspipe

@@ -40,6 +40,11 @@ class StageConfig:
     mitigation: dict | None = None  # dict(lam, gamma, n_sim) or None
     fetch_mail: bool = False        # also fetch mail rows of the subgraph nodes
     precision: int = _C.FP32_3XTF32  # tcgen05 3xTF32 (fp32 parity); _C.FP32_SIMT = CUDA-core baseline
+    fused: bool | None = None  # mspipe_memory_prep + message_build/gru_apply (default: when supported)
+
+    def use_fused(self) -> bool:
+        ok = self.precision == _C.FP32_3XTF32 and self.fanout <= 31 and self.batch <= 8192
+        return ok if self.fused is None else (self.fused and ok)
 
 
 def schedule_ops(nb: int, k: int, schedule: str = "exact"):
@@ -74,7 +79,7 @@ def snapshot_versions(nb: int, k: int, schedule: str = "exact"):
 
 
 class _Slot:
-    def __init__(self, cfg: StageConfig, mail_stride: int, device, staged: bool):
+    def __init__(self, cfg: StageConfig, mail_stride: int, device, staged: bool, ws_bytes: int = 0):
         B, F, M = cfg.batch, cfg.fanout, cfg.mem_dim
         self.samp = _C.alloc_sample(3 * B, F, device, sub=True)
         n = 3 * B * (F + 1)
@@ -87,6 +92,10 @@ class _Slot:
                       if cfg.mitigation else None)
         self.elig = torch.empty((2 * B,), dtype=torch.uint8, device=device) if cfg.mitigation else None
         self.dd = _C.alloc_dedup(B, device)
+        if ws_bytes:  # fused path: message_build(t+k) runs ahead of gru_apply(t), so its outputs are per slot
+            self.ws = torch.empty((ws_bytes,), dtype=torch.uint8, device=device)
+            self.uts = torch.empty((2 * B,), dtype=torch.float64, device=device)
+            self.umail = torch.empty((2 * B, mail_stride), dtype=torch.float32, device=device)
         self.version = -1
         if staged:
             self.inp = dict(src=torch.empty(B, dtype=torch.int32, device=device),
@@ -109,6 +118,8 @@ class MemoryStage:
         self.gru = _C.GruHandle(cfg.mem_dim, cfg.edge_dim, cfg.time_dim, params, self.device, cfg.precision,
                                 max_events=cfg.batch)
         self.upd = _C.alloc_update(cfg.batch, cfg.mem_dim, self.memory.mail_stride, self.device)
+        self.fused = cfg.use_fused()
+        self.ws_bytes = _C.gru_workspace_size(self.gru, cfg.batch) if self.fused else 0
         self.staged = False
         self.slots = None
         self.timing = None  # optional dict name -> list of (start, end) events per op
@@ -119,7 +130,8 @@ class MemoryStage:
         self.E = src.numel()
         self.res = dict(src=src, dst=dst, ts=ts, neg=neg, ef=ef)
         self.staged = False
-        self.slots = [_Slot(self.cfg, self.memory.mail_stride, self.device, False) for _ in range(self.cfg.k + 1)]
+        self.slots = [_Slot(self.cfg, self.memory.mail_stride, self.device, False, self.ws_bytes)
+                      for _ in range(self.cfg.k + 1)]
 
     def bind_host(self, src, dst, ts, neg, ef):
         """Host arrays are pinned; each prep copies its batch H2D (e2e path)."""
@@ -127,7 +139,8 @@ class MemoryStage:
         self.host = {k: torch.as_tensor(v).pin_memory() for k, v in
                      dict(src=src, dst=dst, ts=ts, neg=neg, ef=ef).items()}
         self.staged = True
-        self.slots = [_Slot(self.cfg, self.memory.mail_stride, self.device, True) for _ in range(self.cfg.k + 1)]
+        self.slots = [_Slot(self.cfg, self.memory.mail_stride, self.device, True, self.ws_bytes)
+                      for _ in range(self.cfg.k + 1)]
         self.out_host = dict(nodes=torch.empty(2 * self.cfg.batch, dtype=torch.int32).pin_memory(),
                              num=torch.empty(1, dtype=torch.int32).pin_memory(),
                              mem=torch.empty((2 * self.cfg.batch, self.cfg.mem_dim), dtype=torch.float32).pin_memory())
@@ -186,6 +199,9 @@ class MemoryStage:
         x = self.inputs(i)
         n = x["src"].numel()
         samp = {k: v[: 3 * n] for k, v in sl.samp.items()}
+        if self.fused:
+            self._prep_fused(i, sl, x, n, samp)
+            return
         self._ev("sample")
         _C.sample_batch(self.tcsr, x["src"], x["dst"], x["neg"], x["ts"], cfg.fanout, samp)
         self._ev("sample_end")
@@ -206,11 +222,38 @@ class MemoryStage:
         self._ev("fetch_end")
         self.versions[i] = sl.version
 
+    def _mitigation(self, sl, x, n):
+        cfg = self.cfg
+        if not cfg.mitigation:
+            return None
+        return _C.make_mitigation(self.tcsr, cfg.mitigation["lam"], cfg.mitigation["gamma"], cfg.mitigation["n_sim"],
+                                  cfg.fanout, x["src"], x["dst"], x["ts"], sl.h[: 2 * n], sl.omega[: 2 * n],
+                                  sl.elig[: 2 * n])
+
+    def _prep_fused(self, i, sl, x, n, samp):
+        """mspipe_memory_prep (A1+A2+A3[+A4], one launch) then mspipe_message_build (A5) of batch i."""
+        cfg = self.cfg
+        m = 3 * n * (cfg.fanout + 1)
+        self._ev("prep")
+        sl.version = _C.memory_prep(self.memory, self.tcsr, i, x["src"], x["dst"], x["neg"], x["ts"], cfg.fanout,
+                                    samp, sl.dd, sl.mem[:m], sl.mem_ts[:m],
+                                    sl.mail[:m] if sl.mail is not None else None,
+                                    sl.mail_ts[:m] if sl.mail_ts is not None else None, self._mitigation(sl, x, n))
+        self._ev("prep_end")
+        self.versions[i] = sl.version
+        self._ev("build")
+        _C.message_build(self.gru, x["ts"], x["ef"], sl.mem, sl.mem_ts, cfg.fanout + 1, sl.dd["winner"][: 2 * n],
+                         sl.dd["num"], sl.uts[: 2 * n], sl.umail[: 2 * n], sl.ws,
+                         snap_h=sl.h[: 2 * n] if sl.h is not None else None)
+        self._ev("build_end")
+
     def _upd(self, i):
         n = self.inputs(i)["src"].numel()
         sl = self._slot(i)
         upd = {k: v[: 2 * n] for k, v in self.upd.items() if k not in ("nodes", "winner", "num")}
         upd.update(nodes=sl.dd["nodes"][: 2 * n], winner=sl.dd["winner"][: 2 * n], num=sl.dd["num"])
+        if self.fused:
+            upd.update(ts=sl.uts[: 2 * n], mail=sl.umail[: 2 * n])
         return upd
 
     def update(self, i):
@@ -219,8 +262,13 @@ class MemoryStage:
         x = self.inputs(i)
         n = x["src"].numel()
         self._ev("update")
-        _C.memory_update(self.memory, self.gru, x["src"], x["dst"], x["ts"], x["ef"], sl.mem, sl.mem_ts,
-                         cfg.fanout + 1, self._upd(i), snap_h=sl.h[: 2 * n] if sl.h is not None else None)
+        if self.fused:
+            upd = self._upd(i)
+            _C.gru_apply(self.gru, n, sl.mem, cfg.fanout + 1, upd["winner"], upd["num"], upd["mem"], sl.ws,
+                         snap_h=sl.h[: 2 * n] if sl.h is not None else None)
+        else:
+            _C.memory_update(self.memory, self.gru, x["src"], x["dst"], x["ts"], x["ef"], sl.mem, sl.mem_ts,
+                             cfg.fanout + 1, self._upd(i), snap_h=sl.h[: 2 * n] if sl.h is not None else None)
         self._ev("update_end")
 
     def writeback(self, i):

@@ -121,7 +121,7 @@ def _random_state(num_nodes, M, src, dst, ts, j0, seed):
     return mem, np.maximum(mem_ts, last_dst)
 
 
-def _teacher_forced(dev, name, i, mitigation=None, seed=0, E=None, precision=_C.FP32_3XTF32):
+def _teacher_forced(dev, name, i, mitigation=None, seed=0, E=None, precision=_C.FP32_3XTF32, fused=False):
     cfg = CONFIGS[name]
     src, dst, ts, neg = make_events(cfg, seed, E)
     B, F, M = cfg.batch, cfg.fanout, cfg.mem_dim
@@ -131,7 +131,7 @@ def _teacher_forced(dev, name, i, mitigation=None, seed=0, E=None, precision=_C.
     mem, mem_ts = _random_state(cfg.num_nodes, M, src, dst, ts, j0, seed + i)
     g = build_tcsr(cfg.num_nodes, src, dst, ts, dev)
     sc = StageConfig(cfg.num_nodes, M, cfg.edge_dim, cfg.time_dim, F, B, 0, mitigation=mitigation,
-                     precision=precision)
+                     precision=precision, fused=fused)
     st = MemoryStage(sc, params, g, dev)
     st.memory.mem.copy_(_t(mem, dev))
     st.memory.mem_ts.copy_(_t(mem_ts, dev))
@@ -141,9 +141,12 @@ def _teacher_forced(dev, name, i, mitigation=None, seed=0, E=None, precision=_C.
     st.prep(1)
     sl = st.slots[0]
     n = j1 - j0
-    upd = st._upd(1)  # winners from prep's mspipe_memory_dedup + the update outputs
-    _C.memory_update(st.memory, st.gru, x["src"], x["dst"], x["ts"], x["ef"], sl.mem, sl.mem_ts, F + 1, upd,
-                     snap_h=sl.h[: 2 * n] if sl.h is not None else None)
+    upd = st._upd(1)  # winners from prep's dedup + the update outputs
+    if fused:  # mspipe_memory_prep + mspipe_message_build ran in prep(1); mspipe_gru_apply here
+        st.update(1)
+    else:
+        _C.memory_update(st.memory, st.gru, x["src"], x["dst"], x["ts"], x["ef"], sl.mem, sl.mem_ts, F + 1, upd,
+                         snap_h=sl.h[: 2 * n] if sl.h is not None else None)
     torch.cuda.synchronize()
     _C.check()
     og = oracle.Graph(cfg.num_nodes, src, dst, ts) if mitigation else None
@@ -154,10 +157,19 @@ def _teacher_forced(dev, name, i, mitigation=None, seed=0, E=None, precision=_C.
 
 @pytest.mark.parametrize("name,i,E", [("tiny", 1, None), ("tiny", 50, None), ("wiki", 137, None),
                                       ("lastfm", 400, 300_000), ("gdelt", 3, 20_000)])
-@pytest.mark.parametrize("precision", [_C.FP32_3XTF32, _C.FP32_SIMT])
-def test_update_teacher_forced(dev, name, i, E, precision):
-    st, sl, upd, ref, ev, (mem, mem_ts) = _teacher_forced(dev, name, i, E=E, precision=precision)
+@pytest.mark.parametrize("precision,fused", [(_C.FP32_3XTF32, True), (_C.FP32_3XTF32, False),
+                                             (_C.FP32_SIMT, False)])
+def test_update_teacher_forced(dev, name, i, E, precision, fused):
+    st, sl, upd, ref, ev, (mem, mem_ts) = _teacher_forced(dev, name, i, E=E, precision=precision, fused=fused)
     U = int(upd["num"].item())
+    # A1 outputs of the prep (fused or separate sampler) against the oracle sampler
+    cfg = CONFIGS[name]
+    roots = np.concatenate([ev[0], ev[1], ev[3]])
+    sref = oracle.Graph(cfg.num_nodes, *make_events(cfg, 0, E)[:3]).sample(roots, np.concatenate([ev[2]] * 3),
+                                                                           cfg.fanout)
+    n3 = len(roots)
+    for key in ("nbr", "eid", "ts", "dt", "cnt"):
+        assert np.array_equal(sl.samp[key][:n3].cpu().numpy(), sref[key]), key
     assert U == len(ref["nodes"])
     assert np.array_equal(upd["nodes"][:U].cpu().numpy(), ref["nodes"])
     assert np.array_equal(upd["winner"][:U].cpu().numpy(), ref["winner"])
