@@ -328,9 +328,9 @@ def run_mspipe(args):
 
 def _launches(steps, timed_batches, mit, fused):
     """Kernels of this library per timed step.  fused: prep = k_prep + k_build_x
-    (+ k_mitigate), commit = k_gru_tc + k_writeback; otherwise prep = sampler +
+    (+ k_mitigate), commit = k_gru_tc with the write-back in its epilogue; otherwise prep = sampler +
     dedup + gather (+ mitigation), commit = build + GEMM (or SIMT GRU) + write-back."""
-    per = {"prep": (2 if fused else 3) + (1 if mit else 0), "commit": 2 if fused else 3}
+    per = {"prep": (2 if fused else 3) + (1 if mit else 0), "commit": 1 if fused else 3}
     return int(sum(per[op] for t in timed_batches for op, _ in steps[t]))
 
 

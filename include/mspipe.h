@@ -286,6 +286,20 @@ MSPIPE_API mspipe_status mspipe_gru_apply(const mspipe_gru* gru, int64_t num_eve
                                const int32_t* num_unique, float* out_mem, const void* workspace,
                                size_t ws_bytes, void* stream);
 
+/* A6 + A7 in one launch: mspipe_gru_apply, then mspipe_memory_writeback of
+ * (nodes, num_unique, h', new_ts, new_mail) as version commit_version, the
+ * write-back done by the GEMM epilogue (world == 1).  new_ts / new_mail are
+ * message_build's out_ts / out_mail; out_mem (nullable) still receives h' in
+ * winner order.  Same ordering contract as mspipe_memory_writeback (the
+ * caller orders it after the fetch of iteration commit_version + k). */
+MSPIPE_API mspipe_status mspipe_gru_apply_commit(const mspipe_gru* gru, mspipe_memory* st,
+                                      int64_t commit_version, int64_t num_events,
+                                      const float* snap_mem, int64_t snap_step, const float* snap_h,
+                                      const int32_t* nodes, const int32_t* winner,
+                                      const int32_t* num_unique, const double* new_ts,
+                                      const float* new_mail, float* out_mem, const void* workspace,
+                                      size_t ws_bytes, void* stream);
+
 /* Utility (timing): record `event` (a cudaEvent_t) on `stream` with
  * cudaEventRecordExternal, so that under stream capture it becomes an
  * event-record node of the graph and can still be used for elapsed-time

@@ -26,7 +26,7 @@ EXPORTS = ("mspipe_abi_version", "mspipe_last_error", "mspipe_check", "mspipe_sa
            "mspipe_memory_committed", "mspipe_memory_reset", "mspipe_memory_fetch",
            "mspipe_memory_dedup", "mspipe_gru_create", "mspipe_gru_destroy", "mspipe_memory_update",
            "mspipe_memory_writeback", "mspipe_memory_prep", "mspipe_gru_workspace_size",
-           "mspipe_message_build", "mspipe_gru_apply", "mspipe_util_event_record")
+           "mspipe_message_build", "mspipe_gru_apply", "mspipe_gru_apply_commit", "mspipe_util_event_record")
 
 
 class MspipeError(RuntimeError):
@@ -80,6 +80,7 @@ def lib():
         L.mspipe_gru_workspace_size.restype = C.c_size_t
         L.mspipe_message_build.argtypes = [P, P, i64, P, P, P, i64, P, P, P, P, P, i64, P, C.c_size_t, P]
         L.mspipe_gru_apply.argtypes = [P, i64, P, i64, P, P, P, P, P, C.c_size_t, P]
+        L.mspipe_gru_apply_commit.argtypes = [P, P, i64, i64, P, i64, P, P, P, P, P, P, P, P, C.c_size_t, P]
         if L.mspipe_abi_version() != ABI_VERSION:
             raise RuntimeError(f"libmspipe ABI {L.mspipe_abi_version()} != binding {ABI_VERSION}")
         _lib = L
@@ -276,6 +277,17 @@ def gru_apply(gru: GruHandle, num_events, snap_mem, snap_step, winner, num, out_
     _ck(lib().mspipe_gru_apply(gru.h, int(num_events), ptr(snap_mem), int(snap_step), ptr(snap_h), ptr(winner),
                                ptr(num), ptr(out_mem), ptr(workspace), workspace.numel() * workspace.element_size(),
                                stream_ptr(stream)), "mspipe_gru_apply")
+
+
+def gru_apply_commit(gru: GruHandle, st: MemoryHandle, commit_version, num_events, snap_mem, snap_step, upd,
+                     workspace, snap_h=None, stream=None):
+    """A6+A7 in one launch: reads upd[nodes, winner, num, ts, mail] (dedup + message_build), writes the
+    state rows of version commit_version and upd["mem"] (h' in winner order)."""
+    _ck(lib().mspipe_gru_apply_commit(gru.h, st.h, int(commit_version), int(num_events), ptr(snap_mem),
+                                      int(snap_step), ptr(snap_h), ptr(upd["nodes"]), ptr(upd["winner"]),
+                                      ptr(upd["num"]), ptr(upd["ts"]), ptr(upd["mail"]), ptr(upd.get("mem")),
+                                      ptr(workspace), workspace.numel() * workspace.element_size(),
+                                      stream_ptr(stream)), "mspipe_gru_apply_commit")
 
 
 def alloc_dedup(num_events, device):

@@ -417,6 +417,40 @@ mspipe_status mspipe_gru_apply(const mspipe_gru* gru, int64_t num_events, const 
   return after_launch("gru_apply");
 }
 
+mspipe_status mspipe_gru_apply_commit(const mspipe_gru* gru, mspipe_memory* st,
+                                      int64_t commit_version, int64_t num_events,
+                                      const float* snap_mem, int64_t snap_step, const float* snap_h,
+                                      const int32_t* nodes, const int32_t* winner,
+                                      const int32_t* num_unique, const double* new_ts,
+                                      const float* new_mail, float* out_mem, const void* workspace,
+                                      size_t ws_bytes, void* stream) {
+  if (!gru || !st) return fail(MSPIPE_EINVAL, "gru_apply_commit: NULL handle");
+  if (gru->precision != MSPIPE_FP32_3XTF32)
+    return fail(MSPIPE_EUNSUPPORTED, "gru_apply_commit: only for precision MSPIPE_FP32_3XTF32");
+  if (st->world != 1) return fail(MSPIPE_EUNSUPPORTED, "gru_apply_commit: world > 1");
+  if (gru->d.M != st->mem_dim || gru->d.He != st->edge_dim) return fail(MSPIPE_EINVAL, "gru_apply_commit: dims");
+  if (commit_version != st->committed + 1)
+    return fail(MSPIPE_EORDER, "gru_apply_commit: commit_version=%lld but committed=%lld", (long long)commit_version,
+                (long long)st->committed);
+  if (num_events < 0 || num_events > gru->max_events || snap_step < 1)
+    return fail(MSPIPE_EINVAL, "gru_apply_commit: num_events=%lld snap_step=%lld", (long long)num_events,
+                (long long)snap_step);
+  if (num_events > 0) {
+    if (ws_bytes < mspipe_gru_workspace_size(gru, num_events) || !workspace)
+      return fail(MSPIPE_EINVAL, "gru_apply_commit: workspace of %zu bytes too small", ws_bytes);
+    if (!snap_mem || !nodes || !winner || !num_unique || !new_ts || !new_mail)
+      return fail(MSPIPE_EINVAL, "gru_apply_commit: null input");
+    GruCommit c{nodes, st->mem, st->mem_ts, st->mail, st->mail_ts, new_ts, new_mail, st->num_nodes, st->mail_stride};
+    cudaError_t e = launch_gru_tc(gru->d, gru->wtc, (float*)workspace, nullptr, num_events, nullptr, snap_mem, nullptr,
+                                  snap_step, snap_h, winner, num_unique, out_mem, nullptr, nullptr, 0,
+                                  (cudaStream_t)stream, kGruGemm, &c);
+    if (e != cudaSuccess) return cuda_status(e, "gru_apply_commit: launch");
+  }
+  mspipe_status rc = after_launch("gru_apply_commit");
+  if (rc == MSPIPE_OK) st->committed = commit_version;  // i_upd <- i (Alg. 1 L16)
+  return rc;
+}
+
 mspipe_status mspipe_util_event_record(void* event, void* stream) {
   if (!event) return fail(MSPIPE_EINVAL, "util_event_record: NULL event");
   return cuda_status(cudaEventRecordWithFlags((cudaEvent_t)event, (cudaStream_t)stream, cudaEventRecordExternal),

@@ -279,6 +279,17 @@ struct TcArgs {
   double* out_ts;
   float* out_mail;
   int64_t mail_stride;
+  // fused A7 (commit_mem != nullptr): h' goes straight to mem[node]; the
+  // commit ts and mail rows staged by k_build_x (new_ts, new_mail) are copied
+  // to mem_ts / mail_ts / mail[node]
+  const int32_t* nodes;
+  float* commit_mem;
+  double* commit_mem_ts;
+  float* commit_mail;
+  double* commit_mail_ts;
+  const double* new_ts;
+  const float* new_mail;
+  int64_t num_nodes;
 };
 
 // A5: one warp per (row, chunk).  lane = column inside the chunk.
@@ -342,6 +353,38 @@ __device__ __forceinline__ float4 gates4(const float* pr, const float* pz, const
   return make_float4(out[0], out[1], out[2], out[3]);
 }
 
+// h' of winner u, hidden units j0..j0+3: to out_mem (winner order) and, when
+// the write-back is fused (A7), to the state row of its node.
+__device__ __forceinline__ void store_h4(const TcArgs& a, int32_t u, int32_t node, int32_t j0, float4 h) {
+  if (a.out_mem) *reinterpret_cast<float4*>(a.out_mem + (int64_t)u * a.d.M + j0) = h;
+  if (a.commit_mem && node >= 0) *reinterpret_cast<float4*>(a.commit_mem + (int64_t)node * a.d.M + j0) = h;
+}
+
+// fused A7, rest of the row: mem_ts = mail_ts = t*, mail row = staged x[0:Dm];
+// the float4 columns of the mail row are spread over the hidden tiles.
+__device__ __forceinline__ void commit_rows(const TcArgs& a, int32_t m0, int32_t U, int rb, int re, int jt,
+                                            const int32_t* rownode) {
+  const int J = (int)gridDim.y;
+  const int Q = (int)(a.mail_stride / 4);
+  const int c0 = jt * Q / J, c1 = (jt + 1) * Q / J, nq = c1 - c0;
+  const float4* src = reinterpret_cast<const float4*>(a.new_mail);
+  float4* dst = reinterpret_cast<float4*>(a.commit_mail);
+  for (int it = threadIdx.x; it < (re - rb) * nq; it += blockDim.x) {
+    const int mm = rb + it / nq, c = c0 + it % nq;
+    const int32_t u = m0 + mm, node = rownode[mm];
+    if (u < U && node >= 0) dst[(int64_t)node * Q + c] = __ldg(src + (int64_t)u * Q + c);
+  }
+  if (jt == 0)
+    for (int mm = rb + (int)threadIdx.x; mm < re; mm += blockDim.x) {
+      const int32_t u = m0 + mm, node = rownode[mm];
+      if (u < U && node >= 0) {
+        const double t = __ldg(a.new_ts + u);
+        a.commit_mem_ts[node] = t;
+        a.commit_mail_ts[node] = t;
+      }
+    }
+}
+
 __global__ void __launch_bounds__(tc::kThreads, 1) k_gru_tc(TcArgs a) {
   using namespace tc;
   extern __shared__ uint8_t smem_raw[];
@@ -350,7 +393,8 @@ __global__ void __launch_bounds__(tc::kThreads, 1) k_gru_tc(TcArgs a) {
   uint64_t* empty = full + kStages;
   uint64_t* acc_full = empty + kStages;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 1);
-  float4* hbuf = reinterpret_cast<float4*>(smem + kStages * kStageBytes + 1024);  // [128 rows][kJ/4]
+  int32_t* rownode = reinterpret_cast<int32_t*>(smem + kStages * kStageBytes + 512);  // [128] node of each row
+  float4* hbuf =reinterpret_cast<float4*>(smem + kStages * kStageBytes + 1024);  // [128 rows][kJ/4]
   float4* recv = reinterpret_cast<float4*>(smem + kStages * kStageBytes + 1024 + kHBufBytes);
 
   const GruDesc& d = a.d;
@@ -442,6 +486,7 @@ __global__ void __launch_bounds__(tc::kThreads, 1) k_gru_tc(TcArgs a) {
         hv = __ldg(reinterpret_cast<const float4*>(hrow + j0));
       }
       hbuf[mm * (kJ / 4) + q] = hv;
+      if (q == 0) rownode[mm] = (a.commit_mem && u < U) ? __ldg(a.nodes + u) : -1;
     }
   }
   __syncwarp();
@@ -508,10 +553,10 @@ __global__ void __launch_bounds__(tc::kThreads, 1) k_gru_tc(TcArgs a) {
           pnx[e] = __uint_as_float(r1[jj]) + __ldg(bias + 2 * kJ + jj);
           pnh[e] = __uint_as_float(r1[kJ + jj]) + __ldg(bias + 3 * kJ + jj);
         }
-        *reinterpret_cast<float4*>(a.out_mem + (int64_t)u * d.M + j0) =
-            gates4(pr, pz, pnx, pnh, hbuf[m * (kJ / 4) + q]);
+        store_h4(a, u, rownode[m], j0, gates4(pr, pz, pnx, pnh, hbuf[m * (kJ / 4) + q]));
       }
     }
+    if (a.commit_mem) commit_rows(a, m0, U, 0, kM, jt, rownode);
   } else {
     cluster_sync_all();  // all pushes into recv are visible; nobody writes recv afterwards
     PHASE(6);
@@ -545,9 +590,9 @@ __global__ void __launch_bounds__(tc::kThreads, 1) k_gru_tc(TcArgs a) {
         pnx[e] = (&acc[2].x)[e] + __ldg(bias + 2 * kJ + jj);
         pnh[e] = (&acc[3].x)[e] + __ldg(bias + 3 * kJ + jj);
       }
-      *reinterpret_cast<float4*>(a.out_mem + (int64_t)u * d.M + j0) =
-          gates4(pr, pz, pnx, pnh, hbuf[mm * (kJ / 4) + q]);
+      store_h4(a, u, rownode[mm], j0, gates4(pr, pz, pnx, pnh, hbuf[mm * (kJ / 4) + q]));
     }
+    if (a.commit_mem) commit_rows(a, m0, U, rb, rb + R, jt, rownode);
     PHASE(8);
   }
 }
@@ -576,7 +621,7 @@ cudaError_t launch_gru_tc(const GruDesc& d, const float* wtc, float* xbuf, const
                           const float* edge_feat, const float* snap_mem, const double* snap_mem_ts,
                           int64_t snap_step, const float* snap_h, const int32_t* winner,
                           const int32_t* num_unique, float* out_mem, double* out_ts, float* out_mail,
-                          int64_t mail_stride, cudaStream_t s, int parts) {
+                          int64_t mail_stride, cudaStream_t s, int parts, const GruCommit* commit) {
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(k_gru_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::kSmemBytes);
@@ -584,7 +629,19 @@ cudaError_t launch_gru_tc(const GruDesc& d, const float* wtc, float* xbuf, const
     attr_set = true;
   }
   TcArgs a{d, wtc, xbuf, ts, num_events, edge_feat, snap_mem, snap_mem_ts, snap_step, snap_h, winner,
-           num_unique, out_mem, out_ts, out_mail, mail_stride};
+           num_unique, out_mem, out_ts, out_mail, mail_stride, nullptr, nullptr, nullptr, nullptr, nullptr,
+           nullptr, nullptr, 0};
+  if (commit) {
+    a.nodes = commit->nodes;
+    a.commit_mem = commit->mem;
+    a.commit_mem_ts = commit->mem_ts;
+    a.commit_mail = commit->mail;
+    a.commit_mail_ts = commit->mail_ts;
+    a.new_ts = commit->new_ts;
+    a.new_mail = commit->new_mail;
+    a.num_nodes = commit->num_nodes;
+    a.mail_stride = commit->mail_stride;
+  }
   const int64_t max_rows = 2 * num_events;
   const int64_t mtiles = (max_rows + tc::kM - 1) / tc::kM;
   if (parts & kGruBuild) {

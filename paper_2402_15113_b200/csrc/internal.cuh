@@ -161,11 +161,23 @@ size_t gru_tc_xbuf_floats(const GruDesc& d, int64_t max_events);
 void launch_gru_pack_tc(const float* w_ih, const float* w_hh, const float* b_ih, const float* b_hh,
                         const GruDesc& d, float* wtc, float* bias, cudaStream_t s);
 enum { kGruBuild = 1, kGruGemm = 2 };
+struct GruCommit {  // fused A7 in the GEMM epilogue
+  const int32_t* nodes;
+  float* mem;
+  double* mem_ts;
+  float* mail;
+  double* mail_ts;
+  const double* new_ts;
+  const float* new_mail;
+  int64_t num_nodes;
+  int64_t mail_stride;
+};
 cudaError_t launch_gru_tc(const GruDesc& d, const float* wtc, float* xbuf, const double* ts, int64_t num_events,
                           const float* edge_feat, const float* snap_mem, const double* snap_mem_ts,
                           int64_t snap_step, const float* snap_h, const int32_t* winner,
                           const int32_t* num_unique, float* out_mem, double* out_ts, float* out_mail,
-                          int64_t mail_stride, cudaStream_t s, int parts = kGruBuild | kGruGemm);
+                          int64_t mail_stride, cudaStream_t s, int parts = kGruBuild | kGruGemm,
+                          const GruCommit* commit = nullptr);
 // prep.cu
 cudaError_t launch_prep(const Tcsr& g, const int32_t* src, const int32_t* dst, const int32_t* neg,
                         const double* ts, int64_t num_events, int32_t fanout, int32_t* out_nbr,

@@ -241,6 +241,8 @@ class MemoryStage:
                                     sl.mail_ts[:m] if sl.mail_ts is not None else None, self._mitigation(sl, x, n))
         self._ev("prep_end")
         self.versions[i] = sl.version
+        self._fetched = torch.cuda.Event()  # the state tables have been read for batch i
+        self._fetched.record()
         self._ev("build")
         _C.message_build(self.gru, x["ts"], x["ef"], sl.mem, sl.mem_ts, cfg.fanout + 1, sl.dd["winner"][: 2 * n],
                          sl.dd["num"], sl.uts[: 2 * n], sl.umail[: 2 * n], sl.ws,
@@ -284,8 +286,26 @@ class MemoryStage:
             self.out_host["mem"][:n2].copy_(upd["mem"], non_blocking=True)
 
     def commit(self, i):
+        if self.fused:
+            self.apply_commit(i)
+            return
         self.update(i)
         self.writeback(i)
+
+    def apply_commit(self, i):
+        """Fused A6 + A7 (mspipe_gru_apply_commit): GRU of batch i, write-back in its epilogue."""
+        cfg, sl = self.cfg, self._slot(i)
+        n = self.inputs(i)["src"].numel()
+        upd = self._upd(i)
+        self._ev("update")
+        _C.gru_apply_commit(self.gru, self.memory, i, n, sl.mem, cfg.fanout + 1, upd, sl.ws,
+                            snap_h=sl.h[: 2 * n] if sl.h is not None else None)
+        self._ev("update_end")
+        if self.staged:
+            n2 = upd["nodes"].numel()
+            self.out_host["num"].copy_(upd["num"], non_blocking=True)
+            self.out_host["nodes"][:n2].copy_(upd["nodes"], non_blocking=True)
+            self.out_host["mem"][:n2].copy_(upd["mem"], non_blocking=True)
 
     def run_ops(self, ops, overlap=None):
         """Enqueue ops in order.  With overlap (default when k >= 1), preps of
@@ -315,6 +335,12 @@ class MemoryStage:
                     self.prep(i)
             elif op == "prep":
                 self.prep(i)
+            elif self.fused:
+                # the epilogue writes the tables: wait only for the side stream's
+                # fetch (not its message build, which overlaps this GEMM)
+                if forked:
+                    main.wait_event(self._fetched)
+                self.apply_commit(i)
             else:
                 self.update(i)
                 if forked and not joined:
