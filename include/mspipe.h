@@ -121,9 +121,10 @@ MSPIPE_API mspipe_status mspipe_sample_batch(const mspipe_tcsr* g, const int32_t
  * staleness_k is the build staleness k (= paper k - 1, G8): a fetch for
  * iteration i is legal iff  i-1-k <= committed <= i-1  (Eq. 2, P:L196-L204;
  * Alg. 1 gate "while i - i_upd > k_i: wait").
- * world == 1 only in this build (world > 1 returns MSPIPE_EUNSUPPORTED).
- * create allocates O(num_nodes) int32 scratch + an error flag on the current
- * device; destroy frees them.
+ * world > 1: see "Row E" below (the tables are this rank's shard).
+ * create allocates O(num_nodes) scratch (and, for world > 1, the fixed-capacity
+ * exchange buffers and the NCCL communicator) on the current device; destroy
+ * frees them.
  * ------------------------------------------------------------------------- */
 typedef struct mspipe_memory mspipe_memory;
 
@@ -299,6 +300,57 @@ MSPIPE_API mspipe_status mspipe_gru_apply_commit(const mspipe_gru* gru, mspipe_m
                                       const int32_t* num_unique, const double* new_ts,
                                       const float* new_mail, float* out_mem, const void* workspace,
                                       size_t ws_bytes, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Row E: node memory sharded by node id (world > 1).  owner(v) = v mod world,
+ * local row = v / world: the tables passed to mspipe_memory_create hold this
+ * rank's rows only (ceil((num_nodes - rank) / world) rows).  Every rank runs
+ * the same iterations on its own local batch of each global batch;
+ * the T-CSR is replicated (sampling and dedup stay local).
+ *
+ * With an nccl_unique_id at create, mspipe_memory_fetch and
+ * mspipe_memory_writeback_keyed are collective (every rank calls them with
+ * the same iteration / version, in the same stream order) and run NCCL
+ * all-to-alls on `stream`.  Without one (NULL) the handle is an in-process
+ * rank: the caller drives the phases below for all ranks and moves the
+ * buffers with mspipe_shard_loopback (one process, e.g. G virtual ranks on
+ * one GPU for testing).  MSPipe-S mitigation is not available for world > 1
+ * in this build (MSPIPE_EUNSUPPORTED).
+ *
+ * Phases of a fetch: plan -> exchange(FETCH_IDS) -> serve -> exchange(
+ * FETCH_ROWS) -> finish.  Phases of a commit: pack -> exchange(COMMIT) ->
+ * merge.  The LWW key of a record is key_base + winner pair index, key_base =
+ * 2 x (global index of this rank's first event in the iteration), i.e. the
+ * global pair index of the single-GPU batch G·B; the owner keeps, per node,
+ * the record with the largest key (64-bit atomicMax, then a keyed copy), so
+ * the result does not depend on arrival order.
+ * ------------------------------------------------------------------------- */
+enum { MSPIPE_XCHG_FETCH_IDS = 0, MSPIPE_XCHG_FETCH_ROWS = 1, MSPIPE_XCHG_COMMIT = 2 };
+
+MSPIPE_API int64_t mspipe_memory_local_rows(const mspipe_memory* st); /* [host] rows of this rank's tables */
+/* [host] rank 0 creates the NCCL unique id (128 bytes) and broadcasts it
+ * (e.g. through torch.distributed) before every rank's mspipe_memory_create. */
+MSPIPE_API int32_t mspipe_nccl_unique_id(void* out, int32_t out_bytes);
+MSPIPE_API mspipe_status mspipe_memory_writeback_keyed(mspipe_memory* st, int64_t commit_version,
+                                            const int32_t* nodes, const int32_t* winner,
+                                            const int32_t* num_unique, int64_t max_n, int64_t key_base,
+                                            const float* new_mem, const double* new_ts,
+                                            const float* new_mail, void* stream);
+MSPIPE_API mspipe_status mspipe_shard_fetch_plan(mspipe_memory* st, int64_t iteration, const int32_t* ids,
+                                      int64_t n, int32_t with_mail, void* stream);
+MSPIPE_API mspipe_status mspipe_shard_fetch_serve(mspipe_memory* st, void* stream);
+MSPIPE_API mspipe_status mspipe_shard_fetch_finish(mspipe_memory* st, const int32_t* ids, int64_t n,
+                                        float* out_mem, double* out_mem_ts, float* out_mail,
+                                        double* out_mail_ts, int64_t* out_version, void* stream);
+MSPIPE_API mspipe_status mspipe_shard_commit_pack(mspipe_memory* st, int64_t commit_version,
+                                       const int32_t* nodes, const int32_t* winner,
+                                       const int32_t* num_unique, int64_t max_n, int64_t key_base,
+                                       const float* new_mem, const double* new_ts,
+                                       const float* new_mail, void* stream);
+MSPIPE_API mspipe_status mspipe_shard_commit_merge(mspipe_memory* st, int64_t commit_version, void* stream);
+MSPIPE_API mspipe_status mspipe_shard_exchange(mspipe_memory* st, int32_t kind, void* stream);
+MSPIPE_API mspipe_status mspipe_shard_loopback(mspipe_memory* const* ranks, int32_t world, int32_t kind,
+                                    void* stream);
 
 /* Utility (timing): record `event` (a cudaEvent_t) on `stream` with
  * cudaEventRecordExternal, so that under stream capture it becomes an

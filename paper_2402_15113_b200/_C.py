@@ -26,7 +26,11 @@ EXPORTS = ("mspipe_abi_version", "mspipe_last_error", "mspipe_check", "mspipe_sa
            "mspipe_memory_committed", "mspipe_memory_reset", "mspipe_memory_fetch",
            "mspipe_memory_dedup", "mspipe_gru_create", "mspipe_gru_destroy", "mspipe_memory_update",
            "mspipe_memory_writeback", "mspipe_memory_prep", "mspipe_gru_workspace_size",
-           "mspipe_message_build", "mspipe_gru_apply", "mspipe_gru_apply_commit", "mspipe_util_event_record")
+           "mspipe_message_build", "mspipe_gru_apply", "mspipe_gru_apply_commit", "mspipe_util_event_record",
+           "mspipe_memory_local_rows", "mspipe_nccl_unique_id", "mspipe_memory_writeback_keyed",
+           "mspipe_shard_fetch_plan", "mspipe_shard_fetch_serve", "mspipe_shard_fetch_finish",
+           "mspipe_shard_commit_pack", "mspipe_shard_commit_merge", "mspipe_shard_exchange", "mspipe_shard_loopback")
+XCHG_FETCH_IDS, XCHG_FETCH_ROWS, XCHG_COMMIT = 0, 1, 2
 
 
 class MspipeError(RuntimeError):
@@ -81,6 +85,17 @@ def lib():
         L.mspipe_message_build.argtypes = [P, P, i64, P, P, P, i64, P, P, P, P, P, i64, P, C.c_size_t, P]
         L.mspipe_gru_apply.argtypes = [P, i64, P, i64, P, P, P, P, P, C.c_size_t, P]
         L.mspipe_gru_apply_commit.argtypes = [P, P, i64, i64, P, i64, P, P, P, P, P, P, P, P, C.c_size_t, P]
+        L.mspipe_memory_local_rows.argtypes = [P]
+        L.mspipe_memory_local_rows.restype = i64
+        L.mspipe_nccl_unique_id.argtypes = [P, i32]
+        L.mspipe_memory_writeback_keyed.argtypes = [P, i64, P, P, P, i64, i64, P, P, P, P]
+        L.mspipe_shard_fetch_plan.argtypes = [P, i64, P, i64, i32, P]
+        L.mspipe_shard_fetch_serve.argtypes = [P, P]
+        L.mspipe_shard_fetch_finish.argtypes = [P, P, i64, P, P, P, P, C.POINTER(i64), P]
+        L.mspipe_shard_commit_pack.argtypes = [P, i64, P, P, P, i64, i64, P, P, P, P]
+        L.mspipe_shard_commit_merge.argtypes = [P, i64, P]
+        L.mspipe_shard_exchange.argtypes = [P, i32, P]
+        L.mspipe_shard_loopback.argtypes = [P, i32, i32, P]
         if L.mspipe_abi_version() != ABI_VERSION:
             raise RuntimeError(f"libmspipe ABI {L.mspipe_abi_version()} != binding {ABI_VERSION}")
         _lib = L
@@ -182,17 +197,23 @@ class MemoryHandle:
     """mspipe_memory over caller-owned (here: this object's) state tables."""
 
     def __init__(self, num_nodes, mem_dim, edge_dim, staleness_k, device, rank=0, world=1, nccl_id=None):
+        """world > 1: the tables hold this rank's shard (rows v with v % world == rank);
+        nccl_id (bytes) selects the NCCL transport, None the in-process loopback."""
         self.num_nodes, self.mem_dim, self.edge_dim, self.k = num_nodes, mem_dim, edge_dim, staleness_k
+        self.rank, self.world = rank, world
         self.mail_stride = mail_stride_for(mem_dim, edge_dim)
-        self.mem = torch.zeros((num_nodes, mem_dim), dtype=torch.float32, device=device)
-        self.mem_ts = torch.zeros((num_nodes,), dtype=torch.float64, device=device)
-        self.mail = torch.zeros((num_nodes, self.mail_stride), dtype=torch.float32, device=device)
-        self.mail_ts = torch.zeros((num_nodes,), dtype=torch.float64, device=device)
+        rows = (num_nodes - rank + world - 1) // world
+        self.mem = torch.zeros((rows, mem_dim), dtype=torch.float32, device=device)
+        self.mem_ts = torch.zeros((rows,), dtype=torch.float64, device=device)
+        self.mail = torch.zeros((rows, self.mail_stride), dtype=torch.float32, device=device)
+        self.mail_ts = torch.zeros((rows,), dtype=torch.float64, device=device)
         h = C.c_void_p()
+        self._nccl_id = None if nccl_id is None else C.create_string_buffer(bytes(nccl_id), len(nccl_id))
         _ck(lib().mspipe_memory_create(C.byref(h), num_nodes, mem_dim, edge_dim, staleness_k, ptr(self.mem),
                                        ptr(self.mem_ts), ptr(self.mail), ptr(self.mail_ts), self.mail_stride,
-                                       rank, world, nccl_id), "mspipe_memory_create")
+                                       rank, world, self._nccl_id), "mspipe_memory_create")
         self.h = h
+        assert lib().mspipe_memory_local_rows(h) == rows
 
     def __del__(self):
         if getattr(self, "h", None) and _lib is not None:
@@ -209,6 +230,55 @@ class MemoryHandle:
             for t in (self.mem, self.mem_ts, self.mail, self.mail_ts):
                 t.zero_()
         _ck(lib().mspipe_memory_reset(self.h), "mspipe_memory_reset")
+
+
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    _ck(lib().mspipe_nccl_unique_id(buf, 128), "mspipe_nccl_unique_id")
+    return buf.raw
+
+
+def memory_writeback_keyed(st: MemoryHandle, commit_version, upd, key_base, stream=None):
+    _ck(lib().mspipe_memory_writeback_keyed(st.h, int(commit_version), ptr(upd["nodes"]), ptr(upd["winner"]),
+                                            ptr(upd["num"]), upd["nodes"].numel(), int(key_base), ptr(upd["mem"]),
+                                            ptr(upd["ts"]), ptr(upd["mail"]), stream_ptr(stream)),
+        "mspipe_memory_writeback_keyed")
+
+
+def shard_fetch_plan(st, iteration, ids, with_mail=False, stream=None):
+    _ck(lib().mspipe_shard_fetch_plan(st.h, int(iteration), ptr(ids), ids.numel(), 1 if with_mail else 0,
+                                      stream_ptr(stream)), "mspipe_shard_fetch_plan")
+
+
+def shard_fetch_serve(st, stream=None):
+    _ck(lib().mspipe_shard_fetch_serve(st.h, stream_ptr(stream)), "mspipe_shard_fetch_serve")
+
+
+def shard_fetch_finish(st, ids, out_mem, out_mem_ts, out_mail=None, out_mail_ts=None, stream=None) -> int:
+    v = i64(-1)
+    _ck(lib().mspipe_shard_fetch_finish(st.h, ptr(ids), ids.numel(), ptr(out_mem), ptr(out_mem_ts), ptr(out_mail),
+                                        ptr(out_mail_ts), C.byref(v), stream_ptr(stream)), "mspipe_shard_fetch_finish")
+    return int(v.value)
+
+
+def shard_commit_pack(st, commit_version, upd, key_base, stream=None):
+    _ck(lib().mspipe_shard_commit_pack(st.h, int(commit_version), ptr(upd["nodes"]), ptr(upd["winner"]),
+                                       ptr(upd["num"]), upd["nodes"].numel(), int(key_base), ptr(upd["mem"]),
+                                       ptr(upd["ts"]), ptr(upd["mail"]), stream_ptr(stream)),
+        "mspipe_shard_commit_pack")
+
+
+def shard_commit_merge(st, commit_version, stream=None):
+    _ck(lib().mspipe_shard_commit_merge(st.h, int(commit_version), stream_ptr(stream)), "mspipe_shard_commit_merge")
+
+
+def shard_exchange(st, kind, stream=None):
+    _ck(lib().mspipe_shard_exchange(st.h, int(kind), stream_ptr(stream)), "mspipe_shard_exchange")
+
+
+def shard_loopback(handles, kind, stream=None):
+    arr = (C.c_void_p * len(handles))(*[h.h.value for h in handles])
+    _ck(lib().mspipe_shard_loopback(arr, len(handles), int(kind), stream_ptr(stream)), "mspipe_shard_loopback")
 
 
 def memory_fetch(st: MemoryHandle, iteration, ids, out_mem, out_mem_ts, out_mail=None, out_mail_ts=None,

@@ -9,3 +9,4 @@ from . import _C  # noqa: F401
 from .build import build  # noqa: F401
 from .graph import build_tcsr, build_tcsr_host, gamma_quantile  # noqa: F401
 from .stage import MemoryStage, StageConfig, schedule_ops, snapshot_versions  # noqa: F401
+from .shard import LoopbackShards, ShardRank, key_base, local_range  # noqa: F401

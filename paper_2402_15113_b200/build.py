@@ -10,11 +10,25 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libmspipe.so")
-SOURCES = ["api.cu", "sampler.cu", "memory.cu", "prep.cu", "gru_simt.cu", "gru_tc.cu"]
+SOURCES = ["api.cu", "sampler.cu", "memory.cu", "prep.cu", "gru_simt.cu", "gru_tc.cu", "shard.cu", "nccl_xchg.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+
+
+def _nccl_dir():
+    """NCCL ships with the torch wheel (nvidia/nccl): headers + libnccl.so.2."""
+    import importlib.util
+    spec = importlib.util.find_spec("nvidia")
+    for base in (spec.submodule_search_locations if spec else []):
+        d = os.path.join(base, "nccl")
+        if os.path.exists(os.path.join(d, "include", "nccl.h")):
+            return d
+    raise RuntimeError("nccl.h not found (expected site-packages/nvidia/nccl)")
+
+
+NCCL = _nccl_dir()
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-rdc=true", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC,-fvisibility=hidden", "--expt-relaxed-constexpr",
-         "-I", os.path.join(ROOT, "include"), "-I", CSRC]
+         "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-I", os.path.join(NCCL, "include")]
 
 
 def _stale() -> bool:
@@ -48,7 +62,8 @@ def build(force: bool = False, verbose: bool = False, extra_flags=(), out: str |
             raise RuntimeError("nvcc failed: " + " ".join(cmd))
     tmp = lib + f".{os.getpid()}.tmp"
     subprocess.check_call([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-rdc=true", "-shared", "-o", tmp, *objs,
-                           "-Xcompiler", "-fPIC"])
+                           "-Xcompiler", "-fPIC", "-L", os.path.join(NCCL, "lib"), "-l:libnccl.so.2",
+                           "-Xlinker", "-rpath=" + os.path.join(NCCL, "lib")])
     os.replace(tmp, lib)
     return lib
 

@@ -112,9 +112,8 @@ mspipe_status mspipe_memory_create(mspipe_memory** out, int64_t num_nodes, int32
   int32_t Dm = 2 * mem_dim + edge_dim;
   if (mail_stride < Dm || mail_stride % 4) return fail(MSPIPE_EINVAL, "memory_create: mail_stride=%lld must be >= %d and a multiple of 4", (long long)mail_stride, Dm);
   if (!mem || !mem_ts || !mail || !mail_ts) return fail(MSPIPE_EINVAL, "memory_create: null table");
-  if (world != 1 || rank != 0)
-    return fail(MSPIPE_EUNSUPPORTED, "memory_create: world=%d: sharded memory is not in this build", world);
-  (void)nccl_unique_id;
+  if (world < 1 || world > 64 || rank < 0 || rank >= world)
+    return fail(MSPIPE_EINVAL, "memory_create: rank=%d world=%d (1..64)", rank, world);
   (void)num_sms();  // cache the SM count now: later calls may run under stream capture
   mspipe_memory* st = new mspipe_memory();
   st->num_nodes = num_nodes;
@@ -131,13 +130,37 @@ mspipe_status mspipe_memory_create(mspipe_memory** out, int64_t num_nodes, int32
   st->world = world;
   st->committed = 0;
   cudaGetDevice(&st->device);
+  st->local_rows = (num_nodes - rank + world - 1) / world;
   cudaError_t e = cudaMalloc(&st->scratch, sizeof(int32_t) * (size_t)num_nodes);
   if (e == cudaSuccess) e = cudaMemset(st->scratch, 0xFF, sizeof(int32_t) * (size_t)num_nodes);
+  if (e == cudaSuccess && world > 1) {
+    st->sh_cap = (num_nodes + world - 1) / world;
+    st->sh_capw = st->sh_cap;  // unique nodes per owner never exceed its shard
+    const size_t cw = (size_t)world * st->sh_cap;
+    e = cudaMalloc(&st->sh_needed, (size_t)num_nodes);
+    if (e == cudaSuccess) e = cudaMemset(st->sh_needed, 0, (size_t)num_nodes);
+    if (e == cudaSuccess) e = cudaMalloc(&st->sh_slot_of, sizeof(int32_t) * (size_t)num_nodes);
+    if (e == cudaSuccess) e = cudaMalloc(&st->sh_send_ids, sizeof(int32_t) * cw);
+    if (e == cudaSuccess) e = cudaMalloc(&st->sh_recv_ids, sizeof(int32_t) * cw);
+    if (e == cudaSuccess) e = cudaMalloc(&st->sh_fsend, (size_t)shard_fetch_rec_bytes(st, true) * cw);
+    if (e == cudaSuccess) e = cudaMalloc(&st->sh_frecv, (size_t)shard_fetch_rec_bytes(st, true) * cw);
+    if (e == cudaSuccess) e = cudaMalloc(&st->sh_csend, (size_t)shard_commit_rec_bytes(st) * world * st->sh_capw);
+    if (e == cudaSuccess) e = cudaMalloc(&st->sh_crecv, (size_t)shard_commit_rec_bytes(st) * world * st->sh_capw);
+    if (e == cudaSuccess) e = cudaMalloc(&st->sh_dest, sizeof(int32_t) * (size_t)num_nodes);
+    if (e == cudaSuccess) e = cudaMalloc(&st->sh_keytab, sizeof(unsigned long long) * (size_t)st->local_rows);
+    if (e == cudaSuccess) e = cudaMemset(st->sh_keytab, 0, sizeof(unsigned long long) * (size_t)st->local_rows);
+  }
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   if (e != cudaSuccess) {
-    if (st->scratch) cudaFree(st->scratch);
-    delete st;
+    mspipe_memory_destroy(st);
     return cuda_status(e, "memory_create: scratch");
+  }
+  if (world > 1 && nccl_unique_id) {
+    mspipe_status rc = nccl_comm_init(st, nccl_unique_id);
+    if (rc != MSPIPE_OK) {
+      mspipe_memory_destroy(st);
+      return rc;
+    }
   }
   *out = st;
   return MSPIPE_OK;
@@ -145,16 +168,27 @@ mspipe_status mspipe_memory_create(mspipe_memory** out, int64_t num_nodes, int32
 
 mspipe_status mspipe_memory_destroy(mspipe_memory* st) {
   if (!st) return MSPIPE_OK;
-  if (st->scratch) cudaFree(st->scratch);
+  nccl_comm_destroy(st);
+  void* bufs[] = {st->scratch, st->sh_needed, st->sh_slot_of, st->sh_send_ids, st->sh_recv_ids, st->sh_fsend,
+                  st->sh_frecv, st->sh_csend, st->sh_crecv, st->sh_dest, st->sh_keytab};
+  for (void* b : bufs)
+    if (b) cudaFree(b);
   delete st;
   return MSPIPE_OK;
 }
+
+int64_t mspipe_memory_local_rows(const mspipe_memory* st) { return st ? st->local_rows : -1; }
 
 int64_t mspipe_memory_committed(const mspipe_memory* st) { return st ? st->committed : -1; }
 
 mspipe_status mspipe_memory_reset(mspipe_memory* st) {
   if (!st) return fail(MSPIPE_EINVAL, "memory_reset: NULL handle");
   st->committed = 0;
+  if (st->sh_keytab) {  // keys restart with the stream
+    cudaError_t e = cudaMemset(st->sh_keytab, 0, sizeof(unsigned long long) * (size_t)st->local_rows);
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) return cuda_status(e, "memory_reset");
+  }
   return MSPIPE_OK;
 }
 
@@ -170,6 +204,19 @@ mspipe_status mspipe_memory_fetch(mspipe_memory* st, int64_t iteration, const in
                 (long long)iteration, (long long)st->committed, st->k);
   if (n > 0 && (!ids || !out_mem || !out_mem_ts)) return fail(MSPIPE_EINVAL, "memory_fetch: null ids/outputs");
   if ((out_mail == nullptr) != (out_mail_ts == nullptr)) return fail(MSPIPE_EINVAL, "memory_fetch: out_mail and out_mail_ts go together");
+  if (st->world > 1) {
+    if (mit) return fail(MSPIPE_EUNSUPPORTED, "memory_fetch: mitigation with world > 1 is not in this build");
+    if (!st->nccl_comm) return fail(MSPIPE_EUNSUPPORTED, "memory_fetch: in-process rank: use the mspipe_shard_* phases");
+    cudaStream_t s = (cudaStream_t)stream;
+    mspipe_status rc = mspipe_shard_fetch_plan(st, iteration, ids, n, out_mail != nullptr, stream);
+    if (rc == MSPIPE_OK) rc = mspipe_shard_exchange(st, MSPIPE_XCHG_FETCH_IDS, stream);
+    if (rc == MSPIPE_OK) rc = mspipe_shard_fetch_serve(st, stream);
+    if (rc == MSPIPE_OK) rc = mspipe_shard_exchange(st, MSPIPE_XCHG_FETCH_ROWS, stream);
+    if (rc == MSPIPE_OK)
+      rc = mspipe_shard_fetch_finish(st, ids, n, out_mem, out_mem_ts, out_mail, out_mail_ts, out_version, stream);
+    (void)s;
+    return rc;
+  }
   if (mit) {
     if (!tcsr_ok(mit->g) || !mit->src || !mit->dst || !mit->ts || !mit->out_h || mit->num_events < 0)
       return fail(MSPIPE_EINVAL, "memory_fetch: bad mitigation arguments");
@@ -312,6 +359,7 @@ mspipe_status mspipe_memory_writeback(mspipe_memory* st, int64_t commit_version,
                                       int64_t max_n, const float* new_mem, const double* new_ts,
                                       const float* new_mail, void* stream) {
   if (!st) return fail(MSPIPE_EINVAL, "memory_writeback: NULL handle");
+  if (st->world > 1) return fail(MSPIPE_EINVAL, "memory_writeback: world > 1 needs mspipe_memory_writeback_keyed");
   if (commit_version != st->committed + 1)
     return fail(MSPIPE_EORDER, "memory_writeback: commit_version=%lld but committed=%lld", (long long)commit_version, (long long)st->committed);
   if (max_n < 0) return fail(MSPIPE_EINVAL, "memory_writeback: max_n=%lld", (long long)max_n);
@@ -334,6 +382,7 @@ mspipe_status mspipe_memory_prep(mspipe_memory* st, const mspipe_tcsr* g, int64_
                                  double* out_mem_ts, float* out_mail, double* out_mail_ts,
                                  const mspipe_mitigation* mit, int64_t* out_version, void* stream) {
   if (!st) return fail(MSPIPE_EINVAL, "memory_prep: NULL handle");
+  if (st->world > 1) return fail(MSPIPE_EUNSUPPORTED, "memory_prep: fused prep reads local tables; world > 1 uses the sharded fetch");
   if (!tcsr_ok(g) || g->num_nodes != st->num_nodes) return fail(MSPIPE_EINVAL, "memory_prep: bad T-CSR");
   if (iteration < 1 || num_events < 0 || num_events > 8192 || fanout < 1 || fanout > 31)
     return fail(MSPIPE_EINVAL, "memory_prep: iteration=%lld num_events=%lld (<= 8192) fanout=%d (<= 31)",
@@ -449,6 +498,148 @@ mspipe_status mspipe_gru_apply_commit(const mspipe_gru* gru, mspipe_memory* st,
   mspipe_status rc = after_launch("gru_apply_commit");
   if (rc == MSPIPE_OK) st->committed = commit_version;  // i_upd <- i (Alg. 1 L16)
   return rc;
+}
+
+// ---------------------------------------------------------------------------
+// row E: sharded memory
+// ---------------------------------------------------------------------------
+int32_t mspipe_nccl_unique_id(void* out, int32_t out_bytes) {
+  if (!out || out_bytes < nccl_unique_id_bytes()) return fail(MSPIPE_EINVAL, "nccl_unique_id: buffer < %d bytes", nccl_unique_id_bytes());
+  return nccl_get_unique_id(out);
+}
+
+mspipe_status mspipe_memory_writeback_keyed(mspipe_memory* st, int64_t commit_version,
+                                            const int32_t* nodes, const int32_t* winner,
+                                            const int32_t* num_unique, int64_t max_n, int64_t key_base,
+                                            const float* new_mem, const double* new_ts,
+                                            const float* new_mail, void* stream) {
+  if (!st) return fail(MSPIPE_EINVAL, "memory_writeback_keyed: NULL handle");
+  if (st->world == 1) {
+    (void)winner;
+    (void)key_base;
+    return mspipe_memory_writeback(st, commit_version, nodes, num_unique, max_n, new_mem, new_ts, new_mail, stream);
+  }
+  if (!st->nccl_comm) return fail(MSPIPE_EUNSUPPORTED, "memory_writeback_keyed: in-process rank: use the mspipe_shard_* phases");
+  mspipe_status rc = mspipe_shard_commit_pack(st, commit_version, nodes, winner, num_unique, max_n, key_base, new_mem,
+                                              new_ts, new_mail, stream);
+  if (rc == MSPIPE_OK) rc = mspipe_shard_exchange(st, MSPIPE_XCHG_COMMIT, stream);
+  if (rc == MSPIPE_OK) rc = mspipe_shard_commit_merge(st, commit_version, stream);
+  return rc;
+}
+
+static mspipe_status shard_ok(const mspipe_memory* st, const char* what) {
+  if (!st) return fail(MSPIPE_EINVAL, "%s: NULL handle", what);
+  if (st->world < 2) return fail(MSPIPE_EINVAL, "%s: handle has world == 1", what);
+  return MSPIPE_OK;
+}
+
+mspipe_status mspipe_shard_fetch_plan(mspipe_memory* st, int64_t iteration, const int32_t* ids, int64_t n,
+                                      int32_t with_mail, void* stream) {
+  mspipe_status rc = shard_ok(st, "shard_fetch_plan");
+  if (rc != MSPIPE_OK) return rc;
+  if (iteration < 1 || n < 0 || (n > 0 && !ids)) return fail(MSPIPE_EINVAL, "shard_fetch_plan: iteration=%lld n=%lld", (long long)iteration, (long long)n);
+  if (st->committed < iteration - 1 - st->k || st->committed > iteration - 1)
+    return fail(MSPIPE_ESTALE, "shard_fetch_plan: iteration %lld with committed=%lld violates k=%d",
+                (long long)iteration, (long long)st->committed, st->k);
+  st->sh_with_mail = with_mail ? 1 : 0;
+  shard_fetch_plan(st, ids, n, (cudaStream_t)stream);
+  return after_launch("shard_fetch_plan");
+}
+
+mspipe_status mspipe_shard_fetch_serve(mspipe_memory* st, void* stream) {
+  mspipe_status rc = shard_ok(st, "shard_fetch_serve");
+  if (rc != MSPIPE_OK) return rc;
+  shard_fetch_serve(st, st->sh_with_mail != 0, (cudaStream_t)stream);
+  return after_launch("shard_fetch_serve");
+}
+
+mspipe_status mspipe_shard_fetch_finish(mspipe_memory* st, const int32_t* ids, int64_t n, float* out_mem,
+                                        double* out_mem_ts, float* out_mail, double* out_mail_ts,
+                                        int64_t* out_version, void* stream) {
+  mspipe_status rc = shard_ok(st, "shard_fetch_finish");
+  if (rc != MSPIPE_OK) return rc;
+  if (n > 0 && ((out_mail != nullptr) != (st->sh_with_mail != 0) || (out_mail == nullptr) != (out_mail_ts == nullptr)))
+    return fail(MSPIPE_EINVAL, "shard_fetch_finish: mail outputs must match the plan's with_mail");
+  if (n > 0 && (!ids || !out_mem || !out_mem_ts)) return fail(MSPIPE_EINVAL, "shard_fetch_finish: null ids/outputs");
+  if (n > 0) shard_fetch_finish(st, ids, n, out_mem, out_mem_ts, out_mail, out_mail_ts, (cudaStream_t)stream);
+  if (out_version) *out_version = st->committed;
+  return after_launch("shard_fetch_finish");
+}
+
+mspipe_status mspipe_shard_commit_pack(mspipe_memory* st, int64_t commit_version, const int32_t* nodes,
+                                       const int32_t* winner, const int32_t* num_unique, int64_t max_n,
+                                       int64_t key_base, const float* new_mem, const double* new_ts,
+                                       const float* new_mail, void* stream) {
+  mspipe_status rc = shard_ok(st, "shard_commit_pack");
+  if (rc != MSPIPE_OK) return rc;
+  if (commit_version != st->committed + 1)
+    return fail(MSPIPE_EORDER, "shard_commit_pack: commit_version=%lld but committed=%lld", (long long)commit_version, (long long)st->committed);
+  if (max_n < 0 || max_n > st->num_nodes || key_base < 0)
+    return fail(MSPIPE_EINVAL, "shard_commit_pack: max_n=%lld key_base=%lld", (long long)max_n, (long long)key_base);
+  if (max_n > 0 && (!nodes || !winner || !num_unique || !new_mem || !new_ts || !new_mail))
+    return fail(MSPIPE_EINVAL, "shard_commit_pack: null input");
+  shard_commit_pack(st, nodes, winner, num_unique, max_n, key_base, new_mem, new_ts, new_mail, (cudaStream_t)stream);
+  return after_launch("shard_commit_pack");
+}
+
+mspipe_status mspipe_shard_commit_merge(mspipe_memory* st, int64_t commit_version, void* stream) {
+  mspipe_status rc = shard_ok(st, "shard_commit_merge");
+  if (rc != MSPIPE_OK) return rc;
+  if (commit_version != st->committed + 1)
+    return fail(MSPIPE_EORDER, "shard_commit_merge: commit_version=%lld but committed=%lld", (long long)commit_version, (long long)st->committed);
+  shard_commit_merge(st, (cudaStream_t)stream);
+  rc = after_launch("shard_commit_merge");
+  if (rc == MSPIPE_OK) st->committed = commit_version;
+  return rc;
+}
+
+static void xchg_bufs(mspipe_memory* st, int32_t kind, void** send, void** recv, size_t* chunk) {
+  if (kind == MSPIPE_XCHG_FETCH_IDS) {
+    *send = st->sh_send_ids;
+    *recv = st->sh_recv_ids;
+    *chunk = sizeof(int32_t) * (size_t)st->sh_cap;
+  } else if (kind == MSPIPE_XCHG_FETCH_ROWS) {
+    *send = st->sh_fsend;
+    *recv = st->sh_frecv;
+    *chunk = (size_t)shard_fetch_rec_bytes(st, st->sh_with_mail != 0) * (size_t)st->sh_cap;
+  } else {
+    *send = st->sh_csend;
+    *recv = st->sh_crecv;
+    *chunk = (size_t)shard_commit_rec_bytes(st) * (size_t)st->sh_capw;
+  }
+}
+
+mspipe_status mspipe_shard_exchange(mspipe_memory* st, int32_t kind, void* stream) {
+  mspipe_status rc = shard_ok(st, "shard_exchange");
+  if (rc != MSPIPE_OK) return rc;
+  if (kind < 0 || kind > 2) return fail(MSPIPE_EINVAL, "shard_exchange: kind %d", kind);
+  if (!st->nccl_comm) return fail(MSPIPE_EUNSUPPORTED, "shard_exchange: in-process rank: use mspipe_shard_loopback");
+  void *send, *recv;
+  size_t chunk;
+  xchg_bufs(st, kind, &send, &recv, &chunk);
+  return nccl_alltoall(st, send, recv, chunk, (cudaStream_t)stream);
+}
+
+mspipe_status mspipe_shard_loopback(mspipe_memory* const* ranks, int32_t world, int32_t kind, void* stream) {
+  if (!ranks || world < 2 || kind < 0 || kind > 2) return fail(MSPIPE_EINVAL, "shard_loopback: world=%d kind=%d", world, kind);
+  for (int32_t r = 0; r < world; ++r)
+    if (!ranks[r] || ranks[r]->world != world || ranks[r]->rank != r)
+      return fail(MSPIPE_EINVAL, "shard_loopback: ranks[%d] is not rank %d of a world of %d", r, r, world);
+  cudaStream_t s = (cudaStream_t)stream;
+  for (int32_t r = 0; r < world; ++r) {
+    void *send, *recv_unused;
+    size_t chunk;
+    xchg_bufs(ranks[r], kind, &send, &recv_unused, &chunk);
+    for (int32_t p = 0; p < world; ++p) {  // block p of r's send buffer -> block r of p's receive buffer
+      void *send_p, *recv_p;
+      size_t chunk_p;
+      xchg_bufs(ranks[p], kind, &send_p, &recv_p, &chunk_p);
+      cudaError_t e = cudaMemcpyAsync((char*)recv_p + (size_t)r * chunk, (const char*)send + (size_t)p * chunk, chunk,
+                                      cudaMemcpyDeviceToDevice, s);
+      if (e != cudaSuccess) return cuda_status(e, "shard_loopback");
+    }
+  }
+  return MSPIPE_OK;
 }
 
 mspipe_status mspipe_util_event_record(void* event, void* stream) {

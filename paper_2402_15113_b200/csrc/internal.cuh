@@ -189,6 +189,27 @@ cudaError_t launch_prep(const Tcsr& g, const int32_t* src, const int32_t* dst, c
 
 }  // namespace mspipe
 
+struct mspipe_memory;
+namespace mspipe {
+// shard.cu
+void shard_fetch_plan(mspipe_memory* st, const int32_t* ids, int64_t n, cudaStream_t s);
+void shard_fetch_serve(mspipe_memory* st, bool with_mail, cudaStream_t s);
+void shard_fetch_finish(mspipe_memory* st, const int32_t* ids, int64_t n, float* out_mem, double* out_mem_ts,
+                        float* out_mail, double* out_mail_ts, cudaStream_t s);
+void shard_commit_pack(mspipe_memory* st, const int32_t* nodes, const int32_t* winner, const int32_t* num,
+                       int64_t max_n, int64_t key_base, const float* new_mem, const double* new_ts,
+                       const float* new_mail, cudaStream_t s);
+void shard_commit_merge(mspipe_memory* st, cudaStream_t s);
+int64_t shard_fetch_rec_bytes(const mspipe_memory* st, bool with_mail);
+int64_t shard_commit_rec_bytes(const mspipe_memory* st);
+// nccl_xchg.cu
+mspipe_status nccl_comm_init(mspipe_memory* st, const void* unique_id);
+void nccl_comm_destroy(mspipe_memory* st);
+mspipe_status nccl_alltoall(mspipe_memory* st, const void* send, void* recv, size_t chunk, cudaStream_t s);
+int32_t nccl_unique_id_bytes();
+mspipe_status nccl_get_unique_id(void* out);
+}  // namespace mspipe
+
 struct mspipe_memory {
   int64_t num_nodes;
   int32_t mem_dim, edge_dim, mail_dim, k;
@@ -201,6 +222,22 @@ struct mspipe_memory {
   int64_t committed;
   int32_t* scratch;  // [num_nodes] int32, -1 between calls (self-cleaning)
   int device;
+  // ---- world > 1 (shard.cu) ----
+  int64_t local_rows;       // rows of this rank's shard: nodes v with v % world == rank
+  int64_t sh_cap;           // max rows any shard serves = ceil(num_nodes / world)
+  int64_t sh_capw;          // commit records per peer
+  uint8_t* sh_needed;       // [num_nodes] request marks (cleared by the plan)
+  int32_t* sh_slot_of;      // [num_nodes] slot of id v in its owner's request list
+  int32_t* sh_send_ids;     // [world, sh_cap]
+  int32_t* sh_recv_ids;     // [world, sh_cap]
+  void* sh_fsend;           // fetch replies [world, sh_cap] records
+  void* sh_frecv;
+  void* sh_csend;           // commit records [world, sh_capw]
+  void* sh_crecv;
+  int32_t* sh_dest;         // [num_nodes] record slot of each local winner
+  unsigned long long* sh_keytab;  // [local_rows] LWW key of the committed row
+  int32_t sh_with_mail;     // the in-flight fetch carries mail rows
+  void* nccl_comm;          // ncclComm_t (NULL: in-process loopback transport)
 };
 
 struct mspipe_gru {

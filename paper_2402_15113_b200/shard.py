@@ -1,0 +1,206 @@
+"""Row E driver: the node-memory stage with memory sharded by node id.
+
+Global iteration i covers G·B consecutive events; rank g takes the local batch
+[(i-1)GB + gB, (i-1)GB + (g+1)B) ("each GPU worker retrieves a local batch",
+P:L817).  Each rank samples and deduplicates its local batch against the
+replicated T-CSR, fetches the snapshot rows it needs from their owners
+(v mod G), runs the GRU for its local winners, and sends keyed write-back
+records to the owners, which keep the largest key per node: the result equals
+the single-GPU stage at batch G·B (pin P10, tests/test_gpu_shard.py).
+
+Two transports: one process per GPU over NCCL (the library-owned communicator,
+``ShardRank`` with an ``nccl_id``), or G in-process ranks moved by
+``mspipe_shard_loopback`` (``LoopbackShards``: validation of the whole
+protocol on one GPU).
+"""
+from __future__ import annotations
+
+import torch
+
+from . import _C
+from .stage import StageConfig, _Slot, schedule_ops
+
+
+def local_range(i, rank, world, batch, num_events):
+    """Events of rank's local batch in global iteration i (1-based): [j0, j1)."""
+    j0 = (i - 1) * world * batch + rank * batch
+    return min(j0, num_events), min(j0 + batch, num_events)
+
+
+def key_base(i, rank, world, batch):
+    """LWW key of local pair p is key_base + p = 2 * (global event index) + role."""
+    return 2 * ((i - 1) * world * batch + rank * batch)
+
+
+def num_global_batches(num_events, world, batch):
+    return -(-num_events // (world * batch))
+
+
+class ShardRank:
+    """One rank's handles, slots and ops (ordinary or NCCL-collective calls)."""
+
+    def __init__(self, cfg: StageConfig, params: dict, tcsr: _C.TcsrHandle, device, rank: int, world: int,
+                 nccl_id: bytes | None = None):
+        if cfg.mitigation:
+            raise NotImplementedError("MSPipe-S mitigation with sharded memory is not in this build")
+        self.cfg, self.rank, self.world = cfg, rank, world
+        self.device = torch.device(device)
+        self.tcsr = tcsr
+        self.memory = _C.MemoryHandle(cfg.num_nodes, cfg.mem_dim, cfg.edge_dim, cfg.k, self.device, rank, world,
+                                      nccl_id)
+        self.gru = _C.GruHandle(cfg.mem_dim, cfg.edge_dim, cfg.time_dim, params, self.device, cfg.precision,
+                                max_events=cfg.batch)
+        self.slots = [_Slot(cfg, self.memory.mail_stride, self.device, False) for _ in range(cfg.k + 1)]
+        self.upd = _C.alloc_update(cfg.batch, cfg.mem_dim, self.memory.mail_stride, self.device)
+        self.versions = {}
+
+    def bind_resident(self, src, dst, ts, neg, ef):
+        self.E = src.numel()
+        self.res = dict(src=src, dst=dst, ts=ts, neg=neg, ef=ef)
+
+    def _slot(self, i):
+        return self.slots[(i - 1) % (self.cfg.k + 1)]
+
+    def inputs(self, i):
+        j0, j1 = local_range(i, self.rank, self.world, self.cfg.batch, self.E)
+        return {k: v[j0:j1] for k, v in self.res.items()}
+
+    # -- prep -------------------------------------------------------------
+    def prep_local(self, i):
+        """A1 + A2 on the local batch (no state access)."""
+        sl, x = self._slot(i), self.inputs(i)
+        n = x["src"].numel()
+        samp = {k: v[: 3 * n] for k, v in sl.samp.items()}
+        _C.sample_batch(self.tcsr, x["src"], x["dst"], x["neg"], x["ts"], self.cfg.fanout, samp)
+        _C.memory_dedup(self.memory, x["src"], x["dst"], sl.dd)
+        self._ids = (i, samp["sub"].reshape(-1))
+
+    def _fetch_out(self, i):
+        sl = self._slot(i)
+        ids = self._ids[1]
+        m = ids.numel()
+        return ids, sl.mem[:m], sl.mem_ts[:m], (sl.mail[:m] if sl.mail is not None else None), \
+            (sl.mail_ts[:m] if sl.mail_ts is not None else None)
+
+    def fetch_plan(self, i):
+        ids, _, _, mail, _ = self._fetch_out(i)
+        _C.shard_fetch_plan(self.memory, i, ids, with_mail=mail is not None)
+
+    def fetch_serve(self):
+        _C.shard_fetch_serve(self.memory)
+
+    def fetch_finish(self, i):
+        ids, mem, mem_ts, mail, mail_ts = self._fetch_out(i)
+        self.versions[i] = _C.shard_fetch_finish(self.memory, ids, mem, mem_ts, mail, mail_ts)
+
+    def fetch_collective(self, i):
+        """NCCL: plan, all-to-all, serve, all-to-all, finish inside mspipe_memory_fetch."""
+        ids, mem, mem_ts, mail, mail_ts = self._fetch_out(i)
+        self.versions[i] = _C.memory_fetch(self.memory, i, ids, mem, mem_ts, mail, mail_ts)
+
+    # -- commit -----------------------------------------------------------
+    def _upd(self, i):
+        n = self.inputs(i)["src"].numel()
+        sl = self._slot(i)
+        upd = {k: v[: 2 * n] for k, v in self.upd.items() if k not in ("nodes", "winner", "num")}
+        upd.update(nodes=sl.dd["nodes"][: 2 * n], winner=sl.dd["winner"][: 2 * n], num=sl.dd["num"])
+        return upd
+
+    def update(self, i):
+        """A5 + A6 for the local winners (rank-local)."""
+        sl, x = self._slot(i), self.inputs(i)
+        _C.memory_update(self.memory, self.gru, x["src"], x["dst"], x["ts"], x["ef"], sl.mem, sl.mem_ts,
+                         self.cfg.fanout + 1, self._upd(i))
+
+    def commit_pack(self, i):
+        _C.shard_commit_pack(self.memory, i, self._upd(i), key_base(i, self.rank, self.world, self.cfg.batch))
+
+    def commit_merge(self, i):
+        _C.shard_commit_merge(self.memory, i)
+
+    def writeback_collective(self, i):
+        _C.memory_writeback_keyed(self.memory, i, self._upd(i), key_base(i, self.rank, self.world, self.cfg.batch))
+
+    # -- NCCL driver ---------------------------------------------------------
+    def prep(self, i):
+        self.prep_local(i)
+        self.fetch_collective(i)
+
+    def commit(self, i):
+        self.update(i)
+        self.writeback_collective(i)
+
+    @property
+    def num_batches(self):
+        return num_global_batches(self.E, self.world, self.cfg.batch)
+
+    def step_ops(self, nb=None):
+        nb = self.num_batches if nb is None else nb
+        steps, cur = [], []
+        for op in schedule_ops(nb, self.cfg.k, self.cfg.schedule):
+            cur.append(op)
+            if op[0] == "commit":
+                steps.append(cur)
+                cur = []
+        return steps
+
+    def run_ops(self, ops):
+        for op, i in ops:
+            (self.prep if op == "prep" else self.commit)(i)
+
+    def run(self, nb=None):
+        for ops in self.step_ops(nb):
+            self.run_ops(ops)
+
+
+class LoopbackShards:
+    """G in-process ranks on one device, phases interleaved, buffers moved by
+    mspipe_shard_loopback: the whole sharded protocol without NCCL."""
+
+    def __init__(self, cfg: StageConfig, params: dict, tcsr: _C.TcsrHandle, device, world: int):
+        self.cfg, self.world = cfg, world
+        self.ranks = [ShardRank(cfg, params, tcsr, device, r, world, None) for r in range(world)]
+
+    def bind_resident(self, src, dst, ts, neg, ef):
+        for r in self.ranks:
+            r.bind_resident(src, dst, ts, neg, ef)
+        self.E = src.numel()
+
+    def _xchg(self, kind):
+        _C.shard_loopback([r.memory for r in self.ranks], kind)
+
+    def prep(self, i):
+        for r in self.ranks:
+            r.prep_local(i)
+            r.fetch_plan(i)
+        self._xchg(_C.XCHG_FETCH_IDS)
+        for r in self.ranks:
+            r.fetch_serve()
+        self._xchg(_C.XCHG_FETCH_ROWS)
+        for r in self.ranks:
+            r.fetch_finish(i)
+
+    def commit(self, i):
+        for r in self.ranks:
+            r.update(i)
+            r.commit_pack(i)
+        self._xchg(_C.XCHG_COMMIT)
+        for r in self.ranks:
+            r.commit_merge(i)
+
+    def run(self, nb=None):
+        nb = num_global_batches(self.E, self.world, self.cfg.batch) if nb is None else nb
+        for op, i in schedule_ops(nb, self.cfg.k, self.cfg.schedule):
+            (self.prep if op == "prep" else self.commit)(i)
+
+    def gather(self):
+        """Global tables assembled from the shards (row v lives at rank v % G, row v // G)."""
+        N, G = self.cfg.num_nodes, self.world
+        out = {}
+        for key in ("mem", "mem_ts", "mail", "mail_ts"):
+            parts = [getattr(r.memory, key) for r in self.ranks]
+            full = torch.empty((N,) + tuple(parts[0].shape[1:]), dtype=parts[0].dtype, device=parts[0].device)
+            for g, p in enumerate(parts):
+                full[g::G] = p
+            out[key] = full
+        return out

@@ -1,0 +1,86 @@
+"""Row E on one GPU: G in-process ranks (mspipe_shard_loopback transport), memory
+sharded by node id, each rank on its local batch of every global batch of
+G·B events.  Pin P10: the gathered state equals the oracle at batch G·B
+(timestamps bit-exact, values within the fp32 tolerance)."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from paper_2402_15113_b200 import LoopbackShards, StageConfig, _C, build_tcsr
+from synth import make_workload
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def dev():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    d = torch.device("cuda:0")
+    torch.cuda.set_device(d)
+    return d
+
+
+@pytest.mark.parametrize("name,E,G,k,precision", [
+    ("tiny", None, 2, 0, _C.FP32_3XTF32),
+    ("tiny", None, 4, 1, _C.FP32_3XTF32),
+    ("tiny", 6000, 3, 2, _C.FP32_SIMT),
+    ("lastfm", 40_000, 2, 1, _C.FP32_3XTF32),   # hot nodes: many cross-rank LWW conflicts
+    ("wiki", 50_000, 8, 1, _C.FP32_3XTF32),
+])
+def test_sharded_stream_equals_oracle_at_global_batch(dev, name, E, G, k, precision):
+    w = make_workload(name, seed=1, num_events=E)
+    cfg = w["cfg"]
+    B = cfg.batch // G if name == "wiki" else cfg.batch  # wiki: same global batch as 1 GPU
+    sc = StageConfig(cfg.num_nodes, cfg.mem_dim, cfg.edge_dim, cfg.time_dim, cfg.fanout, B, k,
+                     precision=precision, fetch_mail=True)
+    g = build_tcsr(cfg.num_nodes, w["src"], w["dst"], w["ts"], dev)
+    sh = LoopbackShards(sc, w["params"], g, dev, G)
+    t = {kk: torch.from_numpy(w[kk]).to(dev) for kk in ("src", "dst", "ts", "neg", "ef")}
+    sh.bind_resident(t["src"], t["dst"], t["ts"], t["neg"], t["ef"])
+    sh.run()
+    torch.cuda.synchronize()
+    _C.check()
+    got = {kk: v.cpu().numpy() for kk, v in sh.gather().items()}
+    ref, vers = oracle.run_stream(cfg.num_nodes, w["src"], w["dst"], w["ts"], w["ef"], w["params"], G * B, k)
+    for r in sh.ranks:
+        assert [r.versions[i] for i in range(1, len(vers) + 1)] == vers.tolist()
+    assert np.array_equal(got["mem_ts"], ref["mem_ts"])
+    assert np.array_equal(got["mail_ts"], ref["mail_ts"])
+    gm, om = got["mem"].astype(np.float64), ref["mem"].astype(np.float64)
+    rel = np.linalg.norm(gm - om, axis=1) / np.maximum(np.linalg.norm(om, axis=1), 1e-3)
+    print(f"{name} G={G} k={k}: sharded vs oracle(batch {G * B}) row-rel max {rel.max():.3g}")
+    assert rel.max() <= 1e-4
+    Dm = cfg.mail_dim
+    assert np.allclose(got["mail"][:, :Dm], ref["mail"], rtol=1e-4, atol=1e-5)
+
+
+def test_sharded_fetch_rows_bit_exact(dev):
+    """A3 through the exchange: every fetched row is the owner's row, bitwise."""
+    w = make_workload("tiny", seed=2, num_events=4000)
+    cfg = w["cfg"]
+    G = 4
+    sc = StageConfig(cfg.num_nodes, cfg.mem_dim, cfg.edge_dim, cfg.time_dim, cfg.fanout, 100, 0, fetch_mail=True)
+    g = build_tcsr(cfg.num_nodes, w["src"], w["dst"], w["ts"], dev)
+    sh = LoopbackShards(sc, w["params"], g, dev, G)
+    t = {kk: torch.from_numpy(w[kk]).to(dev) for kk in ("src", "dst", "ts", "neg", "ef")}
+    sh.bind_resident(t["src"], t["dst"], t["ts"], t["neg"], t["ef"])
+    sh.run(nb=5)  # some committed state
+    rng = torch.Generator().manual_seed(0)
+    for r in sh.ranks:  # random state so that every row differs
+        r.memory.mem.copy_(torch.rand(r.memory.mem.shape, generator=rng).to(dev))
+        r.memory.mem_ts.copy_(torch.rand(r.memory.mem_ts.shape, generator=rng, dtype=torch.float64).to(dev))
+        r.memory.mail.copy_(torch.rand(r.memory.mail.shape, generator=rng).to(dev))
+    full = {kk: v.cpu().numpy() for kk, v in sh.gather().items()}
+    sh.prep(6)
+    torch.cuda.synchronize()
+    for r in sh.ranks:
+        sl = r._slot(6)
+        ids = r._ids[1].cpu().numpy()
+        m = len(ids)
+        valid = ids >= 0
+        mem = sl.mem[:m].cpu().numpy()
+        assert np.array_equal(mem[valid], full["mem"][ids[valid]]) and (mem[~valid] == 0).all()
+        assert np.array_equal(sl.mem_ts[:m].cpu().numpy()[valid], full["mem_ts"][ids[valid]])
+        assert np.array_equal(sl.mail[:m].cpu().numpy()[valid], full["mail"][ids[valid]])

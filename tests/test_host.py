@@ -50,10 +50,32 @@ def test_host_status_paths_without_gpu():
     rc = lib.mspipe_memory_create(ctypes.byref(h), 10, 6, 4, 0, None, None, None, None, 16, 0, 1, None)
     assert rc == _C.EINVAL and "mem_dim" in _C.last_error()
     rc = lib.mspipe_memory_create(ctypes.byref(h), 10, 8, 4, 0, ctypes.c_void_p(16), ctypes.c_void_p(16),
-                                  ctypes.c_void_p(16), ctypes.c_void_p(16), 20, 0, 2, None)
-    assert rc == _C.EUNSUPPORTED
+                                  ctypes.c_void_p(16), ctypes.c_void_p(16), 20, 2, 2, None)
+    assert rc == _C.EINVAL and "rank" in _C.last_error()  # rank outside [0, world)
     rc = lib.mspipe_sample_recent(None, None, None, 1, 10, None, None, None, None, None, None, None)
     assert rc == _C.EINVAL
+    rc = lib.mspipe_shard_loopback(None, 2, 0, None)
+    assert rc == _C.EINVAL
+    rc = lib.mspipe_shard_exchange(None, 0, None)
+    assert rc == _C.EINVAL
+
+
+def test_shard_partition_tiles_the_global_batch():
+    """Row E host logic: the G local batches of iteration i tile [(i-1)GB, iGB) and
+    key_base + local pair index = global pair index of the single-GPU batch G·B."""
+    from paper_2402_15113_b200.shard import key_base, local_range, num_global_batches
+    for G in (1, 2, 3, 8):
+        for E, B in ((10_000, 200), (1234, 50), (7, 3)):
+            nb = num_global_batches(E, G, B)
+            covered = []
+            for i in range(1, nb + 1):
+                for g in range(G):
+                    j0, j1 = local_range(i, g, G, B, E)
+                    covered.extend(range(j0, j1))
+                    for a in range(j1 - j0):
+                        for role in (0, 1):
+                            assert key_base(i, g, G, B) + 2 * a + role == 2 * (j0 + a) + role
+            assert covered == list(range(E))
 
 
 @pytest.mark.parametrize("schedule", ["exact", "grouped"])
