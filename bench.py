@@ -155,12 +155,23 @@ def run_mspipe(args):
                      schedule=args.schedule, mitigation=mit, fetch_mail=args.fetch_mail,
                      precision=_C.FP32_3XTF32 if args.gru == "tc" else _C.FP32_SIMT)
     g = build_tcsr(cfg.num_nodes, w["src"], w["dst"], w["ts"], dev)
-    nb = -(-len(w["src"]) // cfg.batch)
-    U_host = _unique_counts(w["src"], w["dst"], cfg.batch)
+    # N > 1: node-id-sharded memory over NCCL (row E); MSPIPE_BENCH_REPLICAS=1 runs
+    # N independent single-GPU replicas instead (ablation)
+    sharded = ws > 1 and os.environ.get("MSPIPE_BENCH_REPLICAS", "0") != "1"
+    G = ws if sharded else 1
+    E = len(w["src"])
+    nb = -(-E // (G * cfg.batch))
+    U_host = _unique_counts(w["src"], w["dst"], G * cfg.batch)
     flush = torch.empty(FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
 
     def make_stage(staged):
-        st = MemoryStage(sc, w["params"], g, dev)
+        if sharded:
+            # every stage owns its communicator: a fresh unique id each time (collective)
+            from paper_2402_15113_b200 import ShardRank
+            from paper_2402_15113_b200.dist import share_nccl_id
+            st = ShardRank(sc, w["params"], g, dev, rank, ws, share_nccl_id(rank))
+        else:
+            st = MemoryStage(sc, w["params"], g, dev)
         if staged:
             st.bind_host(w["src"], w["dst"], w["ts"], w["neg"], w["ef"])
         else:
@@ -250,8 +261,9 @@ def run_mspipe(args):
         tot_ms = float(tt.item())
         dist.barrier()
     timed_batches = [(W + q) % nb for q in range(K)]
-    events = sum(min(cfg.batch, len(w["src"]) - b * cfg.batch) for b in timed_batches)
-    value = ws * events / (tot_ms / 1e3)
+    # events of all ranks in the timed global batches (replicas: every rank its own copy)
+    events = sum(min(G * cfg.batch, E - b * G * cfg.batch) for b in timed_batches) * (ws if not sharded else 1)
+    value = events / (tot_ms / 1e3)
     # ---- roofline of the dominant op ---------------------------------------
     peaks = _peaks()
     mean_U = float(np.mean(U_host[timed_batches]))
@@ -295,8 +307,11 @@ def run_mspipe(args):
                       "mitigation": bool(mit), "fetch_mail": args.fetch_mail, "gru": "fp32-3xtf32-tcgen05" if args.gru == "tc" else "fp32-simt",
                       "l2": ("flushed (256 MiB write) between timed steps, outside the timed events"
                              if args.l2 == "flush" else "warm: steps back to back, state tables L2-resident"),
-                      "parallelism": "single" if ws == 1 else f"replicas{ws}"},
-           "roofline": roof, "gpu_launches": _launches(st.step_ops(), timed_batches, bool(mit), st.fused), "clocks": clocks}
+                      "parallelism": ("single" if ws == 1 else
+                                      f"shard{ws}: node-id-sharded memory, NCCL all-to-all fetch + write-back, "
+                                      f"global batch {G * cfg.batch}" if sharded else f"replicas{ws}")},
+           "roofline": roof, "gpu_launches": _launches(st.step_ops(), timed_batches, bool(mit),
+                                                       getattr(st, "fused", False), sharded), "clocks": clocks}
     if args.profile:
         if rank == 0:
             print(json.dumps(out))
@@ -313,7 +328,7 @@ def run_mspipe(args):
         tt = torch.tensor([tot2], device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         tot2 = float(tt.item())
-    out["e2e"] = {"value": ws * events / (tot2 / 1e3), "unit": UNIT,
+    out["e2e"] = {"value": events / (tot2 / 1e3), "unit": UNIT,
                   "h2d_bytes_per_step": st2.h2d_bytes_per_batch(), "d2h_bytes_per_step": st2.d2h_bytes_per_batch(),
                   "ms_per_step": tot2 / K}
     del graphs2
@@ -326,10 +341,15 @@ def run_mspipe(args):
         dist.destroy_process_group()
 
 
-def _launches(steps, timed_batches, mit, fused):
+def _launches(steps, timed_batches, mit, fused, sharded=False):
     """Kernels of this library per timed step.  fused: prep = k_prep + k_build_x
     (+ k_mitigate), commit = k_gru_tc with the write-back in its epilogue; otherwise prep = sampler +
-    dedup + gather (+ mitigation), commit = build + GEMM (or SIMT GRU) + write-back."""
+    dedup + gather (+ mitigation), commit = build + GEMM (or SIMT GRU) + write-back.  Sharded:
+    prep = sampler + dedup + mark + plan + serve + finish, commit = build + GEMM + clear + pack-plan
+    + pack + merge-key + merge-apply (NCCL kernels not counted)."""
+    if sharded:
+        per = {"prep": 6, "commit": 7}
+        return int(sum(per[op] for t in timed_batches for op, _ in steps[t]))
     per = {"prep": (2 if fused else 3) + (1 if mit else 0), "commit": 1 if fused else 3}
     return int(sum(per[op] for t in timed_batches for op, _ in steps[t]))
 

@@ -18,7 +18,7 @@ from __future__ import annotations
 import torch
 
 from . import _C
-from .stage import StageConfig, _Slot, schedule_ops
+from .stage import StageConfig, _Slot, _TimedOps, schedule_ops
 
 
 def local_range(i, rank, world, batch, num_events):
@@ -36,7 +36,7 @@ def num_global_batches(num_events, world, batch):
     return -(-num_events // (world * batch))
 
 
-class ShardRank:
+class ShardRank(_TimedOps):
     """One rank's handles, slots and ops (ordinary or NCCL-collective calls)."""
 
     def __init__(self, cfg: StageConfig, params: dict, tcsr: _C.TcsrHandle, device, rank: int, world: int,
@@ -53,22 +53,50 @@ class ShardRank:
         self.slots = [_Slot(cfg, self.memory.mail_stride, self.device, False) for _ in range(cfg.k + 1)]
         self.upd = _C.alloc_update(cfg.batch, cfg.mem_dim, self.memory.mail_stride, self.device)
         self.versions = {}
+        self.staged = False
 
     def bind_resident(self, src, dst, ts, neg, ef):
         self.E = src.numel()
         self.res = dict(src=src, dst=dst, ts=ts, neg=neg, ef=ef)
+
+    def bind_host(self, src, dst, ts, neg, ef):
+        """e2e: pinned host stream; each prep copies its local batch H2D, each commit
+        reads its h' rows back."""
+        self.E = int(src.shape[0])
+        self.host = {k: torch.as_tensor(v).pin_memory() for k, v in
+                     dict(src=src, dst=dst, ts=ts, neg=neg, ef=ef).items()}
+        self.staged = True
+        self.slots = [_Slot(self.cfg, self.memory.mail_stride, self.device, True) for _ in range(self.cfg.k + 1)]
+        B = self.cfg.batch
+        self.out_host = dict(num=torch.empty(1, dtype=torch.int32).pin_memory(),
+                             nodes=torch.empty(2 * B, dtype=torch.int32).pin_memory(),
+                             mem=torch.empty((2 * B, self.cfg.mem_dim), dtype=torch.float32).pin_memory())
+
+    def h2d_bytes_per_batch(self):
+        return self.cfg.batch * (4 + 4 + 4 + 8 + 4 * self.cfg.edge_dim)
+
+    def d2h_bytes_per_batch(self):
+        B = self.cfg.batch
+        return 4 + 2 * B * 4 + 2 * B * self.cfg.mem_dim * 4
 
     def _slot(self, i):
         return self.slots[(i - 1) % (self.cfg.k + 1)]
 
     def inputs(self, i):
         j0, j1 = local_range(i, self.rank, self.world, self.cfg.batch, self.E)
-        return {k: v[j0:j1] for k, v in self.res.items()}
+        if not self.staged:
+            return {k: v[j0:j1] for k, v in self.res.items()}
+        return {k: v[: j1 - j0] for k, v in self._slot(i).inp.items()}
 
     # -- prep -------------------------------------------------------------
     def prep_local(self, i):
         """A1 + A2 on the local batch (no state access)."""
-        sl, x = self._slot(i), self.inputs(i)
+        sl = self._slot(i)
+        if self.staged:
+            j0, j1 = local_range(i, self.rank, self.world, self.cfg.batch, self.E)
+            for key in ("src", "dst", "neg", "ts", "ef"):
+                sl.inp[key][: j1 - j0].copy_(self.host[key][j0:j1], non_blocking=True)
+        x = self.inputs(i)
         n = x["src"].numel()
         samp = {k: v[: 3 * n] for k, v in sl.samp.items()}
         _C.sample_batch(self.tcsr, x["src"], x["dst"], x["neg"], x["ts"], self.cfg.fanout, samp)
@@ -123,12 +151,28 @@ class ShardRank:
 
     # -- NCCL driver ---------------------------------------------------------
     def prep(self, i):
+        self._ev("prep")
         self.prep_local(i)
         self.fetch_collective(i)
+        self._ev("prep_end")
 
     def commit(self, i):
+        self._ev("update")
         self.update(i)
+        self._ev("update_end")
+        self._ev("writeback")
         self.writeback_collective(i)
+        self._ev("writeback_end")
+        if self.staged:
+            self.copy_out(i)
+
+    def copy_out(self, i):
+        """e2e: D2H of this batch's result (unique count, winners' node ids, h')."""
+        upd = self._upd(i)
+        n2 = upd["nodes"].numel()
+        self.out_host["num"].copy_(upd["num"], non_blocking=True)
+        self.out_host["nodes"][:n2].copy_(upd["nodes"], non_blocking=True)
+        self.out_host["mem"][:n2].copy_(upd["mem"], non_blocking=True)
 
     @property
     def num_batches(self):
@@ -166,6 +210,22 @@ class LoopbackShards:
             r.bind_resident(src, dst, ts, neg, ef)
         self.E = src.numel()
 
+    def bind_host(self, src, dst, ts, neg, ef):
+        for r in self.ranks:
+            r.bind_host(src, dst, ts, neg, ef)
+        self.E = int(src.shape[0])
+
+    def step_ops(self, nb=None):
+        return self.ranks[0].step_ops(nb)
+
+    def run_ops(self, ops):
+        for op, i in ops:
+            (self.prep if op == "prep" else self.commit)(i)
+
+    def reset(self):
+        for r in self.ranks:
+            r.memory.reset()
+
     def _xchg(self, kind):
         _C.shard_loopback([r.memory for r in self.ranks], kind)
 
@@ -187,11 +247,12 @@ class LoopbackShards:
         self._xchg(_C.XCHG_COMMIT)
         for r in self.ranks:
             r.commit_merge(i)
+            if r.staged:
+                r.copy_out(i)
 
     def run(self, nb=None):
-        nb = num_global_batches(self.E, self.world, self.cfg.batch) if nb is None else nb
-        for op, i in schedule_ops(nb, self.cfg.k, self.cfg.schedule):
-            (self.prep if op == "prep" else self.commit)(i)
+        for ops in self.step_ops(nb):
+            self.run_ops(ops)
 
     def gather(self):
         """Global tables assembled from the shards (row v lives at rank v % G, row v // G)."""

@@ -105,7 +105,36 @@ class _Slot:
                             ef=torch.empty((B, cfg.edge_dim), dtype=torch.float32, device=device))
 
 
-class MemoryStage:
+class _TimedOps:
+    """Optional per-op CUDA timing events (also valid under graph capture)."""
+
+    timing = None
+
+    def reserve_timing_events(self, n):
+        """Materialise n timing events outside any stream capture (torch
+        creates the CUDA event lazily at its first record)."""
+        self._pool = []
+        for _ in range(n):
+            e = torch.cuda.Event(enable_timing=True)
+            e.record()
+            self._pool.append(e)
+        torch.cuda.synchronize()
+        self.timing = {}
+
+    def _ev(self, name):
+        if self.timing is None:
+            return None
+        if getattr(self, "_pool", None):
+            e = self._pool.pop()
+        else:
+            e = torch.cuda.Event(enable_timing=True)
+            e.record()  # materialise (not allowed under capture: reserve_timing_events first)
+        _C.event_record(e)
+        self.timing.setdefault(name, []).append(e)
+        return e
+
+
+class MemoryStage(_TimedOps):
     """Drives libmspipe over an event stream.  Inputs are either resident in
     HBM (``bind_resident``) or staged per batch from pinned host memory
     (``bind_host``: the H2D copy of the batch happens inside prep(i))."""
@@ -164,29 +193,6 @@ class MemoryStage:
     # -- ops ------------------------------------------------------------------
     def _slot(self, i):
         return self.slots[(i - 1) % (self.cfg.k + 1)]
-
-    def reserve_timing_events(self, n):
-        """Materialise n timing events outside any stream capture (torch
-        creates the CUDA event lazily at its first record)."""
-        self._pool = []
-        for _ in range(n):
-            e = torch.cuda.Event(enable_timing=True)
-            e.record()
-            self._pool.append(e)
-        torch.cuda.synchronize()
-        self.timing = {}
-
-    def _ev(self, name):
-        if self.timing is None:
-            return None
-        if getattr(self, "_pool", None):
-            e = self._pool.pop()
-        else:
-            e = torch.cuda.Event(enable_timing=True)
-            e.record()  # materialise (not allowed under capture: reserve_timing_events first)
-        _C.event_record(e)
-        self.timing.setdefault(name, []).append(e)
-        return e
 
     def prep(self, i):
         """A1 sampler, A2 dedup, A3 fetch (+A4 mitigation) of batch i into its slot."""
