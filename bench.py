@@ -46,14 +46,43 @@ def _peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons during the timed region."""
+    """SM clock + throttle reasons during the timed region: an NVML poll thread
+    (every ~2 ms, so even a 20 ms timed region has samples) plus the recipe's
+    nvidia-smi record (gpurun_out/clocks_<pid>.csv) running alongside."""
+
+    REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20, "sw_power_cap": 0x4}
 
     def __init__(self, index):
         self.index = index
         self.proc = None
+        self.samples = []
         self.path = os.path.join(ROOT, "gpurun_out", f"clocks_{os.getpid()}.csv")
 
+    def _nvml_handle(self):
+        import pynvml
+        import torch
+        pynvml.nvmlInit()
+        try:
+            p = torch.cuda.get_device_properties(self.index)
+            bus = f"{p.pci_domain_id:08x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x}.0"
+            return pynvml, pynvml.nvmlDeviceGetHandleByPciBusId(bus)
+        except Exception:
+            return pynvml, pynvml.nvmlDeviceGetHandleByIndex(self.index)
+
+    def _poll(self):
+        nv, h = self.nv, self.h
+        while True:
+            try:
+                self.samples.append((nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM),
+                                     nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM),
+                                     nv.nvmlDeviceGetCurrentClocksEventReasons(h)))
+            except Exception:
+                return
+            if self.stop.wait(0.002):
+                return
+
     def __enter__(self):
+        import threading
         try:
             os.makedirs(os.path.dirname(self.path), exist_ok=True)
             self.f = open(self.path, "w")
@@ -65,9 +94,20 @@ class ClockSampler:
                  "--format=csv,noheader,nounits", "-lms", "100"], stdout=self.f, stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
+        self.thread = None
+        try:
+            self.nv, self.h = self._nvml_handle()
+            self.stop = threading.Event()
+            self.thread = threading.Thread(target=self._poll, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.thread = None
         return self
 
     def __exit__(self, *a):
+        if self.thread is not None:
+            self.stop.set()
+            self.thread.join(timeout=2)
         if self.proc is not None:
             self.proc.terminate()
             try:
@@ -77,23 +117,23 @@ class ClockSampler:
             self.f.close()
 
     def summary(self):
-        if self.proc is None:
-            return None
-        rows = []
-        with open(self.path) as f:
-            for line in f:
-                parts = [x.strip() for x in line.split(",")]
-                if len(parts) >= 7:
-                    try:
-                        rows.append((float(parts[0]), float(parts[1]), parts[3:7]))
-                    except ValueError:
-                        pass
+        rows = [(float(c), float(m), {n for n, bit in self.REASONS.items() if r & bit}) for c, m, r in self.samples]
+        if self.proc is not None:
+            names = list(self.REASONS)
+            with open(self.path) as f:
+                for line in f:
+                    parts = [x.strip() for x in line.split(",")]
+                    if len(parts) >= 7:
+                        try:
+                            rows.append((float(parts[0]), float(parts[1]),
+                                         {names[i] for i, v in enumerate(parts[3:7]) if v.lower() == "active"}))
+                        except ValueError:
+                            pass
         if not rows:
             return None
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for _, _, r in rows for i, v in enumerate(r) if v.lower() == "active"})
         return {"sm_mhz": statistics.median(r[0] for r in rows), "sm_max_mhz": max(r[1] for r in rows),
-                "reasons": reasons, "samples": len(rows)}
+                "reasons": sorted(set().union(*(r[2] for r in rows))), "samples": len(rows),
+                "source": "NVML poll every 2 ms + nvidia-smi -lms 100 during the timed region"}
 
 
 def _dist():
@@ -185,14 +225,10 @@ def run_mspipe(args):
         if timing:
             st.reserve_timing_events(8 * sum(len(o) for o in st.step_ops()) + 16)
         graphs, marks = [], []
-        with torch.cuda.stream(s):
-            for ops in st.step_ops():
-                gr = torch.cuda.CUDAGraph()
-                before = {kk: len(v) for kk, v in (st.timing or {}).items()}
-                with torch.cuda.graph(gr, stream=s):
-                    st.run_ops(ops)
-                graphs.append(gr)
-                marks.append({kk: (before.get(kk, 0), len(v)) for kk, v in (st.timing or {}).items()})
+        for ops in st.step_ops():
+            before = {kk: len(v) for kk, v in (st.timing or {}).items()}
+            graphs.append(_C.StepGraph().capture(lambda: st.run_ops(ops), s))
+            marks.append({kk: (before.get(kk, 0), len(v)) for kk, v in (st.timing or {}).items()})
         st.memory.reset()
         return graphs, marks, s
 
@@ -213,7 +249,7 @@ def run_mspipe(args):
                 e0 = torch.cuda.Event(enable_timing=True)
                 e1 = torch.cuda.Event(enable_timing=True)
                 e0.record(s)
-                graphs[t].replay()
+                graphs[t].replay(s)
                 e1.record(s)
                 if n >= W:
                     pending.append((t, e0, e1))
@@ -277,14 +313,16 @@ def run_mspipe(args):
         # nominal ratio (B200_PROFILING.md); sustained bf16 figure (kernel timed inside a long step)
         peak_tc = peaks["bf16_tflops_sustained"] * (1.1 / 2.25) / 3.0
         ach = alg["update_flops"] / (op_mean[dom] / 1e3) / 1e12
-        roof = {"kernel": "k_gru_tc (+k_dedup) via mspipe_memory_update", "bound": "tensor", "achieved": ach,
+        kname = ("k_gru_tc via mspipe_gru_apply_commit (GEMM + gates + LWW commit epilogue)"
+                 if getattr(st, "fused", False) else "k_build_x + k_gru_tc via mspipe_memory_update")
+        roof = {"kernel": kname, "bound": "tensor", "achieved": ach,
                 "peak": peak_tc, "unit": "TFLOP/s", "frac": ach / peak_tc,
                 "peak_source": f"{peaks['source']} bf16 sustained x 1.1/2.25 (tf32) / 3 (3xTF32 passes)"}
     elif dom == "update":
         sm_clock = 1965.0
         peak_alu = 148 * FP32_FMA_LANES_PER_SM * 2 * sm_clock * 1e6 / 1e12
         ach = alg["update_flops"] / (op_mean[dom] / 1e3) / 1e12
-        roof = {"kernel": "k_gru_simt (+k_dedup) via mspipe_memory_update", "bound": "alu", "achieved": ach,
+        roof = {"kernel": "k_build_x + k_gru_simt via mspipe_memory_update", "bound": "alu", "achieved": ach,
                 "peak": peak_alu, "unit": "TFLOP/s", "frac": ach / peak_alu,
                 "peak_source": "148 SMs x 128 FP32 lanes x 2 x 1965 MHz (guide unit counts, max clock)"}
     else:

@@ -358,6 +358,21 @@ MSPIPE_API mspipe_status mspipe_shard_loopback(mspipe_memory* const* ranks, int3
  * measurement of the captured kernels. */
 MSPIPE_API mspipe_status mspipe_util_event_record(void* event, void* stream);
 
+/* Utility (step graphs): the stage of one step is captured once and replayed
+ * (the "CUDA graphs instead of a tracing compiler" of DESIGN.md §2).
+ *   mspipe_util_graph_begin(stream)            starts a thread-local capture on `stream`
+ *                                               (streams forked from it by event waits join it)
+ *   mspipe_util_graph_end(stream, &exec)       ends it and instantiates; *exec owned by the
+ *                                               caller, freed with mspipe_util_graph_destroy
+ *   mspipe_util_graph_launch(exec, stream)     one replay on `stream`; no other work is added
+ *                                               (no RNG-offset fills, unlike torch.cuda.CUDAGraph)
+ * Errors: MSPIPE_EINVAL for NULL exec, MSPIPE_ECUDA with the runtime's message
+ * (a capture that fails to end is discarded). */
+MSPIPE_API mspipe_status mspipe_util_graph_begin(void* stream);
+MSPIPE_API mspipe_status mspipe_util_graph_end(void* stream, void** out_exec);
+MSPIPE_API mspipe_status mspipe_util_graph_launch(void* exec, void* stream);
+MSPIPE_API mspipe_status mspipe_util_graph_destroy(void* exec);
+
 #ifdef __cplusplus
 }
 #endif

@@ -7,6 +7,7 @@ Names mirror the C entry points without the ``mspipe_`` prefix.
 from __future__ import annotations
 
 import ctypes as C
+import gc
 import os
 
 import torch
@@ -29,7 +30,8 @@ EXPORTS = ("mspipe_abi_version", "mspipe_last_error", "mspipe_check", "mspipe_sa
            "mspipe_message_build", "mspipe_gru_apply", "mspipe_gru_apply_commit", "mspipe_util_event_record",
            "mspipe_memory_local_rows", "mspipe_nccl_unique_id", "mspipe_memory_writeback_keyed",
            "mspipe_shard_fetch_plan", "mspipe_shard_fetch_serve", "mspipe_shard_fetch_finish",
-           "mspipe_shard_commit_pack", "mspipe_shard_commit_merge", "mspipe_shard_exchange", "mspipe_shard_loopback")
+           "mspipe_shard_commit_pack", "mspipe_shard_commit_merge", "mspipe_shard_exchange", "mspipe_shard_loopback",
+           "mspipe_util_graph_begin", "mspipe_util_graph_end", "mspipe_util_graph_launch", "mspipe_util_graph_destroy")
 XCHG_FETCH_IDS, XCHG_FETCH_ROWS, XCHG_COMMIT = 0, 1, 2
 
 
@@ -78,6 +80,10 @@ def lib():
         L.mspipe_memory_update.argtypes = [P, P, P, P, P, i64, P, P, P, i64, P, P, P, P, P, P, P]
         L.mspipe_memory_writeback.argtypes = [P, i64, P, P, i64, P, P, P, P]
         L.mspipe_util_event_record.argtypes = [P, P]
+        L.mspipe_util_graph_begin.argtypes = [P]
+        L.mspipe_util_graph_end.argtypes = [P, C.POINTER(P)]
+        L.mspipe_util_graph_launch.argtypes = [P, P]
+        L.mspipe_util_graph_destroy.argtypes = [P]
         L.mspipe_memory_prep.argtypes = [P, C.POINTER(Tcsr), i64, P, P, P, P, i64, i32, P, P, P, P, P, P, P, P, P, P,
                                          P, P, P, C.POINTER(Mitigation), C.POINTER(i64), P]
         L.mspipe_gru_workspace_size.argtypes = [P, i64]
@@ -134,6 +140,44 @@ def last_error() -> str:
 def event_record(event: torch.cuda.Event, stream=None):
     """Record a timing event so that it is also captured as a graph node."""
     _ck(lib().mspipe_util_event_record(C.c_void_p(event.cuda_event), stream_ptr(stream)), "event_record")
+
+
+class StepGraph:
+    """One captured step (mspipe_util_graph_*).  Capture must not allocate: the
+    stage's buffers are preallocated, and an allocation during capture raises."""
+
+    def __init__(self):
+        self.exec = C.c_void_p()
+
+    def capture(self, fn, stream):
+        # a handle freed by the cyclic GC mid-capture would cudaFree inside it
+        # and invalidate the capture: collect first, and keep the GC off meanwhile
+        gc.collect()
+        was_enabled = gc.isenabled()
+        gc.disable()
+        before = torch.cuda.memory_stats(stream.device).get("allocation.all.allocated", 0)
+        try:
+            with torch.cuda.stream(stream):
+                _ck(lib().mspipe_util_graph_begin(stream_ptr(stream)), "util_graph_begin")
+                try:
+                    fn()
+                finally:
+                    _ck(lib().mspipe_util_graph_end(stream_ptr(stream), C.byref(self.exec)), "util_graph_end")
+        finally:
+            if was_enabled:
+                gc.enable()
+        after = torch.cuda.memory_stats(stream.device).get("allocation.all.allocated", 0)
+        if after != before:
+            raise RuntimeError(f"StepGraph: {after - before} torch allocations during capture")
+        return self
+
+    def replay(self, stream=None):
+        _ck(lib().mspipe_util_graph_launch(self.exec, stream_ptr(stream)), "util_graph_launch")
+
+    def __del__(self):
+        if getattr(self, "exec", None) and self.exec.value and _lib is not None:
+            _lib.mspipe_util_graph_destroy(self.exec)
+            self.exec = C.c_void_p()
 
 
 def sample_recent(g: "TcsrHandle", roots, query_ts, fanout, out, stream=None):

@@ -648,4 +648,36 @@ mspipe_status mspipe_util_event_record(void* event, void* stream) {
                      "util_event_record");
 }
 
+mspipe_status mspipe_util_graph_begin(void* stream) {
+  return cuda_status(cudaStreamBeginCapture((cudaStream_t)stream, cudaStreamCaptureModeThreadLocal),
+                     "util_graph_begin");
+}
+
+mspipe_status mspipe_util_graph_end(void* stream, void** out_exec) {
+  if (!out_exec) return fail(MSPIPE_EINVAL, "util_graph_end: out_exec is NULL");
+  *out_exec = nullptr;
+  cudaGraph_t g = nullptr;
+  cudaError_t e = cudaStreamEndCapture((cudaStream_t)stream, &g);
+  if (e != cudaSuccess) {
+    if (g) cudaGraphDestroy(g);
+    return cuda_status(e, "util_graph_end: end capture");
+  }
+  cudaGraphExec_t x = nullptr;
+  e = cudaGraphInstantiate(&x, g, 0);
+  cudaGraphDestroy(g);
+  if (e != cudaSuccess) return cuda_status(e, "util_graph_end: instantiate");
+  *out_exec = (void*)x;
+  return MSPIPE_OK;
+}
+
+mspipe_status mspipe_util_graph_launch(void* exec, void* stream) {
+  if (!exec) return fail(MSPIPE_EINVAL, "util_graph_launch: NULL exec");
+  return cuda_status(cudaGraphLaunch((cudaGraphExec_t)exec, (cudaStream_t)stream), "util_graph_launch");
+}
+
+mspipe_status mspipe_util_graph_destroy(void* exec) {
+  if (!exec) return MSPIPE_OK;
+  return cuda_status(cudaGraphExecDestroy((cudaGraphExec_t)exec), "util_graph_destroy");
+}
+
 }  // extern "C"

@@ -10,7 +10,7 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smok
 timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?" >> gpurun_out/bench.err
 timeout 900 python bench.py --gru simt --no-cpu > gpurun_out/bench_simt.json 2> gpurun_out/bench_simt.err
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python bench.py --profile --steps 20 --warmup 3 > gpurun_out/ncu_launch_bench.log 2>&1
-for k in k_gru_tc k_build_x k_fetch_gather k_sample_recent k_dedup k_writeback; do
+for k in k_gru_tc k_build_x k_prep; do
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:$k -s 4 -c 1 -o gpurun_out/prof_$k python bench.py --profile --steps 20 --warmup 3 > gpurun_out/ncu_full_$k.log 2>&1
 done
 ls -la gpurun_out

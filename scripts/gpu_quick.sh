@@ -2,7 +2,7 @@
 # Quick GPU iteration: parity tests, a short bench, and the ncu launch list.
 cd "$GRAFT_REPO_ROOT" || exit 1
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests -m gpu -q -x 2>&1 | tail -4 > gpurun_out/pytest_quick.log; cat gpurun_out/pytest_quick.log
+timeout 900 python -m pytest tests -m gpu -q -x 2>&1 | tail -40 > gpurun_out/pytest_quick.log; cat gpurun_out/pytest_quick.log
 timeout 600 python bench.py --no-cpu --steps 100 ${BENCH_EXTRA} > gpurun_out/bench_quick.json 2> gpurun_out/bench_quick.err
 python - <<'PY'
 import json

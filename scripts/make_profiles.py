@@ -28,6 +28,8 @@ KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
 # op (bench.py roofline key) -> kernels whose DRAM traffic makes up one launch of it
 OPS = {"sample": ["k_sample_recent"], "dedup": ["k_dedup"], "fetch": ["k_fetch_gather"],
        "update": ["k_build_x", "k_gru_tc"], "writeback": ["k_writeback"]}
+# fused step (StageConfig.use_fused): prep = k_prep, build = k_build_x, update = k_gru_tc with the commit
+OPS_FUSED = {"prep": ["k_prep"], "build": ["k_build_x"], "update": ["k_gru_tc"]}
 SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "B": 1, "KB": 1e3, "MB": 1e6, "GB": 1e9}
 
 
@@ -124,7 +126,8 @@ def main(tag, config="wiki"):
                 fh.write(f"| {k} | {len(v)} | {sum(v) / len(v) / 1000:.2f} | {share:.3f} |\n")
     tpath = os.path.join(PROF, "ncu_traffic.json")
     allt = json.load(open(tpath)) if os.path.exists(tpath) else {}
-    allt[config] = {op: sum(traffic.get(k, 0.0) for k in ks) for op, ks in OPS.items()
+    ops = OPS_FUSED if "k_prep" in traffic else OPS
+    allt[config] = {op: sum(traffic.get(k, 0.0) for k in ks) for op, ks in ops.items()
                     if all(k in traffic for k in ks)}
     allt[config]["_source"] = f"{tag}_ncu_summary.md (dram__bytes_read.sum + dram__bytes_write.sum per launch)"
     with open(tpath, "w") as fh:

@@ -335,7 +335,11 @@ def test_abi_staleness_and_order_errors(dev):
     assert e.value.status == _C.ESTALE
 
 
-def test_cuda_graph_replay_equals_eager(dev):
+@pytest.mark.parametrize("kind", ["torch", "mspipe", "mspipe_staged"])
+def test_cuda_graph_replay_equals_eager(dev, kind):
+    """Step graphs (torch.cuda.CUDAGraph, or mspipe_util_graph_* as bench.py
+    uses them, with resident or pinned-host inputs) replay the eager stream
+    bit for bit."""
     w = make_workload("tiny", seed=3, num_events=3000)
     cfg = w["cfg"]
     outs = []
@@ -343,24 +347,31 @@ def test_cuda_graph_replay_equals_eager(dev):
         sc = StageConfig(cfg.num_nodes, cfg.mem_dim, cfg.edge_dim, cfg.time_dim, cfg.fanout, cfg.batch, 1)
         g = build_tcsr(cfg.num_nodes, w["src"], w["dst"], w["ts"], dev)
         st = MemoryStage(sc, w["params"], g, dev)
-        t = {kk: _t(w[kk], dev) for kk in ("src", "dst", "ts", "neg", "ef")}
-        st.bind_resident(t["src"], t["dst"], t["ts"], t["neg"], t["ef"])
+        if use_graph and kind == "mspipe_staged":
+            st.bind_host(w["src"], w["dst"], w["ts"], w["neg"], w["ef"])
+        else:
+            t = {kk: _t(w[kk], dev) for kk in ("src", "dst", "ts", "neg", "ef")}
+            st.bind_resident(t["src"], t["dst"], t["ts"], t["neg"], t["ef"])
         if use_graph:
             steps = st.step_ops()
             s = torch.cuda.Stream()
             graphs = []
-            with torch.cuda.stream(s):
-                for ops in steps:
+            for ops in steps:
+                if kind == "torch":
                     gr = torch.cuda.CUDAGraph()
-                    with torch.cuda.graph(gr, stream=s):
+                    with torch.cuda.stream(s), torch.cuda.graph(gr, stream=s):
                         st.run_ops(ops)
-                    graphs.append(gr)
+                else:
+                    gr = _C.StepGraph().capture(lambda: st.run_ops(ops), s)
+                graphs.append(gr)
             st.memory.reset()
-            for gr in graphs:
-                gr.replay()
+            with torch.cuda.stream(s):
+                for gr in graphs:
+                    gr.replay()
         else:
             st.run()
         torch.cuda.synchronize()
+        _C.check()
         outs.append((st.memory.mem.cpu().numpy(), st.memory.mem_ts.cpu().numpy()))
     assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
 
