@@ -135,8 +135,40 @@ MSPIPE_API mspipe_status mspipe_memory_create(mspipe_memory** out, int64_t num_n
                                    const void* nccl_unique_id /* [host] 128 B, NULL iff world==1 */);
 MSPIPE_API mspipe_status mspipe_memory_destroy(mspipe_memory* st);
 MSPIPE_API int64_t mspipe_memory_committed(const mspipe_memory* st); /* [host] last enqueued commit version */
-/* [host] restart an epoch: committed := 0 (the caller re-zeroes the tables, G17). */
+/* [host] restart an epoch: committed := 0 (the caller re-zeroes the tables, G17;
+ * when double-buffered, set 0 is then mirrored into set 1, synchronously). */
 MSPIPE_API mspipe_status mspipe_memory_reset(mspipe_memory* st);
+
+/* Double-buffered state (world == 1).  With staleness k >= 1 the fetch of
+ * batch t+k reads version t-1 while commit t writes version t (Eq. 2,
+ * P:L196-L204); with one table set the commit must wait for that fetch.  With
+ * two sets, version c lives in set c & 1 (set 0 = the tables given to
+ * mspipe_memory_create, set 1 = the tables given here, same shapes, caller-
+ * owned, device); commit c first copies the rows of commit c-1 from set
+ * (c-1)&1 into set c&1, then writes its own rows there.  A fetch or prep reads
+ * the set of version `committed` at the time it is enqueued, so the fetch of
+ * version c-1 and commit c touch different tables and may run concurrently.
+ * Caller's obligation (stream order): a fetch/prep enqueued while committed = c
+ * completes before commit c+2 is enqueued (one commit per pipeline step and a
+ * join per step satisfy it).  Call once, with committed == 0 (else
+ * MSPIPE_EORDER); set 0 is mirrored into set 1 (synchronously).  world > 1:
+ * MSPIPE_EUNSUPPORTED.  Extra device memory besides set 1: (k+3)·N·4 + 8 bytes
+ * (previous-commit winner lists, and the winner stamps mspipe_memory_prep
+ * writes so that mspipe_gru_apply_commit can do the catch-up inside its GEMM
+ * kernel instead of a separate launch). */
+MSPIPE_API mspipe_status mspipe_memory_double_buffer(mspipe_memory* st, float* mem1, double* mem_ts1,
+                                          float* mail1, double* mail_ts1);
+/* [host] bookkeeping after replaying captured work (CUDA graphs): the
+ * handle's `committed` counter advances when a commit is ENQUEUED, so a
+ * capture leaves it at the last captured version and mspipe_memory_reset
+ * rewinds it; after replaying the captured commits up to `version` from a
+ * reset, call this so that the counter (and, double-buffered, the table set
+ * holding the state) match the device again.  No device work. */
+MSPIPE_API mspipe_status mspipe_memory_set_committed(mspipe_memory* st, int64_t version);
+/* [host] the tables holding `version` (version == committed, or committed - 1
+ * when double-buffered; else MSPIPE_EINVAL).  Any output pointer may be NULL. */
+MSPIPE_API mspipe_status mspipe_memory_tables(const mspipe_memory* st, int64_t version, float** mem,
+                                   double** mem_ts, float** mail, double** mail_ts);
 
 /* A4 — similarity-based staleness mitigation (MSPipe-S), applied "in the
  * memory fetching stage".  Targets are the 2B update endpoints

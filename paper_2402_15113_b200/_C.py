@@ -31,7 +31,8 @@ EXPORTS = ("mspipe_abi_version", "mspipe_last_error", "mspipe_check", "mspipe_sa
            "mspipe_memory_local_rows", "mspipe_nccl_unique_id", "mspipe_memory_writeback_keyed",
            "mspipe_shard_fetch_plan", "mspipe_shard_fetch_serve", "mspipe_shard_fetch_finish",
            "mspipe_shard_commit_pack", "mspipe_shard_commit_merge", "mspipe_shard_exchange", "mspipe_shard_loopback",
-           "mspipe_util_graph_begin", "mspipe_util_graph_end", "mspipe_util_graph_launch", "mspipe_util_graph_destroy")
+           "mspipe_util_graph_begin", "mspipe_util_graph_end", "mspipe_util_graph_launch", "mspipe_util_graph_destroy",
+           "mspipe_memory_double_buffer", "mspipe_memory_tables", "mspipe_memory_set_committed")
 XCHG_FETCH_IDS, XCHG_FETCH_ROWS, XCHG_COMMIT = 0, 1, 2
 
 
@@ -80,6 +81,9 @@ def lib():
         L.mspipe_memory_update.argtypes = [P, P, P, P, P, i64, P, P, P, i64, P, P, P, P, P, P, P]
         L.mspipe_memory_writeback.argtypes = [P, i64, P, P, i64, P, P, P, P]
         L.mspipe_util_event_record.argtypes = [P, P]
+        L.mspipe_memory_double_buffer.argtypes = [P, P, P, P, P]
+        L.mspipe_memory_set_committed.argtypes = [P, i64]
+        L.mspipe_memory_tables.argtypes = [P, i64, C.POINTER(P), C.POINTER(P), C.POINTER(P), C.POINTER(P)]
         L.mspipe_util_graph_begin.argtypes = [P]
         L.mspipe_util_graph_end.argtypes = [P, C.POINTER(P)]
         L.mspipe_util_graph_launch.argtypes = [P, P]
@@ -240,24 +244,52 @@ def mail_stride_for(mem_dim, edge_dim):
 class MemoryHandle:
     """mspipe_memory over caller-owned (here: this object's) state tables."""
 
-    def __init__(self, num_nodes, mem_dim, edge_dim, staleness_k, device, rank=0, world=1, nccl_id=None):
+    def __init__(self, num_nodes, mem_dim, edge_dim, staleness_k, device, rank=0, world=1, nccl_id=None,
+                 double_buffer=False):
         """world > 1: the tables hold this rank's shard (rows v with v % world == rank);
-        nccl_id (bytes) selects the NCCL transport, None the in-process loopback."""
+        nccl_id (bytes) selects the NCCL transport, None the in-process loopback.
+        double_buffer: a second table set (mspipe_memory_double_buffer); mem / mem_ts /
+        mail / mail_ts always name the set holding the committed version."""
         self.num_nodes, self.mem_dim, self.edge_dim, self.k = num_nodes, mem_dim, edge_dim, staleness_k
         self.rank, self.world = rank, world
         self.mail_stride = mail_stride_for(mem_dim, edge_dim)
         rows = (num_nodes - rank + world - 1) // world
-        self.mem = torch.zeros((rows, mem_dim), dtype=torch.float32, device=device)
-        self.mem_ts = torch.zeros((rows,), dtype=torch.float64, device=device)
-        self.mail = torch.zeros((rows, self.mail_stride), dtype=torch.float32, device=device)
-        self.mail_ts = torch.zeros((rows,), dtype=torch.float64, device=device)
+
+        def tables():
+            return dict(mem=torch.zeros((rows, mem_dim), dtype=torch.float32, device=device),
+                        mem_ts=torch.zeros((rows,), dtype=torch.float64, device=device),
+                        mail=torch.zeros((rows, self.mail_stride), dtype=torch.float32, device=device),
+                        mail_ts=torch.zeros((rows,), dtype=torch.float64, device=device))
+
+        self._sets = [tables()]
+        t0 = self._sets[0]
         h = C.c_void_p()
         self._nccl_id = None if nccl_id is None else C.create_string_buffer(bytes(nccl_id), len(nccl_id))
-        _ck(lib().mspipe_memory_create(C.byref(h), num_nodes, mem_dim, edge_dim, staleness_k, ptr(self.mem),
-                                       ptr(self.mem_ts), ptr(self.mail), ptr(self.mail_ts), self.mail_stride,
+        _ck(lib().mspipe_memory_create(C.byref(h), num_nodes, mem_dim, edge_dim, staleness_k, ptr(t0["mem"]),
+                                       ptr(t0["mem_ts"]), ptr(t0["mail"]), ptr(t0["mail_ts"]), self.mail_stride,
                                        rank, world, self._nccl_id), "mspipe_memory_create")
         self.h = h
         assert lib().mspipe_memory_local_rows(h) == rows
+        self.double_buffer = bool(double_buffer)
+        if double_buffer:
+            t1 = tables()
+            _ck(lib().mspipe_memory_double_buffer(h, ptr(t1["mem"]), ptr(t1["mem_ts"]), ptr(t1["mail"]),
+                                                  ptr(t1["mail_ts"])), "mspipe_memory_double_buffer")
+            self._sets.append(t1)
+
+    def tables(self, version=None):
+        """The table set holding `version` (default: the committed one)."""
+        if not self.double_buffer:
+            return self._sets[0]
+        v = self.committed if version is None else version
+        out = C.c_void_p()
+        _ck(lib().mspipe_memory_tables(self.h, v, C.byref(out), None, None, None), "mspipe_memory_tables")
+        return self._sets[0] if out.value == self._sets[0]["mem"].data_ptr() else self._sets[1]
+
+    mem = property(lambda self: self.tables()["mem"])
+    mem_ts = property(lambda self: self.tables()["mem_ts"])
+    mail = property(lambda self: self.tables()["mail"])
+    mail_ts = property(lambda self: self.tables()["mail_ts"])
 
     def __del__(self):
         if getattr(self, "h", None) and _lib is not None:
@@ -268,11 +300,16 @@ class MemoryHandle:
     def committed(self):
         return int(lib().mspipe_memory_committed(self.h))
 
+    def set_committed(self, version):
+        """After replaying captured steps from a reset (see mspipe_memory_set_committed)."""
+        _ck(lib().mspipe_memory_set_committed(self.h, int(version)), "mspipe_memory_set_committed")
+
     def reset(self, zero_tables=True):
         """New epoch: committed := 0; tables back to S_0 = 0 (G17)."""
         if zero_tables:
-            for t in (self.mem, self.mem_ts, self.mail, self.mail_ts):
-                t.zero_()
+            for ts in self._sets:
+                for t in ts.values():
+                    t.zero_()
         _ck(lib().mspipe_memory_reset(self.h), "mspipe_memory_reset")
 
 

@@ -166,13 +166,84 @@ mspipe_status mspipe_memory_create(mspipe_memory** out, int64_t num_nodes, int32
   return MSPIPE_OK;
 }
 
+// set 1 <- set 0, no previous commit (version 0 in both sets)
+static mspipe_status db_mirror(mspipe_memory* st) {
+  const size_t N = (size_t)st->num_nodes;
+  cudaError_t e = cudaMemcpy(st->mem1, st->mem, sizeof(float) * N * st->mem_dim, cudaMemcpyDeviceToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(st->mem_ts1, st->mem_ts, sizeof(double) * N, cudaMemcpyDeviceToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(st->mail1, st->mail, sizeof(float) * N * st->mail_stride, cudaMemcpyDeviceToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(st->mail_ts1, st->mail_ts, sizeof(double) * N, cudaMemcpyDeviceToDevice);
+  if (e == cudaSuccess) e = cudaMemset(st->prev_num, 0, 2 * sizeof(int32_t));
+  if (e == cudaSuccess) e = cudaMemset(st->stamps, 0, sizeof(int32_t) * (size_t)(st->k + 1) * N);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  st->prev_max[0] = st->prev_max[1] = 0;
+  for (int r = 0; r <= st->k; ++r) st->stamp_iter[r] = 0;
+  return cuda_status(e, "memory double buffer: mirror");
+}
+
+mspipe_status mspipe_memory_double_buffer(mspipe_memory* st, float* mem1, double* mem_ts1, float* mail1,
+                                          double* mail_ts1) {
+  if (!st) return fail(MSPIPE_EINVAL, "memory_double_buffer: NULL handle");
+  if (st->world != 1) return fail(MSPIPE_EUNSUPPORTED, "memory_double_buffer: world > 1");
+  if (st->db) return fail(MSPIPE_EINVAL, "memory_double_buffer: already double-buffered");
+  if (st->committed != 0) return fail(MSPIPE_EORDER, "memory_double_buffer: committed=%lld (must be 0)", (long long)st->committed);
+  if (!mem1 || !mem_ts1 || !mail1 || !mail_ts1) return fail(MSPIPE_EINVAL, "memory_double_buffer: null table");
+  cudaError_t e = cudaMalloc(&st->prev_nodes, sizeof(int32_t) * 2 * (size_t)st->num_nodes);
+  if (e == cudaSuccess) e = cudaMalloc(&st->prev_num, 2 * sizeof(int32_t));
+  if (e == cudaSuccess) e = cudaMalloc(&st->stamps, sizeof(int32_t) * (size_t)(st->k + 1) * (size_t)st->num_nodes);
+  if (e != cudaSuccess) return cuda_status(e, "memory_double_buffer: alloc");
+  st->stamp_iter = new int64_t[st->k + 1]();
+  st->mem1 = mem1;
+  st->mem_ts1 = mem_ts1;
+  st->mail1 = mail1;
+  st->mail_ts1 = mail_ts1;
+  st->db = 1;
+  return db_mirror(st);
+}
+
+mspipe_status mspipe_memory_set_committed(mspipe_memory* st, int64_t version) {
+  if (!st) return fail(MSPIPE_EINVAL, "memory_set_committed: NULL handle");
+  if (version < 0) return fail(MSPIPE_EINVAL, "memory_set_committed: version=%lld", (long long)version);
+  st->committed = version;
+  return MSPIPE_OK;
+}
+
+mspipe_status mspipe_memory_tables(const mspipe_memory* st, int64_t version, float** mem, double** mem_ts,
+                                   float** mail, double** mail_ts) {
+  if (!st) return fail(MSPIPE_EINVAL, "memory_tables: NULL handle");
+  if (!(version == st->committed || (st->db && version == st->committed - 1 && version >= 0)))
+    return fail(MSPIPE_EINVAL, "memory_tables: version %lld is not held (committed=%lld, double-buffered=%d)",
+                (long long)version, (long long)st->committed, st->db);
+  const TableSet t = table_set(st, version);
+  if (mem) *mem = t.mem;
+  if (mem_ts) *mem_ts = t.mem_ts;
+  if (mail) *mail = t.mail;
+  if (mail_ts) *mail_ts = t.mail_ts;
+  return MSPIPE_OK;
+}
+
+// double-buffered commit c, first half (see k_catchup)
+static cudaError_t db_catchup(mspipe_memory* st, int64_t c, const int32_t* nodes, const int32_t* num, int64_t max_n,
+                              cudaStream_t s) {
+  const int p = (int)(c & 1), q = p ^ 1;
+  const int64_t N = st->num_nodes;
+  const TableSet from = table_set(st, c - 1), to = table_set(st, c);
+  launch_catchup(st->prev_nodes + q * N, st->prev_num + q, st->prev_max[q], from.mem, from.mem_ts, from.mail,
+                 from.mail_ts, to.mem, to.mem_ts, to.mail, to.mail_ts, st->mem_dim, st->mail_stride,
+                 max_n > 0 ? nodes : nullptr, max_n > 0 ? num : nullptr, max_n, st->prev_nodes + p * N,
+                 st->prev_num + p, s);
+  return cudaGetLastError();
+}
+
 mspipe_status mspipe_memory_destroy(mspipe_memory* st) {
   if (!st) return MSPIPE_OK;
   nccl_comm_destroy(st);
   void* bufs[] = {st->scratch, st->sh_needed, st->sh_slot_of, st->sh_send_ids, st->sh_recv_ids, st->sh_fsend,
-                  st->sh_frecv, st->sh_csend, st->sh_crecv, st->sh_dest, st->sh_keytab};
+                  st->sh_frecv, st->sh_csend, st->sh_crecv, st->sh_dest, st->sh_keytab, st->prev_nodes,
+                  st->prev_num, st->stamps};
   for (void* b : bufs)
     if (b) cudaFree(b);
+  delete[] st->stamp_iter;
   delete st;
   return MSPIPE_OK;
 }
@@ -184,6 +255,10 @@ int64_t mspipe_memory_committed(const mspipe_memory* st) { return st ? st->commi
 mspipe_status mspipe_memory_reset(mspipe_memory* st) {
   if (!st) return fail(MSPIPE_EINVAL, "memory_reset: NULL handle");
   st->committed = 0;
+  if (st->db) {  // version 0 = set 0 (the caller's initial state), mirrored into set 1
+    mspipe_status rc = db_mirror(st);
+    if (rc != MSPIPE_OK) return rc;
+  }
   if (st->sh_keytab) {  // keys restart with the stream
     cudaError_t e = cudaMemset(st->sh_keytab, 0, sizeof(unsigned long long) * (size_t)st->local_rows);
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
@@ -224,11 +299,12 @@ mspipe_status mspipe_memory_fetch(mspipe_memory* st, int64_t iteration, const in
       return fail(MSPIPE_EINVAL, "memory_fetch: lambda=%g n_sim=%d fanout=%d (fanout<=16, n_sim<=16)", mit->lambda, mit->n_sim, mit->fanout);
   }
   cudaStream_t s = (cudaStream_t)stream;
+  const TableSet t = table_set(st, st->committed);  // version v(i) = committed (stream order)
   if (n > 0)
-    launch_fetch(ids, n, st->num_nodes, st->mem, st->mem_ts, st->mem_dim, out_mail ? st->mail : nullptr,
-                 st->mail_ts, st->mail_stride, out_mem, out_mem_ts, out_mail, out_mail_ts, s);
+    launch_fetch(ids, n, st->num_nodes, t.mem, t.mem_ts, st->mem_dim, out_mail ? t.mail : nullptr,
+                 t.mail_ts, st->mail_stride, out_mem, out_mem_ts, out_mail, out_mail_ts, s);
   if (mit && mit->num_events > 0)
-    launch_mitigate(to_tcsr(mit->g), mit->src, mit->dst, mit->ts, mit->num_events, st->mem, st->mem_ts,
+    launch_mitigate(to_tcsr(mit->g), mit->src, mit->dst, mit->ts, mit->num_events, t.mem, t.mem_ts,
                     st->mem_dim, mit->lambda, mit->gamma, mit->n_sim, mit->fanout, mit->out_h,
                     mit->out_omega, mit->out_elig, s);
   if (out_version) *out_version = st->committed;
@@ -365,11 +441,19 @@ mspipe_status mspipe_memory_writeback(mspipe_memory* st, int64_t commit_version,
   if (max_n < 0) return fail(MSPIPE_EINVAL, "memory_writeback: max_n=%lld", (long long)max_n);
   if (max_n > 0 && (!nodes || !num_unique || !new_mem || !new_ts || !new_mail))
     return fail(MSPIPE_EINVAL, "memory_writeback: null input");
+  if (st->db) {
+    cudaError_t e = db_catchup(st, commit_version, nodes, num_unique, max_n, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_status(e, "memory_writeback: catch-up");
+  }
+  const TableSet t = table_set(st, commit_version);
   if (max_n > 0)
     launch_writeback(nodes, num_unique, max_n, new_mem, new_ts, new_mail, st->mem_dim, st->mail_stride,
-                     st->mem, st->mem_ts, st->mail, st->mail_ts, st->num_nodes, (cudaStream_t)stream);
+                     t.mem, t.mem_ts, t.mail, t.mail_ts, st->num_nodes, (cudaStream_t)stream);
   mspipe_status rc = after_launch("memory_writeback");
-  if (rc == MSPIPE_OK) st->committed = commit_version;  // i_upd <- i (Alg. 1 L16)
+  if (rc == MSPIPE_OK) {
+    st->committed = commit_version;  // i_upd <- i (Alg. 1 L16)
+    st->prev_max[commit_version & 1] = max_n;
+  }
   return rc;
 }
 
@@ -392,15 +476,19 @@ mspipe_status mspipe_memory_prep(mspipe_memory* st, const mspipe_tcsr* g, int64_
                 (long long)iteration, (long long)st->committed, st->k);
   if ((out_mail == nullptr) != (out_mail_ts == nullptr)) return fail(MSPIPE_EINVAL, "memory_prep: out_mail and out_mail_ts go together");
   cudaStream_t s = (cudaStream_t)stream;
+  const TableSet t = table_set(st, st->committed);
   if (num_events > 0) {
     if (!src || !dst || !neg || !ts || !out_nbr || !out_eid || !out_ts || !out_dt || !out_cnt || !out_sub_ids ||
         !out_nodes || !out_winner || !out_num_unique || !out_mem || !out_mem_ts)
       return fail(MSPIPE_EINVAL, "memory_prep: null input/output");
     cudaError_t e = launch_prep(to_tcsr(g), src, dst, neg, ts, num_events, fanout, out_nbr, out_eid, out_ts, out_dt,
-                                out_cnt, out_sub_ids, st->scratch, out_nodes, out_winner, out_num_unique, st->mem,
-                                st->mem_ts, st->mem_dim, st->mail, st->mail_ts, st->mail_stride, out_mem,
-                                out_mem_ts, out_mail, out_mail_ts, s);
+                                out_cnt, out_sub_ids, st->scratch, out_nodes, out_winner, out_num_unique, t.mem,
+                                t.mem_ts, st->mem_dim, t.mail, t.mail_ts, st->mail_stride, out_mem,
+                                out_mem_ts, out_mail, out_mail_ts, s,
+                                st->db ? st->stamps + (iteration % (st->k + 1)) * st->num_nodes : nullptr,
+                                (int32_t)iteration);
     if (e != cudaSuccess) return cuda_status(e, "memory_prep: launch");
+    if (st->db) st->stamp_iter[iteration % (st->k + 1)] = iteration;
   } else if (out_num_unique) {
     cudaError_t e = cudaMemsetAsync(out_num_unique, 0, sizeof(int32_t), s);
     if (e != cudaSuccess) return cuda_status(e, "memory_prep");
@@ -410,7 +498,7 @@ mspipe_status mspipe_memory_prep(mspipe_memory* st, const mspipe_tcsr* g, int64_
       return fail(MSPIPE_EINVAL, "memory_prep: bad mitigation arguments");
     if (!(mit->lambda >= 0.f && mit->lambda <= 1.f) || mit->n_sim < 0 || mit->n_sim > 16 || mit->fanout < 1 || mit->fanout > 16)
       return fail(MSPIPE_EINVAL, "memory_prep: lambda=%g n_sim=%d fanout=%d", mit->lambda, mit->n_sim, mit->fanout);
-    launch_mitigate(to_tcsr(mit->g), mit->src, mit->dst, mit->ts, mit->num_events, st->mem, st->mem_ts, st->mem_dim,
+    launch_mitigate(to_tcsr(mit->g), mit->src, mit->dst, mit->ts, mit->num_events, t.mem, t.mem_ts, st->mem_dim,
                     mit->lambda, mit->gamma, mit->n_sim, mit->fanout, mit->out_h, mit->out_omega, mit->out_elig, s);
   }
   if (out_version) *out_version = st->committed;
@@ -489,14 +577,44 @@ mspipe_status mspipe_gru_apply_commit(const mspipe_gru* gru, mspipe_memory* st,
       return fail(MSPIPE_EINVAL, "gru_apply_commit: workspace of %zu bytes too small", ws_bytes);
     if (!snap_mem || !nodes || !winner || !num_unique || !new_ts || !new_mail)
       return fail(MSPIPE_EINVAL, "gru_apply_commit: null input");
-    GruCommit c{nodes, st->mem, st->mem_ts, st->mail, st->mail_ts, new_ts, new_mail, st->num_nodes, st->mail_stride};
+  }
+  const int64_t max_n = 2 * num_events;
+  // double-buffered: the GEMM kernel catches up the previous commit's rows
+  // itself when mspipe_memory_prep stamped this batch's winners; otherwise a
+  // separate k_catchup launch goes first
+  const int64_t ring = st->db ? commit_version % (st->k + 1) : 0;
+  const bool fused_catchup = st->db && num_events > 0 && st->stamp_iter[ring] == commit_version;
+  if (st->db && !fused_catchup) {
+    cudaError_t e = db_catchup(st, commit_version, nodes, num_unique, max_n, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_status(e, "gru_apply_commit: catch-up");
+  }
+  if (num_events > 0) {
+    const TableSet t = table_set(st, commit_version);
+    GruCommit c{nodes, t.mem, t.mem_ts, t.mail, t.mail_ts, new_ts, new_mail, st->num_nodes, st->mail_stride};
+    if (fused_catchup) {
+      const int p = (int)(commit_version & 1), q = p ^ 1;
+      const TableSet o = table_set(st, commit_version - 1);
+      c.save_nodes = st->prev_nodes + p * st->num_nodes;
+      c.save_num = st->prev_num + p;
+      c.prev_nodes = st->prev_nodes + q * st->num_nodes;
+      c.prev_num = st->prev_num + q;
+      c.old_mem = o.mem;
+      c.old_mem_ts = o.mem_ts;
+      c.old_mail = o.mail;
+      c.old_mail_ts = o.mail_ts;
+      c.stamp = st->stamps + ring * st->num_nodes;
+      c.iter = (int32_t)commit_version;
+    }
     cudaError_t e = launch_gru_tc(gru->d, gru->wtc, (float*)workspace, nullptr, num_events, nullptr, snap_mem, nullptr,
                                   snap_step, snap_h, winner, num_unique, out_mem, nullptr, nullptr, 0,
                                   (cudaStream_t)stream, kGruGemm, &c);
     if (e != cudaSuccess) return cuda_status(e, "gru_apply_commit: launch");
   }
   mspipe_status rc = after_launch("gru_apply_commit");
-  if (rc == MSPIPE_OK) st->committed = commit_version;  // i_upd <- i (Alg. 1 L16)
+  if (rc == MSPIPE_OK) {
+    st->committed = commit_version;  // i_upd <- i (Alg. 1 L16)
+    st->prev_max[commit_version & 1] = max_n;
+  }
   return rc;
 }
 

@@ -290,7 +290,38 @@ struct TcArgs {
   const double* new_ts;
   const float* new_mail;
   int64_t num_nodes;
+  // double-buffered state (GruCommit)
+  int32_t* save_nodes;
+  int32_t* save_num;
+  const int32_t* prev_nodes;
+  const int32_t* prev_num;
+  const float4* old_mem;
+  const double* old_mem_ts;
+  const float4* old_mail;
+  const double* old_mail_ts;
+  const int32_t* stamp;
+  int32_t iter;
 };
+
+// Double-buffered commit: copy the previous commit's rows (old set -> this
+// commit's set) except this commit's own winners, which the epilogue writes.
+// Warp `wq` of `nw` participating warps; one warp per row.
+__device__ __forceinline__ void catch_up(const TcArgs& a, int64_t wq, int64_t nw, int lane) {
+  const int32_t np = __ldg(a.prev_num);
+  const int Qm = a.d.M / 4, Qa = (int)(a.mail_stride / 4);
+  float4* mem = reinterpret_cast<float4*>(a.commit_mem);
+  float4* mail = reinterpret_cast<float4*>(a.commit_mail);
+  for (int64_t r = wq; r < np; r += nw) {
+    const int32_t v = __ldg(a.prev_nodes + r);
+    if (__ldg(a.stamp + v) == a.iter) continue;
+    for (int c = lane; c < Qm; c += 32) mem[(int64_t)v * Qm + c] = __ldg(a.old_mem + (int64_t)v * Qm + c);
+    for (int c = lane; c < Qa; c += 32) mail[(int64_t)v * Qa + c] = __ldg(a.old_mail + (int64_t)v * Qa + c);
+    if (lane == 0) {
+      a.commit_mem_ts[v] = __ldg(a.old_mem_ts + v);
+      a.commit_mail_ts[v] = __ldg(a.old_mail_ts + v);
+    }
+  }
+}
 
 // A5: one warp per (row, chunk).  lane = column inside the chunk.
 __global__ void __launch_bounds__(256) k_build_x(TcArgs a) {
@@ -406,10 +437,19 @@ __global__ void __launch_bounds__(tc::kThreads, 1) k_gru_tc(TcArgs a) {
   // are the last CTAs the scheduler launches and they exit at once.
   const int32_t mt = blockIdx.z;
   const int32_t m0 = mt * kM;
-  if (m0 >= U) return;  // uniform across the cluster (same blockIdx.z)
   const int jt = blockIdx.y;
   const int S = gridDim.x;
   const int split = blockIdx.x;
+  // CTAs of the active M tiles (at least one tile) share the catch-up
+  const int32_t mt_act = U > 0 ? (U + kM - 1) / kM : 1;
+  const int64_t cta_q = ((int64_t)mt * gridDim.y + jt) * S + split;
+  const int64_t n_cta = (int64_t)mt_act * gridDim.y * S;
+  if (a.save_num && cta_q == 0 && threadIdx.x == 0) *a.save_num = U;
+  if (m0 >= U) {  // uniform across the cluster (same blockIdx.z)
+    if (a.stamp && mt < mt_act) catch_up(a, cta_q * (kThreads / 32) + (threadIdx.x >> 5), n_cta * (kThreads / 32),
+                                         threadIdx.x & 31);
+    return;
+  }
   const int32_t nchunks = d.Kpad / kKC;
   const int32_t c0 = split * nchunks / S, c1 = (split + 1) * nchunks / S;
   const int32_t nc = c1 - c0;  // <= kMaxChunks (host picks S >= nchunks / kMaxChunks)
@@ -486,8 +526,13 @@ __global__ void __launch_bounds__(tc::kThreads, 1) k_gru_tc(TcArgs a) {
         hv = __ldg(reinterpret_cast<const float4*>(hrow + j0));
       }
       hbuf[mm * (kJ / 4) + q] = hv;
-      if (q == 0) rownode[mm] = (a.commit_mem && u < U) ? __ldg(a.nodes + u) : -1;
+      if (q == 0) {
+        const int32_t node = (a.commit_mem && u < U) ? __ldg(a.nodes + u) : -1;
+        rownode[mm] = node;
+        if (a.save_nodes && jt == 0 && node >= 0) a.save_nodes[u] = node;
+      }
     }
+    if (a.stamp) catch_up(a, cta_q * 2 + (warp - 2), n_cta * 2, lane);
   }
   __syncwarp();
 
@@ -629,8 +674,7 @@ cudaError_t launch_gru_tc(const GruDesc& d, const float* wtc, float* xbuf, const
     attr_set = true;
   }
   TcArgs a{d, wtc, xbuf, ts, num_events, edge_feat, snap_mem, snap_mem_ts, snap_step, snap_h, winner,
-           num_unique, out_mem, out_ts, out_mail, mail_stride, nullptr, nullptr, nullptr, nullptr, nullptr,
-           nullptr, nullptr, 0};
+           num_unique, out_mem, out_ts, out_mail, mail_stride};
   if (commit) {
     a.nodes = commit->nodes;
     a.commit_mem = commit->mem;
@@ -641,6 +685,16 @@ cudaError_t launch_gru_tc(const GruDesc& d, const float* wtc, float* xbuf, const
     a.new_mail = commit->new_mail;
     a.num_nodes = commit->num_nodes;
     a.mail_stride = commit->mail_stride;
+    a.save_nodes = commit->save_nodes;
+    a.save_num = commit->save_num;
+    a.prev_nodes = commit->prev_nodes;
+    a.prev_num = commit->prev_num;
+    a.old_mem = reinterpret_cast<const float4*>(commit->old_mem);
+    a.old_mem_ts = commit->old_mem_ts;
+    a.old_mail = reinterpret_cast<const float4*>(commit->old_mail);
+    a.old_mail_ts = commit->old_mail_ts;
+    a.stamp = commit->stamp;
+    a.iter = commit->iter;
   }
   const int64_t max_rows = 2 * num_events;
   const int64_t mtiles = (max_rows + tc::kM - 1) / tc::kM;

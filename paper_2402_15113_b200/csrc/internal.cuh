@@ -138,6 +138,11 @@ void launch_writeback(const int32_t* nodes, const int32_t* num, int64_t max_n,
                       const float* new_mem, const double* new_ts, const float* new_mail,
                       int32_t mem_dim, int64_t mail_stride, float* mem, double* mem_ts,
                       float* mail, double* mail_ts, int64_t num_nodes, cudaStream_t s);
+void launch_catchup(const int32_t* prev_nodes, const int32_t* prev_num, int64_t prev_max, const float* src_mem,
+                    const double* src_mem_ts, const float* src_mail, const double* src_mail_ts, float* dst_mem,
+                    double* dst_mem_ts, float* dst_mail, double* dst_mail_ts, int32_t mem_dim, int64_t mail_stride,
+                    const int32_t* cur_nodes, const int32_t* cur_num, int64_t cur_max, int32_t* save_nodes,
+                    int32_t* save_num, cudaStream_t s);
 // gru_simt.cu
 struct GruDesc {
   int32_t M, He, Dt, Dm, Dx, K, Kpad, Npad;
@@ -171,6 +176,20 @@ struct GruCommit {  // fused A7 in the GEMM epilogue
   const float* new_mail;
   int64_t num_nodes;
   int64_t mail_stride;
+  // double-buffered state (optional): save this commit's winner list for the
+  // next commit and, when `stamp` is set, catch up the previous commit's rows
+  // (prev_nodes from set `old_*`), skipping nodes with stamp[v] == iter
+  // (this commit's winners, stamped by k_prep)
+  int32_t* save_nodes;
+  int32_t* save_num;
+  const int32_t* prev_nodes;
+  const int32_t* prev_num;
+  const float* old_mem;
+  const double* old_mem_ts;
+  const float* old_mail;
+  const double* old_mail_ts;
+  const int32_t* stamp;
+  int32_t iter;
 };
 cudaError_t launch_gru_tc(const GruDesc& d, const float* wtc, float* xbuf, const double* ts, int64_t num_events,
                           const float* edge_feat, const float* snap_mem, const double* snap_mem_ts,
@@ -185,7 +204,8 @@ cudaError_t launch_prep(const Tcsr& g, const int32_t* src, const int32_t* dst, c
                         int32_t* scratch, int32_t* out_nodes, int32_t* out_winner, int32_t* out_num,
                         const float* mem, const double* mem_ts, int32_t mem_dim, const float* mail,
                         const double* mail_ts, int64_t mail_stride, float* out_mem, double* out_mem_ts,
-                        float* out_mail, double* out_mail_ts, cudaStream_t s);
+                        float* out_mail, double* out_mail_ts, cudaStream_t s, int32_t* stamp = nullptr,
+                        int32_t stamp_iter = 0);
 
 }  // namespace mspipe
 
@@ -238,7 +258,38 @@ struct mspipe_memory {
   unsigned long long* sh_keytab;  // [local_rows] LWW key of the committed row
   int32_t sh_with_mail;     // the in-flight fetch carries mail rows
   void* nccl_comm;          // ncclComm_t (NULL: in-process loopback transport)
+  // ---- double-buffered state (mspipe_memory_double_buffer) ----
+  // Set 0 = the tables above, set 1 = a second caller-owned set; version c
+  // lives in set c & 1.  Commit c first copies the rows of commit c-1 from
+  // set (c-1)&1 into set c&1 (catch-up), then writes its own rows there, so a
+  // fetch of version c-1 never shares a table with commit c.
+  int32_t db;
+  float* mem1;
+  double* mem_ts1;
+  float* mail1;
+  double* mail_ts1;
+  int32_t* prev_nodes;  // [2][num_nodes] winners of the last commit of each parity
+  int32_t* prev_num;    // [2]
+  int64_t prev_max[2];  // host bound on prev_num[p] (launch sizing)
+  // winner stamps written by mspipe_memory_prep(i) into ring slot i % (k+1)
+  // (stamp[v] = i); they let commit i's GEMM kernel do the catch-up itself
+  int32_t* stamps;          // [k+1][num_nodes]
+  int64_t* stamp_iter;      // [k+1] host: iteration whose winners ring slot r holds (0 = none)
 };
+
+namespace mspipe {
+struct TableSet {
+  float* mem;
+  double* mem_ts;
+  float* mail;
+  double* mail_ts;
+};
+// the tables holding `version` (valid for version == committed, and committed - 1 when double-buffered)
+inline TableSet table_set(const mspipe_memory* st, int64_t version) {
+  if (st->db && (version & 1)) return {st->mem1, st->mem_ts1, st->mail1, st->mail_ts1};
+  return {st->mem, st->mem_ts, st->mail, st->mail_ts};
+}
+}  // namespace mspipe
 
 struct mspipe_gru {
   mspipe::GruDesc d;

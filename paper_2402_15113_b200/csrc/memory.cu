@@ -351,4 +351,49 @@ void launch_writeback(const int32_t* nodes, const int32_t* num, int64_t max_n,
            mem_ts, (float4*)mail, mail_ts, num_nodes);
 }
 
+// Double-buffered state, first half of commit c: the rows of commit c-1 (one
+// warp per node) from set (c-1)&1 into set c&1, and this commit's winner list
+// saved for commit c+1.  Stream order puts it before the commit's own writes.
+__global__ void __launch_bounds__(256) k_catchup(const int32_t* __restrict__ prev_nodes,
+                                                 const int32_t* __restrict__ prev_num,
+                                                 const float4* __restrict__ src_mem, const double* __restrict__ src_mem_ts,
+                                                 const float4* __restrict__ src_mail,
+                                                 const double* __restrict__ src_mail_ts, float4* __restrict__ dst_mem,
+                                                 double* __restrict__ dst_mem_ts, float4* __restrict__ dst_mail,
+                                                 double* __restrict__ dst_mail_ts, int32_t Qm, int32_t Qa,
+                                                 const int32_t* __restrict__ cur_nodes,
+                                                 const int32_t* __restrict__ cur_num, int32_t* __restrict__ save_nodes,
+                                                 int32_t* __restrict__ save_num) {
+  pdl_begin();
+  const int lane = threadIdx.x & 31;
+  const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
+  const int32_t np = __ldg(prev_num);
+  for (int64_t w = gtid >> 5; w < np; w += nthreads >> 5) {
+    const int32_t v = __ldg(prev_nodes + w);
+    for (int c = lane; c < Qm; c += 32) dst_mem[(int64_t)v * Qm + c] = __ldg(src_mem + (int64_t)v * Qm + c);
+    for (int c = lane; c < Qa; c += 32) dst_mail[(int64_t)v * Qa + c] = __ldg(src_mail + (int64_t)v * Qa + c);
+    if (lane == 0) {
+      dst_mem_ts[v] = __ldg(src_mem_ts + v);
+      dst_mail_ts[v] = __ldg(src_mail_ts + v);
+    }
+  }
+  const int32_t nc = cur_num ? __ldg(cur_num) : 0;
+  for (int64_t i = gtid; i < nc; i += nthreads) save_nodes[i] = __ldg(cur_nodes + i);
+  if (gtid == 0) *save_num = nc;
+}
+
+void launch_catchup(const int32_t* prev_nodes, const int32_t* prev_num, int64_t prev_max, const float* src_mem,
+                    const double* src_mem_ts, const float* src_mail, const double* src_mail_ts, float* dst_mem,
+                    double* dst_mem_ts, float* dst_mail, double* dst_mail_ts, int32_t mem_dim, int64_t mail_stride,
+                    const int32_t* cur_nodes, const int32_t* cur_num, int64_t cur_max, int32_t* save_nodes,
+                    int32_t* save_num, cudaStream_t s) {
+  const int threads = 256;
+  const int64_t work = prev_max * 32 > cur_max ? prev_max * 32 : cur_max;
+  launch_k(k_catchup, dim3(grid_for(work > 0 ? work : 1, threads, 4)), dim3(threads), 0, s, 1, prev_nodes, prev_num,
+           (const float4*)src_mem, src_mem_ts, (const float4*)src_mail, src_mail_ts, (float4*)dst_mem, dst_mem_ts,
+           (float4*)dst_mail, dst_mail_ts, mem_dim / 4, (int32_t)(mail_stride / 4), cur_nodes, cur_num, save_nodes,
+           save_num);
+}
+
 }  // namespace mspipe

@@ -46,6 +46,8 @@ struct PrepArgs {
   double* out_mem_ts;
   float4* out_mail;
   double* out_mail_ts;
+  int32_t* stamp;  // optional: stamp[winner node] = stamp_iter (double-buffered state)
+  int32_t stamp_iter;
 };
 
 // copy `nrows` table rows (ids held by lanes 0..nrows-1, -1 = zero row) of Q
@@ -79,6 +81,11 @@ __global__ void __launch_bounds__(kPrepThreads) k_prep(PrepArgs a) {
   if (blockIdx.x == 0) {
     block_dedup<kPrepThreads, kSmem>(a.src, a.dst, a.B, a.gscratch, sscratch, a.g.num_nodes, a.out_nodes,
                                      a.out_winner, a.out_num);
+    if (a.stamp) {
+      __syncthreads();  // out_nodes / out_num written by this block
+      const int32_t U = *a.out_num;
+      for (int32_t u = threadIdx.x; u < U; u += kPrepThreads) a.stamp[a.out_nodes[u]] = a.stamp_iter;
+    }
     return;
   }
   const int lane = threadIdx.x & 31;
@@ -130,11 +137,12 @@ cudaError_t launch_prep(const Tcsr& g, const int32_t* src, const int32_t* dst, c
                         int32_t* scratch, int32_t* out_nodes, int32_t* out_winner, int32_t* out_num,
                         const float* mem, const double* mem_ts, int32_t mem_dim, const float* mail,
                         const double* mail_ts, int64_t mail_stride, float* out_mem, double* out_mem_ts,
-                        float* out_mail, double* out_mail_ts, cudaStream_t s) {
+                        float* out_mail, double* out_mail_ts, cudaStream_t s, int32_t* stamp,
+                        int32_t stamp_iter) {
   PrepArgs a{g, src, dst, neg, ts, num_events, fanout, out_nbr, out_eid, out_ts, out_dt, out_cnt, out_sub,
              scratch, out_nodes, out_winner, out_num, (const float4*)mem, mem_ts, mem_dim / 4,
              (const float4*)mail, mail_ts, out_mail ? (int32_t)(mail_stride / 4) : 0, (float4*)out_mem, out_mem_ts,
-             (float4*)out_mail, out_mail ? out_mail_ts : nullptr};
+             (float4*)out_mail, out_mail ? out_mail_ts : nullptr, stamp, stamp_iter};
   int64_t blocks = (3 * num_events + kPrepWarps - 1) / kPrepWarps;
   const int64_t cap = (int64_t)num_sms() * 4;
   if (blocks > cap) blocks = cap;

@@ -41,10 +41,14 @@ class StageConfig:
     fetch_mail: bool = False        # also fetch mail rows of the subgraph nodes
     precision: int = _C.FP32_3XTF32  # tcgen05 3xTF32 (fp32 parity); _C.FP32_SIMT = CUDA-core baseline
     fused: bool | None = None  # mspipe_memory_prep + message_build/gru_apply (default: when supported)
+    double_buffer: bool | None = None  # two table sets (mspipe_memory_double_buffer); default: k >= 1
 
     def use_fused(self) -> bool:
         ok = self.precision == _C.FP32_3XTF32 and self.fanout <= 31 and self.batch <= 8192
         return ok if self.fused is None else (self.fused and ok)
+
+    def use_double_buffer(self) -> bool:
+        return self.k >= 1 if self.double_buffer is None else bool(self.double_buffer)
 
 
 def schedule_ops(nb: int, k: int, schedule: str = "exact"):
@@ -143,7 +147,8 @@ class MemoryStage(_TimedOps):
         self.cfg = cfg
         self.device = torch.device(device)
         self.tcsr = tcsr
-        self.memory = _C.MemoryHandle(cfg.num_nodes, cfg.mem_dim, cfg.edge_dim, cfg.k, self.device)
+        self.memory = _C.MemoryHandle(cfg.num_nodes, cfg.mem_dim, cfg.edge_dim, cfg.k, self.device,
+                                      double_buffer=cfg.use_double_buffer())
         self.gru = _C.GruHandle(cfg.mem_dim, cfg.edge_dim, cfg.time_dim, params, self.device, cfg.precision,
                                 max_events=cfg.batch)
         self.upd = _C.alloc_update(cfg.batch, cfg.mem_dim, self.memory.mail_stride, self.device)
@@ -247,8 +252,9 @@ class MemoryStage(_TimedOps):
                                     sl.mail_ts[:m] if sl.mail_ts is not None else None, self._mitigation(sl, x, n))
         self._ev("prep_end")
         self.versions[i] = sl.version
-        self._fetched = torch.cuda.Event()  # the state tables have been read for batch i
-        self._fetched.record()
+        if not self.memory.double_buffer:
+            self._fetched = torch.cuda.Event()  # the state tables have been read for batch i
+            self._fetched.record()
         self._ev("build")
         _C.message_build(self.gru, x["ts"], x["ef"], sl.mem, sl.mem_ts, cfg.fanout + 1, sl.dd["winner"][: 2 * n],
                          sl.dd["num"], sl.uts[: 2 * n], sl.umail[: 2 * n], sl.ws,
@@ -321,7 +327,11 @@ class MemoryStage(_TimedOps):
         side stream is joined before the first writeback of the group, which
         keeps fetch(t+k) between writeback(t-1) and writeback(t) — the exact
         staleness order of Eq. 2 — while overlapping the two halves of the
-        iteration (the paper's pipelining, moved onto the GPU)."""
+        iteration (the paper's pipelining, moved onto the GPU).
+        Double-buffered tables: fetch(t+k) reads version t-1 from the other
+        set than the one commit t writes, so the commit does not wait at all;
+        the join at the end of the group is what keeps that fetch ahead of
+        commit t+1 (which rewrites its set)."""
         overlap = (self.cfg.k >= 1) if overlap is None else overlap
         if not overlap:
             for op, i in ops:
@@ -331,6 +341,7 @@ class MemoryStage(_TimedOps):
         if getattr(self, "side", None) is None or self.side.device != main.device:
             self.side = torch.cuda.Stream(device=main.device)
         commits = {i for op, i in ops if op == "commit"}
+        db = self.memory.double_buffer
         forked = joined = False
         for op, i in ops:
             if op == "prep" and i not in commits:
@@ -344,12 +355,12 @@ class MemoryStage(_TimedOps):
             elif self.fused:
                 # the epilogue writes the tables: wait only for the side stream's
                 # fetch (not its message build, which overlaps this GEMM)
-                if forked:
+                if forked and not db:
                     main.wait_event(self._fetched)
                 self.apply_commit(i)
             else:
                 self.update(i)
-                if forked and not joined:
+                if forked and not joined and not db:
                     main.wait_stream(self.side)
                     joined = True
                 self.writeback(i)

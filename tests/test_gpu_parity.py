@@ -310,6 +310,67 @@ def test_bias_only_closed_form_on_gpu(dev):
     assert ok, err
 
 
+@pytest.mark.parametrize("k,schedule,precision,fused", [(1, "exact", _C.FP32_3XTF32, True),
+                                                         (2, "exact", _C.FP32_3XTF32, True),
+                                                         (2, "grouped", _C.FP32_3XTF32, True),
+                                                         (1, "exact", _C.FP32_3XTF32, False),
+                                                         (3, "exact", _C.FP32_SIMT, False)])
+def test_double_buffered_state_equals_single(dev, k, schedule, precision, fused):
+    """Two table sets (commit t and fetch t+k on different tables, no wait
+    between them) give bit-identical state and fetched snapshots to one set."""
+    w = make_workload("lastfm", seed=4, num_events=40_000)  # hot nodes: rows rewritten every batch
+    cfg = w["cfg"]
+    res = []
+    for db in (False, True):
+        sc = StageConfig(cfg.num_nodes, cfg.mem_dim, cfg.edge_dim, cfg.time_dim, cfg.fanout, cfg.batch, k,
+                         schedule=schedule, fetch_mail=True, precision=precision, fused=fused, double_buffer=db)
+        g = build_tcsr(cfg.num_nodes, w["src"], w["dst"], w["ts"], dev)
+        st = MemoryStage(sc, w["params"], g, dev)
+        assert st.memory.double_buffer == db
+        t = {kk: _t(w[kk], dev) for kk in ("src", "dst", "ts", "neg", "ef")}
+        st.bind_resident(t["src"], t["dst"], t["ts"], t["neg"], t["ef"])
+        snaps = []
+        for ops in st.step_ops():
+            st.run_ops(ops)
+            sl = st._slot(ops[-1][1])
+            snaps.append(sl.mem_ts.cpu().numpy().copy())
+        torch.cuda.synchronize()
+        _C.check()
+        res.append(({kk: getattr(st.memory, kk).cpu().numpy() for kk in ("mem", "mem_ts", "mail", "mail_ts")},
+                    snaps, dict(st.versions)))
+    (a, sa, va), (b, sb, vb) = res
+    assert va == vb
+    for kk in a:
+        assert np.array_equal(a[kk], b[kk]), kk
+    assert all(np.array_equal(x, y) for x, y in zip(sa, sb))
+
+
+def test_double_buffer_abi(dev):
+    cfg = CONFIGS["tiny"]
+    h = _C.MemoryHandle(cfg.num_nodes, 100, 172, 1, dev)
+    t1 = [torch.zeros_like(x) for x in (h.mem, h.mem_ts, h.mail, h.mail_ts)]
+    upd = _C.alloc_update(200, 100, h.mail_stride, dev)
+    _C.memory_writeback(h, 1, upd)
+    with pytest.raises(_C.MspipeError) as e:  # only before the first commit
+        _C._ck(_C.lib().mspipe_memory_double_buffer(h.h, *(_C.ptr(x) for x in t1)), "double_buffer")
+    assert e.value.status == _C.EORDER
+    h2 = _C.MemoryHandle(cfg.num_nodes, 100, 172, 1, dev, double_buffer=True)
+    with pytest.raises(_C.MspipeError) as e:
+        _C._ck(_C.lib().mspipe_memory_double_buffer(h2.h, *(_C.ptr(x) for x in t1)), "double_buffer")
+    assert e.value.status == _C.EINVAL
+    # version bookkeeping: set 0 holds versions 0, 2, ...; version committed - 1 stays readable
+    assert h2.tables(0) is h2._sets[0]
+    _C.memory_writeback(h2, 1, upd)
+    assert h2.tables() is h2._sets[1] and h2.tables(0) is h2._sets[0]
+    with pytest.raises(_C.MspipeError) as e:
+        h2.tables(2)
+    assert e.value.status == _C.EINVAL
+    hw = _C.MemoryHandle(cfg.num_nodes, 100, 172, 1, dev, rank=0, world=2)
+    with pytest.raises(_C.MspipeError) as e:
+        _C._ck(_C.lib().mspipe_memory_double_buffer(hw.h, *(_C.ptr(x) for x in t1)), "double_buffer")
+    assert e.value.status == _C.EUNSUPPORTED
+
+
 # ------------------------------------------------------------------ ABI contract
 def test_abi_staleness_and_order_errors(dev):
     cfg = CONFIGS["tiny"]
@@ -368,6 +429,7 @@ def test_cuda_graph_replay_equals_eager(dev, kind):
             with torch.cuda.stream(s):
                 for gr in graphs:
                     gr.replay()
+            st.memory.set_committed(len(graphs))  # host bookkeeping follows the replayed commits
         else:
             st.run()
         torch.cuda.synchronize()
