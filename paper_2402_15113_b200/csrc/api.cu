@@ -26,6 +26,11 @@ mspipe_status cuda_status(cudaError_t e, const char* what) {
   return fail(MSPIPE_ECUDA, "%s: %s", what, cudaGetErrorString(e));
 }
 
+int env_int(const char* name, int def) {
+  const char* e = getenv(name);
+  return (e && *e) ? atoi(e) : def;
+}
+
 bool pdl_enabled() {
   static int on = -1;
   if (on < 0) {
@@ -177,6 +182,7 @@ static mspipe_status db_mirror(mspipe_memory* st) {
   if (e == cudaSuccess) e = cudaMemset(st->stamps, 0, sizeof(int32_t) * (size_t)(st->k + 1) * N);
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   st->prev_max[0] = st->prev_max[1] = 0;
+  st->caught_up = 0;
   for (int r = 0; r <= st->k; ++r) st->stamp_iter[r] = 0;
   return cuda_status(e, "memory double buffer: mirror");
 }
@@ -222,13 +228,30 @@ mspipe_status mspipe_memory_tables(const mspipe_memory* st, int64_t version, flo
   return MSPIPE_OK;
 }
 
-// double-buffered commit c, first half (see k_catchup)
+// where the catch-up of a double-buffered commit runs: 0 = its own kernel
+// before the commit, 1 = inside the commit's GEMM kernel, 2 = inside the
+// mspipe_memory_prep that precedes the commit (falling back to 1, then 0,
+// when the winners of the commit are not stamped yet)
+static int catchup_mode() { return env_int("MSPIPE_CATCHUP", 2); }
+
+// the catch-up rows of commit c as a CatchUp (stamps of commit c's winners assumed written)
+static CatchUp catchup_args(const mspipe_memory* st, int64_t c) {
+  const int64_t N = st->num_nodes;
+  const int q = (int)((c - 1) & 1);
+  const TableSet o = table_set(st, c - 1), n = table_set(st, c);
+  return CatchUp{st->prev_nodes + q * N, st->prev_num + q, o.mem, o.mem_ts, o.mail, o.mail_ts, n.mem, n.mem_ts,
+                 n.mail, n.mail_ts, st->stamps + (c % (st->k + 1)) * N, (int32_t)c};
+}
+
+// double-buffered commit c, first half (see k_catchup); copy_rows = false when
+// a prep already enqueued them: then only this commit's winner list is saved
 static cudaError_t db_catchup(mspipe_memory* st, int64_t c, const int32_t* nodes, const int32_t* num, int64_t max_n,
-                              cudaStream_t s) {
+                              cudaStream_t s, bool copy_rows = true) {
   const int p = (int)(c & 1), q = p ^ 1;
   const int64_t N = st->num_nodes;
   const TableSet from = table_set(st, c - 1), to = table_set(st, c);
-  launch_catchup(st->prev_nodes + q * N, st->prev_num + q, st->prev_max[q], from.mem, from.mem_ts, from.mail,
+  launch_catchup(st->prev_nodes + q * N, copy_rows ? st->prev_num + q : nullptr, copy_rows ? st->prev_max[q] : 0,
+                 from.mem, from.mem_ts, from.mail,
                  from.mail_ts, to.mem, to.mem_ts, to.mail, to.mail_ts, st->mem_dim, st->mail_stride,
                  max_n > 0 ? nodes : nullptr, max_n > 0 ? num : nullptr, max_n, st->prev_nodes + p * N,
                  st->prev_num + p, s);
@@ -442,7 +465,8 @@ mspipe_status mspipe_memory_writeback(mspipe_memory* st, int64_t commit_version,
   if (max_n > 0 && (!nodes || !num_unique || !new_mem || !new_ts || !new_mail))
     return fail(MSPIPE_EINVAL, "memory_writeback: null input");
   if (st->db) {
-    cudaError_t e = db_catchup(st, commit_version, nodes, num_unique, max_n, (cudaStream_t)stream);
+    cudaError_t e = db_catchup(st, commit_version, nodes, num_unique, max_n, (cudaStream_t)stream,
+                               st->caught_up != commit_version);
     if (e != cudaSuccess) return cuda_status(e, "memory_writeback: catch-up");
   }
   const TableSet t = table_set(st, commit_version);
@@ -481,14 +505,22 @@ mspipe_status mspipe_memory_prep(mspipe_memory* st, const mspipe_tcsr* g, int64_
     if (!src || !dst || !neg || !ts || !out_nbr || !out_eid || !out_ts || !out_dt || !out_cnt || !out_sub_ids ||
         !out_nodes || !out_winner || !out_num_unique || !out_mem || !out_mem_ts)
       return fail(MSPIPE_EINVAL, "memory_prep: null input/output");
+    // double-buffered: this launch may also carry the catch-up of the next
+    // commit c (its winners already stamped, or stamped by this very launch
+    // when c == iteration, k = 0: the commit then follows in stream order)
+    const int64_t c = st->committed + 1;
+    const bool cu = st->db && catchup_mode() == 2 && st->caught_up != c &&
+                    (st->stamp_iter[c % (st->k + 1)] == c || c == iteration);
+    const CatchUp cua = cu ? catchup_args(st, c) : CatchUp{};
     cudaError_t e = launch_prep(to_tcsr(g), src, dst, neg, ts, num_events, fanout, out_nbr, out_eid, out_ts, out_dt,
                                 out_cnt, out_sub_ids, st->scratch, out_nodes, out_winner, out_num_unique, t.mem,
                                 t.mem_ts, st->mem_dim, t.mail, t.mail_ts, st->mail_stride, out_mem,
                                 out_mem_ts, out_mail, out_mail_ts, s,
                                 st->db ? st->stamps + (iteration % (st->k + 1)) * st->num_nodes : nullptr,
-                                (int32_t)iteration);
+                                (int32_t)iteration, cu ? &cua : nullptr);
     if (e != cudaSuccess) return cuda_status(e, "memory_prep: launch");
     if (st->db) st->stamp_iter[iteration % (st->k + 1)] = iteration;
+    if (cu) st->caught_up = c;
   } else if (out_num_unique) {
     cudaError_t e = cudaMemsetAsync(out_num_unique, 0, sizeof(int32_t), s);
     if (e != cudaSuccess) return cuda_status(e, "memory_prep");
@@ -583,28 +615,22 @@ mspipe_status mspipe_gru_apply_commit(const mspipe_gru* gru, mspipe_memory* st,
   // itself when mspipe_memory_prep stamped this batch's winners; otherwise a
   // separate k_catchup launch goes first
   const int64_t ring = st->db ? commit_version % (st->k + 1) : 0;
-  const bool fused_catchup = st->db && num_events > 0 && st->stamp_iter[ring] == commit_version;
-  if (st->db && !fused_catchup) {
-    cudaError_t e = db_catchup(st, commit_version, nodes, num_unique, max_n, (cudaStream_t)stream);
+  const bool done = st->db && st->caught_up == commit_version;  // enqueued by a prep
+  const bool fused_catchup = st->db && !done && num_events > 0 && catchup_mode() >= 1 &&
+                             st->stamp_iter[ring] == commit_version;
+  if (st->db && (num_events == 0 || (!done && !fused_catchup))) {
+    cudaError_t e = db_catchup(st, commit_version, nodes, num_unique, max_n, (cudaStream_t)stream, !done);
     if (e != cudaSuccess) return cuda_status(e, "gru_apply_commit: catch-up");
   }
   if (num_events > 0) {
     const TableSet t = table_set(st, commit_version);
     GruCommit c{nodes, t.mem, t.mem_ts, t.mail, t.mail_ts, new_ts, new_mail, st->num_nodes, st->mail_stride};
-    if (fused_catchup) {
-      const int p = (int)(commit_version & 1), q = p ^ 1;
-      const TableSet o = table_set(st, commit_version - 1);
+    if (done || fused_catchup) {  // the kernel saves this commit's winner list
+      const int p = (int)(commit_version & 1);
       c.save_nodes = st->prev_nodes + p * st->num_nodes;
       c.save_num = st->prev_num + p;
-      c.prev_nodes = st->prev_nodes + q * st->num_nodes;
-      c.prev_num = st->prev_num + q;
-      c.old_mem = o.mem;
-      c.old_mem_ts = o.mem_ts;
-      c.old_mail = o.mail;
-      c.old_mail_ts = o.mail_ts;
-      c.stamp = st->stamps + ring * st->num_nodes;
-      c.iter = (int32_t)commit_version;
     }
+    if (fused_catchup) c.cu = catchup_args(st, commit_version);
     cudaError_t e = launch_gru_tc(gru->d, gru->wtc, (float*)workspace, nullptr, num_events, nullptr, snap_mem, nullptr,
                                   snap_step, snap_h, winner, num_unique, out_mem, nullptr, nullptr, 0,
                                   (cudaStream_t)stream, kGruGemm, &c);

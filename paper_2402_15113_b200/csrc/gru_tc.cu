@@ -293,33 +293,18 @@ struct TcArgs {
   // double-buffered state (GruCommit)
   int32_t* save_nodes;
   int32_t* save_num;
-  const int32_t* prev_nodes;
-  const int32_t* prev_num;
-  const float4* old_mem;
-  const double* old_mem_ts;
-  const float4* old_mail;
-  const double* old_mail_ts;
-  const int32_t* stamp;
-  int32_t iter;
+  CatchUp cu;
 };
 
 // Double-buffered commit: copy the previous commit's rows (old set -> this
 // commit's set) except this commit's own winners, which the epilogue writes.
 // Warp `wq` of `nw` participating warps; one warp per row.
 __device__ __forceinline__ void catch_up(const TcArgs& a, int64_t wq, int64_t nw, int lane) {
-  const int32_t np = __ldg(a.prev_num);
-  const int Qm = a.d.M / 4, Qa = (int)(a.mail_stride / 4);
-  float4* mem = reinterpret_cast<float4*>(a.commit_mem);
-  float4* mail = reinterpret_cast<float4*>(a.commit_mail);
+  const int32_t np = __ldg(a.cu.prev_num);
+  const int32_t Qm = a.d.M / 4, Qa = (int32_t)(a.mail_stride / 4);
   for (int64_t r = wq; r < np; r += nw) {
-    const int32_t v = __ldg(a.prev_nodes + r);
-    if (__ldg(a.stamp + v) == a.iter) continue;
-    for (int c = lane; c < Qm; c += 32) mem[(int64_t)v * Qm + c] = __ldg(a.old_mem + (int64_t)v * Qm + c);
-    for (int c = lane; c < Qa; c += 32) mail[(int64_t)v * Qa + c] = __ldg(a.old_mail + (int64_t)v * Qa + c);
-    if (lane == 0) {
-      a.commit_mem_ts[v] = __ldg(a.old_mem_ts + v);
-      a.commit_mail_ts[v] = __ldg(a.old_mail_ts + v);
-    }
+    const int32_t v = __ldg(a.cu.prev_nodes + r);
+    if (__ldg(a.cu.stamp + v) != a.cu.iter) catchup_row(a.cu, v, Qm, Qa, lane);
   }
 }
 
@@ -446,7 +431,7 @@ __global__ void __launch_bounds__(tc::kThreads, 1) k_gru_tc(TcArgs a) {
   const int64_t n_cta = (int64_t)mt_act * gridDim.y * S;
   if (a.save_num && cta_q == 0 && threadIdx.x == 0) *a.save_num = U;
   if (m0 >= U) {  // uniform across the cluster (same blockIdx.z)
-    if (a.stamp && mt < mt_act) catch_up(a, cta_q * (kThreads / 32) + (threadIdx.x >> 5), n_cta * (kThreads / 32),
+    if (a.cu.stamp && mt < mt_act) catch_up(a, cta_q * (kThreads / 32) + (threadIdx.x >> 5), n_cta * (kThreads / 32),
                                          threadIdx.x & 31);
     return;
   }
@@ -532,7 +517,7 @@ __global__ void __launch_bounds__(tc::kThreads, 1) k_gru_tc(TcArgs a) {
         if (a.save_nodes && jt == 0 && node >= 0) a.save_nodes[u] = node;
       }
     }
-    if (a.stamp) catch_up(a, cta_q * 2 + (warp - 2), n_cta * 2, lane);
+    if (a.cu.stamp) catch_up(a, cta_q * 2 + (warp - 2), n_cta * 2, lane);
   }
   __syncwarp();
 
@@ -687,21 +672,14 @@ cudaError_t launch_gru_tc(const GruDesc& d, const float* wtc, float* xbuf, const
     a.mail_stride = commit->mail_stride;
     a.save_nodes = commit->save_nodes;
     a.save_num = commit->save_num;
-    a.prev_nodes = commit->prev_nodes;
-    a.prev_num = commit->prev_num;
-    a.old_mem = reinterpret_cast<const float4*>(commit->old_mem);
-    a.old_mem_ts = commit->old_mem_ts;
-    a.old_mail = reinterpret_cast<const float4*>(commit->old_mail);
-    a.old_mail_ts = commit->old_mail_ts;
-    a.stamp = commit->stamp;
-    a.iter = commit->iter;
+    a.cu = commit->cu;
   }
   const int64_t max_rows = 2 * num_events;
   const int64_t mtiles = (max_rows + tc::kM - 1) / tc::kM;
   if (parts & kGruBuild) {
     const int64_t warps = mtiles * (d.Kpad / tc::kKC) * tc::kM;
     int64_t blocks = (warps * 32 + 255) / 256;
-    const int64_t cap = (int64_t)num_sms() * 8;
+    const int64_t cap = (int64_t)num_sms() * env_int("MSPIPE_BUILD_BPS", 8);
     if (blocks > cap) blocks = cap;
     cudaError_t e = launch_k(k_build_x, dim3((unsigned)blocks), dim3(256), 0, s, 1, a);
     if (e != cudaSuccess) return e;

@@ -41,7 +41,9 @@ __device__ __forceinline__ void pdl_begin() {
   asm volatile("griddepcontrol.wait;\n" ::: "memory");
 }
 
-bool pdl_enabled();  // env MSPIPE_PDL=0 disables (A/B experiments)
+bool pdl_enabled();  // env MSPIPE_PDL=1 enables (A/B experiments)
+// integer knob from the environment (experiments only; defaults are the tuned values)
+int env_int(const char* name, int def);
 
 // cudaLaunchKernelEx with the PDL attribute (+ an optional (cx,1,1) cluster).
 template <typename... KArgs, typename... Args>
@@ -166,6 +168,51 @@ size_t gru_tc_xbuf_floats(const GruDesc& d, int64_t max_events);
 void launch_gru_pack_tc(const float* w_ih, const float* w_hh, const float* b_ih, const float* b_hh,
                         const GruDesc& d, float* wtc, float* bias, cudaStream_t s);
 enum { kGruBuild = 1, kGruGemm = 2 };
+// double-buffered state: copy the rows of the previous commit (prev_nodes,
+// from set `old_*`) into the next commit's set (`new_*`), skipping the nodes
+// with stamp[v] == iter (that commit's own winners, which it writes itself)
+struct CatchUp {
+  const int32_t* prev_nodes;
+  const int32_t* prev_num;
+  const float* old_mem;
+  const double* old_mem_ts;
+  const float* old_mail;
+  const double* old_mail_ts;
+  float* new_mem;
+  double* new_mem_ts;
+  float* new_mail;
+  double* new_mail_ts;
+  const int32_t* stamp;
+  int32_t iter;
+};
+
+// one warp copies row v of every table (4 x 16 B loads in flight per lane)
+__device__ __forceinline__ void catchup_row(const CatchUp& c, int32_t v, int32_t Qm, int32_t Qa, int lane) {
+  const float4* om = reinterpret_cast<const float4*>(c.old_mem) + (int64_t)v * Qm;
+  const float4* oa = reinterpret_cast<const float4*>(c.old_mail) + (int64_t)v * Qa;
+  float4* nm = reinterpret_cast<float4*>(c.new_mem) + (int64_t)v * Qm;
+  float4* na = reinterpret_cast<float4*>(c.new_mail) + (int64_t)v * Qa;
+  const int total = Qm + Qa;
+  for (int base = 0; base < total; base += 128) {
+    float4 x[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int q = base + u * 32 + lane;
+      if (q < total) x[u] = q < Qm ? __ldg(om + q) : __ldg(oa + (q - Qm));
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int q = base + u * 32 + lane;
+      if (q < Qm) nm[q] = x[u];
+      else if (q < total) na[q - Qm] = x[u];
+    }
+  }
+  if (lane == 0) {
+    c.new_mem_ts[v] = __ldg(c.old_mem_ts + v);
+    c.new_mail_ts[v] = __ldg(c.old_mail_ts + v);
+  }
+}
+
 struct GruCommit {  // fused A7 in the GEMM epilogue
   const int32_t* nodes;
   float* mem;
@@ -182,14 +229,7 @@ struct GruCommit {  // fused A7 in the GEMM epilogue
   // (this commit's winners, stamped by k_prep)
   int32_t* save_nodes;
   int32_t* save_num;
-  const int32_t* prev_nodes;
-  const int32_t* prev_num;
-  const float* old_mem;
-  const double* old_mem_ts;
-  const float* old_mail;
-  const double* old_mail_ts;
-  const int32_t* stamp;
-  int32_t iter;
+  CatchUp cu;  // cu.stamp == nullptr: no catch-up in this kernel
 };
 cudaError_t launch_gru_tc(const GruDesc& d, const float* wtc, float* xbuf, const double* ts, int64_t num_events,
                           const float* edge_feat, const float* snap_mem, const double* snap_mem_ts,
@@ -205,7 +245,7 @@ cudaError_t launch_prep(const Tcsr& g, const int32_t* src, const int32_t* dst, c
                         const float* mem, const double* mem_ts, int32_t mem_dim, const float* mail,
                         const double* mail_ts, int64_t mail_stride, float* out_mem, double* out_mem_ts,
                         float* out_mail, double* out_mail_ts, cudaStream_t s, int32_t* stamp = nullptr,
-                        int32_t stamp_iter = 0);
+                        int32_t stamp_iter = 0, const struct CatchUp* cu = nullptr);
 
 }  // namespace mspipe
 
@@ -275,6 +315,7 @@ struct mspipe_memory {
   // (stamp[v] = i); they let commit i's GEMM kernel do the catch-up itself
   int32_t* stamps;          // [k+1][num_nodes]
   int64_t* stamp_iter;      // [k+1] host: iteration whose winners ring slot r holds (0 = none)
+  int64_t caught_up;        // host: the commit whose catch-up a prep has already enqueued (0 = none)
 };
 
 namespace mspipe {

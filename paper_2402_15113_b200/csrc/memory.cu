@@ -368,7 +368,7 @@ __global__ void __launch_bounds__(256) k_catchup(const int32_t* __restrict__ pre
   const int lane = threadIdx.x & 31;
   const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
-  const int32_t np = __ldg(prev_num);
+  const int32_t np = prev_num ? __ldg(prev_num) : 0;  // NULL: only save this commit's list
   for (int64_t w = gtid >> 5; w < np; w += nthreads >> 5) {
     const int32_t v = __ldg(prev_nodes + w);
     for (int c = lane; c < Qm; c += 32) dst_mem[(int64_t)v * Qm + c] = __ldg(src_mem + (int64_t)v * Qm + c);

@@ -48,6 +48,8 @@ struct PrepArgs {
   double* out_mail_ts;
   int32_t* stamp;  // optional: stamp[winner node] = stamp_iter (double-buffered state)
   int32_t stamp_iter;
+  CatchUp cu;      // optional (cu.stamp != nullptr): the next commit's catch-up rows
+  int32_t Qcu;     // float4 per mail row of the state tables (catch-up)
 };
 
 // copy `nrows` table rows (ids held by lanes 0..nrows-1, -1 = zero row) of Q
@@ -92,7 +94,8 @@ __global__ void __launch_bounds__(kPrepThreads) k_prep(PrepArgs a) {
   const int64_t R = 3 * a.B;
   const int F = a.F, F1 = a.F + 1;
   const int64_t nwarps = (int64_t)(gridDim.x - 1) * kPrepWarps;
-  for (int64_t r = (int64_t)(blockIdx.x - 1) * kPrepWarps + (threadIdx.x >> 5); r < R; r += nwarps) {
+  const int64_t wid = (int64_t)(blockIdx.x - 1) * kPrepWarps + (threadIdx.x >> 5);
+  for (int64_t r = wid; r < R; r += nwarps) {
     const int64_t role = r / a.B, ev = r - role * a.B;
     const int32_t v = role == 0 ? __ldg(a.src + ev) : (role == 1 ? __ldg(a.dst + ev) : __ldg(a.neg + ev));
     const double tq = __ldg(a.ts + ev);
@@ -129,6 +132,14 @@ __global__ void __launch_bounds__(kPrepThreads) k_prep(PrepArgs a) {
     warp_gather_rows(a.mem, a.Qm, gid, F1, a.out_mem, r * F1, lane);
     if (a.Qa > 0) warp_gather_rows(a.mail, a.Qa, gid, F1, a.out_mail, r * F1, lane);
   }
+  if (a.cu.stamp) {  // double-buffered: rows of the previous commit, after this warp's roots
+    const int32_t np = __ldg(a.cu.prev_num);
+    const int64_t r0 = wid + (R - wid + nwarps - 1) / nwarps * nwarps;  // this warp's first item >= R
+    for (int64_t r = r0; r < R + np; r += nwarps) {
+      const int32_t v = __ldg(a.cu.prev_nodes + (r - R));
+      if (__ldg(a.cu.stamp + v) != a.cu.iter) catchup_row(a.cu, v, a.Qm, a.Qcu, lane);
+    }
+  }
 }
 
 cudaError_t launch_prep(const Tcsr& g, const int32_t* src, const int32_t* dst, const int32_t* neg,
@@ -138,16 +149,18 @@ cudaError_t launch_prep(const Tcsr& g, const int32_t* src, const int32_t* dst, c
                         const float* mem, const double* mem_ts, int32_t mem_dim, const float* mail,
                         const double* mail_ts, int64_t mail_stride, float* out_mem, double* out_mem_ts,
                         float* out_mail, double* out_mail_ts, cudaStream_t s, int32_t* stamp,
-                        int32_t stamp_iter) {
+                        int32_t stamp_iter, const CatchUp* cu) {
   PrepArgs a{g, src, dst, neg, ts, num_events, fanout, out_nbr, out_eid, out_ts, out_dt, out_cnt, out_sub,
              scratch, out_nodes, out_winner, out_num, (const float4*)mem, mem_ts, mem_dim / 4,
              (const float4*)mail, mail_ts, out_mail ? (int32_t)(mail_stride / 4) : 0, (float4*)out_mem, out_mem_ts,
-             (float4*)out_mail, out_mail ? out_mail_ts : nullptr, stamp, stamp_iter};
+             (float4*)out_mail, out_mail ? out_mail_ts : nullptr, stamp, stamp_iter, CatchUp{},
+             (int32_t)(mail_stride / 4)};
+  if (cu) a.cu = *cu;
   int64_t blocks = (3 * num_events + kPrepWarps - 1) / kPrepWarps;
-  const int64_t cap = (int64_t)num_sms() * 4;
+  const int64_t cap = (int64_t)num_sms() * env_int("MSPIPE_PREP_BPS", 4);
   if (blocks > cap) blocks = cap;
   blocks += 1;  // block 0: dedup
-  if (g.num_nodes <= kDedupSmemNodes) {
+  if (g.num_nodes <= kDedupSmemNodes && env_int("MSPIPE_PREP_SMEM", 1)) {
     static bool attr = false;
     if (!attr) {
       cudaError_t e = cudaFuncSetAttribute(k_prep<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
