@@ -184,7 +184,7 @@ def run_mspipe(args):
         dist.init_process_group("nccl")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    w = make_workload(args.config, seed=args.seed)
+    w = make_workload(args.config, seed=args.seed, num_events=args.events)
     cfg = w["cfg"]
     k = cfg.staleness_k if args.k is None else args.k
     mit = None
@@ -336,6 +336,16 @@ def run_mspipe(args):
     roof["instrumented_ms_per_step"] = float(np.mean(step_ms_instr)) if step_ms_instr else None
     roof["alg_bytes_per_launch"] = {kk: alg[kk] for kk in op_mean if kk in alg}
     roof["gru_flops_per_launch"] = alg["update_flops"]
+    gather_op = "prep" if "prep" in op_mean else ("fetch" if "fetch" in op_mean else None)
+    if gather_op and dom != gather_op:
+        # the gather/scatter kernel against HBM (north star: >= 60 % of the HBM roofline)
+        ach_g = alg[gather_op] / (op_mean[gather_op] / 1e3) / 1e9
+        roof_gather = {"kernel": "k_prep (A1 sampler + A2 dedup + A3 gather)" if gather_op == "prep"
+                       else "k_fetch_gather", "bound": "hbm", "achieved": ach_g, "peak": peaks["hbm_gbs"],
+                       "unit": "GB/s", "frac": ach_g / peaks["hbm_gbs"], "bytes_per_launch": alg[gather_op],
+                       "traffic": _ncu_traffic(args.config, gather_op)}
+    else:
+        roof_gather = None
     out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": K, "warmup": W,
            "ms_per_step": tot_ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
            "dtype": "f32", "data": "synthetic",
@@ -348,7 +358,7 @@ def run_mspipe(args):
                       "parallelism": ("single" if ws == 1 else
                                       f"shard{ws}: node-id-sharded memory, NCCL all-to-all fetch + write-back, "
                                       f"global batch {G * cfg.batch}" if sharded else f"replicas{ws}")},
-           "roofline": roof, "gpu_launches": _launches(st.step_ops(), timed_batches, bool(mit),
+           "roofline": roof, "roofline_gather": roof_gather, "gpu_launches": _launches(st.step_ops(), timed_batches, bool(mit),
                                                        getattr(st, "fused", False), sharded), "clocks": clocks}
     if args.profile:
         if rank == 0:
@@ -425,7 +435,7 @@ def run_reference(args):
     import oracle
     from paper_2402_15113_b200.graph import gamma_quantile
     from synth import make_workload
-    w = make_workload(args.config, seed=args.seed)
+    w = make_workload(args.config, seed=args.seed, num_events=args.events)
     cfg = w["cfg"]
     k = cfg.staleness_k if args.k is None else args.k
     mit = None
@@ -481,6 +491,8 @@ def main():
     ap.add_argument("--l2", default="flush", choices=["flush", "warm"],
                     help="flush: 256 MiB write between timed steps (default); warm: back-to-back steps")
     ap.add_argument("--cpu-events", type=int, default=157_474)
+    ap.add_argument("--events", type=int, default=None,
+                    help="first N events of the config's stream (default: all; GDELT's 191M needs a cap)")
     ap.add_argument("--profile", action="store_true", help="short run for ncu: no flush/e2e/cpu")
     args = ap.parse_args()
     if args.warmup < 3 and not args.profile:
