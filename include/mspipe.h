@@ -384,6 +384,43 @@ MSPIPE_API mspipe_status mspipe_shard_exchange(mspipe_memory* st, int32_t kind, 
 MSPIPE_API mspipe_status mspipe_shard_loopback(mspipe_memory* const* ranks, int32_t world, int32_t kind,
                                     void* stream);
 
+/* ------------------------------------------------------------------------
+ * F1 — minimal-staleness planner (MSPipe §3.2; Alg. 1)
+ * ------------------------------------------------------------------------
+ * Host functions (no GPU work).  Stages j = 1..5 of an iteration: sample,
+ * fetch feature, fetch memory, train, update memory; tau[j-1] = profiled
+ * duration of stage j (any time unit, >= 0).  Iterations i = 1..num_iters.
+ * Paper staleness k_i >= 1 (k = 1: no staleness): iteration i fetches
+ * memory updated through iteration i - k_i.
+ *
+ * mspipe_plan_timeline: Eq. 3-4.  out_b / out_e [num_iters][5]
+ *   (row i-1, column j-1) = b_i^(j), e_i^(j).  k NULL: Eq. 3 as printed; else
+ *   k[i-1] = k_i >= 1 adds the Alg. 1 gate b_i^(3) >= e_{i-k_i}^(5) (C1;
+ *   i - k_i < 1: no gate).  Errors: MSPIPE_EINVAL (tau < 0, k_i < 1, NULL).
+ * mspipe_plan_min_staleness: the optimisation of P:L300-L307, iteration by
+ *   iteration: least k_i in [1, min(i, k_max)) with e_{i-k_i}^(5) <= b_i^(4) -
+ *   tau^(3), b_i^(4) from the schedule with iteration i's gate relaxed (C2);
+ *   the chosen k_i is then applied as the gate (C1).  Iterations i <= k_max
+ *   with no such k are warm-up: k_i = i (no gate).  Later ones with
+ *   none are infeasible: k_i = k_max - 1 and *out_infeasible_iter = the first
+ *   such i (0 if none; the binding constraint is C2).  out_k [num_iters].
+ * mspipe_stale_histogram: the C3 statistic (Fig. `fig:overlap`) on the
+ *   GPU.  For every batch i (events [(i-1)B, iB)) and every distinct src/dst
+ *   node v of the batch, d = i - (batch of v's previous event), or 0 if v has
+ *   none; out_hist [max_d + 2] (device, int64, overwritten) counts d = 0,
+ *   1..max_d, and > max_d in its last bin.  Under staleness k the stale share
+ *   is sum_{1 <= d <= k-1} hist[d] / sum hist (reading F6); k_max is chosen
+ *   so that it stays <= 50 % (C3).  g must be the T-CSR of the same stream
+ *   (rows in stream order).  Errors: MSPIPE_EINVAL (bad T-CSR, batch < 1,
+ *   max_d outside 1..4096). */
+MSPIPE_API mspipe_status mspipe_plan_timeline(const double* tau, int64_t num_iters, const int32_t* k,
+                                   double* out_b, double* out_e);
+MSPIPE_API mspipe_status mspipe_plan_min_staleness(const double* tau, int64_t num_iters, int32_t k_max,
+                                        int32_t* out_k, int64_t* out_infeasible_iter);
+MSPIPE_API mspipe_status mspipe_stale_histogram(const mspipe_tcsr* g, const int32_t* src, const int32_t* dst,
+                                     int64_t num_events, int64_t batch, int32_t max_d, int64_t* out_hist,
+                                     void* stream);
+
 /* Utility (timing): record `event` (a cudaEvent_t) on `stream` with
  * cudaEventRecordExternal, so that under stream capture it becomes an
  * event-record node of the graph and can still be used for elapsed-time

@@ -53,7 +53,7 @@ def lib():
         L.orc_snapshot_version.argtypes = [i64, i32, i32]
         L.orc_snapshot_version.restype = i64
         L.orc_run_stream.argtypes = [i64, i64, P, P, P, P, i32, i32, i32, P, P, P, P, P, P, i64,
-                                     i32, i32, i32, f32, f64, i32, i32, P, P, P, P, i64, P, P, i32]
+                                     i32, i32, i32, f32, f64, i32, i32, P, P, P, P, i64, P, P, i32, P]
         L.orc_run_stream.restype = i64
         L.orc_delta_t_population.argtypes = [i64, i64, P, P, P, P]
         L.orc_delta_t_population.restype = i64
@@ -191,10 +191,13 @@ def new_state(num_nodes, mem_dim, edge_dim):
 
 
 def run_stream(num_nodes, src, dst, ts, ef, params, batch, k, schedule="exact", mitigation=None,
-               fanout=10, state=None, max_batches=-1, neg=None):
+               fanout=10, state=None, max_batches=-1, neg=None, plan=None):
     """C.2 O1-O8 over the stream; returns (final state, per-batch versions).
     With `neg`, every batch also runs A1 on its 3B roots and gathers the
-    snapshot rows of the subgraph (the whole per-batch path, for timing)."""
+    snapshot rows of the subgraph (the whole per-batch path, for timing).
+    plan (row F1): per-iteration paper staleness k_i (v(i) = max(0, i - k_i));
+    k must then be >= max_i (i - v(i)) - 1 (copies kept)."""
+    planc = None if plan is None else _c(plan, np.int32)
     negc = None if neg is None else _c(neg, np.int32)
     src, dst, ts = _c(src, np.int32), _c(dst, np.int32), _c(ts, np.float64)
     ef = _c(ef, np.float32)
@@ -215,7 +218,7 @@ def run_stream(num_nodes, src, dst, ts, ef, params, batch, k, schedule="exact", 
         k, 1 if schedule == "grouped" else 0, 1 if mit else 0, float(mit["lam"]) if mit else 1.0,
         float(mit["gamma"]) if mit else 0.0, int(mit["n_sim"]) if mit else 5, fanout,
         _p(st["mem"]), _p(st["mem_ts"]), _p(st["mail"]), _p(st["mail_ts"]), max_batches, _p(vers),
-        _p(negc), 0 if negc is None else 1)
+        _p(negc), 0 if negc is None else 1, _p(planc))
     if r < 0:
         raise ValueError(f"orc_run_stream rc={r}")
     return st, vers[:r]

@@ -452,7 +452,7 @@ int64_t orc_run_stream(int64_t N, int64_t E, const int32_t* src, const int32_t* 
                        int32_t k, int32_t schedule, int32_t mit_on, float lambda, double gamma,
                        int32_t n_sim, int32_t fanout, float* mem, double* mem_ts, float* mail,
                        double* mail_ts, int64_t max_batches, int64_t* out_versions,
-                       const int32_t* neg, int32_t subgraph) {
+                       const int32_t* neg, int32_t subgraph, const int32_t* plan_k) {
   if (B < 1 || k < 0 || M < 1) return ORC_EINVAL;
   if (subgraph && !neg) return ORC_EINVAL;
   const int32_t Dm = 2 * M + He;
@@ -478,6 +478,7 @@ int64_t orc_run_stream(int64_t N, int64_t E, const int32_t* src, const int32_t* 
     smts = (double*)malloc(sizeof(double) * R3 * (fanout + 1));
   }
   int32_t R = k + 1;
+  int plan_bad = 0;
   size_t szm = sizeof(float) * (size_t)N * M, szt = sizeof(double) * (size_t)N;
   float** rmem = (float**)malloc(sizeof(float*) * R);
   double** rts = (double**)malloc(sizeof(double*) * R);
@@ -493,7 +494,17 @@ int64_t orc_run_stream(int64_t N, int64_t E, const int32_t* src, const int32_t* 
   double* nts = (double*)malloc(sizeof(double) * 2 * B);
   float* nmail = (float*)malloc(sizeof(float) * 2 * B * Dm);
   for (int64_t i = 1; i <= nb; ++i) {
+    /* plan (row F1): paper staleness k_i, v(i) = max(0, i - k_i) (Alg. 1 gate,
+     * P:L845-L848); the ring of k+1 copies must hold it */
     int64_t v = orc_snapshot_version(i, k, schedule);
+    if (plan_k) {
+      v = i - plan_k[i - 1] > 0 ? i - plan_k[i - 1] : 0;
+      if (plan_k[i - 1] < 1 || i - v > k + 1) {
+        plan_bad = 1;
+        nb = i - 1;
+        break;
+      }
+    }
     if (out_versions) out_versions[i - 1] = v;
     int64_t j0 = (i - 1) * B;
     int64_t nb_ev = (j0 + B <= E) ? B : E - j0;
@@ -551,7 +562,7 @@ int64_t orc_run_stream(int64_t N, int64_t E, const int32_t* src, const int32_t* 
     free(sroots); free(sq); free(snbr); free(seid); free(sts); free(sdt); free(scnt); free(smem); free(smts);
   }
   orc_graph_free(g);
-  return nb;
+  return plan_bad ? ORC_EINVAL : nb;
 }
 
 /* ------------------------------------------------------------------------

@@ -32,7 +32,8 @@ EXPORTS = ("mspipe_abi_version", "mspipe_last_error", "mspipe_check", "mspipe_sa
            "mspipe_shard_fetch_plan", "mspipe_shard_fetch_serve", "mspipe_shard_fetch_finish",
            "mspipe_shard_commit_pack", "mspipe_shard_commit_merge", "mspipe_shard_exchange", "mspipe_shard_loopback",
            "mspipe_util_graph_begin", "mspipe_util_graph_end", "mspipe_util_graph_launch", "mspipe_util_graph_destroy",
-           "mspipe_memory_double_buffer", "mspipe_memory_tables", "mspipe_memory_set_committed")
+           "mspipe_memory_double_buffer", "mspipe_memory_tables", "mspipe_memory_set_committed",
+           "mspipe_plan_timeline", "mspipe_plan_min_staleness", "mspipe_stale_histogram")
 XCHG_FETCH_IDS, XCHG_FETCH_ROWS, XCHG_COMMIT = 0, 1, 2
 
 
@@ -83,6 +84,9 @@ def lib():
         L.mspipe_util_event_record.argtypes = [P, P]
         L.mspipe_memory_double_buffer.argtypes = [P, P, P, P, P]
         L.mspipe_memory_set_committed.argtypes = [P, i64]
+        L.mspipe_plan_timeline.argtypes = [P, i64, P, P, P]
+        L.mspipe_plan_min_staleness.argtypes = [P, i64, i32, P, C.POINTER(i64)]
+        L.mspipe_stale_histogram.argtypes = [C.POINTER(Tcsr), P, P, i64, i64, i32, P, P]
         L.mspipe_memory_tables.argtypes = [P, i64, C.POINTER(P), C.POINTER(P), C.POINTER(P), C.POINTER(P)]
         L.mspipe_util_graph_begin.argtypes = [P]
         L.mspipe_util_graph_end.argtypes = [P, C.POINTER(P)]
@@ -144,6 +148,43 @@ def last_error() -> str:
 def event_record(event: torch.cuda.Event, stream=None):
     """Record a timing event so that it is also captured as a graph node."""
     _ck(lib().mspipe_util_event_record(C.c_void_p(event.cuda_event), stream_ptr(stream)), "event_record")
+
+
+def _host_ptr(a):
+    return C.c_void_p(a.ctypes.data) if a is not None else None
+
+
+def plan_timeline(tau, num_iters, k=None):
+    """Eq. 3-4 on the host (mspipe_plan_timeline): (b, e) arrays [num_iters, 5]."""
+    import numpy as np
+    t = np.ascontiguousarray(tau, dtype=np.float64)
+    assert t.shape == (5,)
+    kk = None if k is None else np.ascontiguousarray(k, dtype=np.int32)
+    b = np.zeros((num_iters, 5))
+    e = np.zeros((num_iters, 5))
+    _ck(lib().mspipe_plan_timeline(_host_ptr(t), int(num_iters), _host_ptr(kk), _host_ptr(b), _host_ptr(e)),
+        "mspipe_plan_timeline")
+    return b, e
+
+
+def plan_min_staleness(tau, num_iters, k_max):
+    """Minimal k_i under C1-C3 (mspipe_plan_min_staleness): (k array, first infeasible iteration or 0)."""
+    import numpy as np
+    t = np.ascontiguousarray(tau, dtype=np.float64)
+    assert t.shape == (5,)
+    k = np.zeros(num_iters, np.int32)
+    bad = i64(0)
+    _ck(lib().mspipe_plan_min_staleness(_host_ptr(t), int(num_iters), int(k_max), _host_ptr(k), C.byref(bad)),
+        "mspipe_plan_min_staleness")
+    return k, int(bad.value)
+
+
+def stale_histogram(g: "TcsrHandle", src, dst, batch, max_d=64, stream=None):
+    """C3 statistic on the GPU (mspipe_stale_histogram): int64 device tensor [max_d + 2]."""
+    out = torch.empty(max_d + 2, dtype=torch.int64, device=src.device)
+    _ck(lib().mspipe_stale_histogram(C.byref(g.c), ptr(src), ptr(dst), src.numel(), int(batch), int(max_d),
+                                     ptr(out), stream_ptr(stream)), "mspipe_stale_histogram")
+    return out
 
 
 class StepGraph:

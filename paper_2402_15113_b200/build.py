@@ -10,7 +10,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libmspipe.so")
-SOURCES = ["api.cu", "sampler.cu", "memory.cu", "prep.cu", "gru_simt.cu", "gru_tc.cu", "shard.cu", "nccl_xchg.cu"]
+SOURCES = ["api.cu", "sampler.cu", "memory.cu", "prep.cu", "gru_simt.cu", "gru_tc.cu", "shard.cu", "nccl_xchg.cu", "planner.cu",
+           "stale.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 

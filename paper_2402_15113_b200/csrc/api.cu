@@ -792,6 +792,19 @@ mspipe_status mspipe_util_event_record(void* event, void* stream) {
                      "util_event_record");
 }
 
+mspipe_status mspipe_stale_histogram(const mspipe_tcsr* g, const int32_t* src, const int32_t* dst,
+                                     int64_t num_events, int64_t batch, int32_t max_d, int64_t* out_hist,
+                                     void* stream) {
+  if (!tcsr_ok(g) || num_events < 0 || batch < 1 || max_d < 1 || max_d > 4096 || !out_hist ||
+      (num_events > 0 && (!src || !dst)))
+    return fail(MSPIPE_EINVAL, "stale_histogram: num_events=%lld batch=%lld max_d=%d (1..4096)", (long long)num_events,
+                (long long)batch, max_d);
+  cudaError_t e = launch_stale_hist(to_tcsr(g), src, dst, num_events, batch, max_d, (unsigned long long*)out_hist,
+                                    (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_status(e, "stale_histogram: launch");
+  return after_launch("stale_histogram");
+}
+
 mspipe_status mspipe_util_graph_begin(void* stream) {
   return cuda_status(cudaStreamBeginCapture((cudaStream_t)stream, cudaStreamCaptureModeThreadLocal),
                      "util_graph_begin");

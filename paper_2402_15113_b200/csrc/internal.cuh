@@ -237,6 +237,9 @@ cudaError_t launch_gru_tc(const GruDesc& d, const float* wtc, float* xbuf, const
                           const int32_t* num_unique, float* out_mem, double* out_ts, float* out_mail,
                           int64_t mail_stride, cudaStream_t s, int parts = kGruBuild | kGruGemm,
                           const GruCommit* commit = nullptr);
+// stale.cu
+cudaError_t launch_stale_hist(const Tcsr& g, const int32_t* src, const int32_t* dst, int64_t E, int64_t B,
+                              int32_t max_d, unsigned long long* hist, cudaStream_t s);
 // prep.cu
 cudaError_t launch_prep(const Tcsr& g, const int32_t* src, const int32_t* dst, const int32_t* neg,
                         const double* ts, int64_t num_events, int32_t fanout, int32_t* out_nbr,

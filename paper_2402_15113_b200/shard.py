@@ -181,7 +181,7 @@ class ShardRank(_TimedOps):
     def step_ops(self, nb=None):
         nb = self.num_batches if nb is None else nb
         steps, cur = [], []
-        for op in schedule_ops(nb, self.cfg.k, self.cfg.schedule):
+        for op in schedule_ops(nb, self.cfg.k, self.cfg.schedule, self.cfg.plan):
             cur.append(op)
             if op[0] == "commit":
                 steps.append(cur)

@@ -42,6 +42,7 @@ class StageConfig:
     precision: int = _C.FP32_3XTF32  # tcgen05 3xTF32 (fp32 parity); _C.FP32_SIMT = CUDA-core baseline
     fused: bool | None = None  # mspipe_memory_prep + message_build/gru_apply (default: when supported)
     double_buffer: bool | None = None  # two table sets (mspipe_memory_double_buffer); default: k >= 1
+    plan: tuple | None = None  # schedule "plan": paper staleness k_i per iteration (row F1)
 
     def use_fused(self) -> bool:
         ok = self.precision == _C.FP32_3XTF32 and self.fanout <= 31 and self.batch <= 8192
@@ -51,9 +52,28 @@ class StageConfig:
         return self.k >= 1 if self.double_buffer is None else bool(self.double_buffer)
 
 
-def schedule_ops(nb: int, k: int, schedule: str = "exact"):
-    """Stream order of prep/commit ops for batches 1..nb."""
+def plan_versions(plan, nb):
+    """v(i) = max(0, i - k_i) for a plan of paper staleness values k_i (row F1)."""
+    return [max(0, i - int(plan[i - 1])) for i in range(1, nb + 1)]
+
+
+def schedule_ops(nb: int, k: int, schedule: str = "exact", plan=None):
+    """Stream order of prep/commit ops for batches 1..nb.  "plan": prep(i) is
+    enqueued right after commit(v(i)), v(i) = max(0, i - k_i) — the Alg. 1
+    gate as stream order; needs k >= max(i - v(i)) - 1."""
     ops = []
+    if schedule == "plan":
+        v = plan_versions(plan, nb)
+        if any(i - vi > k + 1 or vi > i - 1 for i, vi in zip(range(1, nb + 1), v)):
+            raise ValueError("plan needs k_i >= 1 and i - v(i) <= k + 1 (the slots in flight)")
+        after = {}
+        for i, vi in enumerate(v, start=1):
+            after.setdefault(vi, []).append(i)
+        ops += [("prep", i) for i in after.get(0, [])]
+        for t in range(1, nb + 1):
+            ops.append(("commit", t))
+            ops += [("prep", i) for i in after.get(t, [])]
+        return ops
     if schedule == "exact":
         for i in range(1, min(k, nb) + 1):
             ops.append(("prep", i))
@@ -71,10 +91,10 @@ def schedule_ops(nb: int, k: int, schedule: str = "exact"):
     return ops
 
 
-def snapshot_versions(nb: int, k: int, schedule: str = "exact"):
+def snapshot_versions(nb: int, k: int, schedule: str = "exact", plan=None):
     """v(i) the schedule reads (for checks): committed count at prep(i)."""
     v, committed = {}, 0
-    for op, i in schedule_ops(nb, k, schedule):
+    for op, i in schedule_ops(nb, k, schedule, plan):
         if op == "prep":
             v[i] = committed
         else:
@@ -377,7 +397,7 @@ class MemoryStage(_TimedOps):
         """Ops grouped per step (one commit per step; prologue preps in step 0)."""
         nb = self.num_batches if nb is None else nb
         steps, cur = [], []
-        for op in schedule_ops(nb, self.cfg.k, self.cfg.schedule):
+        for op in schedule_ops(nb, self.cfg.k, self.cfg.schedule, self.cfg.plan):
             cur.append(op)
             if op[0] == "commit":
                 steps.append(cur)

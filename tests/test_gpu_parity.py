@@ -462,3 +462,50 @@ def test_two_stream_overlap_equals_serial(dev):
         outs.append([getattr(st.memory, k).cpu().numpy() for k in ("mem", "mem_ts", "mail", "mail_ts")])
     for a, b in zip(*outs):
         assert np.array_equal(a, b)
+
+
+# ------------------------------------------------------------------ row F1
+@pytest.mark.parametrize("name,E,B", [("tiny", None, 200), ("wiki", None, 600), ("lastfm", 300_000, 600),
+                                      ("tiny", 3001, 7)])
+def test_stale_histogram_equals_oracle(dev, name, E, B):
+    """mspipe_stale_histogram (GPU, T-CSR search) == the oracle's batch replay, bit for bit."""
+    from oracle import planner as OP
+    cfg = CONFIGS[name]
+    src, dst, ts, _ = make_events(cfg, 2, E)
+    g = build_tcsr(cfg.num_nodes, src, dst, ts, dev)
+    max_d = 40
+    h = _C.stale_histogram(g, _t(src, dev), _t(dst, dev), B, max_d).cpu().numpy()
+    _, ref = OP.stale_fraction(src, dst, B, [1])
+    want = np.zeros(max_d + 2, np.int64)
+    for d, c in ref.items():
+        want[min(d, max_d + 1)] += c
+    assert np.array_equal(h, want)
+
+
+@pytest.mark.parametrize("fused", [True, False])
+def test_stream_with_plan_equals_oracle(dev, fused):
+    """A per-iteration plan k_i (row F1: prep(i) right after commit(i - k_i)) gives
+    the oracle's state under the same plan."""
+    from paper_2402_15113_b200.planner import stage_config_for_plan
+    w = make_workload("lastfm", seed=6, num_events=36_000)
+    cfg = w["cfg"]
+    nb = -(-36_000 // cfg.batch)
+    rng = np.random.default_rng(6)
+    plan = [min(i, int(rng.integers(1, 5))) for i in range(1, nb + 1)]
+    base = StageConfig(cfg.num_nodes, cfg.mem_dim, cfg.edge_dim, cfg.time_dim, cfg.fanout, cfg.batch, 0,
+                       fetch_mail=True, fused=fused)
+    sc = stage_config_for_plan(base, plan)
+    g = build_tcsr(cfg.num_nodes, w["src"], w["dst"], w["ts"], dev)
+    st = MemoryStage(sc, w["params"], g, dev)
+    t = {kk: _t(w[kk], dev) for kk in ("src", "dst", "ts", "neg", "ef")}
+    st.bind_resident(t["src"], t["dst"], t["ts"], t["neg"], t["ef"])
+    st.run()
+    torch.cuda.synchronize()
+    _C.check()
+    ref, vers = oracle.run_stream(cfg.num_nodes, w["src"], w["dst"], w["ts"], w["ef"], w["params"], cfg.batch,
+                                  sc.k, plan=plan)
+    assert [st.versions[i] for i in range(1, nb + 1)] == vers.tolist()
+    assert np.array_equal(st.memory.mem_ts.cpu().numpy(), ref["mem_ts"])
+    gm, om = st.memory.mem.cpu().numpy().astype(np.float64), ref["mem"].astype(np.float64)
+    rel = np.linalg.norm(gm - om, axis=1) / np.maximum(np.linalg.norm(om, axis=1), 1e-3)
+    assert rel.max() <= 1e-4
