@@ -319,6 +319,31 @@ MSPIPE_API mspipe_status mspipe_gru_apply(const mspipe_gru* gru, int64_t num_eve
                                const int32_t* num_unique, float* out_mem, const void* workspace,
                                size_t ws_bytes, void* stream);
 
+/* A1 + A2 + A3 + A5 in one launch: mspipe_memory_prep (no mitigation) and then
+ * mspipe_message_build of the same batch with snap_mem = out_mem, snap_step =
+ * fanout + 1, snap_h = NULL, winner = out_winner, num_unique = out_num_unique
+ * — same outputs (out_commit_ts / out_commit_mail = message_build's out_ts /
+ * out_mail with the handle's mail_stride; the A-operand images in
+ * `workspace`, >= mspipe_gru_workspace_size(gru, num_events) bytes).  Inside
+ * the kernel the dedup block publishes the pair -> GEMM-row map and the warps
+ * of the winners' roots build their rows (G1, G2, G4, G13) from the tables of
+ * the version read.  num_events <= gru max_events.  Errors as
+ * mspipe_memory_prep, plus MSPIPE_EINVAL (NULL GRU / outputs, dims differ,
+ * workspace too small) and MSPIPE_EUNSUPPORTED (precision other than
+ * MSPIPE_FP32_3XTF32).  Preps of one handle must not run concurrently (they
+ * share the handle's dedup / build scratch): the stage driver issues them on
+ * one stream. */
+MSPIPE_API mspipe_status mspipe_memory_prep_build(mspipe_memory* st, const mspipe_tcsr* g, int64_t iteration,
+                                       const int32_t* src, const int32_t* dst, const int32_t* neg,
+                                       const double* ts, int64_t num_events, int32_t fanout,
+                                       int32_t* out_nbr, int32_t* out_eid, double* out_ts, float* out_dt,
+                                       int32_t* out_cnt, int32_t* out_sub_ids, int32_t* out_nodes,
+                                       int32_t* out_winner, int32_t* out_num_unique, float* out_mem,
+                                       double* out_mem_ts, float* out_mail, double* out_mail_ts,
+                                       int64_t* out_version, const mspipe_gru* gru, const float* edge_feat,
+                                       double* out_commit_ts, float* out_commit_mail, void* workspace,
+                                       size_t ws_bytes, void* stream);
+
 /* A6 + A7 in one launch: mspipe_gru_apply, then mspipe_memory_writeback of
  * (nodes, num_unique, h', new_ts, new_mail) as version commit_version, the
  * write-back done by the GEMM epilogue (world == 1).  new_ts / new_mail are

@@ -33,7 +33,8 @@ EXPORTS = ("mspipe_abi_version", "mspipe_last_error", "mspipe_check", "mspipe_sa
            "mspipe_shard_commit_pack", "mspipe_shard_commit_merge", "mspipe_shard_exchange", "mspipe_shard_loopback",
            "mspipe_util_graph_begin", "mspipe_util_graph_end", "mspipe_util_graph_launch", "mspipe_util_graph_destroy",
            "mspipe_memory_double_buffer", "mspipe_memory_tables", "mspipe_memory_set_committed",
-           "mspipe_plan_timeline", "mspipe_plan_min_staleness", "mspipe_stale_histogram")
+           "mspipe_plan_timeline", "mspipe_plan_min_staleness", "mspipe_stale_histogram",
+           "mspipe_memory_prep_build")
 XCHG_FETCH_IDS, XCHG_FETCH_ROWS, XCHG_COMMIT = 0, 1, 2
 
 
@@ -94,6 +95,8 @@ def lib():
         L.mspipe_util_graph_destroy.argtypes = [P]
         L.mspipe_memory_prep.argtypes = [P, C.POINTER(Tcsr), i64, P, P, P, P, i64, i32, P, P, P, P, P, P, P, P, P, P,
                                          P, P, P, C.POINTER(Mitigation), C.POINTER(i64), P]
+        L.mspipe_memory_prep_build.argtypes = [P, C.POINTER(Tcsr), i64, P, P, P, P, i64, i32, P, P, P, P, P, P, P,
+                                               P, P, P, P, P, P, C.POINTER(i64), P, P, P, P, P, C.c_size_t, P]
         L.mspipe_gru_workspace_size.argtypes = [P, i64]
         L.mspipe_gru_workspace_size.restype = C.c_size_t
         L.mspipe_message_build.argtypes = [P, P, i64, P, P, P, i64, P, P, P, P, P, i64, P, C.c_size_t, P]
@@ -447,6 +450,22 @@ def memory_prep(st: MemoryHandle, g: TcsrHandle, iteration, src, dst, neg, ts, f
                                  ptr(dd["winner"]), ptr(dd["num"]), ptr(out_mem), ptr(out_mem_ts), ptr(out_mail),
                                  ptr(out_mail_ts), C.byref(mitigation) if mitigation is not None else None,
                                  C.byref(v), stream_ptr(stream)), "mspipe_memory_prep")
+    return int(v.value)
+
+
+def memory_prep_build(st: MemoryHandle, g: TcsrHandle, iteration, src, dst, neg, ts, fanout, samp, dd, out_mem,
+                      out_mem_ts, out_mail, out_mail_ts, gru: GruHandle, edge_feat, out_commit_ts, out_commit_mail,
+                      workspace, stream=None) -> int:
+    """A1+A2+A3 and the A5 message build of the same batch in one launch (no mitigation)."""
+    v = i64(-1)
+    _ck(lib().mspipe_memory_prep_build(st.h, C.byref(g.c), int(iteration), ptr(src), ptr(dst), ptr(neg), ptr(ts),
+                                       src.numel(), fanout, ptr(samp["nbr"]), ptr(samp["eid"]), ptr(samp["ts"]),
+                                       ptr(samp["dt"]), ptr(samp["cnt"]), ptr(samp["sub"]), ptr(dd["nodes"]),
+                                       ptr(dd["winner"]), ptr(dd["num"]), ptr(out_mem), ptr(out_mem_ts),
+                                       ptr(out_mail), ptr(out_mail_ts), C.byref(v), gru.h, ptr(edge_feat),
+                                       ptr(out_commit_ts), ptr(out_commit_mail), ptr(workspace),
+                                       workspace.numel() * workspace.element_size(), stream_ptr(stream)),
+        "mspipe_memory_prep_build")
     return int(v.value)
 
 

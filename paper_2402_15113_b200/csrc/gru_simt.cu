@@ -92,7 +92,7 @@ __device__ __forceinline__ float x_elem(const GruArgs& a, const RowInfo& ri, int
   if (k < d.Dm) return __ldg(a.ef + (int64_t)ri.ev[m] * d.He + (k - 2 * M));
   if (k < d.Dx) {
     const int q = k - d.Dm;
-    return cosf(fmaf(__ldg(d.time_w + q), ri.dt[m], __ldg(d.time_b + q)));
+    return time_cos(fmaf(__ldg(d.time_w + q), ri.dt[m], __ldg(d.time_b + q)));
   }
   if (k < d.K) {
     const int kk = k - d.Dx;

@@ -26,18 +26,15 @@
 #include <stdlib.h>
 
 #include "internal.cuh"
+#include "tc_layout.cuh"
 
 namespace mspipe {
 
 namespace tc {
 
-constexpr int kM = 128;                 // rows per tile (UMMA M)
 constexpr int kJ = 16;                  // hidden units per tile
 constexpr int kN = 4 * kJ;              // accumulator columns (UMMA N)
-constexpr int kKC = 32;                 // fp32 per 128 B swizzle row = one K chunk
-constexpr int kATile = kM * kKC * 4;    // 16 KB
 constexpr int kBTile = kN * kKC * 4;    // 8 KB
-constexpr int kABlock = 2 * kATile;     // hi | lo
 constexpr int kBBlock = 2 * kBTile;
 constexpr int kStageBytes = kABlock + kBBlock;  // 48 KB
 constexpr int kStages = 3;
@@ -153,11 +150,6 @@ __device__ __forceinline__ float4 ld_dsmem_f4(uint32_t addr) {
       : "r"(addr));
   return v;
 }
-__device__ __forceinline__ float tf32_rna(float x) {
-  uint32_t r;
-  asm("cvt.rna.tf32.f32 %0, %1;\n" : "=r"(r) : "f"(x));
-  return __uint_as_float(r);
-}
 // SWIZZLE_128B K-major smem descriptor (sm_100: version 1, SBO = 1024 B, LBO field 16 B).
 __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
   uint64_t d = (uint64_t)((saddr >> 4) & 0x3FFFu);
@@ -170,11 +162,6 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
 // kind::tf32 instruction descriptor: D f32, A/B tf32, K-major, M = 128, N = 64.
 constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(kN >> 3) << 17) |
                             ((uint32_t)(kM >> 4) << 24);
-// byte offset of element (row, k) in a [rows x 32] fp32 SWIZZLE_128B K-major tile
-__host__ __device__ __forceinline__ uint32_t sw128_off(uint32_t row, uint32_t k) {
-  return row * 128u + ((((k >> 2) ^ (row & 7u)) & 7u) << 4) + (k & 3u) * 4u;
-}
-
 }  // namespace tc
 
 #ifdef MSPIPE_PHASES
@@ -337,7 +324,7 @@ __global__ void __launch_bounds__(256) k_build_x(TcArgs a) {
       else if (k < d.Dx) {
         const float dt = (float)(__ldg(a.ts + ev) - __ldg(a.snap_ts + rw * a.step));  // Δt (G4)
         const int q = k - d.Dm;
-        v = cosf(fmaf(__ldg(d.time_w + q), dt, __ldg(d.time_b + q)));
+        v = time_cos(fmaf(__ldg(d.time_w + q), dt, __ldg(d.time_b + q)));
       } else if (k < d.K) {
         const int q = k - d.Dx;
         v = a.snap_h ? __ldg(a.snap_h + rw * M + q) : __ldg(a.snap_mem + rw * a.step * M + q);

@@ -41,6 +41,18 @@ __device__ __forceinline__ void pdl_begin() {
   asm volatile("griddepcontrol.wait;\n" ::: "memory");
 }
 
+// Time encoding cos(x), x = fmaf(omega, dt, phi) (G2, G22).  With raw Δt the
+// argument reaches 10^6..10^7, where cosf takes its slow (Payne-Hanek, local
+// memory) reduction path; reduce x mod 2π in double instead (two-term 2π,
+// error ~ |k| 2^-105 + 2^-53|x|, < 1e-9 here) and evaluate cosf on |r| <= π.
+__device__ __forceinline__ float time_cos(float x) {
+  const double xd = (double)x;
+  const double k = rint(xd * 0.15915494309189535);  // 1 / (2π)
+  double r = fma(-k, 6.283185307179586232, xd);
+  r = fma(-k, 2.4492935982947064e-16, r);
+  return cosf((float)r);
+}
+
 bool pdl_enabled();  // env MSPIPE_PDL=1 enables (A/B experiments)
 // integer knob from the environment (experiments only; defaults are the tuned values)
 int env_int(const char* name, int def);
@@ -186,6 +198,18 @@ struct CatchUp {
   int32_t iter;
 };
 
+// fused A5 inside the prep kernel (mspipe_memory_prep_build)
+struct PrepBuild {
+  GruDesc d;
+  float* xbuf;          // GEMM A-operand images (workspace); nullptr: no build
+  const float* ef;      // [B, He] edge features of the batch
+  double* out_ts;       // [U] commit timestamps
+  float* out_mail;      // [U, mail_stride] mail rows
+  int64_t mail_stride;
+  int32_t* upos;        // [2B] pair -> GEMM row (-1: not a winner), library scratch
+  int32_t* sync;        // [2] publish flag, exit count (self-cleaning), library scratch
+};
+
 // one warp copies row v of every table (4 x 16 B loads in flight per lane)
 __device__ __forceinline__ void catchup_row(const CatchUp& c, int32_t v, int32_t Qm, int32_t Qa, int lane) {
   const float4* om = reinterpret_cast<const float4*>(c.old_mem) + (int64_t)v * Qm;
@@ -248,7 +272,8 @@ cudaError_t launch_prep(const Tcsr& g, const int32_t* src, const int32_t* dst, c
                         const float* mem, const double* mem_ts, int32_t mem_dim, const float* mail,
                         const double* mail_ts, int64_t mail_stride, float* out_mem, double* out_mem_ts,
                         float* out_mail, double* out_mail_ts, cudaStream_t s, int32_t* stamp = nullptr,
-                        int32_t stamp_iter = 0, const struct CatchUp* cu = nullptr);
+                        int32_t stamp_iter = 0, const struct CatchUp* cu = nullptr,
+                        const struct PrepBuild* bld = nullptr);
 
 }  // namespace mspipe
 
@@ -319,6 +344,9 @@ struct mspipe_memory {
   int32_t* stamps;          // [k+1][num_nodes]
   int64_t* stamp_iter;      // [k+1] host: iteration whose winners ring slot r holds (0 = none)
   int64_t caught_up;        // host: the commit whose catch-up a prep has already enqueued (0 = none)
+  // fused message build (mspipe_memory_prep_build): pair -> GEMM row, publish flag
+  int32_t* bld_upos;        // [2 * 8192]
+  int32_t* bld_sync;        // [2], self-cleaning
 };
 
 namespace mspipe {

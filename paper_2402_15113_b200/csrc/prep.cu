@@ -12,6 +12,7 @@
 // write-back(i-1-k) and write-back(i-k) (Eq. 2).
 #include "dedup.cuh"
 #include "internal.cuh"
+#include "tc_layout.cuh"
 
 namespace mspipe {
 
@@ -50,7 +51,17 @@ struct PrepArgs {
   int32_t stamp_iter;
   CatchUp cu;      // optional (cu.stamp != nullptr): the next commit's catch-up rows
   int32_t Qcu;     // float4 per mail row of the state tables (catch-up)
+  PrepBuild bld;   // optional (bld.xbuf != nullptr): fused A5 message build
 };
+
+__device__ __forceinline__ int32_t ld_acquire(const int32_t* p) {
+  int32_t v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(int32_t* p, int32_t v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
+}
 
 // copy `nrows` table rows (ids held by lanes 0..nrows-1, -1 = zero row) of Q
 // float4 each into dst rows base..base+nrows-1; 4 loads in flight per lane.
@@ -76,18 +87,87 @@ __device__ __forceinline__ void warp_gather_rows(const float4* __restrict__ tab,
   }
 }
 
+#ifdef MSPIPE_PHASES
+// debug: per-block phase times of the last k_prep launch (globaltimer ns)
+__device__ unsigned long long g_pphase[8192][6];
+__device__ __forceinline__ void pphase(int i) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  atomicMax(&g_pphase[blockIdx.x][i], t);
+}
+#define PPHASE(i) pphase(i)
+#else
+#define PPHASE(i)
+#endif
+
+// the fused build's flag is self-cleaning: the last block to leave resets it
+// (every block has passed its wait by then), so replays start from 0
+__device__ __forceinline__ void prep_exit(const PrepArgs& a) {
+  if (!a.bld.xbuf) return;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const int32_t prev = atomicAdd(a.bld.sync + 1, 1);
+    if (prev == (int32_t)gridDim.x - 1) {
+      a.bld.sync[0] = 0;
+      a.bld.sync[1] = 0;
+      __threadfence();
+    }
+  }
+}
+
+// A5, GEMM row u, K chunk c (one warp, lane = column): the k_build_x work item
+__device__ __forceinline__ void build_chunk(const PrepArgs& a, int32_t u, int32_t c, int lane) {
+  const PrepBuild& b = a.bld;
+  const GruDesc& d = b.d;
+  const int32_t p = a.out_winner[u];  // written by block 0 in this launch: plain load
+  const int64_t ev = p >> 1;
+  const int role = p & 1;
+  const int32_t k = c * tc::kKC + lane;
+  float v = 0.f;
+  if (k < d.M || (k >= d.Dx && k < d.K) || (k >= d.Dm && k < d.Dx)) {
+    const int32_t node = role ? __ldg(a.dst + ev) : __ldg(a.src + ev);
+    const float* sw = reinterpret_cast<const float*>(a.mem) + (int64_t)node * d.M;
+    if (k < d.M) v = __ldg(sw + k);
+    else if (k >= d.Dx) v = __ldg(sw + (k - d.Dx));
+    else v = time_cos(fmaf(__ldg(d.time_w + (k - d.Dm)), (float)(__ldg(a.ts + ev) - __ldg(a.mem_ts + node)),
+                           __ldg(d.time_b + (k - d.Dm))));
+  } else if (k < 2 * d.M) {
+    const int32_t other = role ? __ldg(a.src + ev) : __ldg(a.dst + ev);
+    v = __ldg(reinterpret_cast<const float*>(a.mem) + (int64_t)other * d.M + (k - d.M));
+  } else if (k < d.Dm) {
+    v = __ldg(b.ef + ev * d.He + (k - 2 * d.M));
+  }
+  if (k < b.mail_stride) b.out_mail[(int64_t)u * b.mail_stride + k] = k < d.Dm ? v : 0.f;
+  if (c == 0 && lane == 0) b.out_ts[u] = __ldg(a.ts + ev);
+  tc::store_a(b.xbuf, d.Kpad / tc::kKC, u, k, v);
+}
+
 template <bool kSmem>
 __global__ void __launch_bounds__(kPrepThreads) k_prep(PrepArgs a) {
   extern __shared__ int32_t sscratch[];
   pdl_begin();
+  if (threadIdx.x == 0) PPHASE(0);
   if (blockIdx.x == 0) {
     block_dedup<kPrepThreads, kSmem>(a.src, a.dst, a.B, a.gscratch, sscratch, a.g.num_nodes, a.out_nodes,
                                      a.out_winner, a.out_num);
-    if (a.stamp) {
-      __syncthreads();  // out_nodes / out_num written by this block
+    if (a.stamp || a.bld.xbuf) {
+      __syncthreads();  // out_nodes / out_winner / out_num written by this block
       const int32_t U = *a.out_num;
-      for (int32_t u = threadIdx.x; u < U; u += kPrepThreads) a.stamp[a.out_nodes[u]] = a.stamp_iter;
+      if (a.stamp)
+        for (int32_t u = threadIdx.x; u < U; u += kPrepThreads) a.stamp[a.out_nodes[u]] = a.stamp_iter;
+      if (a.bld.xbuf) {  // pair -> GEMM row, then publish to the build warps
+        for (int64_t p = threadIdx.x; p < 2 * a.B; p += kPrepThreads) a.bld.upos[p] = -1;
+        __syncthreads();
+        for (int32_t u = threadIdx.x; u < U; u += kPrepThreads) a.bld.upos[a.out_winner[u]] = u;
+        __threadfence();
+        __syncthreads();
+        if (threadIdx.x == 0) st_release(a.bld.sync, 1);
+      }
     }
+    if (threadIdx.x == 0) PPHASE(1);
+    prep_exit(a);
+    if (threadIdx.x == 0) PPHASE(4);
     return;
   }
   const int lane = threadIdx.x & 31;
@@ -132,6 +212,7 @@ __global__ void __launch_bounds__(kPrepThreads) k_prep(PrepArgs a) {
     warp_gather_rows(a.mem, a.Qm, gid, F1, a.out_mem, r * F1, lane);
     if (a.Qa > 0) warp_gather_rows(a.mail, a.Qa, gid, F1, a.out_mail, r * F1, lane);
   }
+  if (lane == 0) PPHASE(1);
   if (a.cu.stamp) {  // double-buffered: rows of the previous commit, after this warp's roots
     const int32_t np = __ldg(a.cu.prev_num);
     const int64_t r0 = wid + (R - wid + nwarps - 1) / nwarps * nwarps;  // this warp's first item >= R
@@ -140,6 +221,20 @@ __global__ void __launch_bounds__(kPrepThreads) k_prep(PrepArgs a) {
       if (__ldg(a.cu.stamp + v) != a.cu.iter) catchup_row(a.cu, v, a.Qm, a.Qcu, lane);
     }
   }
+  if (a.bld.xbuf) {
+    // fused A5 once block 0 has published the winners: one warp per (GEMM row,
+    // 32-wide K chunk), every warp of the grid, as k_build_x does
+    if (lane == 0) PPHASE(5);
+    while (ld_acquire(a.bld.sync) == 0) __nanosleep(32);
+    if (lane == 0) PPHASE(2);
+    const int32_t U = *a.out_num;
+    const int32_t nchunks = a.bld.d.Kpad / tc::kKC;
+    for (int64_t it = wid; it < (int64_t)U * nchunks; it += nwarps)
+      build_chunk(a, (int32_t)(it / nchunks), (int32_t)(it % nchunks), lane);
+    if (lane == 0) PPHASE(3);
+  }
+  prep_exit(a);
+  if (threadIdx.x == 0) PPHASE(4);
 }
 
 cudaError_t launch_prep(const Tcsr& g, const int32_t* src, const int32_t* dst, const int32_t* neg,
@@ -149,13 +244,14 @@ cudaError_t launch_prep(const Tcsr& g, const int32_t* src, const int32_t* dst, c
                         const float* mem, const double* mem_ts, int32_t mem_dim, const float* mail,
                         const double* mail_ts, int64_t mail_stride, float* out_mem, double* out_mem_ts,
                         float* out_mail, double* out_mail_ts, cudaStream_t s, int32_t* stamp,
-                        int32_t stamp_iter, const CatchUp* cu) {
+                        int32_t stamp_iter, const CatchUp* cu, const PrepBuild* bld) {
   PrepArgs a{g, src, dst, neg, ts, num_events, fanout, out_nbr, out_eid, out_ts, out_dt, out_cnt, out_sub,
              scratch, out_nodes, out_winner, out_num, (const float4*)mem, mem_ts, mem_dim / 4,
              (const float4*)mail, mail_ts, out_mail ? (int32_t)(mail_stride / 4) : 0, (float4*)out_mem, out_mem_ts,
              (float4*)out_mail, out_mail ? out_mail_ts : nullptr, stamp, stamp_iter, CatchUp{},
              (int32_t)(mail_stride / 4)};
   if (cu) a.cu = *cu;
+  if (bld) a.bld = *bld;
   int64_t blocks = (3 * num_events + kPrepWarps - 1) / kPrepWarps;
   const int64_t cap = (int64_t)num_sms() * env_int("MSPIPE_PREP_BPS", 4);
   if (blocks > cap) blocks = cap;
@@ -175,3 +271,13 @@ cudaError_t launch_prep(const Tcsr& g, const int32_t* src, const int32_t* dst, c
 }
 
 }  // namespace mspipe
+
+#ifdef MSPIPE_PHASES
+extern "C" __attribute__((visibility("default"))) int mspipe_debug_prep_phases(void* host, int n, int reset) {
+  if (reset) {
+    static unsigned long long zero[8192][6];
+    return (int)cudaMemcpyToSymbol(mspipe::g_pphase, zero, sizeof(zero));
+  }
+  return (int)cudaMemcpyFromSymbol(host, mspipe::g_pphase, sizeof(unsigned long long) * 6 * n);
+}
+#endif

@@ -21,6 +21,7 @@ launch-bound otherwise).
 from __future__ import annotations
 
 import dataclasses
+import os
 
 import torch
 
@@ -43,6 +44,10 @@ class StageConfig:
     fused: bool | None = None  # mspipe_memory_prep + message_build/gru_apply (default: when supported)
     double_buffer: bool | None = None  # two table sets (mspipe_memory_double_buffer); default: k >= 1
     plan: tuple | None = None  # schedule "plan": paper staleness k_i per iteration (row F1)
+    # fused path without mitigation: message build inside the prep kernel (mspipe_memory_prep_build).
+    # Off by default: measured slower on the wiki step (30.7 vs 26.0 us; the build waits for the
+    # single dedup block and the longer prep kernel contends with the GEMM).  env MSPIPE_PREP_BUILD=1: A/B
+    prep_build: bool = dataclasses.field(default_factory=lambda: os.environ.get("MSPIPE_PREP_BUILD", "0") == "1")
 
     def use_fused(self) -> bool:
         ok = self.precision == _C.FP32_3XTF32 and self.fanout <= 31 and self.batch <= 8192
@@ -265,6 +270,20 @@ class MemoryStage(_TimedOps):
         """mspipe_memory_prep (A1+A2+A3[+A4], one launch) then mspipe_message_build (A5) of batch i."""
         cfg = self.cfg
         m = 3 * n * (cfg.fanout + 1)
+        if not cfg.mitigation and cfg.prep_build:
+            # one launch: A1 + A2 + A3 + the A5 message build (mspipe_memory_prep_build)
+            self._ev("prep")
+            sl.version = _C.memory_prep_build(self.memory, self.tcsr, i, x["src"], x["dst"], x["neg"], x["ts"],
+                                              cfg.fanout, samp, sl.dd, sl.mem[:m], sl.mem_ts[:m],
+                                              sl.mail[:m] if sl.mail is not None else None,
+                                              sl.mail_ts[:m] if sl.mail_ts is not None else None, self.gru,
+                                              x["ef"], sl.uts[: 2 * n], sl.umail[: 2 * n], sl.ws)
+            self._ev("prep_end")
+            self.versions[i] = sl.version
+            if not self.memory.double_buffer:
+                self._fetched = torch.cuda.Event()  # the state tables have been read for batch i
+                self._fetched.record()
+            return
         self._ev("prep")
         sl.version = _C.memory_prep(self.memory, self.tcsr, i, x["src"], x["dst"], x["neg"], x["ts"], cfg.fanout,
                                     samp, sl.dd, sl.mem[:m], sl.mem_ts[:m],
@@ -364,14 +383,18 @@ class MemoryStage(_TimedOps):
         db = self.memory.double_buffer
         forked = joined = False
         for op, i in ops:
-            if op == "prep" and i not in commits:
+            if op == "prep":
+                # every prep goes to the side stream, in order (preps of one handle
+                # share its scratch); a commit of this group waits for its own prep
                 if not forked:
                     self.side.wait_stream(main)
                     forked = True
                 with torch.cuda.stream(self.side):
                     self.prep(i)
-            elif op == "prep":
-                self.prep(i)
+                if i in commits:
+                    done = torch.cuda.Event()
+                    done.record(self.side)
+                    main.wait_event(done)
             elif self.fused:
                 # the epilogue writes the tables: wait only for the side stream's
                 # fetch (not its message build, which overlaps this GEMM)

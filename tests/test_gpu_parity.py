@@ -509,3 +509,46 @@ def test_stream_with_plan_equals_oracle(dev, fused):
     gm, om = st.memory.mem.cpu().numpy().astype(np.float64), ref["mem"].astype(np.float64)
     rel = np.linalg.norm(gm - om, axis=1) / np.maximum(np.linalg.norm(om, axis=1), 1e-3)
     assert rel.max() <= 1e-4
+
+
+@pytest.mark.parametrize("k", [0, 1, 2])
+def test_prep_build_equals_prep_then_build(dev, k):
+    """mspipe_memory_prep_build (message build inside the prep kernel) leaves the
+    same GEMM operand images, commit rows and final state as mspipe_memory_prep +
+    mspipe_message_build, bit for bit."""
+    w = make_workload("lastfm", seed=8, num_events=24_000)
+    cfg = w["cfg"]
+    res = []
+    for pb in (False, True):
+        sc = StageConfig(cfg.num_nodes, cfg.mem_dim, cfg.edge_dim, cfg.time_dim, cfg.fanout, cfg.batch, k,
+                         fetch_mail=True, prep_build=pb)
+        g = build_tcsr(cfg.num_nodes, w["src"], w["dst"], w["ts"], dev)
+        st = MemoryStage(sc, w["params"], g, dev)
+        assert st.fused
+        t = {kk: _t(w[kk], dev) for kk in ("src", "dst", "ts", "neg", "ef")}
+        st.bind_resident(t["src"], t["dst"], t["ts"], t["neg"], t["ef"])
+        ops = st.step_ops()
+        for o in ops[:-1]:
+            st.run_ops(o)
+        torch.cuda.synchronize()
+        last = max(i for o, i in ops[-1] if o == "commit")
+        sl = st._slot(last)
+        U = int(sl.dd["num"].item())
+        nch = -(-(2 * cfg.mem_dim + cfg.edge_dim + cfg.time_dim + cfg.mem_dim) // 32)
+        mt = -(-U // 128)
+        ws = sl.ws.view(torch.float32)[: mt * nch * 2 * 128 * 32].reshape(-1, 2, 128, 32)  # [block][hi|lo][row][k]
+        ws_rows = ws.cpu().numpy()
+        extra = (sl.uts[:U].cpu().numpy(), sl.umail[:U].cpu().numpy())
+        st.run_ops(ops[-1])
+        torch.cuda.synchronize()
+        _C.check()
+        res.append((ws_rows, U, extra, st.memory.mem.cpu().numpy(), st.memory.mem_ts.cpu().numpy()))
+    (wa, ua, ea, ma, ta), (wb, ub, eb, mb, tb) = res
+    assert ua == ub
+    assert np.array_equal(ea[0], eb[0]) and np.array_equal(ea[1], eb[1])
+    # A images: only rows < U are defined by the build (padding rows are don't-care)
+    for blk in range(wa.shape[0]):
+        mt_i = blk // nch
+        rows = max(0, min(128, ua - 128 * mt_i))
+        assert np.array_equal(wa[blk, :, :rows], wb[blk, :, :rows]), blk
+    assert np.array_equal(ma, mb) and np.array_equal(ta, tb)
