@@ -5,4 +5,5 @@ CUDA path (``paper_2402_15113_b200``).  It draws inputs — event streams,
 negatives, edge features, GRU weights — and holds none of the method's
 arithmetic (no sampling, dedup, staleness, message, GRU or write-back logic).
 """
-from .events import CONFIGS, WorkloadConfig, make_workload, edge_features, gru_params, make_events  # noqa: F401
+from .events import (CONFIGS, WorkloadConfig, edge_features, gru_params, make_events, make_workload,  # noqa: F401
+                     node_features)

@@ -37,6 +37,7 @@ class WorkloadConfig:
     zipf_dst: float
     repeat: float
     mem_dim: int = 100      # PAPER.md L412 "memory dimensions of 100"
+    node_dim: int = 0       # |d_v| (Table `tab:datasets`): 413 for GDELT, else 0
     time_dim: int = 100     # reading G3
     fanout: int = 10        # PAPER.md L412 "10 most recent 1-hop neighbors"
     lam: float = 0.95       # PAPER.md L410 "lambda set to 0.95"
@@ -60,7 +61,8 @@ CONFIGS = {
     "reddit": WorkloadConfig("reddit", 10_984, 10_000, 672_447, 172, 600, 2, True, 4.0, "exp_floor", 1.0, 1.1, 0.6),
     "lastfm": WorkloadConfig("lastfm", 1980, 980, 1_293_103, 128, 600, 2, False, 106.0, "exp_floor", 0.6, 1.1, 0.5),
     "mooc": WorkloadConfig("mooc", 7144, 7047, 411_749, 128, 600, 2, False, 3.6, "exp_floor", 0.9, 1.2, 0.5),
-    "gdelt": WorkloadConfig("gdelt", 16_682, 0, 191_290_882, 186, 4000, 3, False, 0.1, "gdelt", 1.2, 1.2, 0.3),
+    "gdelt": WorkloadConfig("gdelt", 16_682, 0, 191_290_882, 186, 4000, 3, False, 0.1, "gdelt", 1.2, 1.2, 0.3,
+                            node_dim=413),
 }
 
 
@@ -158,6 +160,14 @@ def edge_features(seed: int, eid0: int, n: int, edge_dim: int) -> np.ndarray:
     z = _splitmix64(ctr)
     top = (z >> np.uint64(40)).astype(np.int64) - (1 << 23)
     return (top.astype(np.float32) * np.float32(2.0 ** -23)).astype(np.float32)
+
+
+def node_features(seed: int, num_nodes: int, node_dim: int) -> np.ndarray:
+    """f32 [num_nodes, node_dim] node features, the edge-feature recipe on a
+    separate counter stream (key seed ^ 0x5EED, so node and edge values differ)."""
+    if node_dim == 0:
+        return np.zeros((num_nodes, 0), np.float32)
+    return edge_features(seed ^ 0x5EED, 0, num_nodes, node_dim)
 
 
 def gru_params(mem_dim: int, mail_dim: int, time_dim: int, seed: int = 1234):

@@ -474,3 +474,24 @@ def test_p12_delta_t_population_and_heavy_tail():
     pop = oracle.delta_t_population(cfg.num_nodes, s, d, t)
     med = oracle.quantile_nearest_rank(pop, 0.5)
     assert oracle.quantile_nearest_rank(pop, 0.99) / max(med, 1.0) > 10  # S:L115 heavy tail
+
+
+# ------------------------------------------------------------------ row F2
+def test_f2_feature_fetch_closed_form():
+    """Rows whose values encode their own index (table[i, c] = 1000 i + c): every
+    fetched row must read back as 1000 * id + c, pads as zeros."""
+    from oracle.features import feature_fetch
+    rng = np.random.default_rng(0)
+    N, E, Hn, He = 50, 300, 7, 5
+    nfeat = (1000.0 * np.arange(N)[:, None] + np.arange(Hn)[None, :]).astype(np.float32)
+    efeat = (1000.0 * np.arange(E)[:, None] + np.arange(He)[None, :]).astype(np.float32)
+    sub = rng.integers(-1, N, (12, 4))
+    eid = rng.integers(-1, E, (12, 3))
+    on, oe = feature_fetch(sub, eid, nfeat, efeat)
+    for (r, s), v in np.ndenumerate(sub):
+        want = np.zeros(Hn) if v < 0 else 1000.0 * v + np.arange(Hn)
+        assert np.array_equal(on[r, s], want)
+    for (r, s), v in np.ndenumerate(eid):
+        want = np.zeros(He) if v < 0 else 1000.0 * v + np.arange(He)
+        assert np.array_equal(oe[r, s], want)
+    assert feature_fetch(sub, eid)[0] is None
