@@ -168,8 +168,10 @@ def algorithmic(cfg, stage_cfg, U):
     dedup = 2 * B * 8
     # fused ops: prep = A1 + A2 + A3 in one launch; build = the A5 half of update (its bytes); the
     # apply half (A6) keeps the name "update" and its FLOPs
+    nstride = (cfg.node_dim + 3) // 4 * 4
+    feats = R * (F + 1) * (4 + 8 * nstride) * (1 if cfg.node_dim else 0) + R * F * (4 + 8 * He)
     return dict(sample=sample, dedup=dedup, fetch=fetch, prep=sample + dedup + fetch, build=upd_bytes,
-                update=upd_bytes, update_flops=upd_flops, writeback=wb)
+                update=upd_bytes, update_flops=upd_flops, writeback=wb, features=feats)
 
 
 def run_mspipe(args):
@@ -193,7 +195,8 @@ def run_mspipe(args):
                    n_sim=cfg.n_sim)
     sc = StageConfig(cfg.num_nodes, cfg.mem_dim, cfg.edge_dim, cfg.time_dim, cfg.fanout, cfg.batch, k,
                      schedule=args.schedule, mitigation=mit, fetch_mail=args.fetch_mail,
-                     precision=_C.FP32_3XTF32 if args.gru == "tc" else _C.FP32_SIMT)
+                     precision=_C.FP32_3XTF32 if args.gru == "tc" else _C.FP32_SIMT,
+                     features=args.features, node_dim=cfg.node_dim)
     g = build_tcsr(cfg.num_nodes, w["src"], w["dst"], w["ts"], dev)
     # N > 1: node-id-sharded memory over NCCL (row E); MSPIPE_BENCH_REPLICAS=1 runs
     # N independent single-GPU replicas instead (ablation)
@@ -217,6 +220,10 @@ def run_mspipe(args):
         else:
             t = {kk: torch.from_numpy(w[kk]).to(dev) for kk in ("src", "dst", "ts", "neg", "ef")}
             st.bind_resident(t["src"], t["dst"], t["ts"], t["neg"], t["ef"])
+        if args.features:  # row F2: feature tables resident in HBM (the stream's edge features, node features)
+            from synth import node_features
+            st.bind_features(node_features(args.seed, cfg.num_nodes, cfg.node_dim) if cfg.node_dim else None,
+                             torch.from_numpy(w["ef"]).to(dev))
         return st
 
     def capture(st, timing):
@@ -261,7 +268,7 @@ def run_mspipe(args):
         for t, e0, e1 in pending:
             step_ms.append(e0.elapsed_time(e1))
             if st.timing:
-                for name in ("prep", "build", "sample", "dedup", "fetch", "update", "writeback"):
+                for name in ("prep", "build", "sample", "dedup", "fetch", "update", "writeback", "features"):
                     a, b = marks[t].get(name, (0, 0))
                     ends = st.timing.get(name + "_end", [])
                     for q in range(a, b):
@@ -346,20 +353,26 @@ def run_mspipe(args):
                        "traffic": _ncu_traffic(args.config, gather_op)}
     else:
         roof_gather = None
+    roof_features = None
+    if "features" in op_mean:
+        ach_f = alg["features"] / (op_mean["features"] / 1e3) / 1e9
+        roof_features = {"kernel": "k_feature_fetch (row F2)", "bound": "hbm", "achieved": ach_f,
+                         "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": ach_f / peaks["hbm_gbs"],
+                         "bytes_per_launch": alg["features"]}
     out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": K, "warmup": W,
            "ms_per_step": tot_ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
            "dtype": "f32", "data": "synthetic",
            "config": {"workload": args.config, "events": int(len(w["src"])), "num_nodes": cfg.num_nodes,
                       "batch": cfg.batch, "staleness_k": k, "schedule": args.schedule, "fanout": cfg.fanout,
                       "mem_dim": cfg.mem_dim, "edge_dim": cfg.edge_dim, "time_dim": cfg.time_dim,
-                      "mitigation": bool(mit), "fetch_mail": args.fetch_mail, "gru": "fp32-3xtf32-tcgen05" if args.gru == "tc" else "fp32-simt",
+                      "mitigation": bool(mit), "features": args.features, "fetch_mail": args.fetch_mail, "gru": "fp32-3xtf32-tcgen05" if args.gru == "tc" else "fp32-simt",
                       "l2": ("flushed (256 MiB write) between timed steps, outside the timed events"
                              if args.l2 == "flush" else "warm: steps back to back, state tables L2-resident"),
                       "parallelism": ("single" if ws == 1 else
                                       f"shard{ws}: node-id-sharded memory, NCCL all-to-all fetch + write-back, "
                                       f"global batch {G * cfg.batch}" if sharded else f"replicas{ws}")},
-           "roofline": roof, "roofline_gather": roof_gather, "gpu_launches": _launches(st.step_ops(), timed_batches, bool(mit),
-                                                       getattr(st, "fused", False), sharded), "clocks": clocks}
+           "roofline": roof, "roofline_gather": roof_gather, "roofline_features": roof_features, "gpu_launches": _launches(st.step_ops(), timed_batches, bool(mit),
+                                                       getattr(st, "fused", False), sharded, args.features), "clocks": clocks}
     if args.profile:
         if rank == 0:
             print(json.dumps(out))
@@ -389,7 +402,7 @@ def run_mspipe(args):
         dist.destroy_process_group()
 
 
-def _launches(steps, timed_batches, mit, fused, sharded=False):
+def _launches(steps, timed_batches, mit, fused, sharded=False, features=False):
     """Kernels of this library per timed step.  fused: prep = k_prep + k_build_x
     (+ k_mitigate), commit = k_gru_tc with the write-back in its epilogue; otherwise prep = sampler +
     dedup + gather (+ mitigation), commit = build + GEMM (or SIMT GRU) + write-back.  Sharded:
@@ -398,7 +411,7 @@ def _launches(steps, timed_batches, mit, fused, sharded=False):
     if sharded:
         per = {"prep": 6, "commit": 7}
         return int(sum(per[op] for t in timed_batches for op, _ in steps[t]))
-    per = {"prep": (2 if fused else 3) + (1 if mit else 0), "commit": 1 if fused else 3}
+    per = {"prep": (2 if fused else 3) + (1 if mit else 0) + (1 if features else 0), "commit": 1 if fused else 3}
     return int(sum(per[op] for t in timed_batches for op, _ in steps[t]))
 
 
@@ -500,6 +513,8 @@ def main():
     ap.add_argument("--l2", default="flush", choices=["flush", "warm"],
                     help="flush: 256 MiB write between timed steps (default); warm: back-to-back steps")
     ap.add_argument("--cpu-events", type=int, default=157_474)
+    ap.add_argument("--features", action="store_true",
+                    help="also run row F2 (feature fetch of the sampled subgraphs) in every step")
     ap.add_argument("--events", type=int, default=None,
                     help="first N events of the config's stream (default: all; GDELT's 191M needs a cap)")
     ap.add_argument("--profile", action="store_true", help="short run for ncu: no flush/e2e/cpu")

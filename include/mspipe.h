@@ -410,6 +410,27 @@ MSPIPE_API mspipe_status mspipe_shard_loopback(mspipe_memory* const* ranks, int3
                                     void* stream);
 
 /* ------------------------------------------------------------------------
+ * F2 — feature fetch ("Fetch feature", stage 2 of the pipeline, P:L189,
+ * P:L176-L180) for the sampled subgraphs.  Device pointers.
+ *   sub_ids      [R, fanout+1] subgraph node ids (mspipe_sample_* out_sub_ids;
+ *                -1 = pad), read when node_feat != NULL;
+ *   sampled_eids [R, fanout] eids of the sampled links (out_eid; -1 = pad),
+ *                read when edge_feat != NULL;
+ *   node_feat    [num_nodes, node_stride] (NULL: no node features; GDELT
+ *                |d_v| = 413, Table `tab:datasets` P:L395), edge_feat
+ *                [num_edges, edge_stride] (NULL: none), f32 row-major;
+ *   out_node_feat[r, s, :] = node_feat[sub_ids[r, s], :] (zeros for pads),
+ *   out_edge_feat[r, s, :] = edge_feat[sampled_eids[r, s], :] (zeros for pads).
+ * Strides are in floats; a stride that is a multiple of 4 needs 16-byte
+ * aligned tables (vector copies).  Ids >= num_nodes / num_edges give zero
+ * rows and raise MSPIPE_DEVERR_RANGE.  Errors: MSPIPE_EINVAL. */
+MSPIPE_API mspipe_status mspipe_feature_fetch(const int32_t* sub_ids, const int32_t* sampled_eids,
+                                   int64_t num_roots, int32_t fanout, const float* node_feat,
+                                   int64_t num_nodes, int32_t node_stride, const float* edge_feat,
+                                   int64_t num_edges, int32_t edge_stride, float* out_node_feat,
+                                   float* out_edge_feat, void* stream);
+
+/* ------------------------------------------------------------------------
  * F1 — minimal-staleness planner (MSPipe §3.2; Alg. 1)
  * ------------------------------------------------------------------------
  * Host functions (no GPU work).  Stages j = 1..5 of an iteration: sample,

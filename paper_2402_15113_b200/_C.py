@@ -34,7 +34,7 @@ EXPORTS = ("mspipe_abi_version", "mspipe_last_error", "mspipe_check", "mspipe_sa
            "mspipe_util_graph_begin", "mspipe_util_graph_end", "mspipe_util_graph_launch", "mspipe_util_graph_destroy",
            "mspipe_memory_double_buffer", "mspipe_memory_tables", "mspipe_memory_set_committed",
            "mspipe_plan_timeline", "mspipe_plan_min_staleness", "mspipe_stale_histogram",
-           "mspipe_memory_prep_build")
+           "mspipe_memory_prep_build", "mspipe_feature_fetch")
 XCHG_FETCH_IDS, XCHG_FETCH_ROWS, XCHG_COMMIT = 0, 1, 2
 
 
@@ -97,6 +97,7 @@ def lib():
                                          P, P, P, C.POINTER(Mitigation), C.POINTER(i64), P]
         L.mspipe_memory_prep_build.argtypes = [P, C.POINTER(Tcsr), i64, P, P, P, P, i64, i32, P, P, P, P, P, P, P,
                                                P, P, P, P, P, P, C.POINTER(i64), P, P, P, P, P, C.c_size_t, P]
+        L.mspipe_feature_fetch.argtypes = [P, P, i64, i32, P, i64, i32, P, i64, i32, P, P, P]
         L.mspipe_gru_workspace_size.argtypes = [P, i64]
         L.mspipe_gru_workspace_size.restype = C.c_size_t
         L.mspipe_message_build.argtypes = [P, P, i64, P, P, P, i64, P, P, P, P, P, i64, P, C.c_size_t, P]
@@ -467,6 +468,18 @@ def memory_prep_build(st: MemoryHandle, g: TcsrHandle, iteration, src, dst, neg,
                                        workspace.numel() * workspace.element_size(), stream_ptr(stream)),
         "mspipe_memory_prep_build")
     return int(v.value)
+
+
+def feature_fetch(sub_ids, sampled_eids, fanout, node_feat=None, edge_feat=None, out_node=None, out_edge=None,
+                  stream=None):
+    """F2: node-feature rows of the subgraph nodes, edge-feature rows of the sampled links."""
+    R = (sub_ids if sub_ids is not None else sampled_eids).shape[0]
+    _ck(lib().mspipe_feature_fetch(ptr(sub_ids), ptr(sampled_eids), int(R), int(fanout), ptr(node_feat),
+                                   node_feat.shape[0] if node_feat is not None else 0,
+                                   node_feat.shape[1] if node_feat is not None else 0, ptr(edge_feat),
+                                   edge_feat.shape[0] if edge_feat is not None else 0,
+                                   edge_feat.shape[1] if edge_feat is not None else 0, ptr(out_node), ptr(out_edge),
+                                   stream_ptr(stream)), "mspipe_feature_fetch")
 
 
 def gru_workspace_size(gru: GruHandle, num_events) -> int:

@@ -863,6 +863,26 @@ mspipe_status mspipe_util_event_record(void* event, void* stream) {
                      "util_event_record");
 }
 
+mspipe_status mspipe_feature_fetch(const int32_t* sub_ids, const int32_t* sampled_eids, int64_t num_roots,
+                                   int32_t fanout, const float* node_feat, int64_t num_nodes, int32_t node_stride,
+                                   const float* edge_feat, int64_t num_edges, int32_t edge_stride,
+                                   float* out_node_feat, float* out_edge_feat, void* stream) {
+  if (num_roots < 0 || fanout < 1 || (node_feat && (node_stride < 1 || !out_node_feat || num_nodes < 1)) ||
+      (edge_feat && (edge_stride < 1 || !out_edge_feat || num_edges < 1)))
+    return fail(MSPIPE_EINVAL, "feature_fetch: num_roots=%lld fanout=%d node_stride=%d edge_stride=%d",
+                (long long)num_roots, fanout, node_stride, edge_stride);
+  if (num_roots > 0 && ((node_feat && !sub_ids) || (edge_feat && !sampled_eids)))
+    return fail(MSPIPE_EINVAL, "feature_fetch: null sub_ids / sampled_eids");
+  if ((node_feat && ((uintptr_t)node_feat | (uintptr_t)out_node_feat) % 16 && node_stride % 4 == 0) ||
+      (edge_feat && ((uintptr_t)edge_feat | (uintptr_t)out_edge_feat) % 16 && edge_stride % 4 == 0))
+    return fail(MSPIPE_EINVAL, "feature_fetch: tables with a stride that is a multiple of 4 must be 16-byte aligned");
+  cudaError_t e = launch_feature_fetch(sub_ids, sampled_eids, num_roots, fanout, node_feat, num_nodes, node_stride,
+                                       edge_feat, num_edges, edge_stride, out_node_feat, out_edge_feat,
+                                       (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_status(e, "feature_fetch: launch");
+  return after_launch("feature_fetch");
+}
+
 mspipe_status mspipe_stale_histogram(const mspipe_tcsr* g, const int32_t* src, const int32_t* dst,
                                      int64_t num_events, int64_t batch, int32_t max_d, int64_t* out_hist,
                                      void* stream) {

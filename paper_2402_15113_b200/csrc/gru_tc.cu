@@ -41,7 +41,8 @@ constexpr int kStages = 3;
 constexpr int kThreads = 128;
 constexpr int kHBufBytes = kM * kJ * 4;   // h rows of the tile's hidden units (prefetched)
 constexpr int kRecvBytes = kM * kN * 4;   // K-split partials received from the cluster (S x 128/S rows)
-constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 1024 /*barriers*/ + kHBufBytes + kRecvBytes;
+constexpr int kSmemBytes =
+    kStages * kStageBytes + 1024 /*align*/ + 1024 /*barriers*/ + kHBufBytes + kRecvBytes + kN * 4 /*biases*/;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -365,6 +366,8 @@ __device__ __forceinline__ void store_h4(const TcArgs& a, int32_t u, int32_t nod
 
 // fused A7, rest of the row: mem_ts = mail_ts = t*, mail row = staged x[0:Dm];
 // the float4 columns of the mail row are spread over the hidden tiles.
+// (Prefetching these into shared memory during the main loop was measured
+// slower: the extra loads delay the warps' arrival at the cluster barrier.)
 __device__ __forceinline__ void commit_rows(const TcArgs& a, int32_t m0, int32_t U, int rb, int re, int jt,
                                             const int32_t* rownode) {
   const int J = (int)gridDim.y;
@@ -399,6 +402,8 @@ __global__ void __launch_bounds__(tc::kThreads, 1) k_gru_tc(TcArgs a) {
   int32_t* rownode = reinterpret_cast<int32_t*>(smem + kStages * kStageBytes + 512);  // [128] node of each row
   float4* hbuf =reinterpret_cast<float4*>(smem + kStages * kStageBytes + 1024);  // [128 rows][kJ/4]
   float4* recv = reinterpret_cast<float4*>(smem + kStages * kStageBytes + 1024 + kHBufBytes);
+  // this tile's gate biases, prefetched during the main loop
+  float* sbias = reinterpret_cast<float*>(smem + kStages * kStageBytes + 1024 + kHBufBytes + kRecvBytes);
 
   const GruDesc& d = a.d;
   PHASE(9);
@@ -504,6 +509,7 @@ __global__ void __launch_bounds__(tc::kThreads, 1) k_gru_tc(TcArgs a) {
         if (a.save_nodes && jt == 0 && node >= 0) a.save_nodes[u] = node;
       }
     }
+    for (int i = threadIdx.x - 64; i < kN; i += 64) sbias[i] = __ldg(d.bias + jt * kN + i);
     if (a.cu.stamp) catch_up(a, cta_q * 2 + (warp - 2), n_cta * 2, lane);
   }
   __syncwarp();
@@ -530,7 +536,7 @@ __global__ void __launch_bounds__(tc::kThreads, 1) k_gru_tc(TcArgs a) {
     }
   }
   PHASE(4);
-  const float* bias = d.bias + jt * kN;
+  const float* bias = sbias;
   if (S > 1) {
     // push this CTA's partial row m into the receive buffer of the rank that
     // finalises it: recv[src_rank][m - rb(owner)][16 x float4], float4 index
@@ -565,10 +571,10 @@ __global__ void __launch_bounds__(tc::kThreads, 1) k_gru_tc(TcArgs a) {
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           const int jj = q * 4 + e;
-          pr[e] = __uint_as_float(r0[jj]) + __ldg(bias + jj);
-          pz[e] = __uint_as_float(r0[kJ + jj]) + __ldg(bias + kJ + jj);
-          pnx[e] = __uint_as_float(r1[jj]) + __ldg(bias + 2 * kJ + jj);
-          pnh[e] = __uint_as_float(r1[kJ + jj]) + __ldg(bias + 3 * kJ + jj);
+          pr[e] = __uint_as_float(r0[jj]) + bias[jj];
+          pz[e] = __uint_as_float(r0[kJ + jj]) + bias[kJ + jj];
+          pnx[e] = __uint_as_float(r1[jj]) + bias[2 * kJ + jj];
+          pnh[e] = __uint_as_float(r1[kJ + jj]) + bias[3 * kJ + jj];
         }
         store_h4(a, u, rownode[m], j0, gates4(pr, pz, pnx, pnh, hbuf[m * (kJ / 4) + q]));
       }
@@ -602,10 +608,10 @@ __global__ void __launch_bounds__(tc::kThreads, 1) k_gru_tc(TcArgs a) {
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         const int jj = q * 4 + e;
-        pr[e] = (&acc[0].x)[e] + __ldg(bias + jj);
-        pz[e] = (&acc[1].x)[e] + __ldg(bias + kJ + jj);
-        pnx[e] = (&acc[2].x)[e] + __ldg(bias + 2 * kJ + jj);
-        pnh[e] = (&acc[3].x)[e] + __ldg(bias + 3 * kJ + jj);
+        pr[e] = (&acc[0].x)[e] + bias[jj];
+        pz[e] = (&acc[1].x)[e] + bias[kJ + jj];
+        pnx[e] = (&acc[2].x)[e] + bias[2 * kJ + jj];
+        pnh[e] = (&acc[3].x)[e] + bias[3 * kJ + jj];
       }
       store_h4(a, u, rownode[mm], j0, gates4(pr, pz, pnx, pnh, hbuf[mm * (kJ / 4) + q]));
     }

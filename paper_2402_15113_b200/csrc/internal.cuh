@@ -261,6 +261,10 @@ cudaError_t launch_gru_tc(const GruDesc& d, const float* wtc, float* xbuf, const
                           const int32_t* num_unique, float* out_mem, double* out_ts, float* out_mail,
                           int64_t mail_stride, cudaStream_t s, int parts = kGruBuild | kGruGemm,
                           const GruCommit* commit = nullptr);
+// features.cu
+cudaError_t launch_feature_fetch(const int32_t* sub, const int32_t* eid, int64_t R, int32_t F, const float* nfeat,
+                                 int64_t N, int32_t nstride, const float* efeat, int64_t E, int32_t estride,
+                                 float* out_n, float* out_e, cudaStream_t s);
 // stale.cu
 cudaError_t launch_stale_hist(const Tcsr& g, const int32_t* src, const int32_t* dst, int64_t E, int64_t B,
                               int32_t max_d, unsigned long long* hist, cudaStream_t s);

@@ -44,6 +44,8 @@ class StageConfig:
     fused: bool | None = None  # mspipe_memory_prep + message_build/gru_apply (default: when supported)
     double_buffer: bool | None = None  # two table sets (mspipe_memory_double_buffer); default: k >= 1
     plan: tuple | None = None  # schedule "plan": paper staleness k_i per iteration (row F1)
+    features: bool = False     # row F2: fetch node / edge features of the sampled subgraphs (bind_features)
+    node_dim: int = 0          # |d_v| (GDELT 413); rows padded to a multiple of 4 floats on the device
     # fused path without mitigation: message build inside the prep kernel (mspipe_memory_prep_build).
     # Off by default: measured slower on the wiki step (30.7 vs 26.0 us; the build waits for the
     # single dedup block and the longer prep kernel contends with the GEMM).  env MSPIPE_PREP_BUILD=1: A/B
@@ -107,6 +109,10 @@ def snapshot_versions(nb: int, k: int, schedule: str = "exact", plan=None):
     return [v[i] for i in range(1, nb + 1)]
 
 
+def _pad4(n):
+    return (n + 3) // 4 * 4
+
+
 class _Slot:
     def __init__(self, cfg: StageConfig, mail_stride: int, device, staged: bool, ws_bytes: int = 0):
         B, F, M = cfg.batch, cfg.fanout, cfg.mem_dim
@@ -121,6 +127,10 @@ class _Slot:
                       if cfg.mitigation else None)
         self.elig = torch.empty((2 * B,), dtype=torch.uint8, device=device) if cfg.mitigation else None
         self.dd = _C.alloc_dedup(B, device)
+        if cfg.features:  # row F2 outputs
+            self.nfeat = (torch.empty((3 * B, F + 1, _pad4(cfg.node_dim)), dtype=torch.float32, device=device)
+                          if cfg.node_dim else None)
+            self.efeat = torch.empty((3 * B, F, cfg.edge_dim), dtype=torch.float32, device=device)
         if ws_bytes:  # fused path: message_build(t+k) runs ahead of gru_apply(t), so its outputs are per slot
             self.ws = torch.empty((ws_bytes,), dtype=torch.uint8, device=device)
             self.uts = torch.empty((2 * B,), dtype=torch.float64, device=device)
@@ -241,6 +251,7 @@ class MemoryStage(_TimedOps):
         self._ev("sample")
         _C.sample_batch(self.tcsr, x["src"], x["dst"], x["neg"], x["ts"], cfg.fanout, samp)
         self._ev("sample_end")
+        self._features(sl, samp)
         self._ev("dedup")
         _C.memory_dedup(self.memory, x["src"], x["dst"], sl.dd)
         self._ev("dedup_end")
@@ -257,6 +268,51 @@ class MemoryStage(_TimedOps):
                                      sl.mail_ts[:m] if sl.mail_ts is not None else None, mit)
         self._ev("fetch_end")
         self.versions[i] = sl.version
+
+    def bind_features(self, node_feat=None, edge_feat=None):
+        """Row F2 tables, resident in HBM: node features [N, node_dim] (padded to a
+        multiple of 4 floats) and the edge features of the whole stream [E, He]."""
+        dev = self.device
+        self.feat_tables = {"node": None, "edge": None}
+        if node_feat is not None and self.cfg.node_dim:
+            nf = torch.as_tensor(node_feat, dtype=torch.float32)
+            t = torch.zeros((nf.shape[0], _pad4(nf.shape[1])), dtype=torch.float32, device=dev)
+            t[:, : nf.shape[1]] = nf.to(dev)
+            self.feat_tables["node"] = t
+        if edge_feat is not None:
+            self.feat_tables["edge"] = torch.as_tensor(edge_feat, dtype=torch.float32).to(dev).contiguous()
+        self.fstream = None
+        self._feat_done = []
+
+    def _features(self, sl, samp):
+        """F2 on its own stream, forked after the sampler: it reads only the sample."""
+        if not self.cfg.features:
+            return
+        if not hasattr(self, "feat_tables"):
+            raise RuntimeError("StageConfig.features needs bind_features(node_feat, edge_feat) first")
+        cur = torch.cuda.current_stream()
+        if self.fstream is None or self.fstream.device != cur.device:
+            self.fstream = torch.cuda.Stream(device=cur.device)
+        fork = torch.cuda.Event()
+        fork.record(cur)
+        self.fstream.wait_event(fork)
+        R = samp["sub"].shape[0]
+        with torch.cuda.stream(self.fstream):
+            self._ev("features")
+            _C.feature_fetch(samp["sub"], samp["eid"], self.cfg.fanout, self.feat_tables["node"],
+                             self.feat_tables["edge"], sl.nfeat[:R] if sl.nfeat is not None else None,
+                             sl.efeat[:R] if self.feat_tables["edge"] is not None else None)
+            self._ev("features_end")
+            done = torch.cuda.Event()
+            done.record(self.fstream)
+        self._feat_done.append(done)
+
+    def _join_features(self):
+        main = torch.cuda.current_stream()
+        for e in getattr(self, "_feat_done", []):
+            main.wait_event(e)
+        if getattr(self, "_feat_done", None):
+            self._feat_done = []
 
     def _mitigation(self, sl, x, n):
         cfg = self.cfg
@@ -279,6 +335,7 @@ class MemoryStage(_TimedOps):
                                               sl.mail_ts[:m] if sl.mail_ts is not None else None, self.gru,
                                               x["ef"], sl.uts[: 2 * n], sl.umail[: 2 * n], sl.ws)
             self._ev("prep_end")
+            self._features(sl, samp)
             self.versions[i] = sl.version
             if not self.memory.double_buffer:
                 self._fetched = torch.cuda.Event()  # the state tables have been read for batch i
@@ -290,6 +347,7 @@ class MemoryStage(_TimedOps):
                                     sl.mail[:m] if sl.mail is not None else None,
                                     sl.mail_ts[:m] if sl.mail_ts is not None else None, self._mitigation(sl, x, n))
         self._ev("prep_end")
+        self._features(sl, samp)
         self.versions[i] = sl.version
         if not self.memory.double_buffer:
             self._fetched = torch.cuda.Event()  # the state tables have been read for batch i
@@ -375,6 +433,7 @@ class MemoryStage(_TimedOps):
         if not overlap:
             for op, i in ops:
                 (self.prep if op == "prep" else self.commit)(i)
+            self._join_features()
             return
         main = torch.cuda.current_stream()
         if getattr(self, "side", None) is None or self.side.device != main.device:
@@ -409,6 +468,7 @@ class MemoryStage(_TimedOps):
                 self.writeback(i)
         if forked and not joined:
             main.wait_stream(self.side)
+        self._join_features()
 
     def run(self, nb=None):
         """All batches (or the first nb) in schedule order, one step at a time."""

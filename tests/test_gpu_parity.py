@@ -552,3 +552,42 @@ def test_prep_build_equals_prep_then_build(dev, k):
         rows = max(0, min(128, ua - 128 * mt_i))
         assert np.array_equal(wa[blk, :, :rows], wb[blk, :, :rows]), blk
     assert np.array_equal(ma, mb) and np.array_equal(ta, tb)
+
+
+# ------------------------------------------------------------------ row F2
+@pytest.mark.parametrize("name,E,fused", [("gdelt", 30_000, True), ("gdelt", 30_000, False), ("tiny", None, True)])
+def test_feature_fetch_equals_oracle(dev, name, E, fused):
+    """F2 inside the stage (its own stream, forked after the sampler): node-feature
+    rows of the subgraph nodes and edge-feature rows of the sampled links equal
+    the oracle's gather over the oracle sampler's ids, bit for bit; the state is
+    unchanged by it."""
+    from oracle.features import feature_fetch
+    from synth import node_features
+    w = make_workload(name, seed=9, num_events=E)
+    cfg = w["cfg"]
+    nf = node_features(9, cfg.num_nodes, cfg.node_dim) if cfg.node_dim else None
+    B = 500 if name == "gdelt" else cfg.batch
+    sc = StageConfig(cfg.num_nodes, cfg.mem_dim, cfg.edge_dim, cfg.time_dim, cfg.fanout, B, 1, fused=fused,
+                     features=True, node_dim=cfg.node_dim)
+    g = build_tcsr(cfg.num_nodes, w["src"], w["dst"], w["ts"], dev)
+    st = MemoryStage(sc, w["params"], g, dev)
+    t = {kk: _t(w[kk], dev) for kk in ("src", "dst", "ts", "neg", "ef")}
+    st.bind_resident(t["src"], t["dst"], t["ts"], t["neg"], t["ef"])
+    st.bind_features(nf, t["ef"])
+    ops = st.step_ops()
+    og = oracle.Graph(cfg.num_nodes, w["src"], w["dst"], w["ts"])
+    for o in ops[:6]:
+        st.run_ops(o)
+    torch.cuda.synchronize()
+    _C.check()
+    for i in sorted({i for o in ops[:6] for op, i in o if op == "prep"})[-2:]:
+        j0, j1 = (i - 1) * B, min(i * B, len(w["src"]))
+        roots = np.concatenate([w["src"][j0:j1], w["dst"][j0:j1], w["neg"][j0:j1]])
+        s = og.sample(roots, np.concatenate([w["ts"][j0:j1]] * 3), cfg.fanout)
+        sub = np.concatenate([roots[:, None], s["nbr"]], axis=1)
+        on, oe = feature_fetch(sub, s["eid"], nf, w["ef"])
+        sl = st._slot(i)
+        R = len(roots)
+        assert np.array_equal(sl.efeat[:R].cpu().numpy(), oe)
+        if nf is not None:
+            assert np.array_equal(sl.nfeat[:R, :, : cfg.node_dim].cpu().numpy(), on)
