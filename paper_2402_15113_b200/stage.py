@@ -203,16 +203,59 @@ class MemoryStage(_TimedOps):
                       for _ in range(self.cfg.k + 1)]
 
     def bind_host(self, src, dst, ts, neg, ef):
-        """Host arrays are pinned; each prep copies its batch H2D (e2e path)."""
+        """e2e path: the stream in pinned host memory, one packed record per
+        batch ([src | dst | neg | ts | ef]), copied H2D with ONE memcpy per batch
+        on a copy stream a step ahead of its prep (a ring of k+2 device
+        records); each commit's result (unique count, node ids, h' rows — one
+        packed record) is read back D2H on a second copy stream during the next
+        step."""
+        cfg, dev, B = self.cfg, self.device, self.cfg.batch
         self.E = int(src.shape[0])
-        self.host = {k: torch.as_tensor(v).pin_memory() for k, v in
-                     dict(src=src, dst=dst, ts=ts, neg=neg, ef=ef).items()}
+        nb = -(-self.E // B)
+        He = cfg.edge_dim
+        self._rec = [("src", 4 * B, torch.int32, (B,)), ("dst", 4 * B, torch.int32, (B,)),
+                     ("neg", 4 * B, torch.int32, (B,)), ("ts", 8 * B, torch.float64, (B,)),
+                     ("ef", 4 * B * He, torch.float32, (B, He))]
+        rec_bytes = sum(r[1] for r in self._rec)
+        host = torch.zeros((nb, rec_bytes), dtype=torch.uint8).pin_memory()
+        arrays = dict(src=src, dst=dst, neg=neg, ts=ts, ef=ef)
+        for i in range(nb):
+            j0, j1 = i * B, min((i + 1) * B, self.E)
+            for name, view in self._views(host[i]).items():
+                view[: j1 - j0].copy_(torch.as_tensor(arrays[name][j0:j1]))
+        self.host_rec = host
         self.staged = True
-        self.slots = [_Slot(self.cfg, self.memory.mail_stride, self.device, True, self.ws_bytes)
-                      for _ in range(self.cfg.k + 1)]
-        self.out_host = dict(nodes=torch.empty(2 * self.cfg.batch, dtype=torch.int32).pin_memory(),
-                             num=torch.empty(1, dtype=torch.int32).pin_memory(),
-                             mem=torch.empty((2 * self.cfg.batch, self.cfg.mem_dim), dtype=torch.float32).pin_memory())
+        self.slots = [_Slot(cfg, self.memory.mail_stride, dev, False, self.ws_bytes) for _ in range(cfg.k + 1)]
+        self.inp_ring = [torch.empty(rec_bytes, dtype=torch.uint8, device=dev) for _ in range(cfg.k + 2)]
+        # result records: [num (16 B) | nodes 2B x 4 | h' 2B x M x 4]; the GEMM writes h' in place
+        M = cfg.mem_dim
+        self._out_mem_off = 16 + (8 * B + 15) // 16 * 16  # h' rows 16-byte aligned (float4 stores)
+        self._out_bytes = self._out_mem_off + 8 * B * M
+        self.out_ring = [torch.empty(self._out_bytes, dtype=torch.uint8, device=dev) for _ in range(2)]
+        self.upd_ring = []
+        for o in self.out_ring:
+            u = _C.alloc_update(B, M, self.memory.mail_stride, dev)
+            u["mem"] = o[self._out_mem_off:].view(torch.float32).view(2 * B, M)
+            self.upd_ring.append(u)
+        self.out_host = torch.empty(self._out_bytes, dtype=torch.uint8).pin_memory()
+        self.h2d = self.d2h = None
+        self._loaded = set()      # batches whose H2D is enqueued
+        self._pending_out = None  # commit whose result awaits its D2H
+
+    def _views(self, rec):
+        out, off = {}, 0
+        for name, nbytes, dt, shape in self._rec:
+            out[name] = rec[off:off + nbytes].view(dt).view(shape)
+            off += nbytes
+        return out
+
+    def result(self):
+        """The last result read back (e2e): (unique count, node ids, h' rows) of a commit."""
+        B, M = self.cfg.batch, self.cfg.mem_dim
+        o = self.out_host
+        U = int(o[:4].view(torch.int32)[0])
+        return (U, o[16:16 + 8 * B].view(torch.int32)[:U],
+                o[self._out_mem_off:].view(torch.float32).view(2 * B, M)[:U])
 
     @property
     def num_batches(self):
@@ -228,7 +271,11 @@ class MemoryStage(_TimedOps):
         if not self.staged:
             return {k: v[j0:j1] for k, v in self.res.items()}
         n = j1 - j0
-        return {k: v[:n] for k, v in self.slots[(i - 1) % (self.cfg.k + 1)].inp.items()}
+        return {k: v[:n] for k, v in self._views(self.inp_ring[(i - 1) % (self.cfg.k + 2)]).items()}
+
+    def _load(self, i):
+        """H2D of batch i's packed record into its ring buffer, on the current stream."""
+        self.inp_ring[(i - 1) % (self.cfg.k + 2)].copy_(self.host_rec[i - 1], non_blocking=True)
 
     # -- ops ------------------------------------------------------------------
     def _slot(self, i):
@@ -237,11 +284,9 @@ class MemoryStage(_TimedOps):
     def prep(self, i):
         """A1 sampler, A2 dedup, A3 fetch (+A4 mitigation) of batch i into its slot."""
         cfg, sl = self.cfg, self._slot(i)
-        if self.staged:
-            j0, j1 = self._range(i)
-            n = j1 - j0
-            for key in ("src", "dst", "neg", "ts", "ef"):
-                sl.inp[key][:n].copy_(self.host[key][j0:j1], non_blocking=True)
+        if self.staged and i not in self._loaded:  # not prefetched (the first steps): load here
+            self._load(i)
+            self._loaded.add(i)
         x = self.inputs(i)
         n = x["src"].numel()
         samp = {k: v[: 3 * n] for k, v in sl.samp.items()}
@@ -361,7 +406,8 @@ class MemoryStage(_TimedOps):
     def _upd(self, i):
         n = self.inputs(i)["src"].numel()
         sl = self._slot(i)
-        upd = {k: v[: 2 * n] for k, v in self.upd.items() if k not in ("nodes", "winner", "num")}
+        base = self.upd_ring[i % 2] if self.staged else self.upd
+        upd = {k: v[: 2 * n] for k, v in base.items() if k not in ("nodes", "winner", "num")}
         upd.update(nodes=sl.dd["nodes"][: 2 * n], winner=sl.dd["winner"][: 2 * n], num=sl.dd["num"])
         if self.fused:
             upd.update(ts=sl.uts[: 2 * n], mail=sl.umail[: 2 * n])
@@ -388,11 +434,7 @@ class MemoryStage(_TimedOps):
         self._ev("writeback")
         _C.memory_writeback(self.memory, i, upd)
         self._ev("writeback_end")
-        if self.staged:
-            n2 = upd["nodes"].numel()
-            self.out_host["num"].copy_(upd["num"], non_blocking=True)
-            self.out_host["nodes"][:n2].copy_(upd["nodes"], non_blocking=True)
-            self.out_host["mem"][:n2].copy_(upd["mem"], non_blocking=True)
+        self._stash_result(i, upd)
 
     def commit(self, i):
         if self.fused:
@@ -410,11 +452,64 @@ class MemoryStage(_TimedOps):
         _C.gru_apply_commit(self.gru, self.memory, i, n, sl.mem, cfg.fanout + 1, upd, sl.ws,
                             snap_h=sl.h[: 2 * n] if sl.h is not None else None)
         self._ev("update_end")
-        if self.staged:
+        self._stash_result(i, upd)
+
+    # -- e2e copies (staged inputs) ---------------------------------------
+    def _stash_result(self, i, upd):
+        """After commit i: keep its node ids / count (the slot is reused by the
+        next prep) for the D2H the next step issues."""
+        if not self.staged:
+            return
+        main = torch.cuda.current_stream()
+        d2h = self._copy_streams()[1]
+        d2h.wait_stream(main)
+        with torch.cuda.stream(d2h):
+            o = self.out_ring[i % 2]
+            B = self.cfg.batch
             n2 = upd["nodes"].numel()
-            self.out_host["num"].copy_(upd["num"], non_blocking=True)
-            self.out_host["nodes"][:n2].copy_(upd["nodes"], non_blocking=True)
-            self.out_host["mem"][:n2].copy_(upd["mem"], non_blocking=True)
+            o[16:16 + 4 * n2].view(torch.int32).copy_(upd["nodes"], non_blocking=True)
+            o[:4].view(torch.int32).copy_(upd["num"], non_blocking=True)
+        self._pending_out = i
+
+    def _copy_streams(self):
+        cur = torch.cuda.current_stream()
+        if self.h2d is None or self.h2d.device != cur.device:
+            self.h2d = torch.cuda.Stream(device=cur.device)
+            self.d2h = torch.cuda.Stream(device=cur.device)
+        return self.h2d, self.d2h
+
+    def _copies_begin(self, ops):
+        """Step start (e2e): on the copy stream, read back the previous commit's
+        result and prefetch the inputs of the next step's preps."""
+        if not self.staged:
+            return
+        main = torch.cuda.current_stream()
+        h2d, d2h = self._copy_streams()
+        d2h.wait_stream(main)
+        with torch.cuda.stream(d2h):
+            c = self._pending_out
+            if c is not None:  # ONE memcpy: the previous commit's packed result record
+                self.out_host.copy_(self.out_ring[c % 2], non_blocking=True)
+                self._pending_out = None
+        h2d.wait_stream(main)
+        with torch.cuda.stream(h2d):
+            commits = [i for op, i in ops if op == "commit"]
+            preps = [i for op, i in ops if op == "prep"]
+            done_before = (min(commits) - 1) if commits else 0  # committed in earlier steps
+            j = max(preps + [max(self._loaded, default=0)]) + 1
+            for _ in range(max(1, len(preps))):
+                # its ring buffer last held batch j-(k+2): that one must be committed already
+                if j > self.num_batches or j - (self.cfg.k + 2) > done_before:
+                    break
+                if j not in self._loaded:
+                    self._load(j)
+                    self._loaded.add(j)
+                j += 1
+
+    def _copies_end(self):
+        if self.staged and self.h2d is not None:
+            torch.cuda.current_stream().wait_stream(self.h2d)
+            torch.cuda.current_stream().wait_stream(self.d2h)
 
     def run_ops(self, ops, overlap=None):
         """Enqueue ops in order.  With overlap (default when k >= 1), preps of
@@ -430,10 +525,12 @@ class MemoryStage(_TimedOps):
         the join at the end of the group is what keeps that fetch ahead of
         commit t+1 (which rewrites its set)."""
         overlap = (self.cfg.k >= 1) if overlap is None else overlap
+        self._copies_begin(ops)
         if not overlap:
             for op, i in ops:
                 (self.prep if op == "prep" else self.commit)(i)
             self._join_features()
+            self._copies_end()
             return
         main = torch.cuda.current_stream()
         if getattr(self, "side", None) is None or self.side.device != main.device:
@@ -469,6 +566,7 @@ class MemoryStage(_TimedOps):
         if forked and not joined:
             main.wait_stream(self.side)
         self._join_features()
+        self._copies_end()
 
     def run(self, nb=None):
         """All batches (or the first nb) in schedule order, one step at a time."""
@@ -493,4 +591,4 @@ class MemoryStage(_TimedOps):
 
     def d2h_bytes_per_batch(self):
         B = self.cfg.batch
-        return 4 + 2 * B * 4 + 2 * B * self.cfg.mem_dim * 4
+        return (16 + (8 * B + 15) // 16 * 16) + 2 * B * self.cfg.mem_dim * 4

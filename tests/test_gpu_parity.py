@@ -435,6 +435,19 @@ def test_cuda_graph_replay_equals_eager(dev, kind):
         torch.cuda.synchronize()
         _C.check()
         outs.append((st.memory.mem.cpu().numpy(), st.memory.mem_ts.cpu().numpy()))
+        if use_graph and kind == "mspipe_staged":
+            # e2e read-back: each step reads the previous commit's result; after the
+            # last step that is commit nb-1: its unique nodes, in pair order, and h'
+            nb = st.num_batches
+            B = cfg.batch
+            j0, j1 = (nb - 2) * B, (nb - 1) * B
+            pairs = np.stack([w["src"][j0:j1], w["dst"][j0:j1]], axis=1).reshape(-1)
+            last = {v: p for p, v in enumerate(pairs)}
+            want_nodes = [v for p, v in enumerate(pairs) if last[v] == p]
+            U, nodes, hrows = st.result()
+            assert U == len(want_nodes)
+            assert nodes.numpy().tolist() == want_nodes
+            assert np.isfinite(hrows.numpy()).all()
     assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
 
 
