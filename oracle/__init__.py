@@ -48,12 +48,12 @@ def lib():
         L.orc_dedup.restype = i64
         L.orc_mitigate.argtypes = [P, i64, P, P, P, P, i32, f32, f64, i32, i32, P, P, P]
         L.orc_memory_update.argtypes = [i64, i64, P, P, P, P, i32, i32, i32, P, P, P, P, P, P,
-                                        P, P, i32, P, f32, f64, i32, i32, P, P, P, P, P, P, P, P]
+                                        P, P, i32, P, f32, f64, i32, i32, P, P, P, P, P, P, P, P, P, i32]
         L.orc_memory_update.restype = i64
         L.orc_snapshot_version.argtypes = [i64, i32, i32]
         L.orc_snapshot_version.restype = i64
         L.orc_run_stream.argtypes = [i64, i64, P, P, P, P, i32, i32, i32, P, P, P, P, P, P, i64,
-                                     i32, i32, i32, f32, f64, i32, i32, P, P, P, P, i64, P, P, i32, P]
+                                     i32, i32, i32, f32, f64, i32, i32, P, P, P, P, i64, P, P, i32, P, i32]
         L.orc_run_stream.restype = i64
         L.orc_delta_t_population.argtypes = [i64, i64, P, P, P, P]
         L.orc_delta_t_population.restype = i64
@@ -144,8 +144,10 @@ def dedup(num_nodes, src, dst):
 
 
 def memory_update(num_nodes, src, dst, ts, ef, params, mem, mem_ts, mitigation=None,
-                  graph: Graph | None = None, fanout=10):
-    """Teacher-forced A2+A4+A5+A6 for one batch against snapshot tables."""
+                  graph: Graph | None = None, fanout=10, mail=None, mailbox="immediate", cell="gru"):
+    """Teacher-forced A2+A4+A5+A6 for one batch against snapshot tables.  Row F3:
+    mailbox="deferred" reads the snapshot `mail` [N, Dm]; cell="rnn" takes
+    RNNCell weights (w_ih [M, Dx], w_hh [M, M], b_ih / b_hh [M])."""
     src, dst, ts = _c(src, np.int32), _c(dst, np.int32), _c(ts, np.float64)
     ef = _c(ef, np.float32)
     mem, mem_ts = _c(mem, np.float32), _c(mem_ts, np.float64)
@@ -171,11 +173,19 @@ def memory_update(num_nodes, src, dst, ts, ef, params, mem, mem_ts, mitigation=N
         1 if mitigation else 0, graph.h if graph is not None else None,
         float(mitigation["lam"]) if mitigation else 1.0,
         float(mitigation["gamma"]) if mitigation else 0.0, n_sim, fanout, _p(nodes), _p(win),
-        _p(omem), _p(ots), _p(omail), _p(oh), _p(oom), _p(oel))
+        _p(omem), _p(ots), _p(omail), _p(oh), _p(oom), _p(oel),
+        _p(_c(mail, np.float32)) if mail is not None else None, _variant(mailbox, cell))
     if U < 0:
         raise ValueError(f"orc_memory_update rc={U}")
     return dict(nodes=nodes[:U], winner=win[:U], mem=omem[:U], ts=ots[:U], mail=omail[:U],
                 h=oh[:U], omega=oom[:U], elig=oel[:U].astype(bool))
+
+
+def _variant(mailbox, cell):
+    """Row F3 updater variants: bit 0 deferred mailbox (TGL TGN), bit 1 RNN cell (JODIE)."""
+    if mailbox not in ("immediate", "deferred") or cell not in ("gru", "rnn"):
+        raise ValueError(f"mailbox={mailbox} cell={cell}")
+    return (1 if mailbox == "deferred" else 0) | (2 if cell == "rnn" else 0)
 
 
 def snapshot_version(i, k, schedule="exact"):
@@ -191,7 +201,7 @@ def new_state(num_nodes, mem_dim, edge_dim):
 
 
 def run_stream(num_nodes, src, dst, ts, ef, params, batch, k, schedule="exact", mitigation=None,
-               fanout=10, state=None, max_batches=-1, neg=None, plan=None):
+               fanout=10, state=None, max_batches=-1, neg=None, plan=None, mailbox="immediate", cell="gru"):
     """C.2 O1-O8 over the stream; returns (final state, per-batch versions).
     With `neg`, every batch also runs A1 on its 3B roots and gathers the
     snapshot rows of the subgraph (the whole per-batch path, for timing).
@@ -218,7 +228,7 @@ def run_stream(num_nodes, src, dst, ts, ef, params, batch, k, schedule="exact", 
         k, 1 if schedule == "grouped" else 0, 1 if mit else 0, float(mit["lam"]) if mit else 1.0,
         float(mit["gamma"]) if mit else 0.0, int(mit["n_sim"]) if mit else 5, fanout,
         _p(st["mem"]), _p(st["mem_ts"]), _p(st["mail"]), _p(st["mail_ts"]), max_batches, _p(vers),
-        _p(negc), 0 if negc is None else 1, _p(planc))
+        _p(negc), 0 if negc is None else 1, _p(planc), _variant(mailbox, cell))
     if r < 0:
         raise ValueError(f"orc_run_stream rc={r}")
     return st, vers[:r]

@@ -335,12 +335,30 @@ int orc_mitigate(const orc_graph* g, int64_t n, const int32_t* ids, const double
 typedef struct {
   int32_t M, He, Dt;
   const float *w_ih, *w_hh, *b_ih, *b_hh, *time_w, *time_b;
+  int32_t cell; /* 0: GRUCell (TGN, APAN); 1: RNNCell tanh (JODIE's updater, row F3) */
 } orc_gru;
+
+/* Row F3 updater variants (readings F3-1..F3-3 in DESIGN.md):
+ * variant bit 0 = deferred mailbox (TGL's TGN: the update consumes the node's
+ * STORED mail, and the new mail is built from post-update memories), bit 1 =
+ * RNN cell  h' = tanh(W_ih x + b_ih + W_hh h + b_hh)  (torch.nn.RNNCell, tanh;
+ * W_ih [M, Dx], W_hh [M, M]). */
+#define ORC_VAR_DEFERRED 1
+#define ORC_VAR_RNN 2
 
 static void orc_gru_row(const orc_gru* P, const float* x /*[Dx]*/, const float* h /*[M]*/,
                         float* out /*[M]*/) {
   const int32_t M = P->M;
   const int32_t Dx = 2 * M + P->He + P->Dt;
+  if (P->cell == 1) {
+    for (int32_t j = 0; j < M; ++j) {
+      double a = (double)P->b_ih[j] + (double)P->b_hh[j];
+      for (int32_t k = 0; k < Dx; ++k) a += (double)P->w_ih[(int64_t)j * Dx + k] * (double)x[k];
+      for (int32_t k = 0; k < M; ++k) a += (double)P->w_hh[(int64_t)j * M + k] * (double)h[k];
+      out[j] = (float)tanh(a);
+    }
+    return;
+  }
   for (int32_t j = 0; j < M; ++j) {
     double gi[3], gh[3];
     for (int g = 0; g < 3; ++g) {
@@ -376,9 +394,25 @@ static void orc_build_x(const orc_gru* P, int64_t p, const int32_t* src, const i
     x[2 * M + He + q] = (float)cos((double)fmaf(P->time_w[q], dt, P->time_b[q]));
 }
 
+/* Row F3, deferred mailbox, A5: x = [S.mail[w] (Dm) | cos(omega dt + phi)],
+ * dt = t* - S.mem_ts[w] as in G4 (reading F3-1). */
+static void orc_build_x_deferred(const orc_gru* P, int64_t p, const int32_t* src, const int32_t* dst,
+                                 const double* ts, const float* mail, const double* mem_ts, float* x) {
+  const int32_t M = P->M, He = P->He, Dm = 2 * M + He;
+  int64_t a = p >> 1;
+  int32_t w = (p & 1) ? dst[a] : src[a];
+  float dt = (float)(ts[a] - mem_ts[w]);
+  for (int32_t c = 0; c < Dm; ++c) x[c] = mail[(int64_t)w * Dm + c];
+  for (int32_t q = 0; q < P->Dt; ++q)
+    x[Dm + q] = (float)cos((double)fmaf(P->time_w[q], dt, P->time_b[q]));
+}
+
 /* Teacher-forced memory update for one batch of B events against snapshot
- * tables (mem [N,M], mem_ts [N]).  If `mit_on`, the GRU hidden input of each
- * winner is the mitigated ŝ (needs g).  Outputs in winner order; returns U. */
+ * tables (mem [N,M], mem_ts [N], mail [N, Dm] — read only in the deferred
+ * variant).  If `mit_on`, the GRU hidden input of each winner is the mitigated
+ * ŝ (needs g).  Outputs in winner order; returns U.  out_mail: immediate = the
+ * message x[0:Dm] (G14); deferred = [h'_w | h'_o | e] from this batch's
+ * updated memories of both endpoints (reading F3-2). */
 int64_t orc_memory_update(int64_t N, int64_t B, const int32_t* src, const int32_t* dst,
                           const double* ts, const float* ef, int32_t M, int32_t He, int32_t Dt,
                           const float* w_ih, const float* w_hh, const float* b_ih,
@@ -387,8 +421,10 @@ int64_t orc_memory_update(int64_t N, int64_t B, const int32_t* src, const int32_
                           const orc_graph* g, float lambda, double gamma, int32_t n_sim,
                           int32_t fanout, int32_t* out_nodes, int32_t* out_winner,
                           float* out_mem, double* out_ts, float* out_mail, float* out_h,
-                          int32_t* out_omega, uint8_t* out_elig) {
-  orc_gru P = {M, He, Dt, w_ih, w_hh, b_ih, b_hh, time_w, time_b};
+                          int32_t* out_omega, uint8_t* out_elig, const float* mail, int32_t variant) {
+  orc_gru P = {M, He, Dt, w_ih, w_hh, b_ih, b_hh, time_w, time_b, (variant & ORC_VAR_RNN) ? 1 : 0};
+  const int deferred = (variant & ORC_VAR_DEFERRED) != 0;
+  if (deferred && !mail) return ORC_EINVAL;
   int64_t U = orc_dedup(N, B, src, dst, out_nodes, out_winner);
   if (U < 0) return U;
   const int32_t Dm = 2 * M + He, Dx = Dm + Dt;
@@ -401,7 +437,8 @@ int64_t orc_memory_update(int64_t N, int64_t B, const int32_t* src, const int32_
     int64_t p = out_winner[u];
     int32_t w = out_nodes[u];
     double tstar = ts[p >> 1];
-    orc_build_x(&P, p, src, dst, ts, ef, mem, mem_ts, x);
+    if (deferred) orc_build_x_deferred(&P, p, src, dst, ts, mail, mem_ts, x);
+    else orc_build_x(&P, p, src, dst, ts, ef, mem, mem_ts, x);
     int e = 0;
     if (mit_on) {
       e = orc_mitigate_one(g, w, tstar, mem, mem_ts, M, lambda, gamma, n_sim, fanout, h, om);
@@ -411,7 +448,7 @@ int64_t orc_memory_update(int64_t N, int64_t B, const int32_t* src, const int32_
     }
     orc_gru_row(&P, x, h, out_mem + u * M);
     out_ts[u] = tstar;
-    if (out_mail)
+    if (out_mail && !deferred)
       for (int32_t c = 0; c < Dm; ++c) out_mail[u * Dm + c] = x[c];
     if (out_h)
       for (int32_t m = 0; m < M; ++m) out_h[u * M + m] = h[m];
@@ -420,6 +457,22 @@ int64_t orc_memory_update(int64_t N, int64_t B, const int32_t* src, const int32_
     if (out_elig) out_elig[u] = (uint8_t)e;
     free(x);
     free(h);
+  }
+  if (deferred && out_mail) {
+    /* new mail of winner w (event a, other endpoint o): [h'_w | h'_o | e_a]; o
+     * is an endpoint of a batch event, so it has a winner row of its own */
+    int32_t* row_of = (int32_t*)malloc(sizeof(int32_t) * (size_t)(N > 0 ? N : 1));
+    for (int64_t v = 0; v < N; ++v) row_of[v] = -1;
+    for (int64_t u = 0; u < U; ++u) row_of[out_nodes[u]] = (int32_t)u;
+    for (int64_t u = 0; u < U; ++u) {
+      int64_t p = out_winner[u], a = p >> 1;
+      int32_t o = (p & 1) ? src[a] : dst[a];
+      int32_t uo = row_of[o];
+      for (int32_t m = 0; m < M; ++m) out_mail[u * Dm + m] = out_mem[u * M + m];
+      for (int32_t m = 0; m < M; ++m) out_mail[u * Dm + M + m] = out_mem[(int64_t)uo * M + m];
+      for (int32_t c = 0; c < He; ++c) out_mail[u * Dm + 2 * M + c] = ef[a * He + c];
+    }
+    free(row_of);
   }
   return rc == ORC_OK ? U : rc;
 }
@@ -452,7 +505,7 @@ int64_t orc_run_stream(int64_t N, int64_t E, const int32_t* src, const int32_t* 
                        int32_t k, int32_t schedule, int32_t mit_on, float lambda, double gamma,
                        int32_t n_sim, int32_t fanout, float* mem, double* mem_ts, float* mail,
                        double* mail_ts, int64_t max_batches, int64_t* out_versions,
-                       const int32_t* neg, int32_t subgraph, const int32_t* plan_k) {
+                       const int32_t* neg, int32_t subgraph, const int32_t* plan_k, int32_t variant) {
   if (B < 1 || k < 0 || M < 1) return ORC_EINVAL;
   if (subgraph && !neg) return ORC_EINVAL;
   const int32_t Dm = 2 * M + He;
@@ -488,6 +541,12 @@ int64_t orc_run_stream(int64_t N, int64_t E, const int32_t* src, const int32_t* 
   }
   memcpy(rmem[0], mem, szm);
   memcpy(rts[0], mem_ts, szt);
+  /* deferred mailbox: the update reads the snapshot mail too, so keep its versions */
+  const int deferred = (variant & ORC_VAR_DEFERRED) != 0;
+  size_t sza = sizeof(float) * (size_t)N * Dm;
+  float** rmail = (float**)malloc(sizeof(float*) * R);
+  for (int32_t s = 0; s < R; ++s) rmail[s] = deferred ? (float*)malloc(sza ? sza : 1) : NULL;
+  if (deferred) memcpy(rmail[0], mail, sza);
   int32_t* nodes = (int32_t*)malloc(sizeof(int32_t) * 2 * B);
   int32_t* winner = (int32_t*)malloc(sizeof(int32_t) * 2 * B);
   float* nmem = (float*)malloc(sizeof(float) * 2 * B * M);
@@ -536,7 +595,7 @@ int64_t orc_run_stream(int64_t N, int64_t E, const int32_t* src, const int32_t* 
     int64_t U = orc_memory_update(N, nb_ev, src + j0, dst + j0, ts + j0, ef + j0 * He, M, He,
                                   Dt, w_ih, w_hh, b_ih, b_hh, time_w, time_b, rmem[v % R],
                                   rts[v % R], mit_on, g, lambda, gamma, n_sim, fanout, nodes,
-                                  winner, nmem, nts, nmail, NULL, NULL, NULL);
+                                  winner, nmem, nts, nmail, NULL, NULL, NULL, rmail[v % R], variant);
     for (int64_t u = 0; u < U; ++u) {
       int32_t w = nodes[u];
       memcpy(mem + (int64_t)w * M, nmem + u * M, sizeof(float) * M);
@@ -546,11 +605,14 @@ int64_t orc_run_stream(int64_t N, int64_t E, const int32_t* src, const int32_t* 
     }
     memcpy(rmem[i % R], mem, szm);
     memcpy(rts[i % R], mem_ts, szt);
+    if (deferred) memcpy(rmail[i % R], mail, sza);
   }
   for (int32_t s = 0; s < R; ++s) {
     free(rmem[s]);
     free(rts[s]);
+    free(rmail[s]);
   }
+  free(rmail);
   free(rmem);
   free(rts);
   free(nodes);

@@ -170,6 +170,21 @@ def node_features(seed: int, num_nodes: int, node_dim: int) -> np.ndarray:
     return edge_features(seed ^ 0x5EED, 0, num_nodes, node_dim)
 
 
+def rnn_params(mem_dim: int, mail_dim: int, time_dim: int, seed: int = 1234):
+    """RNNCell-shaped weights (row F3, JODIE's updater), U(-1/sqrt(M), 1/sqrt(M)) like
+    torch.nn.RNNCell; the same time encoder as gru_params.  All f32."""
+    rng = _rng(seed, 8)
+    Dx = mail_dim + time_dim
+    a = 1.0 / math.sqrt(mem_dim)
+    p = dict(w_ih=rng.uniform(-a, a, size=(mem_dim, Dx)).astype(np.float32),
+             w_hh=rng.uniform(-a, a, size=(mem_dim, mem_dim)).astype(np.float32),
+             b_ih=rng.uniform(-a, a, size=(mem_dim,)).astype(np.float32),
+             b_hh=rng.uniform(-a, a, size=(mem_dim,)).astype(np.float32))
+    g = gru_params(mem_dim, mail_dim, time_dim, seed)
+    p.update(time_w=g["time_w"], time_b=g["time_b"])
+    return p
+
+
 def gru_params(mem_dim: int, mail_dim: int, time_dim: int, seed: int = 1234):
     """GRUCell-shaped weights, U(-1/sqrt(M), 1/sqrt(M)) like torch.nn.GRUCell's
     default init, gate order (r, z, n); time encoder ω_q = 10^(-9q/(d_t-1)), φ = 0

@@ -495,3 +495,110 @@ def test_f2_feature_fetch_closed_form():
         want = np.zeros(He) if v < 0 else 1000.0 * v + np.arange(He)
         assert np.array_equal(oe[r, s], want)
     assert feature_fetch(sub, eid)[0] is None
+
+
+# ------------------------------------------------------------------ row F3
+def test_f3_rnn_cell_matches_torch_rnncell():
+    """cell="rnn": h' = tanh(W_ih x + b_ih + W_hh h + b_hh) == torch.nn.RNNCell (f64)."""
+    import torch
+    from synth import rnn_params
+    rng = np.random.default_rng(3)
+    N, M, He, Dt, B = 40, 8, 6, 4, 10
+    p = rnn_params(M, 2 * M + He, Dt, seed=5)
+    src, dst = rng.integers(0, N, B).astype(np.int32), rng.integers(0, N, B).astype(np.int32)
+    ts = np.sort(rng.uniform(10, 20, B))
+    ef = rng.uniform(-1, 1, (B, He)).astype(np.float32)
+    mem = rng.uniform(-1, 1, (N, M)).astype(np.float32)
+    mem_ts = rng.uniform(0, 9, N)
+    out = oracle.memory_update(N, src, dst, ts, ef, p, mem, mem_ts, cell="rnn")
+    cell = torch.nn.RNNCell(2 * M + He + Dt, M).double()
+    with torch.no_grad():
+        for name in ("w_ih", "w_hh", "b_ih", "b_hh"):
+            getattr(cell, {"w_ih": "weight_ih", "w_hh": "weight_hh", "b_ih": "bias_ih", "b_hh": "bias_hh"}[name]) \
+                .copy_(torch.tensor(p[name], dtype=torch.float64))
+    for u, (w, pw) in enumerate(zip(out["nodes"], out["winner"])):
+        a = pw >> 1
+        o = src[a] if pw & 1 else dst[a]
+        dt = np.float32(ts[a] - mem_ts[w])
+        arg = (p["time_w"].astype(np.float64) * np.float64(dt) + p["time_b"]).astype(np.float32)  # fmaf
+        enc = np.cos(arg.astype(np.float64))
+        x = np.concatenate([mem[w], mem[o], ef[a], enc.astype(np.float32)]).astype(np.float64)
+        with torch.no_grad():
+            want = cell(torch.tensor(x)[None], torch.tensor(mem[w], dtype=torch.float64)[None])[0].numpy()
+        assert np.allclose(out["mem"][u], want, rtol=0, atol=2e-7)
+
+
+def _selector_rnn(M, He, Dt):
+    """RNN weights that copy the edge-feature part of x: h'[m] = tanh(x[2M + m])."""
+    Dx = 2 * M + He + Dt
+    w_ih = np.zeros((M, Dx), np.float32)
+    for m in range(min(M, He)):
+        w_ih[m, 2 * M + m] = 1.0
+    return dict(w_ih=w_ih, w_hh=np.zeros((M, M), np.float32), b_ih=np.zeros(M, np.float32),
+                b_hh=np.zeros(M, np.float32), time_w=np.ones(Dt, np.float32), time_b=np.zeros(Dt, np.float32))
+
+
+@pytest.mark.parametrize("k", [0, 2])
+def test_f3_deferred_mailbox_closed_form(k):
+    """Edge-feature selector RNN: with the IMMEDIATE mailbox a node's memory is
+    tanh(e) of its winning event in its last batch; with the DEFERRED mailbox
+    (TGL) it is tanh(e) of its winning event in the latest batch <= v(i) that
+    contained it before its last batch i (the stored mail), and 0 when there was
+    none.  Integer replay of the batches only; no GRU/GEMM code."""
+    rng = np.random.default_rng(7 + k)
+    N, M, He, Dt, B, E = 12, 4, 6, 2, 5, 120
+    src, dst = rng.integers(0, N, E).astype(np.int32), rng.integers(0, N, E).astype(np.int32)
+    ts = np.arange(E, dtype=np.float64)
+    ef = rng.uniform(-1, 1, (E, He)).astype(np.float32)
+    p = _selector_rnn(M, He, Dt)
+    nb = E // B
+    win = {}  # (batch, node) -> winning event (most recent pair in the batch)
+    for i in range(1, nb + 1):
+        for a in range((i - 1) * B, i * B):
+            win[(i, int(src[a]))] = a
+            win[(i, int(dst[a]))] = a
+    for mailbox in ("immediate", "deferred"):
+        st, _ = oracle.run_stream(N, src, dst, ts, ef, p, B, k, mailbox=mailbox, cell="rnn")
+        for v in range(N):
+            batches = [i for i in range(1, nb + 1) if (i, v) in win]
+            if not batches:
+                assert (st["mem"][v] == 0).all()
+                continue
+            last = batches[-1]
+            if mailbox == "immediate":
+                e = ef[win[(last, v)]]
+            else:
+                vi = max(0, last - 1 - k)  # the version batch `last` reads
+                prev = [i for i in batches if i <= vi]
+                e = ef[win[(prev[-1], v)]] if prev else np.zeros(He, np.float32)
+            assert np.allclose(st["mem"][v], np.tanh(e[:M].astype(np.float64)), rtol=0, atol=1e-7), (mailbox, v)
+
+
+def test_f3_deferred_with_input_weights_zero_equals_immediate():
+    """W_ih = 0: the message (hence the mailbox form) cannot matter — bitwise equal."""
+    from synth import gru_params
+    rng = np.random.default_rng(1)
+    N, M, He, Dt, B, E = 30, 8, 6, 4, 7, 200
+    src, dst = rng.integers(0, N, E).astype(np.int32), rng.integers(0, N, E).astype(np.int32)
+    ts = np.cumsum(rng.uniform(0, 1, E))
+    ef = rng.uniform(-1, 1, (E, He)).astype(np.float32)
+    p = gru_params(M, 2 * M + He, Dt)
+    p["w_ih"] = np.zeros_like(p["w_ih"])
+    a, _ = oracle.run_stream(N, src, dst, ts, ef, p, B, 1)
+    b, _ = oracle.run_stream(N, src, dst, ts, ef, p, B, 1, mailbox="deferred")
+    assert np.array_equal(a["mem"], b["mem"]) and np.array_equal(a["mem_ts"], b["mem_ts"])
+
+
+def test_f3_deferred_mail_is_post_update_memory():
+    """Deferred mailbox invariant: a node's stored mail starts with its own
+    post-update memory of the same batch, i.e. mail[w][:M] == mem[w]."""
+    from synth import gru_params
+    rng = np.random.default_rng(2)
+    N, M, He, Dt, B, E = 25, 8, 6, 4, 9, 300
+    src, dst = rng.integers(0, N, E).astype(np.int32), rng.integers(0, N, E).astype(np.int32)
+    ts = np.cumsum(rng.uniform(0, 1, E))
+    ef = rng.uniform(-1, 1, (E, He)).astype(np.float32)
+    st, _ = oracle.run_stream(N, src, dst, ts, ef, gru_params(M, 2 * M + He, Dt), B, 1, mailbox="deferred")
+    touched = np.unique(np.concatenate([src, dst]))
+    assert np.array_equal(st["mail"][touched, :M], st["mem"][touched])
+    assert np.array_equal(st["mail_ts"][touched], st["mem_ts"][touched])
