@@ -232,6 +232,51 @@ MSPIPE_API mspipe_status mspipe_gru_create(mspipe_gru** out, int32_t mem_dim, in
                                 void* stream);
 MSPIPE_API mspipe_status mspipe_gru_destroy(mspipe_gru* p);
 
+/* Row F3 — memory-updater variants the paper trains (TGN, JODIE,
+ * APAN "modified from TGL"; readings F3-1..F3-3 in DESIGN.md).
+ *   cell MSPIPE_CELL_GRU: as mspipe_gru_create (TGN, APAN);
+ *   cell MSPIPE_CELL_RNN: torch.nn.RNNCell (tanh), h' = tanh(W_ih x + b_ih +
+ *     W_hh h + b_hh), w_ih [M, Dx], w_hh [M, M], b_ih [M], b_hh [M] (JODIE's
+ *     updater);
+ *   mailbox MSPIPE_MAILBOX_IMMEDIATE: the message is built from the current
+ *     event (G14; all the entry points above);
+ *   mailbox MSPIPE_MAILBOX_DEFERRED (TGL's TGN): the update consumes the
+ *     node's STORED mail, x = [S.mail[w] (Dm) | cos(w dt + p)], dt = t* -
+ *     S.mem_ts[w]; the new mail [h'_w | h'_o | e] is built from the updated
+ *     memories after the commit.  Path: mspipe_memory_prep (fetching mail
+ *     rows) -> mspipe_message_build_deferred -> mspipe_gru_apply_commit with
+ *     new_mail = NULL -> mspipe_memory_mail_deferred.
+ * Variants need precision MSPIPE_FP32_3XTF32 (else MSPIPE_EUNSUPPORTED);
+ * mspipe_memory_update / mspipe_message_build refuse a deferred handle. */
+enum { MSPIPE_CELL_GRU = 0, MSPIPE_CELL_RNN = 1 };
+enum { MSPIPE_MAILBOX_IMMEDIATE = 0, MSPIPE_MAILBOX_DEFERRED = 1 };
+MSPIPE_API mspipe_status mspipe_updater_create(mspipe_gru** out, int32_t mem_dim, int32_t edge_dim,
+                                    int32_t time_dim, int32_t precision, int32_t cell,
+                                    int32_t mailbox, int64_t max_events, const float* w_ih,
+                                    const float* w_hh, const float* b_ih, const float* b_hh,
+                                    const float* time_w, const float* time_b, void* stream);
+/* A5 of a deferred-mailbox handle: the GEMM operand images of the U winners
+ * from the snapshot rows the prep fetched (snap_mem / snap_mem_ts / snap_mail
+ * [.., mail_stride], row of winner pair p = root row (p odd ? B + p/2 : p/2)
+ * times snap_step), out_ts [<=2B] = the winners' event times. */
+MSPIPE_API mspipe_status mspipe_message_build_deferred(const mspipe_gru* gru, const double* ts,
+                                            int64_t num_events, const float* snap_mem,
+                                            const double* snap_mem_ts, const float* snap_mail,
+                                            int64_t mail_stride, int64_t snap_step,
+                                            const int32_t* winner, const int32_t* num_unique,
+                                            double* out_ts, void* workspace, size_t ws_bytes,
+                                            void* stream);
+/* After commit `commit_version` (== committed, else MSPIPE_EORDER) of a
+ * deferred-mailbox batch: mail[w] = [mem[w] | mem[o] | e_ev], mail_ts[w] =
+ * t_ev for every winner w (event ev, other endpoint o) — reading the memories
+ * that commit wrote.  Stream-ordered after the commit and before the next
+ * fetch of that version. */
+MSPIPE_API mspipe_status mspipe_memory_mail_deferred(mspipe_memory* st, int64_t commit_version,
+                                          const int32_t* src, const int32_t* dst, const double* ts,
+                                          const float* edge_feat, int64_t num_events,
+                                          const int32_t* nodes, const int32_t* winner,
+                                          const int32_t* num_unique, void* stream);
+
 /* A2 — pair expansion and most-recent-message aggregation of one batch.
  *   Event a gives p = 2a (node src_a, other dst_a) and p = 2a+1 (node dst_a,
  *   other src_a); win(w) = max{p : node_p = w} (the message "generated by the

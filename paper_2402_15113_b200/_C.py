@@ -34,7 +34,8 @@ EXPORTS = ("mspipe_abi_version", "mspipe_last_error", "mspipe_check", "mspipe_sa
            "mspipe_util_graph_begin", "mspipe_util_graph_end", "mspipe_util_graph_launch", "mspipe_util_graph_destroy",
            "mspipe_memory_double_buffer", "mspipe_memory_tables", "mspipe_memory_set_committed",
            "mspipe_plan_timeline", "mspipe_plan_min_staleness", "mspipe_stale_histogram",
-           "mspipe_memory_prep_build", "mspipe_feature_fetch")
+           "mspipe_memory_prep_build", "mspipe_feature_fetch", "mspipe_updater_create",
+           "mspipe_message_build_deferred", "mspipe_memory_mail_deferred")
 XCHG_FETCH_IDS, XCHG_FETCH_ROWS, XCHG_COMMIT = 0, 1, 2
 
 
@@ -97,6 +98,9 @@ def lib():
                                          P, P, P, C.POINTER(Mitigation), C.POINTER(i64), P]
         L.mspipe_memory_prep_build.argtypes = [P, C.POINTER(Tcsr), i64, P, P, P, P, i64, i32, P, P, P, P, P, P, P,
                                                P, P, P, P, P, P, C.POINTER(i64), P, P, P, P, P, C.c_size_t, P]
+        L.mspipe_updater_create.argtypes = [C.POINTER(P), i32, i32, i32, i32, i32, i32, i64, P, P, P, P, P, P, P]
+        L.mspipe_message_build_deferred.argtypes = [P, P, i64, P, P, P, i64, i64, P, P, P, P, C.c_size_t, P]
+        L.mspipe_memory_mail_deferred.argtypes = [P, i64, P, P, P, P, i64, P, P, P, P]
         L.mspipe_feature_fetch.argtypes = [P, P, i64, i32, P, i64, i32, P, i64, i32, P, P, P]
         L.mspipe_gru_workspace_size.argtypes = [P, i64]
         L.mspipe_gru_workspace_size.restype = C.c_size_t
@@ -262,17 +266,25 @@ class TcsrHandle:
         self.c = Tcsr(int(num_nodes), int(nbr.numel()), ptr(indptr), ptr(nbr), ptr(eid), ptr(ts))
 
 
+CELL_GRU, CELL_RNN = 0, 1
+MAILBOX_IMMEDIATE, MAILBOX_DEFERRED = 0, 1
+
+
 class GruHandle:
+    """Memory updater (mspipe_updater_create): GRU (default) or RNN cell (row F3),
+    immediate or deferred mailbox (row F3)."""
+
     def __init__(self, mem_dim, edge_dim, time_dim, params: dict, device, precision=FP32_3XTF32, max_events=600,
-                 stream=None):
+                 stream=None, cell=CELL_GRU, mailbox=MAILBOX_IMMEDIATE):
         self.dims = (mem_dim, edge_dim, time_dim)
+        self.cell, self.mailbox = cell, mailbox
         self.w = {k: torch.as_tensor(v, dtype=torch.float32).contiguous().to(device) for k, v in params.items()}
         h = C.c_void_p()
-        _ck(lib().mspipe_gru_create(C.byref(h), mem_dim, edge_dim, time_dim, precision, int(max_events),
-                                    ptr(self.w["w_ih"]),
-                                    ptr(self.w["w_hh"]), ptr(self.w["b_ih"]), ptr(self.w["b_hh"]),
-                                    ptr(self.w["time_w"]), ptr(self.w["time_b"]), stream_ptr(stream)),
-            "mspipe_gru_create")
+        _ck(lib().mspipe_updater_create(C.byref(h), mem_dim, edge_dim, time_dim, precision, int(cell), int(mailbox),
+                                        int(max_events), ptr(self.w["w_ih"]),
+                                        ptr(self.w["w_hh"]), ptr(self.w["b_ih"]), ptr(self.w["b_hh"]),
+                                        ptr(self.w["time_w"]), ptr(self.w["time_b"]), stream_ptr(stream)),
+            "mspipe_updater_create")
         self.h = h
 
     def __del__(self):
@@ -482,6 +494,22 @@ def feature_fetch(sub_ids, sampled_eids, fanout, node_feat=None, edge_feat=None,
                                    stream_ptr(stream)), "mspipe_feature_fetch")
 
 
+def message_build_deferred(gru: GruHandle, ts, snap_mem, snap_mem_ts, snap_mail, snap_step, winner, num, out_ts,
+                           workspace, stream=None):
+    """Row F3 A5 (deferred mailbox): operand images from the snapshot mail rows."""
+    _ck(lib().mspipe_message_build_deferred(gru.h, ptr(ts), ts.numel(), ptr(snap_mem), ptr(snap_mem_ts),
+                                            ptr(snap_mail), snap_mail.shape[1], int(snap_step), ptr(winner), ptr(num),
+                                            ptr(out_ts), ptr(workspace), workspace.numel() * workspace.element_size(),
+                                            stream_ptr(stream)), "mspipe_message_build_deferred")
+
+
+def memory_mail_deferred(st: MemoryHandle, commit_version, src, dst, ts, edge_feat, nodes, winner, num, stream=None):
+    """Row F3: after a deferred-mailbox commit, mail = [mem[w] | mem[o] | e] from the committed memories."""
+    _ck(lib().mspipe_memory_mail_deferred(st.h, int(commit_version), ptr(src), ptr(dst), ptr(ts), ptr(edge_feat),
+                                          src.numel(), ptr(nodes), ptr(winner), ptr(num), stream_ptr(stream)),
+        "mspipe_memory_mail_deferred")
+
+
 def gru_workspace_size(gru: GruHandle, num_events) -> int:
     return int(lib().mspipe_gru_workspace_size(gru.h, int(num_events)))
 
@@ -509,7 +537,7 @@ def gru_apply_commit(gru: GruHandle, st: MemoryHandle, commit_version, num_event
     state rows of version commit_version and upd["mem"] (h' in winner order)."""
     _ck(lib().mspipe_gru_apply_commit(gru.h, st.h, int(commit_version), int(num_events), ptr(snap_mem),
                                       int(snap_step), ptr(snap_h), ptr(upd["nodes"]), ptr(upd["winner"]),
-                                      ptr(upd["num"]), ptr(upd["ts"]), ptr(upd["mail"]), ptr(upd.get("mem")),
+                                      ptr(upd["num"]), ptr(upd["ts"]), ptr(upd.get("mail")), ptr(upd.get("mem")),
                                       ptr(workspace), workspace.numel() * workspace.element_size(),
                                       stream_ptr(stream)), "mspipe_gru_apply_commit")
 

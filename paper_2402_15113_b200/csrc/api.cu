@@ -342,7 +342,20 @@ mspipe_status mspipe_gru_create(mspipe_gru** out, int32_t mem_dim, int32_t edge_
                                 const float* w_ih, const float* w_hh, const float* b_ih,
                                 const float* b_hh, const float* time_w, const float* time_b,
                                 void* stream) {
+  return mspipe_updater_create(out, mem_dim, edge_dim, time_dim, precision, MSPIPE_CELL_GRU,
+                               MSPIPE_MAILBOX_IMMEDIATE, max_events, w_ih, w_hh, b_ih, b_hh, time_w, time_b, stream);
+}
+
+mspipe_status mspipe_updater_create(mspipe_gru** out, int32_t mem_dim, int32_t edge_dim, int32_t time_dim,
+                                    int32_t precision, int32_t cell, int32_t mailbox, int64_t max_events,
+                                    const float* w_ih, const float* w_hh, const float* b_ih, const float* b_hh,
+                                    const float* time_w, const float* time_b, void* stream) {
   if (!out) return fail(MSPIPE_EINVAL, "gru_create: out is NULL");
+  if ((cell != MSPIPE_CELL_GRU && cell != MSPIPE_CELL_RNN) ||
+      (mailbox != MSPIPE_MAILBOX_IMMEDIATE && mailbox != MSPIPE_MAILBOX_DEFERRED))
+    return fail(MSPIPE_EINVAL, "updater_create: cell=%d mailbox=%d", cell, mailbox);
+  if ((cell != MSPIPE_CELL_GRU || mailbox != MSPIPE_MAILBOX_IMMEDIATE) && precision != MSPIPE_FP32_3XTF32)
+    return fail(MSPIPE_EUNSUPPORTED, "updater_create: variants need precision MSPIPE_FP32_3XTF32");
   *out = nullptr;
   if (mem_dim < 4 || mem_dim % 4 || edge_dim < 0 || time_dim < 0 || max_events < 1 || max_events > 16384)
     return fail(MSPIPE_EINVAL, "gru_create: mem_dim=%d edge_dim=%d time_dim=%d max_events=%lld (1..16384)",
@@ -360,6 +373,8 @@ mspipe_status mspipe_gru_create(mspipe_gru** out, int32_t mem_dim, int32_t edge_
   d.Dx = d.Dm + time_dim;
   d.K = d.Dx + mem_dim;
   d.Kpad = (d.K + 31) / 32 * 32;
+  d.cell = cell;
+  d.mailbox = mailbox;
   d.Npad = (mem_dim + 31) / 32 * 128;
   if (precision == MSPIPE_FP32_3XTF32 && d.Kpad / 32 > 64) {
     delete p;
@@ -398,6 +413,46 @@ mspipe_status mspipe_gru_create(mspipe_gru** out, int32_t mem_dim, int32_t edge_
   return MSPIPE_OK;
 }
 
+mspipe_status mspipe_message_build_deferred(const mspipe_gru* gru, const double* ts, int64_t num_events,
+                                            const float* snap_mem, const double* snap_mem_ts,
+                                            const float* snap_mail, int64_t mail_stride, int64_t snap_step,
+                                            const int32_t* winner, const int32_t* num_unique, double* out_ts,
+                                            void* workspace, size_t ws_bytes, void* stream) {
+  if (!gru) return fail(MSPIPE_EINVAL, "message_build_deferred: NULL handle");
+  if (gru->d.mailbox != MSPIPE_MAILBOX_DEFERRED || gru->precision != MSPIPE_FP32_3XTF32)
+    return fail(MSPIPE_EUNSUPPORTED, "message_build_deferred: needs a deferred-mailbox MSPIPE_FP32_3XTF32 handle");
+  if (num_events < 0 || num_events > gru->max_events || snap_step < 1 || mail_stride < gru->d.Dm)
+    return fail(MSPIPE_EINVAL, "message_build_deferred: num_events=%lld snap_step=%lld mail_stride=%lld",
+                (long long)num_events, (long long)snap_step, (long long)mail_stride);
+  if (num_events == 0) return MSPIPE_OK;
+  if (!ts || !snap_mem || !snap_mem_ts || !snap_mail || !winner || !num_unique || !out_ts || !workspace ||
+      ws_bytes < mspipe_gru_workspace_size(gru, num_events))
+    return fail(MSPIPE_EINVAL, "message_build_deferred: null argument or workspace too small");
+  cudaError_t e = launch_build_deferred(gru->d, (float*)workspace, ts, num_events, snap_mem, snap_mem_ts, snap_mail,
+                                        mail_stride, snap_step, winner, num_unique, out_ts, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_status(e, "message_build_deferred: launch");
+  return after_launch("message_build_deferred");
+}
+
+mspipe_status mspipe_memory_mail_deferred(mspipe_memory* st, int64_t commit_version, const int32_t* src,
+                                          const int32_t* dst, const double* ts, const float* edge_feat,
+                                          int64_t num_events, const int32_t* nodes, const int32_t* winner,
+                                          const int32_t* num_unique, void* stream) {
+  if (!st) return fail(MSPIPE_EINVAL, "memory_mail_deferred: NULL handle");
+  if (st->world != 1) return fail(MSPIPE_EUNSUPPORTED, "memory_mail_deferred: world > 1");
+  if (commit_version != st->committed)
+    return fail(MSPIPE_EORDER, "memory_mail_deferred: commit_version=%lld but committed=%lld",
+                (long long)commit_version, (long long)st->committed);
+  if (num_events < 0) return fail(MSPIPE_EINVAL, "memory_mail_deferred: num_events=%lld", (long long)num_events);
+  if (num_events == 0) return MSPIPE_OK;
+  if (!src || !dst || !ts || (st->edge_dim > 0 && !edge_feat) || !nodes || !winner || !num_unique)
+    return fail(MSPIPE_EINVAL, "memory_mail_deferred: null argument");
+  const TableSet t = table_set(st, commit_version);
+  launch_mail_deferred(src, dst, ts, edge_feat, st->edge_dim, nodes, winner, num_unique, 2 * num_events, t.mem,
+                       st->mem_dim, t.mail, t.mail_ts, st->mail_stride, st->num_nodes, (cudaStream_t)stream);
+  return after_launch("memory_mail_deferred");
+}
+
 mspipe_status mspipe_gru_destroy(mspipe_gru* p) {
   if (!p) return MSPIPE_OK;
   if (p->wpack) cudaFree(p->wpack);
@@ -434,6 +489,8 @@ mspipe_status mspipe_memory_update(mspipe_memory* st, const mspipe_gru* gru, con
   if (!st || !gru) return fail(MSPIPE_EINVAL, "memory_update: NULL handle");
   if (gru->d.M != st->mem_dim || gru->d.He != st->edge_dim)
     return fail(MSPIPE_EINVAL, "memory_update: GRU dims (M=%d He=%d) != memory dims (M=%d He=%d)", gru->d.M, gru->d.He, st->mem_dim, st->edge_dim);
+  if (gru->d.mailbox != MSPIPE_MAILBOX_IMMEDIATE)
+    return fail(MSPIPE_EUNSUPPORTED, "memory_update: deferred-mailbox handle (use mspipe_message_build_deferred)");
   if (num_events < 0 || num_events > gru->max_events || snap_step < 1)
     return fail(MSPIPE_EINVAL, "memory_update: num_events=%lld (<= max_events %lld of the GRU handle) snap_step=%lld",
                 (long long)num_events, (long long)gru->max_events, (long long)snap_step);
@@ -525,8 +582,8 @@ mspipe_status mspipe_memory_prep_build(mspipe_memory* st, const mspipe_tcsr* g, 
                                        double* out_commit_ts, float* out_commit_mail, void* workspace,
                                        size_t ws_bytes, void* stream) {
   if (!gru) return fail(MSPIPE_EINVAL, "memory_prep_build: NULL GRU handle");
-  if (gru->precision != MSPIPE_FP32_3XTF32)
-    return fail(MSPIPE_EUNSUPPORTED, "memory_prep_build: only for precision MSPIPE_FP32_3XTF32");
+  if (gru->precision != MSPIPE_FP32_3XTF32 || gru->d.mailbox != MSPIPE_MAILBOX_IMMEDIATE)
+    return fail(MSPIPE_EUNSUPPORTED, "memory_prep_build: only for an immediate-mailbox MSPIPE_FP32_3XTF32 handle");
   if (!st || gru->d.M != st->mem_dim || gru->d.He != st->edge_dim)
     return fail(MSPIPE_EINVAL, "memory_prep_build: NULL memory handle or dims differ from the GRU's");
   if (num_events > gru->max_events)
@@ -622,6 +679,8 @@ mspipe_status mspipe_message_build(const mspipe_gru* gru, const double* ts, int6
   if (!gru) return fail(MSPIPE_EINVAL, "message_build: NULL handle");
   if (gru->precision != MSPIPE_FP32_3XTF32)
     return fail(MSPIPE_EUNSUPPORTED, "message_build: only for precision MSPIPE_FP32_3XTF32 (use mspipe_memory_update)");
+  if (gru->d.mailbox != MSPIPE_MAILBOX_IMMEDIATE)
+    return fail(MSPIPE_EUNSUPPORTED, "message_build: deferred-mailbox handle (use mspipe_message_build_deferred)");
   if (num_events < 0 || num_events > gru->max_events || snap_step < 1 || mail_stride < gru->d.Dm || mail_stride % 4)
     return fail(MSPIPE_EINVAL, "message_build: num_events=%lld snap_step=%lld mail_stride=%lld", (long long)num_events,
                 (long long)snap_step, (long long)mail_stride);
@@ -678,8 +737,9 @@ mspipe_status mspipe_gru_apply_commit(const mspipe_gru* gru, mspipe_memory* st,
   if (num_events > 0) {
     if (ws_bytes < mspipe_gru_workspace_size(gru, num_events) || !workspace)
       return fail(MSPIPE_EINVAL, "gru_apply_commit: workspace of %zu bytes too small", ws_bytes);
-    if (!snap_mem || !nodes || !winner || !num_unique || !new_ts || !new_mail)
-      return fail(MSPIPE_EINVAL, "gru_apply_commit: null input");
+    if (!snap_mem || !nodes || !winner || !num_unique || !new_ts ||
+        (!new_mail && gru->d.mailbox != MSPIPE_MAILBOX_DEFERRED))
+      return fail(MSPIPE_EINVAL, "gru_apply_commit: null input (new_mail may be NULL only for a deferred mailbox)");
   }
   const int64_t max_n = 2 * num_events;
   // double-buffered: the GEMM kernel catches up the previous commit's rows

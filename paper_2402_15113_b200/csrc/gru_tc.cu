@@ -202,7 +202,14 @@ __global__ void k_gru_pack_tc(const float* __restrict__ w_ih, const float* __res
     const int32_t g = n / tc::kJ, jj = n % tc::kJ, j = jt * tc::kJ + jj, k = c * tc::kKC + kk;
     const int32_t M = d.M;
     float v = 0.f;
-    if (j < M) {
+    if (j < M && d.cell == MSPIPE_CELL_RNN) {
+      // RNNCell: only the n blocks, n_x = W_ih x, n_h = W_hh h (tanh(n_x + n_h) in the epilogue)
+      if (k < d.Dx) {
+        if (g == 2) v = w_ih[(int64_t)j * d.Dx + k];
+      } else if (k < d.K) {
+        if (g == 3) v = w_hh[(int64_t)j * M + (k - d.Dx)];
+      }
+    } else if (j < M) {
       if (k < d.Dx) {
         if (g < 3) v = w_ih[(int64_t)(g * M + j) * d.Dx + k];
       } else if (k < d.K) {
@@ -220,7 +227,10 @@ __global__ void k_gru_pack_tc(const float* __restrict__ w_ih, const float* __res
     *reinterpret_cast<float*>(blk + tc::kBTile + off) = lo;
     if (c == 0 && kk == 0) {
       float b = 0.f;
-      if (j < M) {
+      if (j < M && d.cell == MSPIPE_CELL_RNN) {
+        if (g == 2) b = b_ih[j];
+        else if (g == 3) b = b_hh[j];
+      } else if (j < M) {
         if (g == 0) b = b_ih[j] + b_hh[j];
         else if (g == 1) b = b_ih[M + j] + b_hh[M + j];
         else if (g == 2) b = b_ih[2 * M + j];
@@ -344,9 +354,14 @@ __global__ void __launch_bounds__(256) k_build_x(TcArgs a) {
 
 // GRUCell gates (G5): r = σ(.), z = σ(.), n = tanh(x_n + r h_n), h' = (1 - z) n + z h.
 __device__ __forceinline__ float4 gates4(const float* pr, const float* pz, const float* pnx, const float* pnh,
-                                         float4 h) {
+                                         float4 h, int32_t cell) {
   const float* hv = &h.x;
   float out[4];
+  if (cell == MSPIPE_CELL_RNN) {  // RNNCell (row F3): h' = tanh(W_ih x + b_ih + W_hh h + b_hh)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) out[e] = tanhf(pnx[e] + pnh[e]);
+    return make_float4(out[0], out[1], out[2], out[3]);
+  }
 #pragma unroll
   for (int e = 0; e < 4; ++e) {
     const float r = 1.0f / (1.0f + expf(-pr[e]));
@@ -371,6 +386,14 @@ __device__ __forceinline__ void store_h4(const TcArgs& a, int32_t u, int32_t nod
 __device__ __forceinline__ void commit_rows(const TcArgs& a, int32_t m0, int32_t U, int rb, int re, int jt,
                                             const int32_t* rownode) {
   const int J = (int)gridDim.y;
+  if (!a.new_mail) {  // deferred mailbox (row F3): mem_ts only; the mail rows follow the commit
+    if (jt == 0)
+      for (int mm = rb + (int)threadIdx.x; mm < re; mm += blockDim.x) {
+        const int32_t u = m0 + mm, node = rownode[mm];
+        if (u < U && node >= 0) a.commit_mem_ts[node] = __ldg(a.new_ts + u);
+      }
+    return;
+  }
   const int Q = (int)(a.mail_stride / 4);
   const int c0 = jt * Q / J, c1 = (jt + 1) * Q / J, nq = c1 - c0;
   const float4* src = reinterpret_cast<const float4*>(a.new_mail);
@@ -576,7 +599,7 @@ __global__ void __launch_bounds__(tc::kThreads, 1) k_gru_tc(TcArgs a) {
           pnx[e] = __uint_as_float(r1[jj]) + bias[2 * kJ + jj];
           pnh[e] = __uint_as_float(r1[kJ + jj]) + bias[3 * kJ + jj];
         }
-        store_h4(a, u, rownode[m], j0, gates4(pr, pz, pnx, pnh, hbuf[m * (kJ / 4) + q]));
+        store_h4(a, u, rownode[m], j0, gates4(pr, pz, pnx, pnh, hbuf[m * (kJ / 4) + q], d.cell));
       }
     }
     if (a.commit_mem) commit_rows(a, m0, U, 0, kM, jt, rownode);
@@ -613,11 +636,95 @@ __global__ void __launch_bounds__(tc::kThreads, 1) k_gru_tc(TcArgs a) {
         pnx[e] = (&acc[2].x)[e] + bias[2 * kJ + jj];
         pnh[e] = (&acc[3].x)[e] + bias[3 * kJ + jj];
       }
-      store_h4(a, u, rownode[mm], j0, gates4(pr, pz, pnx, pnh, hbuf[mm * (kJ / 4) + q]));
+      store_h4(a, u, rownode[mm], j0, gates4(pr, pz, pnx, pnh, hbuf[mm * (kJ / 4) + q], d.cell));
     }
     if (a.commit_mem) commit_rows(a, m0, U, rb, rb + R, jt, rownode);
     PHASE(8);
   }
+}
+
+// Row F3, deferred mailbox (TGL's TGN), A5: x = [S.mail[w] (Dm) | cos(w dt + p) | h = S.mem[w]],
+// dt = t* - S.mem_ts[w]; one warp per (winner row, K chunk), as k_build_x.
+__global__ void __launch_bounds__(256) k_build_deferred(GruDesc d, float* xbuf, const double* ts, int64_t B,
+                                                        const float* snap_mem, const double* snap_ts,
+                                                        const float* snap_mail, int64_t mail_stride, int64_t step,
+                                                        const int32_t* winner, const int32_t* num_unique,
+                                                        double* out_ts) {
+  pdl_begin();
+  const int32_t U = __ldg(num_unique);
+  const int32_t nchunks = d.Kpad / tc::kKC;
+  const int64_t items = (int64_t)U * nchunks;
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < items; w += nwarps) {
+    const int32_t u = (int32_t)(w / nchunks), c = (int32_t)(w % nchunks);
+    const int32_t k = c * tc::kKC + lane;
+    const int32_t p = __ldg(winner + u);
+    const int64_t ev = p >> 1;
+    const int64_t rw = (p & 1) ? B + ev : ev;  // the winner's root row of the subgraph
+    float v = 0.f;
+    if (k < d.Dm) v = __ldg(snap_mail + rw * step * mail_stride + k);
+    else if (k < d.Dx) {
+      const float dt = (float)(__ldg(ts + ev) - __ldg(snap_ts + rw * step));
+      v = time_cos(fmaf(__ldg(d.time_w + (k - d.Dm)), dt, __ldg(d.time_b + (k - d.Dm))));
+    } else if (k < d.K) v = __ldg(snap_mem + rw * step * d.M + (k - d.Dx));
+    tc::store_a(xbuf, nchunks, u, k, v);
+    if (c == 0 && lane == 0) out_ts[u] = __ldg(ts + ev);
+  }
+}
+
+cudaError_t launch_build_deferred(const GruDesc& d, float* xbuf, const double* ts, int64_t num_events,
+                                  const float* snap_mem, const double* snap_mem_ts, const float* snap_mail,
+                                  int64_t mail_stride, int64_t snap_step, const int32_t* winner,
+                                  const int32_t* num_unique, double* out_ts, cudaStream_t s) {
+  const int64_t warps = 2 * num_events * (d.Kpad / tc::kKC);
+  int64_t blocks = (warps * 32 + 255) / 256;
+  const int64_t cap = (int64_t)num_sms() * 8;
+  if (blocks > cap) blocks = cap;
+  if (blocks < 1) blocks = 1;
+  return launch_k(k_build_deferred, dim3((unsigned)blocks), dim3(256), 0, s, 1, d, xbuf, ts, num_events, snap_mem,
+                  snap_mem_ts, snap_mail, mail_stride, snap_step, winner, num_unique, out_ts);
+}
+
+// Row F3, deferred mailbox, after the commit: the new mail of winner w (event
+// ev, other endpoint o) from the committed memories, [mem[w] | mem[o] | e_ev]
+// (o was updated in the same commit), mail_ts[w] = t_ev.  One warp per winner.
+__global__ void __launch_bounds__(256) k_mail_deferred(const int32_t* src, const int32_t* dst, const double* ts,
+                                                       const float* ef, int32_t He, const int32_t* nodes,
+                                                       const int32_t* winner, const int32_t* num_unique,
+                                                       const float* mem, int32_t M, float* mail, double* mail_ts,
+                                                       int64_t mail_stride, int64_t num_nodes) {
+  pdl_begin();
+  const int32_t U = __ldg(num_unique);
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t u = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; u < U; u += nwarps) {
+    const int32_t w = __ldg(nodes + u), p = __ldg(winner + u);
+    const int64_t ev = p >> 1;
+    const int32_t o = (p & 1) ? __ldg(src + ev) : __ldg(dst + ev);
+    if (w < 0 || w >= num_nodes || o < 0 || o >= num_nodes) continue;
+    float* row = mail + (int64_t)w * mail_stride;
+    for (int c = lane; c < mail_stride; c += 32) {
+      float v = 0.f;
+      if (c < M) v = mem[(int64_t)w * M + c];
+      else if (c < 2 * M) v = mem[(int64_t)o * M + (c - M)];
+      else if (c < 2 * M + He) v = __ldg(ef + ev * He + (c - 2 * M));
+      row[c] = v;
+    }
+    if (lane == 0) mail_ts[w] = __ldg(ts + ev);
+  }
+}
+
+void launch_mail_deferred(const int32_t* src, const int32_t* dst, const double* ts, const float* ef, int32_t He,
+                          const int32_t* nodes, const int32_t* winner, const int32_t* num_unique, int64_t max_n,
+                          const float* mem, int32_t M, float* mail, double* mail_ts, int64_t mail_stride,
+                          int64_t num_nodes, cudaStream_t s) {
+  int64_t blocks = (max_n * 32 + 255) / 256;
+  const int64_t cap = (int64_t)num_sms() * 8;
+  if (blocks > cap) blocks = cap;
+  if (blocks < 1) blocks = 1;
+  launch_k(k_mail_deferred, dim3((unsigned)blocks), dim3(256), 0, s, 1, src, dst, ts, ef, He, nodes, winner,
+           num_unique, mem, M, mail, mail_ts, mail_stride, num_nodes);
 }
 
 constexpr int kMaxChunks = 8;  // 8 x 64 TMEM columns = 512 (the whole TMEM of the SM)

@@ -164,6 +164,8 @@ struct GruDesc {
   const float* bias;    // [Npad]
   const float* time_w;  // [Dt]
   const float* time_b;  // [Dt]
+  int32_t cell;         // MSPIPE_CELL_GRU | MSPIPE_CELL_RNN (row F3)
+  int32_t mailbox;      // MSPIPE_MAILBOX_IMMEDIATE | MSPIPE_MAILBOX_DEFERRED (row F3)
 };
 void launch_gru_pack(const float* w_ih, const float* w_hh, const float* b_ih, const float* b_hh,
                      const GruDesc& d, float* wpack, float* bias, cudaStream_t s);
@@ -255,6 +257,16 @@ struct GruCommit {  // fused A7 in the GEMM epilogue
   int32_t* save_num;
   CatchUp cu;  // cu.stamp == nullptr: no catch-up in this kernel
 };
+// row F3, deferred mailbox: A5 from the snapshot mail rows (snap_mail, rows as snap_mem)
+cudaError_t launch_build_deferred(const GruDesc& d, float* xbuf, const double* ts, int64_t num_events,
+                                  const float* snap_mem, const double* snap_mem_ts, const float* snap_mail,
+                                  int64_t mail_stride, int64_t snap_step, const int32_t* winner,
+                                  const int32_t* num_unique, double* out_ts, cudaStream_t s);
+// row F3, deferred mailbox, after the commit: mail[w] = [mem[w] | mem[o] | e], mail_ts[w] = t
+void launch_mail_deferred(const int32_t* src, const int32_t* dst, const double* ts, const float* ef, int32_t He,
+                          const int32_t* nodes, const int32_t* winner, const int32_t* num_unique, int64_t max_n,
+                          const float* mem, int32_t M, float* mail, double* mail_ts, int64_t mail_stride,
+                          int64_t num_nodes, cudaStream_t s);
 cudaError_t launch_gru_tc(const GruDesc& d, const float* wtc, float* xbuf, const double* ts, int64_t num_events,
                           const float* edge_feat, const float* snap_mem, const double* snap_mem_ts,
                           int64_t snap_step, const float* snap_h, const int32_t* winner,

@@ -44,6 +44,8 @@ class StageConfig:
     fused: bool | None = None  # mspipe_memory_prep + message_build/gru_apply (default: when supported)
     double_buffer: bool | None = None  # two table sets (mspipe_memory_double_buffer); default: k >= 1
     plan: tuple | None = None  # schedule "plan": paper staleness k_i per iteration (row F1)
+    cell: str = "gru"           # row F3: "gru" (TGN, APAN) | "rnn" (JODIE's RNNCell updater)
+    mailbox: str = "immediate"  # row F3: "immediate" (G14) | "deferred" (TGL's TGN; needs fetch_mail)
     features: bool = False     # row F2: fetch node / edge features of the sampled subgraphs (bind_features)
     node_dim: int = 0          # |d_v| (GDELT 413); rows padded to a multiple of 4 floats on the device
     # fused path without mitigation: message build inside the prep kernel (mspipe_memory_prep_build).
@@ -184,10 +186,14 @@ class MemoryStage(_TimedOps):
         self.tcsr = tcsr
         self.memory = _C.MemoryHandle(cfg.num_nodes, cfg.mem_dim, cfg.edge_dim, cfg.k, self.device,
                                       double_buffer=cfg.use_double_buffer())
+        self.deferred = cfg.mailbox == "deferred"
         self.gru = _C.GruHandle(cfg.mem_dim, cfg.edge_dim, cfg.time_dim, params, self.device, cfg.precision,
-                                max_events=cfg.batch)
+                                max_events=cfg.batch, cell=_C.CELL_RNN if cfg.cell == "rnn" else _C.CELL_GRU,
+                                mailbox=_C.MAILBOX_DEFERRED if self.deferred else _C.MAILBOX_IMMEDIATE)
         self.upd = _C.alloc_update(cfg.batch, cfg.mem_dim, self.memory.mail_stride, self.device)
         self.fused = cfg.use_fused()
+        if self.deferred and not (self.fused and cfg.fetch_mail and not cfg.prep_build):
+            raise ValueError("mailbox='deferred' runs on the fused tensor-core path with fetch_mail=True")
         self.ws_bytes = _C.gru_workspace_size(self.gru, cfg.batch) if self.fused else 0
         self.staged = False
         self.slots = None
@@ -398,9 +404,13 @@ class MemoryStage(_TimedOps):
             self._fetched = torch.cuda.Event()  # the state tables have been read for batch i
             self._fetched.record()
         self._ev("build")
-        _C.message_build(self.gru, x["ts"], x["ef"], sl.mem, sl.mem_ts, cfg.fanout + 1, sl.dd["winner"][: 2 * n],
-                         sl.dd["num"], sl.uts[: 2 * n], sl.umail[: 2 * n], sl.ws,
-                         snap_h=sl.h[: 2 * n] if sl.h is not None else None)
+        if self.deferred:  # row F3: the message is the stored mail of the snapshot
+            _C.message_build_deferred(self.gru, x["ts"], sl.mem, sl.mem_ts, sl.mail, cfg.fanout + 1,
+                                      sl.dd["winner"][: 2 * n], sl.dd["num"], sl.uts[: 2 * n], sl.ws)
+        else:
+            _C.message_build(self.gru, x["ts"], x["ef"], sl.mem, sl.mem_ts, cfg.fanout + 1, sl.dd["winner"][: 2 * n],
+                             sl.dd["num"], sl.uts[: 2 * n], sl.umail[: 2 * n], sl.ws,
+                             snap_h=sl.h[: 2 * n] if sl.h is not None else None)
         self._ev("build_end")
 
     def _upd(self, i):
@@ -410,7 +420,7 @@ class MemoryStage(_TimedOps):
         upd = {k: v[: 2 * n] for k, v in base.items() if k not in ("nodes", "winner", "num")}
         upd.update(nodes=sl.dd["nodes"][: 2 * n], winner=sl.dd["winner"][: 2 * n], num=sl.dd["num"])
         if self.fused:
-            upd.update(ts=sl.uts[: 2 * n], mail=sl.umail[: 2 * n])
+            upd.update(ts=sl.uts[: 2 * n], mail=None if self.deferred else sl.umail[: 2 * n])
         return upd
 
     def update(self, i):
@@ -451,6 +461,10 @@ class MemoryStage(_TimedOps):
         self._ev("update")
         _C.gru_apply_commit(self.gru, self.memory, i, n, sl.mem, cfg.fanout + 1, upd, sl.ws,
                             snap_h=sl.h[: 2 * n] if sl.h is not None else None)
+        if self.deferred:  # row F3: new mails from the committed memories of both endpoints
+            x = self.inputs(i)
+            _C.memory_mail_deferred(self.memory, i, x["src"], x["dst"], x["ts"], x["ef"], upd["nodes"], upd["winner"],
+                                    upd["num"])
         self._ev("update_end")
         self._stash_result(i, upd)
 

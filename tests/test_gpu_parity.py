@@ -604,3 +604,59 @@ def test_feature_fetch_equals_oracle(dev, name, E, fused):
         assert np.array_equal(sl.efeat[:R].cpu().numpy(), oe)
         if nf is not None:
             assert np.array_equal(sl.nfeat[:R, :, : cfg.node_dim].cpu().numpy(), on)
+
+
+# ------------------------------------------------------------------ row F3
+@pytest.mark.parametrize("name,k,E", [("tiny", 0, None), ("wiki", 1, 60_000), ("lastfm", 2, 80_000)])
+@pytest.mark.parametrize("cell,mailbox", [("rnn", "immediate"), ("gru", "deferred"), ("rnn", "deferred")])
+def test_updater_variants_free_running(dev, name, k, E, cell, mailbox):
+    """Row F3: RNN-cell updater (JODIE) and deferred mailbox (TGL TGN) over whole
+    streams against the oracle's variants: timestamps bit-exact, memories and
+    mails within the fp32 tolerance."""
+    from synth import rnn_params
+    w = make_workload(name, seed=11, num_events=E)
+    cfg = w["cfg"]
+    params = rnn_params(cfg.mem_dim, cfg.mail_dim, cfg.time_dim) if cell == "rnn" else w["params"]
+    sc = StageConfig(cfg.num_nodes, cfg.mem_dim, cfg.edge_dim, cfg.time_dim, cfg.fanout, cfg.batch, k,
+                     fetch_mail=True, cell=cell, mailbox=mailbox)
+    g = build_tcsr(cfg.num_nodes, w["src"], w["dst"], w["ts"], dev)
+    st = MemoryStage(sc, params, g, dev)
+    t = {kk: _t(w[kk], dev) for kk in ("src", "dst", "ts", "neg", "ef")}
+    st.bind_resident(t["src"], t["dst"], t["ts"], t["neg"], t["ef"])
+    st.run()
+    torch.cuda.synchronize()
+    _C.check()
+    ref, vers = oracle.run_stream(cfg.num_nodes, w["src"], w["dst"], w["ts"], w["ef"], params, cfg.batch, k,
+                                  mailbox=mailbox, cell=cell)
+    assert np.array_equal(st.memory.mem_ts.cpu().numpy(), ref["mem_ts"])
+    assert np.array_equal(st.memory.mail_ts.cpu().numpy(), ref["mail_ts"])
+    gm, om = st.memory.mem.cpu().numpy().astype(np.float64), ref["mem"].astype(np.float64)
+    rel = np.linalg.norm(gm - om, axis=1) / np.maximum(np.linalg.norm(om, axis=1), 1e-3)
+    print(f"{name} k={k} {cell}/{mailbox}: row-rel max {rel.max():.3g}")
+    assert rel.max() <= 1e-4
+    Dm = cfg.mail_dim
+    ok, err = _close(st.memory.mail.cpu().numpy()[:, :Dm], ref["mail"], rtol=1e-4, atol=1e-5)
+    assert ok, err
+
+
+def test_updater_variant_abi(dev):
+    from synth import rnn_params
+    cfg = CONFIGS["tiny"]
+    p = rnn_params(cfg.mem_dim, cfg.mail_dim, cfg.time_dim)
+    with pytest.raises(_C.MspipeError) as e:  # variants are tensor-core only
+        _C.GruHandle(cfg.mem_dim, cfg.edge_dim, cfg.time_dim, p, dev, _C.FP32_SIMT, cell=_C.CELL_RNN)
+    assert e.value.status == _C.EUNSUPPORTED
+    gd = _C.GruHandle(cfg.mem_dim, cfg.edge_dim, cfg.time_dim, gru_params(cfg.mem_dim, cfg.mail_dim, cfg.time_dim),
+                      dev, mailbox=_C.MAILBOX_DEFERRED)
+    h = _C.MemoryHandle(cfg.num_nodes, cfg.mem_dim, cfg.edge_dim, 0, dev)
+    x = torch.zeros(4, dtype=torch.int32, device=dev)
+    upd = _C.alloc_update(4, cfg.mem_dim, h.mail_stride, dev)
+    with pytest.raises(_C.MspipeError) as e:  # the immediate-message entry points refuse a deferred handle
+        _C.memory_update(h, gd, x, x, x.double(), torch.zeros((4, cfg.edge_dim), device=dev),
+                         torch.zeros((12 * 11, cfg.mem_dim), device=dev), torch.zeros(12 * 11, dtype=torch.float64,
+                                                                                      device=dev), 11, upd)
+    assert e.value.status == _C.EUNSUPPORTED
+    with pytest.raises(_C.MspipeError) as e:  # mail rows follow commit `committed`, not another version
+        _C.memory_mail_deferred(h, 3, x, x, x.double(), torch.zeros((4, cfg.edge_dim), device=dev), upd["nodes"],
+                                upd["winner"], upd["num"])
+    assert e.value.status == _C.EORDER
