@@ -195,7 +195,7 @@ def run_mspipe(args):
                    n_sim=cfg.n_sim)
     sc = StageConfig(cfg.num_nodes, cfg.mem_dim, cfg.edge_dim, cfg.time_dim, cfg.fanout, cfg.batch, k,
                      schedule=args.schedule, mitigation=mit, fetch_mail=args.fetch_mail,
-                     precision=_C.FP32_3XTF32 if args.gru == "tc" else _C.FP32_SIMT,
+                     precision={"tc": _C.FP32_3XTF32, "bf16": _C.BF16, "simt": _C.FP32_SIMT}[args.gru],
                      features=args.features, node_dim=cfg.node_dim)
     g = build_tcsr(cfg.num_nodes, w["src"], w["dst"], w["ts"], dev)
     # N > 1: node-id-sharded memory over NCCL (row E); MSPIPE_BENCH_REPLICAS=1 runs
@@ -315,7 +315,13 @@ def run_mspipe(args):
     timeline = {kk: float(np.mean(v)) for kk, v in op_ms.items() if v and "@" in kk}
     dom = max(op_mean, key=op_mean.get) if op_mean else "update"
     clocks = clk.summary()
-    if dom == "update" and args.gru == "tc":
+    if dom == "update" and args.gru == "bf16":
+        peak_tc = peaks["bf16_tflops_sustained"]
+        ach = alg["update_flops"] / (op_mean[dom] / 1e3) / 1e12
+        roof = {"kernel": "k_gru_tc<bf16> via mspipe_gru_apply_commit (GEMM + gates + LWW commit epilogue)",
+                "bound": "tensor", "achieved": ach, "peak": peak_tc, "unit": "TFLOP/s", "frac": ach / peak_tc,
+                "peak_source": f"{peaks['source']} bf16 sustained"}
+    elif dom == "update" and args.gru == "tc":
         # 3xTF32: each useful fp32 MAC costs 3 tf32 MACs; tf32 dense = bf16 x (1.1 / 2.25)
         # nominal ratio (B200_PROFILING.md); sustained bf16 figure (kernel timed inside a long step)
         peak_tc = peaks["bf16_tflops_sustained"] * (1.1 / 2.25) / 3.0
@@ -361,11 +367,12 @@ def run_mspipe(args):
                          "bytes_per_launch": alg["features"]}
     out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": K, "warmup": W,
            "ms_per_step": tot_ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-           "dtype": "f32", "data": "synthetic",
+           "dtype": "bf16-gemm/f32" if args.gru == "bf16" else "f32", "data": "synthetic",
            "config": {"workload": args.config, "events": int(len(w["src"])), "num_nodes": cfg.num_nodes,
                       "batch": cfg.batch, "staleness_k": k, "schedule": args.schedule, "fanout": cfg.fanout,
                       "mem_dim": cfg.mem_dim, "edge_dim": cfg.edge_dim, "time_dim": cfg.time_dim,
-                      "mitigation": bool(mit), "features": args.features, "fetch_mail": args.fetch_mail, "gru": "fp32-3xtf32-tcgen05" if args.gru == "tc" else "fp32-simt",
+                      "mitigation": bool(mit), "features": args.features, "fetch_mail": args.fetch_mail, "gru": {"tc": "fp32-3xtf32-tcgen05", "bf16": "bf16-operands-tcgen05 (fp32 accumulate/state)",
+                              "simt": "fp32-simt"}[args.gru],
                       "l2": ("flushed (256 MiB write) between timed steps, outside the timed events"
                              if args.l2 == "flush" else "warm: steps back to back, state tables L2-resident"),
                       "parallelism": ("single" if ws == 1 else
@@ -507,7 +514,9 @@ def main():
     ap.add_argument("--k", type=int, default=None)
     ap.add_argument("--schedule", default="exact", choices=["exact", "grouped"])
     ap.add_argument("--fetch-mail", action="store_true")
-    ap.add_argument("--gru", default="tc", choices=["tc", "simt"])
+    ap.add_argument("--gru", default="tc", choices=["tc", "bf16", "simt"],
+                    help="tc: 3xTF32 tcgen05 (fp32 parity, default); bf16: tcgen05 bf16 operands "
+                         "(2e-2 tolerance); simt: CUDA-core fp32 baseline")
     ap.add_argument("--no-mitigation", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--l2", default="flush", choices=["flush", "warm"],

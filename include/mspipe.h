@@ -222,7 +222,9 @@ MSPIPE_API mspipe_status mspipe_memory_fetch(mspipe_memory* st, int64_t iteratio
  * max_events events (device memory owned by the handle).
  * precision: MSPIPE_FP32_3XTF32 = tcgen05 tensor cores, fp32 parity via the
  * 3xTF32 split (default); MSPIPE_FP32_SIMT = CUDA-core fp32 (baseline);
- * MSPIPE_BF16 is reserved (EUNSUPPORTED in this build). */
+ * MSPIPE_BF16 = tcgen05 kind::f16 with bf16 operands (message and weights
+ * rounded to bf16, fp32 accumulation and state; the north star's bf16
+ * tolerance 2e-2).  The tensor-core precisions share every entry point. */
 enum { MSPIPE_FP32_SIMT = 0, MSPIPE_FP32_3XTF32 = 1, MSPIPE_BF16 = 2 };
 typedef struct mspipe_gru mspipe_gru;
 MSPIPE_API mspipe_status mspipe_gru_create(mspipe_gru** out, int32_t mem_dim, int32_t edge_dim,

@@ -354,15 +354,16 @@ mspipe_status mspipe_updater_create(mspipe_gru** out, int32_t mem_dim, int32_t e
   if ((cell != MSPIPE_CELL_GRU && cell != MSPIPE_CELL_RNN) ||
       (mailbox != MSPIPE_MAILBOX_IMMEDIATE && mailbox != MSPIPE_MAILBOX_DEFERRED))
     return fail(MSPIPE_EINVAL, "updater_create: cell=%d mailbox=%d", cell, mailbox);
-  if ((cell != MSPIPE_CELL_GRU || mailbox != MSPIPE_MAILBOX_IMMEDIATE) && precision != MSPIPE_FP32_3XTF32)
-    return fail(MSPIPE_EUNSUPPORTED, "updater_create: variants need precision MSPIPE_FP32_3XTF32");
+  if ((cell != MSPIPE_CELL_GRU || mailbox != MSPIPE_MAILBOX_IMMEDIATE) && precision != MSPIPE_FP32_3XTF32 &&
+      !(precision == MSPIPE_BF16 && mailbox == MSPIPE_MAILBOX_IMMEDIATE))
+    return fail(MSPIPE_EUNSUPPORTED, "updater_create: variants need a tensor-core precision (deferred: 3xTF32)");
   *out = nullptr;
   if (mem_dim < 4 || mem_dim % 4 || edge_dim < 0 || time_dim < 0 || max_events < 1 || max_events > 16384)
     return fail(MSPIPE_EINVAL, "gru_create: mem_dim=%d edge_dim=%d time_dim=%d max_events=%lld (1..16384)",
                 mem_dim, edge_dim, time_dim, (long long)max_events);
   if (!w_ih || !w_hh || !b_ih || !b_hh || (time_dim > 0 && (!time_w || !time_b)))
     return fail(MSPIPE_EINVAL, "gru_create: null weight");
-  if (precision != MSPIPE_FP32_SIMT && precision != MSPIPE_FP32_3XTF32)
+  if (precision != MSPIPE_FP32_SIMT && precision != MSPIPE_FP32_3XTF32 && precision != MSPIPE_BF16)
     return fail(MSPIPE_EUNSUPPORTED, "gru_create: precision %d not in this build", precision);
   mspipe_gru* p = new mspipe_gru();
   GruDesc& d = p->d;
@@ -372,11 +373,12 @@ mspipe_status mspipe_updater_create(mspipe_gru** out, int32_t mem_dim, int32_t e
   d.Dm = 2 * mem_dim + edge_dim;
   d.Dx = d.Dm + time_dim;
   d.K = d.Dx + mem_dim;
-  d.Kpad = (d.K + 31) / 32 * 32;
+  d.bf16 = precision == MSPIPE_BF16 ? 1 : 0;
+  d.Kpad = d.bf16 ? (d.K + 63) / 64 * 64 : (d.K + 31) / 32 * 32;
   d.cell = cell;
   d.mailbox = mailbox;
   d.Npad = (mem_dim + 31) / 32 * 128;
-  if (precision == MSPIPE_FP32_3XTF32 && d.Kpad / 32 > 64) {
+  if (precision != MSPIPE_FP32_SIMT && d.Kpad > 2048) {
     delete p;
     return fail(MSPIPE_EUNSUPPORTED, "gru_create: K = 2M + He + Dt + M = %d > 2048 on the tensor-core path", d.K);
   }
@@ -387,7 +389,7 @@ mspipe_status mspipe_updater_create(mspipe_gru** out, int32_t mem_dim, int32_t e
   cudaError_t e = precision == MSPIPE_FP32_SIMT
                       ? cudaMalloc(&p->wpack, sizeof(float) * (size_t)d.Kpad * d.Npad)
                       : cudaMalloc(&p->wtc, sizeof(float) * gru_tc_packed_floats(d));
-  if (e == cudaSuccess && precision == MSPIPE_FP32_3XTF32)
+  if (e == cudaSuccess && precision != MSPIPE_FP32_SIMT)
     e = cudaMalloc(&p->xbuf, sizeof(float) * gru_tc_xbuf_floats(d, max_events));
   if (e == cudaSuccess) e = cudaMalloc(&p->bias, sizeof(float) * (size_t)d.Npad);
   if (e == cudaSuccess) e = cudaMalloc(&p->time_w, sizeof(float) * (size_t)(time_dim > 0 ? time_dim : 1));
@@ -502,7 +504,7 @@ mspipe_status mspipe_memory_update(mspipe_memory* st, const mspipe_gru* gru, con
   int32_t* out_winner = const_cast<int32_t*>(winner);
   int32_t* out_num_unique = const_cast<int32_t*>(num_unique);
   int32_t* out_nodes = nullptr;
-  if (gru->precision == MSPIPE_FP32_3XTF32) {
+  if (gru->precision != MSPIPE_FP32_SIMT) {
     cudaError_t e = launch_gru_tc(gru->d, gru->wtc, gru->xbuf, ts, num_events, edge_feat, snap_mem, snap_mem_ts, snap_step,
                                   snap_h, out_winner, out_num_unique, out_mem, out_ts, out_mail, st->mail_stride, s);
     if (e != cudaSuccess) return cuda_status(e, "memory_update: tcgen05 GRU launch");
@@ -666,7 +668,7 @@ static mspipe_status prep_impl(mspipe_memory* st, const mspipe_tcsr* g, int64_t 
 }
 
 size_t mspipe_gru_workspace_size(const mspipe_gru* gru, int64_t num_events) {
-  if (!gru || gru->precision != MSPIPE_FP32_3XTF32 || num_events < 0) return 0;
+  if (!gru || gru->precision == MSPIPE_FP32_SIMT || num_events < 0) return 0;
   return sizeof(float) * gru_tc_xbuf_floats(gru->d, num_events);
 }
 
@@ -677,7 +679,7 @@ mspipe_status mspipe_message_build(const mspipe_gru* gru, const double* ts, int6
                                    const int32_t* num_unique, double* out_ts, float* out_mail,
                                    int64_t mail_stride, void* workspace, size_t ws_bytes, void* stream) {
   if (!gru) return fail(MSPIPE_EINVAL, "message_build: NULL handle");
-  if (gru->precision != MSPIPE_FP32_3XTF32)
+  if (gru->precision == MSPIPE_FP32_SIMT)
     return fail(MSPIPE_EUNSUPPORTED, "message_build: only for precision MSPIPE_FP32_3XTF32 (use mspipe_memory_update)");
   if (gru->d.mailbox != MSPIPE_MAILBOX_IMMEDIATE)
     return fail(MSPIPE_EUNSUPPORTED, "message_build: deferred-mailbox handle (use mspipe_message_build_deferred)");
@@ -701,7 +703,7 @@ mspipe_status mspipe_gru_apply(const mspipe_gru* gru, int64_t num_events, const 
                                const int32_t* num_unique, float* out_mem, const void* workspace,
                                size_t ws_bytes, void* stream) {
   if (!gru) return fail(MSPIPE_EINVAL, "gru_apply: NULL handle");
-  if (gru->precision != MSPIPE_FP32_3XTF32)
+  if (gru->precision == MSPIPE_FP32_SIMT)
     return fail(MSPIPE_EUNSUPPORTED, "gru_apply: only for precision MSPIPE_FP32_3XTF32 (use mspipe_memory_update)");
   if (num_events < 0 || num_events > gru->max_events || snap_step < 1)
     return fail(MSPIPE_EINVAL, "gru_apply: num_events=%lld snap_step=%lld", (long long)num_events, (long long)snap_step);
@@ -724,7 +726,7 @@ mspipe_status mspipe_gru_apply_commit(const mspipe_gru* gru, mspipe_memory* st,
                                       const float* new_mail, float* out_mem, const void* workspace,
                                       size_t ws_bytes, void* stream) {
   if (!gru || !st) return fail(MSPIPE_EINVAL, "gru_apply_commit: NULL handle");
-  if (gru->precision != MSPIPE_FP32_3XTF32)
+  if (gru->precision == MSPIPE_FP32_SIMT)
     return fail(MSPIPE_EUNSUPPORTED, "gru_apply_commit: only for precision MSPIPE_FP32_3XTF32");
   if (st->world != 1) return fail(MSPIPE_EUNSUPPORTED, "gru_apply_commit: world > 1");
   if (gru->d.M != st->mem_dim || gru->d.He != st->edge_dim) return fail(MSPIPE_EINVAL, "gru_apply_commit: dims");

@@ -23,6 +23,7 @@
 //    (1,1,S); the S partial tiles are summed through distributed shared memory
 //    in fixed rank order (deterministic) and each rank applies the gates to
 //    128/S rows.
+#include <cuda_bf16.h>
 #include <stdlib.h>
 
 #include "internal.cuh"
@@ -101,6 +102,17 @@ __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+__device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
                    smem_u32(bar))
@@ -163,6 +175,11 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
 // kind::tf32 instruction descriptor: D f32, A/B tf32, K-major, M = 128, N = 64.
 constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(kN >> 3) << 17) |
                             ((uint32_t)(kM >> 4) << 24);
+// kind::f16 instruction descriptor (MSPIPE_BF16): D f32, A/B bf16, K-major, M = 128, N = 64.
+constexpr uint32_t kIdescBf = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kN >> 3) << 17) |
+                              ((uint32_t)(kM >> 4) << 24);
+constexpr int kBBlock16 = kN * kKC16 * 2;            // 8 KB
+constexpr int kStageBytes16 = kATile16 + kBBlock16;  // 24 KB
 }  // namespace tc
 
 #ifdef MSPIPE_PHASES
@@ -188,6 +205,44 @@ int gru_tc_jtiles(const GruDesc& d) { return (d.M + tc::kJ - 1) / tc::kJ; }
 // [hi image 8 KB | lo image 8 KB] of the B operand, N = 64 rows n = g*16 + jj
 // (gate g in r, z, n_x, n_h), K-major SWIZZLE_128B; bias[jt*64 + n].
 // ---------------------------------------------------------------------------
+// B-operand value of row n = g*16 + jj of hidden tile jt at K index k (0 outside)
+__device__ __forceinline__ float wval(const float* __restrict__ w_ih, const float* __restrict__ w_hh,
+                                      const GruDesc& d, int32_t g, int32_t j, int32_t k) {
+  const int32_t M = d.M;
+  if (j >= M) return 0.f;
+  if (d.cell == MSPIPE_CELL_RNN) {  // RNNCell: n_x = W_ih x, n_h = W_hh h
+    if (k < d.Dx) return g == 2 ? w_ih[(int64_t)j * d.Dx + k] : 0.f;
+    if (k < d.K) return g == 3 ? w_hh[(int64_t)j * M + (k - d.Dx)] : 0.f;
+    return 0.f;
+  }
+  if (k < d.Dx) return g < 3 ? w_ih[(int64_t)(g * M + j) * d.Dx + k] : 0.f;
+  if (k < d.K) {
+    const int32_t q = k - d.Dx;
+    if (g == 0) return w_hh[(int64_t)j * M + q];
+    if (g == 1) return w_hh[(int64_t)(M + j) * M + q];
+    if (g == 3) return w_hh[(int64_t)(2 * M + j) * M + q];
+  }
+  return 0.f;
+}
+
+// bf16 weights (MSPIPE_BF16): per (jt, 64-wide K chunk) one 8 KB SWIZZLE_128B
+// K-major image of the 64 B-operand rows, round-to-nearest bf16
+__global__ void k_gru_pack_bf16(const float* __restrict__ w_ih, const float* __restrict__ w_hh, GruDesc d,
+                                int32_t jtiles, uint8_t* __restrict__ wtc) {
+  const int32_t nchunks = d.Kpad / tc::kKC16;
+  const int64_t total = (int64_t)jtiles * nchunks * tc::kN * tc::kKC16;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t kk = (int32_t)(t % tc::kKC16);
+    const int32_t n = (int32_t)((t / tc::kKC16) % tc::kN);
+    const int32_t c = (int32_t)((t / (tc::kKC16 * tc::kN)) % nchunks);
+    const int32_t jt = (int32_t)(t / ((int64_t)tc::kKC16 * tc::kN * nchunks));
+    const float v = wval(w_ih, w_hh, d, n / tc::kJ, jt * tc::kJ + n % tc::kJ, c * tc::kKC16 + kk);
+    uint8_t* blk = wtc + ((int64_t)jt * nchunks + c) * (tc::kN * tc::kKC16 * 2);
+    *reinterpret_cast<__nv_bfloat16*>(blk + tc::sw128_off16((uint32_t)n, (uint32_t)kk)) = __float2bfloat16_rn(v);
+  }
+}
+
 __global__ void k_gru_pack_tc(const float* __restrict__ w_ih, const float* __restrict__ w_hh,
                               const float* __restrict__ b_ih, const float* __restrict__ b_hh, GruDesc d,
                               int32_t jtiles, float* __restrict__ wtc, float* __restrict__ bias) {
@@ -201,24 +256,7 @@ __global__ void k_gru_pack_tc(const float* __restrict__ w_ih, const float* __res
     const int32_t jt = (int32_t)(t / ((int64_t)tc::kKC * tc::kN * nchunks));
     const int32_t g = n / tc::kJ, jj = n % tc::kJ, j = jt * tc::kJ + jj, k = c * tc::kKC + kk;
     const int32_t M = d.M;
-    float v = 0.f;
-    if (j < M && d.cell == MSPIPE_CELL_RNN) {
-      // RNNCell: only the n blocks, n_x = W_ih x, n_h = W_hh h (tanh(n_x + n_h) in the epilogue)
-      if (k < d.Dx) {
-        if (g == 2) v = w_ih[(int64_t)j * d.Dx + k];
-      } else if (k < d.K) {
-        if (g == 3) v = w_hh[(int64_t)j * M + (k - d.Dx)];
-      }
-    } else if (j < M) {
-      if (k < d.Dx) {
-        if (g < 3) v = w_ih[(int64_t)(g * M + j) * d.Dx + k];
-      } else if (k < d.K) {
-        const int32_t q = k - d.Dx;
-        if (g == 0) v = w_hh[(int64_t)j * M + q];
-        else if (g == 1) v = w_hh[(int64_t)(M + j) * M + q];
-        else if (g == 3) v = w_hh[(int64_t)(2 * M + j) * M + q];
-      }
-    }
+    const float v = wval(w_ih, w_hh, d, g, j, k);
     const float hi = tc::tf32_rna(v);
     const float lo = tc::tf32_rna(v - hi);
     char* blk = reinterpret_cast<char*>(wtc) + ((int64_t)jt * nchunks + c) * tc::kBBlock;
@@ -242,11 +280,13 @@ __global__ void k_gru_pack_tc(const float* __restrict__ w_ih, const float* __res
 }
 
 size_t gru_tc_packed_floats(const GruDesc& d) {
+  if (d.bf16) return (size_t)gru_tc_jtiles(d) * (d.Kpad / tc::kKC16) * (tc::kN * tc::kKC16 * 2 / 4);
   return (size_t)gru_tc_jtiles(d) * (d.Kpad / tc::kKC) * (tc::kBBlock / 4);
 }
 
 size_t gru_tc_xbuf_floats(const GruDesc& d, int64_t max_events) {
   const int64_t mtiles = (2 * max_events + tc::kM - 1) / tc::kM;
+  if (d.bf16) return (size_t)mtiles * (d.Kpad / tc::kKC16) * (tc::kATile16 / 4);
   return (size_t)mtiles * (d.Kpad / tc::kKC) * (tc::kABlock / 4);
 }
 
@@ -256,7 +296,22 @@ void launch_gru_pack_tc(const float* w_ih, const float* w_hh, const float* b_ih,
   const int64_t total = (int64_t)gru_tc_packed_floats(d) / 2;
   int64_t blocks = (total + threads - 1) / threads;
   if (blocks > 4096) blocks = 4096;
-  k_gru_pack_tc<<<(unsigned)blocks, threads, 0, s>>>(w_ih, w_hh, b_ih, b_hh, d, gru_tc_jtiles(d), wtc, bias);
+  if (!d.bf16) {
+    k_gru_pack_tc<<<(unsigned)blocks, threads, 0, s>>>(w_ih, w_hh, b_ih, b_hh, d, gru_tc_jtiles(d), wtc, bias);
+    return;
+  }
+  // bf16: the weight images, then the biases (k_gru_pack_tc's bias pass over one chunk, into scratch)
+  const int64_t total16 = (int64_t)gru_tc_jtiles(d) * (d.Kpad / tc::kKC16) * tc::kN * tc::kKC16;
+  int64_t b16 = (total16 + threads - 1) / threads;
+  if (b16 > 4096) b16 = 4096;
+  k_gru_pack_bf16<<<(unsigned)b16, threads, 0, s>>>(w_ih, w_hh, d, gru_tc_jtiles(d), (uint8_t*)wtc);
+  GruDesc one = d;
+  one.Kpad = tc::kKC;  // a single 32-wide chunk: k_gru_pack_tc then writes every bias once
+  float* scratch = nullptr;
+  if (cudaMallocAsync(&scratch, sizeof(float) * gru_tc_jtiles(d) * (tc::kBBlock / 4), s) != cudaSuccess) return;
+  k_gru_pack_tc<<<(unsigned)gru_tc_jtiles(d), threads, 0, s>>>(w_ih, w_hh, b_ih, b_hh, one, gru_tc_jtiles(d),
+                                                               scratch, bias);
+  cudaFreeAsync(scratch, s);
 }
 
 // ---------------------------------------------------------------------------
@@ -306,9 +361,68 @@ __device__ __forceinline__ void catch_up(const TcArgs& a, int64_t wq, int64_t nw
   }
 }
 
+// A5 value of winner pair p, column k of x = [s_w | s_o | e | cos(w dt + p) | h]
+__device__ __forceinline__ float msg_val(const TcArgs& a, int32_t p, int32_t k) {
+  const GruDesc& d = a.d;
+  const int32_t M = d.M;
+  const int32_t ev = p >> 1, role = p & 1;
+  const int64_t rw = role ? a.B + ev : ev;
+  const int64_t ro = role ? ev : a.B + ev;
+  if (k < M) return __ldg(a.snap_mem + rw * a.step * M + k);
+  if (k < 2 * M) return __ldg(a.snap_mem + ro * a.step * M + (k - M));
+  if (k < d.Dm) return __ldg(a.ef + (int64_t)ev * d.He + (k - 2 * M));
+  if (k < d.Dx) {
+    const float dt = (float)(__ldg(a.ts + ev) - __ldg(a.snap_ts + rw * a.step));  // Δt (G4)
+    const int q = k - d.Dm;
+    return time_cos(fmaf(__ldg(d.time_w + q), dt, __ldg(d.time_b + q)));
+  }
+  if (k < d.K) {
+    const int q = k - d.Dx;
+    return a.snap_h ? __ldg(a.snap_h + rw * M + q) : __ldg(a.snap_mem + rw * a.step * M + q);
+  }
+  return 0.f;
+}
+
+// A5 with bf16 operands (MSPIPE_BF16): one warp per (row, 64-wide chunk), two
+// columns per lane; the mail row and commit ts stay fp32.
+__device__ __forceinline__ void build_bf16(const TcArgs& a) {
+  const GruDesc& d = a.d;
+  const int32_t U = __ldg(a.num_unique);
+  const int32_t nchunks = d.Kpad / tc::kKC16;
+  const int32_t mtiles = (U + tc::kM - 1) / tc::kM;
+  const int64_t items = (int64_t)mtiles * nchunks * tc::kM;
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < items; w += nwarps) {
+    const int32_t row = (int32_t)(w % tc::kM);
+    const int32_t c = (int32_t)((w / tc::kM) % nchunks);
+    const int32_t mt = (int32_t)(w / ((int64_t)tc::kM * nchunks));
+    const int32_t u = mt * tc::kM + row;
+    const int32_t k0 = c * tc::kKC16 + 2 * lane;
+    float v0 = 0.f, v1 = 0.f;
+    if (u < U) {
+      const int32_t p = __ldg(a.winner + u);
+      v0 = msg_val(a, p, k0);
+      v1 = msg_val(a, p, k0 + 1);
+      if (a.out_mail) {
+        if (k0 < a.mail_stride) a.out_mail[(int64_t)u * a.mail_stride + k0] = k0 < d.Dm ? v0 : 0.f;
+        if (k0 + 1 < a.mail_stride) a.out_mail[(int64_t)u * a.mail_stride + k0 + 1] = k0 + 1 < d.Dm ? v1 : 0.f;
+      }
+      if (c == 0 && lane == 0) a.out_ts[u] = __ldg(a.ts + (p >> 1));
+    }
+    uint8_t* blk = reinterpret_cast<uint8_t*>(a.xbuf) + ((int64_t)mt * nchunks + c) * tc::kATile16;
+    *reinterpret_cast<__nv_bfloat162*>(blk + tc::sw128_off16((uint32_t)row, (uint32_t)(2 * lane))) =
+        __floats2bfloat162_rn(v0, v1);
+  }
+}
+
 // A5: one warp per (row, chunk).  lane = column inside the chunk.
 __global__ void __launch_bounds__(256) k_build_x(TcArgs a) {
   pdl_begin();
+  if (a.d.bf16) {
+    build_bf16(a);
+    return;
+  }
   const GruDesc& d = a.d;
   const int32_t U = __ldg(a.num_unique);
   const int32_t nchunks = d.Kpad / tc::kKC;
@@ -396,12 +510,30 @@ __device__ __forceinline__ void commit_rows(const TcArgs& a, int32_t m0, int32_t
   }
   const int Q = (int)(a.mail_stride / 4);
   const int c0 = jt * Q / J, c1 = (jt + 1) * Q / J, nq = c1 - c0;
-  const float4* src = reinterpret_cast<const float4*>(a.new_mail);
-  float4* dst = reinterpret_cast<float4*>(a.commit_mail);
-  for (int it = threadIdx.x; it < (re - rb) * nq; it += blockDim.x) {
-    const int mm = rb + it / nq, c = c0 + it % nq;
-    const int32_t u = m0 + mm, node = rownode[mm];
-    if (u < U && node >= 0) dst[(int64_t)node * Q + c] = __ldg(src + (int64_t)u * Q + c);
+  const float4* __restrict__ src = reinterpret_cast<const float4*>(a.new_mail);
+  float4* __restrict__ dst = reinterpret_cast<float4*>(a.commit_mail);
+  // 4 loads in flight per thread before their stores (a load-store-load loop
+  // serialises on L2 latency: 13 round trips per thread for 128 rows)
+  const int total = (re - rb) * nq;
+  for (int base = threadIdx.x; base < total; base += 4 * blockDim.x) {
+    float4 v[4];
+    int64_t to[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int it = base + q * blockDim.x;
+      to[q] = -1;
+      if (it < total) {
+        const int mm = rb + it / nq, c = c0 + it % nq;
+        const int32_t u = m0 + mm, node = rownode[mm];
+        if (u < U && node >= 0) {
+          v[q] = __ldg(src + (int64_t)u * Q + c);
+          to[q] = (int64_t)node * Q + c;
+        }
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (to[q] >= 0) dst[to[q]] = v[q];
   }
   if (jt == 0)
     for (int mm = rb + (int)threadIdx.x; mm < re; mm += blockDim.x) {
@@ -414,19 +546,26 @@ __device__ __forceinline__ void commit_rows(const TcArgs& a, int32_t m0, int32_t
     }
 }
 
+// kBf: bf16 operands (MSPIPE_BF16): 64-wide K chunks of 24 KB stages, one
+// accumulator per CTA for its K range (bf16 tolerance, north star 2e-2); the
+// K split and partial-sum exchange are the tf32 kernel's.
+template <bool kBf>
 __global__ void __launch_bounds__(tc::kThreads, 1) k_gru_tc(TcArgs a) {
   using namespace tc;
+  constexpr int SB = kBf ? kStageBytes16 : kStageBytes;
+  constexpr int AB = kBf ? kATile16 : kABlock;
+  constexpr int BB = kBf ? kBBlock16 : kBBlock;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * SB);
   uint64_t* empty = full + kStages;
   uint64_t* acc_full = empty + kStages;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 1);
-  int32_t* rownode = reinterpret_cast<int32_t*>(smem + kStages * kStageBytes + 512);  // [128] node of each row
-  float4* hbuf =reinterpret_cast<float4*>(smem + kStages * kStageBytes + 1024);  // [128 rows][kJ/4]
-  float4* recv = reinterpret_cast<float4*>(smem + kStages * kStageBytes + 1024 + kHBufBytes);
+  int32_t* rownode = reinterpret_cast<int32_t*>(smem + kStages * SB + 512);  // [128] node of each row
+  float4* hbuf = reinterpret_cast<float4*>(smem + kStages * SB + 1024);  // [128 rows][kJ/4]
+  float4* recv = reinterpret_cast<float4*>(smem + kStages * SB + 1024 + kHBufBytes);
   // this tile's gate biases, prefetched during the main loop
-  float* sbias = reinterpret_cast<float*>(smem + kStages * kStageBytes + 1024 + kHBufBytes + kRecvBytes);
+  float* sbias = reinterpret_cast<float*>(smem + kStages * SB + 1024 + kHBufBytes + kRecvBytes);
 
   const GruDesc& d = a.d;
   PHASE(9);
@@ -450,10 +589,10 @@ __global__ void __launch_bounds__(tc::kThreads, 1) k_gru_tc(TcArgs a) {
                                          threadIdx.x & 31);
     return;
   }
-  const int32_t nchunks = d.Kpad / kKC;
+  const int32_t nchunks = d.Kpad / (kBf ? kKC16 : kKC);
   const int32_t c0 = split * nchunks / S, c1 = (split + 1) * nchunks / S;
-  const int32_t nc = c1 - c0;  // <= kMaxChunks (host picks S >= nchunks / kMaxChunks)
-  const uint32_t tcols = nc <= 2 ? 128u : (nc <= 4 ? 256u : 512u);
+  const int32_t nc = c1 - c0;  // tf32: <= kMaxChunks (host picks S >= nchunks / kMaxChunks)
+  const uint32_t tcols = kBf ? 64u : (nc <= 2 ? 128u : (nc <= 4 ? 256u : 512u));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
@@ -473,16 +612,16 @@ __global__ void __launch_bounds__(tc::kThreads, 1) k_gru_tc(TcArgs a) {
 
   if (warp == 0 && lane == 0) {
     // loader: one A block (32 KB) + one B block (16 KB) per stage
-    const char* abase = reinterpret_cast<const char*>(a.xbuf) + (int64_t)mt * nchunks * kABlock;
-    const char* bbase = reinterpret_cast<const char*>(a.wtc) + (int64_t)jt * nchunks * kBBlock;
+    const char* abase = reinterpret_cast<const char*>(a.xbuf) + (int64_t)mt * nchunks * AB;
+    const char* bbase = reinterpret_cast<const char*>(a.wtc) + (int64_t)jt * nchunks * BB;
     for (int ci = 0; ci < nc; ++ci) {
       const int s = ci % kStages;
       const uint32_t ph = (uint32_t)(ci / kStages) & 1u;
       mbar_wait(&empty[s], ph ^ 1u);
-      uint8_t* st = smem + s * kStageBytes;
-      mbar_arrive_expect_tx(&full[s], kStageBytes);
-      bulk_g2s(st, abase + (int64_t)(c0 + ci) * kABlock, kABlock, &full[s]);
-      bulk_g2s(st + kABlock, bbase + (int64_t)(c0 + ci) * kBBlock, kBBlock, &full[s]);
+      uint8_t* st = smem + s * SB;
+      mbar_arrive_expect_tx(&full[s], SB);
+      bulk_g2s(st, abase + (int64_t)(c0 + ci) * AB, AB, &full[s]);
+      bulk_g2s(st + AB, bbase + (int64_t)(c0 + ci) * BB, BB, &full[s]);
     }
   } else if (warp == 1 && lane == 0) {
     // MMA issuer.  Each K chunk accumulates into its OWN 64-column TMEM
@@ -495,16 +634,25 @@ __global__ void __launch_bounds__(tc::kThreads, 1) k_gru_tc(TcArgs a) {
       const uint32_t ph = (uint32_t)(ci / kStages) & 1u;
       mbar_wait(&full[s], ph);
       tc_fence_after();
-      const uint32_t base = smem_u32(smem + s * kStageBytes);
-      const uint64_t da_hi = sw128_desc(base), da_lo = sw128_desc(base + kATile);
-      const uint64_t db_hi = sw128_desc(base + kABlock), db_lo = sw128_desc(base + kABlock + kBTile);
-      const uint32_t tacc = tmem + (uint32_t)(ci * kN);
+      const uint32_t base = smem_u32(smem + s * SB);
+      if (kBf) {  // 4 MMAs of K = 16 (32 B along K) into the single accumulator
+        const uint64_t da = sw128_desc(base), db = sw128_desc(base + AB);
 #pragma unroll
-      for (int kk = 0; kk < kKC / 8; ++kk) {
-        const uint64_t adv = (uint64_t)(kk * 32) >> 4;  // 8 tf32 = 32 B along K inside the swizzle row
-        mma_tf32(tacc, da_lo + adv, db_hi + adv, kIdesc, kk != 0);
-        mma_tf32(tacc, da_hi + adv, db_lo + adv, kIdesc, 1u);
-        mma_tf32(tacc, da_hi + adv, db_hi + adv, kIdesc, 1u);
+        for (int kk = 0; kk < kKC16 / 16; ++kk) {
+          const uint64_t adv = (uint64_t)(kk * 32) >> 4;
+          mma_bf16(tmem, da + adv, db + adv, kIdescBf, (ci | kk) != 0);
+        }
+      } else {
+        const uint64_t da_hi = sw128_desc(base), da_lo = sw128_desc(base + kATile);
+        const uint64_t db_hi = sw128_desc(base + kABlock), db_lo = sw128_desc(base + kABlock + kBTile);
+        const uint32_t tacc = tmem + (uint32_t)(ci * kN);
+#pragma unroll
+        for (int kk = 0; kk < kKC / 8; ++kk) {
+          const uint64_t adv = (uint64_t)(kk * 32) >> 4;  // 8 tf32 = 32 B along K inside the swizzle row
+          mma_tf32(tacc, da_lo + adv, db_hi + adv, kIdesc, kk != 0);
+          mma_tf32(tacc, da_hi + adv, db_lo + adv, kIdesc, 1u);
+          mma_tf32(tacc, da_hi + adv, db_hi + adv, kIdesc, 1u);
+        }
       }
       mma_commit(&empty[s]);
     }
@@ -547,7 +695,7 @@ __global__ void __launch_bounds__(tc::kThreads, 1) k_gru_tc(TcArgs a) {
   MSPIPE_TMEM_LD32(tbase, r0);
   MSPIPE_TMEM_LD32(tbase + 32, r1);
   tmem_wait_ld();
-  for (int ci = 1; ci < nc; ++ci) {
+  for (int ci = 1; ci < (kBf ? 1 : nc); ++ci) {
     uint32_t t0[32], t1[32];
     MSPIPE_TMEM_LD32(tbase + ci * kN, t0);
     MSPIPE_TMEM_LD32(tbase + ci * kN + 32, t1);
@@ -737,8 +885,9 @@ int gru_tc_splits(int64_t max_rows, const GruDesc& d) {
     const char* e = getenv("MSPIPE_TC_SPLITS");  // debugging / experiments only
     forced = e ? atoi(e) : 0;
   }
-  const int nchunks = d.Kpad / tc::kKC;
-  int64_t s_min = (nchunks + kMaxChunks - 1) / kMaxChunks;  // one TMEM buffer per chunk
+  const int nchunks = d.Kpad / (d.bf16 ? tc::kKC16 : tc::kKC);
+  // tf32: one TMEM buffer per chunk; bf16: a single accumulator, no minimum
+  int64_t s_min = d.bf16 ? 1 : (nchunks + kMaxChunks - 1) / kMaxChunks;
   if (forced > 0) return (int)(forced > s_min ? forced : s_min);
   const int64_t tiles = ((max_rows + tc::kM - 1) / tc::kM) * gru_tc_jtiles(d);
   int64_t s = 1;
@@ -754,7 +903,10 @@ cudaError_t launch_gru_tc(const GruDesc& d, const float* wtc, float* xbuf, const
                           int64_t mail_stride, cudaStream_t s, int parts, const GruCommit* commit) {
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(k_gru_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::kSmemBytes);
+    cudaError_t e = cudaFuncSetAttribute(k_gru_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         tc::kSmemBytes);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(k_gru_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::kSmemBytes);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
@@ -777,7 +929,7 @@ cudaError_t launch_gru_tc(const GruDesc& d, const float* wtc, float* xbuf, const
   const int64_t max_rows = 2 * num_events;
   const int64_t mtiles = (max_rows + tc::kM - 1) / tc::kM;
   if (parts & kGruBuild) {
-    const int64_t warps = mtiles * (d.Kpad / tc::kKC) * tc::kM;
+    const int64_t warps = mtiles * (d.Kpad / (d.bf16 ? tc::kKC16 : tc::kKC)) * tc::kM;
     int64_t blocks = (warps * 32 + 255) / 256;
     const int64_t cap = (int64_t)num_sms() * env_int("MSPIPE_BUILD_BPS", 8);
     if (blocks > cap) blocks = cap;
@@ -786,8 +938,11 @@ cudaError_t launch_gru_tc(const GruDesc& d, const float* wtc, float* xbuf, const
   }
   if (!(parts & kGruGemm)) return cudaSuccess;
   const int S = gru_tc_splits(max_rows, d);
-  return launch_k(k_gru_tc, dim3((unsigned)S, (unsigned)gru_tc_jtiles(d), (unsigned)mtiles), dim3(tc::kThreads),
-                  tc::kSmemBytes, s, (unsigned)S, a);
+  if (d.bf16)
+    return launch_k(k_gru_tc<true>, dim3((unsigned)S, (unsigned)gru_tc_jtiles(d), (unsigned)mtiles),
+                    dim3(tc::kThreads), tc::kSmemBytes, s, (unsigned)S, a);
+  return launch_k(k_gru_tc<false>, dim3((unsigned)S, (unsigned)gru_tc_jtiles(d), (unsigned)mtiles),
+                  dim3(tc::kThreads), tc::kSmemBytes, s, (unsigned)S, a);
 }
 
 }  // namespace mspipe

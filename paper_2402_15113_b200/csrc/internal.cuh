@@ -164,6 +164,7 @@ struct GruDesc {
   const float* bias;    // [Npad]
   const float* time_w;  // [Dt]
   const float* time_b;  // [Dt]
+  int32_t bf16;         // 1: bf16 tensor-core operands (MSPIPE_BF16), Kpad a multiple of 64
   int32_t cell;         // MSPIPE_CELL_GRU | MSPIPE_CELL_RNN (row F3)
   int32_t mailbox;      // MSPIPE_MAILBOX_IMMEDIATE | MSPIPE_MAILBOX_DEFERRED (row F3)
 };

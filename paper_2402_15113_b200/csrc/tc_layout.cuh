@@ -34,5 +34,13 @@ __device__ __forceinline__ void store_a(float* xbuf, int32_t nchunks, int32_t u,
   *reinterpret_cast<float*>(blk + kATile + off) = lo;
 }
 
+// bf16 operands (MSPIPE_BF16): one 128 B swizzle row holds 64 bf16 = one K chunk
+constexpr int kKC16 = 64;
+constexpr int kATile16 = kM * kKC16 * 2;  // 16 KB
+
+__host__ __device__ __forceinline__ uint32_t sw128_off16(uint32_t row, uint32_t k) {
+  return row * 128u + ((((k >> 3) ^ (row & 7u)) & 7u) << 4) + (k & 7u) * 2u;
+}
+
 }  // namespace tc
 }  // namespace mspipe

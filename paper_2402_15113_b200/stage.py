@@ -54,7 +54,7 @@ class StageConfig:
     prep_build: bool = dataclasses.field(default_factory=lambda: os.environ.get("MSPIPE_PREP_BUILD", "0") == "1")
 
     def use_fused(self) -> bool:
-        ok = self.precision == _C.FP32_3XTF32 and self.fanout <= 31 and self.batch <= 8192
+        ok = self.precision in (_C.FP32_3XTF32, _C.BF16) and self.fanout <= 31 and self.batch <= 8192
         return ok if self.fused is None else (self.fused and ok)
 
     def use_double_buffer(self) -> bool:

@@ -14,7 +14,9 @@ w = make_workload(name, num_events=60000)
 cfg = w["cfg"]
 dev = torch.device("cuda:0")
 g = build_tcsr(cfg.num_nodes, w["src"], w["dst"], w["ts"], dev)
-st = MemoryStage(StageConfig(cfg.num_nodes, 100, cfg.edge_dim, 100, 10, cfg.batch, cfg.staleness_k), w["params"], g, dev)
+prec = _C.BF16 if (len(sys.argv) > 2 and sys.argv[2] == "bf16") else _C.FP32_3XTF32
+st = MemoryStage(StageConfig(cfg.num_nodes, 100, cfg.edge_dim, 100, 10, cfg.batch, cfg.staleness_k, precision=prec),
+                 w["params"], g, dev)
 t = {k: torch.from_numpy(w[k]).to(dev) for k in ("src", "dst", "ts", "neg", "ef")}
 st.bind_resident(t["src"], t["dst"], t["ts"], t["neg"], t["ef"])
 ops = st.step_ops()

@@ -660,3 +660,46 @@ def test_updater_variant_abi(dev):
         _C.memory_mail_deferred(h, 3, x, x, x.double(), torch.zeros((4, cfg.edge_dim), device=dev), upd["nodes"],
                                 upd["winner"], upd["num"])
     assert e.value.status == _C.EORDER
+
+
+# ------------------------------------------------------------------ bf16 updater
+BF16_TOL = 2e-2  # north star: "2e-2 if a bf16 GRU path is enabled"
+
+
+@pytest.mark.parametrize("name,i,E", [("tiny", 1, None), ("wiki", 137, None), ("gdelt", 3, 20_000)])
+def test_update_teacher_forced_bf16(dev, name, i, E):
+    """MSPIPE_BF16 (tcgen05 kind::f16, bf16 operands, fp32 accumulation): h' within
+    2e-2 of the f64-accumulated oracle; everything integer or copied stays exact."""
+    st, sl, upd, ref, ev, (mem, mem_ts) = _teacher_forced(dev, name, i, E=E, precision=_C.BF16, fused=True)
+    U = int(upd["num"].item())
+    assert np.array_equal(upd["nodes"][:U].cpu().numpy(), ref["nodes"])
+    assert np.array_equal(upd["ts"][:U].cpu().numpy(), ref["ts"])
+    Dm = ref["mail"].shape[1]
+    assert np.array_equal(upd["mail"][:U].cpu().numpy()[:, :Dm], ref["mail"])
+    g, o = upd["mem"][:U].cpu().numpy().astype(np.float64), ref["mem"].astype(np.float64)
+    err = np.abs(g - o).max()
+    print(f"{name} bf16 teacher-forced max abs err {err:.3g}")
+    assert err <= BF16_TOL
+
+
+@pytest.mark.parametrize("name,k,E,cell", [("wiki", 1, 60_000, "gru"), ("lastfm", 2, 60_000, "gru"),
+                                           ("tiny", 0, None, "rnn")])
+def test_stream_free_running_bf16(dev, name, k, E, cell):
+    from synth import rnn_params
+    w = make_workload(name, seed=12, num_events=E)
+    cfg = w["cfg"]
+    params = rnn_params(cfg.mem_dim, cfg.mail_dim, cfg.time_dim) if cell == "rnn" else w["params"]
+    sc = StageConfig(cfg.num_nodes, cfg.mem_dim, cfg.edge_dim, cfg.time_dim, cfg.fanout, cfg.batch, k,
+                     precision=_C.BF16, cell=cell)
+    g = build_tcsr(cfg.num_nodes, w["src"], w["dst"], w["ts"], dev)
+    st = MemoryStage(sc, params, g, dev)
+    t = {kk: _t(w[kk], dev) for kk in ("src", "dst", "ts", "neg", "ef")}
+    st.bind_resident(t["src"], t["dst"], t["ts"], t["neg"], t["ef"])
+    st.run()
+    torch.cuda.synchronize()
+    _C.check()
+    ref, _ = oracle.run_stream(cfg.num_nodes, w["src"], w["dst"], w["ts"], w["ef"], params, cfg.batch, k, cell=cell)
+    assert np.array_equal(st.memory.mem_ts.cpu().numpy(), ref["mem_ts"])
+    err = np.abs(st.memory.mem.cpu().numpy().astype(np.float64) - ref["mem"]).max()
+    print(f"{name} k={k} {cell} bf16 free-running max abs err {err:.3g}")
+    assert err <= BF16_TOL
