@@ -703,3 +703,47 @@ def test_stream_free_running_bf16(dev, name, k, E, cell):
     err = np.abs(st.memory.mem.cpu().numpy().astype(np.float64) - ref["mem"]).max()
     print(f"{name} k={k} {cell} bf16 free-running max abs err {err:.3g}")
     assert err <= BF16_TOL
+
+
+# ------------------------------------------------------------------ bench launch configuration
+@pytest.mark.parametrize("name,E,gru", [("wiki", None, "tc"), ("gdelt", 80_000, "tc"), ("reddit", 60_000, "tc"),
+                                        ("wiki", None, "bf16")])
+def test_bench_configuration_matches_oracle(dev, name, E, gru):
+    """The configuration bench.py times — per-step graphs (mspipe_util_graph_*)
+    replayed after a reset, the config's own batch and staleness k, double-
+    buffered tables, fused kernels, two streams, MSPipe-S where the config has
+    it — at the workload's full size (GDELT / Reddit: a prefix), against the
+    oracle: timestamps bit-exact, memories within the tolerance."""
+    from paper_2402_15113_b200 import gamma_quantile
+    w = make_workload(name, seed=0, num_events=E)
+    cfg = w["cfg"]
+    mit = None
+    if cfg.mitigation:
+        mit = dict(lam=cfg.lam, gamma=gamma_quantile(cfg.num_nodes, w["src"], w["dst"], w["ts"], cfg.quantile_p),
+                   n_sim=cfg.n_sim)
+    sc = StageConfig(cfg.num_nodes, cfg.mem_dim, cfg.edge_dim, cfg.time_dim, cfg.fanout, cfg.batch,
+                     cfg.staleness_k, mitigation=mit, precision=_C.BF16 if gru == "bf16" else _C.FP32_3XTF32)
+    g = build_tcsr(cfg.num_nodes, w["src"], w["dst"], w["ts"], dev)
+    st = MemoryStage(sc, w["params"], g, dev)
+    assert st.memory.double_buffer == (cfg.staleness_k >= 1)
+    t = {kk: _t(w[kk], dev) for kk in ("src", "dst", "ts", "neg", "ef")}
+    st.bind_resident(t["src"], t["dst"], t["ts"], t["neg"], t["ef"])
+    s = torch.cuda.Stream()
+    graphs = [_C.StepGraph().capture(lambda: st.run_ops(ops), s) for ops in st.step_ops()]
+    st.memory.reset()
+    with torch.cuda.stream(s):
+        for gr in graphs:
+            gr.replay()
+    st.memory.set_committed(len(graphs))
+    torch.cuda.synchronize()
+    _C.check()
+    ref, _ = oracle.run_stream(cfg.num_nodes, w["src"], w["dst"], w["ts"], w["ef"], w["params"], cfg.batch,
+                               cfg.staleness_k, mitigation=mit, fanout=cfg.fanout)
+    assert np.array_equal(st.memory.mem_ts.cpu().numpy(), ref["mem_ts"])
+    gm, om = st.memory.mem.cpu().numpy().astype(np.float64), ref["mem"].astype(np.float64)
+    if gru == "bf16":
+        assert np.abs(gm - om).max() <= BF16_TOL
+    else:
+        rel = np.linalg.norm(gm - om, axis=1) / np.maximum(np.linalg.norm(om, axis=1), 1e-3)
+        print(f"{name} bench configuration: row-rel max {rel.max():.3g}")
+        assert rel.max() <= 1e-4
