@@ -182,10 +182,14 @@ def run_mspipe(args):
     from synth import make_workload
 
     ws, rank, local = _dist()
-    if ws > 1:
-        dist.init_process_group("nccl")
+    # the device first: NCCL collectives of the process group (the unique-id
+    # broadcast, barriers, the max over ranks) run on the current device
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    if ws > 1:
+        # NCCL: connect peers at communicator init, not lazily inside a graph capture
+        os.environ.setdefault("NCCL_RUNTIME_CONNECT", "0")
+        dist.init_process_group("nccl", device_id=dev)
     w = make_workload(args.config, seed=args.seed, num_events=args.events)
     cfg = w["cfg"]
     k = cfg.staleness_k if args.k is None else args.k

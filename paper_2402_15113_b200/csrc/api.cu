@@ -104,6 +104,8 @@ mspipe_status mspipe_sample_batch(const mspipe_tcsr* g, const int32_t* src, cons
   return after_launch("sample_batch");
 }
 
+static mspipe_status nccl_warmup(mspipe_memory* st);
+
 mspipe_status mspipe_memory_create(mspipe_memory** out, int64_t num_nodes, int32_t mem_dim,
                                    int32_t edge_dim, int32_t staleness_k, float* mem,
                                    double* mem_ts, float* mail, double* mail_ts,
@@ -165,6 +167,7 @@ mspipe_status mspipe_memory_create(mspipe_memory** out, int64_t num_nodes, int32
   }
   if (world > 1 && nccl_unique_id) {
     mspipe_status rc = nccl_comm_init(st, nccl_unique_id);
+    if (rc == MSPIPE_OK) rc = nccl_warmup(st);
     if (rc != MSPIPE_OK) {
       mspipe_memory_destroy(st);
       return rc;
@@ -884,6 +887,29 @@ static void xchg_bufs(mspipe_memory* st, int32_t kind, void** send, void** recv,
     *recv = st->sh_crecv;
     *chunk = (size_t)shard_commit_rec_bytes(st) * (size_t)st->sh_capw;
   }
+}
+
+// One eager exchange of every kind at the sizes the step uses (fetch rows with
+// mail = the largest), so NCCL sets up its peer connections now: a lazy
+// connection setup inside a CUDA-graph capture would allocate and break it.
+static mspipe_status nccl_warmup(mspipe_memory* st) {
+  cudaStream_t s = nullptr;
+  cudaError_t e = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+  if (e != cudaSuccess) return cuda_status(e, "memory_create: NCCL warm-up stream");
+  const int32_t with_mail = st->sh_with_mail;
+  st->sh_with_mail = 1;
+  mspipe_status rc = MSPIPE_OK;
+  for (int32_t kind = 0; kind < 3 && rc == MSPIPE_OK; ++kind) {
+    void *send, *recv;
+    size_t chunk;
+    xchg_bufs(st, kind, &send, &recv, &chunk);
+    rc = nccl_alltoall(st, send, recv, chunk, s);
+  }
+  st->sh_with_mail = with_mail;
+  e = cudaStreamSynchronize(s);
+  cudaStreamDestroy(s);
+  if (rc == MSPIPE_OK && e != cudaSuccess) rc = cuda_status(e, "memory_create: NCCL warm-up");
+  return rc;
 }
 
 mspipe_status mspipe_shard_exchange(mspipe_memory* st, int32_t kind, void* stream) {
