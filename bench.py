@@ -383,7 +383,8 @@ def run_mspipe(args):
                                       f"shard{ws}: node-id-sharded memory, NCCL all-to-all fetch + write-back, "
                                       f"global batch {G * cfg.batch}" if sharded else f"replicas{ws}")},
            "roofline": roof, "roofline_gather": roof_gather, "roofline_features": roof_features, "gpu_launches": _launches(st.step_ops(), timed_batches, bool(mit),
-                                                       getattr(st, "fused", False), sharded, args.features), "clocks": clocks}
+                                                       getattr(st, "fused", False), sharded, args.features,
+                                                       getattr(st, "gemm_build", False)), "clocks": clocks}
     if args.profile:
         if rank == 0:
             print(json.dumps(out))
@@ -413,7 +414,7 @@ def run_mspipe(args):
         dist.destroy_process_group()
 
 
-def _launches(steps, timed_batches, mit, fused, sharded=False, features=False):
+def _launches(steps, timed_batches, mit, fused, sharded=False, features=False, gemm_build=False):
     """Kernels of this library per timed step.  fused: prep = k_prep + k_build_x
     (+ k_mitigate), commit = k_gru_tc with the write-back in its epilogue; otherwise prep = sampler +
     dedup + gather (+ mitigation), commit = build + GEMM (or SIMT GRU) + write-back.  Sharded:
@@ -422,7 +423,8 @@ def _launches(steps, timed_batches, mit, fused, sharded=False, features=False):
     if sharded:
         per = {"prep": 6, "commit": 7}
         return int(sum(per[op] for t in timed_batches for op, _ in steps[t]))
-    per = {"prep": (2 if fused else 3) + (1 if mit else 0) + (1 if features else 0), "commit": 1 if fused else 3}
+    per = {"prep": (1 if gemm_build else 2 if fused else 3) + (1 if mit else 0) + (1 if features else 0),
+           "commit": 1 if fused else 3}
     return int(sum(per[op] for t in timed_batches for op, _ in steps[t]))
 
 

@@ -405,6 +405,23 @@ MSPIPE_API mspipe_status mspipe_gru_apply_commit(const mspipe_gru* gru, mspipe_m
                                       const float* new_mail, float* out_mem, const void* workspace,
                                       size_t ws_bytes, void* stream);
 
+/* A5 + A6 + A7 in ONE launch (3xTF32, immediate mailbox, no mitigation):
+ * exactly mspipe_message_build (snap_h = NULL) + mspipe_gru_apply_commit of
+ * the same batch, but the GEMM kernel builds its A operand in shared memory
+ * from the snapshot rows (snap_mem / snap_mem_ts rows as in
+ * mspipe_message_build), so no operand images or staged mail rows exist and
+ * no workspace is needed; it writes h' (out_mem, nullable, winner order), and
+ * the rows, timestamps and mail rows of version commit_version.  ts /
+ * edge_feat: the batch's events.  Same ordering contract as
+ * mspipe_gru_apply_commit. */
+MSPIPE_API mspipe_status mspipe_gru_build_apply_commit(const mspipe_gru* gru, mspipe_memory* st,
+                                            int64_t commit_version, int64_t num_events,
+                                            const double* ts, const float* edge_feat,
+                                            const float* snap_mem, const double* snap_mem_ts,
+                                            int64_t snap_step, const int32_t* nodes,
+                                            const int32_t* winner, const int32_t* num_unique,
+                                            float* out_mem, void* stream);
+
 /* ---------------------------------------------------------------------------
  * Row E: node memory sharded by node id (world > 1).  owner(v) = v mod world,
  * local row = v / world: the tables passed to mspipe_memory_create hold this

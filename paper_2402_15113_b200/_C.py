@@ -35,7 +35,7 @@ EXPORTS = ("mspipe_abi_version", "mspipe_last_error", "mspipe_check", "mspipe_sa
            "mspipe_memory_double_buffer", "mspipe_memory_tables", "mspipe_memory_set_committed",
            "mspipe_plan_timeline", "mspipe_plan_min_staleness", "mspipe_stale_histogram",
            "mspipe_memory_prep_build", "mspipe_feature_fetch", "mspipe_updater_create",
-           "mspipe_message_build_deferred", "mspipe_memory_mail_deferred")
+           "mspipe_message_build_deferred", "mspipe_memory_mail_deferred", "mspipe_gru_build_apply_commit")
 XCHG_FETCH_IDS, XCHG_FETCH_ROWS, XCHG_COMMIT = 0, 1, 2
 
 
@@ -101,6 +101,7 @@ def lib():
         L.mspipe_updater_create.argtypes = [C.POINTER(P), i32, i32, i32, i32, i32, i32, i64, P, P, P, P, P, P, P]
         L.mspipe_message_build_deferred.argtypes = [P, P, i64, P, P, P, i64, i64, P, P, P, P, C.c_size_t, P]
         L.mspipe_memory_mail_deferred.argtypes = [P, i64, P, P, P, P, i64, P, P, P, P]
+        L.mspipe_gru_build_apply_commit.argtypes = [P, P, i64, i64, P, P, P, P, i64, P, P, P, P, P]
         L.mspipe_feature_fetch.argtypes = [P, P, i64, i32, P, i64, i32, P, i64, i32, P, P, P]
         L.mspipe_gru_workspace_size.argtypes = [P, i64]
         L.mspipe_gru_workspace_size.restype = C.c_size_t
@@ -540,6 +541,15 @@ def gru_apply_commit(gru: GruHandle, st: MemoryHandle, commit_version, num_event
                                       ptr(upd["num"]), ptr(upd["ts"]), ptr(upd.get("mail")), ptr(upd.get("mem")),
                                       ptr(workspace), workspace.numel() * workspace.element_size(),
                                       stream_ptr(stream)), "mspipe_gru_apply_commit")
+
+
+def gru_build_apply_commit(gru: GruHandle, st: MemoryHandle, commit_version, ts, edge_feat, snap_mem, snap_mem_ts,
+                           snap_step, upd, stream=None):
+    """A5+A6+A7 in one launch: the GEMM kernel builds its operand from the snapshot rows."""
+    _ck(lib().mspipe_gru_build_apply_commit(gru.h, st.h, int(commit_version), ts.numel(), ptr(ts), ptr(edge_feat),
+                                            ptr(snap_mem), ptr(snap_mem_ts), int(snap_step), ptr(upd["nodes"]),
+                                            ptr(upd["winner"]), ptr(upd["num"]), ptr(upd.get("mem")),
+                                            stream_ptr(stream)), "mspipe_gru_build_apply_commit")
 
 
 def alloc_dedup(num_events, device):

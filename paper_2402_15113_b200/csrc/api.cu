@@ -780,6 +780,51 @@ mspipe_status mspipe_gru_apply_commit(const mspipe_gru* gru, mspipe_memory* st,
   return rc;
 }
 
+mspipe_status mspipe_gru_build_apply_commit(const mspipe_gru* gru, mspipe_memory* st, int64_t commit_version,
+                                            int64_t num_events, const double* ts, const float* edge_feat,
+                                            const float* snap_mem, const double* snap_mem_ts, int64_t snap_step,
+                                            const int32_t* nodes, const int32_t* winner, const int32_t* num_unique,
+                                            float* out_mem, void* stream) {
+  if (!gru || !st) return fail(MSPIPE_EINVAL, "gru_build_apply_commit: NULL handle");
+  if (gru->precision != MSPIPE_FP32_3XTF32 || gru->d.mailbox != MSPIPE_MAILBOX_IMMEDIATE)
+    return fail(MSPIPE_EUNSUPPORTED, "gru_build_apply_commit: needs an immediate-mailbox MSPIPE_FP32_3XTF32 handle");
+  if (st->world != 1) return fail(MSPIPE_EUNSUPPORTED, "gru_build_apply_commit: world > 1");
+  if (gru->d.M != st->mem_dim || gru->d.He != st->edge_dim) return fail(MSPIPE_EINVAL, "gru_build_apply_commit: dims");
+  if (commit_version != st->committed + 1)
+    return fail(MSPIPE_EORDER, "gru_build_apply_commit: commit_version=%lld but committed=%lld",
+                (long long)commit_version, (long long)st->committed);
+  if (num_events < 0 || num_events > gru->max_events || snap_step < 1)
+    return fail(MSPIPE_EINVAL, "gru_build_apply_commit: num_events=%lld snap_step=%lld", (long long)num_events,
+                (long long)snap_step);
+  if (num_events > 0 && (!ts || (st->edge_dim > 0 && !edge_feat) || !snap_mem || !snap_mem_ts || !nodes ||
+                         !winner || !num_unique))
+    return fail(MSPIPE_EINVAL, "gru_build_apply_commit: null input");
+  const int64_t max_n = 2 * num_events;
+  const bool done = st->db && st->caught_up == commit_version;
+  if (st->db && (num_events == 0 || !done)) {  // catch-up not enqueued by a prep: its own kernel first
+    cudaError_t e = db_catchup(st, commit_version, nodes, num_unique, max_n, (cudaStream_t)stream, !done);
+    if (e != cudaSuccess) return cuda_status(e, "gru_build_apply_commit: catch-up");
+  }
+  if (num_events > 0) {
+    const TableSet t = table_set(st, commit_version);
+    GruCommit c{nodes, t.mem, t.mem_ts, t.mail, t.mail_ts, nullptr, nullptr, st->num_nodes, st->mail_stride};
+    if (done) {  // the kernel saves this commit's winner list
+      const int p = (int)(commit_version & 1);
+      c.save_nodes = st->prev_nodes + p * st->num_nodes;
+      c.save_num = st->prev_num + p;
+    }
+    cudaError_t e = launch_gru_fb(gru->d, gru->wtc, ts, num_events, edge_feat, snap_mem, snap_mem_ts, snap_step,
+                                  winner, num_unique, out_mem, c, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_status(e, "gru_build_apply_commit: launch");
+  }
+  mspipe_status rc = after_launch("gru_build_apply_commit");
+  if (rc == MSPIPE_OK) {
+    st->committed = commit_version;
+    st->prev_max[commit_version & 1] = max_n;
+  }
+  return rc;
+}
+
 // ---------------------------------------------------------------------------
 // row E: sharded memory
 // ---------------------------------------------------------------------------

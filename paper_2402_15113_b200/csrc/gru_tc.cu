@@ -875,6 +875,322 @@ void launch_mail_deferred(const int32_t* src, const int32_t* dst, const double* 
            num_unique, mem, M, mail, mail_ts, mail_stride, num_nodes);
 }
 
+// ---------------------------------------------------------------------------
+// k_gru_fb — A5 + A6 + A7 in ONE kernel (mspipe_gru_build_apply_commit, 3xTF32,
+// immediate mailbox, no mitigation).  The CTA builds its own A operand in
+// shared memory instead of loading images written by k_build_x: 6 builder
+// warps gather the message x = [s_w | s_o | e | cos(w dt + p) | h] of its 128
+// rows for its K range chunk by chunk, split hi | lo into the SWIZZLE_128B
+// stage buffers, fence the generic->async proxy and arrive on the stage's
+// full barrier; one thread streams the B images with cp.async.bulk; the MMA
+// issuer, TMEM buffers, K-split exchange and GRU epilogue are k_gru_tc's.
+// The mail rows of the commit ([s_w | s_o | e], G14) are written to the state
+// table by the builders (chunk c by the CTA with jt = c mod J), mem_ts /
+// mail_ts by the epilogue.  One launch instead of k_build_x + k_gru_tc, and no
+// operand images in HBM.
+// ---------------------------------------------------------------------------
+int gru_tc_splits(int64_t max_rows, const GruDesc& d);
+constexpr int kFBThreads = 256;
+constexpr int kFBBuilders = kFBThreads - 64;
+
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(tc::smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void builders_sync() {
+  asm volatile("bar.sync 1, %0;\n" ::"r"(kFBBuilders) : "memory");
+}
+
+// x[k] of winner pair p with its Δt precomputed (the k_build_x value)
+__device__ __forceinline__ float xval(const TcArgs& a, int32_t p, int32_t k, float dt) {
+  const GruDesc& d = a.d;
+  const int32_t M = d.M;
+  const int32_t ev = p >> 1, role = p & 1;
+  const int64_t rw = role ? a.B + ev : ev;
+  const int64_t ro = role ? ev : a.B + ev;
+  const float* __restrict__ snap = a.snap_mem;
+  if (k < M) return __ldg(snap + rw * a.step * M + k);
+  if (k < 2 * M) return __ldg(snap + ro * a.step * M + (k - M));
+  if (k < d.Dm) return __ldg(a.ef + (int64_t)ev * d.He + (k - 2 * M));
+  if (k < d.Dx) return time_cos(fmaf(__ldg(d.time_w + (k - d.Dm)), dt, __ldg(d.time_b + (k - d.Dm))));
+  if (k < d.K) return __ldg(snap + rw * a.step * M + (k - d.Dx));
+  return 0.f;
+}
+
+__global__ void __launch_bounds__(kFBThreads, 1) k_gru_fb(TcArgs a) {
+  using namespace tc;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
+  uint64_t* empty = full + kStages;
+  uint64_t* acc_full = empty + kStages;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 1);
+  int32_t* rownode = reinterpret_cast<int32_t*>(smem + kStages * kStageBytes + 512);
+  float4* hbuf = reinterpret_cast<float4*>(smem + kStages * kStageBytes + 1024);
+  float4* recv = reinterpret_cast<float4*>(smem + kStages * kStageBytes + 1024 + kHBufBytes);
+  float* sbias = reinterpret_cast<float*>(smem + kStages * kStageBytes + 1024 + kHBufBytes + kRecvBytes);
+  int32_t* rpair = reinterpret_cast<int32_t*>(sbias + kN);  // [128] winner pair of each row, -1 past U
+  float* rdt = reinterpret_cast<float*>(rpair + kM);        // [128] Δt of each row (G4)
+
+  const GruDesc& d = a.d;
+  pdl_begin();
+  const int32_t U = __ldg(a.num_unique);
+  const int32_t mt = blockIdx.z;
+  const int32_t m0 = mt * kM;
+  const int jt = blockIdx.y;
+  const int J = (int)gridDim.y;
+  const int S = gridDim.x;
+  const int split = blockIdx.x;
+  if (a.save_num && mt == 0 && jt == 0 && split == 0 && threadIdx.x == 0) *a.save_num = U;
+  if (m0 >= U) return;  // uniform across the cluster
+  const int32_t nchunks = d.Kpad / kKC;
+  const int32_t c0 = split * nchunks / S, c1 = (split + 1) * nchunks / S;
+  const int32_t nc = c1 - c0;
+  const uint32_t tcols = nc <= 2 ? 128u : (nc <= 4 ? 256u : 512u);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int rank = S > 1 ? (int)cluster_rank() : 0;
+  const int rb = rank * kM / S, re = (rank + 1) * kM / S;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1 + kFBBuilders);  // the B copy's expect_tx + every builder
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(acc_full, 1);
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, tcols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0 && lane == 0) {
+    const char* bbase = reinterpret_cast<const char*>(a.wtc) + (int64_t)jt * nchunks * kBBlock;
+    for (int ci = 0; ci < nc; ++ci) {
+      const int s = ci % kStages;
+      const uint32_t ph = (uint32_t)(ci / kStages) & 1u;
+      mbar_wait(&empty[s], ph ^ 1u);
+      mbar_arrive_expect_tx(&full[s], kBBlock);
+      bulk_g2s(smem + s * kStageBytes + kABlock, bbase + (int64_t)(c0 + ci) * kBBlock, kBBlock, &full[s]);
+    }
+  } else if (warp == 1 && lane == 0) {
+    for (int ci = 0; ci < nc; ++ci) {
+      const int s = ci % kStages;
+      const uint32_t ph = (uint32_t)(ci / kStages) & 1u;
+      mbar_wait(&full[s], ph);
+      tc_fence_after();
+      const uint32_t base = smem_u32(smem + s * kStageBytes);
+      const uint64_t da_hi = sw128_desc(base), da_lo = sw128_desc(base + kATile);
+      const uint64_t db_hi = sw128_desc(base + kABlock), db_lo = sw128_desc(base + kABlock + kBTile);
+      const uint32_t tacc = tmem + (uint32_t)(ci * kN);
+#pragma unroll
+      for (int kk = 0; kk < kKC / 8; ++kk) {
+        const uint64_t adv = (uint64_t)(kk * 32) >> 4;
+        mma_tf32(tacc, da_lo + adv, db_hi + adv, kIdesc, kk != 0);
+        mma_tf32(tacc, da_hi + adv, db_lo + adv, kIdesc, 1u);
+        mma_tf32(tacc, da_hi + adv, db_hi + adv, kIdesc, 1u);
+      }
+      mma_commit(&empty[s]);
+    }
+    mma_commit(acc_full);
+  } else if (warp >= 2) {
+    const int bt = threadIdx.x - 64;
+    // rows: winner pair, Δt, committed node; h and biases for the epilogue
+    for (int r = bt; r < kM; r += kFBBuilders) {
+      const int32_t u = m0 + r;
+      int32_t p = -1, node = -1;
+      float dt = 0.f;
+      if (u < U) {
+        p = __ldg(a.winner + u);
+        const int64_t ev = p >> 1;
+        const int64_t rw = (p & 1) ? a.B + ev : ev;
+        dt = (float)(__ldg(a.ts + ev) - __ldg(a.snap_ts + rw * a.step));
+        node = __ldg(a.nodes + u);
+        if (a.save_nodes && jt == 0 && split == 0) a.save_nodes[u] = node;
+      }
+      rpair[r] = p;
+      rdt[r] = dt;
+      rownode[r] = node;
+    }
+    for (int it = bt; it < (re - rb) * (kJ / 4); it += kFBBuilders) {
+      const int mm = rb + it / (kJ / 4), q = it % (kJ / 4);
+      const int32_t u = m0 + mm, j0 = jt * kJ + q * 4;
+      float4 hv = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (u < U && j0 < d.M) {
+        const int32_t p = __ldg(a.winner + u);
+        const int64_t rw = (p & 1) ? a.B + (p >> 1) : (p >> 1);
+        hv = __ldg(reinterpret_cast<const float4*>(a.snap_mem + rw * a.step * d.M + j0));
+      }
+      hbuf[mm * (kJ / 4) + q] = hv;
+    }
+    for (int i = bt; i < kN; i += kFBBuilders) sbias[i] = __ldg(d.bias + jt * kN + i);
+    builders_sync();
+    // the A operand of this CTA's K range, chunk by chunk into the stage ring
+    float* __restrict__ mail = a.commit_mail;
+    for (int ci = 0; ci < nc; ++ci) {
+      const int s = ci % kStages;
+      const uint32_t ph = (uint32_t)(ci / kStages) & 1u;
+      mbar_wait(&empty[s], ph ^ 1u);
+      uint8_t* st = smem + s * kStageBytes;
+      const int32_t c = c0 + ci;
+      const bool mailw = a.commit_mail && (c % J) == jt;
+      for (int e = bt; e < kM * kKC; e += kFBBuilders) {
+        const int row = e >> 5, col = e & 31;
+        const int32_t k = c * kKC + col;
+        const int32_t p = rpair[row];
+        const float v = p >= 0 ? xval(a, p, k, rdt[row]) : 0.f;
+        const float hi = tf32_rna(v);
+        const uint32_t off = sw128_off((uint32_t)row, (uint32_t)col);
+        *reinterpret_cast<float*>(st + off) = hi;
+        *reinterpret_cast<float*>(st + kATile + off) = tf32_rna(v - hi);
+        if (mailw && p >= 0 && k < a.mail_stride)
+          mail[(int64_t)rownode[row] * a.mail_stride + k] = k < d.Dm ? v : 0.f;
+      }
+      fence_proxy_async_smem();  // generic-proxy smem writes -> visible to the tensor core
+      mbar_arrive(&full[s]);
+    }
+  }
+  __syncwarp();
+
+  // ---------------- epilogue (warps 0-3 own the 128 TMEM lanes)
+  mbar_wait(acc_full, 0);
+  tc_fence_after();
+  const int m = (warp & 3) * 32 + lane;
+  uint32_t r0[32], r1[32];
+  if (warp < 4) {
+    const uint32_t tbase = tmem + ((uint32_t)(warp * 32) << 16);
+    MSPIPE_TMEM_LD32(tbase, r0);
+    MSPIPE_TMEM_LD32(tbase + 32, r1);
+    tmem_wait_ld();
+    for (int ci = 1; ci < nc; ++ci) {
+      uint32_t t0[32], t1[32];
+      MSPIPE_TMEM_LD32(tbase + ci * kN, t0);
+      MSPIPE_TMEM_LD32(tbase + ci * kN + 32, t1);
+      tmem_wait_ld();
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        r0[i] = __float_as_uint(__fadd_rn(__uint_as_float(r0[i]), __uint_as_float(t0[i])));
+        r1[i] = __float_as_uint(__fadd_rn(__uint_as_float(r1[i]), __uint_as_float(t1[i])));
+      }
+    }
+    if (S > 1) {
+      const int R = kM / S;
+      const int owner = m / R, lm = m % R;
+      const uint32_t dst =
+          mapa(smem_u32(recv) + (uint32_t)((cluster_rank() * R + lm) * (kN / 4)) * 16u, (uint32_t)owner);
+#pragma unroll
+      for (int c4 = 0; c4 < 8; ++c4) {
+        st_dsmem_f4(dst + 16u * (uint32_t)(c4 ^ (lm & 15)), __uint_as_float(r0[4 * c4]),
+                    __uint_as_float(r0[4 * c4 + 1]), __uint_as_float(r0[4 * c4 + 2]),
+                    __uint_as_float(r0[4 * c4 + 3]));
+        st_dsmem_f4(dst + 16u * (uint32_t)((8 + c4) ^ (lm & 15)), __uint_as_float(r1[4 * c4]),
+                    __uint_as_float(r1[4 * c4 + 1]), __uint_as_float(r1[4 * c4 + 2]),
+                    __uint_as_float(r1[4 * c4 + 3]));
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem, tcols);
+  }
+  const float* bias = sbias;
+  if (S == 1) {
+    const int32_t u = m0 + m;
+    if (warp < 4 && u < U) {
+#pragma unroll
+      for (int q = 0; q < kJ / 4; ++q) {
+        const int32_t j0 = jt * kJ + q * 4;
+        if (j0 >= d.M) break;
+        float pr[4], pz[4], pnx[4], pnh[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int jj = q * 4 + e;
+          pr[e] = __uint_as_float(r0[jj]) + bias[jj];
+          pz[e] = __uint_as_float(r0[kJ + jj]) + bias[kJ + jj];
+          pnx[e] = __uint_as_float(r1[jj]) + bias[2 * kJ + jj];
+          pnh[e] = __uint_as_float(r1[kJ + jj]) + bias[3 * kJ + jj];
+        }
+        store_h4(a, u, rownode[m], j0, gates4(pr, pz, pnx, pnh, hbuf[m * (kJ / 4) + q], d.cell));
+      }
+    }
+  } else {
+    cluster_sync_all();
+    const int R = kM / S;
+    for (int it = threadIdx.x; it < R * (kJ / 4); it += blockDim.x) {
+      const int lm = it / (kJ / 4), q = it % (kJ / 4);
+      const int mm = rb + lm;
+      const int32_t u = m0 + mm;
+      const int32_t j0 = jt * kJ + q * 4;
+      if (u >= U || j0 >= d.M) continue;
+      float4 acc[4];
+#pragma unroll
+      for (int g = 0; g < 4; ++g) acc[g] = recv[(0 * R + lm) * (kN / 4) + ((g * (kJ / 4) + q) ^ (lm & 15))];
+      for (int sr = 1; sr < S; ++sr)
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+          const float4 v = recv[(sr * R + lm) * (kN / 4) + ((g * (kJ / 4) + q) ^ (lm & 15))];
+          acc[g].x += v.x;
+          acc[g].y += v.y;
+          acc[g].z += v.z;
+          acc[g].w += v.w;
+        }
+      float pr[4], pz[4], pnx[4], pnh[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int jj = q * 4 + e;
+        pr[e] = (&acc[0].x)[e] + bias[jj];
+        pz[e] = (&acc[1].x)[e] + bias[kJ + jj];
+        pnx[e] = (&acc[2].x)[e] + bias[2 * kJ + jj];
+        pnh[e] = (&acc[3].x)[e] + bias[3 * kJ + jj];
+      }
+      store_h4(a, u, rownode[mm], j0, gates4(pr, pz, pnx, pnh, hbuf[mm * (kJ / 4) + q], d.cell));
+    }
+  }
+  // commit timestamps (G14: mem_ts = mail_ts = t* of the winner)
+  if (jt == 0 && a.commit_mem)
+    for (int mm = rb + (int)threadIdx.x; mm < re; mm += blockDim.x) {
+      const int32_t u = m0 + mm, node = rownode[mm];
+      if (u < U && node >= 0) {
+        const double t = __ldg(a.ts + (rpair[mm] >> 1));
+        a.commit_mem_ts[node] = t;
+        a.commit_mail_ts[node] = t;
+      }
+    }
+}
+
+cudaError_t launch_gru_fb(const GruDesc& d, const float* wtc, const double* ts, int64_t num_events,
+                          const float* edge_feat, const float* snap_mem, const double* snap_mem_ts,
+                          int64_t snap_step, const int32_t* winner, const int32_t* num_unique, float* out_mem,
+                          const GruCommit& commit, cudaStream_t s) {
+  static bool attr_set = false;
+  const size_t smem = (size_t)tc::kSmemBytes + 2 * tc::kM * 4;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(k_gru_fb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  TcArgs a{d, wtc, nullptr, ts, num_events, edge_feat, snap_mem, snap_mem_ts, snap_step, nullptr, winner,
+           num_unique, out_mem, nullptr, nullptr, commit.mail_stride};
+  a.nodes = commit.nodes;
+  a.commit_mem = commit.mem;
+  a.commit_mem_ts = commit.mem_ts;
+  a.commit_mail = commit.mail;
+  a.commit_mail_ts = commit.mail_ts;
+  a.num_nodes = commit.num_nodes;
+  a.save_nodes = commit.save_nodes;
+  a.save_num = commit.save_num;
+  const int64_t max_rows = 2 * num_events;
+  const int64_t mtiles = (max_rows + tc::kM - 1) / tc::kM;
+  const int S = gru_tc_splits(max_rows, d);
+  return launch_k(k_gru_fb, dim3((unsigned)S, (unsigned)gru_tc_jtiles(d), (unsigned)mtiles), dim3(kFBThreads), smem,
+                  s, (unsigned)S, a);
+}
+
 constexpr int kMaxChunks = 8;  // 8 x 64 TMEM columns = 512 (the whole TMEM of the SM)
 
 int gru_tc_splits(int64_t max_rows, const GruDesc& d) {

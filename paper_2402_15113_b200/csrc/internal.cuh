@@ -268,6 +268,11 @@ void launch_mail_deferred(const int32_t* src, const int32_t* dst, const double* 
                           const int32_t* nodes, const int32_t* winner, const int32_t* num_unique, int64_t max_n,
                           const float* mem, int32_t M, float* mail, double* mail_ts, int64_t mail_stride,
                           int64_t num_nodes, cudaStream_t s);
+// A5 + A6 + A7 in one kernel: the CTA builds its A operand in shared memory (gru_tc.cu, k_gru_fb)
+cudaError_t launch_gru_fb(const GruDesc& d, const float* wtc, const double* ts, int64_t num_events,
+                          const float* edge_feat, const float* snap_mem, const double* snap_mem_ts,
+                          int64_t snap_step, const int32_t* winner, const int32_t* num_unique, float* out_mem,
+                          const GruCommit& commit, cudaStream_t s);
 cudaError_t launch_gru_tc(const GruDesc& d, const float* wtc, float* xbuf, const double* ts, int64_t num_events,
                           const float* edge_feat, const float* snap_mem, const double* snap_mem_ts,
                           int64_t snap_step, const float* snap_h, const int32_t* winner,

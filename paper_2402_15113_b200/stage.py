@@ -48,6 +48,11 @@ class StageConfig:
     mailbox: str = "immediate"  # row F3: "immediate" (G14) | "deferred" (TGL's TGN; needs fetch_mail)
     features: bool = False     # row F2: fetch node / edge features of the sampled subgraphs (bind_features)
     node_dim: int = 0          # |d_v| (GDELT 413); rows padded to a multiple of 4 floats on the device
+    # fused 3xTF32 path without mitigation: the GEMM kernel builds its own operand
+    # (mspipe_gru_build_apply_commit).  Off by default: measured 73 vs 25 us per wiki
+    # step — 6 builder warps per SM cannot keep enough loads in flight to gather the
+    # operand (k_build_x spreads the same gather over ~10^4 warps).  env MSPIPE_GEMM_BUILD=1: A/B
+    gemm_build: bool = dataclasses.field(default_factory=lambda: os.environ.get("MSPIPE_GEMM_BUILD", "0") == "1")
     # fused path without mitigation: message build inside the prep kernel (mspipe_memory_prep_build).
     # Off by default: measured slower on the wiki step (30.7 vs 26.0 us; the build waits for the
     # single dedup block and the longer prep kernel contends with the GEMM).  env MSPIPE_PREP_BUILD=1: A/B
@@ -192,6 +197,8 @@ class MemoryStage(_TimedOps):
                                 mailbox=_C.MAILBOX_DEFERRED if self.deferred else _C.MAILBOX_IMMEDIATE)
         self.upd = _C.alloc_update(cfg.batch, cfg.mem_dim, self.memory.mail_stride, self.device)
         self.fused = cfg.use_fused()
+        self.gemm_build = (self.fused and cfg.gemm_build and not cfg.mitigation and not self.deferred
+                           and cfg.precision == _C.FP32_3XTF32 and not cfg.prep_build)
         if self.deferred and not (self.fused and cfg.fetch_mail and not cfg.prep_build):
             raise ValueError("mailbox='deferred' runs on the fused tensor-core path with fetch_mail=True")
         self.ws_bytes = _C.gru_workspace_size(self.gru, cfg.batch) if self.fused else 0
@@ -403,6 +410,8 @@ class MemoryStage(_TimedOps):
         if not self.memory.double_buffer:
             self._fetched = torch.cuda.Event()  # the state tables have been read for batch i
             self._fetched.record()
+        if self.gemm_build:  # the commit's GEMM kernel builds the message itself
+            return
         self._ev("build")
         if self.deferred:  # row F3: the message is the stored mail of the snapshot
             _C.message_build_deferred(self.gru, x["ts"], sl.mem, sl.mem_ts, sl.mail, cfg.fanout + 1,
@@ -431,6 +440,10 @@ class MemoryStage(_TimedOps):
         self._ev("update")
         if self.fused:
             upd = self._upd(i)
+            if self.gemm_build:  # the prep left the build to the commit kernel: build here for the plain apply
+                _C.message_build(self.gru, x["ts"], x["ef"], sl.mem, sl.mem_ts, cfg.fanout + 1,
+                                 sl.dd["winner"][: 2 * n], sl.dd["num"], sl.uts[: 2 * n], sl.umail[: 2 * n], sl.ws)
+                upd.update(ts=sl.uts[: 2 * n], mail=sl.umail[: 2 * n])
             _C.gru_apply(self.gru, n, sl.mem, cfg.fanout + 1, upd["winner"], upd["num"], upd["mem"], sl.ws,
                          snap_h=sl.h[: 2 * n] if sl.h is not None else None)
         else:
@@ -459,8 +472,13 @@ class MemoryStage(_TimedOps):
         n = self.inputs(i)["src"].numel()
         upd = self._upd(i)
         self._ev("update")
-        _C.gru_apply_commit(self.gru, self.memory, i, n, sl.mem, cfg.fanout + 1, upd, sl.ws,
-                            snap_h=sl.h[: 2 * n] if sl.h is not None else None)
+        if self.gemm_build:
+            x = self.inputs(i)
+            _C.gru_build_apply_commit(self.gru, self.memory, i, x["ts"], x["ef"], sl.mem, sl.mem_ts, cfg.fanout + 1,
+                                      upd)
+        else:
+            _C.gru_apply_commit(self.gru, self.memory, i, n, sl.mem, cfg.fanout + 1, upd, sl.ws,
+                                snap_h=sl.h[: 2 * n] if sl.h is not None else None)
         if self.deferred:  # row F3: new mails from the committed memories of both endpoints
             x = self.inputs(i)
             _C.memory_mail_deferred(self.memory, i, x["src"], x["dst"], x["ts"], x["ef"], upd["nodes"], upd["winner"],

@@ -747,3 +747,31 @@ def test_bench_configuration_matches_oracle(dev, name, E, gru):
         rel = np.linalg.norm(gm - om, axis=1) / np.maximum(np.linalg.norm(om, axis=1), 1e-3)
         print(f"{name} bench configuration: row-rel max {rel.max():.3g}")
         assert rel.max() <= 1e-4
+
+
+
+@pytest.mark.parametrize("name,k,E", [("tiny", 0, None), ("wiki", 1, 60_000), ("lastfm", 2, 60_000)])
+def test_gemm_build_path_equals_oracle(dev, name, k, E):
+    """mspipe_gru_build_apply_commit (operand built inside the GEMM kernel, off by
+    default) over whole streams against the oracle."""
+    w = make_workload(name, seed=13, num_events=E)
+    cfg = w["cfg"]
+    sc = StageConfig(cfg.num_nodes, cfg.mem_dim, cfg.edge_dim, cfg.time_dim, cfg.fanout, cfg.batch, k,
+                     fetch_mail=True, gemm_build=True)
+    g = build_tcsr(cfg.num_nodes, w["src"], w["dst"], w["ts"], dev)
+    st = MemoryStage(sc, w["params"], g, dev)
+    assert st.gemm_build
+    t = {kk: _t(w[kk], dev) for kk in ("src", "dst", "ts", "neg", "ef")}
+    st.bind_resident(t["src"], t["dst"], t["ts"], t["neg"], t["ef"])
+    st.run()
+    torch.cuda.synchronize()
+    _C.check()
+    ref, _ = oracle.run_stream(cfg.num_nodes, w["src"], w["dst"], w["ts"], w["ef"], w["params"], cfg.batch, k)
+    assert np.array_equal(st.memory.mem_ts.cpu().numpy(), ref["mem_ts"])
+    assert np.array_equal(st.memory.mail_ts.cpu().numpy(), ref["mail_ts"])
+    gm, om = st.memory.mem.cpu().numpy().astype(np.float64), ref["mem"].astype(np.float64)
+    rel = np.linalg.norm(gm - om, axis=1) / np.maximum(np.linalg.norm(om, axis=1), 1e-3)
+    assert rel.max() <= 1e-4
+    Dm = cfg.mail_dim  # mail = [s_w | s_o | e]: memory values, so within the fp32 tolerance
+    ok, err = _close(st.memory.mail.cpu().numpy()[:, :Dm], ref["mail"], rtol=1e-4, atol=1e-5)
+    assert ok, err
