@@ -1,22 +1,25 @@
 """The per-batch node-memory stage as a stream-ordered schedule of ABI calls.
 
 For batch (iteration) i, 1-based:
-    prep(i)   = mspipe_sample_batch(i) -> subgraph ids, then mspipe_memory_fetch(i)
-                (snapshot rows of the 3B(𝒩+1) subgraph nodes, P:L818, P:L1153;
-                optional MSPipe-S mitigation of the 2B update targets)
-    commit(i) = mspipe_memory_update(i) (dedup + message + GRU) then
-                mspipe_memory_writeback(i)  (i_upd <- i)
+    prep(i)   = A1 sampler + A2 dedup + A3 snapshot fetch of the 3B(𝒩+1) subgraph
+                rows [+ A4 MSPipe-S of the 2B targets, P:L317]
+                [+ F2 feature fetch on its own stream] + A5 message build;
+                fused: mspipe_memory_prep + mspipe_message_build
+    commit(i) = A6 GRU + A7 write-back of version i (i_upd <- i);
+                fused: mspipe_gru_apply_commit (one kernel)
 
-The staleness bound becomes an ORDER on one stream (no host waits): with the
+The staleness bound becomes an ORDER on the streams (no host waits): with the
 exact schedule prep(i) is enqueued right after commit(i-1-k), so it reads
 version v(i) = i-1-k (Eq. 2; the gate of Alg. 1 L8-L11 is the
-check inside mspipe_memory_fetch).  k+1 snapshot slots hold the prepared
-batches in flight — the paper's "K additional subgraphs" (P:L557,
-P:L1171-L1175).  The grouped schedule fetches k+1 batches after one commit.
+library's staleness check).  k+1 snapshot slots hold the prepared batches in
+flight — the paper's "K additional subgraphs".  The
+grouped schedule fetches k+1 batches after one commit; the "plan" schedule
+(row F1) follows per-iteration k_i.  With k >= 1 the state tables are double-
+buffered, so prep(t+k) and commit(t) run concurrently on two streams.
 
-A *step* (bench.py) is one batch: its ops are [prep(t+k), commit(t)].  Steps
-are captured once into CUDA graphs and replayed (µs-scale batches are
-launch-bound otherwise).
+A *step* (bench.py) is one commit and the preps enqueued with it.  Steps are
+captured once into CUDA graphs and replayed (µs-scale batches are launch-bound
+otherwise).
 """
 from __future__ import annotations
 
@@ -544,18 +547,17 @@ class MemoryStage(_TimedOps):
             torch.cuda.current_stream().wait_stream(self.d2h)
 
     def run_ops(self, ops, overlap=None):
-        """Enqueue ops in order.  With overlap (default when k >= 1), preps of
-        batches not committed in this op group go to a side stream: they only
-        read the T-CSR and (fetch) the state tables, and the tables change
-        only in writeback, so prep(t+k) runs concurrently with update(t); the
-        side stream is joined before the first writeback of the group, which
-        keeps fetch(t+k) between writeback(t-1) and writeback(t) — the exact
-        staleness order of Eq. 2 — while overlapping the two halves of the
-        iteration (the paper's pipelining, moved onto the GPU).
-        Double-buffered tables: fetch(t+k) reads version t-1 from the other
-        set than the one commit t writes, so the commit does not wait at all;
-        the join at the end of the group is what keeps that fetch ahead of
-        commit t+1 (which rewrites its set)."""
+        """Enqueue ops in order.  With overlap (default when k >= 1) every prep
+        goes to a side stream, in order (preps share the handle's scratch); a
+        commit of the same group waits for its own prep.  Preps only read the
+        T-CSR and the state tables, so prep(t+k) runs concurrently with
+        commit(t) — the paper's pipelining of fetch with update,
+        moved onto the GPU.  One table set: the commit waits for that fetch
+        (its write would change rows the fetch of version t-1 reads), which
+        keeps the exact staleness order of Eq. 2.  Double-buffered tables:
+        fetch(t+k) reads version t-1 from the other set than the one commit t
+        writes, so the commit does not wait at all; the join at the end of the
+        group keeps that fetch ahead of commit t+1 (which rewrites its set)."""
         overlap = (self.cfg.k >= 1) if overlap is None else overlap
         self._copies_begin(ops)
         if not overlap:
