@@ -402,7 +402,8 @@ def run_mspipe(args):
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         tot2 = float(tt.item())
     out["e2e"] = {"value": events / (tot2 / 1e3), "unit": UNIT,
-                  "h2d_bytes_per_step": st2.h2d_bytes_per_batch(), "d2h_bytes_per_step": st2.d2h_bytes_per_batch(),
+                  "h2d_bytes_per_step": st2.h2d_bytes_per_batch(), "d2h_bytes_per_step": (st2.d2h_bytes_per_batch(mean_U) if not sharded
+                                                                         else st2.d2h_bytes_per_batch()),
                   "ms_per_step": tot2 / K}
     del graphs2
     # ---- CPU oracle beside it (rank 0, N = 1 only) ---------------------------

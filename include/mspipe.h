@@ -548,6 +548,16 @@ MSPIPE_API mspipe_status mspipe_util_event_record(void* event, void* stream);
  * Errors: MSPIPE_EINVAL for NULL exec, MSPIPE_ECUDA with the runtime's message
  * (a capture that fails to end is discarded). */
 MSPIPE_API mspipe_status mspipe_util_graph_begin(void* stream);
+/* Utility (e2e read-back): copy the first *num (device) rows of two device
+ * arrays a [.., a_row_bytes] and b [.., b_row_bytes] into host_a / host_b —
+ * mapped pinned host memory (cudaHostAlloc; mapped under UVA) written by the
+ * kernel over PCIe — and *num into *host_num.  Whole 16-byte words are
+ * copied (up to 12 bytes past the last row; the host buffers must hold
+ * max_rows rows); row bytes multiples of 4, pointers 16-byte aligned (else
+ * MSPIPE_EINVAL); max_rows sizes the grid. */
+MSPIPE_API mspipe_status mspipe_util_rows_to_host(const int32_t* num, int32_t* host_num, const void* a,
+                                       void* host_a, int64_t a_row_bytes, const void* b, void* host_b,
+                                       int64_t b_row_bytes, int64_t max_rows, void* stream);
 MSPIPE_API mspipe_status mspipe_util_graph_end(void* stream, void** out_exec);
 MSPIPE_API mspipe_status mspipe_util_graph_launch(void* exec, void* stream);
 MSPIPE_API mspipe_status mspipe_util_graph_destroy(void* exec);

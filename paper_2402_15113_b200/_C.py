@@ -35,7 +35,8 @@ EXPORTS = ("mspipe_abi_version", "mspipe_last_error", "mspipe_check", "mspipe_sa
            "mspipe_memory_double_buffer", "mspipe_memory_tables", "mspipe_memory_set_committed",
            "mspipe_plan_timeline", "mspipe_plan_min_staleness", "mspipe_stale_histogram",
            "mspipe_memory_prep_build", "mspipe_feature_fetch", "mspipe_updater_create",
-           "mspipe_message_build_deferred", "mspipe_memory_mail_deferred", "mspipe_gru_build_apply_commit")
+           "mspipe_message_build_deferred", "mspipe_memory_mail_deferred", "mspipe_gru_build_apply_commit",
+           "mspipe_util_rows_to_host")
 XCHG_FETCH_IDS, XCHG_FETCH_ROWS, XCHG_COMMIT = 0, 1, 2
 
 
@@ -90,6 +91,7 @@ def lib():
         L.mspipe_plan_min_staleness.argtypes = [P, i64, i32, P, C.POINTER(i64)]
         L.mspipe_stale_histogram.argtypes = [C.POINTER(Tcsr), P, P, i64, i64, i32, P, P]
         L.mspipe_memory_tables.argtypes = [P, i64, C.POINTER(P), C.POINTER(P), C.POINTER(P), C.POINTER(P)]
+        L.mspipe_util_rows_to_host.argtypes = [P, P, P, P, i64, P, P, i64, i64, P]
         L.mspipe_util_graph_begin.argtypes = [P]
         L.mspipe_util_graph_end.argtypes = [P, C.POINTER(P)]
         L.mspipe_util_graph_launch.argtypes = [P, P]
@@ -194,6 +196,15 @@ def stale_histogram(g: "TcsrHandle", src, dst, batch, max_d=64, stream=None):
     _ck(lib().mspipe_stale_histogram(C.byref(g.c), ptr(src), ptr(dst), src.numel(), int(batch), int(max_d),
                                      ptr(out), stream_ptr(stream)), "mspipe_stale_histogram")
     return out
+
+
+def rows_to_host(num, host_num, a, host_a, b, host_b, max_rows, stream=None):
+    """Zero-copy read-back of the first *num rows of a and b into pinned host tensors."""
+    def hp(t):
+        return C.c_void_p(t.data_ptr())
+    _ck(lib().mspipe_util_rows_to_host(ptr(num), hp(host_num), ptr(a), hp(host_a), a[0].numel() * a.element_size(),
+                                       ptr(b), hp(host_b), b[0].numel() * b.element_size(), int(max_rows),
+                                       stream_ptr(stream)), "mspipe_util_rows_to_host")
 
 
 class StepGraph:

@@ -1029,6 +1029,17 @@ mspipe_status mspipe_stale_histogram(const mspipe_tcsr* g, const int32_t* src, c
   return after_launch("stale_histogram");
 }
 
+mspipe_status mspipe_util_rows_to_host(const int32_t* num, int32_t* host_num, const void* a, void* host_a,
+                                       int64_t a_row_bytes, const void* b, void* host_b, int64_t b_row_bytes,
+                                       int64_t max_rows, void* stream) {
+  if (!num || !host_num || max_rows < 0 || a_row_bytes < 0 || b_row_bytes < 0 || a_row_bytes % 4 ||
+      b_row_bytes % 4 || (a_row_bytes && (!a || !host_a)) || (b_row_bytes && (!b || !host_b)) ||
+      ((uintptr_t)a | (uintptr_t)host_a | (uintptr_t)b | (uintptr_t)host_b) % 16)
+    return fail(MSPIPE_EINVAL, "util_rows_to_host: row bytes must be multiples of 4, pointers 16-byte aligned");
+  launch_rows_to_host(num, host_num, a, host_a, a_row_bytes, b, host_b, b_row_bytes, max_rows, (cudaStream_t)stream);
+  return after_launch("util_rows_to_host");
+}
+
 mspipe_status mspipe_util_graph_begin(void* stream) {
   return cuda_status(cudaStreamBeginCapture((cudaStream_t)stream, cudaStreamCaptureModeThreadLocal),
                      "util_graph_begin");

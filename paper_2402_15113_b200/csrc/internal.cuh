@@ -152,6 +152,8 @@ void launch_writeback(const int32_t* nodes, const int32_t* num, int64_t max_n,
                       const float* new_mem, const double* new_ts, const float* new_mail,
                       int32_t mem_dim, int64_t mail_stride, float* mem, double* mem_ts,
                       float* mail, double* mail_ts, int64_t num_nodes, cudaStream_t s);
+void launch_rows_to_host(const int32_t* num, int32_t* host_num, const void* a, void* host_a, int64_t a_row_bytes,
+                         const void* b, void* host_b, int64_t b_row_bytes, int64_t max_rows, cudaStream_t s);
 void launch_catchup(const int32_t* prev_nodes, const int32_t* prev_num, int64_t prev_max, const float* src_mem,
                     const double* src_mem_ts, const float* src_mail, const double* src_mail_ts, float* dst_mem,
                     double* dst_mem_ts, float* dst_mail, double* dst_mail_ts, int32_t mem_dim, int64_t mail_stride,

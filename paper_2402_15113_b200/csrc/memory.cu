@@ -396,4 +396,30 @@ void launch_catchup(const int32_t* prev_nodes, const int32_t* prev_num, int64_t 
            save_num);
 }
 
+// Zero-copy read-back (e2e): the first *num rows of two device arrays straight
+// into mapped pinned host memory over PCIe, and *num itself.  Only the rows
+// that exist cross the bus (a fixed-size memcpy would move max rows).
+__global__ void __launch_bounds__(256) k_rows_to_host(const int32_t* __restrict__ num, int32_t* host_num,
+                                                      const uint4* __restrict__ a, uint4* host_a, int64_t a_row_bytes,
+                                                      const uint4* __restrict__ b, uint4* host_b,
+                                                      int64_t b_row_bytes) {
+  pdl_begin();
+  const int32_t n = __ldg(num);
+  // whole 16-byte words covering the first n rows (the host buffers hold max rows)
+  const int64_t na = ((int64_t)n * a_row_bytes + 15) / 16, nt = na + ((int64_t)n * b_row_bytes + 15) / 16;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nt; i += (int64_t)gridDim.x * blockDim.x) {
+    if (i < na) host_a[i] = __ldg(a + i);
+    else host_b[i - na] = __ldg(b + (i - na));
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) *host_num = n;
+}
+
+void launch_rows_to_host(const int32_t* num, int32_t* host_num, const void* a, void* host_a, int64_t a_row_bytes,
+                         const void* b, void* host_b, int64_t b_row_bytes, int64_t max_rows, cudaStream_t s) {
+  const int threads = 256;
+  const int64_t work = max_rows * (a_row_bytes + b_row_bytes) / 16;
+  launch_k(k_rows_to_host, dim3(grid_for(work > 0 ? work : 1, threads, 4)), dim3(threads), 0, s, 1, num, host_num,
+           (const uint4*)a, (uint4*)host_a, a_row_bytes, (const uint4*)b, (uint4*)host_b, b_row_bytes);
+}
+
 }  // namespace mspipe

@@ -495,15 +495,10 @@ class MemoryStage(_TimedOps):
         next prep) for the D2H the next step issues."""
         if not self.staged:
             return
-        main = torch.cuda.current_stream()
-        d2h = self._copy_streams()[1]
-        d2h.wait_stream(main)
-        with torch.cuda.stream(d2h):
-            o = self.out_ring[i % 2]
-            B = self.cfg.batch
-            n2 = upd["nodes"].numel()
-            o[16:16 + 4 * n2].view(torch.int32).copy_(upd["nodes"], non_blocking=True)
-            o[:4].view(torch.int32).copy_(upd["num"], non_blocking=True)
+        o = self.out_ring[i % 2]  # on the commit's stream, right behind it (two small copies)
+        n2 = upd["nodes"].numel()
+        o[16:16 + 4 * n2].view(torch.int32).copy_(upd["nodes"], non_blocking=True)
+        o[:4].view(torch.int32).copy_(upd["num"], non_blocking=True)
         self._pending_out = i
 
     def _copy_streams(self):
@@ -514,19 +509,32 @@ class MemoryStage(_TimedOps):
         return self.h2d, self.d2h
 
     def _copies_begin(self, ops):
-        """Step start (e2e): on the copy stream, read back the previous commit's
-        result and prefetch the inputs of the next step's preps."""
+        """Step start (e2e): remember the step's start; the copies themselves are
+        captured after the step's kernels (_copies_issue) so that in the graph
+        the kernel nodes come first, but depend only on this start."""
         if not self.staged:
             return
-        main = torch.cuda.current_stream()
+        self._step_start = torch.cuda.Event()
+        self._step_start.record()
+        self._read_back = self._pending_out  # the previous commit (this step's commit re-sets _pending_out)
+        self._pending_out = None
+
+    def _copies_issue(self, ops):
+        """On the copy streams, from the step start: read back the previous
+        commit's result (only its U rows cross PCIe: a zero-copy kernel into the
+        pinned record) and prefetch the inputs of the next step's preps."""
         h2d, d2h = self._copy_streams()
-        d2h.wait_stream(main)
+        d2h.wait_event(self._step_start)
         with torch.cuda.stream(d2h):
-            c = self._pending_out
-            if c is not None:  # ONE memcpy: the previous commit's packed result record
-                self.out_host.copy_(self.out_ring[c % 2], non_blocking=True)
-                self._pending_out = None
-        h2d.wait_stream(main)
+            c = self._read_back
+            if c is not None:
+                o, B, M = self.out_ring[c % 2], self.cfg.batch, self.cfg.mem_dim
+                _C.rows_to_host(o[:4].view(torch.int32), self.out_host[:4].view(torch.int32),
+                                o[16:16 + 8 * B].view(torch.int32).view(2 * B, 1),
+                                self.out_host[16:16 + 8 * B].view(torch.int32).view(2 * B, 1),
+                                o[self._out_mem_off:].view(torch.float32).view(2 * B, M),
+                                self.out_host[self._out_mem_off:].view(torch.float32).view(2 * B, M), 2 * B)
+        h2d.wait_event(self._step_start)
         with torch.cuda.stream(h2d):
             commits = [i for op, i in ops if op == "commit"]
             preps = [i for op, i in ops if op == "prep"]
@@ -541,7 +549,9 @@ class MemoryStage(_TimedOps):
                     self._loaded.add(j)
                 j += 1
 
-    def _copies_end(self):
+    def _copies_end(self, ops):
+        if self.staged:
+            self._copies_issue(ops)
         if self.staged and self.h2d is not None:
             torch.cuda.current_stream().wait_stream(self.h2d)
             torch.cuda.current_stream().wait_stream(self.d2h)
@@ -564,7 +574,7 @@ class MemoryStage(_TimedOps):
             for op, i in ops:
                 (self.prep if op == "prep" else self.commit)(i)
             self._join_features()
-            self._copies_end()
+            self._copies_end(ops)
             return
         main = torch.cuda.current_stream()
         if getattr(self, "side", None) is None or self.side.device != main.device:
@@ -600,7 +610,7 @@ class MemoryStage(_TimedOps):
         if forked and not joined:
             main.wait_stream(self.side)
         self._join_features()
-        self._copies_end()
+        self._copies_end(ops)
 
     def run(self, nb=None):
         """All batches (or the first nb) in schedule order, one step at a time."""
@@ -623,6 +633,8 @@ class MemoryStage(_TimedOps):
         B = self.cfg.batch
         return B * (4 + 4 + 4 + 8 + 4 * self.cfg.edge_dim)
 
-    def d2h_bytes_per_batch(self):
-        B = self.cfg.batch
-        return (16 + (8 * B + 15) // 16 * 16) + 2 * B * self.cfg.mem_dim * 4
+    def d2h_bytes_per_batch(self, mean_unique=None):
+        """Bytes read back per step: the count and the U committed rows (ids + h');
+        mean_unique = the mean U of the timed batches (None: the 2B upper bound)."""
+        U = 2 * self.cfg.batch if mean_unique is None else mean_unique
+        return 4 + U * (4 + 4 * self.cfg.mem_dim)
