@@ -125,6 +125,61 @@ __device__ __forceinline__ int64_t warp_recent_end(const Tcsr& g, int32_t v, dou
   return lo + __popc(__ballot_sync(0xffffffffu, below));
 }
 
+// warp_recent_end plus the sample itself: lane s < F receives entry end-1-s
+// (nbr, eid, ts) or nbr = eid = -1 past the row start.  The last window's ts,
+// nbr and eid are loaded in ONE round and handed out by shuffles, so a row of
+// at most 32 entries (most rows) costs one dependent round less than
+// warp_recent_end followed by the loads; entries below the last window (a long
+// row whose F most recent straddle it) are loaded directly.
+__device__ __forceinline__ int64_t warp_recent_sample(const Tcsr& g, int32_t v, double tq, int lane, int F,
+                                                      int64_t* beg_out, int32_t* nbr_out, int32_t* eid_out,
+                                                      double* ts_out) {
+  *nbr_out = -1;
+  *eid_out = -1;
+  *ts_out = 0.0;
+  if (v < 0 || v >= g.num_nodes) {
+    if (lane == 0) raise_dev(MSPIPE_DEVERR_RANGE);
+    *beg_out = 0;
+    return 0;
+  }
+  const int64_t beg = __ldg(g.indptr + v);
+  int64_t lo = beg, hi = __ldg(g.indptr + v + 1);
+  while (hi - lo > 32) {
+    const int64_t span = hi - lo;
+    const int64_t p = lo + ((int64_t)(lane + 1) * span) / 33;
+    const bool below = __ldg(g.ts + p) < tq;
+    const int c = __popc(__ballot_sync(0xffffffffu, below));
+    const int64_t plast = __shfl_sync(0xffffffffu, p, c > 0 ? c - 1 : 0);
+    const int64_t pfirst = __shfl_sync(0xffffffffu, p, c < 32 ? c : 31);
+    if (c > 0) lo = plast + 1;
+    if (c < 32) hi = pfirst;
+  }
+  const int64_t q = lo + lane;
+  const bool in = q < hi;
+  const double tq_q = in ? __ldg(g.ts + q) : 0.0;
+  const int32_t nb_q = in ? __ldg(g.nbr + q) : -1;
+  const int32_t ei_q = in ? __ldg(g.eid + q) : -1;
+  const int64_t end = lo + __popc(__ballot_sync(0xffffffffu, in && tq_q < tq));
+  const int64_t e = end - 1 - lane;  // this lane's output slot s = lane
+  const int src_lane = (int)(e - lo);
+  const int32_t nb_s = __shfl_sync(0xffffffffu, nb_q, src_lane & 31);
+  const int32_t ei_s = __shfl_sync(0xffffffffu, ei_q, src_lane & 31);
+  const double ts_s = __shfl_sync(0xffffffffu, tq_q, src_lane & 31);
+  if (lane < F && e >= beg) {
+    if (e >= lo) {
+      *nbr_out = nb_s;
+      *eid_out = ei_s;
+      *ts_out = ts_s;
+    } else {
+      *nbr_out = __ldg(g.nbr + e);
+      *eid_out = __ldg(g.eid + e);
+      *ts_out = __ldg(g.ts + e);
+    }
+  }
+  *beg_out = beg;
+  return end;
+}
+
 inline Tcsr to_tcsr(const mspipe_tcsr* g) {
   return Tcsr{g->num_nodes, g->nnz, g->indptr, g->nbr, g->eid, g->ts};
 }

@@ -68,22 +68,26 @@ __device__ __forceinline__ void st_release(int32_t* p, int32_t v) {
 __device__ __forceinline__ void warp_gather_rows(const float4* __restrict__ tab, int32_t Q, int32_t my_id,
                                                  int nrows, float4* __restrict__ dst, int64_t dst_row0,
                                                  int lane) {
+  // kU float4 loads in flight per lane before their stores: the whole subgraph
+  // (11 rows x 25 float4 for M = 100) in one dependent round instead of three
+  constexpr int kU = 12;
   const int total = nrows * Q;
   const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
-  for (int base = 0; base < total; base += 32 * 4) {
-    float4 v[4];
-    int idx[4];
+  for (int base = 0; base < total; base += 32 * kU) {
+    float4 v[kU];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      idx[u] = base + u * 32 + lane;
-      const int s = idx[u] < total ? idx[u] / Q : 0;
+    for (int u = 0; u < kU; ++u) {
+      const int idx = base + u * 32 + lane;
+      const int s = idx < total ? idx / Q : 0;
       const int32_t id = __shfl_sync(0xffffffffu, my_id, s);
-      const int c = idx[u] - s * Q;
-      v[u] = (idx[u] < total && id >= 0) ? __ldg(tab + (int64_t)id * Q + c) : z;
+      const int c = idx - s * Q;
+      v[u] = (idx < total && id >= 0) ? __ldg(tab + (int64_t)id * Q + c) : z;
     }
 #pragma unroll
-    for (int u = 0; u < 4; ++u)
-      if (idx[u] < total) dst[dst_row0 * Q + idx[u]] = v[u];
+    for (int u = 0; u < kU; ++u) {
+      const int idx = base + u * 32 + lane;
+      if (idx < total) dst[dst_row0 * Q + idx] = v[u];
+    }
   }
 }
 
@@ -151,6 +155,7 @@ __global__ void __launch_bounds__(kPrepThreads) k_prep(PrepArgs a) {
   if (blockIdx.x == 0) {
     block_dedup<kPrepThreads, kSmem>(a.src, a.dst, a.B, a.gscratch, sscratch, a.g.num_nodes, a.out_nodes,
                                      a.out_winner, a.out_num);
+    if (threadIdx.x == 0) PPHASE(2);
     if (a.stamp || a.bld.xbuf) {
       __syncthreads();  // out_nodes / out_winner / out_num written by this block
       const int32_t U = *a.out_num;
@@ -180,27 +185,22 @@ __global__ void __launch_bounds__(kPrepThreads) k_prep(PrepArgs a) {
     const int32_t v = role == 0 ? __ldg(a.src + ev) : (role == 1 ? __ldg(a.dst + ev) : __ldg(a.neg + ev));
     const double tq = __ldg(a.ts + ev);
     int64_t beg;
-    const int64_t end = warp_recent_end(a.g, v, tq, lane, &beg);
+    int32_t nbs, eis;
+    double tss;
+    const int64_t end = warp_recent_sample(a.g, v, tq, lane, F, &beg, &nbs, &eis, &tss);
     const int32_t cnt = (int32_t)min64(end - beg, (int64_t)F);
     // A1 outputs; lane s < F = slot s (newest first); lane s in [1, F] also holds subgraph id s
-    int32_t id = lane == 0 ? v : -1;
     if (lane < F) {
       const int64_t o = r * F + lane;
-      if (lane < cnt) {
-        const int64_t q = end - 1 - lane;
-        const double tsq = __ldg(a.g.ts + q);
-        a.out_nbr[o] = __ldg(a.g.nbr + q);
-        a.out_eid[o] = __ldg(a.g.eid + q);
-        a.out_ts[o] = tsq;
-        a.out_dt[o] = (float)(tq - tsq);
-      } else {
-        a.out_nbr[o] = -1;
-        a.out_eid[o] = -1;
-        a.out_ts[o] = 0.0;
-        a.out_dt[o] = 0.0f;
-      }
+      const bool ok = lane < cnt;
+      a.out_nbr[o] = ok ? nbs : -1;
+      a.out_eid[o] = ok ? eis : -1;
+      a.out_ts[o] = ok ? tss : 0.0;
+      a.out_dt[o] = ok ? (float)(tq - tss) : 0.0f;
     }
-    if (lane >= 1 && lane <= F && lane - 1 < cnt) id = __ldg(a.g.nbr + (end - lane));
+    const int32_t nb_prev = __shfl_up_sync(0xffffffffu, nbs, 1);  // slot lane-1 -> subgraph id lane
+    int32_t id = lane == 0 ? v : -1;
+    if (lane >= 1 && lane <= F && lane - 1 < cnt) id = nb_prev;
     if (lane == 0) a.out_cnt[r] = cnt;
     if (lane <= F) a.out_sub[r * F1 + lane] = id;
     // A3: the subgraph's snapshot rows (pads and out-of-range ids give zero rows)
