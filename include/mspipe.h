@@ -292,6 +292,18 @@ MSPIPE_API mspipe_status mspipe_memory_dedup(mspipe_memory* st, const int32_t* s
                                   int64_t num_events, int32_t* out_nodes, int32_t* out_winner,
                                   int32_t* out_num_unique, void* stream);
 
+/* A2 for iteration `iteration` of the stage: exactly mspipe_memory_dedup, and
+ * with double-buffered state it also stamps the winners' nodes for that
+ * iteration (what mspipe_memory_prep's dedup block does), so a later
+ * mspipe_memory_prep called WITHOUT dedup outputs can carry the catch-up of
+ * this batch's commit.  Lets the dedup (state-independent, G6) run on its own
+ * stream ahead of the message build (mspipe_message_build_tables) while the
+ * sampler and gather run.  Same limits and outputs as mspipe_memory_dedup;
+ * iteration >= 1. */
+MSPIPE_API mspipe_status mspipe_memory_winners(mspipe_memory* st, int64_t iteration, const int32_t* src,
+                                    const int32_t* dst, int64_t num_events, int32_t* out_nodes,
+                                    int32_t* out_winner, int32_t* out_num_unique, void* stream);
+
 /* A5 + A6 — message build and GRU update of the U winners of one batch of
  * num_events events (winner / num_unique from mspipe_memory_dedup; global
  * eids are the caller's business; edge_feat holds this batch's rows
@@ -335,7 +347,9 @@ MSPIPE_API mspipe_status mspipe_memory_writeback(mspipe_memory* st, int64_t comm
  * mitigation when `mit` is given): exactly mspipe_sample_batch, then
  * mspipe_memory_dedup, then mspipe_memory_fetch(ids = out_sub_ids,
  * n = 3B(𝒩+1)) with the same arguments and outputs as those calls.  The same
- * staleness gate applies.  fanout <= 31; num_events <= 8192. */
+ * staleness gate applies.  fanout <= 31; num_events <= 8192.
+ * out_nodes, out_winner and out_num_unique all NULL: no dedup (A1 + A3 only;
+ * the winners come from mspipe_memory_winners of the same iteration). */
 MSPIPE_API mspipe_status mspipe_memory_prep(mspipe_memory* st, const mspipe_tcsr* g, int64_t iteration,
                                  const int32_t* src, const int32_t* dst, const int32_t* neg,
                                  const double* ts, int64_t num_events, int32_t fanout,
@@ -361,6 +375,20 @@ MSPIPE_API mspipe_status mspipe_message_build(const mspipe_gru* gru, const doubl
                                    const float* snap_h, const int32_t* winner,
                                    const int32_t* num_unique, double* out_ts, float* out_mail,
                                    int64_t mail_stride, void* workspace, size_t ws_bytes, void* stream);
+/* A5 from the state tables instead of a snapshot buffer: exactly
+ * mspipe_message_build with S = the tables of version v(iteration) (the
+ * version mspipe_memory_prep of the same iteration reads, Eq. 2, P:L196-L204;
+ * same gate, MSPIPE_ESTALE otherwise; *out_version = v), snap_h = NULL, and
+ * S.mem[w] = mem[node_w] read by node id (src / dst: the batch's endpoints).
+ * The caller orders it like the fetch: after commit v, before commit v + 1
+ * rewrites the rows it reads (with double-buffered state: before commit v + 2).
+ * Needs a tensor-core, immediate-mailbox handle with world == 1. */
+MSPIPE_API mspipe_status mspipe_message_build_tables(const mspipe_gru* gru, const mspipe_memory* st,
+                                          int64_t iteration, const int32_t* src, const int32_t* dst,
+                                          const double* ts, int64_t num_events, const float* edge_feat,
+                                          const int32_t* winner, const int32_t* num_unique, double* out_ts,
+                                          float* out_mail, void* workspace, size_t ws_bytes,
+                                          int64_t* out_version, void* stream);
 MSPIPE_API mspipe_status mspipe_gru_apply(const mspipe_gru* gru, int64_t num_events, const float* snap_mem,
                                int64_t snap_step, const float* snap_h, const int32_t* winner,
                                const int32_t* num_unique, float* out_mem, const void* workspace,
@@ -395,7 +423,9 @@ MSPIPE_API mspipe_status mspipe_memory_prep_build(mspipe_memory* st, const mspip
  * (nodes, num_unique, h', new_ts, new_mail) as version commit_version, the
  * write-back done by the GEMM epilogue (world == 1).  new_ts / new_mail are
  * message_build's out_ts / out_mail; out_mem (nullable) still receives h' in
- * winner order.  Same ordering contract as mspipe_memory_writeback (the
+ * winner order.  snap_mem may be NULL (immediate mailbox, snap_h NULL): the
+ * GRU's hidden input h = S.mem[w] is then read from new_mail[u][0:mem_dim]
+ * (the mail row starts with S.mem[w], G14).  Same ordering contract as mspipe_memory_writeback (the
  * caller orders it after the fetch of iteration commit_version + k). */
 MSPIPE_API mspipe_status mspipe_gru_apply_commit(const mspipe_gru* gru, mspipe_memory* st,
                                       int64_t commit_version, int64_t num_events,

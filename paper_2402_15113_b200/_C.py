@@ -36,7 +36,7 @@ EXPORTS = ("mspipe_abi_version", "mspipe_last_error", "mspipe_check", "mspipe_sa
            "mspipe_plan_timeline", "mspipe_plan_min_staleness", "mspipe_stale_histogram",
            "mspipe_memory_prep_build", "mspipe_feature_fetch", "mspipe_updater_create",
            "mspipe_message_build_deferred", "mspipe_memory_mail_deferred", "mspipe_gru_build_apply_commit",
-           "mspipe_util_rows_to_host")
+           "mspipe_util_rows_to_host", "mspipe_memory_winners", "mspipe_message_build_tables")
 XCHG_FETCH_IDS, XCHG_FETCH_ROWS, XCHG_COMMIT = 0, 1, 2
 
 
@@ -82,6 +82,9 @@ def lib():
         L.mspipe_gru_create.argtypes = [C.POINTER(P), i32, i32, i32, i32, i64, P, P, P, P, P, P, P]
         L.mspipe_gru_destroy.argtypes = [P]
         L.mspipe_memory_dedup.argtypes = [P, P, P, i64, P, P, P, P]
+        L.mspipe_memory_winners.argtypes = [P, i64, P, P, i64, P, P, P, P]
+        L.mspipe_message_build_tables.argtypes = [P, P, i64, P, P, P, i64, P, P, P, P, P, P, C.c_size_t,
+                                                  C.POINTER(i64), P]
         L.mspipe_memory_update.argtypes = [P, P, P, P, P, i64, P, P, P, i64, P, P, P, P, P, P, P]
         L.mspipe_memory_writeback.argtypes = [P, i64, P, P, i64, P, P, P, P]
         L.mspipe_util_event_record.argtypes = [P, P]
@@ -455,6 +458,24 @@ def memory_dedup(st: MemoryHandle, src, dst, out, stream=None):
     return out
 
 
+def memory_winners(st: MemoryHandle, iteration, src, dst, out, stream=None):
+    """A2 of iteration `iteration` (dedup + double-buffer stamps): fills out["nodes"], out["winner"], out["num"]."""
+    _ck(lib().mspipe_memory_winners(st.h, int(iteration), ptr(src), ptr(dst), src.numel(), ptr(out["nodes"]),
+                                    ptr(out["winner"]), ptr(out["num"]), stream_ptr(stream)), "mspipe_memory_winners")
+    return out
+
+
+def message_build_tables(gru: GruHandle, st: MemoryHandle, iteration, src, dst, ts, edge_feat, winner, num, out_ts,
+                         out_mail, workspace, stream=None) -> int:
+    """A5 from the state tables of the version iteration's fetch reads; returns that version."""
+    v = i64(-1)
+    _ck(lib().mspipe_message_build_tables(gru.h, st.h, int(iteration), ptr(src), ptr(dst), ptr(ts), ts.numel(),
+                                          ptr(edge_feat), ptr(winner), ptr(num), ptr(out_ts), ptr(out_mail),
+                                          ptr(workspace), workspace.numel() * workspace.element_size(), C.byref(v),
+                                          stream_ptr(stream)), "mspipe_message_build_tables")
+    return int(v.value)
+
+
 def memory_update(st: MemoryHandle, gru: GruHandle, src, dst, ts, edge_feat, snap_mem, snap_mem_ts, snap_step,
                   out, snap_h=None, stream=None):
     """A5+A6: reads out["winner"], out["num"] (from memory_dedup); fills out["mem"], out["ts"], out["mail"]."""
@@ -469,10 +490,11 @@ def memory_prep(st: MemoryHandle, g: TcsrHandle, iteration, src, dst, neg, ts, f
                 out_mail=None, out_mail_ts=None, mitigation: Mitigation | None = None, stream=None) -> int:
     """A1+A2+A3(+A4) fused: fills samp (alloc_sample), dd (alloc_dedup) and the fetched rows."""
     v = i64(-1)
+    dd = dd if dd is not None else {}  # None: no dedup (mspipe_memory_winners does it)
     _ck(lib().mspipe_memory_prep(st.h, C.byref(g.c), int(iteration), ptr(src), ptr(dst), ptr(neg), ptr(ts),
                                  src.numel(), fanout, ptr(samp["nbr"]), ptr(samp["eid"]), ptr(samp["ts"]),
-                                 ptr(samp["dt"]), ptr(samp["cnt"]), ptr(samp["sub"]), ptr(dd["nodes"]),
-                                 ptr(dd["winner"]), ptr(dd["num"]), ptr(out_mem), ptr(out_mem_ts), ptr(out_mail),
+                                 ptr(samp["dt"]), ptr(samp["cnt"]), ptr(samp["sub"]), ptr(dd.get("nodes")),
+                                 ptr(dd.get("winner")), ptr(dd.get("num")), ptr(out_mem), ptr(out_mem_ts), ptr(out_mail),
                                  ptr(out_mail_ts), C.byref(mitigation) if mitigation is not None else None,
                                  C.byref(v), stream_ptr(stream)), "mspipe_memory_prep")
     return int(v.value)

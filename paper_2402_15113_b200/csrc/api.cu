@@ -484,6 +484,29 @@ mspipe_status mspipe_memory_dedup(mspipe_memory* st, const int32_t* src, const i
   return after_launch("memory_dedup");
 }
 
+mspipe_status mspipe_memory_winners(mspipe_memory* st, int64_t iteration, const int32_t* src, const int32_t* dst,
+                                    int64_t num_events, int32_t* out_nodes, int32_t* out_winner,
+                                    int32_t* out_num_unique, void* stream) {
+  if (!st) return fail(MSPIPE_EINVAL, "memory_winners: NULL handle");
+  if (iteration < 1) return fail(MSPIPE_EINVAL, "memory_winners: iteration=%lld", (long long)iteration);
+  if (num_events < 0 || num_events > 16384)
+    return fail(MSPIPE_EINVAL, "memory_winners: num_events=%lld (0..16384)", (long long)num_events);
+  if (!out_num_unique) return fail(MSPIPE_EINVAL, "memory_winners: null out_num_unique");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t ring = iteration % (st->k + 1);
+  if (num_events == 0) {
+    mspipe_status rc = cuda_status(cudaMemsetAsync(out_num_unique, 0, sizeof(int32_t), s), "memory_winners");
+    if (rc == MSPIPE_OK && st->db) st->stamp_iter[ring] = iteration;  // no winners: nothing to stamp
+    return rc;
+  }
+  if (!src || !dst || !out_nodes || !out_winner) return fail(MSPIPE_EINVAL, "memory_winners: null input/output");
+  launch_dedup(src, dst, num_events, st->scratch, st->num_nodes, out_nodes, out_winner, out_num_unique, s,
+               st->db ? st->stamps + ring * st->num_nodes : nullptr, (int32_t)iteration);
+  mspipe_status rc = after_launch("memory_winners");
+  if (rc == MSPIPE_OK && st->db) st->stamp_iter[ring] = iteration;
+  return rc;
+}
+
 mspipe_status mspipe_memory_update(mspipe_memory* st, const mspipe_gru* gru, const int32_t* src,
                                    const int32_t* dst, const double* ts, int64_t num_events,
                                    const float* edge_feat, const float* snap_mem,
@@ -623,16 +646,24 @@ static mspipe_status prep_impl(mspipe_memory* st, const mspipe_tcsr* g, int64_t 
   if ((out_mail == nullptr) != (out_mail_ts == nullptr)) return fail(MSPIPE_EINVAL, "memory_prep: out_mail and out_mail_ts go together");
   cudaStream_t s = (cudaStream_t)stream;
   const TableSet t = table_set(st, st->committed);
+  // no dedup outputs: the A2 part is left to mspipe_memory_winners
+  const bool dedup = out_nodes || out_winner || out_num_unique;
+  if (dedup && ba == nullptr && !(out_nodes && out_winner && out_num_unique))
+    return fail(MSPIPE_EINVAL, "memory_prep: out_nodes / out_winner / out_num_unique go together");
+  if (!dedup && ba) return fail(MSPIPE_EINVAL, "memory_prep_build: needs the dedup outputs");
   if (num_events > 0) {
     if (!src || !dst || !neg || !ts || !out_nbr || !out_eid || !out_ts || !out_dt || !out_cnt || !out_sub_ids ||
-        !out_nodes || !out_winner || !out_num_unique || !out_mem || !out_mem_ts)
+        (dedup && (!out_nodes || !out_winner || !out_num_unique)) || !out_mem || !out_mem_ts)
       return fail(MSPIPE_EINVAL, "memory_prep: null input/output");
     // double-buffered: this launch may also carry the catch-up of the next
     // commit c (its winners already stamped, or stamped by this very launch
-    // when c == iteration, k = 0: the commit then follows in stream order)
+    // when c == iteration, k = 0: the commit then follows in stream order).
+    // Without the dedup block the stamps of c == iteration may still be in
+    // flight on another stream: the commit's GEMM then catches up instead.
     const int64_t c = st->committed + 1;
     const bool cu = st->db && catchup_mode() == 2 && st->caught_up != c &&
-                    (st->stamp_iter[c % (st->k + 1)] == c || c == iteration);
+                    (dedup ? (st->stamp_iter[c % (st->k + 1)] == c || c == iteration)
+                           : (c != iteration && st->stamp_iter[c % (st->k + 1)] == c));
     const CatchUp cua = cu ? catchup_args(st, c) : CatchUp{};
     PrepBuild pb{};
     if (ba) {
@@ -649,10 +680,10 @@ static mspipe_status prep_impl(mspipe_memory* st, const mspipe_tcsr* g, int64_t 
                                 out_cnt, out_sub_ids, st->scratch, out_nodes, out_winner, out_num_unique, t.mem,
                                 t.mem_ts, st->mem_dim, t.mail, t.mail_ts, st->mail_stride, out_mem,
                                 out_mem_ts, out_mail, out_mail_ts, s,
-                                st->db ? st->stamps + (iteration % (st->k + 1)) * st->num_nodes : nullptr,
+                                (st->db && dedup) ? st->stamps + (iteration % (st->k + 1)) * st->num_nodes : nullptr,
                                 (int32_t)iteration, cu ? &cua : nullptr, ba ? &pb : nullptr);
     if (e != cudaSuccess) return cuda_status(e, "memory_prep: launch");
-    if (st->db) st->stamp_iter[iteration % (st->k + 1)] = iteration;
+    if (st->db && dedup) st->stamp_iter[iteration % (st->k + 1)] = iteration;
     if (cu) st->caught_up = c;
   } else if (out_num_unique) {
     cudaError_t e = cudaMemsetAsync(out_num_unique, 0, sizeof(int32_t), s);
@@ -701,6 +732,37 @@ mspipe_status mspipe_message_build(const mspipe_gru* gru, const double* ts, int6
   return after_launch("message_build");
 }
 
+mspipe_status mspipe_message_build_tables(const mspipe_gru* gru, const mspipe_memory* st, int64_t iteration,
+                                          const int32_t* src, const int32_t* dst, const double* ts,
+                                          int64_t num_events, const float* edge_feat, const int32_t* winner,
+                                          const int32_t* num_unique, double* out_ts, float* out_mail,
+                                          void* workspace, size_t ws_bytes, int64_t* out_version, void* stream) {
+  if (!gru || !st) return fail(MSPIPE_EINVAL, "message_build_tables: NULL handle");
+  if (gru->precision == MSPIPE_FP32_SIMT || gru->d.mailbox != MSPIPE_MAILBOX_IMMEDIATE)
+    return fail(MSPIPE_EUNSUPPORTED, "message_build_tables: needs a tensor-core, immediate-mailbox handle");
+  if (st->world != 1) return fail(MSPIPE_EUNSUPPORTED, "message_build_tables: world > 1");
+  if (gru->d.M != st->mem_dim || gru->d.He != st->edge_dim) return fail(MSPIPE_EINVAL, "message_build_tables: dims");
+  if (iteration < 1 || num_events < 0 || num_events > gru->max_events)
+    return fail(MSPIPE_EINVAL, "message_build_tables: iteration=%lld num_events=%lld (<= max_events %lld)",
+                (long long)iteration, (long long)num_events, (long long)gru->max_events);
+  if (st->committed < iteration - 1 - st->k || st->committed > iteration - 1)  // the fetch's gate (Alg. 1 L8-L11)
+    return fail(MSPIPE_ESTALE, "message_build_tables: iteration %lld with committed=%lld violates k=%d",
+                (long long)iteration, (long long)st->committed, st->k);
+  if (out_version) *out_version = st->committed;
+  if (num_events == 0) return MSPIPE_OK;
+  if (ws_bytes < mspipe_gru_workspace_size(gru, num_events) || !workspace)
+    return fail(MSPIPE_EINVAL, "message_build_tables: workspace of %zu bytes < %zu", ws_bytes,
+                mspipe_gru_workspace_size(gru, num_events));
+  if (!src || !dst || !ts || (gru->d.He > 0 && !edge_feat) || !winner || !num_unique || !out_ts || !out_mail)
+    return fail(MSPIPE_EINVAL, "message_build_tables: null input/output");
+  const TableSet t = table_set(st, st->committed);
+  cudaError_t e = launch_gru_tc(gru->d, gru->wtc, (float*)workspace, ts, num_events, edge_feat, t.mem, t.mem_ts, 1,
+                                nullptr, winner, num_unique, nullptr, out_ts, out_mail, st->mail_stride,
+                                (cudaStream_t)stream, kGruBuild, nullptr, src, dst);
+  if (e != cudaSuccess) return cuda_status(e, "message_build_tables: launch");
+  return after_launch("message_build_tables");
+}
+
 mspipe_status mspipe_gru_apply(const mspipe_gru* gru, int64_t num_events, const float* snap_mem,
                                int64_t snap_step, const float* snap_h, const int32_t* winner,
                                const int32_t* num_unique, float* out_mem, const void* workspace,
@@ -742,9 +804,10 @@ mspipe_status mspipe_gru_apply_commit(const mspipe_gru* gru, mspipe_memory* st,
   if (num_events > 0) {
     if (ws_bytes < mspipe_gru_workspace_size(gru, num_events) || !workspace)
       return fail(MSPIPE_EINVAL, "gru_apply_commit: workspace of %zu bytes too small", ws_bytes);
-    if (!snap_mem || !nodes || !winner || !num_unique || !new_ts ||
-        (!new_mail && gru->d.mailbox != MSPIPE_MAILBOX_DEFERRED))
+    if (!nodes || !winner || !num_unique || !new_ts || (!new_mail && gru->d.mailbox != MSPIPE_MAILBOX_DEFERRED))
       return fail(MSPIPE_EINVAL, "gru_apply_commit: null input (new_mail may be NULL only for a deferred mailbox)");
+    if (!snap_mem && (snap_h || gru->d.mailbox == MSPIPE_MAILBOX_DEFERRED))
+      return fail(MSPIPE_EINVAL, "gru_apply_commit: snap_mem may be NULL only with snap_h NULL and an immediate mailbox");
   }
   const int64_t max_n = 2 * num_events;
   // double-buffered: the GEMM kernel catches up the previous commit's rows

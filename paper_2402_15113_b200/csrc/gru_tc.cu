@@ -29,6 +29,8 @@
 #include "internal.cuh"
 #include "tc_layout.cuh"
 
+#include <algorithm>
+
 namespace mspipe {
 
 namespace tc {
@@ -44,6 +46,8 @@ constexpr int kHBufBytes = kM * kJ * 4;   // h rows of the tile's hidden units (
 constexpr int kRecvBytes = kM * kN * 4;   // K-split partials received from the cluster (S x 128/S rows)
 constexpr int kSmemBytes =
     kStages * kStageBytes + 1024 /*align*/ + 1024 /*barriers*/ + kHBufBytes + kRecvBytes + kN * 4 /*biases*/;
+// the persistent k_gru_tc: two receive buffers (tile parity)
+constexpr int kSmemBytesP = kSmemBytes + kRecvBytes;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -199,6 +203,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #endif
 
 int gru_tc_jtiles(const GruDesc& d) { return (d.M + tc::kJ - 1) / tc::kJ; }
+__device__ __forceinline__ int gru_tc_jtiles_dev(const GruDesc& d) { return (d.M + tc::kJ - 1) / tc::kJ; }
 
 // ---------------------------------------------------------------------------
 // weight packing: per (hidden tile jt, K chunk c) a 16 KB block
@@ -347,7 +352,22 @@ struct TcArgs {
   int32_t* save_nodes;
   int32_t* save_num;
   CatchUp cu;
+  // build from the state tables (mspipe_message_build_tables): tsrc/tdst are
+  // the batch's endpoints, snap_mem / snap_ts the tables of the version read,
+  // indexed by node id instead of by snapshot row
+  const int32_t* tsrc;
+  const int32_t* tdst;
+  // GEMM: h (the GRU hidden input) is new_mail[u][0:M] (= S.mem[w], G14)
+  int32_t h_from_mail;
 };
+
+// row index of the state S.mem[w] of pair (ev, role) in snap_mem (times M) /
+// snap_ts: the snapshot row (root layout, stride `step`) or, building from the
+// tables, the node id itself
+__device__ __forceinline__ int64_t snap_row(const TcArgs& a, int32_t ev, int role) {
+  if (a.tsrc) return role ? __ldg(a.tdst + ev) : __ldg(a.tsrc + ev);
+  return (role ? a.B + ev : (int64_t)ev) * a.step;
+}
 
 // Double-buffered commit: copy the previous commit's rows (old set -> this
 // commit's set) except this commit's own winners, which the epilogue writes.
@@ -366,19 +386,18 @@ __device__ __forceinline__ float msg_val(const TcArgs& a, int32_t p, int32_t k) 
   const GruDesc& d = a.d;
   const int32_t M = d.M;
   const int32_t ev = p >> 1, role = p & 1;
-  const int64_t rw = role ? a.B + ev : ev;
-  const int64_t ro = role ? ev : a.B + ev;
-  if (k < M) return __ldg(a.snap_mem + rw * a.step * M + k);
-  if (k < 2 * M) return __ldg(a.snap_mem + ro * a.step * M + (k - M));
+  if (k < M) return __ldg(a.snap_mem + snap_row(a, ev, role) * M + k);
+  if (k < 2 * M) return __ldg(a.snap_mem + snap_row(a, ev, role ^ 1) * M + (k - M));
   if (k < d.Dm) return __ldg(a.ef + (int64_t)ev * d.He + (k - 2 * M));
   if (k < d.Dx) {
-    const float dt = (float)(__ldg(a.ts + ev) - __ldg(a.snap_ts + rw * a.step));  // Δt (G4)
+    const float dt = (float)(__ldg(a.ts + ev) - __ldg(a.snap_ts + snap_row(a, ev, role)));  // Δt (G4)
     const int q = k - d.Dm;
     return time_cos(fmaf(__ldg(d.time_w + q), dt, __ldg(d.time_b + q)));
   }
   if (k < d.K) {
     const int q = k - d.Dx;
-    return a.snap_h ? __ldg(a.snap_h + rw * M + q) : __ldg(a.snap_mem + rw * a.step * M + q);
+    return a.snap_h ? __ldg(a.snap_h + (role ? a.B + ev : (int64_t)ev) * M + q)
+                    : __ldg(a.snap_mem + snap_row(a, ev, role) * M + q);
   }
   return 0.f;
 }
@@ -441,18 +460,17 @@ __global__ void __launch_bounds__(256) k_build_x(TcArgs a) {
     if (u < U) {
       const int32_t p = __ldg(a.winner + u);
       const int32_t ev = p >> 1, role = p & 1;
-      const int64_t rw = role ? a.B + ev : ev;
-      const int64_t ro = role ? ev : a.B + ev;
-      if (k < M) v = __ldg(a.snap_mem + rw * a.step * M + k);
-      else if (k < 2 * M) v = __ldg(a.snap_mem + ro * a.step * M + (k - M));
+      if (k < M) v = __ldg(a.snap_mem + snap_row(a, ev, role) * M + k);
+      else if (k < 2 * M) v = __ldg(a.snap_mem + snap_row(a, ev, role ^ 1) * M + (k - M));
       else if (k < d.Dm) v = __ldg(a.ef + (int64_t)ev * d.He + (k - 2 * M));
       else if (k < d.Dx) {
-        const float dt = (float)(__ldg(a.ts + ev) - __ldg(a.snap_ts + rw * a.step));  // Δt (G4)
+        const float dt = (float)(__ldg(a.ts + ev) - __ldg(a.snap_ts + snap_row(a, ev, role)));  // Δt (G4)
         const int q = k - d.Dm;
         v = time_cos(fmaf(__ldg(d.time_w + q), dt, __ldg(d.time_b + q)));
       } else if (k < d.K) {
         const int q = k - d.Dx;
-        v = a.snap_h ? __ldg(a.snap_h + rw * M + q) : __ldg(a.snap_mem + rw * a.step * M + q);
+        v = a.snap_h ? __ldg(a.snap_h + (role ? a.B + ev : (int64_t)ev) * M + q)
+                     : __ldg(a.snap_mem + snap_row(a, ev, role) * M + q);
       }
       if (k < a.mail_stride) a.out_mail[(int64_t)u * a.mail_stride + k] = k < d.Dm ? v : 0.f;
       if (c == 0 && lane == 0) a.out_ts[u] = __ldg(a.ts + ev);
@@ -497,9 +515,8 @@ __device__ __forceinline__ void store_h4(const TcArgs& a, int32_t u, int32_t nod
 // the float4 columns of the mail row are spread over the hidden tiles.
 // (Prefetching these into shared memory during the main loop was measured
 // slower: the extra loads delay the warps' arrival at the cluster barrier.)
-__device__ __forceinline__ void commit_rows(const TcArgs& a, int32_t m0, int32_t U, int rb, int re, int jt,
+__device__ __forceinline__ void commit_rows(const TcArgs& a, int32_t m0, int32_t U, int rb, int re, int jt, int J,
                                             const int32_t* rownode) {
-  const int J = (int)gridDim.y;
   if (!a.new_mail) {  // deferred mailbox (row F3): mem_ts only; the mail rows follow the commit
     if (jt == 0)
       for (int mm = rb + (int)threadIdx.x; mm < re; mm += blockDim.x) {
@@ -549,6 +566,15 @@ __device__ __forceinline__ void commit_rows(const TcArgs& a, int32_t m0, int32_t
 // kBf: bf16 operands (MSPIPE_BF16): 64-wide K chunks of 24 KB stages, one
 // accumulator per CTA for its K range (bf16 tolerance, north star 2e-2); the
 // K split and partial-sum exchange are the tf32 kernel's.
+// Persistent over tiles: grid (S, clusters); cluster c takes tiles
+// q = c, c + clusters, ... of the mt_act x J tiles of the U rows (U read on
+// the device), so no CTA is launched for the empty tiles of the 2B bound.
+// Per tile: the loader streams the K chunks of (mt, jt) through the stage
+// ring (chunk counter continued across tiles, so stage phases carry over) and
+// issues the next tile's first kStages chunks as soon as this tile's MMAs are
+// done, overlapping them with the epilogue; the K-split partials go through
+// two receive buffers (tile parity), so one cluster barrier per tile orders
+// every push after the owner's reads of two tiles before.
 template <bool kBf>
 __global__ void __launch_bounds__(tc::kThreads, 1) k_gru_tc(TcArgs a) {
   using namespace tc;
@@ -563,37 +589,31 @@ __global__ void __launch_bounds__(tc::kThreads, 1) k_gru_tc(TcArgs a) {
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 1);
   int32_t* rownode = reinterpret_cast<int32_t*>(smem + kStages * SB + 512);  // [128] node of each row
   float4* hbuf = reinterpret_cast<float4*>(smem + kStages * SB + 1024);  // [128 rows][kJ/4]
-  float4* recv = reinterpret_cast<float4*>(smem + kStages * SB + 1024 + kHBufBytes);
+  float4* recv2 = reinterpret_cast<float4*>(smem + kStages * SB + 1024 + kHBufBytes);  // [2][kRecvBytes]
   // this tile's gate biases, prefetched during the main loop
-  float* sbias = reinterpret_cast<float*>(smem + kStages * SB + 1024 + kHBufBytes + kRecvBytes);
+  float* sbias = reinterpret_cast<float*>(smem + kStages * SB + 1024 + kHBufBytes + 2 * kRecvBytes);
 
   const GruDesc& d = a.d;
   PHASE(9);
   pdl_begin();
   const int32_t U = __ldg(a.num_unique);
-  // grid (S, jtiles, mtiles): the K split is the cluster dimension and the
-  // M tile the slowest one, so tiles beyond U (known only on the device)
-  // are the last CTAs the scheduler launches and they exit at once.
-  const int32_t mt = blockIdx.z;
-  const int32_t m0 = mt * kM;
-  const int jt = blockIdx.y;
+  const int J = gru_tc_jtiles_dev(d);
   const int S = gridDim.x;
   const int split = blockIdx.x;
-  // CTAs of the active M tiles (at least one tile) share the catch-up
-  const int32_t mt_act = U > 0 ? (U + kM - 1) / kM : 1;
-  const int64_t cta_q = ((int64_t)mt * gridDim.y + jt) * S + split;
-  const int64_t n_cta = (int64_t)mt_act * gridDim.y * S;
+  const int64_t mt_act = U > 0 ? (U + kM - 1) / kM : 0;
+  const int64_t tiles = mt_act * J;
+  const int64_t cta_q = (int64_t)blockIdx.y * S + split;
+  const int64_t n_cta = (int64_t)gridDim.y * S;
   if (a.save_num && cta_q == 0 && threadIdx.x == 0) *a.save_num = U;
-  if (m0 >= U) {  // uniform across the cluster (same blockIdx.z)
-    if (a.cu.stamp && mt < mt_act) catch_up(a, cta_q * (kThreads / 32) + (threadIdx.x >> 5), n_cta * (kThreads / 32),
-                                         threadIdx.x & 31);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if ((int64_t)blockIdx.y >= tiles) {  // no tile for this cluster (uniform across it)
+    if (a.cu.stamp && warp >= 2) catch_up(a, cta_q * 2 + (warp - 2), n_cta * 2, lane);
     return;
   }
   const int32_t nchunks = d.Kpad / (kBf ? kKC16 : kKC);
   const int32_t c0 = split * nchunks / S, c1 = (split + 1) * nchunks / S;
   const int32_t nc = c1 - c0;  // tf32: <= kMaxChunks (host picks S >= nchunks / kMaxChunks)
   const uint32_t tcols = kBf ? 64u : (nc <= 2 ? 128u : (nc <= 4 ? 256u : 512u));
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
@@ -609,185 +629,207 @@ __global__ void __launch_bounds__(tc::kThreads, 1) k_gru_tc(TcArgs a) {
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  const int rank = S > 1 ? (int)cluster_rank() : 0;
 
-  if (warp == 0 && lane == 0) {
-    // loader: one A block (32 KB) + one B block (16 KB) per stage
-    const char* abase = reinterpret_cast<const char*>(a.xbuf) + (int64_t)mt * nchunks * AB;
-    const char* bbase = reinterpret_cast<const char*>(a.wtc) + (int64_t)jt * nchunks * BB;
-    for (int ci = 0; ci < nc; ++ci) {
-      const int s = ci % kStages;
-      const uint32_t ph = (uint32_t)(ci / kStages) & 1u;
-      mbar_wait(&empty[s], ph ^ 1u);
-      uint8_t* st = smem + s * SB;
-      mbar_arrive_expect_tx(&full[s], SB);
-      bulk_g2s(st, abase + (int64_t)(c0 + ci) * AB, AB, &full[s]);
-      bulk_g2s(st + AB, bbase + (int64_t)(c0 + ci) * BB, BB, &full[s]);
-    }
-  } else if (warp == 1 && lane == 0) {
-    // MMA issuer.  Each K chunk accumulates into its OWN 64-column TMEM
-    // buffer (12 MMAs): the tensor core's accumulation truncates, so the error
-    // grows with the MMAs per accumulator (measured: max 5.2e-6 for 222 MMAs,
-    // 1.0e-6 for 28); the epilogue then adds the buffers in fp32 registers
-    // with round-to-nearest, in chunk order.
-    for (int ci = 0; ci < nc; ++ci) {
-      const int s = ci % kStages;
-      const uint32_t ph = (uint32_t)(ci / kStages) & 1u;
-      mbar_wait(&full[s], ph);
-      tc_fence_after();
-      const uint32_t base = smem_u32(smem + s * SB);
-      if (kBf) {  // 4 MMAs of K = 16 (32 B along K) into the single accumulator
-        const uint64_t da = sw128_desc(base), db = sw128_desc(base + AB);
+  // loader: chunk ci of the tile with sequence number ti (global chunk counter g = ti*nc + ci)
+  auto load_chunk = [&](int64_t ti, int32_t mt_l, int jt_l, int ci) {
+    const int64_t g = ti * nc + ci;
+    const int s = (int)(g % kStages);
+    const uint32_t ph = (uint32_t)(g / kStages) & 1u;
+    mbar_wait(&empty[s], ph ^ 1u);
+    uint8_t* st = smem + s * SB;
+    mbar_arrive_expect_tx(&full[s], SB);
+    bulk_g2s(st, reinterpret_cast<const char*>(a.xbuf) + ((int64_t)mt_l * nchunks + c0 + ci) * AB, AB, &full[s]);
+    bulk_g2s(st + AB, reinterpret_cast<const char*>(a.wtc) + ((int64_t)jt_l * nchunks + c0 + ci) * BB, BB, &full[s]);
+  };
+  int pre = 0;  // chunks of the current tile the loader already issued (at the previous tile's end)
+  int64_t ti = 0;
+  for (int64_t q = blockIdx.y; q < tiles; q += gridDim.y, ++ti) {
+    const int32_t mt = (int32_t)(q / J);
+    const int jt = (int)(q % J);
+    const int32_t m0 = mt * kM;
+    float4* recv = recv2 + (ti & 1) * (kRecvBytes / 16);
+    if (warp == 0 && lane == 0) {
+      for (int ci = pre; ci < nc; ++ci) load_chunk(ti, mt, jt, ci);
+    } else if (warp == 1 && lane == 0) {
+      // MMA issuer.  Each K chunk accumulates into its OWN 64-column TMEM
+      // buffer (12 MMAs): the tensor core's accumulation truncates, so the error
+      // grows with the MMAs per accumulator (measured: max 5.2e-6 for 222 MMAs,
+      // 1.0e-6 for 28); the epilogue then adds the buffers in fp32 registers
+      // with round-to-nearest, in chunk order.
+      for (int ci = 0; ci < nc; ++ci) {
+        const int64_t g = ti * nc + ci;
+        const int s = (int)(g % kStages);
+        const uint32_t ph = (uint32_t)(g / kStages) & 1u;
+        mbar_wait(&full[s], ph);
+        tc_fence_after();
+        const uint32_t base = smem_u32(smem + s * SB);
+        if (kBf) {  // 4 MMAs of K = 16 (32 B along K) into the single accumulator
+          const uint64_t da = sw128_desc(base), db = sw128_desc(base + AB);
 #pragma unroll
-        for (int kk = 0; kk < kKC16 / 16; ++kk) {
-          const uint64_t adv = (uint64_t)(kk * 32) >> 4;
-          mma_bf16(tmem, da + adv, db + adv, kIdescBf, (ci | kk) != 0);
-        }
-      } else {
-        const uint64_t da_hi = sw128_desc(base), da_lo = sw128_desc(base + kATile);
-        const uint64_t db_hi = sw128_desc(base + kABlock), db_lo = sw128_desc(base + kABlock + kBTile);
-        const uint32_t tacc = tmem + (uint32_t)(ci * kN);
+          for (int kk = 0; kk < kKC16 / 16; ++kk) {
+            const uint64_t adv = (uint64_t)(kk * 32) >> 4;
+            mma_bf16(tmem, da + adv, db + adv, kIdescBf, (ci | kk) != 0);
+          }
+        } else {
+          const uint64_t da_hi = sw128_desc(base), da_lo = sw128_desc(base + kATile);
+          const uint64_t db_hi = sw128_desc(base + kABlock), db_lo = sw128_desc(base + kABlock + kBTile);
+          const uint32_t tacc = tmem + (uint32_t)(ci * kN);
 #pragma unroll
-        for (int kk = 0; kk < kKC / 8; ++kk) {
-          const uint64_t adv = (uint64_t)(kk * 32) >> 4;  // 8 tf32 = 32 B along K inside the swizzle row
-          mma_tf32(tacc, da_lo + adv, db_hi + adv, kIdesc, kk != 0);
-          mma_tf32(tacc, da_hi + adv, db_lo + adv, kIdesc, 1u);
-          mma_tf32(tacc, da_hi + adv, db_hi + adv, kIdesc, 1u);
+          for (int kk = 0; kk < kKC / 8; ++kk) {
+            const uint64_t adv = (uint64_t)(kk * 32) >> 4;  // 8 tf32 = 32 B along K inside the swizzle row
+            mma_tf32(tacc, da_lo + adv, db_hi + adv, kIdesc, kk != 0);
+            mma_tf32(tacc, da_hi + adv, db_lo + adv, kIdesc, 1u);
+            mma_tf32(tacc, da_hi + adv, db_hi + adv, kIdesc, 1u);
+          }
+        }
+        mma_commit(&empty[s]);
+      }
+      mma_commit(acc_full);
+      PHASE_T(2);
+    } else if (warp >= 2) {
+      // idle warps: prefetch h (the GRU hidden input: snap_h, the snapshot
+      // row, or the staged mail row, G13/G14) of the rows this CTA will
+      // finalise, 4 hidden units per item
+      const int rb = rank * kM / S, re = (rank + 1) * kM / S;
+      for (int it = threadIdx.x - 64; it < (re - rb) * (kJ / 4); it += 64) {
+        const int mm = rb + it / (kJ / 4), qq = it % (kJ / 4);
+        const int32_t u = m0 + mm, j0 = jt * kJ + qq * 4;
+        float4 hv = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (u < U && j0 < d.M) {  // M % 4 == 0: a quad is all valid or all padding
+          const float* hrow;
+          if (a.h_from_mail) {
+            hrow = a.new_mail + (int64_t)u * a.mail_stride;
+          } else {
+            const int32_t p = __ldg(a.winner + u);
+            const int64_t rw = (p & 1) ? a.B + (p >> 1) : (p >> 1);
+            hrow = a.snap_h ? a.snap_h + rw * d.M : a.snap_mem + rw * a.step * d.M;
+          }
+          hv = __ldg(reinterpret_cast<const float4*>(hrow + j0));
+        }
+        hbuf[mm * (kJ / 4) + qq] = hv;
+        if (qq == 0) {
+          const int32_t node = (a.commit_mem && u < U) ? __ldg(a.nodes + u) : -1;
+          rownode[mm] = node;
+          if (a.save_nodes && jt == 0 && node >= 0) a.save_nodes[u] = node;
         }
       }
-      mma_commit(&empty[s]);
+      for (int i = threadIdx.x - 64; i < kN; i += 64) sbias[i] = __ldg(d.bias + jt * kN + i);
+      if (ti == 0 && a.cu.stamp) catch_up(a, cta_q * 2 + (warp - 2), n_cta * 2, lane);
     }
-    mma_commit(acc_full);
-    PHASE_T(2);
-  } else if (warp >= 2) {
-    // idle warps: prefetch h (the GRU hidden input: snap_h or the snapshot
-    // row, G13) of the rows this CTA will finalise, 4 hidden units per item
-    const int rank = S > 1 ? (int)cluster_rank() : 0;
-    const int rb = rank * kM / S, re = (rank + 1) * kM / S;
-    for (int it = threadIdx.x - 64; it < (re - rb) * (kJ / 4); it += 64) {
-      const int mm = rb + it / (kJ / 4), q = it % (kJ / 4);
-      const int32_t u = m0 + mm, j0 = jt * kJ + q * 4;
-      float4 hv = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (u < U && j0 < d.M) {  // M % 4 == 0: a quad is all valid or all padding
-        const int32_t p = __ldg(a.winner + u);
-        const int64_t rw = (p & 1) ? a.B + (p >> 1) : (p >> 1);
-        const float* hrow = a.snap_h ? a.snap_h + rw * d.M : a.snap_mem + rw * a.step * d.M;
-        hv = __ldg(reinterpret_cast<const float4*>(hrow + j0));
-      }
-      hbuf[mm * (kJ / 4) + q] = hv;
-      if (q == 0) {
-        const int32_t node = (a.commit_mem && u < U) ? __ldg(a.nodes + u) : -1;
-        rownode[mm] = node;
-        if (a.save_nodes && jt == 0 && node >= 0) a.save_nodes[u] = node;
-      }
-    }
-    for (int i = threadIdx.x - 64; i < kN; i += 64) sbias[i] = __ldg(d.bias + jt * kN + i);
-    if (a.cu.stamp) catch_up(a, cta_q * 2 + (warp - 2), n_cta * 2, lane);
-  }
-  __syncwarp();
+    __syncwarp();
 
-  // ---------------- epilogue: TMEM -> registers (thread = row)
-  mbar_wait(acc_full, 0);
-  PHASE(3);
-  tc_fence_after();
-  const int m = warp * 32 + lane;
-  const uint32_t tbase = tmem + ((uint32_t)(warp * 32) << 16);
-  uint32_t r0[32], r1[32];
-  MSPIPE_TMEM_LD32(tbase, r0);
-  MSPIPE_TMEM_LD32(tbase + 32, r1);
-  tmem_wait_ld();
-  for (int ci = 1; ci < (kBf ? 1 : nc); ++ci) {
-    uint32_t t0[32], t1[32];
-    MSPIPE_TMEM_LD32(tbase + ci * kN, t0);
-    MSPIPE_TMEM_LD32(tbase + ci * kN + 32, t1);
-    tmem_wait_ld();
-#pragma unroll
-    for (int i = 0; i < 32; ++i) {
-      r0[i] = __float_as_uint(__fadd_rn(__uint_as_float(r0[i]), __uint_as_float(t0[i])));
-      r1[i] = __float_as_uint(__fadd_rn(__uint_as_float(r1[i]), __uint_as_float(t1[i])));
-    }
-  }
-  PHASE(4);
-  const float* bias = sbias;
-  if (S > 1) {
-    // push this CTA's partial row m into the receive buffer of the rank that
-    // finalises it: recv[src_rank][m - rb(owner)][16 x float4], float4 index
-    // XOR-swizzled by the row so the owner's reads are conflict-free.
-    // Fire-and-forget remote stores instead of latency-bound remote loads.
-    const int R = kM / S;
-    const int owner = m / R, lm = m % R;
-    const uint32_t dst = mapa(smem_u32(recv) + (uint32_t)((cluster_rank() * R + lm) * (kN / 4)) * 16u, (uint32_t)owner);
-#pragma unroll
-    for (int c4 = 0; c4 < 8; ++c4) {
-      st_dsmem_f4(dst + 16u * (uint32_t)(c4 ^ (lm & 15)), __uint_as_float(r0[4 * c4]), __uint_as_float(r0[4 * c4 + 1]),
-                  __uint_as_float(r0[4 * c4 + 2]), __uint_as_float(r0[4 * c4 + 3]));
-      st_dsmem_f4(dst + 16u * (uint32_t)((8 + c4) ^ (lm & 15)), __uint_as_float(r1[4 * c4]),
-                  __uint_as_float(r1[4 * c4 + 1]), __uint_as_float(r1[4 * c4 + 2]), __uint_as_float(r1[4 * c4 + 3]));
-    }
-  }
-  tc_fence_before();
-  __syncthreads();  // hbuf complete
-  PHASE(5);
-  if (warp == 2) {
+    // ---------------- epilogue: TMEM -> registers (thread = row)
+    mbar_wait(acc_full, (uint32_t)(ti & 1));
+    PHASE(3);
     tc_fence_after();
-    tmem_dealloc(tmem, tcols);
-  }
-  if (S == 1) {
-    const int32_t u = m0 + m;
-    if (u < U) {
+    if (warp == 0 && lane == 0) {  // the stages are free: start the next tile's loads now
+      pre = 0;
+      const int64_t qn = q + gridDim.y;
+      if (qn < tiles)
+        for (; pre < nc && pre < kStages; ++pre) load_chunk(ti + 1, (int32_t)(qn / J), (int)(qn % J), pre);
+    }
+    const int m = warp * 32 + lane;
+    const uint32_t tbase = tmem + ((uint32_t)(warp * 32) << 16);
+    uint32_t r0[32], r1[32];
+    MSPIPE_TMEM_LD32(tbase, r0);
+    MSPIPE_TMEM_LD32(tbase + 32, r1);
+    tmem_wait_ld();
+    for (int ci = 1; ci < (kBf ? 1 : nc); ++ci) {
+      uint32_t t0[32], t1[32];
+      MSPIPE_TMEM_LD32(tbase + ci * kN, t0);
+      MSPIPE_TMEM_LD32(tbase + ci * kN + 32, t1);
+      tmem_wait_ld();
 #pragma unroll
-      for (int q = 0; q < kJ / 4; ++q) {
-        const int32_t j0 = jt * kJ + q * 4;
-        if (j0 >= d.M) break;
+      for (int i = 0; i < 32; ++i) {
+        r0[i] = __float_as_uint(__fadd_rn(__uint_as_float(r0[i]), __uint_as_float(t0[i])));
+        r1[i] = __float_as_uint(__fadd_rn(__uint_as_float(r1[i]), __uint_as_float(t1[i])));
+      }
+    }
+    PHASE(4);
+    const float* bias = sbias;
+    if (S > 1) {
+      // push this CTA's partial row m into the receive buffer of the rank that
+      // finalises it: recv[src_rank][m - rb(owner)][16 x float4], float4 index
+      // XOR-swizzled by the row so the owner's reads are conflict-free.
+      // Fire-and-forget remote stores instead of latency-bound remote loads.
+      const int R = kM / S;
+      const int owner = m / R, lm = m % R;
+      const uint32_t dst = mapa(smem_u32(recv) + (uint32_t)((rank * R + lm) * (kN / 4)) * 16u, (uint32_t)owner);
+#pragma unroll
+      for (int c4 = 0; c4 < 8; ++c4) {
+        st_dsmem_f4(dst + 16u * (uint32_t)(c4 ^ (lm & 15)), __uint_as_float(r0[4 * c4]), __uint_as_float(r0[4 * c4 + 1]),
+                    __uint_as_float(r0[4 * c4 + 2]), __uint_as_float(r0[4 * c4 + 3]));
+        st_dsmem_f4(dst + 16u * (uint32_t)((8 + c4) ^ (lm & 15)), __uint_as_float(r1[4 * c4]),
+                    __uint_as_float(r1[4 * c4 + 1]), __uint_as_float(r1[4 * c4 + 2]), __uint_as_float(r1[4 * c4 + 3]));
+      }
+    }
+    tc_fence_before();
+    __syncthreads();  // hbuf complete; every TMEM read of this tile done (the next tile's MMAs may start)
+    PHASE(5);
+    if (S == 1) {
+      const int32_t u = m0 + m;
+      if (u < U) {
+#pragma unroll
+        for (int qq = 0; qq < kJ / 4; ++qq) {
+          const int32_t j0 = jt * kJ + qq * 4;
+          if (j0 >= d.M) break;
+          float pr[4], pz[4], pnx[4], pnh[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int jj = qq * 4 + e;
+            pr[e] = __uint_as_float(r0[jj]) + bias[jj];
+            pz[e] = __uint_as_float(r0[kJ + jj]) + bias[kJ + jj];
+            pnx[e] = __uint_as_float(r1[jj]) + bias[2 * kJ + jj];
+            pnh[e] = __uint_as_float(r1[kJ + jj]) + bias[3 * kJ + jj];
+          }
+          store_h4(a, u, rownode[m], j0, gates4(pr, pz, pnx, pnh, hbuf[m * (kJ / 4) + qq], d.cell));
+        }
+      }
+      if (a.commit_mem) commit_rows(a, m0, U, 0, kM, jt, J, rownode);
+    } else {
+      cluster_sync_all();  // all pushes into recv are visible
+      PHASE(6);
+      const int R = kM / S;
+      const int rb = rank * R;
+      for (int it = threadIdx.x; it < R * (kJ / 4); it += kThreads) {
+        const int lm = it / (kJ / 4), qq = it % (kJ / 4);
+        const int mm = rb + lm;
+        const int32_t u = m0 + mm;
+        const int32_t j0 = jt * kJ + qq * 4;
+        if (u >= U || j0 >= d.M) continue;
+        float4 acc[4];
+#pragma unroll
+        for (int g = 0; g < 4; ++g) acc[g] = recv[(0 * R + lm) * (kN / 4) + ((g * (kJ / 4) + qq) ^ (lm & 15))];
+        for (int sr = 1; sr < S; ++sr)  // fixed rank order: deterministic sum
+#pragma unroll
+          for (int g = 0; g < 4; ++g) {
+            const float4 v = recv[(sr * R + lm) * (kN / 4) + ((g * (kJ / 4) + qq) ^ (lm & 15))];
+            acc[g].x += v.x;
+            acc[g].y += v.y;
+            acc[g].z += v.z;
+            acc[g].w += v.w;
+          }
+        if (it == threadIdx.x) PHASE(7);
         float pr[4], pz[4], pnx[4], pnh[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-          const int jj = q * 4 + e;
-          pr[e] = __uint_as_float(r0[jj]) + bias[jj];
-          pz[e] = __uint_as_float(r0[kJ + jj]) + bias[kJ + jj];
-          pnx[e] = __uint_as_float(r1[jj]) + bias[2 * kJ + jj];
-          pnh[e] = __uint_as_float(r1[kJ + jj]) + bias[3 * kJ + jj];
+          const int jj = qq * 4 + e;
+          pr[e] = (&acc[0].x)[e] + bias[jj];
+          pz[e] = (&acc[1].x)[e] + bias[kJ + jj];
+          pnx[e] = (&acc[2].x)[e] + bias[2 * kJ + jj];
+          pnh[e] = (&acc[3].x)[e] + bias[3 * kJ + jj];
         }
-        store_h4(a, u, rownode[m], j0, gates4(pr, pz, pnx, pnh, hbuf[m * (kJ / 4) + q], d.cell));
+        store_h4(a, u, rownode[mm], j0, gates4(pr, pz, pnx, pnh, hbuf[mm * (kJ / 4) + qq], d.cell));
       }
+      if (a.commit_mem) commit_rows(a, m0, U, rb, rb + R, jt, J, rownode);
+      PHASE(8);
     }
-    if (a.commit_mem) commit_rows(a, m0, U, 0, kM, jt, rownode);
-  } else {
-    cluster_sync_all();  // all pushes into recv are visible; nobody writes recv afterwards
-    PHASE(6);
-    const int R = kM / S;
-    const int rb = (int)cluster_rank() * R;
-    for (int it = threadIdx.x; it < R * (kJ / 4); it += kThreads) {
-      const int lm = it / (kJ / 4), q = it % (kJ / 4);
-      const int mm = rb + lm;
-      const int32_t u = m0 + mm;
-      const int32_t j0 = jt * kJ + q * 4;
-      if (u >= U || j0 >= d.M) continue;
-      float4 acc[4];
-#pragma unroll
-      for (int g = 0; g < 4; ++g) acc[g] = recv[(0 * R + lm) * (kN / 4) + ((g * (kJ / 4) + q) ^ (lm & 15))];
-      for (int sr = 1; sr < S; ++sr)  // fixed rank order: deterministic sum
-#pragma unroll
-        for (int g = 0; g < 4; ++g) {
-          const float4 v = recv[(sr * R + lm) * (kN / 4) + ((g * (kJ / 4) + q) ^ (lm & 15))];
-          acc[g].x += v.x;
-          acc[g].y += v.y;
-          acc[g].z += v.z;
-          acc[g].w += v.w;
-        }
-      if (it == threadIdx.x) PHASE(7);
-      float pr[4], pz[4], pnx[4], pnh[4];
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int jj = q * 4 + e;
-        pr[e] = (&acc[0].x)[e] + bias[jj];
-        pz[e] = (&acc[1].x)[e] + bias[kJ + jj];
-        pnx[e] = (&acc[2].x)[e] + bias[2 * kJ + jj];
-        pnh[e] = (&acc[3].x)[e] + bias[3 * kJ + jj];
-      }
-      store_h4(a, u, rownode[mm], j0, gates4(pr, pz, pnx, pnh, hbuf[mm * (kJ / 4) + q], d.cell));
-    }
-    if (a.commit_mem) commit_rows(a, m0, U, rb, rb + R, jt, rownode);
-    PHASE(8);
+    __syncthreads();  // hbuf / rownode / sbias are rewritten by the next tile's prefetch
+  }
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem, tcols);
   }
 }
 
@@ -1193,6 +1235,34 @@ cudaError_t launch_gru_fb(const GruDesc& d, const float* wtc, const double* ts, 
 
 constexpr int kMaxChunks = 8;  // 8 x 64 TMEM columns = 512 (the whole TMEM of the SM)
 
+// co-resident clusters of S CTAs of k_gru_tc (cached per S; env MSPIPE_TC_CLUSTERS overrides)
+static int64_t gru_tc_clusters(int S, bool bf16) {
+  static int64_t cache[2][17] = {};
+  int64_t& c = cache[bf16 ? 1 : 0][S & 15];
+  if (c > 0) return c;
+  const int forced = env_int("MSPIPE_TC_CLUSTERS", 0);
+  if (forced > 0) return c = forced;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)S, 1, 1);
+  cfg.blockDim = dim3(tc::kThreads);
+  cfg.dynamicSmemBytes = tc::kSmemBytesP;
+  cudaLaunchAttribute attr;
+  attr.id = cudaLaunchAttributeClusterDimension;
+  attr.val.clusterDim.x = (unsigned)S;
+  attr.val.clusterDim.y = 1;
+  attr.val.clusterDim.z = 1;
+  cfg.attrs = &attr;
+  cfg.numAttrs = 1;
+  int n = 0;
+  const cudaError_t e = bf16 ? cudaOccupancyMaxActiveClusters(&n, k_gru_tc<true>, &cfg)
+                             : cudaOccupancyMaxActiveClusters(&n, k_gru_tc<false>, &cfg);
+  if (e != cudaSuccess || n <= 0) {
+    (void)cudaGetLastError();
+    n = num_sms() / S;
+  }
+  return c = n;
+}
+
 int gru_tc_splits(int64_t max_rows, const GruDesc& d) {
   // K-split = cluster size.  Powers of two pack the GPCs (measured: 5-CTA
   // clusters of 1-CTA-per-SM blocks spill into a second wave, 4 do not).
@@ -1216,13 +1286,16 @@ cudaError_t launch_gru_tc(const GruDesc& d, const float* wtc, float* xbuf, const
                           const float* edge_feat, const float* snap_mem, const double* snap_mem_ts,
                           int64_t snap_step, const float* snap_h, const int32_t* winner,
                           const int32_t* num_unique, float* out_mem, double* out_ts, float* out_mail,
-                          int64_t mail_stride, cudaStream_t s, int parts, const GruCommit* commit) {
+                          int64_t mail_stride, cudaStream_t s, int parts, const GruCommit* commit,
+                          const int32_t* tab_src, const int32_t* tab_dst) {
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(k_gru_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         tc::kSmemBytes);
+                                         tc::kSmemBytesP);
     if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(k_gru_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::kSmemBytes);
+      e = cudaFuncSetAttribute(k_gru_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::kSmemBytesP);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_gru_tc<false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_gru_tc<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
@@ -1241,7 +1314,10 @@ cudaError_t launch_gru_tc(const GruDesc& d, const float* wtc, float* xbuf, const
     a.save_nodes = commit->save_nodes;
     a.save_num = commit->save_num;
     a.cu = commit->cu;
+    a.h_from_mail = snap_mem == nullptr && snap_h == nullptr;
   }
+  a.tsrc = tab_src;
+  a.tdst = tab_dst;
   const int64_t max_rows = 2 * num_events;
   const int64_t mtiles = (max_rows + tc::kM - 1) / tc::kM;
   if (parts & kGruBuild) {
@@ -1254,11 +1330,15 @@ cudaError_t launch_gru_tc(const GruDesc& d, const float* wtc, float* xbuf, const
   }
   if (!(parts & kGruGemm)) return cudaSuccess;
   const int S = gru_tc_splits(max_rows, d);
+  // persistent grid: as many S-CTA clusters as are co-resident (one CTA per
+  // SM: the stage ring fills shared memory), at most one per tile of the bound
+  const int64_t max_tiles = mtiles * gru_tc_jtiles(d);
+  const int64_t nclust = std::min<int64_t>(max_tiles, gru_tc_clusters(S, d.bf16));
   if (d.bf16)
-    return launch_k(k_gru_tc<true>, dim3((unsigned)S, (unsigned)gru_tc_jtiles(d), (unsigned)mtiles),
-                    dim3(tc::kThreads), tc::kSmemBytes, s, (unsigned)S, a);
-  return launch_k(k_gru_tc<false>, dim3((unsigned)S, (unsigned)gru_tc_jtiles(d), (unsigned)mtiles),
-                  dim3(tc::kThreads), tc::kSmemBytes, s, (unsigned)S, a);
+    return launch_k(k_gru_tc<true>, dim3((unsigned)S, (unsigned)nclust), dim3(tc::kThreads), tc::kSmemBytesP, s,
+                    (unsigned)S, a);
+  return launch_k(k_gru_tc<false>, dim3((unsigned)S, (unsigned)nclust), dim3(tc::kThreads), tc::kSmemBytesP, s,
+                  (unsigned)S, a);
 }
 
 }  // namespace mspipe

@@ -202,7 +202,7 @@ void launch_mitigate(const Tcsr& g, const int32_t* src, const int32_t* dst, cons
                      int32_t* out_omega, uint8_t* out_elig, cudaStream_t s);
 void launch_dedup(const int32_t* src, const int32_t* dst, int64_t num_events, int32_t* scratch,
                   int64_t num_nodes, int32_t* out_nodes, int32_t* out_winner, int32_t* out_num,
-                  cudaStream_t s);
+                  cudaStream_t s, int32_t* stamp = nullptr, int32_t stamp_iter = 0);
 void launch_writeback(const int32_t* nodes, const int32_t* num, int64_t max_n,
                       const float* new_mem, const double* new_ts, const float* new_mail,
                       int32_t mem_dim, int64_t mail_stride, float* mem, double* mem_ts,
@@ -335,7 +335,8 @@ cudaError_t launch_gru_tc(const GruDesc& d, const float* wtc, float* xbuf, const
                           int64_t snap_step, const float* snap_h, const int32_t* winner,
                           const int32_t* num_unique, float* out_mem, double* out_ts, float* out_mail,
                           int64_t mail_stride, cudaStream_t s, int parts = kGruBuild | kGruGemm,
-                          const GruCommit* commit = nullptr);
+                          const GruCommit* commit = nullptr, const int32_t* tab_src = nullptr,
+                          const int32_t* tab_dst = nullptr);
 // features.cu
 cudaError_t launch_feature_fetch(const int32_t* sub, const int32_t* eid, int64_t R, int32_t F, const float* nfeat,
                                  int64_t N, int32_t nstride, const float* efeat, int64_t E, int32_t estride,

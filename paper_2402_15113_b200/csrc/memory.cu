@@ -258,15 +258,21 @@ template <bool kSmem>
 __global__ void __launch_bounds__(kDedupThreads) k_dedup(
     const int32_t* __restrict__ src, const int32_t* __restrict__ dst, int64_t B,
     int32_t* __restrict__ gscratch, int64_t N, int32_t* __restrict__ out_nodes,
-    int32_t* __restrict__ out_winner, int32_t* __restrict__ out_num) {
+    int32_t* __restrict__ out_winner, int32_t* __restrict__ out_num, int32_t* __restrict__ stamp,
+    int32_t stamp_iter) {
   pdl_begin();
   extern __shared__ int32_t sscratch[];
   block_dedup<kDedupThreads, kSmem>(src, dst, B, gscratch, sscratch, N, out_nodes, out_winner, out_num);
+  if (stamp) {  // double-buffered state: stamp[winner node] = iteration (as k_prep's dedup block)
+    __syncthreads();
+    const int32_t U = *out_num;
+    for (int32_t u = threadIdx.x; u < U; u += kDedupThreads) stamp[out_nodes[u]] = stamp_iter;
+  }
 }
 
 void launch_dedup(const int32_t* src, const int32_t* dst, int64_t num_events, int32_t* scratch,
                   int64_t num_nodes, int32_t* out_nodes, int32_t* out_winner, int32_t* out_num,
-                  cudaStream_t s) {
+                  cudaStream_t s, int32_t* stamp, int32_t stamp_iter) {
   if (num_nodes <= kDedupSmemNodes) {
     static bool attr = false;
     if (!attr) {
@@ -275,10 +281,10 @@ void launch_dedup(const int32_t* src, const int32_t* dst, int64_t num_events, in
       attr = true;
     }
     launch_k(k_dedup<true>, dim3(1), dim3(kDedupThreads), num_nodes * sizeof(int32_t), s, 1, src, dst, num_events,
-             scratch, num_nodes, out_nodes, out_winner, out_num);
+             scratch, num_nodes, out_nodes, out_winner, out_num, stamp, stamp_iter);
   } else {
     launch_k(k_dedup<false>, dim3(1), dim3(kDedupThreads), 0, s, 1, src, dst, num_events, scratch, num_nodes,
-             out_nodes, out_winner, out_num);
+             out_nodes, out_winner, out_num, stamp, stamp_iter);
   }
 }
 

@@ -52,6 +52,7 @@ struct PrepArgs {
   CatchUp cu;      // optional (cu.stamp != nullptr): the next commit's catch-up rows
   int32_t Qcu;     // float4 per mail row of the state tables (catch-up)
   PrepBuild bld;   // optional (bld.xbuf != nullptr): fused A5 message build
+  int32_t dedup;   // 1: block 0 deduplicates (A2); 0: no dedup block (done by mspipe_memory_winners)
 };
 
 __device__ __forceinline__ int32_t ld_acquire(const int32_t* p) {
@@ -152,7 +153,7 @@ __global__ void __launch_bounds__(kPrepThreads) k_prep(PrepArgs a) {
   extern __shared__ int32_t sscratch[];
   pdl_begin();
   if (threadIdx.x == 0) PPHASE(0);
-  if (blockIdx.x == 0) {
+  if (a.dedup && blockIdx.x == 0) {
     block_dedup<kPrepThreads, kSmem>(a.src, a.dst, a.B, a.gscratch, sscratch, a.g.num_nodes, a.out_nodes,
                                      a.out_winner, a.out_num);
     if (threadIdx.x == 0) PPHASE(2);
@@ -178,8 +179,8 @@ __global__ void __launch_bounds__(kPrepThreads) k_prep(PrepArgs a) {
   const int lane = threadIdx.x & 31;
   const int64_t R = 3 * a.B;
   const int F = a.F, F1 = a.F + 1;
-  const int64_t nwarps = (int64_t)(gridDim.x - 1) * kPrepWarps;
-  const int64_t wid = (int64_t)(blockIdx.x - 1) * kPrepWarps + (threadIdx.x >> 5);
+  const int64_t nwarps = (int64_t)(gridDim.x - a.dedup) * kPrepWarps;
+  const int64_t wid = (int64_t)(blockIdx.x - a.dedup) * kPrepWarps + (threadIdx.x >> 5);
   for (int64_t r = wid; r < R; r += nwarps) {
     const int64_t role = r / a.B, ev = r - role * a.B;
     const int32_t v = role == 0 ? __ldg(a.src + ev) : (role == 1 ? __ldg(a.dst + ev) : __ldg(a.neg + ev));
@@ -252,9 +253,11 @@ cudaError_t launch_prep(const Tcsr& g, const int32_t* src, const int32_t* dst, c
              (int32_t)(mail_stride / 4)};
   if (cu) a.cu = *cu;
   if (bld) a.bld = *bld;
+  a.dedup = out_num != nullptr;
   int64_t blocks = (3 * num_events + kPrepWarps - 1) / kPrepWarps;
   const int64_t cap = (int64_t)num_sms() * env_int("MSPIPE_PREP_BPS", 4);
   if (blocks > cap) blocks = cap;
+  if (!a.dedup) return launch_k(k_prep<false>, dim3((unsigned)blocks), dim3(kPrepThreads), 0, s, 1, a);
   blocks += 1;  // block 0: dedup
   if (g.num_nodes <= kDedupSmemNodes && env_int("MSPIPE_PREP_SMEM", 1)) {
     static bool attr = false;

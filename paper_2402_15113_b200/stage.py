@@ -60,6 +60,14 @@ class StageConfig:
     # Off by default: measured slower on the wiki step (30.7 vs 26.0 us; the build waits for the
     # single dedup block and the longer prep kernel contends with the GEMM).  env MSPIPE_PREP_BUILD=1: A/B
     prep_build: bool = dataclasses.field(default_factory=lambda: os.environ.get("MSPIPE_PREP_BUILD", "0") == "1")
+    # fused path without mitigation: the message build reads the state tables of the fetched
+    # version directly (mspipe_message_build_tables) on a third stream, right after the dedup
+    # (mspipe_memory_winners), concurrently with the sampler + gather of the same prep, so the
+    # build no longer waits for the gather.  Off by default: measured slower on the wiki
+    # step (28.9 vs 25.2 us; the one-CTA dedup kernel, 6.8 us cold, then heads the build's
+    # chain, and four concurrent kernels contend for the SMs).  env MSPIPE_DIRECT_BUILD=1: A/B
+    direct_build: bool = dataclasses.field(
+        default_factory=lambda: os.environ.get("MSPIPE_DIRECT_BUILD", "0") == "1")
 
     def use_fused(self) -> bool:
         ok = self.precision in (_C.FP32_3XTF32, _C.BF16) and self.fanout <= 31 and self.batch <= 8192
@@ -202,6 +210,9 @@ class MemoryStage(_TimedOps):
         self.fused = cfg.use_fused()
         self.gemm_build = (self.fused and cfg.gemm_build and not cfg.mitigation and not self.deferred
                            and cfg.precision == _C.FP32_3XTF32 and not cfg.prep_build)
+        self.direct = (self.fused and cfg.direct_build and not cfg.mitigation and not self.deferred
+                       and not cfg.prep_build and not self.gemm_build)
+        self.bstream = None
         if self.deferred and not (self.fused and cfg.fetch_mail and not cfg.prep_build):
             raise ValueError("mailbox='deferred' runs on the fused tensor-core path with fetch_mail=True")
         self.ws_bytes = _C.gru_workspace_size(self.gru, cfg.batch) if self.fused else 0
@@ -402,6 +413,9 @@ class MemoryStage(_TimedOps):
                 self._fetched = torch.cuda.Event()  # the state tables have been read for batch i
                 self._fetched.record()
             return
+        if self.direct:
+            self._prep_direct(i, sl, x, n, samp, m)
+            return
         self._ev("prep")
         sl.version = _C.memory_prep(self.memory, self.tcsr, i, x["src"], x["dst"], x["neg"], x["ts"], cfg.fanout,
                                     samp, sl.dd, sl.mem[:m], sl.mem_ts[:m],
@@ -424,6 +438,39 @@ class MemoryStage(_TimedOps):
                              sl.dd["num"], sl.uts[: 2 * n], sl.umail[: 2 * n], sl.ws,
                              snap_h=sl.h[: 2 * n] if sl.h is not None else None)
         self._ev("build_end")
+
+    def _prep_direct(self, i, sl, x, n, samp, m):
+        """Three launches on two streams: mspipe_memory_winners (A2) then
+        mspipe_message_build_tables (A5, from the tables of the fetched
+        version) on a build stream, while mspipe_memory_prep without its dedup
+        block (A1 + A3) samples and gathers; the build stream joins at the end."""
+        cfg = self.cfg
+        cur = torch.cuda.current_stream()
+        if self.bstream is None or self.bstream.device != cur.device:
+            self.bstream = torch.cuda.Stream(device=cur.device, priority=int(os.environ.get("MSPIPE_BUILD_PRIO", "0")))
+        self.bstream.wait_stream(cur)
+        with torch.cuda.stream(self.bstream):
+            self._ev("dedup")
+            _C.memory_winners(self.memory, i, x["src"], x["dst"], sl.dd)
+            self._ev("dedup_end")
+            self._ev("build")
+            vb = _C.message_build_tables(self.gru, self.memory, i, x["src"], x["dst"], x["ts"], x["ef"],
+                                         sl.dd["winner"][: 2 * n], sl.dd["num"], sl.uts[: 2 * n], sl.umail[: 2 * n],
+                                         sl.ws)
+            self._ev("build_end")
+        self._ev("prep")
+        sl.version = _C.memory_prep(self.memory, self.tcsr, i, x["src"], x["dst"], x["neg"], x["ts"], cfg.fanout,
+                                    samp, None, sl.mem[:m], sl.mem_ts[:m],
+                                    sl.mail[:m] if sl.mail is not None else None,
+                                    sl.mail_ts[:m] if sl.mail_ts is not None else None, None)
+        self._ev("prep_end")
+        assert vb == sl.version, (vb, sl.version)
+        self._features(sl, samp)
+        cur.wait_stream(self.bstream)
+        self.versions[i] = sl.version
+        if not self.memory.double_buffer:
+            self._fetched = torch.cuda.Event()  # the state tables have been read for batch i
+            self._fetched.record()
 
     def _upd(self, i):
         n = self.inputs(i)["src"].numel()
@@ -480,8 +527,9 @@ class MemoryStage(_TimedOps):
             _C.gru_build_apply_commit(self.gru, self.memory, i, x["ts"], x["ef"], sl.mem, sl.mem_ts, cfg.fanout + 1,
                                       upd)
         else:
-            _C.gru_apply_commit(self.gru, self.memory, i, n, sl.mem, cfg.fanout + 1, upd, sl.ws,
-                                snap_h=sl.h[: 2 * n] if sl.h is not None else None)
+            # direct build: h = S.mem[w] is the first M floats of the staged mail row (G14)
+            _C.gru_apply_commit(self.gru, self.memory, i, n, None if self.direct else sl.mem, cfg.fanout + 1, upd,
+                                sl.ws, snap_h=sl.h[: 2 * n] if sl.h is not None else None)
         if self.deferred:  # row F3: new mails from the committed memories of both endpoints
             x = self.inputs(i)
             _C.memory_mail_deferred(self.memory, i, x["src"], x["dst"], x["ts"], x["ef"], upd["nodes"], upd["winner"],
@@ -578,7 +626,7 @@ class MemoryStage(_TimedOps):
             return
         main = torch.cuda.current_stream()
         if getattr(self, "side", None) is None or self.side.device != main.device:
-            self.side = torch.cuda.Stream(device=main.device)
+            self.side = torch.cuda.Stream(device=main.device, priority=int(os.environ.get("MSPIPE_SIDE_PRIO", "0")))
         commits = {i for op, i in ops if op == "commit"}
         db = self.memory.double_buffer
         forked = joined = False

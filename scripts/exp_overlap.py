@@ -16,7 +16,7 @@ from synth import make_workload
 
 name = sys.argv[1] if len(sys.argv) > 1 else "wiki"
 kk = int(sys.argv[2]) if len(sys.argv) > 2 else None
-w = make_workload(name)
+w = make_workload(name, num_events=int(os.environ["EXP_EVENTS"]) if os.environ.get("EXP_EVENTS") else None)
 cfg = w["cfg"]
 k = cfg.staleness_k if kk is None else kk
 dev = torch.device("cuda:0")

@@ -534,7 +534,7 @@ def test_prep_build_equals_prep_then_build(dev, k):
     res = []
     for pb in (False, True):
         sc = StageConfig(cfg.num_nodes, cfg.mem_dim, cfg.edge_dim, cfg.time_dim, cfg.fanout, cfg.batch, k,
-                         fetch_mail=True, prep_build=pb)
+                         fetch_mail=True, prep_build=pb, direct_build=False)
         g = build_tcsr(cfg.num_nodes, w["src"], w["dst"], w["ts"], dev)
         st = MemoryStage(sc, w["params"], g, dev)
         assert st.fused
@@ -568,6 +568,56 @@ def test_prep_build_equals_prep_then_build(dev, k):
 
 
 # ------------------------------------------------------------------ row F2
+@pytest.mark.parametrize("name,k,schedule,E,prec", [("tiny", 0, "exact", 6_000, _C.FP32_3XTF32),
+                                                    ("lastfm", 1, "exact", 24_000, _C.FP32_3XTF32),
+                                                    ("wiki", 2, "grouped", 24_000, _C.FP32_3XTF32),
+                                                    ("wiki", 1, "exact", 24_000, _C.BF16)])
+def test_direct_build_equals_snapshot_build(dev, name, k, schedule, E, prec):
+    """mspipe_memory_winners + mspipe_message_build_tables (the build reads the
+    state tables of the fetched version, concurrently with the dedup-less
+    mspipe_memory_prep) leave the same GEMM operand images, commit rows and
+    final state as mspipe_memory_prep + mspipe_message_build from the snapshot
+    rows, bit for bit; and the direct path equals the oracle (versions, mem_ts
+    bit-exact, memory within 1e-4 row-relative; bf16: 2e-2)."""
+    w = make_workload(name, seed=9, num_events=E)
+    cfg = w["cfg"]
+    res = []
+    for direct in (False, True):
+        sc = StageConfig(cfg.num_nodes, cfg.mem_dim, cfg.edge_dim, cfg.time_dim, cfg.fanout, cfg.batch, k,
+                         schedule=schedule, fetch_mail=True, direct_build=direct, precision=prec)
+        g = build_tcsr(cfg.num_nodes, w["src"], w["dst"], w["ts"], dev)
+        st = MemoryStage(sc, w["params"], g, dev)
+        assert st.fused and st.direct == direct
+        t = {kk: _t(w[kk], dev) for kk in ("src", "dst", "ts", "neg", "ef")}
+        st.bind_resident(t["src"], t["dst"], t["ts"], t["neg"], t["ef"])
+        ops = st.step_ops()
+        for o in ops[:-1]:
+            st.run_ops(o)
+        torch.cuda.synchronize()
+        last = max(i for o, i in ops[-1] if o == "commit")
+        sl = st._slot(last)
+        U = int(sl.dd["num"].item())
+        extra = (sl.uts[:U].cpu().numpy(), sl.umail[:U].cpu().numpy(), sl.dd["nodes"][:U].cpu().numpy())
+        st.run_ops(ops[-1])
+        torch.cuda.synchronize()
+        _C.check()
+        res.append((U, extra, st.memory.mem.cpu().numpy(), st.memory.mem_ts.cpu().numpy(),
+                    st.memory.mail.cpu().numpy(), dict(st.versions)))
+    (ua, ea, ma, ta, la, va), (ub, eb, mb, tb, lb, vb) = res
+    assert ua == ub and va == vb
+    # the last batch's staged commit rows (ts, mail), winners, and the final state, bit for bit
+    assert all(np.array_equal(x, y) for x, y in zip(ea, eb))
+    assert np.array_equal(ma, mb) and np.array_equal(ta, tb) and np.array_equal(la, lb)
+    ref, vers = oracle.run_stream(cfg.num_nodes, w["src"], w["dst"], w["ts"], w["ef"], w["params"], cfg.batch, k,
+                                  schedule, fanout=cfg.fanout)
+    assert [vb[i] for i in range(1, len(vers) + 1)] == vers.tolist()
+    assert np.array_equal(tb, ref["mem_ts"])
+    rel = (np.linalg.norm(mb.astype(np.float64) - ref["mem"], axis=1) /
+           np.maximum(np.linalg.norm(ref["mem"], axis=1), 1e-3))
+    print(f"{name} k={k} {schedule} direct build: row-rel max {rel.max():.3g}")
+    assert rel.max() <= (2e-2 if prec == _C.BF16 else 1e-4)
+
+
 @pytest.mark.parametrize("name,E,fused", [("gdelt", 30_000, True), ("gdelt", 30_000, False), ("tiny", None, True)])
 def test_feature_fetch_equals_oracle(dev, name, E, fused):
     """F2 inside the stage (its own stream, forked after the sampler): node-feature
