@@ -1237,11 +1237,11 @@ constexpr int kMaxChunks = 8;  // 8 x 64 TMEM columns = 512 (the whole TMEM of t
 
 // co-resident clusters of S CTAs of k_gru_tc (cached per S; env MSPIPE_TC_CLUSTERS overrides)
 static int64_t gru_tc_clusters(int S, bool bf16) {
+  const int forced = env_int("MSPIPE_TC_CLUSTERS", 0);  // experiments: read at every launch
+  if (forced > 0) return forced;
   static int64_t cache[2][17] = {};
   int64_t& c = cache[bf16 ? 1 : 0][S & 15];
   if (c > 0) return c;
-  const int forced = env_int("MSPIPE_TC_CLUSTERS", 0);
-  if (forced > 0) return c = forced;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)S, 1, 1);
   cfg.blockDim = dim3(tc::kThreads);

@@ -17,6 +17,12 @@
 namespace mspipe {
 
 constexpr int kPrepThreads = 512;
+// two blocks per SM (<= 64 registers): at GDELT's 12,000 roots the latency-bound
+// root warps need the occupancy (one block per SM ran the roots in ~5 waves), and
+// a k_prep block then still fits beside a k_gru_tc CTA
+#ifndef MSPIPE_PREP_MINB
+#define MSPIPE_PREP_MINB 2
+#endif
 constexpr int kPrepWarps = kPrepThreads / 32;
 
 struct PrepArgs {
@@ -149,7 +155,7 @@ __device__ __forceinline__ void build_chunk(const PrepArgs& a, int32_t u, int32_
 }
 
 template <bool kSmem>
-__global__ void __launch_bounds__(kPrepThreads) k_prep(PrepArgs a) {
+__global__ void __launch_bounds__(kPrepThreads, MSPIPE_PREP_MINB) k_prep(PrepArgs a) {
   extern __shared__ int32_t sscratch[];
   pdl_begin();
   if (threadIdx.x == 0) PPHASE(0);
