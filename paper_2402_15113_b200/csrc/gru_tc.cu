@@ -359,6 +359,7 @@ struct TcArgs {
   const int32_t* tdst;
   // GEMM: h (the GRU hidden input) is new_mail[u][0:M] (= S.mem[w], G14)
   int32_t h_from_mail;
+  int32_t cpb;  // K chunks per TMEM accumulator buffer (k_gru_tc, tf32)
 };
 
 // row index of the state S.mem[w] of pair (ev, role) in snap_mem (times M) /
@@ -575,6 +576,11 @@ __device__ __forceinline__ void commit_rows(const TcArgs& a, int32_t m0, int32_t
 // done, overlapping them with the epilogue; the K-split partials go through
 // two receive buffers (tile parity), so one cluster barrier per tile orders
 // every push after the owner's reads of two tiles before.
+#ifndef MSPIPE_PF_GEMM
+#define MSPIPE_PF_GEMM 0  // measured: no effect on the wiki step (24.9 vs 24.7 us)
+#endif
+constexpr bool kPfGemm = MSPIPE_PF_GEMM != 0;
+
 template <bool kBf>
 __global__ void __launch_bounds__(tc::kThreads, 1) k_gru_tc(TcArgs a) {
   using namespace tc;
@@ -613,7 +619,11 @@ __global__ void __launch_bounds__(tc::kThreads, 1) k_gru_tc(TcArgs a) {
   const int32_t nchunks = d.Kpad / (kBf ? kKC16 : kKC);
   const int32_t c0 = split * nchunks / S, c1 = (split + 1) * nchunks / S;
   const int32_t nc = c1 - c0;  // tf32: <= kMaxChunks (host picks S >= nchunks / kMaxChunks)
-  const uint32_t tcols = kBf ? 64u : (nc <= 2 ? 128u : (nc <= 4 ? 256u : 512u));
+  // tf32: K chunk ci accumulates into TMEM buffer ci / cpb (cpb chunks per
+  // 64-column buffer; 1 unless the K range exceeds kMaxChunks buffers)
+  const int cpb = a.cpb > 0 ? a.cpb : 1;
+  const int nbuf = (nc + cpb - 1) / cpb;
+  const uint32_t tcols = kBf ? 64u : (nbuf <= 2 ? 128u : (nbuf <= 4 ? 256u : 512u));
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
@@ -642,6 +652,14 @@ __global__ void __launch_bounds__(tc::kThreads, 1) k_gru_tc(TcArgs a) {
     bulk_g2s(st, reinterpret_cast<const char*>(a.xbuf) + ((int64_t)mt_l * nchunks + c0 + ci) * AB, AB, &full[s]);
     bulk_g2s(st + AB, reinterpret_cast<const char*>(a.wtc) + ((int64_t)jt_l * nchunks + c0 + ci) * BB, BB, &full[s]);
   };
+  // L2 warm-up of a tile's chunks beyond the stage ring (their bulk copies
+  // wait for MMAs to free a stage; by then they hit L2)
+  auto warm_tile = [&](int32_t mt_l, int jt_l) {
+    for (int ci = kStages; ci < nc; ++ci) {
+      l2_prefetch(reinterpret_cast<const char*>(a.xbuf) + ((int64_t)mt_l * nchunks + c0 + ci) * AB, AB);
+      l2_prefetch(reinterpret_cast<const char*>(a.wtc) + ((int64_t)jt_l * nchunks + c0 + ci) * BB, BB);
+    }
+  };
   int pre = 0;  // chunks of the current tile the loader already issued (at the previous tile's end)
   int64_t ti = 0;
   for (int64_t q = blockIdx.y; q < tiles; q += gridDim.y, ++ti) {
@@ -650,6 +668,7 @@ __global__ void __launch_bounds__(tc::kThreads, 1) k_gru_tc(TcArgs a) {
     const int32_t m0 = mt * kM;
     float4* recv = recv2 + (ti & 1) * (kRecvBytes / 16);
     if (warp == 0 && lane == 0) {
+      if (ti == 0 && kPfGemm) warm_tile(mt, jt);
       for (int ci = pre; ci < nc; ++ci) load_chunk(ti, mt, jt, ci);
     } else if (warp == 1 && lane == 0) {
       // MMA issuer.  Each K chunk accumulates into its OWN 64-column TMEM
@@ -674,11 +693,11 @@ __global__ void __launch_bounds__(tc::kThreads, 1) k_gru_tc(TcArgs a) {
         } else {
           const uint64_t da_hi = sw128_desc(base), da_lo = sw128_desc(base + kATile);
           const uint64_t db_hi = sw128_desc(base + kABlock), db_lo = sw128_desc(base + kABlock + kBTile);
-          const uint32_t tacc = tmem + (uint32_t)(ci * kN);
+          const uint32_t tacc = tmem + (uint32_t)((ci / cpb) * kN);
 #pragma unroll
           for (int kk = 0; kk < kKC / 8; ++kk) {
             const uint64_t adv = (uint64_t)(kk * 32) >> 4;  // 8 tf32 = 32 B along K inside the swizzle row
-            mma_tf32(tacc, da_lo + adv, db_hi + adv, kIdesc, kk != 0);
+            mma_tf32(tacc, da_lo + adv, db_hi + adv, kIdesc, (kk != 0 || ci % cpb != 0) ? 1u : 0u);
             mma_tf32(tacc, da_hi + adv, db_lo + adv, kIdesc, 1u);
             mma_tf32(tacc, da_hi + adv, db_hi + adv, kIdesc, 1u);
           }
@@ -726,8 +745,10 @@ __global__ void __launch_bounds__(tc::kThreads, 1) k_gru_tc(TcArgs a) {
     if (warp == 0 && lane == 0) {  // the stages are free: start the next tile's loads now
       pre = 0;
       const int64_t qn = q + gridDim.y;
-      if (qn < tiles)
+      if (qn < tiles) {
         for (; pre < nc && pre < kStages; ++pre) load_chunk(ti + 1, (int32_t)(qn / J), (int)(qn % J), pre);
+        if (kPfGemm) warm_tile((int32_t)(qn / J), (int)(qn % J));
+      }
     }
     const int m = warp * 32 + lane;
     const uint32_t tbase = tmem + ((uint32_t)(warp * 32) << 16);
@@ -735,10 +756,10 @@ __global__ void __launch_bounds__(tc::kThreads, 1) k_gru_tc(TcArgs a) {
     MSPIPE_TMEM_LD32(tbase, r0);
     MSPIPE_TMEM_LD32(tbase + 32, r1);
     tmem_wait_ld();
-    for (int ci = 1; ci < (kBf ? 1 : nc); ++ci) {
+    for (int bi = 1; bi < (kBf ? 1 : nbuf); ++bi) {
       uint32_t t0[32], t1[32];
-      MSPIPE_TMEM_LD32(tbase + ci * kN, t0);
-      MSPIPE_TMEM_LD32(tbase + ci * kN + 32, t1);
+      MSPIPE_TMEM_LD32(tbase + bi * kN, t0);
+      MSPIPE_TMEM_LD32(tbase + bi * kN + 32, t1);
       tmem_wait_ld();
 #pragma unroll
       for (int i = 0; i < 32; ++i) {
@@ -1266,15 +1287,11 @@ static int64_t gru_tc_clusters(int S, bool bf16) {
 int gru_tc_splits(int64_t max_rows, const GruDesc& d) {
   // K-split = cluster size.  Powers of two pack the GPCs (measured: 5-CTA
   // clusters of 1-CTA-per-SM blocks spill into a second wave, 4 do not).
-  static int forced = -1;
-  if (forced < 0) {
-    const char* e = getenv("MSPIPE_TC_SPLITS");  // debugging / experiments only
-    forced = e ? atoi(e) : 0;
-  }
+  const int forced = env_int("MSPIPE_TC_SPLITS", 0);  // experiments only: read at every launch
   const int nchunks = d.Kpad / (d.bf16 ? tc::kKC16 : tc::kKC);
   // tf32: one TMEM buffer per chunk; bf16: a single accumulator, no minimum
   int64_t s_min = d.bf16 ? 1 : (nchunks + kMaxChunks - 1) / kMaxChunks;
-  if (forced > 0) return (int)(forced > s_min ? forced : s_min);
+  if (forced > 0) return forced;  // below s_min the chunks share TMEM buffers (TcArgs::cpb)
   const int64_t tiles = ((max_rows + tc::kM - 1) / tc::kM) * gru_tc_jtiles(d);
   int64_t s = 1;
   while (s < 8 && tiles * s * 2 <= 2 * (int64_t)num_sms() && s * 2 <= nchunks / 2) s *= 2;
@@ -1330,6 +1347,11 @@ cudaError_t launch_gru_tc(const GruDesc& d, const float* wtc, float* xbuf, const
   }
   if (!(parts & kGruGemm)) return cudaSuccess;
   const int S = gru_tc_splits(max_rows, d);
+  if (!d.bf16) {
+    const int nchunks = d.Kpad / tc::kKC;
+    const int nc_max = (nchunks + S - 1) / S;
+    a.cpb = (nc_max + kMaxChunks - 1) / kMaxChunks;
+  }
   // persistent grid: as many S-CTA clusters as are co-resident (one CTA per
   // SM: the stage ring fills shared memory), at most one per tile of the bound
   const int64_t max_tiles = mtiles * gru_tc_jtiles(d);

@@ -41,6 +41,36 @@ __device__ __forceinline__ void pdl_begin() {
   asm volatile("griddepcontrol.wait;\n" ::: "memory");
 }
 
+// ---- L2 warm-up --------------------------------------------------------
+// cp.async.bulk.prefetch.L2 of read-only tables a latency-bound kernel is about
+// to probe: the dependent probes (T-CSR rows, state rows) then hit L2 instead
+// of HBM.  Grid-wide: the ranges are cut into 32 KB chunks, one bulk prefetch
+// per (thread, chunk); each range's tail below 16 bytes is skipped.
+struct PfRange {
+  const void* p;
+  int64_t bytes;
+};
+constexpr int kMaxPf = 6;
+__device__ __forceinline__ void l2_prefetch(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(p), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void l2_prefetch_ranges(const PfRange* r, int n, int64_t tid, int64_t nthreads) {
+  constexpr int64_t kChunk = 32768;
+  int64_t first = 0;  // global chunk index of range i's first chunk
+  for (int i = 0; i < n; ++i) {
+    const int64_t nb = r[i].bytes & ~int64_t(15);
+    const int64_t chunks = (nb + kChunk - 1) / kChunk;
+    int64_t g = tid;
+    if (g < first) g += (first - g + nthreads - 1) / nthreads * nthreads;
+    for (; g < first + chunks; g += nthreads) {
+      const int64_t off = (g - first) * kChunk;
+      const int64_t len = nb - off < kChunk ? nb - off : kChunk;
+      l2_prefetch(static_cast<const char*>(r[i].p) + off, (uint32_t)len);
+    }
+    first += chunks;
+  }
+}
+
 // Time encoding cos(x), x = fmaf(omega, dt, phi) (G2, G22).  With raw Δt the
 // argument reaches 10^6..10^7, where cosf takes its slow (Payne-Hanek, local
 // memory) reduction path; reduce x mod 2π in double instead (two-term 2π,

@@ -178,6 +178,9 @@ def test_update_teacher_forced(dev, name, i, E, precision, fused):
     mail = upd["mail"][:U].cpu().numpy()
     assert np.array_equal(mail[:, :Dm], ref["mail"])  # copies of snapshot rows + ef
     assert (mail[:, Dm:] == 0).all()
+    g64, o64 = upd["mem"][:U].cpu().numpy().astype(np.float64), ref["mem"].astype(np.float64)
+    print(f"{name} i={i} fused={fused}: h' max abs err {np.abs(g64 - o64).max():.3g}, "
+          f"max err / (1e-4|o| + 1e-6) {(np.abs(g64 - o64) / (1e-4 * np.abs(o64) + 1e-6)).max():.3g}")
     ok, err = _close(upd["mem"][:U].cpu().numpy(), ref["mem"])
     assert ok, f"GRU mismatch max abs {err}"
     # A3 fetch: copied rows are the state rows of the subgraph ids (pads zero)
