@@ -828,3 +828,60 @@ def test_gemm_build_path_equals_oracle(dev, name, k, E):
     Dm = cfg.mail_dim  # mail = [s_w | s_o | e]: memory values, so within the fp32 tolerance
     ok, err = _close(st.memory.mail.cpu().numpy()[:, :Dm], ref["mail"], rtol=1e-4, atol=1e-5)
     assert ok, err
+
+
+# ------------------------------------------------- sizes and degenerate batches
+def _run_stream(dev, w, B, k, schedule="exact", **kw):
+    cfg = w["cfg"]
+    sc = StageConfig(cfg.num_nodes, cfg.mem_dim, cfg.edge_dim, cfg.time_dim, cfg.fanout, B, k, schedule=schedule,
+                     **kw)
+    g = build_tcsr(cfg.num_nodes, w["src"], w["dst"], w["ts"], dev)
+    st = MemoryStage(sc, w["params"], g, dev)
+    t = {kk: _t(w[kk], dev) for kk in ("src", "dst", "ts", "neg", "ef")}
+    st.bind_resident(t["src"], t["dst"], t["ts"], t["neg"], t["ef"])
+    st.run()
+    torch.cuda.synchronize()
+    _C.check()
+    ref, vers = oracle.run_stream(cfg.num_nodes, w["src"], w["dst"], w["ts"], w["ef"], w["params"], B, k, schedule,
+                                  fanout=cfg.fanout)
+    assert [st.versions[i] for i in range(1, len(vers) + 1)] == vers.tolist()
+    assert np.array_equal(st.memory.mem_ts.cpu().numpy(), ref["mem_ts"])
+    assert np.array_equal(st.memory.mail_ts.cpu().numpy(), ref["mail_ts"])
+    gm, om = st.memory.mem.cpu().numpy().astype(np.float64), ref["mem"].astype(np.float64)
+    rel = np.linalg.norm(gm - om, axis=1) / np.maximum(np.linalg.norm(om, axis=1), 1e-3)
+    assert rel.max() <= 1e-4, rel.max()
+    ok, err = _close(st.memory.mail.cpu().numpy()[:, :cfg.mail_dim], ref["mail"], rtol=1e-4, atol=1e-5)
+    assert ok, err
+    return rel.max()
+
+
+@pytest.mark.parametrize("clusters", [0, 1, 3])
+def test_max_batch_ragged_tail_and_tile_loop(dev, clusters, monkeypatch):
+    """The largest batch the fused prep takes (B = 8192: U up to 16,384 GEMM rows,
+    up to 128 M tiles x 7 hidden tiles) on a GDELT-shaped stream with a ragged
+    last batch, k = 1; with the persistent GEMM forced onto 1 or 3 clusters, one
+    cluster walks dozens of tiles (stage phases, the early loads of the next
+    tile and the two receive buffers all cycle).  Equals the oracle."""
+    if clusters:
+        monkeypatch.setenv("MSPIPE_TC_CLUSTERS", str(clusters))
+    w = make_workload("gdelt", seed=5, num_events=3 * 8192 + 17)
+    rel = _run_stream(dev, w, 8192, 1)
+    print(f"B=8192 clusters={clusters or 'auto'}: row-rel max {rel:.3g}")
+
+
+def test_degenerate_batches(dev):
+    """Batches whose events all repeat one pair (U = 2), self-loops (a node is
+    both endpoints: one winner per event), a node hit by every event of a batch
+    (LastFM's hot node at its extreme), and a one-event last batch; k = 0 and 2."""
+    cfg = CONFIGS["tiny"]
+    B = 64
+    src = np.concatenate([np.full(B, 3), np.arange(B) % 7, np.full(B, 5), np.arange(B) + 100, [9]]).astype(np.int32)
+    dst = np.concatenate([np.full(B, 4), np.arange(B) % 7, (np.arange(B) * 13) % 997, np.full(B, 100), [9]])
+    dst = dst.astype(np.int32)
+    E = len(src)
+    ts = np.floor(np.cumsum(np.random.default_rng(3).exponential(0.7, E))).astype(np.float64)
+    neg = np.random.default_rng(4).integers(0, cfg.num_nodes, E).astype(np.int32)
+    w = dict(cfg=cfg, src=src, dst=dst, ts=ts, neg=neg, ef=edge_features(7, 0, E, cfg.edge_dim),
+             params=gru_params(cfg.mem_dim, cfg.mail_dim, cfg.time_dim))
+    for k in (0, 2):
+        _run_stream(dev, w, B, k)
