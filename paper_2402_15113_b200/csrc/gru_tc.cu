@@ -70,6 +70,18 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+// wait with cluster-scope acquire: the phase was completed by st.async bytes from other CTAs
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAITC_%=:\n"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra.uni WAITC_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
 __device__ __forceinline__ void fence_barrier_init() {
   asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
 }
@@ -135,8 +147,15 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
         "=r"(r[29]), "=r"(r[30]), "=r"(r[31])                                                               \
       : "r"(taddr))
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
+#ifndef MSPIPE_CLUSTER_FENCE
+#define MSPIPE_CLUSTER_FENCE 0
+#endif
 __device__ __forceinline__ void cluster_sync_all() {
+#if MSPIPE_CLUSTER_FENCE  // timing experiment only: no release (DSMEM visibility not guaranteed)
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+#else
   asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+#endif
 }
 __device__ __forceinline__ uint32_t cluster_rank() {
   uint32_t r;
@@ -154,6 +173,17 @@ __device__ __forceinline__ const void* mapa_generic(const void* p, uint32_t rank
   asm volatile("mapa.u64 %0, %1, %2;\n" : "=l"(r) : "l"(reinterpret_cast<uint64_t>(p)), "r"(rank));
   return reinterpret_cast<const void*>(r);
 }
+// asynchronous remote store whose bytes complete a transaction on the
+// destination CTA's mbarrier (remote_bar: mapa'd address of that barrier)
+__device__ __forceinline__ void st_async_f4(uint32_t addr, float x, float y, float z, float w, uint32_t remote_bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.f32 [%0], {%1,%2,%3,%4}, [%5];\n" ::"r"(addr),
+               "f"(x), "f"(y), "f"(z), "f"(w), "r"(remote_bar)
+               : "memory");
+}
+__device__ __forceinline__ void cluster_arrive_relaxed() {
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory"); }
 __device__ __forceinline__ void st_dsmem_f4(uint32_t addr, float x, float y, float z, float w) {
   asm volatile("st.shared::cluster.v4.f32 [%0], {%1,%2,%3,%4};\n" ::"r"(addr), "f"(x), "f"(y), "f"(z), "f"(w)
                : "memory");
@@ -485,6 +515,61 @@ __global__ void __launch_bounds__(256) k_build_x(TcArgs a) {
   }
 }
 
+// A5, one warp per winner row u < U (no padding rows: rows >= U of the last M
+// tile only feed output rows the epilogue drops): every lane issues the loads
+// of its column in all kRowChunks chunks in one round, then converts and stores.
+constexpr int kRowChunks = 20;  // Kpad / 32 <= 20 (K <= 640); else k_build_x
+__global__ void __launch_bounds__(256) k_build_rows(TcArgs a) {
+  pdl_begin();
+  const GruDesc& d = a.d;
+  const int32_t U = __ldg(a.num_unique);
+  const int32_t nchunks = d.Kpad / tc::kKC;
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int32_t M = d.M;
+  for (int64_t u = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; u < U; u += nwarps) {
+    const int32_t p = __ldg(a.winner + u);
+    const int32_t ev = p >> 1, role = p & 1;
+    const int64_t rw = snap_row(a, ev, role), ro = snap_row(a, ev, role ^ 1);
+    const float* sw = a.snap_mem + rw * M;
+    const float* so = a.snap_mem + ro * M;
+    const float* hrow = a.snap_h ? a.snap_h + (role ? a.B + ev : (int64_t)ev) * M : sw;
+    const double t_ev = __ldg(a.ts + ev), t_w = __ldg(a.snap_ts + rw);
+    float v[kRowChunks];
+#pragma unroll
+    for (int c = 0; c < kRowChunks; ++c) {
+      const int32_t k = c * tc::kKC + lane;
+      v[c] = 0.f;
+      if (c < nchunks) {
+        if (k < M) v[c] = __ldg(sw + k);
+        else if (k < 2 * M) v[c] = __ldg(so + (k - M));
+        else if (k < d.Dm) v[c] = __ldg(a.ef + (int64_t)ev * d.He + (k - 2 * M));
+        else if (k >= d.Dx && k < d.K) v[c] = __ldg(hrow + (k - d.Dx));
+      }
+    }
+    const float dt = (float)(t_ev - t_w);  // Δt (G4)
+    const int32_t mt = (int32_t)(u / tc::kM), row = (int32_t)(u % tc::kM);
+#pragma unroll
+    for (int c = 0; c < kRowChunks; ++c) {
+      if (c >= nchunks) break;
+      const int32_t k = c * tc::kKC + lane;
+      float x = v[c];
+      if (k >= d.Dm && k < d.Dx) {
+        const int q = k - d.Dm;
+        x = time_cos(fmaf(__ldg(d.time_w + q), dt, __ldg(d.time_b + q)));
+      }
+      if (k < a.mail_stride) a.out_mail[u * a.mail_stride + k] = k < d.Dm ? x : 0.f;
+      const float hi = tc::tf32_rna(x);
+      const float lo = tc::tf32_rna(x - hi);
+      char* blk = reinterpret_cast<char*>(a.xbuf) + ((int64_t)mt * nchunks + c) * tc::kABlock;
+      const uint32_t off = tc::sw128_off((uint32_t)row, (uint32_t)lane);
+      *reinterpret_cast<float*>(blk + off) = hi;
+      *reinterpret_cast<float*>(blk + tc::kATile + off) = lo;
+    }
+    if (lane == 0) a.out_ts[u] = t_ev;
+  }
+}
+
 // GRUCell gates (G5): r = σ(.), z = σ(.), n = tanh(x_n + r h_n), h' = (1 - z) n + z h.
 __device__ __forceinline__ float4 gates4(const float* pr, const float* pz, const float* pnx, const float* pnh,
                                          float4 h, int32_t cell) {
@@ -580,6 +665,16 @@ __device__ __forceinline__ void commit_rows(const TcArgs& a, int32_t m0, int32_t
 #define MSPIPE_PF_GEMM 0  // measured: no effect on the wiki step (24.9 vs 24.7 us)
 #endif
 constexpr bool kPfGemm = MSPIPE_PF_GEMM != 0;
+#ifndef MSPIPE_MAIL_PF
+#define MSPIPE_MAIL_PF 1
+#endif
+constexpr bool kMailPf = MSPIPE_MAIL_PF != 0;
+// K-split partials pushed with st.async completing bytes on the owner's
+// mbarrier (no cluster barrier between the pushes and the reduction)
+#ifndef MSPIPE_ASYNC_PUSH
+#define MSPIPE_ASYNC_PUSH 1
+#endif
+constexpr bool kAsyncPush = MSPIPE_ASYNC_PUSH != 0;
 
 template <bool kBf>
 __global__ void __launch_bounds__(tc::kThreads, 1) k_gru_tc(TcArgs a) {
@@ -593,6 +688,7 @@ __global__ void __launch_bounds__(tc::kThreads, 1) k_gru_tc(TcArgs a) {
   uint64_t* empty = full + kStages;
   uint64_t* acc_full = empty + kStages;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 1);
+  uint64_t* rfull = acc_full + 2;  // K-split partials of the tile received (st.async bytes)
   int32_t* rownode = reinterpret_cast<int32_t*>(smem + kStages * SB + 512);  // [128] node of each row
   float4* hbuf = reinterpret_cast<float4*>(smem + kStages * SB + 1024);  // [128 rows][kJ/4]
   float4* recv2 = reinterpret_cast<float4*>(smem + kStages * SB + 1024 + kHBufBytes);  // [2][kRecvBytes]
@@ -602,23 +698,18 @@ __global__ void __launch_bounds__(tc::kThreads, 1) k_gru_tc(TcArgs a) {
   const GruDesc& d = a.d;
   PHASE(9);
   pdl_begin();
+  // U (written by the previous step's prep) is a cold HBM read: it is consumed
+  // only after the setup and the first tile's speculative loads below
   const int32_t U = __ldg(a.num_unique);
   const int J = gru_tc_jtiles_dev(d);
   const int S = gridDim.x;
   const int split = blockIdx.x;
-  const int64_t mt_act = U > 0 ? (U + kM - 1) / kM : 0;
-  const int64_t tiles = mt_act * J;
   const int64_t cta_q = (int64_t)blockIdx.y * S + split;
   const int64_t n_cta = (int64_t)gridDim.y * S;
-  if (a.save_num && cta_q == 0 && threadIdx.x == 0) *a.save_num = U;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if ((int64_t)blockIdx.y >= tiles) {  // no tile for this cluster (uniform across it)
-    if (a.cu.stamp && warp >= 2) catch_up(a, cta_q * 2 + (warp - 2), n_cta * 2, lane);
-    return;
-  }
   const int32_t nchunks = d.Kpad / (kBf ? kKC16 : kKC);
   const int32_t c0 = split * nchunks / S, c1 = (split + 1) * nchunks / S;
-  const int32_t nc = c1 - c0;  // tf32: <= kMaxChunks (host picks S >= nchunks / kMaxChunks)
+  const int32_t nc = c1 - c0;  // tf32: <= kMaxChunks buffers of cpb chunks
   // tf32: K chunk ci accumulates into TMEM buffer ci / cpb (cpb chunks per
   // 64-column buffer; 1 unless the K range exceeds kMaxChunks buffers)
   const int cpb = a.cpb > 0 ? a.cpb : 1;
@@ -631,6 +722,7 @@ __global__ void __launch_bounds__(tc::kThreads, 1) k_gru_tc(TcArgs a) {
       mbar_init(&empty[s], 1);
     }
     mbar_init(acc_full, 1);
+    mbar_init(rfull, 1);
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc(tmem_slot, tcols);
@@ -638,6 +730,9 @@ __global__ void __launch_bounds__(tc::kThreads, 1) k_gru_tc(TcArgs a) {
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  // kAsyncPush: the peers may target rfull only once it is initialised; the
+  // matching wait comes right before this CTA's first push (long satisfied)
+  if (kAsyncPush && S > 1) cluster_arrive_relaxed();
   const uint32_t tmem = *tmem_slot;
   const int rank = S > 1 ? (int)cluster_rank() : 0;
 
@@ -660,13 +755,29 @@ __global__ void __launch_bounds__(tc::kThreads, 1) k_gru_tc(TcArgs a) {
       l2_prefetch(reinterpret_cast<const char*>(a.wtc) + ((int64_t)jt_l * nchunks + c0 + ci) * BB, BB);
     }
   };
-  int pre = 0;  // chunks of the current tile the loader already issued (at the previous tile's end)
+  // the cluster's first tile (q = blockIdx.y) is issued before U is known: the
+  // workspace holds every M tile of the 2B bound, so the reads are in bounds
+  int pre = 0;  // chunks of the current tile the loader already issued
+  if (warp == 0 && lane == 0)
+    for (; pre < nc && pre < kStages; ++pre) load_chunk(0, (int32_t)(blockIdx.y / J), (int)(blockIdx.y % J), pre);
+  const int64_t mt_act = U > 0 ? (U + kM - 1) / kM : 0;
+  const int64_t tiles = mt_act * J;
+  if (a.save_num && cta_q == 0 && threadIdx.x == 0) *a.save_num = U;
+  if ((int64_t)blockIdx.y >= tiles) {  // no tile for this cluster (uniform across it)
+    if (warp == 0 && lane == 0)
+      for (int s = 0; s < pre; ++s) mbar_wait(&full[s], 0u);  // drain the speculative copies
+    if (a.cu.stamp && warp >= 2) catch_up(a, cta_q * 2 + (warp - 2), n_cta * 2, lane);
+    if (kAsyncPush && S > 1) cluster_wait();
+    __syncthreads();
+    if (warp == 2) tmem_dealloc(tmem, tcols);
+    return;
+  }
   int64_t ti = 0;
   for (int64_t q = blockIdx.y; q < tiles; q += gridDim.y, ++ti) {
     const int32_t mt = (int32_t)(q / J);
     const int jt = (int)(q % J);
     const int32_t m0 = mt * kM;
-    float4* recv = recv2 + (ti & 1) * (kRecvBytes / 16);
+    float4* recv = recv2 + (kAsyncPush ? 0 : (ti & 1)) * (kRecvBytes / 16);
     if (warp == 0 && lane == 0) {
       if (ti == 0 && kPfGemm) warm_tile(mt, jt);
       for (int ci = pre; ci < nc; ++ci) load_chunk(ti, mt, jt, ci);
@@ -711,6 +822,14 @@ __global__ void __launch_bounds__(tc::kThreads, 1) k_gru_tc(TcArgs a) {
       // row, or the staged mail row, G13/G14) of the rows this CTA will
       // finalise, 4 hidden units per item
       const int rb = rank * kM / S, re = (rank + 1) * kM / S;
+      if (kMailPf && a.commit_mem && a.new_mail) {
+        // warm the commit epilogue's mail-row slices (staged by k_build_x a step ago) into L2
+        const int Q = (int)(a.mail_stride / 4);
+        const int cq0 = jt * Q / J, nq = (jt + 1) * Q / J - cq0;
+        for (int mm = rb + (int)threadIdx.x - 64; mm < re; mm += 64)
+          if (m0 + mm < U && nq > 0)
+            l2_prefetch(a.new_mail + ((int64_t)(m0 + mm) * Q + cq0) * 4, (uint32_t)nq * 16u);
+      }
       for (int it = threadIdx.x - 64; it < (re - rb) * (kJ / 4); it += 64) {
         const int mm = rb + it / (kJ / 4), qq = it % (kJ / 4);
         const int32_t u = m0 + mm, j0 = jt * kJ + qq * 4;
@@ -777,6 +896,20 @@ __global__ void __launch_bounds__(tc::kThreads, 1) k_gru_tc(TcArgs a) {
       const int R = kM / S;
       const int owner = m / R, lm = m % R;
       const uint32_t dst = mapa(smem_u32(recv) + (uint32_t)((rank * R + lm) * (kN / 4)) * 16u, (uint32_t)owner);
+      if (kAsyncPush) {
+        if (ti == 0) cluster_wait();  // every rfull of the cluster is initialised
+        if (threadIdx.x == 0) mbar_arrive_expect_tx(rfull, (uint32_t)(kM * kN * 4));  // S x R rows x kN floats
+        const uint32_t rbar = mapa(smem_u32(rfull), (uint32_t)owner);
+#pragma unroll
+        for (int c4 = 0; c4 < 8; ++c4) {
+          st_async_f4(dst + 16u * (uint32_t)(c4 ^ (lm & 15)), __uint_as_float(r0[4 * c4]),
+                      __uint_as_float(r0[4 * c4 + 1]), __uint_as_float(r0[4 * c4 + 2]), __uint_as_float(r0[4 * c4 + 3]),
+                      rbar);
+          st_async_f4(dst + 16u * (uint32_t)((8 + c4) ^ (lm & 15)), __uint_as_float(r1[4 * c4]),
+                      __uint_as_float(r1[4 * c4 + 1]), __uint_as_float(r1[4 * c4 + 2]), __uint_as_float(r1[4 * c4 + 3]),
+                      rbar);
+        }
+      } else
 #pragma unroll
       for (int c4 = 0; c4 < 8; ++c4) {
         st_dsmem_f4(dst + 16u * (uint32_t)(c4 ^ (lm & 15)), __uint_as_float(r0[4 * c4]), __uint_as_float(r0[4 * c4 + 1]),
@@ -785,6 +918,7 @@ __global__ void __launch_bounds__(tc::kThreads, 1) k_gru_tc(TcArgs a) {
                     __uint_as_float(r1[4 * c4 + 1]), __uint_as_float(r1[4 * c4 + 2]), __uint_as_float(r1[4 * c4 + 3]));
       }
     }
+    PHASE(1);
     tc_fence_before();
     __syncthreads();  // hbuf complete; every TMEM read of this tile done (the next tile's MMAs may start)
     PHASE(5);
@@ -809,7 +943,17 @@ __global__ void __launch_bounds__(tc::kThreads, 1) k_gru_tc(TcArgs a) {
       }
       if (a.commit_mem) commit_rows(a, m0, U, 0, kM, jt, J, rownode);
     } else {
-      cluster_sync_all();  // all pushes into recv are visible
+      if (kAsyncPush) {
+        mbar_wait_cluster(rfull, (uint32_t)(ti & 1));  // all S x R partial rows have landed
+      } else {
+#ifdef MSPIPE_PHASES
+        asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+        PHASE(7);
+        asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+#else
+        cluster_sync_all();  // all pushes into recv are visible
+#endif
+      }
       PHASE(6);
       const int R = kM / S;
       const int rb = rank * R;
@@ -831,7 +975,6 @@ __global__ void __launch_bounds__(tc::kThreads, 1) k_gru_tc(TcArgs a) {
             acc[g].z += v.z;
             acc[g].w += v.w;
           }
-        if (it == threadIdx.x) PHASE(7);
         float pr[4], pz[4], pnx[4], pnh[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
@@ -847,6 +990,8 @@ __global__ void __launch_bounds__(tc::kThreads, 1) k_gru_tc(TcArgs a) {
       PHASE(8);
     }
     __syncthreads();  // hbuf / rownode / sbias are rewritten by the next tile's prefetch
+    // single receive buffer: every CTA's reads of it precede the next tile's pushes
+    if (kAsyncPush && S > 1 && q + gridDim.y < tiles) cluster_sync_all();
   }
   if (warp == 2) {
     tc_fence_after();
@@ -1337,11 +1482,19 @@ cudaError_t launch_gru_tc(const GruDesc& d, const float* wtc, float* xbuf, const
   a.tdst = tab_dst;
   const int64_t max_rows = 2 * num_events;
   const int64_t mtiles = (max_rows + tc::kM - 1) / tc::kM;
-  if (parts & kGruBuild) {
+  if ((parts & kGruBuild) && !d.bf16 && d.Kpad / tc::kKC <= kRowChunks && env_int("MSPIPE_BUILD_ROWS", 0)) {
+    int64_t blocks = (max_rows * 32 + 255) / 256;  // one warp per row of the 2B bound (rows >= U exit)
+    const int64_t cap = (int64_t)num_sms() * env_int("MSPIPE_BUILD_BPS", 8);
+    if (blocks > cap) blocks = cap;
+    cudaError_t e = launch_k(k_build_rows, dim3((unsigned)blocks), dim3(256), 0, s, 1, a);
+    if (e != cudaSuccess) return e;
+  } else if (parts & kGruBuild) {
     const int64_t warps = mtiles * (d.Kpad / (d.bf16 ? tc::kKC16 : tc::kKC)) * tc::kM;
     int64_t blocks = (warps * 32 + 255) / 256;
     const int64_t cap = (int64_t)num_sms() * env_int("MSPIPE_BUILD_BPS", 8);
     if (blocks > cap) blocks = cap;
+    static int co = -1;
+    apply_carveout(k_build_x, co);
     cudaError_t e = launch_k(k_build_x, dim3((unsigned)blocks), dim3(256), 0, s, 1, a);
     if (e != cudaSuccess) return e;
   }

@@ -86,6 +86,15 @@ __device__ __forceinline__ float time_cos(float x) {
 bool pdl_enabled();  // env MSPIPE_PDL=1 enables (A/B experiments)
 // integer knob from the environment (experiments only; defaults are the tuned values)
 int env_int(const char* name, int def);
+// shared-memory carveout preference of a kernel (percent; env MSPIPE_CARVEOUT,
+// unset = the driver's choice), applied once per kernel
+template <typename F>
+inline void apply_carveout(F* kernel, int& applied) {
+  const int c = env_int("MSPIPE_CARVEOUT", -1);
+  if (c == applied) return;
+  applied = c;
+  (void)cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, c);
+}
 
 // cudaLaunchKernelEx with the PDL attribute (+ an optional (cx,1,1) cluster).
 template <typename... KArgs, typename... Args>

@@ -280,6 +280,9 @@ cudaError_t launch_prep(const Tcsr& g, const int32_t* src, const int32_t* dst, c
   int64_t blocks = (3 * num_events + kPrepWarps - 1) / kPrepWarps;
   const int64_t cap = (int64_t)num_sms() * env_int("MSPIPE_PREP_BPS", 4);
   if (blocks > cap) blocks = cap;
+  static int co0 = -1, co1 = -1;
+  apply_carveout(k_prep<false>, co0);
+  apply_carveout(k_prep<true>, co1);
   if (!a.dedup) return launch_k(k_prep<false>, dim3((unsigned)blocks), dim3(kPrepThreads), 0, s, 1, a);
   blocks += 1;  // block 0: dedup
   if (g.num_nodes <= kDedupSmemNodes && env_int("MSPIPE_PREP_SMEM", 1)) {

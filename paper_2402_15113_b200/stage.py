@@ -77,6 +77,11 @@ class StageConfig:
         return self.k >= 1 if self.double_buffer is None else bool(self.double_buffer)
 
 
+# timing diagnostics (scripts/exp_overlap.py): "prep" or "commit" runs only that half of every
+# step (results are meaningless); unset in every real run
+_DEBUG_ONLY = os.environ.get("MSPIPE_DEBUG_ONLY", "")
+
+
 def plan_versions(plan, nb):
     """v(i) = max(0, i - k_i) for a plan of paper staleness values k_i (row F1)."""
     return [max(0, i - int(plan[i - 1])) for i in range(1, nb + 1)]
@@ -631,6 +636,8 @@ class MemoryStage(_TimedOps):
         db = self.memory.double_buffer
         forked = joined = False
         for op, i in ops:
+            if op == "prep" and _DEBUG_ONLY == "commit":  # timing diagnostics only: the prep is not run
+                continue
             if op == "prep":
                 # every prep goes to the side stream, in order (preps of one handle
                 # share its scratch); a commit of this group waits for its own prep
@@ -648,6 +655,9 @@ class MemoryStage(_TimedOps):
                 # fetch (not its message build, which overlaps this GEMM)
                 if forked and not db:
                     main.wait_event(self._fetched)
+                if _DEBUG_ONLY == "prep":  # timing diagnostics only: the commit is not run
+                    self.memory.set_committed(i)
+                    continue
                 self.apply_commit(i)
             else:
                 self.update(i)

@@ -4,7 +4,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 os.environ["MSPIPE_LIB"] = "/tmp/libmspipe_dbg.so"  # before the package import
 from paper_2402_15113_b200.build import build
-dbg = build(force=True, extra_flags=["-DMSPIPE_PHASES"], out="/tmp/libmspipe_dbg.so")
+dbg = build(force=True, extra_flags=["-DMSPIPE_PHASES"] + os.environ.get("EXP_FLAGS", "").split(),
+            out="/tmp/libmspipe_dbg.so")
 os.environ["MSPIPE_LIB"] = dbg
 import numpy as np, torch
 from paper_2402_15113_b200 import MemoryStage, StageConfig, _C, build_tcsr
@@ -23,6 +24,15 @@ ops = st.step_ops()
 for i in range(20):
     st.run_ops(ops[i])
 torch.cuda.synchronize()
+if os.environ.get("EXP_COLD"):  # the recorded step alone (its prep skipped), after an L2 flush
+    import paper_2402_15113_b200.stage as stage_mod
+    flush = torch.empty(256 << 18, dtype=torch.float32, device=dev)
+    flush.fill_(1.0)
+    torch.cuda.synchronize()
+    stage_mod._DEBUG_ONLY = "commit"
+    st.run_ops(ops[20])
+    torch.cuda.synchronize()
+    stage_mod._DEBUG_ONLY = ""
 L = ctypes.CDLL(dbg)
 buf = np.zeros((8192, 10), np.uint64)
 print("copy rc", L.mspipe_debug_phases(buf.ctypes.data_as(ctypes.c_void_p), 8192))
@@ -31,10 +41,10 @@ used = buf[:, 9] > 0
 ph = buf[used].astype(np.int64)
 print("U", U, "CTAs recorded", used.sum())
 t0 = ph[:, 9].min()
-names = {9: "entry", 0: "setup", 2: "mma_done", 3: "acc_full", 4: "tmem_sum", 5: "sync", 6: "cluster1", 1: "mapa", 7: "dsmem_ld", 8: "end"}
+names = {9: "entry", 0: "setup", 2: "mma_done", 3: "acc_full", 4: "tmem_sum", 1: "pushed", 5: "sync", 7: "arrived", 6: "cluster1", 8: "end"}
 act = ph[:, 3] > 0
 print("active CTAs", act.sum())
-for k in [9, 0, 2, 3, 4, 5, 6, 1, 7, 8]:
+for k in [9, 0, 2, 3, 4, 1, 5, 7, 6, 8]:
     col = ph[act, k] - t0
     print(f"{names[k]:10s} min {col.min()/1e3:8.2f} med {np.median(col)/1e3:8.2f} max {col.max()/1e3:8.2f} us")
 dead = ~act

@@ -30,6 +30,14 @@ def run(overlap, db, fused=None, steps=300, warm=10, l2=True):
                      double_buffer=db, fused=fused)
     st = MemoryStage(sc, w["params"], g, dev)
     st.bind_resident(t["src"], t["dst"], t["ts"], t["neg"], t["ef"])
+    import paper_2402_15113_b200.stage as stage_mod
+    if stage_mod._DEBUG_ONLY == "commit":  # fill every slot with a real prep first (realistic U per commit)
+        stage_mod._DEBUG_ONLY = ""
+        for ops in st.step_ops()[:8]:
+            st.run_ops(ops, overlap=overlap)
+        torch.cuda.synchronize()
+        st.memory.reset()
+        stage_mod._DEBUG_ONLY = "commit"
     s = torch.cuda.Stream()
     graphs = [_C.StepGraph().capture(lambda: st.run_ops(ops, overlap=overlap), s) for ops in st.step_ops()]
     st.memory.reset()
@@ -55,6 +63,14 @@ def run(overlap, db, fused=None, steps=300, warm=10, l2=True):
 
 
 print(f"{name} k={k} B={cfg.batch}")
+if os.environ.get("EXP_HALVES"):
+    # each half of the step alone (stage._DEBUG_ONLY is read per run), then both
+    import paper_2402_15113_b200.stage as stage_mod
+    for only in ("prep", "commit", ""):
+        stage_mod._DEBUG_ONLY = only
+        m, md = run(True, True)
+        print(f"only={only or 'both':6s}: mean {m:6.2f} us  median {md:6.2f} us")
+    sys.exit(0)
 if os.environ.get("EXP_KNOBS"):
     # EXP_KNOBS="MSPIPE_CATCHUP=0,1,2;MSPIPE_PREP_SMEM=1,0": one knob varied at a time from the defaults
     for spec in os.environ["EXP_KNOBS"].split(";"):
