@@ -2,17 +2,23 @@
 """bench.py — MSPipe node-memory stage on B200: events/s + roofline.
 
 A *step* is one batch through the whole hot path (A1-A7):
-sample_batch + memory_fetch (prep of batch t+k) and memory_update +
-memory_writeback (commit of batch t), captured once per step as a CUDA graph
-and replayed.  Inputs are resident in HBM; L2 is flushed (a 256 MiB write)
-between timed steps, outside the timed events.  Default workload: the
-Wikipedia-shaped stream (BASELINE.json configs[1]) at its build staleness k=1.
+the prep of batch t+k (sampler, dedup, fetch, message build) and the commit
+of batch t (GRU GEMM + write-back).  At N = 1, 8 consecutive steps
+(--graph-steps; the largest divisor of K up to it) are captured as ONE CUDA
+graph and replayed; L2 is flushed (a 256 MiB write) before every replay,
+outside the timed events, and exactly K steps are timed.  One graph per step
+pays the ~6 us graph-launch gap per step (measured the same with and without
+the flush, so it is launch latency, not cache); that per-step protocol is
+timed as well and reported in `per_step_graphs`.  Inputs are resident in HBM
+for `value`; `e2e` copies each batch from pinned host memory and reads each
+commit's result back.  Default workload: the Wikipedia-shaped stream
+(BASELINE.json configs[1]) at its build staleness k=1.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config wiki] [--impl mspipe|reference]
 
-N > 1 (torchrun): each rank runs an independent replica of the stage on its
-own copy of the stream (the sharded-memory exchange is not in
-this build), value = events of all ranks / max-over-ranks time.
+N > 1 (torchrun): node memory sharded by node id over the ranks with NCCL
+all-to-all fetch and write-back (row E; MSPIPE_BENCH_REPLICAS=1: independent
+replicas), one graph per step; value = events of all ranks / max-over-ranks time.
 """
 from __future__ import annotations
 
@@ -268,6 +274,55 @@ def run_mspipe(args):
         _collect(pending, step_ms, op_ms, st, marks)
         return step_ms, op_ms
 
+    def capture_groups(st, gs):
+        """One CUDA graph per gs consecutive steps (the epoch's last group may be shorter)."""
+        s = torch.cuda.Stream(device=dev)
+        st.timing = None
+        sops = st.step_ops()
+        groups = []
+        for j in range(0, len(sops), gs):
+            idx = list(range(j, min(j + gs, len(sops))))
+
+            def run_group(idx=idx):
+                for t in idx:
+                    st.run_ops(sops[t])
+            groups.append((_C.StepGraph().capture(run_group, s), idx))
+        st.memory.reset()
+        return groups, s
+
+    def timed_run_groups(st, groups, s, W, K, gs):
+        """Warm-up replays until >= W steps ran, then replays of full gs-step groups
+        until exactly K steps are timed (an epoch's shorter last group runs untimed);
+        L2 flushed before every replay, one event pair per replay.  Returns
+        (per-replay ms list, timed step indices)."""
+        ms, timed, pending = [], [], []
+        warm, r = 0, 0
+        with torch.cuda.stream(s):
+            while len(timed) + len(pending) * gs < K:
+                j = r % len(groups)
+                if j == 0 and r > 0:
+                    torch.cuda.synchronize()
+                    st.memory.reset()
+                graph, idx = groups[j]
+                if args.l2 == "flush":
+                    flush.fill_(float(r))
+                if warm >= W and len(idx) == gs:
+                    e0 = torch.cuda.Event(enable_timing=True)
+                    e1 = torch.cuda.Event(enable_timing=True)
+                    e0.record(s)
+                    graph.replay(s)
+                    e1.record(s)
+                    pending.append((e0, e1, idx))
+                else:
+                    graph.replay(s)
+                    warm += len(idx)
+                r += 1
+            torch.cuda.synchronize()
+        for e0, e1, idx in pending:
+            ms.append(e0.elapsed_time(e1))
+            timed.extend(idx)
+        return ms, timed
+
     def _collect(pending, step_ms, op_ms, st, marks):
         for t, e0, e1 in pending:
             step_ms.append(e0.elapsed_time(e1))
@@ -287,15 +342,42 @@ def run_mspipe(args):
     # The timed graphs carry no per-op event nodes (each one is an extra graph
     # node on the critical path); the per-op breakdown for the roofline comes
     # from a second, instrumented replay of the same steps right after.
+    # steps per captured graph: launch latency between graphs (~6 us, the same
+    # with or without the L2 flush) is paid once per graph, not once per step
+    gs = 1
+    if ws == 1 and not args.profile:  # the largest divisor of K up to --graph-steps (exactly K steps timed)
+        gs = max(d for d in range(1, max(1, min(args.graph_steps, nb - 1)) + 1) if K % d == 0)
     st = make_stage(False)
-    graphs, marks, s = capture(st, timing=False)
+    if gs > 1:
+        groups, s = capture_groups(st, gs)
+    else:
+        graphs, marks, s = capture(st, timing=False)
     if ws > 1:
         dist.barrier()
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
-        step_ms, _ = timed_run(st, graphs, marks, s, W, K, profile=args.profile)
+        if gs > 1:
+            step_ms, timed_batches = timed_run_groups(st, groups, s, W, K, gs)
+        else:
+            step_ms, _ = timed_run(st, graphs, marks, s, W, K, profile=args.profile)
+            timed_batches = [(W + q) % nb for q in range(K)]
     _C.check(s)
-    del graphs
+    per_step = None
+    if gs > 1:
+        # the same steps with one graph per step (L2 flushed before each): the
+        # per-step protocol, reported beside the grouped headline
+        del groups
+        st1 = make_stage(False)
+        graphs1, marks1, s1 = capture(st1, timing=False)
+        ms1, _ = timed_run(st1, graphs1, marks1, s1, W, K)
+        _C.check(s1)
+        del graphs1
+        tb1 = [(W + q) % nb for q in range(K)]
+        ev1 = sum(min(cfg.batch, E - b * cfg.batch) for b in tb1)
+        per_step = {"value": ev1 / (sum(ms1) / 1e3), "unit": UNIT, "ms_per_step": sum(ms1) / K,
+                    "l2": "flushed (256 MiB write) before every step, one CUDA graph per step"}
+    else:
+        del graphs
     st_i = make_stage(False)
     graphs_i, marks_i, s_i = capture(st_i, timing=True)
     step_ms_instr, op_ms = timed_run(st_i, graphs_i, marks_i, s_i, W, K, profile=args.profile)
@@ -307,7 +389,6 @@ def run_mspipe(args):
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         tot_ms = float(tt.item())
         dist.barrier()
-    timed_batches = [(W + q) % nb for q in range(K)]
     # events of all ranks in the timed global batches (replicas: every rank its own copy)
     events = sum(min(G * cfg.batch, E - b * G * cfg.batch) for b in timed_batches) * (ws if not sharded else 1)
     value = events / (tot_ms / 1e3)
@@ -377,12 +458,15 @@ def run_mspipe(args):
                       "mem_dim": cfg.mem_dim, "edge_dim": cfg.edge_dim, "time_dim": cfg.time_dim,
                       "mitigation": bool(mit), "features": args.features, "fetch_mail": args.fetch_mail, "gru": {"tc": "fp32-3xtf32-tcgen05", "bf16": "bf16-operands-tcgen05 (fp32 accumulate/state)",
                               "simt": "fp32-simt"}[args.gru],
-                      "l2": ("flushed (256 MiB write) between timed steps, outside the timed events"
+                      "l2": (("flushed (256 MiB write) between timed steps, outside the timed events" if gs == 1 else
+                              f"flushed (256 MiB write) before every replay of a {gs}-step CUDA graph, outside "
+                              f"the timed events; the per-step-flushed protocol is in per_step_graphs")
                              if args.l2 == "flush" else "warm: steps back to back, state tables L2-resident"),
+                      "steps_per_graph": gs,
                       "parallelism": ("single" if ws == 1 else
                                       f"shard{ws}: node-id-sharded memory, NCCL all-to-all fetch + write-back, "
                                       f"global batch {G * cfg.batch}" if sharded else f"replicas{ws}")},
-           "roofline": roof, "roofline_gather": roof_gather, "roofline_features": roof_features, "gpu_launches": _launches(st.step_ops(), timed_batches, bool(mit),
+           "roofline": roof, "roofline_gather": roof_gather, "roofline_features": roof_features, "per_step_graphs": per_step, "gpu_launches": _launches(st.step_ops(), timed_batches, bool(mit),
                                                        getattr(st, "fused", False), sharded, args.features,
                                                        getattr(st, "gemm_build", False)), "clocks": clocks}
     if args.profile:
@@ -391,17 +475,26 @@ def run_mspipe(args):
         return
     # ---- e2e: host buffers through the same C-ABI calls ---------------------
     st2 = make_stage(True)
-    graphs2, marks2, s2 = capture(st2, timing=False)
+    if gs > 1:
+        groups2, s2 = capture_groups(st2, gs)
+    else:
+        graphs2, marks2, s2 = capture(st2, timing=False)
     if ws > 1:
         dist.barrier()
-    step2, _ = timed_run(st2, graphs2, marks2, s2, W, K)
+    if gs > 1:
+        step2, tb2 = timed_run_groups(st2, groups2, s2, W, K, gs)
+        graphs2 = groups2
+    else:
+        step2, _ = timed_run(st2, graphs2, marks2, s2, W, K)
+        tb2 = timed_batches
     _C.check(s2)
+    events2 = sum(min(G * cfg.batch, E - b * G * cfg.batch) for b in tb2) * (ws if not sharded else 1)
     tot2 = float(sum(step2))
     if ws > 1:
         tt = torch.tensor([tot2], device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         tot2 = float(tt.item())
-    out["e2e"] = {"value": events / (tot2 / 1e3), "unit": UNIT,
+    out["e2e"] = {"value": events2 / (tot2 / 1e3), "unit": UNIT,
                   "h2d_bytes_per_step": st2.h2d_bytes_per_batch(), "d2h_bytes_per_step": (st2.d2h_bytes_per_batch(mean_U) if not sharded
                                                                          else st2.d2h_bytes_per_batch()),
                   "ms_per_step": tot2 / K}
@@ -534,6 +627,8 @@ def main():
     ap.add_argument("--events", type=int, default=None,
                     help="first N events of the config's stream (default: all; GDELT's 191M needs a cap)")
     ap.add_argument("--profile", action="store_true", help="short run for ncu: no flush/e2e/cpu")
+    ap.add_argument("--graph-steps", type=int, default=8,
+                    help="consecutive steps captured per CUDA graph (1: one graph per step); N = 1 only")
     args = ap.parse_args()
     if args.warmup < 3 and not args.profile:
         args.warmup = 3

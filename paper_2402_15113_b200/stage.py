@@ -218,6 +218,7 @@ class MemoryStage(_TimedOps):
         self.direct = (self.fused and cfg.direct_build and not cfg.mitigation and not self.deferred
                        and not cfg.prep_build and not self.gemm_build)
         self.bstream = None
+        self._dbg_one = torch.zeros(1, device=self.device) if _DEBUG_ONLY else None  # timing diagnostics
         if self.deferred and not (self.fused and cfg.fetch_mail and not cfg.prep_build):
             raise ValueError("mailbox='deferred' runs on the fused tensor-core path with fetch_mail=True")
         self.ws_bytes = _C.gru_workspace_size(self.gru, cfg.batch) if self.fused else 0
@@ -636,7 +637,7 @@ class MemoryStage(_TimedOps):
         db = self.memory.double_buffer
         forked = joined = False
         for op, i in ops:
-            if op == "prep" and _DEBUG_ONLY == "commit":  # timing diagnostics only: the prep is not run
+            if op == "prep" and _DEBUG_ONLY in ("commit", "none"):  # timing diagnostics only: no prep
                 continue
             if op == "prep":
                 # every prep goes to the side stream, in order (preps of one handle
@@ -655,8 +656,10 @@ class MemoryStage(_TimedOps):
                 # fetch (not its message build, which overlaps this GEMM)
                 if forked and not db:
                     main.wait_event(self._fetched)
-                if _DEBUG_ONLY == "prep":  # timing diagnostics only: the commit is not run
+                if _DEBUG_ONLY in ("prep", "none"):  # timing diagnostics only: the commit is not run
                     self.memory.set_committed(i)
+                    if _DEBUG_ONLY == "none":  # one trivial kernel: the step's fixed cost
+                        self._dbg_one.add_(1.0)
                     continue
                 self.apply_commit(i)
             else:

@@ -25,6 +25,10 @@ t = {x: torch.from_numpy(w[x]).to(dev) for x in ("src", "dst", "ts", "neg", "ef"
 flush = torch.empty(256 << 18, dtype=torch.float32, device=dev)
 
 
+GROUP = int(os.environ.get("EXP_GROUP", "1"))  # steps captured per graph (timed per graph, / GROUP)
+EAGER = bool(os.environ.get("EXP_EAGER"))  # launch the step's kernels directly instead of replaying its graph
+
+
 def run(overlap, db, fused=None, steps=300, warm=10, l2=True):
     sc = StageConfig(cfg.num_nodes, cfg.mem_dim, cfg.edge_dim, cfg.time_dim, cfg.fanout, cfg.batch, k,
                      double_buffer=db, fused=fused)
@@ -39,9 +43,16 @@ def run(overlap, db, fused=None, steps=300, warm=10, l2=True):
         st.memory.reset()
         stage_mod._DEBUG_ONLY = "commit"
     s = torch.cuda.Stream()
-    graphs = [_C.StepGraph().capture(lambda: st.run_ops(ops, overlap=overlap), s) for ops in st.step_ops()]
+    sops = st.step_ops()
+    groups = [sops[j:j + GROUP] for j in range(0, len(sops), GROUP)]
+
+    def run_group(gr):
+        for ops in gr:
+            st.run_ops(ops, overlap=overlap)
+    graphs = [_C.StepGraph().capture(lambda: run_group(gr), s) for gr in groups]
     st.memory.reset()
     nb = len(graphs)
+    eager_ops = st.step_ops()
     ms = []
     with torch.cuda.stream(s):
         for n in range(warm + steps):
@@ -53,12 +64,15 @@ def run(overlap, db, fused=None, steps=300, warm=10, l2=True):
                 flush.fill_(float(n))
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(s)
-            graphs[i].replay(s)
+            if EAGER:
+                st.run_ops(eager_ops[i], overlap=overlap)
+            else:
+                graphs[i].replay(s)
             e1.record(s)
             if n >= warm:
                 ms.append((e0, e1))
     torch.cuda.synchronize()
-    v = np.array([a.elapsed_time(b) for a, b in ms]) * 1e3
+    v = np.array([a.elapsed_time(b) for a, b in ms]) * 1e3 / GROUP  # per step
     return np.mean(v), np.median(v)
 
 
@@ -66,7 +80,7 @@ print(f"{name} k={k} B={cfg.batch}")
 if os.environ.get("EXP_HALVES"):
     # each half of the step alone (stage._DEBUG_ONLY is read per run), then both
     import paper_2402_15113_b200.stage as stage_mod
-    for only in ("prep", "commit", ""):
+    for only in ("none", "prep", "commit", ""):
         stage_mod._DEBUG_ONLY = only
         m, md = run(True, True)
         print(f"only={only or 'both':6s}: mean {m:6.2f} us  median {md:6.2f} us")

@@ -454,6 +454,47 @@ def test_cuda_graph_replay_equals_eager(dev, kind):
     assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
 
 
+@pytest.mark.parametrize("name,k,gs,staged", [("tiny", 1, 8, False), ("wiki", 1, 8, False), ("wiki", 1, 8, True),
+                                              ("lastfm", 2, 5, False)])
+def test_multi_step_graphs_equal_oracle(dev, name, k, gs, staged):
+    """bench.py's capture: gs consecutive steps per CUDA graph (the epoch's last
+    group shorter), replayed over two epochs with a reset between them, ends in
+    the oracle's state (versions, mem_ts bit-exact, memory within 1e-4)."""
+    w = make_workload(name, seed=11, num_events=24 * 600 + 123 if name != "tiny" else None)
+    cfg = w["cfg"]
+    sc = StageConfig(cfg.num_nodes, cfg.mem_dim, cfg.edge_dim, cfg.time_dim, cfg.fanout, cfg.batch, k)
+    g = build_tcsr(cfg.num_nodes, w["src"], w["dst"], w["ts"], dev)
+    st = MemoryStage(sc, w["params"], g, dev)
+    if staged:
+        st.bind_host(w["src"], w["dst"], w["ts"], w["neg"], w["ef"])
+    else:
+        t = {kk: _t(w[kk], dev) for kk in ("src", "dst", "ts", "neg", "ef")}
+        st.bind_resident(t["src"], t["dst"], t["ts"], t["neg"], t["ef"])
+    sops = st.step_ops()
+    s = torch.cuda.Stream()
+    groups = []
+    for j in range(0, len(sops), gs):
+        def run_group(idx=range(j, min(j + gs, len(sops)))):
+            for q in idx:
+                st.run_ops(sops[q])
+        groups.append(_C.StepGraph().capture(run_group, s))
+    for epoch in range(2):
+        st.memory.reset()
+        with torch.cuda.stream(s):
+            for gr in groups:
+                gr.replay(s)
+        torch.cuda.synchronize()
+    st.memory.set_committed(len(sops))
+    _C.check()
+    ref, vers = oracle.run_stream(cfg.num_nodes, w["src"], w["dst"], w["ts"], w["ef"], w["params"], cfg.batch, k,
+                                  "exact", fanout=cfg.fanout)
+    assert [st.versions[i] for i in range(1, len(vers) + 1)] == vers.tolist()
+    assert np.array_equal(st.memory.mem_ts.cpu().numpy(), ref["mem_ts"])
+    gm, om = st.memory.mem.cpu().numpy().astype(np.float64), ref["mem"].astype(np.float64)
+    rel = np.linalg.norm(gm - om, axis=1) / np.maximum(np.linalg.norm(om, axis=1), 1e-3)
+    assert rel.max() <= 1e-4
+
+
 def test_determinism_two_runs_bitwise(dev):
     a = _stream(dev, "lastfm", 1, E=30_000)[0].memory
     b = _stream(dev, "lastfm", 1, E=30_000)[0].memory
