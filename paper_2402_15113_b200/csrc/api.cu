@@ -106,6 +106,28 @@ mspipe_status mspipe_sample_batch(const mspipe_tcsr* g, const int32_t* src, cons
 
 static mspipe_status nccl_warmup(mspipe_memory* st);
 
+// a library-owned stream (one per device, non-blocking) and a fork / join
+// event pair for work the library runs beside the caller's stream; inside a
+// stream capture the record / wait pairs become graph edges
+static cudaError_t aux_stream(cudaStream_t* side, cudaEvent_t* fork, cudaEvent_t* join) {
+  static cudaStream_t streams[64] = {};
+  static cudaEvent_t forks[64] = {}, joins[64] = {};
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+  if (!streams[dev]) {
+    e = cudaStreamCreateWithFlags(&streams[dev], cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&forks[dev], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&joins[dev], cudaEventDisableTiming);
+    if (e != cudaSuccess) return e;
+  }
+  *side = streams[dev];
+  *fork = forks[dev];
+  *join = joins[dev];
+  return cudaSuccess;
+}
+
 mspipe_status mspipe_memory_create(mspipe_memory** out, int64_t num_nodes, int32_t mem_dim,
                                    int32_t edge_dim, int32_t staleness_k, float* mem,
                                    double* mem_ts, float* mail, double* mail_ts,
@@ -159,6 +181,11 @@ mspipe_status mspipe_memory_create(mspipe_memory** out, int64_t num_nodes, int32
     if (e == cudaSuccess) e = cudaMalloc(&st->sh_dest, sizeof(int32_t) * (size_t)num_nodes);
     if (e == cudaSuccess) e = cudaMalloc(&st->sh_keytab, sizeof(unsigned long long) * (size_t)st->local_rows);
     if (e == cudaSuccess) e = cudaMemset(st->sh_keytab, 0, sizeof(unsigned long long) * (size_t)st->local_rows);
+  }
+  if (e == cudaSuccess) {  // the library's side stream exists before any stream capture needs it
+    cudaStream_t side;
+    cudaEvent_t f, j;
+    e = aux_stream(&side, &f, &j);
   }
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   if (e != cudaSuccess) {
@@ -830,10 +857,34 @@ mspipe_status mspipe_gru_apply_commit(const mspipe_gru* gru, mspipe_memory* st,
       c.save_num = st->prev_num + p;
     }
     if (fused_catchup) c.cu = catchup_args(st, commit_version);
+    // split commit: mem_ts / mail / mail_ts of the winners do not depend on the
+    // GEMM (the staged mail row and t*), so a k_writeback on a forked branch
+    // writes them while the GEMM runs; its epilogue then stores only h'
+    // (different table, same rows: no overlap with the catch-up, which skips
+    // this commit's winners)
+    cudaStream_t s = (cudaStream_t)stream;
+    const bool split = new_mail && gru->d.mailbox == MSPIPE_MAILBOX_IMMEDIATE && env_int("MSPIPE_SPLIT_COMMIT", 1);
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    if (split) {
+      cudaError_t e = aux_stream(&side, &ev_fork, &ev_join);
+      if (e == cudaSuccess) e = cudaEventRecord(ev_fork, s);
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(side, ev_fork, 0);
+      if (e != cudaSuccess) return cuda_status(e, "gru_apply_commit: fork");
+      launch_writeback(nodes, num_unique, max_n, nullptr, new_ts, new_mail, 0, st->mail_stride, t.mem, t.mem_ts,
+                       t.mail, t.mail_ts, st->num_nodes, side);
+      e = cudaEventRecord(ev_join, side);
+      if (e != cudaSuccess) return cuda_status(e, "gru_apply_commit: writeback branch");
+      c.skip_meta = 1;
+    }
     cudaError_t e = launch_gru_tc(gru->d, gru->wtc, (float*)workspace, nullptr, num_events, nullptr, snap_mem, nullptr,
                                   snap_step, snap_h, winner, num_unique, out_mem, nullptr, nullptr, 0,
-                                  (cudaStream_t)stream, kGruGemm, &c);
+                                  s, kGruGemm, &c);
     if (e != cudaSuccess) return cuda_status(e, "gru_apply_commit: launch");
+    if (split) {
+      e = cudaStreamWaitEvent(s, ev_join, 0);
+      if (e != cudaSuccess) return cuda_status(e, "gru_apply_commit: join");
+    }
   }
   mspipe_status rc = after_launch("gru_apply_commit");
   if (rc == MSPIPE_OK) {

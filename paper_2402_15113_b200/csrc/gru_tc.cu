@@ -390,6 +390,7 @@ struct TcArgs {
   // GEMM: h (the GRU hidden input) is new_mail[u][0:M] (= S.mem[w], G14)
   int32_t h_from_mail;
   int32_t cpb;  // K chunks per TMEM accumulator buffer (k_gru_tc, tf32)
+  int32_t skip_meta;  // fused A7: mem_ts / mail / mail_ts written by a concurrent k_writeback instead
 };
 
 // row index of the state S.mem[w] of pair (ev, role) in snap_mem (times M) /
@@ -941,7 +942,7 @@ __global__ void __launch_bounds__(tc::kThreads, 1) k_gru_tc(TcArgs a) {
           store_h4(a, u, rownode[m], j0, gates4(pr, pz, pnx, pnh, hbuf[m * (kJ / 4) + qq], d.cell));
         }
       }
-      if (a.commit_mem) commit_rows(a, m0, U, 0, kM, jt, J, rownode);
+      if (a.commit_mem && !a.skip_meta) commit_rows(a, m0, U, 0, kM, jt, J, rownode);
     } else {
       if (kAsyncPush) {
         mbar_wait_cluster(rfull, (uint32_t)(ti & 1));  // all S x R partial rows have landed
@@ -986,7 +987,7 @@ __global__ void __launch_bounds__(tc::kThreads, 1) k_gru_tc(TcArgs a) {
         }
         store_h4(a, u, rownode[mm], j0, gates4(pr, pz, pnx, pnh, hbuf[mm * (kJ / 4) + qq], d.cell));
       }
-      if (a.commit_mem) commit_rows(a, m0, U, rb, rb + R, jt, J, rownode);
+      if (a.commit_mem && !a.skip_meta) commit_rows(a, m0, U, rb, rb + R, jt, J, rownode);
       PHASE(8);
     }
     __syncthreads();  // hbuf / rownode / sbias are rewritten by the next tile's prefetch
@@ -1477,6 +1478,7 @@ cudaError_t launch_gru_tc(const GruDesc& d, const float* wtc, float* xbuf, const
     a.save_num = commit->save_num;
     a.cu = commit->cu;
     a.h_from_mail = snap_mem == nullptr && snap_h == nullptr;
+    a.skip_meta = commit->skip_meta;
   }
   a.tsrc = tab_src;
   a.tdst = tab_dst;
