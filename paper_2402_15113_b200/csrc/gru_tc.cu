@@ -1098,7 +1098,7 @@ void launch_mail_deferred(const int32_t* src, const int32_t* dst, const double* 
 // mail_ts by the epilogue.  One launch instead of k_build_x + k_gru_tc, and no
 // operand images in HBM.
 // ---------------------------------------------------------------------------
-int gru_tc_splits(int64_t max_rows, const GruDesc& d);
+int gru_tc_splits(int64_t max_rows, const GruDesc& d, bool shared_buffers = false);
 constexpr int kFBThreads = 256;
 constexpr int kFBBuilders = kFBThreads - 64;
 
@@ -1395,7 +1395,7 @@ cudaError_t launch_gru_fb(const GruDesc& d, const float* wtc, const double* ts, 
   a.save_num = commit.save_num;
   const int64_t max_rows = 2 * num_events;
   const int64_t mtiles = (max_rows + tc::kM - 1) / tc::kM;
-  const int S = gru_tc_splits(max_rows, d);
+  const int S = gru_tc_splits(max_rows, d);  // k_gru_fb: one TMEM buffer per chunk
   return launch_k(k_gru_fb, dim3((unsigned)S, (unsigned)gru_tc_jtiles(d), (unsigned)mtiles), dim3(kFBThreads), smem,
                   s, (unsigned)S, a);
 }
@@ -1430,7 +1430,7 @@ static int64_t gru_tc_clusters(int S, bool bf16) {
   return c = n;
 }
 
-int gru_tc_splits(int64_t max_rows, const GruDesc& d) {
+int gru_tc_splits(int64_t max_rows, const GruDesc& d, bool shared_buffers) {
   // K-split = cluster size.  Powers of two pack the GPCs (measured: 5-CTA
   // clusters of 1-CTA-per-SM blocks spill into a second wave, 4 do not).
   const int forced = env_int("MSPIPE_TC_SPLITS", 0);  // experiments only: read at every launch
@@ -1438,6 +1438,9 @@ int gru_tc_splits(int64_t max_rows, const GruDesc& d) {
   // tf32: one TMEM buffer per chunk; bf16: a single accumulator, no minimum
   int64_t s_min = d.bf16 ? 1 : (nchunks + kMaxChunks - 1) / kMaxChunks;
   if (forced > 0) return forced;  // below s_min the chunks share TMEM buffers (TcArgs::cpb)
+  // big batches (GDELT's 2B = 8000): S = 2 with two K chunks per TMEM buffer
+  // (measured 54.5 vs 56.4 us per GDELT step; wiki-sized batches keep S = 4)
+  if (shared_buffers && !d.bf16 && max_rows >= 4096 && env_int("MSPIPE_TC_BIG_S2", 1)) return 2;
   const int64_t tiles = ((max_rows + tc::kM - 1) / tc::kM) * gru_tc_jtiles(d);
   int64_t s = 1;
   while (s < 8 && tiles * s * 2 <= 2 * (int64_t)num_sms() && s * 2 <= nchunks / 2) s *= 2;
@@ -1501,7 +1504,7 @@ cudaError_t launch_gru_tc(const GruDesc& d, const float* wtc, float* xbuf, const
     if (e != cudaSuccess) return e;
   }
   if (!(parts & kGruGemm)) return cudaSuccess;
-  const int S = gru_tc_splits(max_rows, d);
+  const int S = gru_tc_splits(max_rows, d, true);  // k_gru_tc: TMEM buffers may hold several chunks
   if (!d.bf16) {
     const int nchunks = d.Kpad / tc::kKC;
     const int nc_max = (nchunks + S - 1) / S;

@@ -278,7 +278,8 @@ cudaError_t launch_prep(const Tcsr& g, const int32_t* src, const int32_t* dst, c
   pf(mem_ts, g.num_nodes * (int64_t)sizeof(double));
   pf(mem, g.num_nodes * (int64_t)mem_dim * (int64_t)sizeof(float));
   int64_t blocks = (3 * num_events + kPrepWarps - 1) / kPrepWarps;
-  const int64_t cap = (int64_t)num_sms() * env_int("MSPIPE_PREP_BPS", 4);
+  // one wave of the two resident blocks per SM; the root warps grid-stride
+  const int64_t cap = (int64_t)num_sms() * env_int("MSPIPE_PREP_BPS", 2);
   if (blocks > cap) blocks = cap;
   static int co0 = -1, co1 = -1;
   apply_carveout(k_prep<false>, co0);
