@@ -284,8 +284,8 @@ def run_mspipe(args):
             idx = list(range(j, min(j + gs, len(sops))))
 
             def run_group(idx=idx):
-                for t in idx:
-                    st.run_ops(sops[t])
+                for t in idx:  # e2e copies join only at the graph's end
+                    st.run_ops(sops[t], join_copies=(t == idx[-1]))
             groups.append((_C.StepGraph().capture(run_group, s), idx))
         st.memory.reset()
         return groups, s

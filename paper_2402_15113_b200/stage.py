@@ -80,6 +80,7 @@ class StageConfig:
 # timing diagnostics (scripts/exp_overlap.py): "prep" or "commit" runs only that half of every
 # step (results are meaningless); unset in every real run
 _DEBUG_ONLY = os.environ.get("MSPIPE_DEBUG_ONLY", "")
+_E2E_SKIP = os.environ.get("MSPIPE_E2E_SKIP", "")  # "h2d" | "d2h": drop that copy (e2e timing diagnostics)
 
 
 def plan_versions(plan, nb):
@@ -264,7 +265,9 @@ class MemoryStage(_TimedOps):
         M = cfg.mem_dim
         self._out_mem_off = 16 + (8 * B + 15) // 16 * 16  # h' rows 16-byte aligned (float4 stores)
         self._out_bytes = self._out_mem_off + 8 * B * M
-        self.out_ring = [torch.empty(self._out_bytes, dtype=torch.uint8, device=dev) for _ in range(2)]
+        # result records: record i % 2 is written by commit(i) and read back during the next step
+        self._nout = 2
+        self.out_ring = [torch.empty(self._out_bytes, dtype=torch.uint8, device=dev) for _ in range(self._nout)]
         self.upd_ring = []
         for o in self.out_ring:
             u = _C.alloc_update(B, M, self.memory.mail_stride, dev)
@@ -272,6 +275,7 @@ class MemoryStage(_TimedOps):
             self.upd_ring.append(u)
         self.out_host = torch.empty(self._out_bytes, dtype=torch.uint8).pin_memory()
         self.h2d = self.d2h = None
+        self._h2d_pending, self._d2h_pending = {}, {}  # copies not yet joined (multi-step graphs)
         self._loaded = set()      # batches whose H2D is enqueued
         self._pending_out = None  # commit whose result awaits its D2H
 
@@ -320,6 +324,7 @@ class MemoryStage(_TimedOps):
         if self.staged and i not in self._loaded:  # not prefetched (the first steps): load here
             self._load(i)
             self._loaded.add(i)
+        self._wait_h2d(i)
         x = self.inputs(i)
         n = x["src"].numel()
         samp = {k: v[: 3 * n] for k, v in sl.samp.items()}
@@ -481,7 +486,7 @@ class MemoryStage(_TimedOps):
     def _upd(self, i):
         n = self.inputs(i)["src"].numel()
         sl = self._slot(i)
-        base = self.upd_ring[i % 2] if self.staged else self.upd
+        base = self.upd_ring[i % self._nout] if self.staged else self.upd
         upd = {k: v[: 2 * n] for k, v in base.items() if k not in ("nodes", "winner", "num")}
         upd.update(nodes=sl.dd["nodes"][: 2 * n], winner=sl.dd["winner"][: 2 * n], num=sl.dd["num"])
         if self.fused:
@@ -519,11 +524,13 @@ class MemoryStage(_TimedOps):
         if self.fused:
             self.apply_commit(i)
             return
+        self._wait_d2h(i)
         self.update(i)
         self.writeback(i)
 
     def apply_commit(self, i):
         """Fused A6 + A7 (mspipe_gru_apply_commit): GRU of batch i, write-back in its epilogue."""
+        self._wait_d2h(i)
         cfg, sl = self.cfg, self._slot(i)
         n = self.inputs(i)["src"].numel()
         upd = self._upd(i)
@@ -549,7 +556,7 @@ class MemoryStage(_TimedOps):
         next prep) for the D2H the next step issues."""
         if not self.staged:
             return
-        o = self.out_ring[i % 2]  # on the commit's stream, right behind it (two small copies)
+        o = self.out_ring[i % self._nout]  # on the commit's stream, right behind it (two small copies)
         n2 = upd["nodes"].numel()
         o[16:16 + 4 * n2].view(torch.int32).copy_(upd["nodes"], non_blocking=True)
         o[:4].view(torch.int32).copy_(upd["num"], non_blocking=True)
@@ -581,8 +588,10 @@ class MemoryStage(_TimedOps):
         d2h.wait_event(self._step_start)
         with torch.cuda.stream(d2h):
             c = self._read_back
+            if _E2E_SKIP == "d2h":  # timing diagnostics only
+                c = None
             if c is not None:
-                o, B, M = self.out_ring[c % 2], self.cfg.batch, self.cfg.mem_dim
+                o, B, M = self.out_ring[c % self._nout], self.cfg.batch, self.cfg.mem_dim
                 _C.rows_to_host(o[:4].view(torch.int32), self.out_host[:4].view(torch.int32),
                                 o[16:16 + 8 * B].view(torch.int32).view(2 * B, 1),
                                 self.out_host[16:16 + 8 * B].view(torch.int32).view(2 * B, 1),
@@ -599,18 +608,42 @@ class MemoryStage(_TimedOps):
                 if j > self.num_batches or j - (self.cfg.k + 2) > done_before:
                     break
                 if j not in self._loaded:
-                    self._load(j)
+                    if _E2E_SKIP != "h2d":  # timing diagnostics only
+                        self._load(j)
                     self._loaded.add(j)
+                    ev = torch.cuda.Event()
+                    ev.record(h2d)
+                    self._h2d_pending[j] = ev
                 j += 1
+        if c is not None:
+            ev = torch.cuda.Event()
+            ev.record(d2h)
+            self._d2h_pending[c] = ev
 
-    def _copies_end(self, ops):
+    def _copies_end(self, ops, join=True):
+        """join=False (inside a multi-step graph): no join of the copy streams at
+        the step's end; the prep of a prefetched batch waits for its H2D and the
+        commit that reuses a result record waits for that record's read-back."""
         if self.staged:
             self._copies_issue(ops)
-        if self.staged and self.h2d is not None:
+        if self.staged and self.h2d is not None and join:
             torch.cuda.current_stream().wait_stream(self.h2d)
             torch.cuda.current_stream().wait_stream(self.d2h)
+            self._h2d_pending.clear()
+            self._d2h_pending.clear()
 
-    def run_ops(self, ops, overlap=None):
+    def _wait_h2d(self, i):
+        ev = self._h2d_pending.pop(i, None) if self.staged else None
+        if ev is not None:
+            torch.cuda.current_stream().wait_event(ev)
+
+    def _wait_d2h(self, i):
+        # commit i rewrites result record i % 2, last read back for commit i - 2
+        ev = self._d2h_pending.pop(i - self._nout, None) if self.staged else None
+        if ev is not None:
+            torch.cuda.current_stream().wait_event(ev)
+
+    def run_ops(self, ops, overlap=None, join_copies=True):
         """Enqueue ops in order.  With overlap (default when k >= 1) every prep
         goes to a side stream, in order (preps share the handle's scratch); a
         commit of the same group waits for its own prep.  Preps only read the
@@ -628,7 +661,7 @@ class MemoryStage(_TimedOps):
             for op, i in ops:
                 (self.prep if op == "prep" else self.commit)(i)
             self._join_features()
-            self._copies_end(ops)
+            self._copies_end(ops, join_copies)
             return
         main = torch.cuda.current_stream()
         if getattr(self, "side", None) is None or self.side.device != main.device:
@@ -671,7 +704,7 @@ class MemoryStage(_TimedOps):
         if forked and not joined:
             main.wait_stream(self.side)
         self._join_features()
-        self._copies_end(ops)
+        self._copies_end(ops, join_copies)
 
     def run(self, nb=None):
         """All batches (or the first nb) in schedule order, one step at a time."""
