@@ -510,15 +510,18 @@ def run_mspipe(args):
 
 def _launches(steps, timed_batches, mit, fused, sharded=False, features=False, gemm_build=False):
     """Kernels of this library per timed step.  fused: prep = k_prep + k_build_x
-    (+ k_mitigate), commit = k_gru_tc with the write-back in its epilogue; otherwise prep = sampler +
+    (+ k_mitigate), commit = k_gru_tc (h' rows) + k_writeback (mem_ts / mail); otherwise prep = sampler +
     dedup + gather (+ mitigation), commit = build + GEMM (or SIMT GRU) + write-back.  Sharded:
     prep = sampler + dedup + mark + plan + serve + finish, commit = build + GEMM + clear + pack-plan
     + pack + merge-key + merge-apply (NCCL kernels not counted)."""
     if sharded:
         per = {"prep": 6, "commit": 7}
         return int(sum(per[op] for t in timed_batches for op, _ in steps[t]))
+    # fused commit: k_gru_tc (+ the k_writeback branch of mem_ts / mail unless MSPIPE_SPLIT_COMMIT=0;
+    # gemm_build's k_gru_fb writes everything itself)
+    split = fused and not gemm_build and os.environ.get("MSPIPE_SPLIT_COMMIT", "1") != "0"
     per = {"prep": (1 if gemm_build else 2 if fused else 3) + (1 if mit else 0) + (1 if features else 0),
-           "commit": 1 if fused else 3}
+           "commit": (2 if split else 1) if fused else 3}
     return int(sum(per[op] for t in timed_batches for op, _ in steps[t]))
 
 
