@@ -435,6 +435,20 @@ MSPIPE_API mspipe_status mspipe_gru_apply_commit(const mspipe_gru* gru, mspipe_m
                                       const float* new_mail, float* out_mem, const void* workspace,
                                       size_t ws_bytes, void* stream);
 
+/* mspipe_gru_apply_commit that also fills a result record for a host read-back:
+ * out_nodes [<=2B] = the U winner node ids (nodes[0..U)) and *out_num = U,
+ * written by the GEMM kernel itself (no extra copy after the commit).  Both
+ * device pointers, required (MSPIPE_EINVAL if NULL); an empty batch writes
+ * *out_num = 0.  Otherwise exactly mspipe_gru_apply_commit. */
+MSPIPE_API mspipe_status mspipe_gru_apply_commit_out(const mspipe_gru* gru, mspipe_memory* st,
+                                          int64_t commit_version, int64_t num_events,
+                                          const float* snap_mem, int64_t snap_step, const float* snap_h,
+                                          const int32_t* nodes, const int32_t* winner,
+                                          const int32_t* num_unique, const double* new_ts,
+                                          const float* new_mail, float* out_mem, int32_t* out_nodes,
+                                          int32_t* out_num, const void* workspace, size_t ws_bytes,
+                                          void* stream);
+
 /* A5 + A6 + A7 in ONE launch (3xTF32, immediate mailbox, no mitigation):
  * exactly mspipe_message_build (snap_h = NULL) + mspipe_gru_apply_commit of
  * the same batch, but the GEMM kernel builds its A operand in shared memory

@@ -36,7 +36,8 @@ EXPORTS = ("mspipe_abi_version", "mspipe_last_error", "mspipe_check", "mspipe_sa
            "mspipe_plan_timeline", "mspipe_plan_min_staleness", "mspipe_stale_histogram",
            "mspipe_memory_prep_build", "mspipe_feature_fetch", "mspipe_updater_create",
            "mspipe_message_build_deferred", "mspipe_memory_mail_deferred", "mspipe_gru_build_apply_commit",
-           "mspipe_util_rows_to_host", "mspipe_memory_winners", "mspipe_message_build_tables")
+           "mspipe_util_rows_to_host", "mspipe_memory_winners", "mspipe_message_build_tables",
+           "mspipe_gru_apply_commit_out")
 XCHG_FETCH_IDS, XCHG_FETCH_ROWS, XCHG_COMMIT = 0, 1, 2
 
 
@@ -113,6 +114,8 @@ def lib():
         L.mspipe_message_build.argtypes = [P, P, i64, P, P, P, i64, P, P, P, P, P, i64, P, C.c_size_t, P]
         L.mspipe_gru_apply.argtypes = [P, i64, P, i64, P, P, P, P, P, C.c_size_t, P]
         L.mspipe_gru_apply_commit.argtypes = [P, P, i64, i64, P, i64, P, P, P, P, P, P, P, P, C.c_size_t, P]
+        L.mspipe_gru_apply_commit_out.argtypes = [P, P, i64, i64, P, i64, P, P, P, P, P, P, P, P, P, P,
+                                                  C.c_size_t, P]
         L.mspipe_memory_local_rows.argtypes = [P]
         L.mspipe_memory_local_rows.restype = i64
         L.mspipe_nccl_unique_id.argtypes = [P, i32]
@@ -566,9 +569,18 @@ def gru_apply(gru: GruHandle, num_events, snap_mem, snap_step, winner, num, out_
 
 
 def gru_apply_commit(gru: GruHandle, st: MemoryHandle, commit_version, num_events, snap_mem, snap_step, upd,
-                     workspace, snap_h=None, stream=None):
+                     workspace, snap_h=None, stream=None, out_nodes=None, out_num=None):
     """A6+A7 in one launch: reads upd[nodes, winner, num, ts, mail] (dedup + message_build), writes the
-    state rows of version commit_version and upd["mem"] (h' in winner order)."""
+    state rows of version commit_version and upd["mem"] (h' in winner order); with out_nodes / out_num
+    (mspipe_gru_apply_commit_out) also the result record's winner ids and U."""
+    if out_nodes is not None or out_num is not None:
+        _ck(lib().mspipe_gru_apply_commit_out(gru.h, st.h, int(commit_version), int(num_events), ptr(snap_mem),
+                                              int(snap_step), ptr(snap_h), ptr(upd["nodes"]), ptr(upd["winner"]),
+                                              ptr(upd["num"]), ptr(upd["ts"]), ptr(upd.get("mail")),
+                                              ptr(upd.get("mem")), ptr(out_nodes), ptr(out_num), ptr(workspace),
+                                              workspace.numel() * workspace.element_size(), stream_ptr(stream)),
+            "mspipe_gru_apply_commit_out")
+        return
     _ck(lib().mspipe_gru_apply_commit(gru.h, st.h, int(commit_version), int(num_events), ptr(snap_mem),
                                       int(snap_step), ptr(snap_h), ptr(upd["nodes"]), ptr(upd["winner"]),
                                       ptr(upd["num"]), ptr(upd["ts"]), ptr(upd.get("mail")), ptr(upd.get("mem")),

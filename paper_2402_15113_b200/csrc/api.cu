@@ -810,6 +810,13 @@ mspipe_status mspipe_gru_apply(const mspipe_gru* gru, int64_t num_events, const 
   return after_launch("gru_apply");
 }
 
+static mspipe_status apply_commit_impl(const mspipe_gru* gru, mspipe_memory* st, int64_t commit_version,
+                                       int64_t num_events, const float* snap_mem, int64_t snap_step,
+                                       const float* snap_h, const int32_t* nodes, const int32_t* winner,
+                                       const int32_t* num_unique, const double* new_ts, const float* new_mail,
+                                       float* out_mem, int32_t* out_nodes, int32_t* out_num,
+                                       const void* workspace, size_t ws_bytes, void* stream);
+
 mspipe_status mspipe_gru_apply_commit(const mspipe_gru* gru, mspipe_memory* st,
                                       int64_t commit_version, int64_t num_events,
                                       const float* snap_mem, int64_t snap_step, const float* snap_h,
@@ -817,6 +824,28 @@ mspipe_status mspipe_gru_apply_commit(const mspipe_gru* gru, mspipe_memory* st,
                                       const int32_t* num_unique, const double* new_ts,
                                       const float* new_mail, float* out_mem, const void* workspace,
                                       size_t ws_bytes, void* stream) {
+  return apply_commit_impl(gru, st, commit_version, num_events, snap_mem, snap_step, snap_h, nodes, winner,
+                           num_unique, new_ts, new_mail, out_mem, nullptr, nullptr, workspace, ws_bytes, stream);
+}
+
+mspipe_status mspipe_gru_apply_commit_out(const mspipe_gru* gru, mspipe_memory* st, int64_t commit_version,
+                                          int64_t num_events, const float* snap_mem, int64_t snap_step,
+                                          const float* snap_h, const int32_t* nodes, const int32_t* winner,
+                                          const int32_t* num_unique, const double* new_ts,
+                                          const float* new_mail, float* out_mem, int32_t* out_nodes,
+                                          int32_t* out_num, const void* workspace, size_t ws_bytes,
+                                          void* stream) {
+  if (!out_nodes || !out_num) return fail(MSPIPE_EINVAL, "gru_apply_commit_out: null out_nodes / out_num");
+  return apply_commit_impl(gru, st, commit_version, num_events, snap_mem, snap_step, snap_h, nodes, winner,
+                           num_unique, new_ts, new_mail, out_mem, out_nodes, out_num, workspace, ws_bytes, stream);
+}
+
+static mspipe_status apply_commit_impl(const mspipe_gru* gru, mspipe_memory* st, int64_t commit_version,
+                                       int64_t num_events, const float* snap_mem, int64_t snap_step,
+                                       const float* snap_h, const int32_t* nodes, const int32_t* winner,
+                                       const int32_t* num_unique, const double* new_ts, const float* new_mail,
+                                       float* out_mem, int32_t* out_nodes, int32_t* out_num,
+                                       const void* workspace, size_t ws_bytes, void* stream) {
   if (!gru || !st) return fail(MSPIPE_EINVAL, "gru_apply_commit: NULL handle");
   if (gru->precision == MSPIPE_FP32_SIMT)
     return fail(MSPIPE_EUNSUPPORTED, "gru_apply_commit: only for precision MSPIPE_FP32_3XTF32");
@@ -836,6 +865,10 @@ mspipe_status mspipe_gru_apply_commit(const mspipe_gru* gru, mspipe_memory* st,
     if (!snap_mem && (snap_h || gru->d.mailbox == MSPIPE_MAILBOX_DEFERRED))
       return fail(MSPIPE_EINVAL, "gru_apply_commit: snap_mem may be NULL only with snap_h NULL and an immediate mailbox");
   }
+  if (num_events == 0 && out_num) {  // an empty batch's result record: U = 0
+    cudaError_t e = cudaMemsetAsync(out_num, 0, sizeof(int32_t), (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_status(e, "gru_apply_commit: out_num");
+  }
   const int64_t max_n = 2 * num_events;
   // double-buffered: the GEMM kernel catches up the previous commit's rows
   // itself when mspipe_memory_prep stamped this batch's winners; otherwise a
@@ -851,6 +884,8 @@ mspipe_status mspipe_gru_apply_commit(const mspipe_gru* gru, mspipe_memory* st,
   if (num_events > 0) {
     const TableSet t = table_set(st, commit_version);
     GruCommit c{nodes, t.mem, t.mem_ts, t.mail, t.mail_ts, new_ts, new_mail, st->num_nodes, st->mail_stride};
+    c.res_nodes = out_nodes;
+    c.res_num = out_num;
     if (done || fused_catchup) {  // the kernel saves this commit's winner list
       const int p = (int)(commit_version & 1);
       c.save_nodes = st->prev_nodes + p * st->num_nodes;

@@ -391,6 +391,8 @@ struct TcArgs {
   int32_t h_from_mail;
   int32_t cpb;  // K chunks per TMEM accumulator buffer (k_gru_tc, tf32)
   int32_t skip_meta;  // fused A7: mem_ts / mail / mail_ts written by a concurrent k_writeback instead
+  int32_t* res_nodes;  // optional result record: winner node ids [U] and U (host read-back)
+  int32_t* res_num;
 };
 
 // row index of the state S.mem[w] of pair (ev, role) in snap_mem (times M) /
@@ -763,7 +765,10 @@ __global__ void __launch_bounds__(tc::kThreads, 1) k_gru_tc(TcArgs a) {
     for (; pre < nc && pre < kStages; ++pre) load_chunk(0, (int32_t)(blockIdx.y / J), (int)(blockIdx.y % J), pre);
   const int64_t mt_act = U > 0 ? (U + kM - 1) / kM : 0;
   const int64_t tiles = mt_act * J;
-  if (a.save_num && cta_q == 0 && threadIdx.x == 0) *a.save_num = U;
+  if (cta_q == 0 && threadIdx.x == 0) {
+    if (a.save_num) *a.save_num = U;
+    if (a.res_num) *a.res_num = U;
+  }
   if ((int64_t)blockIdx.y >= tiles) {  // no tile for this cluster (uniform across it)
     if (warp == 0 && lane == 0)
       for (int s = 0; s < pre; ++s) mbar_wait(&full[s], 0u);  // drain the speculative copies
@@ -851,6 +856,7 @@ __global__ void __launch_bounds__(tc::kThreads, 1) k_gru_tc(TcArgs a) {
           const int32_t node = (a.commit_mem && u < U) ? __ldg(a.nodes + u) : -1;
           rownode[mm] = node;
           if (a.save_nodes && jt == 0 && node >= 0) a.save_nodes[u] = node;
+          if (a.res_nodes && jt == 0 && u < U) a.res_nodes[u] = node;
         }
       }
       for (int i = threadIdx.x - 64; i < kN; i += 64) sbias[i] = __ldg(d.bias + jt * kN + i);
@@ -1482,6 +1488,8 @@ cudaError_t launch_gru_tc(const GruDesc& d, const float* wtc, float* xbuf, const
     a.cu = commit->cu;
     a.h_from_mail = snap_mem == nullptr && snap_h == nullptr;
     a.skip_meta = commit->skip_meta;
+    a.res_nodes = commit->res_nodes;
+    a.res_num = commit->res_num;
   }
   a.tsrc = tab_src;
   a.tdst = tab_dst;

@@ -354,6 +354,8 @@ struct GruCommit {  // fused A7 in the GEMM epilogue
   int32_t* save_num;
   CatchUp cu;  // cu.stamp == nullptr: no catch-up in this kernel
   int32_t skip_meta;  // 1: the epilogue writes only h' rows (mem_ts / mail / mail_ts by k_writeback)
+  int32_t* res_nodes;  // optional: winner node ids [U] and U into a result record
+  int32_t* res_num;
 };
 // row F3, deferred mailbox: A5 from the snapshot mail rows (snap_mail, rows as snap_mem)
 cudaError_t launch_build_deferred(const GruDesc& d, float* xbuf, const double* ts, int64_t num_events,

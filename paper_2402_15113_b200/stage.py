@@ -540,15 +540,23 @@ class MemoryStage(_TimedOps):
             _C.gru_build_apply_commit(self.gru, self.memory, i, x["ts"], x["ef"], sl.mem, sl.mem_ts, cfg.fanout + 1,
                                       upd)
         else:
-            # direct build: h = S.mem[w] is the first M floats of the staged mail row (G14)
+            # direct build: h = S.mem[w] is the first M floats of the staged mail row (G14).
+            # e2e: the GEMM also writes the result record's winner ids and U (no copies after it)
+            rec = {}
+            if self.staged:
+                o = self.out_ring[i % self._nout]
+                rec = dict(out_nodes=o[16:16 + 4 * 2 * n].view(torch.int32), out_num=o[:4].view(torch.int32))
             _C.gru_apply_commit(self.gru, self.memory, i, n, None if self.direct else sl.mem, cfg.fanout + 1, upd,
-                                sl.ws, snap_h=sl.h[: 2 * n] if sl.h is not None else None)
+                                sl.ws, snap_h=sl.h[: 2 * n] if sl.h is not None else None, **rec)
         if self.deferred:  # row F3: new mails from the committed memories of both endpoints
             x = self.inputs(i)
             _C.memory_mail_deferred(self.memory, i, x["src"], x["dst"], x["ts"], x["ef"], upd["nodes"], upd["winner"],
                                     upd["num"])
         self._ev("update_end")
-        self._stash_result(i, upd)
+        if self.staged and not self.gemm_build:
+            self._pending_out = i  # the GEMM filled the result record
+        else:
+            self._stash_result(i, upd)
 
     # -- e2e copies (staged inputs) ---------------------------------------
     def _stash_result(self, i, upd):
