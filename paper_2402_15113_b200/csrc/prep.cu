@@ -79,7 +79,10 @@ __device__ __forceinline__ void warp_gather_rows(const float4* __restrict__ tab,
                                                  int lane) {
   // kU float4 loads in flight per lane before their stores: the whole subgraph
   // (11 rows x 25 float4 for M = 100) in one dependent round instead of three
-  constexpr int kU = 12;
+#ifndef MSPIPE_PREP_KU
+#define MSPIPE_PREP_KU 12
+#endif
+  constexpr int kU = MSPIPE_PREP_KU;
   const int total = nrows * Q;
   const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
   for (int base = 0; base < total; base += 32 * kU) {
