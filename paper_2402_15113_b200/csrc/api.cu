@@ -109,22 +109,24 @@ static mspipe_status nccl_warmup(mspipe_memory* st);
 // a library-owned stream (one per device, non-blocking) and a fork / join
 // event pair for work the library runs beside the caller's stream; inside a
 // stream capture the record / wait pairs become graph edges
-static cudaError_t aux_stream(cudaStream_t* side, cudaEvent_t* fork, cudaEvent_t* join) {
-  static cudaStream_t streams[64] = {};
-  static cudaEvent_t forks[64] = {}, joins[64] = {};
+// which: 0 = the commit's write-back branch, 1 = the prep's mitigation branch
+// (separate streams: one shared stream would order the two branches)
+static cudaError_t aux_stream(cudaStream_t* side, cudaEvent_t* fork, cudaEvent_t* join, int which = 0) {
+  static cudaStream_t streams[2][64] = {};
+  static cudaEvent_t forks[2][64] = {}, joins[2][64] = {};
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
-  if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
-  if (!streams[dev]) {
-    e = cudaStreamCreateWithFlags(&streams[dev], cudaStreamNonBlocking);
-    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&forks[dev], cudaEventDisableTiming);
-    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&joins[dev], cudaEventDisableTiming);
+  if (dev < 0 || dev >= 64 || which < 0 || which > 1) return cudaErrorInvalidDevice;
+  if (!streams[which][dev]) {
+    e = cudaStreamCreateWithFlags(&streams[which][dev], cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&forks[which][dev], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&joins[which][dev], cudaEventDisableTiming);
     if (e != cudaSuccess) return e;
   }
-  *side = streams[dev];
-  *fork = forks[dev];
-  *join = joins[dev];
+  *side = streams[which][dev];
+  *fork = forks[which][dev];
+  *join = joins[which][dev];
   return cudaSuccess;
 }
 
@@ -185,7 +187,8 @@ mspipe_status mspipe_memory_create(mspipe_memory** out, int64_t num_nodes, int32
   if (e == cudaSuccess) {  // the library's side stream exists before any stream capture needs it
     cudaStream_t side;
     cudaEvent_t f, j;
-    e = aux_stream(&side, &f, &j);
+    e = aux_stream(&side, &f, &j, 0);
+    if (e == cudaSuccess) e = aux_stream(&side, &f, &j, 1);
   }
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   if (e != cudaSuccess) {
@@ -673,6 +676,25 @@ static mspipe_status prep_impl(mspipe_memory* st, const mspipe_tcsr* g, int64_t 
   if ((out_mail == nullptr) != (out_mail_ts == nullptr)) return fail(MSPIPE_EINVAL, "memory_prep: out_mail and out_mail_ts go together");
   cudaStream_t s = (cudaStream_t)stream;
   const TableSet t = table_set(st, st->committed);
+  // A4 reads only the T-CSR and the tables of the version read, not k_prep's
+  // outputs: it runs on a forked branch beside k_prep (MSPIPE_MIT_BRANCH=0: after it)
+  bool mit_branch = false;
+  cudaEvent_t mit_join = nullptr;
+  if (mit && mit->num_events > 0 && tcsr_ok(mit->g) && mit->src && mit->dst && mit->ts && mit->out_h &&
+      mit->lambda >= 0.f && mit->lambda <= 1.f && mit->n_sim >= 0 && mit->n_sim <= 16 && mit->fanout >= 1 &&
+      mit->fanout <= 16 && env_int("MSPIPE_MIT_BRANCH", 1)) {
+    cudaStream_t side;
+    cudaEvent_t fork;
+    cudaError_t e = aux_stream(&side, &fork, &mit_join, 1);
+    if (e == cudaSuccess) e = cudaEventRecord(fork, s);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(side, fork, 0);
+    if (e != cudaSuccess) return cuda_status(e, "memory_prep: mitigation fork");
+    launch_mitigate(to_tcsr(mit->g), mit->src, mit->dst, mit->ts, mit->num_events, t.mem, t.mem_ts, st->mem_dim,
+                    mit->lambda, mit->gamma, mit->n_sim, mit->fanout, mit->out_h, mit->out_omega, mit->out_elig, side);
+    e = cudaEventRecord(mit_join, side);
+    if (e != cudaSuccess) return cuda_status(e, "memory_prep: mitigation branch");
+    mit_branch = true;
+  }
   // no dedup outputs: the A2 part is left to mspipe_memory_winners
   const bool dedup = out_nodes || out_winner || out_num_unique;
   if (dedup && ba == nullptr && !(out_nodes && out_winner && out_num_unique))
@@ -721,8 +743,13 @@ static mspipe_status prep_impl(mspipe_memory* st, const mspipe_tcsr* g, int64_t 
       return fail(MSPIPE_EINVAL, "memory_prep: bad mitigation arguments");
     if (!(mit->lambda >= 0.f && mit->lambda <= 1.f) || mit->n_sim < 0 || mit->n_sim > 16 || mit->fanout < 1 || mit->fanout > 16)
       return fail(MSPIPE_EINVAL, "memory_prep: lambda=%g n_sim=%d fanout=%d", mit->lambda, mit->n_sim, mit->fanout);
-    launch_mitigate(to_tcsr(mit->g), mit->src, mit->dst, mit->ts, mit->num_events, t.mem, t.mem_ts, st->mem_dim,
-                    mit->lambda, mit->gamma, mit->n_sim, mit->fanout, mit->out_h, mit->out_omega, mit->out_elig, s);
+    if (mit_branch) {  // joined back: the message build after this call reads out_h
+      cudaError_t e = cudaStreamWaitEvent(s, mit_join, 0);
+      if (e != cudaSuccess) return cuda_status(e, "memory_prep: mitigation join");
+    } else {
+      launch_mitigate(to_tcsr(mit->g), mit->src, mit->dst, mit->ts, mit->num_events, t.mem, t.mem_ts, st->mem_dim,
+                      mit->lambda, mit->gamma, mit->n_sim, mit->fanout, mit->out_h, mit->out_omega, mit->out_elig, s);
+    }
   }
   if (out_version) *out_version = st->committed;
   return after_launch("memory_prep");
