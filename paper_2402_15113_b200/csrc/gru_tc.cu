@@ -679,8 +679,11 @@ constexpr bool kMailPf = MSPIPE_MAIL_PF != 0;
 #endif
 constexpr bool kAsyncPush = MSPIPE_ASYNC_PUSH != 0;
 
+#ifndef MSPIPE_GEMM_MINB
+#define MSPIPE_GEMM_MINB 1  // register cap (min blocks per SM) of k_gru_tc: co-residence with prep / build
+#endif
 template <bool kBf>
-__global__ void __launch_bounds__(tc::kThreads, 1) k_gru_tc(TcArgs a) {
+__global__ void __launch_bounds__(tc::kThreads, MSPIPE_GEMM_MINB) k_gru_tc(TcArgs a) {
   using namespace tc;
   constexpr int SB = kBf ? kStageBytes16 : kStageBytes;
   constexpr int AB = kBf ? kATile16 : kABlock;
