@@ -428,6 +428,10 @@ def run_mspipe(args):
         roof = {"kernel": dom, "bound": "hbm", "achieved": ach, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                 "frac": ach / peaks["hbm_gbs"], "peak_source": peaks["source"]}
     roof["traffic"] = _ncu_traffic(args.config, dom)
+    if roof.get("bound") == "tensor":
+        roof["note"] = (f"{mean_U:.0f} GEMM rows per batch ({int(-(-mean_U // 128))} M tiles of 128): the contraction "
+                        "is a few us of tensor work; the launch is bound by dependent latency (operand chunk "
+                        "loads, the K-split partial exchange, the commit epilogue), DESIGN.md section 5")
     roof["op_ms_mean"] = op_mean
     roof["op_share"] = {kk: v / sum(op_mean.values()) for kk, v in op_mean.items()} if op_mean else None
     roof["step_timeline_ms"] = dict(sorted(timeline.items(), key=lambda kv: kv[1]))
