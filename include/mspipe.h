@@ -39,7 +39,7 @@
 extern "C" {
 #endif
 
-#define MSPIPE_ABI_VERSION 1
+#define MSPIPE_ABI_VERSION 2
 
 #if defined(__GNUC__)
 #define MSPIPE_API __attribute__((visibility("default")))
@@ -135,9 +135,13 @@ MSPIPE_API mspipe_status mspipe_memory_create(mspipe_memory** out, int64_t num_n
                                    const void* nccl_unique_id /* [host] 128 B, NULL iff world==1 */);
 MSPIPE_API mspipe_status mspipe_memory_destroy(mspipe_memory* st);
 MSPIPE_API int64_t mspipe_memory_committed(const mspipe_memory* st); /* [host] last enqueued commit version */
-/* [host] restart an epoch: committed := 0 (the caller re-zeroes the tables, G17;
- * when double-buffered, set 0 is then mirrored into set 1, synchronously). */
-MSPIPE_API mspipe_status mspipe_memory_reset(mspipe_memory* st);
+/* [host] restart an epoch: committed := 0; zero_tables != 0 re-zeroes this
+ * rank's tables (S_0 = 0, G17; else the caller has written the initial state);
+ * when double-buffered, set 0 is then mirrored into set 1.  Every device write
+ * is enqueued on `stream` (so it is ordered after the caller's earlier work on
+ * that stream) and the call returns after `stream` has drained.  Errors:
+ * EINVAL (NULL handle), ECUDA. */
+MSPIPE_API mspipe_status mspipe_memory_reset(mspipe_memory* st, int32_t zero_tables, void* stream);
 
 /* Double-buffered state (world == 1).  With staleness k >= 1 the fetch of
  * batch t+k reads version t-1 while commit t writes version t (Eq. 2,

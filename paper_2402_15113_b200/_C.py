@@ -17,7 +17,7 @@ LIB_PATH = os.environ.get("MSPIPE_LIB") or os.path.join(_HERE, "libmspipe.so")  
 
 OK, EINVAL, ERANGE, ESTALE, EORDER, EUNSUPPORTED, ECUDA, ENCCL = 0, -1, -2, -3, -4, -5, -6, -7
 FP32_SIMT, FP32_3XTF32, BF16 = 0, 1, 2
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 P = C.c_void_p
 i32, i64, f32, f64 = C.c_int32, C.c_int64, C.c_float, C.c_double
@@ -77,7 +77,7 @@ def lib():
         L.mspipe_memory_destroy.argtypes = [P]
         L.mspipe_memory_committed.argtypes = [P]
         L.mspipe_memory_committed.restype = i64
-        L.mspipe_memory_reset.argtypes = [P]
+        L.mspipe_memory_reset.argtypes = [P, i32, P]
         L.mspipe_memory_fetch.argtypes = [P, i64, P, i64, P, P, P, P, C.POINTER(Mitigation),
                                           C.POINTER(i64), P]
         L.mspipe_gru_create.argtypes = [C.POINTER(P), i32, i32, i32, i32, i64, P, P, P, P, P, P, P]
@@ -379,13 +379,11 @@ class MemoryHandle:
         """After replaying captured steps from a reset (see mspipe_memory_set_committed)."""
         _ck(lib().mspipe_memory_set_committed(self.h, int(version)), "mspipe_memory_set_committed")
 
-    def reset(self, zero_tables=True):
-        """New epoch: committed := 0; tables back to S_0 = 0 (G17)."""
-        if zero_tables:
-            for ts in self._sets:
-                for t in ts.values():
-                    t.zero_()
-        _ck(lib().mspipe_memory_reset(self.h), "mspipe_memory_reset")
+    def reset(self, zero_tables=True, stream=None):
+        """New epoch: committed := 0; tables back to S_0 = 0 (G17).  The library
+        zeroes and mirrors on `stream` (default: the current torch stream), so
+        the reset is ordered after the caller's earlier work on it."""
+        _ck(lib().mspipe_memory_reset(self.h, 1 if zero_tables else 0, stream_ptr(stream)), "mspipe_memory_reset")
 
 
 def nccl_unique_id() -> bytes:

@@ -106,28 +106,29 @@ mspipe_status mspipe_sample_batch(const mspipe_tcsr* g, const int32_t* src, cons
 
 static mspipe_status nccl_warmup(mspipe_memory* st);
 
-// a library-owned stream (one per device, non-blocking) and a fork / join
-// event pair for work the library runs beside the caller's stream; inside a
-// stream capture the record / wait pairs become graph edges
-// which: 0 = the commit's write-back branch, 1 = the prep's mitigation branch
-// (separate streams: one shared stream would order the two branches)
-static cudaError_t aux_stream(cudaStream_t* side, cudaEvent_t* fork, cudaEvent_t* join, int which = 0) {
-  static cudaStream_t streams[2][64] = {};
-  static cudaEvent_t forks[2][64] = {}, joins[2][64] = {};
-  int dev = 0;
-  cudaError_t e = cudaGetDevice(&dev);
-  if (e != cudaSuccess) return e;
-  if (dev < 0 || dev >= 64 || which < 0 || which > 1) return cudaErrorInvalidDevice;
-  if (!streams[which][dev]) {
-    e = cudaStreamCreateWithFlags(&streams[which][dev], cudaStreamNonBlocking);
-    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&forks[which][dev], cudaEventDisableTiming);
-    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&joins[which][dev], cudaEventDisableTiming);
-    if (e != cudaSuccess) return e;
-  }
-  *side = streams[which][dev];
-  *fork = forks[which][dev];
-  *join = joins[which][dev];
+// a library-owned stream of the handle (non-blocking) and a fork / join event
+// pair for work the library runs beside the caller's stream; inside a stream
+// capture the record / wait pairs become graph edges.  which: 0 = the commit's
+// write-back branch, 1 = the prep's mitigation branch (separate streams: one
+// shared stream would order the two branches).  Created by
+// mspipe_memory_create; one host thread per handle (header), so no locking.
+static cudaError_t aux_stream(mspipe_memory* st, cudaStream_t* side, cudaEvent_t* fork, cudaEvent_t* join,
+                              int which) {
+  if (which < 0 || which > 1 || !st->aux[which]) return cudaErrorInvalidResourceHandle;
+  *side = st->aux[which];
+  *fork = st->aux_fork[which];
+  *join = st->aux_join[which];
   return cudaSuccess;
+}
+
+static cudaError_t aux_create(mspipe_memory* st) {
+  cudaError_t e = cudaSuccess;
+  for (int w = 0; w < 2 && e == cudaSuccess; ++w) {
+    e = cudaStreamCreateWithFlags(&st->aux[w], cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&st->aux_fork[w], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&st->aux_join[w], cudaEventDisableTiming);
+  }
+  return e;
 }
 
 mspipe_status mspipe_memory_create(mspipe_memory** out, int64_t num_nodes, int32_t mem_dim,
@@ -184,12 +185,7 @@ mspipe_status mspipe_memory_create(mspipe_memory** out, int64_t num_nodes, int32
     if (e == cudaSuccess) e = cudaMalloc(&st->sh_keytab, sizeof(unsigned long long) * (size_t)st->local_rows);
     if (e == cudaSuccess) e = cudaMemset(st->sh_keytab, 0, sizeof(unsigned long long) * (size_t)st->local_rows);
   }
-  if (e == cudaSuccess) {  // the library's side stream exists before any stream capture needs it
-    cudaStream_t side;
-    cudaEvent_t f, j;
-    e = aux_stream(&side, &f, &j, 0);
-    if (e == cudaSuccess) e = aux_stream(&side, &f, &j, 1);
-  }
+  if (e == cudaSuccess) e = aux_create(st);  // the side streams exist before any stream capture needs them
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   if (e != cudaSuccess) {
     mspipe_memory_destroy(st);
@@ -207,16 +203,19 @@ mspipe_status mspipe_memory_create(mspipe_memory** out, int64_t num_nodes, int32
   return MSPIPE_OK;
 }
 
-// set 1 <- set 0, no previous commit (version 0 in both sets)
-static mspipe_status db_mirror(mspipe_memory* st) {
+// set 1 <- set 0, no previous commit (version 0 in both sets); every copy is
+// ordered on `s` (the caller's stream: its earlier writes to set 0, e.g. a
+// re-zeroing, are seen) and the host waits for `s` before the bookkeeping
+static mspipe_status db_mirror(mspipe_memory* st, cudaStream_t s) {
   const size_t N = (size_t)st->num_nodes;
-  cudaError_t e = cudaMemcpy(st->mem1, st->mem, sizeof(float) * N * st->mem_dim, cudaMemcpyDeviceToDevice);
-  if (e == cudaSuccess) e = cudaMemcpy(st->mem_ts1, st->mem_ts, sizeof(double) * N, cudaMemcpyDeviceToDevice);
-  if (e == cudaSuccess) e = cudaMemcpy(st->mail1, st->mail, sizeof(float) * N * st->mail_stride, cudaMemcpyDeviceToDevice);
-  if (e == cudaSuccess) e = cudaMemcpy(st->mail_ts1, st->mail_ts, sizeof(double) * N, cudaMemcpyDeviceToDevice);
-  if (e == cudaSuccess) e = cudaMemset(st->prev_num, 0, 2 * sizeof(int32_t));
-  if (e == cudaSuccess) e = cudaMemset(st->stamps, 0, sizeof(int32_t) * (size_t)(st->k + 1) * N);
-  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  cudaError_t e = cudaMemcpyAsync(st->mem1, st->mem, sizeof(float) * N * st->mem_dim, cudaMemcpyDeviceToDevice, s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(st->mem_ts1, st->mem_ts, sizeof(double) * N, cudaMemcpyDeviceToDevice, s);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(st->mail1, st->mail, sizeof(float) * N * st->mail_stride, cudaMemcpyDeviceToDevice, s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(st->mail_ts1, st->mail_ts, sizeof(double) * N, cudaMemcpyDeviceToDevice, s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(st->prev_num, 0, 2 * sizeof(int32_t), s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(st->stamps, 0, sizeof(int32_t) * (size_t)(st->k + 1) * N, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
   st->prev_max[0] = st->prev_max[1] = 0;
   st->caught_up = 0;
   for (int r = 0; r <= st->k; ++r) st->stamp_iter[r] = 0;
@@ -240,7 +239,7 @@ mspipe_status mspipe_memory_double_buffer(mspipe_memory* st, float* mem1, double
   st->mail1 = mail1;
   st->mail_ts1 = mail_ts1;
   st->db = 1;
-  return db_mirror(st);
+  return db_mirror(st, cudaStreamLegacy);
 }
 
 mspipe_status mspipe_memory_set_committed(mspipe_memory* st, int64_t version) {
@@ -302,6 +301,11 @@ mspipe_status mspipe_memory_destroy(mspipe_memory* st) {
                   st->prev_num, st->stamps, st->bld_upos, st->bld_sync};
   for (void* b : bufs)
     if (b) cudaFree(b);
+  for (int w = 0; w < 2; ++w) {
+    if (st->aux_fork[w]) cudaEventDestroy(st->aux_fork[w]);
+    if (st->aux_join[w]) cudaEventDestroy(st->aux_join[w]);
+    if (st->aux[w]) cudaStreamDestroy(st->aux[w]);
+  }
   delete[] st->stamp_iter;
   delete st;
   return MSPIPE_OK;
@@ -311,19 +315,29 @@ int64_t mspipe_memory_local_rows(const mspipe_memory* st) { return st ? st->loca
 
 int64_t mspipe_memory_committed(const mspipe_memory* st) { return st ? st->committed : -1; }
 
-mspipe_status mspipe_memory_reset(mspipe_memory* st) {
+mspipe_status mspipe_memory_reset(mspipe_memory* st, int32_t zero_tables, void* stream) {
   if (!st) return fail(MSPIPE_EINVAL, "memory_reset: NULL handle");
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t N = (size_t)st->local_rows;
+  cudaError_t e = cudaSuccess;
+  if (zero_tables) {  // S_0 = 0 (G17), stream-ordered behind the caller's earlier work
+    e = cudaMemsetAsync(st->mem, 0, sizeof(float) * N * st->mem_dim, s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(st->mem_ts, 0, sizeof(double) * N, s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(st->mail, 0, sizeof(float) * N * st->mail_stride, s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(st->mail_ts, 0, sizeof(double) * N, s);
+    if (e != cudaSuccess) return cuda_status(e, "memory_reset: zero");
+  }
   st->committed = 0;
   if (st->db) {  // version 0 = set 0 (the caller's initial state), mirrored into set 1
-    mspipe_status rc = db_mirror(st);
+    mspipe_status rc = db_mirror(st, s);
     if (rc != MSPIPE_OK) return rc;
   }
   if (st->sh_keytab) {  // keys restart with the stream
-    cudaError_t e = cudaMemset(st->sh_keytab, 0, sizeof(unsigned long long) * (size_t)st->local_rows);
-    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    e = cudaMemsetAsync(st->sh_keytab, 0, sizeof(unsigned long long) * (size_t)st->local_rows, s);
     if (e != cudaSuccess) return cuda_status(e, "memory_reset");
   }
-  return MSPIPE_OK;
+  e = cudaStreamSynchronize(s);
+  return cuda_status(e, "memory_reset");
 }
 
 mspipe_status mspipe_memory_fetch(mspipe_memory* st, int64_t iteration, const int32_t* ids,
@@ -674,18 +688,32 @@ static mspipe_status prep_impl(mspipe_memory* st, const mspipe_tcsr* g, int64_t 
     return fail(MSPIPE_ESTALE, "memory_prep: iteration %lld with committed=%lld violates k=%d",
                 (long long)iteration, (long long)st->committed, st->k);
   if ((out_mail == nullptr) != (out_mail_ts == nullptr)) return fail(MSPIPE_EINVAL, "memory_prep: out_mail and out_mail_ts go together");
+  // every argument is validated before any fork or launch (an error return
+  // leaves no branch unjoined and nothing enqueued)
+  const bool dedup = out_nodes || out_winner || out_num_unique;
+  if (dedup && ba == nullptr && !(out_nodes && out_winner && out_num_unique))
+    return fail(MSPIPE_EINVAL, "memory_prep: out_nodes / out_winner / out_num_unique go together");
+  if (!dedup && ba) return fail(MSPIPE_EINVAL, "memory_prep_build: needs the dedup outputs");
+  if (num_events > 0 &&
+      (!src || !dst || !neg || !ts || !out_nbr || !out_eid || !out_ts || !out_dt || !out_cnt || !out_sub_ids ||
+       (dedup && (!out_nodes || !out_winner || !out_num_unique)) || !out_mem || !out_mem_ts))
+    return fail(MSPIPE_EINVAL, "memory_prep: null input/output");
+  if (mit && mit->num_events > 0) {
+    if (!tcsr_ok(mit->g) || !mit->src || !mit->dst || !mit->ts || !mit->out_h)
+      return fail(MSPIPE_EINVAL, "memory_prep: bad mitigation arguments");
+    if (!(mit->lambda >= 0.f && mit->lambda <= 1.f) || mit->n_sim < 0 || mit->n_sim > 16 || mit->fanout < 1 || mit->fanout > 16)
+      return fail(MSPIPE_EINVAL, "memory_prep: lambda=%g n_sim=%d fanout=%d", mit->lambda, mit->n_sim, mit->fanout);
+  }
   cudaStream_t s = (cudaStream_t)stream;
   const TableSet t = table_set(st, st->committed);
   // A4 reads only the T-CSR and the tables of the version read, not k_prep's
   // outputs: it runs on a forked branch beside k_prep (MSPIPE_MIT_BRANCH=0: after it)
   bool mit_branch = false;
   cudaEvent_t mit_join = nullptr;
-  if (mit && mit->num_events > 0 && tcsr_ok(mit->g) && mit->src && mit->dst && mit->ts && mit->out_h &&
-      mit->lambda >= 0.f && mit->lambda <= 1.f && mit->n_sim >= 0 && mit->n_sim <= 16 && mit->fanout >= 1 &&
-      mit->fanout <= 16 && env_int("MSPIPE_MIT_BRANCH", 1)) {
+  if (mit && mit->num_events > 0 && env_int("MSPIPE_MIT_BRANCH", 1)) {
     cudaStream_t side;
     cudaEvent_t fork;
-    cudaError_t e = aux_stream(&side, &fork, &mit_join, 1);
+    cudaError_t e = aux_stream(st, &side, &fork, &mit_join, 1);
     if (e == cudaSuccess) e = cudaEventRecord(fork, s);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(side, fork, 0);
     if (e != cudaSuccess) return cuda_status(e, "memory_prep: mitigation fork");
@@ -695,15 +723,7 @@ static mspipe_status prep_impl(mspipe_memory* st, const mspipe_tcsr* g, int64_t 
     if (e != cudaSuccess) return cuda_status(e, "memory_prep: mitigation branch");
     mit_branch = true;
   }
-  // no dedup outputs: the A2 part is left to mspipe_memory_winners
-  const bool dedup = out_nodes || out_winner || out_num_unique;
-  if (dedup && ba == nullptr && !(out_nodes && out_winner && out_num_unique))
-    return fail(MSPIPE_EINVAL, "memory_prep: out_nodes / out_winner / out_num_unique go together");
-  if (!dedup && ba) return fail(MSPIPE_EINVAL, "memory_prep_build: needs the dedup outputs");
   if (num_events > 0) {
-    if (!src || !dst || !neg || !ts || !out_nbr || !out_eid || !out_ts || !out_dt || !out_cnt || !out_sub_ids ||
-        (dedup && (!out_nodes || !out_winner || !out_num_unique)) || !out_mem || !out_mem_ts)
-      return fail(MSPIPE_EINVAL, "memory_prep: null input/output");
     // double-buffered: this launch may also carry the catch-up of the next
     // commit c (its winners already stamped, or stamped by this very launch
     // when c == iteration, k = 0: the commit then follows in stream order).
@@ -739,10 +759,6 @@ static mspipe_status prep_impl(mspipe_memory* st, const mspipe_tcsr* g, int64_t 
     if (e != cudaSuccess) return cuda_status(e, "memory_prep");
   }
   if (mit && mit->num_events > 0) {
-    if (!tcsr_ok(mit->g) || !mit->src || !mit->dst || !mit->ts || !mit->out_h)
-      return fail(MSPIPE_EINVAL, "memory_prep: bad mitigation arguments");
-    if (!(mit->lambda >= 0.f && mit->lambda <= 1.f) || mit->n_sim < 0 || mit->n_sim > 16 || mit->fanout < 1 || mit->fanout > 16)
-      return fail(MSPIPE_EINVAL, "memory_prep: lambda=%g n_sim=%d fanout=%d", mit->lambda, mit->n_sim, mit->fanout);
     if (mit_branch) {  // joined back: the message build after this call reads out_h
       cudaError_t e = cudaStreamWaitEvent(s, mit_join, 0);
       if (e != cudaSuccess) return cuda_status(e, "memory_prep: mitigation join");
@@ -929,7 +945,7 @@ static mspipe_status apply_commit_impl(const mspipe_gru* gru, mspipe_memory* st,
     cudaStream_t side = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     if (split) {
-      cudaError_t e = aux_stream(&side, &ev_fork, &ev_join);
+      cudaError_t e = aux_stream(st, &side, &ev_fork, &ev_join, 0);
       if (e == cudaSuccess) e = cudaEventRecord(ev_fork, s);
       if (e == cudaSuccess) e = cudaStreamWaitEvent(side, ev_fork, 0);
       if (e != cudaSuccess) return cuda_status(e, "gru_apply_commit: fork");

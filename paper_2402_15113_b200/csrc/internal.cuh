@@ -469,6 +469,11 @@ struct mspipe_memory {
   // fused message build (mspipe_memory_prep_build): pair -> GEMM row, publish flag
   int32_t* bld_upos;        // [2 * 8192]
   int32_t* bld_sync;        // [2], self-cleaning
+  // library-owned branches beside the caller's stream, per handle (created at
+  // mspipe_memory_create, so never lazily under a stream capture): 0 = the
+  // commit's write-back branch, 1 = the prep's mitigation branch
+  cudaStream_t aux[2];
+  cudaEvent_t aux_fork[2], aux_join[2];
 };
 
 namespace mspipe {

@@ -315,6 +315,75 @@ def test_p4_bias_only_closed_form(k, schedule):
     assert np.allclose(st["mem"], want[:, None], rtol=0, atol=3e-7)
 
 
+# ---------------------------------------------------------------- F1 plan mode (per-iteration k_i)
+@pytest.mark.parametrize("plan_k,key", [(1, "k0_exact"), (2, "k1_exact")])
+def test_plan_worked_example_constant_plans(plan_k, key):
+    """Plan mode with a constant paper staleness k_i: "k=1 represents the
+    baseline method of TGL without applying staleness", so k_i = 1 is
+    the build-k 0 run and k_i = 2 the build-k 1 run of the hand-worked example
+    (C.5 values, golden/worked_example.json)."""
+    g = _load("worked_example.json")
+    ev = g["events"]
+    exp = g["bias_only_units_of_tanh_c"][key]
+    M, He, Dt, c = 4, 3, 2, 0.7
+    ef = edge_features(0, 0, 6, He)
+    st, vers = oracle.run_stream(4, ev["src"], ev["dst"], ev["ts"], ef, _bias_only(M, He, Dt, c),
+                                 g["batch"], plan_k - 1, plan=[plan_k] * 3)
+    want = np.array(exp["mem"])[:, None] * math.tanh(c)
+    assert np.allclose(st["mem"], np.broadcast_to(want, (4, M)), rtol=0, atol=2e-7)
+    assert list(st["mem_ts"]) == exp["mem_ts"]
+    # Alg. 1 gate (P:L844-L847): iteration i reads the memory updated through i - k_i
+    assert list(vers) == [max(0, i - plan_k) for i in (1, 2, 3)]
+
+
+@pytest.mark.parametrize("kk", [0, 1, 3])
+def test_plan_constant_equals_exact_schedule_bitwise(kk):
+    """k_i = k + 1 for every i reads v(i) = max(0, i - 1 - k), the exact
+    schedule of build staleness k (G8): the whole state must be the
+    same bits with random GRU weights (not only in the closed form)."""
+    cfg = CONFIGS["tiny"]
+    E, B = 3000, cfg.batch
+    src, dst, ts, _ = make_events(cfg, 5, E)
+    ef = edge_features(5, 0, E, cfg.edge_dim)
+    p = gru_params(cfg.mem_dim, cfg.mail_dim, cfg.time_dim)
+    nb = -(-E // B)
+    a, va = oracle.run_stream(cfg.num_nodes, src, dst, ts, ef, p, B, kk, "exact")
+    b, vb = oracle.run_stream(cfg.num_nodes, src, dst, ts, ef, p, B, kk, plan=[kk + 1] * nb)
+    assert np.array_equal(va, vb)
+    for key in ("mem", "mem_ts", "mail", "mail_ts"):
+        assert np.array_equal(a[key], b[key]), key
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_plan_bias_only_closed_form_random_plans(seed):
+    """P4 for plan mode: mem[w] = tanh(c)(1 - 2^-m_w), the integer replay run
+    with v(i) = max(0, i - k_i) written out here from Alg. 1's gate
+    (P:L844-L847), for random plans with 1 <= k_i <= 4."""
+    cfg = CONFIGS["tiny"]
+    E, B, N = 4000, 200, cfg.num_nodes
+    src, dst, ts, _ = make_events(cfg, 7 + seed, E)
+    M, He, Dt, c = 6, 4, 3, 0.9
+    prm = _bias_only(M, He, Dt, c)
+    ef = edge_features(0, 0, E, He)
+    nb = E // B
+    rng = np.random.default_rng(seed)
+    plan = rng.integers(1, 5, nb).astype(np.int32)
+    kmax = int(max(i - max(0, i - int(plan[i - 1])) for i in range(1, nb + 1))) - 1
+    st, vers = oracle.run_stream(N, src, dst, ts, ef, prm, B, kmax, plan=plan)
+    hist = [np.zeros(N, np.int64)]
+    for i in range(1, nb + 1):
+        v = max(0, i - int(plan[i - 1]))
+        assert vers[i - 1] == v
+        snap = hist[v]
+        live = hist[-1].copy()
+        for a in range((i - 1) * B, i * B):
+            for w in (src[a], dst[a]):
+                live[w] = snap[w] + 1
+        hist.append(live)
+    want = math.tanh(c) * (1.0 - 2.0 ** (-hist[-1].astype(np.float64)))
+    assert np.allclose(st["mem"], want[:, None], rtol=0, atol=3e-7)
+
+
 # ---------------------------------------------------------------- P6 message blocks
 @pytest.mark.parametrize("block", ["self", "other", "edge"])
 def test_p6_message_block_closed_forms(block):
