@@ -11,8 +11,13 @@ pays the ~6 us graph-launch gap per step (measured the same with and without
 the flush, so it is launch latency, not cache); that per-step protocol is
 timed as well and reported in `per_step_graphs`.  Inputs are resident in HBM
 for `value`; `e2e` copies each batch from pinned host memory and reads each
-commit's result back.  Default workload: the Wikipedia-shaped stream
-(BASELINE.json configs[1]) at its build staleness k=1.
+commit's result back.  Default workload: the GDELT-shaped stream (BASELINE.json
+configs[4], the largest single-GPU configuration: B = 4000, build k = 3), its
+first 1,000 batches (4M events, the prefix the GPU tests check against the
+oracle) run over a T-CSR built from the WHOLE 191M-event stream, so the
+sampler searches rows of full-stream length.  The K timed steps are repeated
+as whole K-step blocks until >= 0.1 s is timed (each block bracketed by
+synchronisation; `value` is the median block).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config wiki] [--impl mspipe|reference]
 
@@ -196,7 +201,8 @@ def run_mspipe(args):
         # NCCL: connect peers at communicator init, not lazily inside a graph capture
         os.environ.setdefault("NCCL_RUNTIME_CONNECT", "0")
         dist.init_process_group("nccl", device_id=dev)
-    w = make_workload(args.config, seed=args.seed, num_events=args.events)
+    events, tcsr_events = _window(args)
+    w = make_workload(args.config, seed=args.seed, num_events=events, tcsr_events=tcsr_events)
     cfg = w["cfg"]
     k = cfg.staleness_k if args.k is None else args.k
     mit = None
@@ -207,7 +213,9 @@ def run_mspipe(args):
                      schedule=args.schedule, mitigation=mit, fetch_mail=args.fetch_mail,
                      precision={"tc": _C.FP32_3XTF32, "bf16": _C.BF16, "simt": _C.FP32_SIMT}[args.gru],
                      features=args.features, node_dim=cfg.node_dim)
-    g = build_tcsr(cfg.num_nodes, w["src"], w["dst"], w["ts"], dev)
+    g = build_tcsr(cfg.num_nodes, *w.get("tcsr", (w["src"], w["dst"], w["ts"])), dev)
+    nnz = int(g.nbr.numel())
+    w.pop("tcsr", None)
     # N > 1: node-id-sharded memory over NCCL (row E); MSPIPE_BENCH_REPLICAS=1 runs
     # N independent single-GPU replicas instead (ablation)
     sharded = ws > 1 and os.environ.get("MSPIPE_BENCH_REPLICAS", "0") != "1"
@@ -216,6 +224,7 @@ def run_mspipe(args):
     nb = -(-E // (G * cfg.batch))
     U_host = _unique_counts(w["src"], w["dst"], G * cfg.batch)
     flush = torch.empty(FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
+    resident = {}
 
     def make_stage(staged):
         if sharded:
@@ -227,8 +236,10 @@ def run_mspipe(args):
             st = MemoryStage(sc, w["params"], g, dev)
         if staged:
             st.bind_host(w["src"], w["dst"], w["ts"], w["neg"], w["ef"])
-        else:
-            t = {kk: torch.from_numpy(w[kk]).to(dev) for kk in ("src", "dst", "ts", "neg", "ef")}
+        else:  # the device copy of the inputs is made once and shared by every stage
+            if not resident:
+                resident.update({kk: torch.from_numpy(w[kk]).to(dev) for kk in ("src", "dst", "ts", "neg", "ef")})
+            t = resident
             st.bind_resident(t["src"], t["dst"], t["ts"], t["neg"], t["ef"])
         if args.features:  # row F2: feature tables resident in HBM (the stream's edge features, node features)
             from synth import node_features
@@ -236,32 +247,28 @@ def run_mspipe(args):
                              torch.from_numpy(w["ef"]).to(dev))
         return st
 
-    def capture(st, timing):
+    def capture(st):
+        """One CUDA graph per step (the per-step protocol)."""
         s = torch.cuda.Stream(device=dev)
         st.timing = None
-        if timing:
-            st.reserve_timing_events(8 * sum(len(o) for o in st.step_ops()) + 16)
-        graphs, marks = [], []
-        for ops in st.step_ops():
-            before = {kk: len(v) for kk, v in (st.timing or {}).items()}
-            graphs.append(_C.StepGraph().capture(lambda: st.run_ops(ops), s))
-            marks.append({kk: (before.get(kk, 0), len(v)) for kk, v in (st.timing or {}).items()})
-        st.memory.reset()
-        return graphs, marks, s
+        graphs = [_C.StepGraph().capture(lambda ops=ops: st.run_ops(ops), s) for ops in st.step_ops()]
+        st.memory.reset(stream=s)
+        return graphs, s
 
-    def timed_run(st, graphs, marks, s, W, K, profile=False):
-        """W warm-up + K timed steps (wrapping over epochs); returns per-step ms and per-op ms."""
-        step_ms, op_ms = [], {}
-        pending = []
-        total = W + K
+    def timed_run(st, graphs, s, W, K):
+        """One K-step block from an epoch start: reset, W warm-up steps, K timed
+        steps (wrapping over epochs), L2 flushed before every step; per-step ms."""
+        step_ms, pending = [], []
         with torch.cuda.stream(s):
-            for n in range(total):
+            st.memory.reset(stream=s)
+            for n in range(W + K):
                 t = n % nb
                 if t == 0 and n > 0:
                     torch.cuda.synchronize()
-                    _collect(pending, step_ms, op_ms, st, marks)
-                    st.memory.reset()
-                if not profile and args.l2 == "flush":
+                    step_ms += [e0.elapsed_time(e1) for e0, e1 in pending]
+                    pending.clear()
+                    st.memory.reset(stream=s)
+                if args.l2 == "flush":
                     flush.fill_(float(n))
                 e0 = torch.cuda.Event(enable_timing=True)
                 e1 = torch.cuda.Event(enable_timing=True)
@@ -269,16 +276,22 @@ def run_mspipe(args):
                 graphs[t].replay(s)
                 e1.record(s)
                 if n >= W:
-                    pending.append((t, e0, e1))
+                    pending.append((e0, e1))
             torch.cuda.synchronize()
-        _collect(pending, step_ms, op_ms, st, marks)
-        return step_ms, op_ms
+        step_ms += [e0.elapsed_time(e1) for e0, e1 in pending]
+        return step_ms
 
-    def capture_groups(st, gs):
-        """One CUDA graph per gs consecutive steps (the epoch's last group may be shorter)."""
+    def capture_groups(st, gs, op=None):
+        """One CUDA graph per gs consecutive steps (the epoch's last group may be
+        shorter).  op: bracket that op (and nothing else) with event nodes; the
+        group's events are st.timing[op][a:b] / st.timing[op + '_end'][a:b]."""
         s = torch.cuda.Stream(device=dev)
         st.timing = None
+        st.timing_only = None
         sops = st.step_ops()
+        if op is not None:
+            st.timing_only = {op}
+            st.reserve_timing_events(2 * 2 * len(sops) + 16)
         groups = []
         for j in range(0, len(sops), gs):
             idx = list(range(j, min(j + gs, len(sops))))
@@ -286,24 +299,28 @@ def run_mspipe(args):
             def run_group(idx=idx):
                 for t in idx:  # e2e copies join only at the graph's end
                     st.run_ops(sops[t], join_copies=(t == idx[-1]))
-            groups.append((_C.StepGraph().capture(run_group, s), idx))
-        st.memory.reset()
+            a = len((st.timing or {}).get(op, []))
+            gr = _C.StepGraph().capture(run_group, s)
+            groups.append((gr, idx, a, len((st.timing or {}).get(op, []))))
+        st.memory.reset(stream=s)
         return groups, s
 
-    def timed_run_groups(st, groups, s, W, K, gs):
-        """Warm-up replays until >= W steps ran, then replays of full gs-step groups
-        until exactly K steps are timed (an epoch's shorter last group runs untimed);
-        L2 flushed before every replay, one event pair per replay.  Returns
-        (per-replay ms list, timed step indices)."""
-        ms, timed, pending = [], [], []
+    def timed_run_groups(st, groups, s, W, K, gs, op=None):
+        """One K-step block from an epoch start: reset, warm-up replays until >= W
+        steps ran, then replays of full gs-step groups until exactly K steps are
+        timed (an epoch's shorter last group runs untimed); L2 flushed before
+        every replay, one event pair per replay.  op: also returns the bracketed
+        op's durations (the host waits after every timed replay to read them)."""
+        ms, timed, pending, op_ms = [], [], [], []
         warm, r = 0, 0
         with torch.cuda.stream(s):
+            st.memory.reset(stream=s)
             while len(timed) + len(pending) * gs < K:
                 j = r % len(groups)
                 if j == 0 and r > 0:
                     torch.cuda.synchronize()
-                    st.memory.reset()
-                graph, idx = groups[j]
+                    st.memory.reset(stream=s)
+                graph, idx, a, b = groups[j]
                 if args.l2 == "flush":
                     flush.fill_(float(r))
                 if warm >= W and len(idx) == gs:
@@ -313,6 +330,9 @@ def run_mspipe(args):
                     graph.replay(s)
                     e1.record(s)
                     pending.append((e0, e1, idx))
+                    if op is not None:
+                        e1.synchronize()
+                        op_ms += [st.timing[op][q].elapsed_time(st.timing[op + "_end"][q]) for q in range(a, b)]
                 else:
                     graph.replay(s)
                     warm += len(idx)
@@ -321,146 +341,126 @@ def run_mspipe(args):
         for e0, e1, idx in pending:
             ms.append(e0.elapsed_time(e1))
             timed.extend(idx)
-        return ms, timed
+        return ms, timed, op_ms
 
-    def _collect(pending, step_ms, op_ms, st, marks):
-        for t, e0, e1 in pending:
-            step_ms.append(e0.elapsed_time(e1))
-            if st.timing:
-                for name in ("prep", "build", "sample", "dedup", "fetch", "update", "writeback", "features"):
-                    a, b = marks[t].get(name, (0, 0))
-                    ends = st.timing.get(name + "_end", [])
-                    for q in range(a, b):
-                        op_ms.setdefault(name, []).append(st.timing[name][q].elapsed_time(ends[q]))
-                        # offsets inside the step (diagnostic timeline)
-                        op_ms.setdefault(name + "@start", []).append(e0.elapsed_time(st.timing[name][q]))
-                        op_ms.setdefault(name + "@end", []).append(e0.elapsed_time(ends[q]))
-        pending.clear()
+    def max_over_ranks(x):
+        if ws == 1:
+            return x
+        tt = torch.tensor([x], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        return float(tt.item())
 
     W, K = args.warmup, args.steps
-    # ---- device-resident run (the `value`) ---------------------------------
-    # The timed graphs carry no per-op event nodes (each one is an extra graph
-    # node on the critical path); the per-op breakdown for the roofline comes
-    # from a second, instrumented replay of the same steps right after.
     # steps per captured graph: launch latency between graphs (~6 us, the same
     # with or without the L2 flush) is paid once per graph, not once per step
     gs = 1
     if ws == 1 and not args.profile:  # the largest divisor of K up to --graph-steps (exactly K steps timed)
         gs = max(d for d in range(1, max(1, min(args.graph_steps, nb - 1)) + 1) if K % d == 0)
-    st = make_stage(False)
-    if gs > 1:
-        groups, s = capture_groups(st, gs)
-    else:
-        graphs, marks, s = capture(st, timing=False)
-    if ws > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    with ClockSampler(local) as clk:
+
+    def run_blocks(staged):
+        """K-step blocks (each from an epoch start, W warm-up steps untimed) until
+        >= MIN_TIMED_MS is timed: the block count comes from the first block's
+        max-over-ranks time, so every rank runs the same number.  Returns a list
+        of (max-over-ranks ms of the block, timed batch indices) and the clocks."""
+        st = make_stage(staged)
         if gs > 1:
-            step_ms, timed_batches = timed_run_groups(st, groups, s, W, K, gs)
+            groups, s = capture_groups(st, gs)
         else:
-            step_ms, _ = timed_run(st, graphs, marks, s, W, K, profile=args.profile)
-            timed_batches = [(W + q) % nb for q in range(K)]
-    _C.check(s)
+            graphs, s = capture(st)
+        if ws > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        blocks, nblocks = [], 1
+        with ClockSampler(local) as clk:
+            while len(blocks) < nblocks:
+                if gs > 1:
+                    step_ms, tb, _ = timed_run_groups(st, groups, s, W, K, gs)
+                else:
+                    step_ms = timed_run(st, graphs, s, W, K)
+                    tb = [(W + q) % nb for q in range(K)]
+                if ws > 1:
+                    dist.barrier()
+                blocks.append((max_over_ranks(float(sum(step_ms))), tb))
+                if len(blocks) == 1 and not args.profile:
+                    nblocks = int(min(MAX_BLOCKS, max(1, -(-MIN_TIMED_MS // max(blocks[0][0], 1e-3)))))
+        _C.check(s)
+        return blocks, clk.summary(), st
+
+    def block_value(blocks):
+        """(median block rate, its ms per step, every block's rate)."""
+        rates = [sum(min(G * cfg.batch, E - b * G * cfg.batch) for b in tb) * (ws if not sharded else 1) / (ms / 1e3)
+                 for ms, tb in blocks]
+        order = sorted(range(len(rates)), key=rates.__getitem__)
+        med = order[len(order) // 2]
+        return rates[med], blocks[med][0] / K, rates, blocks[med][1]
+
+    # ---- device-resident run (the `value`) ---------------------------------
+    blocks, clocks, st = run_blocks(False)
+    value, ms_step, rates, timed_batches = block_value(blocks)
     per_step = None
     if gs > 1:
         # the same steps with one graph per step (L2 flushed before each): the
         # per-step protocol, reported beside the grouped headline
-        del groups
         st1 = make_stage(False)
-        graphs1, marks1, s1 = capture(st1, timing=False)
-        ms1, _ = timed_run(st1, graphs1, marks1, s1, W, K)
+        graphs1, s1 = capture(st1)
+        ms1 = timed_run(st1, graphs1, s1, W, K)
         _C.check(s1)
-        del graphs1
+        del graphs1, st1
         tb1 = [(W + q) % nb for q in range(K)]
         ev1 = sum(min(cfg.batch, E - b * cfg.batch) for b in tb1)
         per_step = {"value": ev1 / (sum(ms1) / 1e3), "unit": UNIT, "ms_per_step": sum(ms1) / K,
                     "l2": "flushed (256 MiB write) before every step, one CUDA graph per step"}
-    else:
-        del graphs
-    st_i = make_stage(False)
-    graphs_i, marks_i, s_i = capture(st_i, timing=True)
-    step_ms_instr, op_ms = timed_run(st_i, graphs_i, marks_i, s_i, W, K, profile=args.profile)
-    _C.check(s_i)
-    del graphs_i
-    tot_ms = float(sum(step_ms))
-    if ws > 1:
-        tt = torch.tensor([tot_ms], device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        tot_ms = float(tt.item())
-        dist.barrier()
-    # events of all ranks in the timed global batches (replicas: every rank its own copy)
-    events = sum(min(G * cfg.batch, E - b * G * cfg.batch) for b in timed_batches) * (ws if not sharded else 1)
-    value = events / (tot_ms / 1e3)
+    # ---- per-op durations: the same grouped steps, ONE op bracketed per run --
+    op_mean, op_instr_step = {}, {}
+    if ws == 1 and getattr(st, "fused", False) and not args.profile:
+        for op in ("prep", "update"):
+            sti = make_stage(False)
+            gi, si = capture_groups(sti, gs, op=op)
+            ms_i, _, opm = timed_run_groups(sti, gi, si, W, K, gs, op=op)
+            _C.check(si)
+            del gi, sti
+            if opm:
+                op_mean[op] = float(np.mean(opm))
+                op_instr_step[op] = float(sum(ms_i)) / K
     # ---- roofline of the dominant op ---------------------------------------
     peaks = _peaks()
     mean_U = float(np.mean(U_host[timed_batches]))
     alg = algorithmic(cfg, sc, mean_U)
-    op_mean = {kk: float(np.mean(v)) for kk, v in op_ms.items() if v and "@" not in kk}
-    timeline = {kk: float(np.mean(v)) for kk, v in op_ms.items() if v and "@" in kk}
+    traffic = _ncu_traffic(args.config)
     dom = max(op_mean, key=op_mean.get) if op_mean else "update"
-    clocks = clk.summary()
-    if dom == "update" and args.gru == "bf16":
-        peak_tc = peaks["bf16_tflops_sustained"]
-        ach = alg["update_flops"] / (op_mean[dom] / 1e3) / 1e12
-        roof = {"kernel": "k_gru_tc<bf16> via mspipe_gru_apply_commit (GEMM + gates + LWW commit epilogue)",
-                "bound": "tensor", "achieved": ach, "peak": peak_tc, "unit": "TFLOP/s", "frac": ach / peak_tc,
-                "peak_source": f"{peaks['source']} bf16 sustained"}
-    elif dom == "update" and args.gru == "tc":
-        # 3xTF32: each useful fp32 MAC costs 3 tf32 MACs; tf32 dense = bf16 x (1.1 / 2.25)
-        # nominal ratio (B200_PROFILING.md); sustained bf16 figure (kernel timed inside a long step)
-        peak_tc = peaks["bf16_tflops_sustained"] * (1.1 / 2.25) / 3.0
-        ach = alg["update_flops"] / (op_mean[dom] / 1e3) / 1e12
-        kname = ("k_gru_tc via mspipe_gru_apply_commit (GEMM + gates + LWW commit epilogue)"
-                 if getattr(st, "fused", False) else "k_build_x + k_gru_tc via mspipe_memory_update")
-        roof = {"kernel": kname, "bound": "tensor", "achieved": ach,
-                "peak": peak_tc, "unit": "TFLOP/s", "frac": ach / peak_tc,
-                "peak_source": f"{peaks['source']} bf16 sustained x 1.1/2.25 (tf32) / 3 (3xTF32 passes)"}
-    elif dom == "update":
-        sm_clock = 1965.0
-        peak_alu = 148 * FP32_FMA_LANES_PER_SM * 2 * sm_clock * 1e6 / 1e12
-        ach = alg["update_flops"] / (op_mean[dom] / 1e3) / 1e12
-        roof = {"kernel": "k_build_x + k_gru_simt via mspipe_memory_update", "bound": "alu", "achieved": ach,
-                "peak": peak_alu, "unit": "TFLOP/s", "frac": ach / peak_alu,
-                "peak_source": "148 SMs x 128 FP32 lanes x 2 x 1965 MHz (guide unit counts, max clock)"}
-    else:
-        ach = alg[dom] / (op_mean[dom] / 1e3) / 1e9
-        roof = {"kernel": dom, "bound": "hbm", "achieved": ach, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                "frac": ach / peaks["hbm_gbs"], "peak_source": peaks["source"]}
-    roof["traffic"] = _ncu_traffic(args.config, dom)
-    if roof.get("bound") == "tensor":
-        roof["note"] = (f"{mean_U:.0f} GEMM rows per batch ({int(-(-mean_U // 128))} M tiles of 128): the contraction "
-                        "is a few us of tensor work; the launch is bound by dependent latency (operand chunk "
-                        "loads, the K-split partial exchange, the commit epilogue), DESIGN.md section 5")
-    roof["op_ms_mean"] = op_mean
-    roof["op_share"] = {kk: v / sum(op_mean.values()) for kk, v in op_mean.items()} if op_mean else None
-    roof["step_timeline_ms"] = dict(sorted(timeline.items(), key=lambda kv: kv[1]))
-    roof["instrumented_ms_per_step"] = float(np.mean(step_ms_instr)) if step_ms_instr else None
-    roof["alg_bytes_per_launch"] = {kk: alg[kk] for kk in op_mean if kk in alg}
+    rooflines = {}
+    for op, t_ms in op_mean.items():
+        if op == "update":
+            r = _tensor_roofline(args.gru, alg["update_flops"], t_ms, peaks, st)
+        else:
+            ach = alg[op] / (t_ms / 1e3) / 1e9
+            r = {"kernel": "k_prep (A1 sampler + A2 dedup + A3 subgraph gather)", "bound": "hbm", "achieved": ach,
+                 "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": ach / peaks["hbm_gbs"],
+                 "peak_source": peaks["source"] + " copy bandwidth", "bytes_per_launch": alg[op]}
+        r["launch_ms_mean"] = t_ms
+        r["launch_ms_source"] = ("CUDA events around this op only, inside the same grouped step graphs (host waits "
+                                 "after each replay); instrumented ms/step %.4f vs %.4f uninstrumented"
+                                 % (op_instr_step[op], ms_step))
+        r["launch_within_step"] = bool(t_ms <= op_instr_step[op] + 1e-9)
+        ncu = (traffic or {}).get({"prep": "k_prep", "update": "k_gru_tc"}[op])
+        r["traffic"] = ncu["dram_bytes"] if ncu else None
+        if ncu:
+            r["ncu"] = ncu
+        rooflines[op] = r
+    roof = rooflines.get(dom) or _tensor_roofline(args.gru, alg["update_flops"], ms_step, peaks, st)
+    roof["dominant_of"] = {k2: v for k2, v in op_mean.items()}
     roof["gru_flops_per_launch"] = alg["update_flops"]
-    gather_op = "prep" if "prep" in op_mean else ("fetch" if "fetch" in op_mean else None)
-    if gather_op and dom != gather_op:
-        # the gather/scatter kernel against HBM (north star: >= 60 % of the HBM roofline)
-        ach_g = alg[gather_op] / (op_mean[gather_op] / 1e3) / 1e9
-        roof_gather = {"kernel": "k_prep (A1 sampler + A2 dedup + A3 gather)" if gather_op == "prep"
-                       else "k_fetch_gather", "bound": "hbm", "achieved": ach_g, "peak": peaks["hbm_gbs"],
-                       "unit": "GB/s", "frac": ach_g / peaks["hbm_gbs"], "bytes_per_launch": alg[gather_op],
-                       "traffic": _ncu_traffic(args.config, gather_op)}
-    else:
-        roof_gather = None
+    roof_gather = rooflines.get("prep")
     roof_features = None
-    if "features" in op_mean:
-        ach_f = alg["features"] / (op_mean["features"] / 1e3) / 1e9
-        roof_features = {"kernel": "k_feature_fetch (row F2)", "bound": "hbm", "achieved": ach_f,
-                         "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": ach_f / peaks["hbm_gbs"],
-                         "bytes_per_launch": alg["features"]}
     out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": K, "warmup": W,
-           "ms_per_step": tot_ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+           "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
            "dtype": "bf16-gemm/f32" if args.gru == "bf16" else "f32", "data": "synthetic",
-           "config": {"workload": args.config, "events": int(len(w["src"])), "num_nodes": cfg.num_nodes,
+           "config": {"workload": args.config, "events": int(E), "tcsr_events": int(tcsr_events or E),
+                      "tcsr_nnz": nnz, "num_nodes": cfg.num_nodes,
                       "batch": cfg.batch, "staleness_k": k, "schedule": args.schedule, "fanout": cfg.fanout,
                       "mem_dim": cfg.mem_dim, "edge_dim": cfg.edge_dim, "time_dim": cfg.time_dim,
-                      "mitigation": bool(mit), "features": args.features, "fetch_mail": args.fetch_mail, "gru": {"tc": "fp32-3xtf32-tcgen05", "bf16": "bf16-operands-tcgen05 (fp32 accumulate/state)",
+                      "mitigation": bool(mit), "features": args.features, "fetch_mail": args.fetch_mail,
+                      "gru": {"tc": "fp32-3xtf32-tcgen05", "bf16": "bf16-operands-tcgen05 (fp32 accumulate/state)",
                               "simt": "fp32-simt"}[args.gru],
                       "l2": (("flushed (256 MiB write) between timed steps, outside the timed events" if gs == 1 else
                               f"flushed (256 MiB write) before every replay of a {gs}-step CUDA graph, outside "
@@ -470,39 +470,32 @@ def run_mspipe(args):
                       "parallelism": ("single" if ws == 1 else
                                       f"shard{ws}: node-id-sharded memory, NCCL all-to-all fetch + write-back, "
                                       f"global batch {G * cfg.batch}" if sharded else f"replicas{ws}")},
-           "roofline": roof, "roofline_gather": roof_gather, "roofline_features": roof_features, "per_step_graphs": per_step, "gpu_launches": _launches(st.step_ops(), timed_batches, bool(mit),
-                                                       getattr(st, "fused", False), sharded, args.features,
-                                                       getattr(st, "gemm_build", False)), "clocks": clocks}
+           "blocks": {"count": len(blocks), "timed_ms_total": float(sum(b[0] for b in blocks)),
+                      "rates": rates, "rule": f"K-step blocks (reset + W warm-up each) until >= {MIN_TIMED_MS} ms; "
+                                              "value = the median block"},
+           "roofline": roof, "roofline_gather": roof_gather, "roofline_features": roof_features,
+           "per_step_graphs": per_step,
+           "gpu_launches": _launches(st.step_ops(), timed_batches, bool(mit), getattr(st, "fused", False), sharded,
+                                     args.features, getattr(st, "gemm_build", False)),
+           "clocks": clocks}
+    if sharded:
+        out["exchange"] = _exchange_report(st, cfg, ws, ms_step)
     if args.profile:
         if rank == 0:
             print(json.dumps(out))
         return
+    del st
     # ---- e2e: host buffers through the same C-ABI calls ---------------------
-    st2 = make_stage(True)
-    if gs > 1:
-        groups2, s2 = capture_groups(st2, gs)
-    else:
-        graphs2, marks2, s2 = capture(st2, timing=False)
-    if ws > 1:
-        dist.barrier()
-    if gs > 1:
-        step2, tb2 = timed_run_groups(st2, groups2, s2, W, K, gs)
-        graphs2 = groups2
-    else:
-        step2, _ = timed_run(st2, graphs2, marks2, s2, W, K)
-        tb2 = timed_batches
-    _C.check(s2)
-    events2 = sum(min(G * cfg.batch, E - b * G * cfg.batch) for b in tb2) * (ws if not sharded else 1)
-    tot2 = float(sum(step2))
-    if ws > 1:
-        tt = torch.tensor([tot2], device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        tot2 = float(tt.item())
-    out["e2e"] = {"value": events2 / (tot2 / 1e3), "unit": UNIT,
-                  "h2d_bytes_per_step": st2.h2d_bytes_per_batch(), "d2h_bytes_per_step": (st2.d2h_bytes_per_batch(mean_U) if not sharded
-                                                                         else st2.d2h_bytes_per_batch()),
-                  "ms_per_step": tot2 / K}
-    del graphs2
+    blocks2, _, st2 = run_blocks(True)
+    v2, ms2, _, _ = block_value(blocks2)
+    out["e2e"] = {"value": v2, "unit": UNIT, "h2d_bytes_per_step": st2.h2d_bytes_per_batch(),
+                  "d2h_bytes_per_step": (st2.d2h_bytes_per_batch(mean_U) if not sharded
+                                         else st2.d2h_bytes_per_batch()),
+                  "ms_per_step": ms2, "blocks": len(blocks2)}
+    del st2
+    # ---- HBM probe: A3 / A7 kernels on a table that misses L2
+    if rank == 0 and ws == 1 and not args.no_probe:
+        out["hbm_probe"] = hbm_probe(dev, cfg, peaks, flush, args.seed)
     # ---- CPU oracle beside it (rank 0, N = 1 only) ---------------------------
     if rank == 0 and ws == 1 and not args.no_cpu:
         out["cpu_baseline"] = cpu_baseline(w, cfg, k, args.schedule, mit, args.cpu_events)
@@ -510,6 +503,121 @@ def run_mspipe(args):
         print(json.dumps(out))
     if ws > 1:
         dist.destroy_process_group()
+
+
+MIN_TIMED_MS = 100.0
+MAX_BLOCKS = 50
+
+
+def _window(args):
+    """(events the batches run over, events the T-CSR is built from)."""
+    if args.config == "gdelt":
+        ev = args.events if args.events is not None else GDELT_WINDOW
+        tev = args.tcsr_events if args.tcsr_events is not None else None  # None: the whole stream
+        from synth import CONFIGS
+        return ev, (CONFIGS["gdelt"].num_events if tev is None else max(tev, ev))
+    return args.events, (max(args.tcsr_events, args.events or 0) if args.tcsr_events else None)
+
+
+GDELT_WINDOW = 4_000_000  # the first 1,000 batches (SURVEY D.7), parity-tested against the oracle
+
+
+def _tensor_roofline(gru, flops, t_ms, peaks, st):
+    ach = flops / (t_ms / 1e3) / 1e12
+    if gru == "bf16":
+        peak = peaks["bf16_tflops_sustained"]
+        return {"kernel": "k_gru_tc<bf16> via mspipe_gru_apply_commit (GEMM + gates + LWW commit epilogue)",
+                "bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
+                "peak_source": f"{peaks['source']} bf16 sustained"}
+    if gru == "tc":
+        # 3xTF32: each useful fp32 MAC costs 3 tf32 MACs; tf32 dense = bf16 x (1.1 / 2.25)
+        # nominal ratio (B200_PROFILING.md); sustained bf16 figure (kernel timed inside a long step)
+        peak = peaks["bf16_tflops_sustained"] * (1.1 / 2.25) / 3.0
+        kname = ("k_gru_tc via mspipe_gru_apply_commit (GEMM + gates + LWW commit epilogue)"
+                 if getattr(st, "fused", False) else "k_build_x + k_gru_tc via mspipe_memory_update")
+        return {"kernel": kname, "bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s",
+                "frac": ach / peak,
+                "peak_source": f"{peaks['source']} bf16 sustained x 1.1/2.25 (tf32) / 3 (3xTF32 passes)"}
+    peak = 148 * FP32_FMA_LANES_PER_SM * 2 * 1965.0 * 1e6 / 1e12
+    return {"kernel": "k_build_x + k_gru_simt via mspipe_memory_update", "bound": "alu", "achieved": ach,
+            "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
+            "peak_source": "148 SMs x 128 FP32 lanes x 2 x 1965 MHz (guide unit counts, max clock)"}
+
+
+def _exchange_report(st, cfg, ws, ms_step):
+    """Row E: bytes each rank sends per global iteration over NCCL (fetch ids +
+    replies, commit records) and the achieved rate against NVLink 5's 900 GB/s
+    per direction."""
+    try:
+        b = st.exchange_bytes_per_iter()
+    except Exception as e:  # noqa: BLE001
+        return {"error": str(e)}
+    return {"bytes_per_iter_per_rank": b, "nvlink_gbs": b / (ms_step / 1e3) / 1e9 if ms_step > 0 else None,
+            "nvlink_peak_gbs": 900.0, "note": "bytes over the whole step time (an upper bound on the exchange "
+                                              "time), so the rate is a lower bound on the link rate"}
+
+
+def hbm_probe(dev, cfg, peaks, flush, seed):
+    """the product's A3 gather (mspipe_memory_fetch ->
+    k_fetch_gather) and A7 scatter (mspipe_memory_writeback -> k_writeback) on
+    N = 10^7-row tables (mem 4 GB + mail ~15 GB) with uniform ids, so rows miss
+    the 126 MB L2: effective GB/s (algorithmic bytes / CUDA-event time, L2
+    flushed before every launch) against the measured copy bandwidth."""
+    import torch
+    from paper_2402_15113_b200 import _C
+    N, M, He = 10_000_000, cfg.mem_dim, cfg.edge_dim
+    try:
+        h = _C.MemoryHandle(N, M, He, 0, dev)
+    except Exception as e:  # noqa: BLE001
+        return {"error": f"tables: {e}"}
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(seed + 77)
+    stride = h.mail_stride
+    row = 4 * M + 8
+    res = {"num_nodes": N, "table_bytes": N * (4 * M + 8 + 4 * stride + 8), "ids": "uniform over [0, N)",
+           "l2": "flushed (256 MiB write) before every launch"}
+
+    def timeit(fn, reps=20):
+        ts_ = []
+        for r in range(reps + 2):
+            flush.fill_(float(r))
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+            fn()
+            e1.record()
+            e1.synchronize()
+            if r >= 2:
+                ts_.append(e0.elapsed_time(e1))
+        return float(np.median(ts_))
+
+    for n, tag in ((3 * cfg.batch * (cfg.fanout + 1), "batch"), (1 << 20, "large")):
+        ids = torch.randint(0, N, (n,), generator=gen, device=dev, dtype=torch.int32)
+        om = torch.empty((n, M), device=dev)
+        ots = torch.empty(n, dtype=torch.float64, device=dev)
+        t = timeit(lambda: _C.memory_fetch(h, 1, ids, om, ots))
+        b = n * (4 + 2 * row)
+        res[f"fetch_{tag}"] = {"kernel": "k_fetch_gather (A3, mem rows + mem_ts)", "rows": n, "bytes": b, "ms": t,
+                               "achieved_gbs": b / (t / 1e3) / 1e9, "frac": b / (t / 1e3) / 1e9 / peaks["hbm_gbs"]}
+        del om, ots
+    for U, tag in ((2 * cfg.batch, "batch"), (1 << 18, "large")):
+        upd = _C.alloc_update(U // 2, M, stride, dev)
+        upd["nodes"][:U] = torch.randperm(N, generator=gen, device=dev)[:U].int()
+        upd["num"].fill_(U)
+        upd["mem"].uniform_(-1, 1, generator=gen)
+        upd["mail"].uniform_(-1, 1, generator=gen)
+        upd["ts"].fill_(1.0)
+        t = timeit(lambda: _C.memory_writeback(h, h.committed + 1, upd))
+        b = U * (4 + 2 * (4 * M + 8 + 4 * stride + 8))
+        res[f"writeback_{tag}"] = {"kernel": "k_writeback (A7, mem + mem_ts + mail + mail_ts rows)", "rows": U,
+                                   "bytes": b, "ms": t, "achieved_gbs": b / (t / 1e3) / 1e9,
+                                   "frac": b / (t / 1e3) / 1e9 / peaks["hbm_gbs"]}
+        del upd
+    _C.check()
+    del h
+    torch.cuda.empty_cache()
+    res["peak_gbs"] = peaks["hbm_gbs"]
+    return res
 
 
 def _launches(steps, timed_batches, mit, fused, sharded=False, features=False, gemm_build=False):
@@ -529,38 +637,67 @@ def _launches(steps, timed_batches, mit, fused, sharded=False, features=False, g
     return int(sum(per[op] for t in timed_batches for op, _ in steps[t]))
 
 
-def _ncu_traffic(config, dom):
+def _ncu_traffic(config):
+    """Per-launch DRAM bytes and L2 hit rate of each kernel from ONE committed
+    `ncu --set full` capture of this config (profiles/ncu_traffic.json, written
+    by scripts/make_profiles.py from the .ncu-rep summaries), or None."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if not os.path.exists(p):
         return None
     with open(p) as f:
         d = json.load(f)
-    return d.get(config, {}).get(dom)
+    return d.get(config)
 
 
 CPU_MIN_S = 10.0
 
 
+def _cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 def cpu_baseline(w, cfg, k, schedule, mit, n_events):
+    """The oracle as it stands on the host's cores (T = all usable threads), on a
+    bounded sample of the same workload: whole passes over its first n_events
+    events until >= CPU_MIN_S; plus one pass of a smaller sample at T = 1."""
     import oracle
     threads = len(os.sched_getaffinity(0))
-    oracle.set_threads(threads)
     E = min(n_events, len(w["src"]))
     sl = slice(0, E)
+
+    def one(sl_):
+        oracle.run_stream(cfg.num_nodes, w["src"][sl_], w["dst"][sl_], w["ts"][sl_], w["ef"][sl_], w["params"],
+                          cfg.batch, k, schedule, mitigation=mit, fanout=cfg.fanout, neg=w["neg"][sl_])
+
+    oracle.set_threads(threads)
     # whole epochs of the sample (each from the initial state, as the GPU epochs)
     # until at least CPU_MIN_S of CPU work
     passes, t0 = 0, time.perf_counter()
     while True:
-        oracle.run_stream(cfg.num_nodes, w["src"][sl], w["dst"][sl], w["ts"][sl], w["ef"][sl], w["params"],
-                          cfg.batch, k, schedule, mitigation=mit, fanout=cfg.fanout, neg=w["neg"][sl])
+        one(sl)
         passes += 1
         dt = time.perf_counter() - t0
         if dt >= CPU_MIN_S or passes >= 50:
             break
-    return {"value": passes * E / dt, "unit": UNIT, "cores": threads, "kind": "oracle",
+    E1 = min(E, 20 * cfg.batch)
+    oracle.set_threads(1)
+    t1 = time.perf_counter()
+    one(slice(0, E1))
+    dt1 = time.perf_counter() - t1
+    oracle.set_threads(threads)
+    return {"value": passes * E / dt, "unit": UNIT, "cores": threads, "kind": "oracle", "cpu_model": _cpu_model(),
             "sample": f"first {E} events ({-(-E // cfg.batch)} batches) of the same stream x {passes} epoch(s), "
                       f"full per-batch path (sampler, subgraph gather, dedup, {'mitigation, ' if mit else ''}"
-                      f"message, f64 GRU, commit), {dt:.1f} s"}
+                      f"message, f64 GRU, commit), {dt:.1f} s",
+            "t1": {"value": E1 / dt1, "unit": UNIT, "cores": 1,
+                   "sample": f"first {E1} events ({-(-E1 // cfg.batch)} batches), one pass, {dt1:.1f} s"}}
 
 
 def run_reference(args):
@@ -571,7 +708,9 @@ def run_reference(args):
     import oracle
     from paper_2402_15113_b200.graph import gamma_quantile
     from synth import make_workload
-    w = make_workload(args.config, seed=args.seed, num_events=args.events)
+    # the batches' window only: the oracle's sampler needs no events past it
+    # (strict ts < t_q), so its prefix-built graph answers as the full T-CSR does
+    w = make_workload(args.config, seed=args.seed, num_events=_window(args)[0])
     cfg = w["cfg"]
     k = cfg.staleness_k if args.k is None else args.k
     mit = None
@@ -611,7 +750,7 @@ def run_reference(args):
            "config": {"workload": args.config, "batch": cfg.batch, "staleness_k": k, "schedule": args.schedule,
                       "fanout": cfg.fanout, "mem_dim": cfg.mem_dim, "edge_dim": cfg.edge_dim,
                       "mitigation": bool(mit), "parallelism": "host cores"},
-           "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle",
+           "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle", "cpu_model": _cpu_model(),
                             "sample": f"batches {W + 1}..{W + K} of the stream (after {W} untimed), full per-batch path"},
            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out))
@@ -623,7 +762,8 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="mspipe", choices=["mspipe", "reference"])
-    ap.add_argument("--config", default="wiki")
+    ap.add_argument("--config", default="gdelt",
+                    help="workload (synth.CONFIGS); default gdelt, the largest single-GPU configuration")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--k", type=int, default=None)
     ap.add_argument("--schedule", default="exact", choices=["exact", "grouped"])
@@ -639,7 +779,12 @@ def main():
     ap.add_argument("--features", action="store_true",
                     help="also run row F2 (feature fetch of the sampled subgraphs) in every step")
     ap.add_argument("--events", type=int, default=None,
-                    help="first N events of the config's stream (default: all; GDELT's 191M needs a cap)")
+                    help="first N events of the config's stream the batches run over (default: all; GDELT: the "
+                         "first 4,000,000 = 1,000 batches)")
+    ap.add_argument("--tcsr-events", type=int, default=None,
+                    help="events the sampler's T-CSR is built from (default: the whole stream for GDELT, else "
+                         "--events)")
+    ap.add_argument("--no-probe", action="store_true", help="skip the N = 10^7 HBM probe of the A3/A7 kernels")
     ap.add_argument("--profile", action="store_true", help="short run for ncu: no flush/e2e/cpu")
     ap.add_argument("--graph-steps", type=int, default=8,
                     help="consecutive steps captured per CUDA graph (1: one graph per step); N = 1 only")

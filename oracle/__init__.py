@@ -55,6 +55,8 @@ def lib():
         L.orc_run_stream.argtypes = [i64, i64, P, P, P, P, i32, i32, i32, P, P, P, P, P, P, i64,
                                      i32, i32, i32, f32, f64, i32, i32, P, P, P, P, i64, P, P, i32, P, i32]
         L.orc_run_stream.restype = i64
+        L.orc_run_stream_ex.argtypes = L.orc_run_stream.argtypes + [P]
+        L.orc_run_stream_ex.restype = i64
         L.orc_delta_t_population.argtypes = [i64, i64, P, P, P, P]
         L.orc_delta_t_population.restype = i64
         L.orc_quantile_nearest_rank.argtypes = [i64, P, f64]
@@ -200,13 +202,22 @@ def new_state(num_nodes, mem_dim, edge_dim):
                 mail=np.zeros((num_nodes, Dm), np.float32), mail_ts=np.zeros(num_nodes))
 
 
+class _Dump(C.Structure):
+    _fields_ = [("n", C.c_int64), ("batches", C.c_void_p), ("sub_ids", C.c_void_p), ("mem", C.c_void_p),
+                ("mem_ts", C.c_void_p)]
+
+
 def run_stream(num_nodes, src, dst, ts, ef, params, batch, k, schedule="exact", mitigation=None,
-               fanout=10, state=None, max_batches=-1, neg=None, plan=None, mailbox="immediate", cell="gru"):
+               fanout=10, state=None, max_batches=-1, neg=None, plan=None, mailbox="immediate", cell="gru",
+               dump_batches=None):
     """C.2 O1-O8 over the stream; returns (final state, per-batch versions).
     With `neg`, every batch also runs A1 on its 3B roots and gathers the
     snapshot rows of the subgraph (the whole per-batch path, for timing).
     plan (row F1): per-iteration paper staleness k_i (v(i) = max(0, i - k_i));
-    k must then be >= max_i (i - v(i)) - 1 (copies kept)."""
+    k must then be >= max_i (i - v(i)) - 1 (copies kept).
+    dump_batches (needs neg): 1-based iterations whose A3s output (subgraph ids
+    [3B, fanout+1], rows of S_{v(i)} and their mem_ts) is returned as a third
+    value {"batches", "sub_ids", "mem", "mem_ts"} (P:L818, P:L1153)."""
     planc = None if plan is None else _c(plan, np.int32)
     negc = None if neg is None else _c(neg, np.int32)
     src, dst, ts = _c(src, np.int32), _c(dst, np.int32), _c(ts, np.float64)
@@ -222,15 +233,28 @@ def run_stream(num_nodes, src, dst, ts, ef, params, batch, k, schedule="exact", 
         nb = min(nb, max_batches)
     vers = np.zeros(max(nb, 1), np.int64)
     mit = mitigation
-    r = lib().orc_run_stream(
+    dump, dres = None, None
+    if dump_batches is not None:
+        if negc is None:
+            raise ValueError("dump_batches needs neg (the subgraph roots)")
+        db = np.ascontiguousarray(np.sort(np.asarray(dump_batches, np.int64)))
+        slots = 3 * batch * (fanout + 1)
+        dres = dict(batches=db, sub_ids=np.full((len(db), slots), -2, np.int32),
+                    mem=np.zeros((len(db), slots, M), np.float32), mem_ts=np.zeros((len(db), slots)))
+        dump = _Dump(len(db), db.ctypes.data, dres["sub_ids"].ctypes.data, dres["mem"].ctypes.data,
+                     dres["mem_ts"].ctypes.data)
+    r = lib().orc_run_stream_ex(
         num_nodes, E, _p(src), _p(dst), _p(ts), _p(ef), M, He, Dt, _p(pr["w_ih"]),
         _p(pr["w_hh"]), _p(pr["b_ih"]), _p(pr["b_hh"]), _p(pr["time_w"]), _p(pr["time_b"]), batch,
         k, 1 if schedule == "grouped" else 0, 1 if mit else 0, float(mit["lam"]) if mit else 1.0,
         float(mit["gamma"]) if mit else 0.0, int(mit["n_sim"]) if mit else 5, fanout,
         _p(st["mem"]), _p(st["mem_ts"]), _p(st["mail"]), _p(st["mail_ts"]), max_batches, _p(vers),
-        _p(negc), 0 if negc is None else 1, _p(planc), _variant(mailbox, cell))
+        _p(negc), 0 if negc is None else 1, _p(planc), _variant(mailbox, cell),
+        C.byref(dump) if dump is not None else None)
     if r < 0:
         raise ValueError(f"orc_run_stream rc={r}")
+    if dres is not None:
+        return st, vers[:r], dres
     return st, vers[:r]
 
 

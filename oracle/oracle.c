@@ -498,6 +498,28 @@ int64_t orc_snapshot_version(int64_t i, int32_t k, int32_t schedule) {
  * final state out).  Keeps k+1 full state copies (one per version still
  * readable).  Returns number of batches run.
  * ---------------------------------------------------------------------- */
+/* Test hook (no arithmetic): copies of the A3s output (subgraph ids and the
+ * snapshot rows S_{v(i)} gathered for them) of the listed batches, so tests
+ * can compare the GPU's subgraph fetch with the oracle's, batch by batch.
+ * batches: ascending 1-based iterations; outputs [n, 3B(fanout+1)(, M)]. */
+typedef struct {
+  int64_t n;
+  const int64_t* batches;
+  int32_t* sub_ids;
+  float* mem;
+  double* mem_ts;
+} orc_dump;
+
+int64_t orc_run_stream_ex(int64_t N, int64_t E, const int32_t* src, const int32_t* dst,
+                          const double* ts, const float* ef, int32_t M, int32_t He, int32_t Dt,
+                          const float* w_ih, const float* w_hh, const float* b_ih,
+                          const float* b_hh, const float* time_w, const float* time_b, int64_t B,
+                          int32_t k, int32_t schedule, int32_t mit_on, float lambda, double gamma,
+                          int32_t n_sim, int32_t fanout, float* mem, double* mem_ts, float* mail,
+                          double* mail_ts, int64_t max_batches, int64_t* out_versions,
+                          const int32_t* neg, int32_t subgraph, const int32_t* plan_k, int32_t variant,
+                          const orc_dump* dump);
+
 int64_t orc_run_stream(int64_t N, int64_t E, const int32_t* src, const int32_t* dst,
                        const double* ts, const float* ef, int32_t M, int32_t He, int32_t Dt,
                        const float* w_ih, const float* w_hh, const float* b_ih,
@@ -506,8 +528,24 @@ int64_t orc_run_stream(int64_t N, int64_t E, const int32_t* src, const int32_t* 
                        int32_t n_sim, int32_t fanout, float* mem, double* mem_ts, float* mail,
                        double* mail_ts, int64_t max_batches, int64_t* out_versions,
                        const int32_t* neg, int32_t subgraph, const int32_t* plan_k, int32_t variant) {
+  return orc_run_stream_ex(N, E, src, dst, ts, ef, M, He, Dt, w_ih, w_hh, b_ih, b_hh, time_w, time_b, B, k,
+                           schedule, mit_on, lambda, gamma, n_sim, fanout, mem, mem_ts, mail, mail_ts,
+                           max_batches, out_versions, neg, subgraph, plan_k, variant, NULL);
+}
+
+int64_t orc_run_stream_ex(int64_t N, int64_t E, const int32_t* src, const int32_t* dst,
+                          const double* ts, const float* ef, int32_t M, int32_t He, int32_t Dt,
+                          const float* w_ih, const float* w_hh, const float* b_ih,
+                          const float* b_hh, const float* time_w, const float* time_b, int64_t B,
+                          int32_t k, int32_t schedule, int32_t mit_on, float lambda, double gamma,
+                          int32_t n_sim, int32_t fanout, float* mem, double* mem_ts, float* mail,
+                          double* mail_ts, int64_t max_batches, int64_t* out_versions,
+                          const int32_t* neg, int32_t subgraph, const int32_t* plan_k, int32_t variant,
+                          const orc_dump* dump) {
   if (B < 1 || k < 0 || M < 1) return ORC_EINVAL;
   if (subgraph && !neg) return ORC_EINVAL;
+  if (dump && dump->n > 0 && !subgraph) return ORC_EINVAL;
+  int64_t d_next = 0; /* next entry of dump->batches */
   const int32_t Dm = 2 * M + He;
   int64_t nb = (E + B - 1) / B;
   if (max_batches >= 0 && max_batches < nb) nb = max_batches;
@@ -590,6 +628,16 @@ int64_t orc_run_stream(int64_t N, int64_t E, const int32_t* src, const int32_t* 
             smts[r * (fanout + 1) + c] = 0.0;
           }
         }
+      }
+      if (dump && d_next < dump->n && dump->batches[d_next] == i) {
+        const int64_t slots = R3 * (fanout + 1), used = 3 * nb_ev * (fanout + 1);
+        int32_t* di = dump->sub_ids + d_next * slots;
+        for (int64_t r = 0; r < 3 * nb_ev; ++r)
+          for (int32_t c = 0; c <= fanout; ++c)
+            di[r * (fanout + 1) + c] = (c == 0) ? sroots[r] : snbr[r * fanout + c - 1];
+        memcpy(dump->mem + d_next * slots * M, smem, sizeof(float) * used * M);
+        memcpy(dump->mem_ts + d_next * slots, smts, sizeof(double) * used);
+        ++d_next;
       }
     }
     int64_t U = orc_memory_update(N, nb_ev, src + j0, dst + j0, ts + j0, ef + j0 * He, M, He,

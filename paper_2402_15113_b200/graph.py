@@ -34,9 +34,33 @@ def build_tcsr_host(num_nodes, src, dst, ts):
     return dict(indptr=indptr, nbr=other.astype(np.int32), eid=e.astype(np.int32), ts=ts[e])
 
 
+def build_tcsr_torch(num_nodes, src, dst, ts, device):
+    """The same T-CSR built on `device`: entries in stream order (event j's src
+    entry, then its dst entry unless j is a self-loop), stably sorted by node,
+    so each row is in (eid, role) order — GDELT's 382M entries in well under a
+    second on the GPU, where the host lexsort takes minutes."""
+    dev = torch.device(device)
+    s = torch.as_tensor(np.asarray(src, np.int32)).to(dev)
+    d = torch.as_tensor(np.asarray(dst, np.int32)).to(dev)
+    t = torch.as_tensor(np.asarray(ts, np.float64)).to(dev)
+    E = s.numel()
+    keep = torch.ones((E, 2), dtype=torch.bool, device=dev)
+    keep[:, 1] = s != d  # a self-loop is one entry (S:L124)
+    keep = keep.reshape(-1)
+    node = torch.stack([s, d], 1).reshape(-1)[keep]
+    order = torch.sort(node, stable=True).indices
+    del node
+    other = torch.stack([d, s], 1).reshape(-1)[keep][order]
+    e = torch.arange(E, dtype=torch.int32, device=dev).repeat_interleave(2)[keep][order]
+    del order, keep
+    cnt = torch.bincount(torch.cat([s, d[s != d]]).long(), minlength=num_nodes)
+    indptr = torch.zeros(num_nodes + 1, dtype=torch.int64, device=dev)
+    torch.cumsum(cnt, 0, out=indptr[1:])
+    return dict(indptr=indptr, nbr=other.contiguous(), eid=e.contiguous(), ts=t[e.long()].contiguous())
+
+
 def build_tcsr(num_nodes, src, dst, ts, device) -> _C.TcsrHandle:
-    h = build_tcsr_host(num_nodes, src, dst, ts)
-    t = {k: torch.from_numpy(v).to(device) for k, v in h.items()}
+    t = build_tcsr_torch(num_nodes, src, dst, ts, device)
     return _C.TcsrHandle(num_nodes, t["indptr"], t["nbr"], t["eid"], t["ts"])
 
 

@@ -184,8 +184,12 @@ class _TimedOps:
         torch.cuda.synchronize()
         self.timing = {}
 
+    timing_only = None  # optional set of op names to bracket (the others get no event nodes)
+
     def _ev(self, name):
         if self.timing is None:
+            return None
+        if self.timing_only is not None and name.removesuffix("_end") not in self.timing_only:
             return None
         if getattr(self, "_pool", None):
             e = self._pool.pop()

@@ -1,12 +1,12 @@
 """Summarise gpurun_out/ ncu artefacts into tracked files under profiles/.
 
-  python scripts/make_profiles.py <round-tag> [config]
+  python scripts/make_profiles.py <round-tag>
 
 Writes profiles/<tag>_ncu_summary.md (key metrics of each --set full capture,
-with units, plus the top stall-sampled SASS lines), profiles/<tag>_launches.csv
-(the --metrics gpu__time_duration.sum launch list) and merges the per-op DRAM
-traffic per launch into profiles/ncu_traffic.json (read by bench.py for
-roofline.traffic).
+with units, plus the top stall-sampled SASS lines), profiles/<tag>_launches*.csv
+(the --metrics gpu__time_duration.sum launch lists) and, per config and per
+kernel, ONE capture's DRAM bytes / L2 hit rate / duration per launch into
+profiles/ncu_traffic.json (read by bench.py for roofline.traffic).
 """
 import collections
 import csv
@@ -63,50 +63,70 @@ def top_sass(rep, n=12):
     return [(100 * v / tot, s) for v, s in items[:n]]
 
 
-def main(tag, config="wiki"):
+def _num(d, u, k):
+    if k not in d or d[k] in ("", "n/a"):
+        return None
+    return float(d[k].replace(",", "")) * SCALE.get(u.get(k, ""), 1)
+
+
+def main(tag):
+    """Captures are gpurun_out/prof_<config>_<kernel>.ncu-rep, each ONE launch
+    (`-k regex:<kernel> -s <skip> -c 1`).  ncu_traffic.json gets, per config and
+    per kernel, that launch's DRAM bytes, L2 hit rate and duration — never a sum
+    over captures or configs."""
     os.makedirs(PROF, exist_ok=True)
-    lines = [f"# ncu summary {tag} (config {config})", "",
-             "Captured with `ncu --set full --clock-control none --import-source on` inside "
-             "`python bench.py --profile --steps 20 --warmup 3` on one B200 (ncu flushes caches between "
-             "replays: cold-cache, serialised).", ""]
-    traffic = {}
+    lines = [f"# ncu summary {tag}", "",
+             "Each section is ONE launch captured with `ncu --set full --clock-control none --import-source on "
+             "-k regex:<kernel> -s <skip> -c 1` inside `python bench.py --profile --config <config>` on one B200 "
+             "(ncu flushes caches between its replays: cold-cache, serialised).", ""]
+    tpath = os.path.join(PROF, "ncu_traffic.json")
+    allt = json.load(open(tpath)) if os.path.exists(tpath) else {}
     for f in sorted(os.listdir(OUT)):
         if not (f.startswith("prof_") and f.endswith(".ncu-rep")):
             continue
+        parts = f[len("prof_"):-len(".ncu-rep")].split("_", 1)
+        if len(parts) != 2:
+            continue
+        config, kern = parts
         h, units, rows = raw(os.path.join(OUT, f))
-        for row in rows:
-            d = dict(zip(h, row))
-            u = dict(zip(h, units))
+        seen = set()
+        for li, row in enumerate(rows):  # a "multi" capture holds one launch of each of several kernels
+            d, u = dict(zip(h, row)), dict(zip(h, units))
             name = d.get("Kernel Name", "?")
-            lines.append(f"## {name[:100]}")
-            lines.append("")
-            lines.append("| metric | value | unit |")
-            lines.append("|---|---|---|")
-            for k in KEYS:
-                if k in d:
-                    lines.append(f"| {k} | {d[k]} | {u.get(k, '')} |")
-            dram = 0.0
-            for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
-                if k in d:
-                    dram += float(d[k].replace(",", "")) * SCALE.get(u.get(k, "byte"), 1)
             short = name.split("(")[0].split("::")[-1].split("<")[0].replace("void ", "").strip()
-            traffic[short] = traffic.get(short, 0.0) + dram
+            if short in seen:
+                continue
+            seen.add(short)
+            lines += [f"## {config}: {name[:100]}", "", f"capture `{f}`, launch {li + 1} of {len(rows)}", "",
+                      "| metric | value | unit |", "|---|---|---|"]
+            lines += [f"| {k} | {d[k]} | {u.get(k, '')} |" for k in KEYS if k in d]
+            dram = (_num(d, u, "dram__bytes_read.sum") or 0.0) + (_num(d, u, "dram__bytes_write.sum") or 0.0)
+            rec = {"dram_bytes": dram, "dram_read_bytes": _num(d, u, "dram__bytes_read.sum"),
+                   "dram_write_bytes": _num(d, u, "dram__bytes_write.sum"),
+                   "l2_hit_pct": _num(d, u, "lts__t_sector_hit_rate.pct"),
+                   "l2_bytes": _num(d, u, "lts__t_bytes.sum"),
+                   "duration_ns": _num(d, u, "gpu__time_duration.sum"),
+                   "dram_throughput_pct": _num(d, u, "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"),
+                   "tensor_active_pct": _num(d, u,
+                                             "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed"),
+                   "warps_active_pct": _num(d, u, "sm__warps_active.avg.pct_of_peak_sustained_active"),
+                   "source": f"profiles/{tag}_ncu_summary.md ({f}, launch {li + 1}: one launch)"}
+            allt.setdefault(config, {})[short] = rec
             lines.append("")
-            sass = top_sass(os.path.join(OUT, f))
-            if sass:
-                lines.append("top stall-sampled SASS:")
-                lines.append("")
-                lines.append("```")
-                for p, s in sass:
-                    lines.append(f"{p:5.1f}%  {s[:110]}")
-                lines.append("```")
-                lines.append("")
+        sass = top_sass(os.path.join(OUT, f)) if len(rows) == 1 else []
+        if sass:
+            lines += ["top stall-sampled SASS:", "", "```"]
+            lines += [f"{p_:5.1f}%  {s_[:110]}" for p_, s_ in sass]
+            lines += ["```", ""]
     with open(os.path.join(PROF, f"{tag}_ncu_summary.md"), "w") as fh:
         fh.write("\n".join(lines) + "\n")
-    # launch list
-    lc = os.path.join(OUT, "launches.csv")
-    if os.path.exists(lc):
-        shutil.copy(lc, os.path.join(PROF, f"{tag}_launches.csv"))
+    # launch lists: gpurun_out/launches*.csv
+    for f in sorted(os.listdir(OUT)):
+        if not (f.startswith("launches") and f.endswith(".csv")):
+            continue
+        suffix = f[len("launches"):-len(".csv")]
+        lc = os.path.join(OUT, f)
+        shutil.copy(lc, os.path.join(PROF, f"{tag}_launches{suffix}.csv"))
         rows = list(csv.reader(open(lc)))
         hdr, data = None, collections.defaultdict(list)
         for r in rows:
@@ -116,25 +136,21 @@ def main(tag, config="wiki"):
             if hdr and len(r) == len(hdr):
                 d = dict(zip(hdr, r))
                 if d.get("Metric Name") == "gpu__time_duration.sum":
-                    data[d["Kernel Name"].split("(")[0]].append(float(d["Metric Value"]))
-        tot = sum(sum(v) for k, v in data.items() if "mspipe" in k and "pack" not in k)
-        with open(os.path.join(PROF, f"{tag}_launches_summary.md"), "w") as fh:
-            fh.write(f"# ncu launch list {tag}: per-kernel device time (cold-cache, serialised)\n\n")
-            fh.write("| kernel | launches | mean us | share of the library's per-step kernel time |\n|---|---|---|---|\n")
+                    data[d["Kernel Name"].split("(")[0]].append(float(d["Metric Value"].replace(",", "")))
+        mine = {k: v for k, v in data.items() if "mspipe" in k and "pack" not in k}
+        tot = sum(sum(v) for v in mine.values()) or 1.0
+        out = os.path.join(PROF, f"{tag}_launches{suffix}_summary.md")
+        with open(out, "w") as fh:
+            fh.write(f"# ncu launch list {tag}{suffix}: per-kernel device time (cold-cache, serialised)\n\n")
+            fh.write("| kernel | launches | mean us | share of the library's kernel time |\n|---|---|---|---|\n")
             for k, v in sorted(data.items(), key=lambda kv: -sum(kv[1])):
-                share = sum(v) / tot if "mspipe" in k and "pack" not in k else float("nan")
+                share = sum(v) / tot if k in mine else float("nan")
                 fh.write(f"| {k} | {len(v)} | {sum(v) / len(v) / 1000:.2f} | {share:.3f} |\n")
-    tpath = os.path.join(PROF, "ncu_traffic.json")
-    allt = json.load(open(tpath)) if os.path.exists(tpath) else {}
-    ops = OPS_FUSED if "k_prep" in traffic else OPS
-    allt[config] = {op: sum(traffic.get(k, 0.0) for k in ks) for op, ks in ops.items()
-                    if all(k in traffic for k in ks)}
-    allt[config]["_source"] = f"{tag}_ncu_summary.md (dram__bytes_read.sum + dram__bytes_write.sum per launch)"
+        print(open(out).read())
     with open(tpath, "w") as fh:
         json.dump(allt, fh, indent=1)
-    print(open(os.path.join(PROF, f"{tag}_launches_summary.md")).read() if os.path.exists(lc) else "")
-    print(json.dumps(allt[config], indent=1))
+    print(json.dumps(allt, indent=1))
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], sys.argv[2] if len(sys.argv) > 2 else "wiki")
+    main(sys.argv[1])

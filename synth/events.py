@@ -87,7 +87,9 @@ def _repeat_fill(key: np.ndarray, fresh: np.ndarray, repeat_mask: np.ndarray) ->
     """Within each group of equal `key` (in stream order), a position whose
     repeat_mask is set copies the value of the previous position of that
     group; the first position of a group is always fresh."""
-    order = np.argsort(key, kind="stable")
+    # the stable order is unique; a 16-bit key takes numpy's radix sort (GDELT: ~5x faster)
+    small = key.size and 0 <= key.min() and key.max() < 32768
+    order = np.argsort(key.astype(np.int16) if small else key, kind="stable")
     k_sorted = key[order]
     first = np.ones(len(order), dtype=bool)
     first[1:] = k_sorted[1:] != k_sorted[:-1]
@@ -202,10 +204,28 @@ def gru_params(mem_dim: int, mail_dim: int, time_dim: int, seed: int = 1234):
     return dict(w_ih=w_ih, w_hh=w_hh, b_ih=b_ih, b_hh=b_hh, time_w=time_w, time_b=time_b)
 
 
-def make_workload(name: str, seed: int = 0, num_events: int | None = None, with_features: bool = True):
+def make_workload(name: str, seed: int = 0, num_events: int | None = None, with_features: bool = True,
+                  tcsr_events: int | None = None):
+    """The first `num_events` events of the config's stream (default: all) with
+    their edge features and the GRU weights.  tcsr_events > num_events (None:
+    the whole stream) also returns that longer stream's (src, dst, ts) as
+    "tcsr": the sampler's T-CSR is then built over it, so rows have their
+    full-stream lengths (GDELT: 22,934 entries on average) while the batches
+    run over the prefix.  The stream is prefix-consistent (every draw is
+    sequential), so the prefix is the first events of the longer stream, and
+    the sampler's strict ts < t_q never sees an event past the prefix."""
     cfg = CONFIGS[name]
-    src, dst, ts, neg = make_events(cfg, seed, num_events)
+    E = cfg.num_events if num_events is None else int(num_events)
+    Et = E if tcsr_events is None else min(int(tcsr_events), cfg.num_events)
+    if Et > E:
+        fsrc, fdst, fts, fneg = make_events(cfg, seed, Et)
+        src, dst, ts, neg = fsrc[:E].copy(), fdst[:E].copy(), fts[:E].copy(), fneg[:E].copy()
+        del fneg
+    else:
+        src, dst, ts, neg = make_events(cfg, seed, E)
     out = dict(cfg=cfg, src=src, dst=dst, ts=ts, neg=neg, seed=seed)
+    if Et > E:
+        out["tcsr"] = (fsrc, fdst, fts)
     if with_features:
         out["ef"] = edge_features(seed, 0, len(src), cfg.edge_dim)
     out["params"] = gru_params(cfg.mem_dim, cfg.mail_dim, cfg.time_dim)

@@ -109,6 +109,11 @@ def test_tcsr_rows_are_time_sorted_incident_lists():
         assert np.array_equal(h["ts"][a:b], ts[e])
         assert ((src[e] == v) | (dst[e] == v)).all()
         assert np.array_equal(h["nbr"][a:b], np.where(src[e] == v, dst[e], src[e]))
+    # the device builder (torch sort; run here on the CPU) gives the same arrays
+    from paper_2402_15113_b200.graph import build_tcsr_torch
+    t = build_tcsr_torch(cfg.num_nodes, src, dst, ts, "cpu")
+    for key in ("indptr", "nbr", "eid", "ts"):
+        assert np.array_equal(t[key].numpy(), h[key]), key
 
 
 @pytest.mark.parametrize("name", ["wiki", "reddit"])
