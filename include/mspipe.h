@@ -578,6 +578,27 @@ MSPIPE_API mspipe_status mspipe_plan_min_staleness(const double* tau, int64_t nu
 MSPIPE_API mspipe_status mspipe_stale_histogram(const mspipe_tcsr* g, const int32_t* src, const int32_t* dst,
                                      int64_t num_events, int64_t batch, int32_t max_d, int64_t* out_hist,
                                      void* stream);
+/* [host] stale shares from a histogram of mspipe_stale_histogram (copied to
+ * the host): out[q] = sum_{1 <= d <= k_q - 1} hist[d] / sum hist for the paper
+ * staleness k_q = k_values[q] >= 1 (k = 1: 0, no staleness; reading
+ * F6), 0 for an empty histogram.  nbins = max_d + 2.  Errors: MSPIPE_EINVAL
+ * (NULL, nbins < 2, k_q < 1). */
+MSPIPE_API mspipe_status mspipe_plan_stale_fractions(const int64_t* hist, int32_t nbins, const int32_t* k_values,
+                                          int32_t nk, double* out);
+/* Staleness error (MSPipe §5.5, Fig. `fig:staleness_error`;
+ * Theorem 1's ε_s): *out (device f64) = ‖x − s‖_F over the U = *num_unique
+ * update targets of one batch of num_events events, x = rows_a (what the
+ * updater consumed: the stale snapshot rows S_{v(i)} or MSPipe-S's mitigated
+ * rows) and s = rows_b (the precise memory S_{i−1} of a k = 0 run of the same
+ * stream, reading F7).  winner [U] are the dedup winners (pair p = 2a + role);
+ * both row arrays are in root layout: the row of pair p is at
+ * rows + ((p & 1)·num_events + (p >> 1))·stride·mem_dim floats (stride = 𝒩+1 for
+ * a prep's subgraph rows, 1 for a [2B, M] array).  f64 accumulation in a fixed
+ * order: deterministic.  Errors: MSPIPE_EINVAL (NULL, bad sizes). */
+MSPIPE_API mspipe_status mspipe_staleness_error(const int32_t* winner, const int32_t* num_unique,
+                                     int64_t num_events, const float* rows_a, int64_t stride_a,
+                                     const float* rows_b, int64_t stride_b, int32_t mem_dim, double* out,
+                                     void* stream);
 
 /* Utility (timing): record `event` (a cudaEvent_t) on `stream` with
  * cudaEventRecordExternal, so that under stream capture it becomes an

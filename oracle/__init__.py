@@ -57,6 +57,9 @@ def lib():
         L.orc_run_stream.restype = i64
         L.orc_run_stream_ex.argtypes = L.orc_run_stream.argtypes + [P]
         L.orc_run_stream_ex.restype = i64
+        L.orc_staleness_error_series.argtypes = [i64, i64, P, P, P, P, i32, i32, i32, P, P, P, P, P, P, i64,
+                                                 i32, i32, i32, f32, f64, i32, i32, i64, P]
+        L.orc_staleness_error_series.restype = i64
         L.orc_delta_t_population.argtypes = [i64, i64, P, P, P, P]
         L.orc_delta_t_population.restype = i64
         L.orc_quantile_nearest_rank.argtypes = [i64, P, f64]
@@ -256,6 +259,30 @@ def run_stream(num_nodes, src, dst, ts, ef, params, batch, k, schedule="exact", 
     if dres is not None:
         return st, vers[:r], dres
     return st, vers[:r]
+
+
+def staleness_error_series(num_nodes, src, dst, ts, ef, params, batch, k, schedule="exact", mitigation=None,
+                           fanout=10, max_batches=-1):
+    """Row F1 analytics: per iteration, ‖x − s‖_F over
+    the batch's update targets, x = the stale run's GRU hidden input (stale read,
+    or MSPipe-S's mitigated row), s = a k = 0 run's S_{i-1} (reading F7)."""
+    src, dst, ts = _c(src, np.int32), _c(dst, np.int32), _c(ts, np.float64)
+    ef = _c(ef, np.float32)
+    pr = {kk: _c(v, np.float32) for kk, v in params.items()}
+    M, He, Dt = pr["w_hh"].shape[1], ef.shape[1], len(pr["time_w"])
+    nb = -(-len(src) // batch)
+    if max_batches >= 0:
+        nb = min(nb, max_batches)
+    out = np.zeros(max(nb, 1), np.float64)
+    mit = mitigation
+    r = lib().orc_staleness_error_series(
+        num_nodes, len(src), _p(src), _p(dst), _p(ts), _p(ef), M, He, Dt, _p(pr["w_ih"]), _p(pr["w_hh"]),
+        _p(pr["b_ih"]), _p(pr["b_hh"]), _p(pr["time_w"]), _p(pr["time_b"]), batch, k,
+        1 if schedule == "grouped" else 0, 1 if mit else 0, float(mit["lam"]) if mit else 1.0,
+        float(mit["gamma"]) if mit else 0.0, int(mit["n_sim"]) if mit else 5, fanout, max_batches, _p(out))
+    if r < 0:
+        raise ValueError(f"orc_staleness_error_series rc={r}")
+    return out[:r]
 
 
 def delta_t_population(num_nodes, src, dst, ts):

@@ -676,6 +676,95 @@ int64_t orc_run_stream_ex(int64_t N, int64_t E, const int32_t* src, const int32_
 }
 
 /* ------------------------------------------------------------------------
+ * Row F1 analytics: staleness error series (MSPipe §5.5, Fig.
+ * `fig:staleness_error`; Theorem 1's ε_s; SPEC staleness_error).
+ * Two runs of the same stream in lockstep:
+ *   the stale run  (build staleness k, schedule, MSPipe-S if mit_on) and
+ *   the reference  (k = 0: "a synchronous (k=0) oracle run with identical
+ *                   seeds and data order").
+ * For iteration i, over the update targets w of batch i (the dedup winners,
+ * identical in both runs): x_w = the GRU hidden input of the stale run (the
+ * stale snapshot row S̃_{v(i)}[w], or the mitigated ŝ_w) and s_w = the
+ * reference's S_{i-1}[w];  out_err[i-1] = sqrt(Σ_w Σ_c (x_w,c − s_w,c)^2),
+ * summed in f64 in (winner, column) order (reading F7).  Returns nb.
+ * ---------------------------------------------------------------------- */
+int64_t orc_staleness_error_series(int64_t N, int64_t E, const int32_t* src, const int32_t* dst,
+                                   const double* ts, const float* ef, int32_t M, int32_t He, int32_t Dt,
+                                   const float* w_ih, const float* w_hh, const float* b_ih,
+                                   const float* b_hh, const float* time_w, const float* time_b, int64_t B,
+                                   int32_t k, int32_t schedule, int32_t mit_on, float lambda, double gamma,
+                                   int32_t n_sim, int32_t fanout, int64_t max_batches, double* out_err) {
+  if (B < 1 || k < 0 || M < 1 || !out_err) return ORC_EINVAL;
+  const int32_t Dm = 2 * M + He;
+  int64_t nb = (E + B - 1) / B;
+  if (max_batches >= 0 && max_batches < nb) nb = max_batches;
+  orc_graph* g = mit_on ? orc_graph_create(N, E, src, dst, ts) : NULL;
+  const int32_t R = k + 1;
+  size_t szm = sizeof(float) * (size_t)N * M, szt = sizeof(double) * (size_t)N;
+  /* stale run: the live state plus a ring of the k+1 versions still readable */
+  float* mem = (float*)calloc((size_t)N * M + 1, sizeof(float));
+  double* mem_ts = (double*)calloc((size_t)N + 1, sizeof(double));
+  float** rmem = (float**)malloc(sizeof(float*) * R);
+  double** rts = (double**)malloc(sizeof(double*) * R);
+  for (int32_t r = 0; r < R; ++r) {
+    rmem[r] = (float*)calloc((size_t)N * M + 1, sizeof(float));
+    rts[r] = (double*)calloc((size_t)N + 1, sizeof(double));
+  }
+  /* reference run (k = 0): its live state is S_{i-1} at iteration i */
+  float* rf_mem = (float*)calloc((size_t)N * M + 1, sizeof(float));
+  double* rf_ts = (double*)calloc((size_t)N + 1, sizeof(double));
+  int32_t* nodes = (int32_t*)malloc(sizeof(int32_t) * 2 * B);
+  int32_t* winner = (int32_t*)malloc(sizeof(int32_t) * 2 * B);
+  float* nmem = (float*)malloc(sizeof(float) * 2 * B * M);
+  double* nts = (double*)malloc(sizeof(double) * 2 * B);
+  float* nmail = (float*)malloc(sizeof(float) * 2 * B * Dm);
+  float* nh = (float*)malloc(sizeof(float) * 2 * B * M);
+  int64_t rc = nb;
+  for (int64_t i = 1; i <= nb; ++i) {
+    int64_t v = orc_snapshot_version(i, k, schedule);
+    int64_t j0 = (i - 1) * B;
+    int64_t n = (j0 + B <= E) ? B : E - j0;
+    /* stale run: update from S_{v(i)}, x = its GRU hidden input */
+    int64_t U = orc_memory_update(N, n, src + j0, dst + j0, ts + j0, ef + j0 * He, M, He, Dt, w_ih, w_hh,
+                                  b_ih, b_hh, time_w, time_b, rmem[v % R], rts[v % R], mit_on, g, lambda,
+                                  gamma, n_sim, fanout, nodes, winner, nmem, nts, nmail, nh, NULL, NULL, NULL, 0);
+    if (U < 0) {
+      rc = U;
+      break;
+    }
+    double acc = 0.0;
+    for (int64_t u = 0; u < U; ++u)
+      for (int32_t c = 0; c < M; ++c) {
+        double d = (double)nh[u * M + c] - (double)rf_mem[(int64_t)nodes[u] * M + c];
+        acc += d * d;
+      }
+    out_err[i - 1] = sqrt(acc);
+    for (int64_t u = 0; u < U; ++u) {
+      memcpy(mem + (int64_t)nodes[u] * M, nmem + u * M, sizeof(float) * M);
+      mem_ts[nodes[u]] = nts[u];
+    }
+    memcpy(rmem[i % R], mem, szm);
+    memcpy(rts[i % R], mem_ts, szt);
+    /* reference run: update from its own S_{i-1}, then commit */
+    U = orc_memory_update(N, n, src + j0, dst + j0, ts + j0, ef + j0 * He, M, He, Dt, w_ih, w_hh, b_ih, b_hh,
+                          time_w, time_b, rf_mem, rf_ts, 0, NULL, 1.0f, 0.0, n_sim, fanout, nodes, winner, nmem,
+                          nts, nmail, NULL, NULL, NULL, NULL, 0);
+    for (int64_t u = 0; u < U; ++u) {
+      memcpy(rf_mem + (int64_t)nodes[u] * M, nmem + u * M, sizeof(float) * M);
+      rf_ts[nodes[u]] = nts[u];
+    }
+  }
+  for (int32_t r = 0; r < R; ++r) {
+    free(rmem[r]);
+    free(rts[r]);
+  }
+  free(rmem); free(rts); free(mem); free(mem_ts); free(rf_mem); free(rf_ts);
+  free(nodes); free(winner); free(nmem); free(nts); free(nmail); free(nh);
+  orc_graph_free(g);
+  return rc;
+}
+
+/* ------------------------------------------------------------------------
  * γ helper (A-8): Δt population = for each event j and each endpoint v
  * (self-loop once), ts_j - ts of v's previous event; first appearances are
  * excluded (G16).  Quantile is nearest-rank.

@@ -37,7 +37,7 @@ EXPORTS = ("mspipe_abi_version", "mspipe_last_error", "mspipe_check", "mspipe_sa
            "mspipe_memory_prep_build", "mspipe_feature_fetch", "mspipe_updater_create",
            "mspipe_message_build_deferred", "mspipe_memory_mail_deferred", "mspipe_gru_build_apply_commit",
            "mspipe_util_rows_to_host", "mspipe_memory_winners", "mspipe_message_build_tables",
-           "mspipe_gru_apply_commit_out")
+           "mspipe_gru_apply_commit_out", "mspipe_plan_stale_fractions", "mspipe_staleness_error")
 XCHG_FETCH_IDS, XCHG_FETCH_ROWS, XCHG_COMMIT = 0, 1, 2
 
 
@@ -94,6 +94,8 @@ def lib():
         L.mspipe_plan_timeline.argtypes = [P, i64, P, P, P]
         L.mspipe_plan_min_staleness.argtypes = [P, i64, i32, P, C.POINTER(i64)]
         L.mspipe_stale_histogram.argtypes = [C.POINTER(Tcsr), P, P, i64, i64, i32, P, P]
+        L.mspipe_plan_stale_fractions.argtypes = [P, i32, P, i32, P]
+        L.mspipe_staleness_error.argtypes = [P, P, i64, P, i64, P, i64, i32, P, P]
         L.mspipe_memory_tables.argtypes = [P, i64, C.POINTER(P), C.POINTER(P), C.POINTER(P), C.POINTER(P)]
         L.mspipe_util_rows_to_host.argtypes = [P, P, P, P, i64, P, P, i64, i64, P]
         L.mspipe_util_graph_begin.argtypes = [P]
@@ -194,6 +196,24 @@ def plan_min_staleness(tau, num_iters, k_max):
     _ck(lib().mspipe_plan_min_staleness(_host_ptr(t), int(num_iters), int(k_max), _host_ptr(k), C.byref(bad)),
         "mspipe_plan_min_staleness")
     return k, int(bad.value)
+
+
+def plan_stale_fractions(hist, k_values):
+    """Stale share per paper staleness k (mspipe_plan_stale_fractions, host)."""
+    import numpy as np
+    h = np.ascontiguousarray(hist.cpu().numpy() if isinstance(hist, torch.Tensor) else hist, dtype=np.int64)
+    k = np.ascontiguousarray(k_values, dtype=np.int32)
+    out = np.zeros(len(k), np.float64)
+    _ck(lib().mspipe_plan_stale_fractions(_host_ptr(h), len(h), _host_ptr(k), len(k), _host_ptr(out)),
+        "mspipe_plan_stale_fractions")
+    return out
+
+
+def staleness_error(winner, num_unique, num_events, rows_a, stride_a, rows_b, stride_b, mem_dim, out, stream=None):
+    """‖x − s‖_F of one batch's update targets into the device f64 scalar `out`."""
+    _ck(lib().mspipe_staleness_error(ptr(winner), ptr(num_unique), int(num_events), ptr(rows_a), int(stride_a),
+                                     ptr(rows_b), int(stride_b), int(mem_dim), ptr(out), stream_ptr(stream)),
+        "mspipe_staleness_error")
 
 
 def stale_histogram(g: "TcsrHandle", src, dst, batch, max_d=64, stream=None):
@@ -577,7 +597,7 @@ def gru_apply_commit(gru: GruHandle, st: MemoryHandle, commit_version, num_event
                                               ptr(upd["num"]), ptr(upd["ts"]), ptr(upd.get("mail")),
                                               ptr(upd.get("mem")), ptr(out_nodes), ptr(out_num), ptr(workspace),
                                               workspace.numel() * workspace.element_size(), stream_ptr(stream)),
-            "mspipe_gru_apply_commit_out")
+            "mspipe_gru_apply_commit_out", "mspipe_plan_stale_fractions", "mspipe_staleness_error")
         return
     _ck(lib().mspipe_gru_apply_commit(gru.h, st.h, int(commit_version), int(num_events), ptr(snap_mem),
                                       int(snap_step), ptr(snap_h), ptr(upd["nodes"]), ptr(upd["winner"]),

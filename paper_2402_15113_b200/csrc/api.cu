@@ -1221,6 +1221,19 @@ mspipe_status mspipe_stale_histogram(const mspipe_tcsr* g, const int32_t* src, c
   return after_launch("stale_histogram");
 }
 
+mspipe_status mspipe_staleness_error(const int32_t* winner, const int32_t* num_unique, int64_t num_events,
+                                     const float* rows_a, int64_t stride_a, const float* rows_b, int64_t stride_b,
+                                     int32_t mem_dim, double* out, void* stream) {
+  if (num_events < 0 || stride_a < 1 || stride_b < 1 || mem_dim < 1)
+    return fail(MSPIPE_EINVAL, "staleness_error: num_events=%lld strides %lld/%lld mem_dim=%d",
+                (long long)num_events, (long long)stride_a, (long long)stride_b, mem_dim);
+  if (!winner || !num_unique || !rows_a || !rows_b || !out) return fail(MSPIPE_EINVAL, "staleness_error: null pointer");
+  cudaError_t e = launch_staleness_error(winner, num_unique, num_events, rows_a, stride_a, rows_b, stride_b, mem_dim,
+                                         out, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_status(e, "staleness_error: launch");
+  return after_launch("staleness_error");
+}
+
 mspipe_status mspipe_util_rows_to_host(const int32_t* num, int32_t* host_num, const void* a, void* host_a,
                                        int64_t a_row_bytes, const void* b, void* host_b, int64_t b_row_bytes,
                                        int64_t max_rows, void* stream) {

@@ -384,6 +384,9 @@ cudaError_t launch_feature_fetch(const int32_t* sub, const int32_t* eid, int64_t
                                  int64_t N, int32_t nstride, const float* efeat, int64_t E, int32_t estride,
                                  float* out_n, float* out_e, cudaStream_t s);
 // stale.cu
+cudaError_t launch_staleness_error(const int32_t* winner, const int32_t* num_unique, int64_t num_events,
+                                  const float* rows_a, int64_t stride_a, const float* rows_b, int64_t stride_b,
+                                  int32_t mem_dim, double* out, cudaStream_t s);
 cudaError_t launch_stale_hist(const Tcsr& g, const int32_t* src, const int32_t* dst, int64_t E, int64_t B,
                               int32_t max_d, unsigned long long* hist, cudaStream_t s);
 // prep.cu

@@ -108,4 +108,20 @@ mspipe_status mspipe_plan_min_staleness(const double* tau, int64_t num_iters, in
   return MSPIPE_OK;
 }
 
+mspipe_status mspipe_plan_stale_fractions(const int64_t* hist, int32_t nbins, const int32_t* k_values,
+                                          int32_t nk, double* out) {
+  if (!hist || !k_values || !out || nbins < 2 || nk < 0)
+    return mspipe::fail(MSPIPE_EINVAL, "plan_stale_fractions: NULL or nbins=%d nk=%d", nbins, nk);
+  int64_t tot = 0;
+  for (int32_t d = 0; d < nbins; ++d) tot += hist[d];
+  for (int32_t q = 0; q < nk; ++q) {
+    const int32_t k = k_values[q];
+    if (k < 1) return mspipe::fail(MSPIPE_EINVAL, "plan_stale_fractions: k=%d < 1", k);
+    int64_t stale = 0;  // bins d = 1 .. k-1 (the last bin holds d > max_d)
+    for (int32_t d = 1; d <= k - 1 && d < nbins; ++d) stale += hist[d];
+    out[q] = tot ? (double)stale / (double)tot : 0.0;
+  }
+  return MSPIPE_OK;
+}
+
 }  // extern "C"

@@ -70,3 +70,51 @@ cudaError_t launch_stale_hist(const Tcsr& g, const int32_t* src, const int32_t* 
 }
 
 }  // namespace mspipe
+
+// ---------------------------------------------------------------------------
+// Row F1 analytics — the staleness error of MSPipe §5.5 (Fig.
+// `fig:staleness_error`; Theorem 1's ε_s): for iteration i,
+//     ‖x^(i) − s^(i)‖_F  over the batch's update targets w ∈ U_i,
+// x = the memory the updater consumed (the stale read s̃ = S_{v(i)}[w], or the
+// mitigated ŝ_w of MSPipe-S) and s = the precise memory S_{i−1}[w] of a k = 0
+// run of the same stream (reading F7).  Rows come in root layout: target w of
+// pair p = 2a + role is root r = role·n + a, its row at base + r·stride·M.
+// One block, f64 accumulation in a fixed order (deterministic).
+// ---------------------------------------------------------------------------
+namespace mspipe {
+
+constexpr int kErrThreads = 256;
+
+__global__ void __launch_bounds__(kErrThreads) k_staleness_error(const int32_t* __restrict__ winner,
+                                                                 const int32_t* __restrict__ num, int64_t n,
+                                                                 const float* __restrict__ xa, int64_t stride_a,
+                                                                 const float* __restrict__ xb, int64_t stride_b,
+                                                                 int32_t M, double* __restrict__ out) {
+  __shared__ double part[kErrThreads];
+  pdl_begin();
+  const int32_t U = *num;
+  double acc = 0.0;
+  for (int64_t q = threadIdx.x; q < (int64_t)U * M; q += kErrThreads) {
+    const int64_t u = q / M, c = q - u * M;
+    const int32_t p = __ldg(winner + u);
+    const int64_t r = (int64_t)(p & 1) * n + (p >> 1);
+    const double d = (double)__ldg(xa + r * stride_a * M + c) - (double)__ldg(xb + r * stride_b * M + c);
+    acc = fma(d, d, acc);
+  }
+  part[threadIdx.x] = acc;
+  __syncthreads();
+  for (int w = kErrThreads / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) part[threadIdx.x] += part[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = sqrt(part[0]);
+}
+
+cudaError_t launch_staleness_error(const int32_t* winner, const int32_t* num_unique, int64_t num_events,
+                                  const float* rows_a, int64_t stride_a, const float* rows_b, int64_t stride_b,
+                                  int32_t mem_dim, double* out, cudaStream_t s) {
+  return launch_k(k_staleness_error, dim3(1), dim3(kErrThreads), 0, s, 1, winner, num_unique, num_events, rows_a,
+                  stride_a, rows_b, stride_b, mem_dim, out);
+}
+
+}  // namespace mspipe

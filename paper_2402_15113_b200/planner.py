@@ -17,20 +17,13 @@ import numpy as np
 import torch
 
 from . import _C
-from .stage import StageConfig
+from .stage import MemoryStage, StageConfig
 
 
 def stale_fractions(hist, k_values):
     """Share of (batch, node) updates read stale under paper staleness k
-    (reading F6): sum_{1 <= d <= k-1} hist[d] / sum(hist)."""
-    h = np.asarray(hist.cpu() if isinstance(hist, torch.Tensor) else hist, dtype=np.int64)
-    tot = h.sum()
-    cum = np.cumsum(h)
-    out = []
-    for k in k_values:
-        stale = cum[min(k - 1, len(h) - 1)] - h[0] if k >= 2 else 0
-        out.append(float(stale) / tot if tot else 0.0)
-    return np.array(out)
+    (reading F6), computed by mspipe_plan_stale_fractions."""
+    return _C.plan_stale_fractions(hist, k_values)
 
 
 def k_max_for_stream(g, src, dst, batch, limit=0.5, max_d=64):
@@ -75,3 +68,31 @@ class StageProfile:
         fetch = prep - sample
         update = op_ms.get("build", 0.0) + op_ms.get("update", 0.0) + op_ms.get("writeback", 0.0)
         return cls((sample, feature_ms, fetch, train_ms, update))
+
+
+def staleness_error_series(cfg: StageConfig, params: dict, tcsr, device, src, dst, ts, neg, ef):
+    """Row F1 analytics (MSPipe §5.5, Fig. `fig:staleness_error`):
+    the stage under `cfg` (staleness k, MSPipe-S if cfg.mitigation) and a k = 0
+    reference stage of the same stream run in lockstep, one step each; after
+    step t both still hold batch t's fetched rows, and mspipe_staleness_error
+    writes ‖x − s‖_F over batch t's update targets (x = the GRU hidden input
+    the stale stage consumed, s = the reference's S_{t-1} rows; reading F7).
+    Returns the device f64 series [num_batches]."""
+    ref_cfg = dataclasses.replace(cfg, k=0, mitigation=None, schedule="exact", plan=None, double_buffer=None)
+    a, b = MemoryStage(cfg, params, tcsr, device), MemoryStage(ref_cfg, params, tcsr, device)
+    for st in (a, b):
+        st.bind_resident(src, dst, ts, neg, ef)
+    sa, sb = a.step_ops(), b.step_ops()
+    if len(sa) != len(sb):
+        raise ValueError("the two schedules must commit one batch per step")
+    out = torch.zeros(len(sa), dtype=torch.float64, device=device)
+    F1, B, E = cfg.fanout + 1, cfg.batch, src.numel()
+    for t, (oa, ob) in enumerate(zip(sa, sb), start=1):
+        a.run_ops(oa)
+        b.run_ops(ob)
+        la, lb = a._slot(t), b._slot(t)
+        n = min(B, E - (t - 1) * B)
+        rows_a, stride_a = (la.h, 1) if cfg.mitigation else (la.mem, F1)
+        _C.staleness_error(la.dd["winner"], la.dd["num"], n, rows_a, stride_a, lb.mem, F1, cfg.mem_dim,
+                           out[t - 1:t])
+    return out

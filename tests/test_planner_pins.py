@@ -4,6 +4,8 @@ simulation of the same resources, brute-force minimality of the solver, the
 paper's Table 1 stage shares against its Table 2 speedups
  and its "range from 2 to 4", and the stale-node fraction
 against a from-scratch replay."""
+import math
+
 import numpy as np
 import pytest
 
@@ -157,3 +159,94 @@ def test_stale_fraction_closed_forms():
 def test_k_max_rule():
     assert P.k_max_from_fraction({1: 0.0, 2: 0.3, 3: 0.5, 4: 0.6}) == 4
     assert P.k_max_from_fraction({2: 0.9}) == 1
+
+
+# ---------------------------------------------------------------- staleness error (F1 analytics)
+def _bias_only(M, He, Dt, c):
+    Dx = 2 * M + He + Dt
+    p = dict(w_ih=np.zeros((3 * M, Dx), np.float32), w_hh=np.zeros((3 * M, M), np.float32),
+             b_ih=np.zeros(3 * M, np.float32), b_hh=np.zeros(3 * M, np.float32),
+             time_w=np.ones(Dt, np.float32), time_b=np.zeros(Dt, np.float32))
+    p["b_ih"][2 * M:] = c
+    return p
+
+
+def test_staleness_error_k0_is_zero():
+    """k = 0 run vs itself -> 0 for random weights."""
+    import oracle
+    from synth import make_workload
+    w = make_workload("tiny", seed=1, num_events=3000)
+    c = w["cfg"]
+    e = oracle.staleness_error_series(c.num_nodes, w["src"], w["dst"], w["ts"], w["ef"], w["params"], c.batch, 0)
+    assert len(e) == 15 and (e == 0.0).all()
+
+
+@pytest.mark.parametrize("k,schedule", [(1, "exact"), (3, "exact"), (2, "grouped")])
+def test_staleness_error_bias_only_closed_form(k, schedule):
+    """Bias-only GRU (W = 0, b_in = c): a node's memory after m updates is
+    tanh(c)(1 - 2^-m) (pin P4), so the error of iteration i is
+    sqrt(sum_w M tanh(c)^2 (2^-m~_w - 2^-m_w)^2) over the batch's update
+    targets, m~ from the stale run's integer replay read at v(i) and m from the
+    k = 0 replay read at i - 1 (both written out here from Eq. 2)."""
+    import oracle
+    from synth import CONFIGS, edge_features, make_events
+    cfg = CONFIGS["tiny"]
+    E, B, N = 3000, 150, cfg.num_nodes
+    src, dst, ts, _ = make_events(cfg, 4, E)
+    M, He, Dt, c = 5, 3, 2, 0.8
+    ef = edge_features(0, 0, E, He)
+    got = oracle.staleness_error_series(N, src, dst, ts, ef, _bias_only(M, He, Dt, c), B, k, schedule)
+    stale = [np.zeros(N, np.int64)]
+    ref = np.zeros(N, np.int64)
+    want = []
+    for i in range(1, E // B + 1):
+        v = max(0, i - 1 - k) if schedule == "exact" else (k + 1) * ((i - 1) // (k + 1))
+        snap = stale[v]
+        targets = sorted(set(src[(i - 1) * B:i * B].tolist()) | set(dst[(i - 1) * B:i * B].tolist()))
+        d = np.array([2.0 ** -snap[w] - 2.0 ** -ref[w] for w in targets])
+        want.append(math.sqrt(M * math.tanh(c) ** 2 * float((d * d).sum())))
+        live = stale[-1].copy()
+        new_ref = ref.copy()
+        for a in range((i - 1) * B, i * B):
+            for w in (src[a], dst[a]):
+                live[w] = snap[w] + 1
+                new_ref[w] = ref[w] + 1
+        stale.append(live)
+        ref = new_ref
+    assert np.allclose(got, want, rtol=1e-6, atol=1e-6)
+    assert (got > 0).any()
+
+
+def test_staleness_error_mitigated_not_above_unmitigated_in_mean():
+    """on a toy run with k = 2 the per-iteration series is finite and
+    bounded, and the MSPipe-S series is <= the unmitigated one in mean (the
+    property Fig. `fig:staleness_error` shows)."""
+    import oracle
+    from synth import make_workload
+    w = make_workload("tiny", seed=0, num_events=6000)
+    c = w["cfg"]
+    mit = dict(lam=0.95, gamma=oracle.gamma(c.num_nodes, w["src"], w["dst"], w["ts"], 0.99), n_sim=5)
+    a = oracle.staleness_error_series(c.num_nodes, w["src"], w["dst"], w["ts"], w["ef"], w["params"], c.batch, 2)
+    b = oracle.staleness_error_series(c.num_nodes, w["src"], w["dst"], w["ts"], w["ef"], w["params"], c.batch, 2,
+                                      mitigation=mit)
+    assert np.isfinite(a).all() and np.isfinite(b).all()
+    # |x - s| <= 2 per element (P8: memories in [-1, 1]): ||.||_F <= 2 sqrt(U M)
+    assert a.max() <= 2 * math.sqrt(2 * c.batch * c.mem_dim)
+    assert b.mean() <= a.mean()
+
+
+def test_library_stale_fractions_equal_oracle():
+    """mspipe_plan_stale_fractions (host, in the library) on the oracle's C3
+    histogram gives the oracle's fractions bit for bit (reading F6)."""
+    from oracle import planner as OP
+    from paper_2402_15113_b200 import _C
+    from synth import CONFIGS, make_events
+    cfg = CONFIGS["wiki"]
+    src, dst, _, _ = make_events(cfg, 2, 60_000)
+    ks = list(range(1, 12))
+    fr, hist = OP.stale_fraction(src, dst, 600, ks)
+    max_d = 40
+    h = np.zeros(max_d + 2, np.int64)
+    for d, n in hist.items():
+        h[min(d, max_d + 1)] += n
+    assert np.array_equal(_C.plan_stale_fractions(h, ks), fr)
