@@ -480,14 +480,17 @@ __global__ void __launch_bounds__(256) k_build_x(TcArgs a) {
   const int32_t U = __ldg(a.num_unique);
   const int32_t nchunks = d.Kpad / tc::kKC;
   const int32_t mtiles = (U + tc::kM - 1) / tc::kM;
-  const int64_t items = (int64_t)mtiles * nchunks * tc::kM;
+  // items < 2^31 (U <= 16384 rows, <= 20 chunks): 32-bit index arithmetic (a
+  // 64-bit division by the runtime chunk count cost ~70 instructions per lane)
+  const uint32_t items = (uint32_t)mtiles * (uint32_t)nchunks * tc::kM;
   const int lane = threadIdx.x & 31;
-  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
   const int32_t M = d.M;
-  for (int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < items; w += nwarps) {
+  for (uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < items; w += nwarps) {
     const int32_t row = (int32_t)(w % tc::kM);
-    const int32_t c = (int32_t)((w / tc::kM) % nchunks);
-    const int32_t mt = (int32_t)(w / ((int64_t)tc::kM * nchunks));
+    const uint32_t cm = w / tc::kM;
+    const int32_t mt = (int32_t)(cm / (uint32_t)nchunks);
+    const int32_t c = (int32_t)(cm - (uint32_t)mt * (uint32_t)nchunks);
     const int32_t u = mt * tc::kM + row;
     const int32_t k = c * tc::kKC + lane;
     float v = 0.f;

@@ -139,6 +139,19 @@ struct Tcsr {
 // (ts is sorted, so the true lanes are a prefix) shrinks the range 33x; a row
 // of L entries costs ceil(log33(L/32)) + 1 dependent rounds instead of log2(L).
 // An id outside [0, N) gives an empty row and raises MSPIPE_DEVERR_RANGE.
+// ((lane + 1) * span) / 33 without a 64-bit division (~70 instructions on the
+// integer pipe, once per lane per probe round): for products below 2^32 the
+// quotient is umulhi(x, ceil(2^37 / 33)) >> 5, exact for every x < 2^32
+// (ceil(2^37/33) * 33 - 2^37 = 4 <= 2^(37-32)); rows of >= 2^27 entries keep
+// the division.
+__device__ __forceinline__ int64_t probe_offset33(int lane, int64_t span) {
+  if (span < (int64_t(1) << 27)) {
+    const uint32_t x = (uint32_t)(lane + 1) * (uint32_t)span;
+    return (int64_t)(__umulhi(x, 0xF83E0F84u) >> 5);
+  }
+  return ((int64_t)(lane + 1) * span) / 33;
+}
+
 __device__ __forceinline__ int64_t warp_recent_end(const Tcsr& g, int32_t v, double tq, int lane,
                                                    int64_t* beg_out) {
   if (v < 0 || v >= g.num_nodes) {
@@ -150,7 +163,7 @@ __device__ __forceinline__ int64_t warp_recent_end(const Tcsr& g, int32_t v, dou
   int64_t lo = beg, hi = __ldg(g.indptr + v + 1);
   while (hi - lo > 32) {
     const int64_t span = hi - lo;
-    const int64_t p = lo + ((int64_t)(lane + 1) * span) / 33;  // strictly inside [lo, hi)
+    const int64_t p = lo + probe_offset33(lane, span);  // strictly inside [lo, hi)
     const bool below = __ldg(g.ts + p) < tq;
     const int c = __popc(__ballot_sync(0xffffffffu, below));
     const int64_t plast = __shfl_sync(0xffffffffu, p, c > 0 ? c - 1 : 0);
@@ -185,7 +198,7 @@ __device__ __forceinline__ int64_t warp_recent_sample(const Tcsr& g, int32_t v, 
   int64_t lo = beg, hi = __ldg(g.indptr + v + 1);
   while (hi - lo > 32) {
     const int64_t span = hi - lo;
-    const int64_t p = lo + ((int64_t)(lane + 1) * span) / 33;
+    const int64_t p = lo + probe_offset33(lane, span);
     const bool below = __ldg(g.ts + p) < tq;
     const int c = __popc(__ballot_sync(0xffffffffu, below));
     const int64_t plast = __shfl_sync(0xffffffffu, p, c > 0 ? c - 1 : 0);

@@ -13,18 +13,69 @@ static inline unsigned grid_for(int64_t work_items, int threads, int per_sm) {
 }
 
 // ---------------------------------------------------------------------------
+// Warp row copy: nrows (<= 32) rows of Q float4.  Row s comes from
+// src + (kSrcIds ? id_s : src_row0 + s)·Q and goes to
+// dst + (kDstIds ? id_s : dst_row0 + s)·Q, id_s held by lane s (shuffled);
+// a negative source id gives a zero row, a negative destination id skips the
+// row.  The nrows·Q elements are flattened over the 32 lanes (no idle lanes
+// for Q = 25), kU 16-byte loads in flight per lane before their stores, and
+// the (row, column) of each element is advanced incrementally (no division).
+// ---------------------------------------------------------------------------
+template <int kU, bool kSrcIds, bool kDstIds>
+__device__ __forceinline__ void warp_copy_rows(const float4* __restrict__ src, int64_t src_row0,
+                                               float4* __restrict__ dst, int64_t dst_row0, int32_t Q, int nrows,
+                                               int32_t my_id, int lane) {
+  const int total = nrows * Q;
+  const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+  const int q32 = 32 / Q, r32 = 32 - q32 * Q;
+  int s = lane / Q, c = lane - (lane / Q) * Q;
+  for (int base = 0; base < total; base += 32 * kU) {
+    float4 v[kU];
+    const int s0 = s, c0 = c;
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const bool in = base + u * 32 + lane < total;
+      const int32_t id = kSrcIds ? __shfl_sync(0xffffffffu, my_id, s < nrows ? s : 0) : 0;
+      const int64_t srow = kSrcIds ? (int64_t)id : src_row0 + s;
+      v[u] = (in && srow >= 0) ? __ldg(src + srow * Q + c) : z;
+      s += q32;
+      c += r32;
+      if (c >= Q) {
+        c -= Q;
+        ++s;
+      }
+    }
+    // the stores walk the same (row, column) sequence again (no per-load index registers)
+    s = s0;
+    c = c0;
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const bool in = base + u * 32 + lane < total;
+      const int32_t id = kDstIds ? __shfl_sync(0xffffffffu, my_id, s < nrows ? s : 0) : 0;
+      const int64_t drow = kDstIds ? (int64_t)id : dst_row0 + s;
+      if (in && drow >= 0) dst[drow * Q + c] = v[u];
+      s += q32;
+      c += r32;
+      if (c >= Q) {
+        c -= Q;
+        ++s;
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // A3 — gather rows of the state tables into dense snapshot buffers
 // ("fetches the required ... node memory vectors"; Eq. 2 reads
-// s~^(i-k)).  A warp moves kRows rows per step: it first loads
-// the kRows ids, then issues every 16-byte row-vector load of those rows, then
-// the stores, so kRows x (row / 512 B) requests are in flight per warp and no
-// per-element index arithmetic (division) is needed.  Each row read is one
-// contiguous 400 B (mem) / 1.5 KB (mail) segment and each write is dense.
-// id -1 = pad (zero row, ts 0).
+// s~^(i-k)).  A warp moves kFetchRows rows per step: their ids
+// (one per lane), then warp_copy_rows of the mem rows (and the mail rows),
+// then the row timestamps.  Each row read is one contiguous 400 B (mem) /
+// 1.5 KB (mail) segment and each write is dense.  id -1 = pad (zero row, ts 0).
 // ---------------------------------------------------------------------------
-constexpr int kFetchRows = 4;
+constexpr int kFetchRows = 8;
+constexpr int kCopyU = 8;
 
-__global__ void __launch_bounds__(256) k_fetch_gather(
+__global__ void __launch_bounds__(256, 4) k_fetch_gather(
     const int32_t* __restrict__ ids, int64_t n, int64_t N, const float4* __restrict__ mem,
     const double* __restrict__ mem_ts, int32_t Qm, const float4* __restrict__ mail,
     const double* __restrict__ mail_ts, int32_t Qa, float4* __restrict__ out_mem,
@@ -33,38 +84,17 @@ __global__ void __launch_bounds__(256) k_fetch_gather(
   pdl_begin();
   const int lane = threadIdx.x & 31;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
   for (int64_t base = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * kFetchRows; base < n;
        base += nwarps * kFetchRows) {
-    int32_t id[kFetchRows];
-#pragma unroll
-    for (int r = 0; r < kFetchRows; ++r) {
-      id[r] = base + r < n ? __ldg(ids + base + r) : -1;
-      if (lane == 0 && (id[r] < -1 || id[r] >= N)) raise_dev(MSPIPE_DEVERR_RANGE);
-      if (id[r] >= N) id[r] = -1;
-    }
-    for (int32_t c = lane; c < Qm; c += 32) {
-      float4 v[kFetchRows];
-#pragma unroll
-      for (int r = 0; r < kFetchRows; ++r) v[r] = id[r] >= 0 ? __ldg(mem + (int64_t)id[r] * Qm + c) : z;
-#pragma unroll
-      for (int r = 0; r < kFetchRows; ++r)
-        if (base + r < n) out_mem[(base + r) * Qm + c] = v[r];
-    }
-    if (lane < kFetchRows && base + lane < n) {
-      int32_t my = id[0];
-#pragma unroll
-      for (int r = 1; r < kFetchRows; ++r) my = lane == r ? id[r] : my;
-      out_mem_ts[base + lane] = my >= 0 ? __ldg(mem_ts + my) : 0.0;
-      if (out_mail_ts) out_mail_ts[base + lane] = my >= 0 ? __ldg(mail_ts + my) : 0.0;
-    }
-    for (int32_t c = lane; c < Qa; c += 32) {
-      float4 v[kFetchRows];
-#pragma unroll
-      for (int r = 0; r < kFetchRows; ++r) v[r] = id[r] >= 0 ? __ldg(mail + (int64_t)id[r] * Qa + c) : z;
-#pragma unroll
-      for (int r = 0; r < kFetchRows; ++r)
-        if (base + r < n) out_mail[(base + r) * Qa + c] = v[r];
+    const int nrows = (int)min64(kFetchRows, n - base);
+    int32_t id = lane < nrows ? __ldg(ids + base + lane) : -1;
+    if (lane < nrows && (id < -1 || id >= N)) raise_dev(MSPIPE_DEVERR_RANGE);
+    if (id >= N || id < -1) id = -1;
+    warp_copy_rows<kCopyU, true, false>(mem, 0, out_mem, base, Qm, nrows, id, lane);
+    if (Qa > 0) warp_copy_rows<kCopyU, true, false>(mail, 0, out_mail, base, Qa, nrows, id, lane);
+    if (lane < nrows) {
+      out_mem_ts[base + lane] = id >= 0 ? __ldg(mem_ts + id) : 0.0;
+      if (out_mail_ts) out_mail_ts[base + lane] = id >= 0 ? __ldg(mail_ts + id) : 0.0;
     }
   }
 }
@@ -76,7 +106,7 @@ void launch_fetch(const int32_t* ids, int64_t n, int64_t num_nodes, const float*
   const int32_t Qm = mem_dim / 4;
   const int32_t Qa = mail ? (int32_t)(mail_stride / 4) : 0;
   const int threads = 256;
-  launch_k(k_fetch_gather, dim3(grid_for((n + kFetchRows - 1) / kFetchRows * 32, threads, 8)), dim3(threads), 0, s,
+  launch_k(k_fetch_gather, dim3(grid_for((n + kFetchRows - 1) / kFetchRows * 32, threads, 4)), dim3(threads), 0, s,
            1, ids, n, num_nodes, (const float4*)mem, mem_ts, Qm, (const float4*)mail, mail_ts, Qa, (float4*)out_mem,
            out_mem_ts, (float4*)out_mail, out_mail_ts);
 }
@@ -294,7 +324,7 @@ void launch_dedup(const int32_t* src, const int32_t* dst, int64_t num_events, in
 // copy; a warp moves kFetchRows rows per step (loads of all rows first, then
 // the stores).  U is read on the device.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_writeback(
+__global__ void __launch_bounds__(256, 4) k_writeback(
     const int32_t* __restrict__ nodes, const int32_t* __restrict__ num, int64_t max_n,
     const float4* __restrict__ new_mem, const double* __restrict__ new_ts,
     const float4* __restrict__ new_mail, int32_t Qm, int32_t Qa, float4* __restrict__ mem,
@@ -306,42 +336,18 @@ __global__ void __launch_bounds__(256) k_writeback(
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t base = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * kFetchRows; base < U;
        base += nwarps * kFetchRows) {
-    int32_t node[kFetchRows];
-#pragma unroll
-    for (int r = 0; r < kFetchRows; ++r) {
-      node[r] = base + r < U ? __ldg(nodes + base + r) : -1;
-      if (base + r < U && (node[r] < 0 || node[r] >= N)) {
-        if (lane == 0) raise_dev(MSPIPE_DEVERR_RANGE);
-        node[r] = -1;
-      }
+    const int nrows = (int)min64(kFetchRows, U - base);
+    int32_t node = lane < nrows ? __ldg(nodes + base + lane) : -1;
+    if (lane < nrows && (node < 0 || node >= N)) {
+      raise_dev(MSPIPE_DEVERR_RANGE);
+      node = -1;
     }
-    for (int32_t c = lane; c < Qm; c += 32) {
-      float4 v[kFetchRows];
-#pragma unroll
-      for (int r = 0; r < kFetchRows; ++r)
-        if (node[r] >= 0) v[r] = __ldg(new_mem + (base + r) * Qm + c);
-#pragma unroll
-      for (int r = 0; r < kFetchRows; ++r)
-        if (node[r] >= 0) mem[(int64_t)node[r] * Qm + c] = v[r];
-    }
-    for (int32_t c = lane; c < Qa; c += 32) {
-      float4 v[kFetchRows];
-#pragma unroll
-      for (int r = 0; r < kFetchRows; ++r)
-        if (node[r] >= 0) v[r] = __ldg(new_mail + (base + r) * Qa + c);
-#pragma unroll
-      for (int r = 0; r < kFetchRows; ++r)
-        if (node[r] >= 0) mail[(int64_t)node[r] * Qa + c] = v[r];
-    }
-    if (lane < kFetchRows) {
-      int32_t my = node[0];
-#pragma unroll
-      for (int r = 1; r < kFetchRows; ++r) my = lane == r ? node[r] : my;
-      if (my >= 0) {
-        const double t1 = __ldg(new_ts + base + lane);
-        mem_ts[my] = t1;
-        mail_ts[my] = t1;
-      }
+    if (Qm > 0) warp_copy_rows<kCopyU, false, true>(new_mem, base, mem, 0, Qm, nrows, node, lane);
+    if (Qa > 0) warp_copy_rows<kCopyU, false, true>(new_mail, base, mail, 0, Qa, nrows, node, lane);
+    if (node >= 0) {
+      const double t1 = __ldg(new_ts + base + lane);
+      mem_ts[node] = t1;
+      mail_ts[node] = t1;
     }
   }
 }
@@ -352,7 +358,7 @@ void launch_writeback(const int32_t* nodes, const int32_t* num, int64_t max_n,
                       float* mail, double* mail_ts, int64_t num_nodes, cudaStream_t s) {
   const int32_t Qm = mem_dim / 4, Qa = (int32_t)(mail_stride / 4);
   const int threads = 256;
-  launch_k(k_writeback, dim3(grid_for((max_n + kFetchRows - 1) / kFetchRows * 32, threads, 8)), dim3(threads), 0, s,
+  launch_k(k_writeback, dim3(grid_for((max_n + kFetchRows - 1) / kFetchRows * 32, threads, 4)), dim3(threads), 0, s,
            1, nodes, num, max_n, (const float4*)new_mem, new_ts, (const float4*)new_mail, Qm, Qa, (float4*)mem,
            mem_ts, (float4*)mail, mail_ts, num_nodes);
 }

@@ -73,27 +73,35 @@ __device__ __forceinline__ void st_release(int32_t* p, int32_t v) {
 }
 
 // copy `nrows` table rows (ids held by lanes 0..nrows-1, -1 = zero row) of Q
-// float4 each into dst rows base..base+nrows-1; 4 loads in flight per lane.
+// float4 each into dst rows base..base+nrows-1; kU loads in flight per lane.
 __device__ __forceinline__ void warp_gather_rows(const float4* __restrict__ tab, int32_t Q, int32_t my_id,
                                                  int nrows, float4* __restrict__ dst, int64_t dst_row0,
                                                  int lane) {
   // kU float4 loads in flight per lane before their stores: the whole subgraph
   // (11 rows x 25 float4 for M = 100) in one dependent round instead of three
 #ifndef MSPIPE_PREP_KU
-#define MSPIPE_PREP_KU 12
+#define MSPIPE_PREP_KU 9
 #endif
   constexpr int kU = MSPIPE_PREP_KU;
   const int total = nrows * Q;
   const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+  // (row s, column c) of this lane's element; the next one is 32 elements on:
+  // advance by (q32, r32) with one conditional wrap instead of a division per load
+  int s = lane / Q, c = lane - (lane / Q) * Q;
+  const int q32 = 32 / Q, r32 = 32 - q32 * Q;
   for (int base = 0; base < total; base += 32 * kU) {
     float4 v[kU];
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
       const int idx = base + u * 32 + lane;
-      const int s = idx < total ? idx / Q : 0;
-      const int32_t id = __shfl_sync(0xffffffffu, my_id, s);
-      const int c = idx - s * Q;
+      const int32_t id = __shfl_sync(0xffffffffu, my_id, s < nrows ? s : 0);
       v[u] = (idx < total && id >= 0) ? __ldg(tab + (int64_t)id * Q + c) : z;
+      s += q32;
+      c += r32;
+      if (c >= Q) {
+        c -= Q;
+        ++s;
+      }
     }
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
