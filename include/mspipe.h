@@ -296,18 +296,6 @@ MSPIPE_API mspipe_status mspipe_memory_dedup(mspipe_memory* st, const int32_t* s
                                   int64_t num_events, int32_t* out_nodes, int32_t* out_winner,
                                   int32_t* out_num_unique, void* stream);
 
-/* A2 for iteration `iteration` of the stage: exactly mspipe_memory_dedup, and
- * with double-buffered state it also stamps the winners' nodes for that
- * iteration (what mspipe_memory_prep's dedup block does), so a later
- * mspipe_memory_prep called WITHOUT dedup outputs can carry the catch-up of
- * this batch's commit.  Lets the dedup (state-independent, G6) run on its own
- * stream ahead of the message build (mspipe_message_build_tables) while the
- * sampler and gather run.  Same limits and outputs as mspipe_memory_dedup;
- * iteration >= 1. */
-MSPIPE_API mspipe_status mspipe_memory_winners(mspipe_memory* st, int64_t iteration, const int32_t* src,
-                                    const int32_t* dst, int64_t num_events, int32_t* out_nodes,
-                                    int32_t* out_winner, int32_t* out_num_unique, void* stream);
-
 /* A5 + A6 — message build and GRU update of the U winners of one batch of
  * num_events events (winner / num_unique from mspipe_memory_dedup; global
  * eids are the caller's business; edge_feat holds this batch's rows
@@ -353,7 +341,7 @@ MSPIPE_API mspipe_status mspipe_memory_writeback(mspipe_memory* st, int64_t comm
  * n = 3B(𝒩+1)) with the same arguments and outputs as those calls.  The same
  * staleness gate applies.  fanout <= 31; num_events <= 8192.
  * out_nodes, out_winner and out_num_unique all NULL: no dedup (A1 + A3 only;
- * the winners come from mspipe_memory_winners of the same iteration). */
+ * the winners then come from mspipe_memory_dedup). */
 MSPIPE_API mspipe_status mspipe_memory_prep(mspipe_memory* st, const mspipe_tcsr* g, int64_t iteration,
                                  const int32_t* src, const int32_t* dst, const int32_t* neg,
                                  const double* ts, int64_t num_events, int32_t fanout,
@@ -379,49 +367,10 @@ MSPIPE_API mspipe_status mspipe_message_build(const mspipe_gru* gru, const doubl
                                    const float* snap_h, const int32_t* winner,
                                    const int32_t* num_unique, double* out_ts, float* out_mail,
                                    int64_t mail_stride, void* workspace, size_t ws_bytes, void* stream);
-/* A5 from the state tables instead of a snapshot buffer: exactly
- * mspipe_message_build with S = the tables of version v(iteration) (the
- * version mspipe_memory_prep of the same iteration reads, Eq. 2, P:L196-L204;
- * same gate, MSPIPE_ESTALE otherwise; *out_version = v), snap_h = NULL, and
- * S.mem[w] = mem[node_w] read by node id (src / dst: the batch's endpoints).
- * The caller orders it like the fetch: after commit v, before commit v + 1
- * rewrites the rows it reads (with double-buffered state: before commit v + 2).
- * Needs a tensor-core, immediate-mailbox handle with world == 1. */
-MSPIPE_API mspipe_status mspipe_message_build_tables(const mspipe_gru* gru, const mspipe_memory* st,
-                                          int64_t iteration, const int32_t* src, const int32_t* dst,
-                                          const double* ts, int64_t num_events, const float* edge_feat,
-                                          const int32_t* winner, const int32_t* num_unique, double* out_ts,
-                                          float* out_mail, void* workspace, size_t ws_bytes,
-                                          int64_t* out_version, void* stream);
 MSPIPE_API mspipe_status mspipe_gru_apply(const mspipe_gru* gru, int64_t num_events, const float* snap_mem,
                                int64_t snap_step, const float* snap_h, const int32_t* winner,
                                const int32_t* num_unique, float* out_mem, const void* workspace,
                                size_t ws_bytes, void* stream);
-
-/* A1 + A2 + A3 + A5 in one launch: mspipe_memory_prep (no mitigation) and then
- * mspipe_message_build of the same batch with snap_mem = out_mem, snap_step =
- * fanout + 1, snap_h = NULL, winner = out_winner, num_unique = out_num_unique
- * — same outputs (out_commit_ts / out_commit_mail = message_build's out_ts /
- * out_mail with the handle's mail_stride; the A-operand images in
- * `workspace`, >= mspipe_gru_workspace_size(gru, num_events) bytes).  Inside
- * the kernel the dedup block publishes the pair -> GEMM-row map and the warps
- * of the winners' roots build their rows (G1, G2, G4, G13) from the tables of
- * the version read.  num_events <= gru max_events.  Errors as
- * mspipe_memory_prep, plus MSPIPE_EINVAL (NULL GRU / outputs, dims differ,
- * workspace too small) and MSPIPE_EUNSUPPORTED (precision other than
- * MSPIPE_FP32_3XTF32).  Preps of one handle must not run concurrently (they
- * share the handle's dedup / build scratch): the stage driver issues them on
- * one stream. */
-MSPIPE_API mspipe_status mspipe_memory_prep_build(mspipe_memory* st, const mspipe_tcsr* g, int64_t iteration,
-                                       const int32_t* src, const int32_t* dst, const int32_t* neg,
-                                       const double* ts, int64_t num_events, int32_t fanout,
-                                       int32_t* out_nbr, int32_t* out_eid, double* out_ts, float* out_dt,
-                                       int32_t* out_cnt, int32_t* out_sub_ids, int32_t* out_nodes,
-                                       int32_t* out_winner, int32_t* out_num_unique, float* out_mem,
-                                       double* out_mem_ts, float* out_mail, double* out_mail_ts,
-                                       int64_t* out_version, const mspipe_gru* gru, const float* edge_feat,
-                                       double* out_commit_ts, float* out_commit_mail, void* workspace,
-                                       size_t ws_bytes, void* stream);
 
 /* A6 + A7 in one launch: mspipe_gru_apply, then mspipe_memory_writeback of
  * (nodes, num_unique, h', new_ts, new_mail) as version commit_version, the
@@ -452,23 +401,6 @@ MSPIPE_API mspipe_status mspipe_gru_apply_commit_out(const mspipe_gru* gru, mspi
                                           const float* new_mail, float* out_mem, int32_t* out_nodes,
                                           int32_t* out_num, const void* workspace, size_t ws_bytes,
                                           void* stream);
-
-/* A5 + A6 + A7 in ONE launch (3xTF32, immediate mailbox, no mitigation):
- * exactly mspipe_message_build (snap_h = NULL) + mspipe_gru_apply_commit of
- * the same batch, but the GEMM kernel builds its A operand in shared memory
- * from the snapshot rows (snap_mem / snap_mem_ts rows as in
- * mspipe_message_build), so no operand images or staged mail rows exist and
- * no workspace is needed; it writes h' (out_mem, nullable, winner order), and
- * the rows, timestamps and mail rows of version commit_version.  ts /
- * edge_feat: the batch's events.  Same ordering contract as
- * mspipe_gru_apply_commit. */
-MSPIPE_API mspipe_status mspipe_gru_build_apply_commit(const mspipe_gru* gru, mspipe_memory* st,
-                                            int64_t commit_version, int64_t num_events,
-                                            const double* ts, const float* edge_feat,
-                                            const float* snap_mem, const double* snap_mem_ts,
-                                            int64_t snap_step, const int32_t* nodes,
-                                            const int32_t* winner, const int32_t* num_unique,
-                                            float* out_mem, void* stream);
 
 /* ---------------------------------------------------------------------------
  * Row E: node memory sharded by node id (world > 1).  owner(v) = v mod world,

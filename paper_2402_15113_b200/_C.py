@@ -34,9 +34,9 @@ EXPORTS = ("mspipe_abi_version", "mspipe_last_error", "mspipe_check", "mspipe_sa
            "mspipe_util_graph_begin", "mspipe_util_graph_end", "mspipe_util_graph_launch", "mspipe_util_graph_destroy",
            "mspipe_memory_double_buffer", "mspipe_memory_tables", "mspipe_memory_set_committed",
            "mspipe_plan_timeline", "mspipe_plan_min_staleness", "mspipe_stale_histogram",
-           "mspipe_memory_prep_build", "mspipe_feature_fetch", "mspipe_updater_create",
-           "mspipe_message_build_deferred", "mspipe_memory_mail_deferred", "mspipe_gru_build_apply_commit",
-           "mspipe_util_rows_to_host", "mspipe_memory_winners", "mspipe_message_build_tables",
+           "mspipe_feature_fetch", "mspipe_updater_create",
+           "mspipe_message_build_deferred", "mspipe_memory_mail_deferred",
+           "mspipe_util_rows_to_host",
            "mspipe_gru_apply_commit_out", "mspipe_plan_stale_fractions", "mspipe_staleness_error")
 XCHG_FETCH_IDS, XCHG_FETCH_ROWS, XCHG_COMMIT = 0, 1, 2
 
@@ -83,9 +83,6 @@ def lib():
         L.mspipe_gru_create.argtypes = [C.POINTER(P), i32, i32, i32, i32, i64, P, P, P, P, P, P, P]
         L.mspipe_gru_destroy.argtypes = [P]
         L.mspipe_memory_dedup.argtypes = [P, P, P, i64, P, P, P, P]
-        L.mspipe_memory_winners.argtypes = [P, i64, P, P, i64, P, P, P, P]
-        L.mspipe_message_build_tables.argtypes = [P, P, i64, P, P, P, i64, P, P, P, P, P, P, C.c_size_t,
-                                                  C.POINTER(i64), P]
         L.mspipe_memory_update.argtypes = [P, P, P, P, P, i64, P, P, P, i64, P, P, P, P, P, P, P]
         L.mspipe_memory_writeback.argtypes = [P, i64, P, P, i64, P, P, P, P]
         L.mspipe_util_event_record.argtypes = [P, P]
@@ -104,12 +101,9 @@ def lib():
         L.mspipe_util_graph_destroy.argtypes = [P]
         L.mspipe_memory_prep.argtypes = [P, C.POINTER(Tcsr), i64, P, P, P, P, i64, i32, P, P, P, P, P, P, P, P, P, P,
                                          P, P, P, C.POINTER(Mitigation), C.POINTER(i64), P]
-        L.mspipe_memory_prep_build.argtypes = [P, C.POINTER(Tcsr), i64, P, P, P, P, i64, i32, P, P, P, P, P, P, P,
-                                               P, P, P, P, P, P, C.POINTER(i64), P, P, P, P, P, C.c_size_t, P]
         L.mspipe_updater_create.argtypes = [C.POINTER(P), i32, i32, i32, i32, i32, i32, i64, P, P, P, P, P, P, P]
         L.mspipe_message_build_deferred.argtypes = [P, P, i64, P, P, P, i64, i64, P, P, P, P, C.c_size_t, P]
         L.mspipe_memory_mail_deferred.argtypes = [P, i64, P, P, P, P, i64, P, P, P, P]
-        L.mspipe_gru_build_apply_commit.argtypes = [P, P, i64, i64, P, P, P, P, i64, P, P, P, P, P]
         L.mspipe_feature_fetch.argtypes = [P, P, i64, i32, P, i64, i32, P, i64, i32, P, P, P]
         L.mspipe_gru_workspace_size.argtypes = [P, i64]
         L.mspipe_gru_workspace_size.restype = C.c_size_t
@@ -479,22 +473,8 @@ def memory_dedup(st: MemoryHandle, src, dst, out, stream=None):
     return out
 
 
-def memory_winners(st: MemoryHandle, iteration, src, dst, out, stream=None):
-    """A2 of iteration `iteration` (dedup + double-buffer stamps): fills out["nodes"], out["winner"], out["num"]."""
-    _ck(lib().mspipe_memory_winners(st.h, int(iteration), ptr(src), ptr(dst), src.numel(), ptr(out["nodes"]),
-                                    ptr(out["winner"]), ptr(out["num"]), stream_ptr(stream)), "mspipe_memory_winners")
-    return out
 
 
-def message_build_tables(gru: GruHandle, st: MemoryHandle, iteration, src, dst, ts, edge_feat, winner, num, out_ts,
-                         out_mail, workspace, stream=None) -> int:
-    """A5 from the state tables of the version iteration's fetch reads; returns that version."""
-    v = i64(-1)
-    _ck(lib().mspipe_message_build_tables(gru.h, st.h, int(iteration), ptr(src), ptr(dst), ptr(ts), ts.numel(),
-                                          ptr(edge_feat), ptr(winner), ptr(num), ptr(out_ts), ptr(out_mail),
-                                          ptr(workspace), workspace.numel() * workspace.element_size(), C.byref(v),
-                                          stream_ptr(stream)), "mspipe_message_build_tables")
-    return int(v.value)
 
 
 def memory_update(st: MemoryHandle, gru: GruHandle, src, dst, ts, edge_feat, snap_mem, snap_mem_ts, snap_step,
@@ -511,7 +491,7 @@ def memory_prep(st: MemoryHandle, g: TcsrHandle, iteration, src, dst, neg, ts, f
                 out_mail=None, out_mail_ts=None, mitigation: Mitigation | None = None, stream=None) -> int:
     """A1+A2+A3(+A4) fused: fills samp (alloc_sample), dd (alloc_dedup) and the fetched rows."""
     v = i64(-1)
-    dd = dd if dd is not None else {}  # None: no dedup (mspipe_memory_winners does it)
+    dd = dd if dd is not None else {}  # None: no dedup (A1 + A3 only)
     _ck(lib().mspipe_memory_prep(st.h, C.byref(g.c), int(iteration), ptr(src), ptr(dst), ptr(neg), ptr(ts),
                                  src.numel(), fanout, ptr(samp["nbr"]), ptr(samp["eid"]), ptr(samp["ts"]),
                                  ptr(samp["dt"]), ptr(samp["cnt"]), ptr(samp["sub"]), ptr(dd.get("nodes")),
@@ -521,20 +501,6 @@ def memory_prep(st: MemoryHandle, g: TcsrHandle, iteration, src, dst, neg, ts, f
     return int(v.value)
 
 
-def memory_prep_build(st: MemoryHandle, g: TcsrHandle, iteration, src, dst, neg, ts, fanout, samp, dd, out_mem,
-                      out_mem_ts, out_mail, out_mail_ts, gru: GruHandle, edge_feat, out_commit_ts, out_commit_mail,
-                      workspace, stream=None) -> int:
-    """A1+A2+A3 and the A5 message build of the same batch in one launch (no mitigation)."""
-    v = i64(-1)
-    _ck(lib().mspipe_memory_prep_build(st.h, C.byref(g.c), int(iteration), ptr(src), ptr(dst), ptr(neg), ptr(ts),
-                                       src.numel(), fanout, ptr(samp["nbr"]), ptr(samp["eid"]), ptr(samp["ts"]),
-                                       ptr(samp["dt"]), ptr(samp["cnt"]), ptr(samp["sub"]), ptr(dd["nodes"]),
-                                       ptr(dd["winner"]), ptr(dd["num"]), ptr(out_mem), ptr(out_mem_ts),
-                                       ptr(out_mail), ptr(out_mail_ts), C.byref(v), gru.h, ptr(edge_feat),
-                                       ptr(out_commit_ts), ptr(out_commit_mail), ptr(workspace),
-                                       workspace.numel() * workspace.element_size(), stream_ptr(stream)),
-        "mspipe_memory_prep_build")
-    return int(v.value)
 
 
 def feature_fetch(sub_ids, sampled_eids, fanout, node_feat=None, edge_feat=None, out_node=None, out_edge=None,
@@ -606,13 +572,6 @@ def gru_apply_commit(gru: GruHandle, st: MemoryHandle, commit_version, num_event
                                       stream_ptr(stream)), "mspipe_gru_apply_commit")
 
 
-def gru_build_apply_commit(gru: GruHandle, st: MemoryHandle, commit_version, ts, edge_feat, snap_mem, snap_mem_ts,
-                           snap_step, upd, stream=None):
-    """A5+A6+A7 in one launch: the GEMM kernel builds its operand from the snapshot rows."""
-    _ck(lib().mspipe_gru_build_apply_commit(gru.h, st.h, int(commit_version), ts.numel(), ptr(ts), ptr(edge_feat),
-                                            ptr(snap_mem), ptr(snap_mem_ts), int(snap_step), ptr(upd["nodes"]),
-                                            ptr(upd["winner"]), ptr(upd["num"]), ptr(upd.get("mem")),
-                                            stream_ptr(stream)), "mspipe_gru_build_apply_commit")
 
 
 def alloc_dedup(num_events, device):

@@ -31,16 +31,6 @@ int env_int(const char* name, int def) {
   return (e && *e) ? atoi(e) : def;
 }
 
-bool pdl_enabled() {
-  static int on = -1;
-  if (on < 0) {
-    // measured on the wiki step (32.6 us without vs 35.0 us with): off by default
-    const char* e = getenv("MSPIPE_PDL");
-    on = (e && e[0] == '1') ? 1 : 0;
-  }
-  return on != 0;
-}
-
 static mspipe_status after_launch(const char* what) {
   return cuda_status(cudaGetLastError(), what);
 }
@@ -165,9 +155,6 @@ mspipe_status mspipe_memory_create(mspipe_memory** out, int64_t num_nodes, int32
   st->local_rows = (num_nodes - rank + world - 1) / world;
   cudaError_t e = cudaMalloc(&st->scratch, sizeof(int32_t) * (size_t)num_nodes);
   if (e == cudaSuccess) e = cudaMemset(st->scratch, 0xFF, sizeof(int32_t) * (size_t)num_nodes);
-  if (e == cudaSuccess) e = cudaMalloc(&st->bld_upos, sizeof(int32_t) * 2 * 8192);  // 2B pairs, B <= 8192
-  if (e == cudaSuccess) e = cudaMalloc(&st->bld_sync, sizeof(int32_t) * 2);
-  if (e == cudaSuccess) e = cudaMemset(st->bld_sync, 0, sizeof(int32_t) * 2);
   if (e == cudaSuccess && world > 1) {
     st->sh_cap = (num_nodes + world - 1) / world;
     st->sh_capw = st->sh_cap;  // unique nodes per owner never exceed its shard
@@ -298,7 +285,7 @@ mspipe_status mspipe_memory_destroy(mspipe_memory* st) {
   nccl_comm_destroy(st);
   void* bufs[] = {st->scratch, st->sh_needed, st->sh_slot_of, st->sh_send_ids, st->sh_recv_ids, st->sh_fsend,
                   st->sh_frecv, st->sh_csend, st->sh_crecv, st->sh_dest, st->sh_keytab, st->prev_nodes,
-                  st->prev_num, st->stamps, st->bld_upos, st->bld_sync};
+                  st->prev_num, st->stamps};
   for (void* b : bufs)
     if (b) cudaFree(b);
   for (int w = 0; w < 2; ++w) {
@@ -528,28 +515,6 @@ mspipe_status mspipe_memory_dedup(mspipe_memory* st, const int32_t* src, const i
   return after_launch("memory_dedup");
 }
 
-mspipe_status mspipe_memory_winners(mspipe_memory* st, int64_t iteration, const int32_t* src, const int32_t* dst,
-                                    int64_t num_events, int32_t* out_nodes, int32_t* out_winner,
-                                    int32_t* out_num_unique, void* stream) {
-  if (!st) return fail(MSPIPE_EINVAL, "memory_winners: NULL handle");
-  if (iteration < 1) return fail(MSPIPE_EINVAL, "memory_winners: iteration=%lld", (long long)iteration);
-  if (num_events < 0 || num_events > 16384)
-    return fail(MSPIPE_EINVAL, "memory_winners: num_events=%lld (0..16384)", (long long)num_events);
-  if (!out_num_unique) return fail(MSPIPE_EINVAL, "memory_winners: null out_num_unique");
-  cudaStream_t s = (cudaStream_t)stream;
-  const int64_t ring = iteration % (st->k + 1);
-  if (num_events == 0) {
-    mspipe_status rc = cuda_status(cudaMemsetAsync(out_num_unique, 0, sizeof(int32_t), s), "memory_winners");
-    if (rc == MSPIPE_OK && st->db) st->stamp_iter[ring] = iteration;  // no winners: nothing to stamp
-    return rc;
-  }
-  if (!src || !dst || !out_nodes || !out_winner) return fail(MSPIPE_EINVAL, "memory_winners: null input/output");
-  launch_dedup(src, dst, num_events, st->scratch, st->num_nodes, out_nodes, out_winner, out_num_unique, s,
-               st->db ? st->stamps + ring * st->num_nodes : nullptr, (int32_t)iteration);
-  mspipe_status rc = after_launch("memory_winners");
-  if (rc == MSPIPE_OK && st->db) st->stamp_iter[ring] = iteration;
-  return rc;
-}
 
 mspipe_status mspipe_memory_update(mspipe_memory* st, const mspipe_gru* gru, const int32_t* src,
                                    const int32_t* dst, const double* ts, int64_t num_events,
@@ -613,71 +578,14 @@ mspipe_status mspipe_memory_writeback(mspipe_memory* st, int64_t commit_version,
   return rc;
 }
 
-struct BuildArgs {  // mspipe_memory_prep_build's extra arguments
-  const mspipe_gru* gru;
-  const float* edge_feat;
-  double* out_ts;
-  float* out_mail;
-  void* workspace;
-  size_t ws_bytes;
-};
 
-static mspipe_status prep_impl(mspipe_memory* st, const mspipe_tcsr* g, int64_t iteration, const int32_t* src,
-                               const int32_t* dst, const int32_t* neg, const double* ts, int64_t num_events,
-                               int32_t fanout, int32_t* out_nbr, int32_t* out_eid, double* out_ts, float* out_dt,
-                               int32_t* out_cnt, int32_t* out_sub_ids, int32_t* out_nodes, int32_t* out_winner,
-                               int32_t* out_num_unique, float* out_mem, double* out_mem_ts, float* out_mail,
-                               double* out_mail_ts, const mspipe_mitigation* mit, int64_t* out_version,
-                               void* stream, const BuildArgs* ba);
-
-mspipe_status mspipe_memory_prep(mspipe_memory* st, const mspipe_tcsr* g, int64_t iteration,
-                                 const int32_t* src, const int32_t* dst, const int32_t* neg,
-                                 const double* ts, int64_t num_events, int32_t fanout,
-                                 int32_t* out_nbr, int32_t* out_eid, double* out_ts, float* out_dt,
-                                 int32_t* out_cnt, int32_t* out_sub_ids, int32_t* out_nodes,
-                                 int32_t* out_winner, int32_t* out_num_unique, float* out_mem,
-                                 double* out_mem_ts, float* out_mail, double* out_mail_ts,
-                                 const mspipe_mitigation* mit, int64_t* out_version, void* stream) {
-  return prep_impl(st, g, iteration, src, dst, neg, ts, num_events, fanout, out_nbr, out_eid, out_ts, out_dt, out_cnt,
-                   out_sub_ids, out_nodes, out_winner, out_num_unique, out_mem, out_mem_ts, out_mail, out_mail_ts, mit,
-                   out_version, stream, nullptr);
-}
-
-mspipe_status mspipe_memory_prep_build(mspipe_memory* st, const mspipe_tcsr* g, int64_t iteration,
-                                       const int32_t* src, const int32_t* dst, const int32_t* neg,
-                                       const double* ts, int64_t num_events, int32_t fanout,
-                                       int32_t* out_nbr, int32_t* out_eid, double* out_ts, float* out_dt,
-                                       int32_t* out_cnt, int32_t* out_sub_ids, int32_t* out_nodes,
-                                       int32_t* out_winner, int32_t* out_num_unique, float* out_mem,
-                                       double* out_mem_ts, float* out_mail, double* out_mail_ts,
-                                       int64_t* out_version, const mspipe_gru* gru, const float* edge_feat,
-                                       double* out_commit_ts, float* out_commit_mail, void* workspace,
-                                       size_t ws_bytes, void* stream) {
-  if (!gru) return fail(MSPIPE_EINVAL, "memory_prep_build: NULL GRU handle");
-  if (gru->precision != MSPIPE_FP32_3XTF32 || gru->d.mailbox != MSPIPE_MAILBOX_IMMEDIATE)
-    return fail(MSPIPE_EUNSUPPORTED, "memory_prep_build: only for an immediate-mailbox MSPIPE_FP32_3XTF32 handle");
-  if (!st || gru->d.M != st->mem_dim || gru->d.He != st->edge_dim)
-    return fail(MSPIPE_EINVAL, "memory_prep_build: NULL memory handle or dims differ from the GRU's");
-  if (num_events > gru->max_events)
-    return fail(MSPIPE_EINVAL, "memory_prep_build: num_events=%lld > max_events %lld of the GRU handle",
-                (long long)num_events, (long long)gru->max_events);
-  if (num_events > 0 && (!out_commit_ts || !out_commit_mail || (st->edge_dim > 0 && !edge_feat) || !workspace ||
-                         ws_bytes < mspipe_gru_workspace_size(gru, num_events)))
-    return fail(MSPIPE_EINVAL, "memory_prep_build: null build output / edge features, or workspace < %zu bytes",
-                mspipe_gru_workspace_size(gru, num_events));
-  const BuildArgs ba{gru, edge_feat, out_commit_ts, out_commit_mail, workspace, ws_bytes};
-  return prep_impl(st, g, iteration, src, dst, neg, ts, num_events, fanout, out_nbr, out_eid, out_ts, out_dt, out_cnt,
-                   out_sub_ids, out_nodes, out_winner, out_num_unique, out_mem, out_mem_ts, out_mail, out_mail_ts,
-                   nullptr, out_version, stream, &ba);
-}
-
-static mspipe_status prep_impl(mspipe_memory* st, const mspipe_tcsr* g, int64_t iteration, const int32_t* src,
-                               const int32_t* dst, const int32_t* neg, const double* ts, int64_t num_events,
-                               int32_t fanout, int32_t* out_nbr, int32_t* out_eid, double* out_ts, float* out_dt,
-                               int32_t* out_cnt, int32_t* out_sub_ids, int32_t* out_nodes, int32_t* out_winner,
-                               int32_t* out_num_unique, float* out_mem, double* out_mem_ts, float* out_mail,
-                               double* out_mail_ts, const mspipe_mitigation* mit, int64_t* out_version,
-                               void* stream, const BuildArgs* ba) {
+mspipe_status mspipe_memory_prep(mspipe_memory* st, const mspipe_tcsr* g, int64_t iteration, const int32_t* src,
+                                 const int32_t* dst, const int32_t* neg, const double* ts, int64_t num_events,
+                                 int32_t fanout, int32_t* out_nbr, int32_t* out_eid, double* out_ts, float* out_dt,
+                                 int32_t* out_cnt, int32_t* out_sub_ids, int32_t* out_nodes, int32_t* out_winner,
+                                 int32_t* out_num_unique, float* out_mem, double* out_mem_ts, float* out_mail,
+                                 double* out_mail_ts, const mspipe_mitigation* mit, int64_t* out_version,
+                                 void* stream) {
   if (!st) return fail(MSPIPE_EINVAL, "memory_prep: NULL handle");
   if (st->world > 1) return fail(MSPIPE_EUNSUPPORTED, "memory_prep: fused prep reads local tables; world > 1 uses the sharded fetch");
   if (!tcsr_ok(g) || g->num_nodes != st->num_nodes) return fail(MSPIPE_EINVAL, "memory_prep: bad T-CSR");
@@ -691,9 +599,8 @@ static mspipe_status prep_impl(mspipe_memory* st, const mspipe_tcsr* g, int64_t 
   // every argument is validated before any fork or launch (an error return
   // leaves no branch unjoined and nothing enqueued)
   const bool dedup = out_nodes || out_winner || out_num_unique;
-  if (dedup && ba == nullptr && !(out_nodes && out_winner && out_num_unique))
+  if (dedup && !(out_nodes && out_winner && out_num_unique))
     return fail(MSPIPE_EINVAL, "memory_prep: out_nodes / out_winner / out_num_unique go together");
-  if (!dedup && ba) return fail(MSPIPE_EINVAL, "memory_prep_build: needs the dedup outputs");
   if (num_events > 0 &&
       (!src || !dst || !neg || !ts || !out_nbr || !out_eid || !out_ts || !out_dt || !out_cnt || !out_sub_ids ||
        (dedup && (!out_nodes || !out_winner || !out_num_unique)) || !out_mem || !out_mem_ts))
@@ -734,23 +641,12 @@ static mspipe_status prep_impl(mspipe_memory* st, const mspipe_tcsr* g, int64_t 
                     (dedup ? (st->stamp_iter[c % (st->k + 1)] == c || c == iteration)
                            : (c != iteration && st->stamp_iter[c % (st->k + 1)] == c));
     const CatchUp cua = cu ? catchup_args(st, c) : CatchUp{};
-    PrepBuild pb{};
-    if (ba) {
-      pb.d = ba->gru->d;
-      pb.xbuf = (float*)ba->workspace;
-      pb.ef = ba->edge_feat;
-      pb.out_ts = ba->out_ts;
-      pb.out_mail = ba->out_mail;
-      pb.mail_stride = st->mail_stride;
-      pb.upos = st->bld_upos;
-      pb.sync = st->bld_sync;
-    }
     cudaError_t e = launch_prep(to_tcsr(g), src, dst, neg, ts, num_events, fanout, out_nbr, out_eid, out_ts, out_dt,
                                 out_cnt, out_sub_ids, st->scratch, out_nodes, out_winner, out_num_unique, t.mem,
                                 t.mem_ts, st->mem_dim, t.mail, t.mail_ts, st->mail_stride, out_mem,
                                 out_mem_ts, out_mail, out_mail_ts, s,
                                 (st->db && dedup) ? st->stamps + (iteration % (st->k + 1)) * st->num_nodes : nullptr,
-                                (int32_t)iteration, cu ? &cua : nullptr, ba ? &pb : nullptr);
+                                (int32_t)iteration, cu ? &cua : nullptr);
     if (e != cudaSuccess) return cuda_status(e, "memory_prep: launch");
     if (st->db && dedup) st->stamp_iter[iteration % (st->k + 1)] = iteration;
     if (cu) st->caught_up = c;
@@ -802,36 +698,6 @@ mspipe_status mspipe_message_build(const mspipe_gru* gru, const double* ts, int6
   return after_launch("message_build");
 }
 
-mspipe_status mspipe_message_build_tables(const mspipe_gru* gru, const mspipe_memory* st, int64_t iteration,
-                                          const int32_t* src, const int32_t* dst, const double* ts,
-                                          int64_t num_events, const float* edge_feat, const int32_t* winner,
-                                          const int32_t* num_unique, double* out_ts, float* out_mail,
-                                          void* workspace, size_t ws_bytes, int64_t* out_version, void* stream) {
-  if (!gru || !st) return fail(MSPIPE_EINVAL, "message_build_tables: NULL handle");
-  if (gru->precision == MSPIPE_FP32_SIMT || gru->d.mailbox != MSPIPE_MAILBOX_IMMEDIATE)
-    return fail(MSPIPE_EUNSUPPORTED, "message_build_tables: needs a tensor-core, immediate-mailbox handle");
-  if (st->world != 1) return fail(MSPIPE_EUNSUPPORTED, "message_build_tables: world > 1");
-  if (gru->d.M != st->mem_dim || gru->d.He != st->edge_dim) return fail(MSPIPE_EINVAL, "message_build_tables: dims");
-  if (iteration < 1 || num_events < 0 || num_events > gru->max_events)
-    return fail(MSPIPE_EINVAL, "message_build_tables: iteration=%lld num_events=%lld (<= max_events %lld)",
-                (long long)iteration, (long long)num_events, (long long)gru->max_events);
-  if (st->committed < iteration - 1 - st->k || st->committed > iteration - 1)  // the fetch's gate (Alg. 1 L8-L11)
-    return fail(MSPIPE_ESTALE, "message_build_tables: iteration %lld with committed=%lld violates k=%d",
-                (long long)iteration, (long long)st->committed, st->k);
-  if (out_version) *out_version = st->committed;
-  if (num_events == 0) return MSPIPE_OK;
-  if (ws_bytes < mspipe_gru_workspace_size(gru, num_events) || !workspace)
-    return fail(MSPIPE_EINVAL, "message_build_tables: workspace of %zu bytes < %zu", ws_bytes,
-                mspipe_gru_workspace_size(gru, num_events));
-  if (!src || !dst || !ts || (gru->d.He > 0 && !edge_feat) || !winner || !num_unique || !out_ts || !out_mail)
-    return fail(MSPIPE_EINVAL, "message_build_tables: null input/output");
-  const TableSet t = table_set(st, st->committed);
-  cudaError_t e = launch_gru_tc(gru->d, gru->wtc, (float*)workspace, ts, num_events, edge_feat, t.mem, t.mem_ts, 1,
-                                nullptr, winner, num_unique, nullptr, out_ts, out_mail, st->mail_stride,
-                                (cudaStream_t)stream, kGruBuild, nullptr, src, dst);
-  if (e != cudaSuccess) return cuda_status(e, "message_build_tables: launch");
-  return after_launch("message_build_tables");
-}
 
 mspipe_status mspipe_gru_apply(const mspipe_gru* gru, int64_t num_events, const float* snap_mem,
                                int64_t snap_step, const float* snap_h, const int32_t* winner,
@@ -972,50 +838,6 @@ static mspipe_status apply_commit_impl(const mspipe_gru* gru, mspipe_memory* st,
   return rc;
 }
 
-mspipe_status mspipe_gru_build_apply_commit(const mspipe_gru* gru, mspipe_memory* st, int64_t commit_version,
-                                            int64_t num_events, const double* ts, const float* edge_feat,
-                                            const float* snap_mem, const double* snap_mem_ts, int64_t snap_step,
-                                            const int32_t* nodes, const int32_t* winner, const int32_t* num_unique,
-                                            float* out_mem, void* stream) {
-  if (!gru || !st) return fail(MSPIPE_EINVAL, "gru_build_apply_commit: NULL handle");
-  if (gru->precision != MSPIPE_FP32_3XTF32 || gru->d.mailbox != MSPIPE_MAILBOX_IMMEDIATE)
-    return fail(MSPIPE_EUNSUPPORTED, "gru_build_apply_commit: needs an immediate-mailbox MSPIPE_FP32_3XTF32 handle");
-  if (st->world != 1) return fail(MSPIPE_EUNSUPPORTED, "gru_build_apply_commit: world > 1");
-  if (gru->d.M != st->mem_dim || gru->d.He != st->edge_dim) return fail(MSPIPE_EINVAL, "gru_build_apply_commit: dims");
-  if (commit_version != st->committed + 1)
-    return fail(MSPIPE_EORDER, "gru_build_apply_commit: commit_version=%lld but committed=%lld",
-                (long long)commit_version, (long long)st->committed);
-  if (num_events < 0 || num_events > gru->max_events || snap_step < 1)
-    return fail(MSPIPE_EINVAL, "gru_build_apply_commit: num_events=%lld snap_step=%lld", (long long)num_events,
-                (long long)snap_step);
-  if (num_events > 0 && (!ts || (st->edge_dim > 0 && !edge_feat) || !snap_mem || !snap_mem_ts || !nodes ||
-                         !winner || !num_unique))
-    return fail(MSPIPE_EINVAL, "gru_build_apply_commit: null input");
-  const int64_t max_n = 2 * num_events;
-  const bool done = st->db && st->caught_up == commit_version;
-  if (st->db && (num_events == 0 || !done)) {  // catch-up not enqueued by a prep: its own kernel first
-    cudaError_t e = db_catchup(st, commit_version, nodes, num_unique, max_n, (cudaStream_t)stream, !done);
-    if (e != cudaSuccess) return cuda_status(e, "gru_build_apply_commit: catch-up");
-  }
-  if (num_events > 0) {
-    const TableSet t = table_set(st, commit_version);
-    GruCommit c{nodes, t.mem, t.mem_ts, t.mail, t.mail_ts, nullptr, nullptr, st->num_nodes, st->mail_stride};
-    if (done) {  // the kernel saves this commit's winner list
-      const int p = (int)(commit_version & 1);
-      c.save_nodes = st->prev_nodes + p * st->num_nodes;
-      c.save_num = st->prev_num + p;
-    }
-    cudaError_t e = launch_gru_fb(gru->d, gru->wtc, ts, num_events, edge_feat, snap_mem, snap_mem_ts, snap_step,
-                                  winner, num_unique, out_mem, c, (cudaStream_t)stream);
-    if (e != cudaSuccess) return cuda_status(e, "gru_build_apply_commit: launch");
-  }
-  mspipe_status rc = after_launch("gru_build_apply_commit");
-  if (rc == MSPIPE_OK) {
-    st->committed = commit_version;
-    st->prev_max[commit_version & 1] = max_n;
-  }
-  return rc;
-}
 
 // ---------------------------------------------------------------------------
 // row E: sharded memory

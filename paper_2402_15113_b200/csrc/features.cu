@@ -38,7 +38,6 @@ __global__ void __launch_bounds__(kFeatThreads) k_feature_fetch(
     const int32_t* __restrict__ sub, const int32_t* __restrict__ eid, int64_t R, int32_t F,
     const float* __restrict__ nfeat, int64_t N, int32_t nstride, const float* __restrict__ efeat, int64_t E,
     int32_t estride, float* __restrict__ out_n, float* __restrict__ out_e) {
-  pdl_begin();
   const int lane = threadIdx.x & 31;
   const int64_t rows_n = nfeat ? R * (F + 1) : 0;
   const int64_t rows_e = efeat ? R * F : 0;

@@ -117,7 +117,6 @@ __global__ void __launch_bounds__(kThreads) k_gru_simt(
   __shared__ __align__(16) float As[2][kMT][kKC + 4];
   __shared__ __align__(16) float Bs[2][kKC][kNT];
   __shared__ RowInfo ri;
-  pdl_begin();
   const int32_t U = __ldg(num_unique);
   const int32_t m0 = blockIdx.x * kMT;
   if (m0 >= U) return;

@@ -147,15 +147,8 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
         "=r"(r[29]), "=r"(r[30]), "=r"(r[31])                                                               \
       : "r"(taddr))
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
-#ifndef MSPIPE_CLUSTER_FENCE
-#define MSPIPE_CLUSTER_FENCE 0
-#endif
 __device__ __forceinline__ void cluster_sync_all() {
-#if MSPIPE_CLUSTER_FENCE  // timing experiment only: no release (DSMEM visibility not guaranteed)
-  asm volatile("barrier.cluster.arrive.relaxed.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
-#else
   asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
-#endif
 }
 __device__ __forceinline__ uint32_t cluster_rank() {
   uint32_t r;
@@ -471,7 +464,6 @@ __device__ __forceinline__ void build_bf16(const TcArgs& a) {
 
 // A5: one warp per (row, chunk).  lane = column inside the chunk.
 __global__ void __launch_bounds__(256) k_build_x(TcArgs a) {
-  pdl_begin();
   if (a.d.bf16) {
     build_bf16(a);
     return;
@@ -518,61 +510,6 @@ __global__ void __launch_bounds__(256) k_build_x(TcArgs a) {
     const uint32_t off = tc::sw128_off((uint32_t)row, (uint32_t)lane);
     *reinterpret_cast<float*>(blk + off) = hi;
     *reinterpret_cast<float*>(blk + tc::kATile + off) = lo;
-  }
-}
-
-// A5, one warp per winner row u < U (no padding rows: rows >= U of the last M
-// tile only feed output rows the epilogue drops): every lane issues the loads
-// of its column in all kRowChunks chunks in one round, then converts and stores.
-constexpr int kRowChunks = 20;  // Kpad / 32 <= 20 (K <= 640); else k_build_x
-__global__ void __launch_bounds__(256) k_build_rows(TcArgs a) {
-  pdl_begin();
-  const GruDesc& d = a.d;
-  const int32_t U = __ldg(a.num_unique);
-  const int32_t nchunks = d.Kpad / tc::kKC;
-  const int lane = threadIdx.x & 31;
-  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const int32_t M = d.M;
-  for (int64_t u = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; u < U; u += nwarps) {
-    const int32_t p = __ldg(a.winner + u);
-    const int32_t ev = p >> 1, role = p & 1;
-    const int64_t rw = snap_row(a, ev, role), ro = snap_row(a, ev, role ^ 1);
-    const float* sw = a.snap_mem + rw * M;
-    const float* so = a.snap_mem + ro * M;
-    const float* hrow = a.snap_h ? a.snap_h + (role ? a.B + ev : (int64_t)ev) * M : sw;
-    const double t_ev = __ldg(a.ts + ev), t_w = __ldg(a.snap_ts + rw);
-    float v[kRowChunks];
-#pragma unroll
-    for (int c = 0; c < kRowChunks; ++c) {
-      const int32_t k = c * tc::kKC + lane;
-      v[c] = 0.f;
-      if (c < nchunks) {
-        if (k < M) v[c] = __ldg(sw + k);
-        else if (k < 2 * M) v[c] = __ldg(so + (k - M));
-        else if (k < d.Dm) v[c] = __ldg(a.ef + (int64_t)ev * d.He + (k - 2 * M));
-        else if (k >= d.Dx && k < d.K) v[c] = __ldg(hrow + (k - d.Dx));
-      }
-    }
-    const float dt = (float)(t_ev - t_w);  // Δt (G4)
-    const int32_t mt = (int32_t)(u / tc::kM), row = (int32_t)(u % tc::kM);
-#pragma unroll
-    for (int c = 0; c < kRowChunks; ++c) {
-      if (c >= nchunks) break;
-      const int32_t k = c * tc::kKC + lane;
-      float x = v[c];
-      if (k >= d.Dm && k < d.Dx) {
-        const int q = k - d.Dm;
-        x = time_cos(fmaf(__ldg(d.time_w + q), dt, __ldg(d.time_b + q)));
-      }
-      if (k < a.mail_stride) a.out_mail[u * a.mail_stride + k] = k < d.Dm ? x : 0.f;
-      const float hi = tc::tf32_rna(x);
-      const float lo = tc::tf32_rna(x - hi);
-      char* blk = reinterpret_cast<char*>(a.xbuf) + ((int64_t)mt * nchunks + c) * tc::kABlock;
-      const uint32_t off = tc::sw128_off((uint32_t)row, (uint32_t)lane);
-      *reinterpret_cast<float*>(blk + off) = hi;
-      *reinterpret_cast<float*>(blk + tc::kATile + off) = lo;
-    }
-    if (lane == 0) a.out_ts[u] = t_ev;
   }
 }
 
@@ -667,10 +604,6 @@ __device__ __forceinline__ void commit_rows(const TcArgs& a, int32_t m0, int32_t
 // done, overlapping them with the epilogue; the K-split partials go through
 // two receive buffers (tile parity), so one cluster barrier per tile orders
 // every push after the owner's reads of two tiles before.
-#ifndef MSPIPE_PF_GEMM
-#define MSPIPE_PF_GEMM 0  // measured: no effect on the wiki step (24.9 vs 24.7 us)
-#endif
-constexpr bool kPfGemm = MSPIPE_PF_GEMM != 0;
 #ifndef MSPIPE_MAIL_PF
 #define MSPIPE_MAIL_PF 1
 #endif
@@ -682,11 +615,8 @@ constexpr bool kMailPf = MSPIPE_MAIL_PF != 0;
 #endif
 constexpr bool kAsyncPush = MSPIPE_ASYNC_PUSH != 0;
 
-#ifndef MSPIPE_GEMM_MINB
-#define MSPIPE_GEMM_MINB 1  // register cap (min blocks per SM) of k_gru_tc: co-residence with prep / build
-#endif
 template <bool kBf>
-__global__ void __launch_bounds__(tc::kThreads, MSPIPE_GEMM_MINB) k_gru_tc(TcArgs a) {
+__global__ void __launch_bounds__(tc::kThreads, 1) k_gru_tc(TcArgs a) {
   using namespace tc;
   constexpr int SB = kBf ? kStageBytes16 : kStageBytes;
   constexpr int AB = kBf ? kATile16 : kABlock;
@@ -706,7 +636,6 @@ __global__ void __launch_bounds__(tc::kThreads, MSPIPE_GEMM_MINB) k_gru_tc(TcArg
 
   const GruDesc& d = a.d;
   PHASE(9);
-  pdl_begin();
   // U (written by the previous step's prep) is a cold HBM read: it is consumed
   // only after the setup and the first tile's speculative loads below
   const int32_t U = __ldg(a.num_unique);
@@ -756,14 +685,6 @@ __global__ void __launch_bounds__(tc::kThreads, MSPIPE_GEMM_MINB) k_gru_tc(TcArg
     bulk_g2s(st, reinterpret_cast<const char*>(a.xbuf) + ((int64_t)mt_l * nchunks + c0 + ci) * AB, AB, &full[s]);
     bulk_g2s(st + AB, reinterpret_cast<const char*>(a.wtc) + ((int64_t)jt_l * nchunks + c0 + ci) * BB, BB, &full[s]);
   };
-  // L2 warm-up of a tile's chunks beyond the stage ring (their bulk copies
-  // wait for MMAs to free a stage; by then they hit L2)
-  auto warm_tile = [&](int32_t mt_l, int jt_l) {
-    for (int ci = kStages; ci < nc; ++ci) {
-      l2_prefetch(reinterpret_cast<const char*>(a.xbuf) + ((int64_t)mt_l * nchunks + c0 + ci) * AB, AB);
-      l2_prefetch(reinterpret_cast<const char*>(a.wtc) + ((int64_t)jt_l * nchunks + c0 + ci) * BB, BB);
-    }
-  };
   // the cluster's first tile (q = blockIdx.y) is issued before U is known: the
   // workspace holds every M tile of the 2B bound, so the reads are in bounds
   int pre = 0;  // chunks of the current tile the loader already issued
@@ -791,7 +712,6 @@ __global__ void __launch_bounds__(tc::kThreads, MSPIPE_GEMM_MINB) k_gru_tc(TcArg
     const int32_t m0 = mt * kM;
     float4* recv = recv2 + (kAsyncPush ? 0 : (ti & 1)) * (kRecvBytes / 16);
     if (warp == 0 && lane == 0) {
-      if (ti == 0 && kPfGemm) warm_tile(mt, jt);
       for (int ci = pre; ci < nc; ++ci) load_chunk(ti, mt, jt, ci);
     } else if (warp == 1 && lane == 0) {
       // MMA issuer.  Each K chunk accumulates into its OWN 64-column TMEM
@@ -879,7 +799,6 @@ __global__ void __launch_bounds__(tc::kThreads, MSPIPE_GEMM_MINB) k_gru_tc(TcArg
       const int64_t qn = q + gridDim.y;
       if (qn < tiles) {
         for (; pre < nc && pre < kStages; ++pre) load_chunk(ti + 1, (int32_t)(qn / J), (int)(qn % J), pre);
-        if (kPfGemm) warm_tile((int32_t)(qn / J), (int)(qn % J));
       }
     }
     const int m = warp * 32 + lane;
@@ -1019,7 +938,6 @@ __global__ void __launch_bounds__(256) k_build_deferred(GruDesc d, float* xbuf, 
                                                         const float* snap_mail, int64_t mail_stride, int64_t step,
                                                         const int32_t* winner, const int32_t* num_unique,
                                                         double* out_ts) {
-  pdl_begin();
   const int32_t U = __ldg(num_unique);
   const int32_t nchunks = d.Kpad / tc::kKC;
   const int64_t items = (int64_t)U * nchunks;
@@ -1063,7 +981,6 @@ __global__ void __launch_bounds__(256) k_mail_deferred(const int32_t* src, const
                                                        const int32_t* winner, const int32_t* num_unique,
                                                        const float* mem, int32_t M, float* mail, double* mail_ts,
                                                        int64_t mail_stride, int64_t num_nodes) {
-  pdl_begin();
   const int32_t U = __ldg(num_unique);
   const int lane = threadIdx.x & 31;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -1097,320 +1014,6 @@ void launch_mail_deferred(const int32_t* src, const int32_t* dst, const double* 
 }
 
 // ---------------------------------------------------------------------------
-// k_gru_fb — A5 + A6 + A7 in ONE kernel (mspipe_gru_build_apply_commit, 3xTF32,
-// immediate mailbox, no mitigation).  The CTA builds its own A operand in
-// shared memory instead of loading images written by k_build_x: 6 builder
-// warps gather the message x = [s_w | s_o | e | cos(w dt + p) | h] of its 128
-// rows for its K range chunk by chunk, split hi | lo into the SWIZZLE_128B
-// stage buffers, fence the generic->async proxy and arrive on the stage's
-// full barrier; one thread streams the B images with cp.async.bulk; the MMA
-// issuer, TMEM buffers, K-split exchange and GRU epilogue are k_gru_tc's.
-// The mail rows of the commit ([s_w | s_o | e], G14) are written to the state
-// table by the builders (chunk c by the CTA with jt = c mod J), mem_ts /
-// mail_ts by the epilogue.  One launch instead of k_build_x + k_gru_tc, and no
-// operand images in HBM.
-// ---------------------------------------------------------------------------
-int gru_tc_splits(int64_t max_rows, const GruDesc& d, bool shared_buffers = false);
-constexpr int kFBThreads = 256;
-constexpr int kFBBuilders = kFBThreads - 64;
-
-__device__ __forceinline__ void fence_proxy_async_smem() {
-  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(tc::smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void builders_sync() {
-  asm volatile("bar.sync 1, %0;\n" ::"r"(kFBBuilders) : "memory");
-}
-
-// x[k] of winner pair p with its Δt precomputed (the k_build_x value)
-__device__ __forceinline__ float xval(const TcArgs& a, int32_t p, int32_t k, float dt) {
-  const GruDesc& d = a.d;
-  const int32_t M = d.M;
-  const int32_t ev = p >> 1, role = p & 1;
-  const int64_t rw = role ? a.B + ev : ev;
-  const int64_t ro = role ? ev : a.B + ev;
-  const float* __restrict__ snap = a.snap_mem;
-  if (k < M) return __ldg(snap + rw * a.step * M + k);
-  if (k < 2 * M) return __ldg(snap + ro * a.step * M + (k - M));
-  if (k < d.Dm) return __ldg(a.ef + (int64_t)ev * d.He + (k - 2 * M));
-  if (k < d.Dx) return time_cos(fmaf(__ldg(d.time_w + (k - d.Dm)), dt, __ldg(d.time_b + (k - d.Dm))));
-  if (k < d.K) return __ldg(snap + rw * a.step * M + (k - d.Dx));
-  return 0.f;
-}
-
-__global__ void __launch_bounds__(kFBThreads, 1) k_gru_fb(TcArgs a) {
-  using namespace tc;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
-  uint64_t* empty = full + kStages;
-  uint64_t* acc_full = empty + kStages;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 1);
-  int32_t* rownode = reinterpret_cast<int32_t*>(smem + kStages * kStageBytes + 512);
-  float4* hbuf = reinterpret_cast<float4*>(smem + kStages * kStageBytes + 1024);
-  float4* recv = reinterpret_cast<float4*>(smem + kStages * kStageBytes + 1024 + kHBufBytes);
-  float* sbias = reinterpret_cast<float*>(smem + kStages * kStageBytes + 1024 + kHBufBytes + kRecvBytes);
-  int32_t* rpair = reinterpret_cast<int32_t*>(sbias + kN);  // [128] winner pair of each row, -1 past U
-  float* rdt = reinterpret_cast<float*>(rpair + kM);        // [128] Δt of each row (G4)
-
-  const GruDesc& d = a.d;
-  pdl_begin();
-  const int32_t U = __ldg(a.num_unique);
-  const int32_t mt = blockIdx.z;
-  const int32_t m0 = mt * kM;
-  const int jt = blockIdx.y;
-  const int J = (int)gridDim.y;
-  const int S = gridDim.x;
-  const int split = blockIdx.x;
-  if (a.save_num && mt == 0 && jt == 0 && split == 0 && threadIdx.x == 0) *a.save_num = U;
-  if (m0 >= U) return;  // uniform across the cluster
-  const int32_t nchunks = d.Kpad / kKC;
-  const int32_t c0 = split * nchunks / S, c1 = (split + 1) * nchunks / S;
-  const int32_t nc = c1 - c0;
-  const uint32_t tcols = nc <= 2 ? 128u : (nc <= 4 ? 256u : 512u);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int rank = S > 1 ? (int)cluster_rank() : 0;
-  const int rb = rank * kM / S, re = (rank + 1) * kM / S;
-
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < kStages; ++s) {
-      mbar_init(&full[s], 1 + kFBBuilders);  // the B copy's expect_tx + every builder
-      mbar_init(&empty[s], 1);
-    }
-    mbar_init(acc_full, 1);
-    fence_barrier_init();
-  }
-  if (warp == 2) tmem_alloc(tmem_slot, tcols);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-
-  if (warp == 0 && lane == 0) {
-    const char* bbase = reinterpret_cast<const char*>(a.wtc) + (int64_t)jt * nchunks * kBBlock;
-    for (int ci = 0; ci < nc; ++ci) {
-      const int s = ci % kStages;
-      const uint32_t ph = (uint32_t)(ci / kStages) & 1u;
-      mbar_wait(&empty[s], ph ^ 1u);
-      mbar_arrive_expect_tx(&full[s], kBBlock);
-      bulk_g2s(smem + s * kStageBytes + kABlock, bbase + (int64_t)(c0 + ci) * kBBlock, kBBlock, &full[s]);
-    }
-  } else if (warp == 1 && lane == 0) {
-    for (int ci = 0; ci < nc; ++ci) {
-      const int s = ci % kStages;
-      const uint32_t ph = (uint32_t)(ci / kStages) & 1u;
-      mbar_wait(&full[s], ph);
-      tc_fence_after();
-      const uint32_t base = smem_u32(smem + s * kStageBytes);
-      const uint64_t da_hi = sw128_desc(base), da_lo = sw128_desc(base + kATile);
-      const uint64_t db_hi = sw128_desc(base + kABlock), db_lo = sw128_desc(base + kABlock + kBTile);
-      const uint32_t tacc = tmem + (uint32_t)(ci * kN);
-#pragma unroll
-      for (int kk = 0; kk < kKC / 8; ++kk) {
-        const uint64_t adv = (uint64_t)(kk * 32) >> 4;
-        mma_tf32(tacc, da_lo + adv, db_hi + adv, kIdesc, kk != 0);
-        mma_tf32(tacc, da_hi + adv, db_lo + adv, kIdesc, 1u);
-        mma_tf32(tacc, da_hi + adv, db_hi + adv, kIdesc, 1u);
-      }
-      mma_commit(&empty[s]);
-    }
-    mma_commit(acc_full);
-  } else if (warp >= 2) {
-    const int bt = threadIdx.x - 64;
-    // rows: winner pair, Δt, committed node; h and biases for the epilogue
-    for (int r = bt; r < kM; r += kFBBuilders) {
-      const int32_t u = m0 + r;
-      int32_t p = -1, node = -1;
-      float dt = 0.f;
-      if (u < U) {
-        p = __ldg(a.winner + u);
-        const int64_t ev = p >> 1;
-        const int64_t rw = (p & 1) ? a.B + ev : ev;
-        dt = (float)(__ldg(a.ts + ev) - __ldg(a.snap_ts + rw * a.step));
-        node = __ldg(a.nodes + u);
-        if (a.save_nodes && jt == 0 && split == 0) a.save_nodes[u] = node;
-      }
-      rpair[r] = p;
-      rdt[r] = dt;
-      rownode[r] = node;
-    }
-    for (int it = bt; it < (re - rb) * (kJ / 4); it += kFBBuilders) {
-      const int mm = rb + it / (kJ / 4), q = it % (kJ / 4);
-      const int32_t u = m0 + mm, j0 = jt * kJ + q * 4;
-      float4 hv = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (u < U && j0 < d.M) {
-        const int32_t p = __ldg(a.winner + u);
-        const int64_t rw = (p & 1) ? a.B + (p >> 1) : (p >> 1);
-        hv = __ldg(reinterpret_cast<const float4*>(a.snap_mem + rw * a.step * d.M + j0));
-      }
-      hbuf[mm * (kJ / 4) + q] = hv;
-    }
-    for (int i = bt; i < kN; i += kFBBuilders) sbias[i] = __ldg(d.bias + jt * kN + i);
-    builders_sync();
-    // the A operand of this CTA's K range, chunk by chunk into the stage ring
-    float* __restrict__ mail = a.commit_mail;
-    for (int ci = 0; ci < nc; ++ci) {
-      const int s = ci % kStages;
-      const uint32_t ph = (uint32_t)(ci / kStages) & 1u;
-      mbar_wait(&empty[s], ph ^ 1u);
-      uint8_t* st = smem + s * kStageBytes;
-      const int32_t c = c0 + ci;
-      const bool mailw = a.commit_mail && (c % J) == jt;
-      for (int e = bt; e < kM * kKC; e += kFBBuilders) {
-        const int row = e >> 5, col = e & 31;
-        const int32_t k = c * kKC + col;
-        const int32_t p = rpair[row];
-        const float v = p >= 0 ? xval(a, p, k, rdt[row]) : 0.f;
-        const float hi = tf32_rna(v);
-        const uint32_t off = sw128_off((uint32_t)row, (uint32_t)col);
-        *reinterpret_cast<float*>(st + off) = hi;
-        *reinterpret_cast<float*>(st + kATile + off) = tf32_rna(v - hi);
-        if (mailw && p >= 0 && k < a.mail_stride)
-          mail[(int64_t)rownode[row] * a.mail_stride + k] = k < d.Dm ? v : 0.f;
-      }
-      fence_proxy_async_smem();  // generic-proxy smem writes -> visible to the tensor core
-      mbar_arrive(&full[s]);
-    }
-  }
-  __syncwarp();
-
-  // ---------------- epilogue (warps 0-3 own the 128 TMEM lanes)
-  mbar_wait(acc_full, 0);
-  tc_fence_after();
-  const int m = (warp & 3) * 32 + lane;
-  uint32_t r0[32], r1[32];
-  if (warp < 4) {
-    const uint32_t tbase = tmem + ((uint32_t)(warp * 32) << 16);
-    MSPIPE_TMEM_LD32(tbase, r0);
-    MSPIPE_TMEM_LD32(tbase + 32, r1);
-    tmem_wait_ld();
-    for (int ci = 1; ci < nc; ++ci) {
-      uint32_t t0[32], t1[32];
-      MSPIPE_TMEM_LD32(tbase + ci * kN, t0);
-      MSPIPE_TMEM_LD32(tbase + ci * kN + 32, t1);
-      tmem_wait_ld();
-#pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        r0[i] = __float_as_uint(__fadd_rn(__uint_as_float(r0[i]), __uint_as_float(t0[i])));
-        r1[i] = __float_as_uint(__fadd_rn(__uint_as_float(r1[i]), __uint_as_float(t1[i])));
-      }
-    }
-    if (S > 1) {
-      const int R = kM / S;
-      const int owner = m / R, lm = m % R;
-      const uint32_t dst =
-          mapa(smem_u32(recv) + (uint32_t)((cluster_rank() * R + lm) * (kN / 4)) * 16u, (uint32_t)owner);
-#pragma unroll
-      for (int c4 = 0; c4 < 8; ++c4) {
-        st_dsmem_f4(dst + 16u * (uint32_t)(c4 ^ (lm & 15)), __uint_as_float(r0[4 * c4]),
-                    __uint_as_float(r0[4 * c4 + 1]), __uint_as_float(r0[4 * c4 + 2]),
-                    __uint_as_float(r0[4 * c4 + 3]));
-        st_dsmem_f4(dst + 16u * (uint32_t)((8 + c4) ^ (lm & 15)), __uint_as_float(r1[4 * c4]),
-                    __uint_as_float(r1[4 * c4 + 1]), __uint_as_float(r1[4 * c4 + 2]),
-                    __uint_as_float(r1[4 * c4 + 3]));
-      }
-    }
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 2) {
-    tc_fence_after();
-    tmem_dealloc(tmem, tcols);
-  }
-  const float* bias = sbias;
-  if (S == 1) {
-    const int32_t u = m0 + m;
-    if (warp < 4 && u < U) {
-#pragma unroll
-      for (int q = 0; q < kJ / 4; ++q) {
-        const int32_t j0 = jt * kJ + q * 4;
-        if (j0 >= d.M) break;
-        float pr[4], pz[4], pnx[4], pnh[4];
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const int jj = q * 4 + e;
-          pr[e] = __uint_as_float(r0[jj]) + bias[jj];
-          pz[e] = __uint_as_float(r0[kJ + jj]) + bias[kJ + jj];
-          pnx[e] = __uint_as_float(r1[jj]) + bias[2 * kJ + jj];
-          pnh[e] = __uint_as_float(r1[kJ + jj]) + bias[3 * kJ + jj];
-        }
-        store_h4(a, u, rownode[m], j0, gates4(pr, pz, pnx, pnh, hbuf[m * (kJ / 4) + q], d.cell));
-      }
-    }
-  } else {
-    cluster_sync_all();
-    const int R = kM / S;
-    for (int it = threadIdx.x; it < R * (kJ / 4); it += blockDim.x) {
-      const int lm = it / (kJ / 4), q = it % (kJ / 4);
-      const int mm = rb + lm;
-      const int32_t u = m0 + mm;
-      const int32_t j0 = jt * kJ + q * 4;
-      if (u >= U || j0 >= d.M) continue;
-      float4 acc[4];
-#pragma unroll
-      for (int g = 0; g < 4; ++g) acc[g] = recv[(0 * R + lm) * (kN / 4) + ((g * (kJ / 4) + q) ^ (lm & 15))];
-      for (int sr = 1; sr < S; ++sr)
-#pragma unroll
-        for (int g = 0; g < 4; ++g) {
-          const float4 v = recv[(sr * R + lm) * (kN / 4) + ((g * (kJ / 4) + q) ^ (lm & 15))];
-          acc[g].x += v.x;
-          acc[g].y += v.y;
-          acc[g].z += v.z;
-          acc[g].w += v.w;
-        }
-      float pr[4], pz[4], pnx[4], pnh[4];
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int jj = q * 4 + e;
-        pr[e] = (&acc[0].x)[e] + bias[jj];
-        pz[e] = (&acc[1].x)[e] + bias[kJ + jj];
-        pnx[e] = (&acc[2].x)[e] + bias[2 * kJ + jj];
-        pnh[e] = (&acc[3].x)[e] + bias[3 * kJ + jj];
-      }
-      store_h4(a, u, rownode[mm], j0, gates4(pr, pz, pnx, pnh, hbuf[mm * (kJ / 4) + q], d.cell));
-    }
-  }
-  // commit timestamps (G14: mem_ts = mail_ts = t* of the winner)
-  if (jt == 0 && a.commit_mem)
-    for (int mm = rb + (int)threadIdx.x; mm < re; mm += blockDim.x) {
-      const int32_t u = m0 + mm, node = rownode[mm];
-      if (u < U && node >= 0) {
-        const double t = __ldg(a.ts + (rpair[mm] >> 1));
-        a.commit_mem_ts[node] = t;
-        a.commit_mail_ts[node] = t;
-      }
-    }
-}
-
-cudaError_t launch_gru_fb(const GruDesc& d, const float* wtc, const double* ts, int64_t num_events,
-                          const float* edge_feat, const float* snap_mem, const double* snap_mem_ts,
-                          int64_t snap_step, const int32_t* winner, const int32_t* num_unique, float* out_mem,
-                          const GruCommit& commit, cudaStream_t s) {
-  static bool attr_set = false;
-  const size_t smem = (size_t)tc::kSmemBytes + 2 * tc::kM * 4;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(k_gru_fb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
-  TcArgs a{d, wtc, nullptr, ts, num_events, edge_feat, snap_mem, snap_mem_ts, snap_step, nullptr, winner,
-           num_unique, out_mem, nullptr, nullptr, commit.mail_stride};
-  a.nodes = commit.nodes;
-  a.commit_mem = commit.mem;
-  a.commit_mem_ts = commit.mem_ts;
-  a.commit_mail = commit.mail;
-  a.commit_mail_ts = commit.mail_ts;
-  a.num_nodes = commit.num_nodes;
-  a.save_nodes = commit.save_nodes;
-  a.save_num = commit.save_num;
-  const int64_t max_rows = 2 * num_events;
-  const int64_t mtiles = (max_rows + tc::kM - 1) / tc::kM;
-  const int S = gru_tc_splits(max_rows, d);  // k_gru_fb: one TMEM buffer per chunk
-  return launch_k(k_gru_fb, dim3((unsigned)S, (unsigned)gru_tc_jtiles(d), (unsigned)mtiles), dim3(kFBThreads), smem,
-                  s, (unsigned)S, a);
-}
 
 constexpr int kMaxChunks = 8;  // 8 x 64 TMEM columns = 512 (the whole TMEM of the SM)
 
@@ -1501,19 +1104,11 @@ cudaError_t launch_gru_tc(const GruDesc& d, const float* wtc, float* xbuf, const
   a.tdst = tab_dst;
   const int64_t max_rows = 2 * num_events;
   const int64_t mtiles = (max_rows + tc::kM - 1) / tc::kM;
-  if ((parts & kGruBuild) && !d.bf16 && d.Kpad / tc::kKC <= kRowChunks && env_int("MSPIPE_BUILD_ROWS", 0)) {
-    int64_t blocks = (max_rows * 32 + 255) / 256;  // one warp per row of the 2B bound (rows >= U exit)
-    const int64_t cap = (int64_t)num_sms() * env_int("MSPIPE_BUILD_BPS", 8);
-    if (blocks > cap) blocks = cap;
-    cudaError_t e = launch_k(k_build_rows, dim3((unsigned)blocks), dim3(256), 0, s, 1, a);
-    if (e != cudaSuccess) return e;
-  } else if (parts & kGruBuild) {
+  if (parts & kGruBuild) {
     const int64_t warps = mtiles * (d.Kpad / (d.bf16 ? tc::kKC16 : tc::kKC)) * tc::kM;
     int64_t blocks = (warps * 32 + 255) / 256;
     const int64_t cap = (int64_t)num_sms() * env_int("MSPIPE_BUILD_BPS", 8);
     if (blocks > cap) blocks = cap;
-    static int co = -1;
-    apply_carveout(k_build_x, co);
     cudaError_t e = launch_k(k_build_x, dim3((unsigned)blocks), dim3(256), 0, s, 1, a);
     if (e != cudaSuccess) return e;
   }

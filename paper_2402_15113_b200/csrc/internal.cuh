@@ -30,45 +30,9 @@ inline int num_sms() {
   return n;
 }
 
-// ---- Programmatic Dependent Launch --------------------------------------
-// Every kernel of the library starts with pdl_begin(): it lets the next
-// kernel of the stream be launched at once (its launch latency overlaps this
-// kernel) and then waits until the previous kernel of the stream has
-// completed with its memory visible, before any global memory access.  No-ops
-// when a kernel is launched without the programmatic-serialization attribute.
-__device__ __forceinline__ void pdl_begin() {
-  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
-  asm volatile("griddepcontrol.wait;\n" ::: "memory");
-}
-
-// ---- L2 warm-up --------------------------------------------------------
-// cp.async.bulk.prefetch.L2 of read-only tables a latency-bound kernel is about
-// to probe: the dependent probes (T-CSR rows, state rows) then hit L2 instead
-// of HBM.  Grid-wide: the ranges are cut into 32 KB chunks, one bulk prefetch
-// per (thread, chunk); each range's tail below 16 bytes is skipped.
-struct PfRange {
-  const void* p;
-  int64_t bytes;
-};
-constexpr int kMaxPf = 6;
+// ---- L2 warm-up of a range a later bulk copy will read ------------------
 __device__ __forceinline__ void l2_prefetch(const void* p, uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(p), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void l2_prefetch_ranges(const PfRange* r, int n, int64_t tid, int64_t nthreads) {
-  constexpr int64_t kChunk = 32768;
-  int64_t first = 0;  // global chunk index of range i's first chunk
-  for (int i = 0; i < n; ++i) {
-    const int64_t nb = r[i].bytes & ~int64_t(15);
-    const int64_t chunks = (nb + kChunk - 1) / kChunk;
-    int64_t g = tid;
-    if (g < first) g += (first - g + nthreads - 1) / nthreads * nthreads;
-    for (; g < first + chunks; g += nthreads) {
-      const int64_t off = (g - first) * kChunk;
-      const int64_t len = nb - off < kChunk ? nb - off : kChunk;
-      l2_prefetch(static_cast<const char*>(r[i].p) + off, (uint32_t)len);
-    }
-    first += chunks;
-  }
 }
 
 // Time encoding cos(x), x = fmaf(omega, dt, phi) (G2, G22).  With raw Δt the
@@ -83,20 +47,9 @@ __device__ __forceinline__ float time_cos(float x) {
   return cosf((float)r);
 }
 
-bool pdl_enabled();  // env MSPIPE_PDL=1 enables (A/B experiments)
 // integer knob from the environment (experiments only; defaults are the tuned values)
 int env_int(const char* name, int def);
-// shared-memory carveout preference of a kernel (percent; env MSPIPE_CARVEOUT,
-// unset = the driver's choice), applied once per kernel
-template <typename F>
-inline void apply_carveout(F* kernel, int& applied) {
-  const int c = env_int("MSPIPE_CARVEOUT", -1);
-  if (c == applied) return;
-  applied = c;
-  (void)cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, c);
-}
-
-// cudaLaunchKernelEx with the PDL attribute (+ an optional (cx,1,1) cluster).
+// cudaLaunchKernelEx with an optional (cx,1,1) cluster.
 template <typename... KArgs, typename... Args>
 cudaError_t launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
                      unsigned cluster_x, Args&&... args) {
@@ -105,13 +58,8 @@ cudaError_t launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t sme
   cfg.blockDim = block;
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
-  cudaLaunchAttribute attr[2];
+  cudaLaunchAttribute attr[1];
   unsigned n = 0;
-  if (pdl_enabled()) {
-    attr[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[n].val.programmaticStreamSerializationAllowed = 1;
-    ++n;
-  }
   if (cluster_x > 1) {
     attr[n].id = cudaLaunchAttributeClusterDimension;
     attr[n].val.clusterDim.x = cluster_x;
@@ -311,17 +259,6 @@ struct CatchUp {
 };
 
 // fused A5 inside the prep kernel (mspipe_memory_prep_build)
-struct PrepBuild {
-  GruDesc d;
-  float* xbuf;          // GEMM A-operand images (workspace); nullptr: no build
-  const float* ef;      // [B, He] edge features of the batch
-  double* out_ts;       // [U] commit timestamps
-  float* out_mail;      // [U, mail_stride] mail rows
-  int64_t mail_stride;
-  int32_t* upos;        // [2B] pair -> GEMM row (-1: not a winner), library scratch
-  int32_t* sync;        // [2] publish flag, exit count (self-cleaning), library scratch
-};
-
 // one warp copies row v of every table (4 x 16 B loads in flight per lane)
 __device__ __forceinline__ void catchup_row(const CatchUp& c, int32_t v, int32_t Qm, int32_t Qa, int lane) {
   const float4* om = reinterpret_cast<const float4*>(c.old_mem) + (int64_t)v * Qm;
@@ -380,11 +317,6 @@ void launch_mail_deferred(const int32_t* src, const int32_t* dst, const double* 
                           const int32_t* nodes, const int32_t* winner, const int32_t* num_unique, int64_t max_n,
                           const float* mem, int32_t M, float* mail, double* mail_ts, int64_t mail_stride,
                           int64_t num_nodes, cudaStream_t s);
-// A5 + A6 + A7 in one kernel: the CTA builds its A operand in shared memory (gru_tc.cu, k_gru_fb)
-cudaError_t launch_gru_fb(const GruDesc& d, const float* wtc, const double* ts, int64_t num_events,
-                          const float* edge_feat, const float* snap_mem, const double* snap_mem_ts,
-                          int64_t snap_step, const int32_t* winner, const int32_t* num_unique, float* out_mem,
-                          const GruCommit& commit, cudaStream_t s);
 cudaError_t launch_gru_tc(const GruDesc& d, const float* wtc, float* xbuf, const double* ts, int64_t num_events,
                           const float* edge_feat, const float* snap_mem, const double* snap_mem_ts,
                           int64_t snap_step, const float* snap_h, const int32_t* winner,
@@ -410,8 +342,7 @@ cudaError_t launch_prep(const Tcsr& g, const int32_t* src, const int32_t* dst, c
                         const float* mem, const double* mem_ts, int32_t mem_dim, const float* mail,
                         const double* mail_ts, int64_t mail_stride, float* out_mem, double* out_mem_ts,
                         float* out_mail, double* out_mail_ts, cudaStream_t s, int32_t* stamp = nullptr,
-                        int32_t stamp_iter = 0, const struct CatchUp* cu = nullptr,
-                        const struct PrepBuild* bld = nullptr);
+                        int32_t stamp_iter = 0, const struct CatchUp* cu = nullptr);
 
 }  // namespace mspipe
 
@@ -482,9 +413,6 @@ struct mspipe_memory {
   int32_t* stamps;          // [k+1][num_nodes]
   int64_t* stamp_iter;      // [k+1] host: iteration whose winners ring slot r holds (0 = none)
   int64_t caught_up;        // host: the commit whose catch-up a prep has already enqueued (0 = none)
-  // fused message build (mspipe_memory_prep_build): pair -> GEMM row, publish flag
-  int32_t* bld_upos;        // [2 * 8192]
-  int32_t* bld_sync;        // [2], self-cleaning
   // library-owned branches beside the caller's stream, per handle (created at
   // mspipe_memory_create, so never lazily under a stream capture): 0 = the
   // commit's write-back branch, 1 = the prep's mitigation branch

@@ -81,7 +81,6 @@ __global__ void __launch_bounds__(256, 4) k_fetch_gather(
     const double* __restrict__ mail_ts, int32_t Qa, float4* __restrict__ out_mem,
     double* __restrict__ out_mem_ts, float4* __restrict__ out_mail,
     double* __restrict__ out_mail_ts) {
-  pdl_begin();
   const int lane = threadIdx.x & 31;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t base = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * kFetchRows; base < n;
@@ -149,7 +148,6 @@ __global__ void __launch_bounds__(32 * kMitWarps) k_mitigate(
     const double* __restrict__ mem_ts, int32_t M, float lambda, double gamma, int32_t n_sim,
     int32_t F, float* __restrict__ out_h, int32_t* __restrict__ out_omega,
     uint8_t* __restrict__ out_elig) {
-  pdl_begin();
   __shared__ MitWarpSmem sm_all[kMitWarps];
   const int lane = threadIdx.x & 31;
   MitWarpSmem& sm = sm_all[threadIdx.x >> 5];
@@ -290,7 +288,6 @@ __global__ void __launch_bounds__(kDedupThreads) k_dedup(
     int32_t* __restrict__ gscratch, int64_t N, int32_t* __restrict__ out_nodes,
     int32_t* __restrict__ out_winner, int32_t* __restrict__ out_num, int32_t* __restrict__ stamp,
     int32_t stamp_iter) {
-  pdl_begin();
   extern __shared__ int32_t sscratch[];
   block_dedup<kDedupThreads, kSmem>(src, dst, B, gscratch, sscratch, N, out_nodes, out_winner, out_num);
   if (stamp) {  // double-buffered state: stamp[winner node] = iteration (as k_prep's dedup block)
@@ -330,7 +327,6 @@ __global__ void __launch_bounds__(256, 4) k_writeback(
     const float4* __restrict__ new_mail, int32_t Qm, int32_t Qa, float4* __restrict__ mem,
     double* __restrict__ mem_ts, float4* __restrict__ mail, double* __restrict__ mail_ts,
     int64_t N) {
-  pdl_begin();
   const int64_t U = min64((int64_t)__ldg(num), max_n);
   const int lane = threadIdx.x & 31;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -376,7 +372,6 @@ __global__ void __launch_bounds__(256) k_catchup(const int32_t* __restrict__ pre
                                                  const int32_t* __restrict__ cur_nodes,
                                                  const int32_t* __restrict__ cur_num, int32_t* __restrict__ save_nodes,
                                                  int32_t* __restrict__ save_num) {
-  pdl_begin();
   const int lane = threadIdx.x & 31;
   const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
@@ -415,7 +410,6 @@ __global__ void __launch_bounds__(256) k_rows_to_host(const int32_t* __restrict_
                                                       const uint4* __restrict__ a, uint4* host_a, int64_t a_row_bytes,
                                                       const uint4* __restrict__ b, uint4* host_b,
                                                       int64_t b_row_bytes) {
-  pdl_begin();
   const int32_t n = __ldg(num);
   // whole 16-byte words covering the first n rows (the host buffers hold max rows)
   const int64_t na = ((int64_t)n * a_row_bytes + 15) / 16, nt = na + ((int64_t)n * b_row_bytes + 15) / 16;

@@ -12,7 +12,6 @@
 // write-back(i-1-k) and write-back(i-k) (Eq. 2).
 #include "dedup.cuh"
 #include "internal.cuh"
-#include "tc_layout.cuh"
 
 namespace mspipe {
 
@@ -57,20 +56,8 @@ struct PrepArgs {
   int32_t stamp_iter;
   CatchUp cu;      // optional (cu.stamp != nullptr): the next commit's catch-up rows
   int32_t Qcu;     // float4 per mail row of the state tables (catch-up)
-  PrepBuild bld;   // optional (bld.xbuf != nullptr): fused A5 message build
-  int32_t dedup;   // 1: block 0 deduplicates (A2); 0: no dedup block (done by mspipe_memory_winners)
-  PfRange pf[kMaxPf];  // tables warmed into L2 at entry (T-CSR, state rows)
-  int32_t npf;
+  int32_t dedup;   // 1: block 0 deduplicates (A2); 0: no dedup block
 };
-
-__device__ __forceinline__ int32_t ld_acquire(const int32_t* p) {
-  int32_t v;
-  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release(int32_t* p, int32_t v) {
-  asm volatile("st.release.gpu.global.b32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
-}
 
 // copy `nrows` table rows (ids held by lanes 0..nrows-1, -1 = zero row) of Q
 // float4 each into dst rows base..base+nrows-1; kU loads in flight per lane.
@@ -124,78 +111,20 @@ __device__ __forceinline__ void pphase(int i) {
 #define PPHASE(i)
 #endif
 
-// the fused build's flag is self-cleaning: the last block to leave resets it
-// (every block has passed its wait by then), so replays start from 0
-__device__ __forceinline__ void prep_exit(const PrepArgs& a) {
-  if (!a.bld.xbuf) return;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    const int32_t prev = atomicAdd(a.bld.sync + 1, 1);
-    if (prev == (int32_t)gridDim.x - 1) {
-      a.bld.sync[0] = 0;
-      a.bld.sync[1] = 0;
-      __threadfence();
-    }
-  }
-}
-
-// A5, GEMM row u, K chunk c (one warp, lane = column): the k_build_x work item
-__device__ __forceinline__ void build_chunk(const PrepArgs& a, int32_t u, int32_t c, int lane) {
-  const PrepBuild& b = a.bld;
-  const GruDesc& d = b.d;
-  const int32_t p = a.out_winner[u];  // written by block 0 in this launch: plain load
-  const int64_t ev = p >> 1;
-  const int role = p & 1;
-  const int32_t k = c * tc::kKC + lane;
-  float v = 0.f;
-  if (k < d.M || (k >= d.Dx && k < d.K) || (k >= d.Dm && k < d.Dx)) {
-    const int32_t node = role ? __ldg(a.dst + ev) : __ldg(a.src + ev);
-    const float* sw = reinterpret_cast<const float*>(a.mem) + (int64_t)node * d.M;
-    if (k < d.M) v = __ldg(sw + k);
-    else if (k >= d.Dx) v = __ldg(sw + (k - d.Dx));
-    else v = time_cos(fmaf(__ldg(d.time_w + (k - d.Dm)), (float)(__ldg(a.ts + ev) - __ldg(a.mem_ts + node)),
-                           __ldg(d.time_b + (k - d.Dm))));
-  } else if (k < 2 * d.M) {
-    const int32_t other = role ? __ldg(a.src + ev) : __ldg(a.dst + ev);
-    v = __ldg(reinterpret_cast<const float*>(a.mem) + (int64_t)other * d.M + (k - d.M));
-  } else if (k < d.Dm) {
-    v = __ldg(b.ef + ev * d.He + (k - 2 * d.M));
-  }
-  if (k < b.mail_stride) b.out_mail[(int64_t)u * b.mail_stride + k] = k < d.Dm ? v : 0.f;
-  if (c == 0 && lane == 0) b.out_ts[u] = __ldg(a.ts + ev);
-  tc::store_a(b.xbuf, d.Kpad / tc::kKC, u, k, v);
-}
-
 template <bool kSmem>
 __global__ void __launch_bounds__(kPrepThreads, MSPIPE_PREP_MINB) k_prep(PrepArgs a) {
   extern __shared__ int32_t sscratch[];
-  pdl_begin();
   if (threadIdx.x == 0) PPHASE(0);
-  // chunk g to thread g / gridDim.x of block g % gridDim.x: spread over the SMs' bulk-copy units
-  if (a.npf) l2_prefetch_ranges(a.pf, a.npf, (int64_t)threadIdx.x * gridDim.x + blockIdx.x,
-                                (int64_t)gridDim.x * blockDim.x);
   if (a.dedup && blockIdx.x == 0) {
     block_dedup<kPrepThreads, kSmem>(a.src, a.dst, a.B, a.gscratch, sscratch, a.g.num_nodes, a.out_nodes,
                                      a.out_winner, a.out_num);
     if (threadIdx.x == 0) PPHASE(2);
-    if (a.stamp || a.bld.xbuf) {
+    if (a.stamp) {
       __syncthreads();  // out_nodes / out_winner / out_num written by this block
       const int32_t U = *a.out_num;
-      if (a.stamp)
-        for (int32_t u = threadIdx.x; u < U; u += kPrepThreads) a.stamp[a.out_nodes[u]] = a.stamp_iter;
-      if (a.bld.xbuf) {  // pair -> GEMM row, then publish to the build warps
-        for (int64_t p = threadIdx.x; p < 2 * a.B; p += kPrepThreads) a.bld.upos[p] = -1;
-        __syncthreads();
-        for (int32_t u = threadIdx.x; u < U; u += kPrepThreads) a.bld.upos[a.out_winner[u]] = u;
-        __threadfence();
-        __syncthreads();
-        if (threadIdx.x == 0) st_release(a.bld.sync, 1);
-      }
+      for (int32_t u = threadIdx.x; u < U; u += kPrepThreads) a.stamp[a.out_nodes[u]] = a.stamp_iter;
     }
     if (threadIdx.x == 0) PPHASE(1);
-    prep_exit(a);
-    if (threadIdx.x == 0) PPHASE(4);
     return;
   }
   const int lane = threadIdx.x & 31;
@@ -244,19 +173,6 @@ __global__ void __launch_bounds__(kPrepThreads, MSPIPE_PREP_MINB) k_prep(PrepArg
       if (__ldg(a.cu.stamp + v) != a.cu.iter) catchup_row(a.cu, v, a.Qm, a.Qcu, lane);
     }
   }
-  if (a.bld.xbuf) {
-    // fused A5 once block 0 has published the winners: one warp per (GEMM row,
-    // 32-wide K chunk), every warp of the grid, as k_build_x does
-    if (lane == 0) PPHASE(5);
-    while (ld_acquire(a.bld.sync) == 0) __nanosleep(32);
-    if (lane == 0) PPHASE(2);
-    const int32_t U = *a.out_num;
-    const int32_t nchunks = a.bld.d.Kpad / tc::kKC;
-    for (int64_t it = wid; it < (int64_t)U * nchunks; it += nwarps)
-      build_chunk(a, (int32_t)(it / nchunks), (int32_t)(it % nchunks), lane);
-    if (lane == 0) PPHASE(3);
-  }
-  prep_exit(a);
   if (threadIdx.x == 0) PPHASE(4);
 }
 
@@ -267,34 +183,18 @@ cudaError_t launch_prep(const Tcsr& g, const int32_t* src, const int32_t* dst, c
                         const float* mem, const double* mem_ts, int32_t mem_dim, const float* mail,
                         const double* mail_ts, int64_t mail_stride, float* out_mem, double* out_mem_ts,
                         float* out_mail, double* out_mail_ts, cudaStream_t s, int32_t* stamp,
-                        int32_t stamp_iter, const CatchUp* cu, const PrepBuild* bld) {
+                        int32_t stamp_iter, const CatchUp* cu) {
   PrepArgs a{g, src, dst, neg, ts, num_events, fanout, out_nbr, out_eid, out_ts, out_dt, out_cnt, out_sub,
              scratch, out_nodes, out_winner, out_num, (const float4*)mem, mem_ts, mem_dim / 4,
              (const float4*)mail, mail_ts, out_mail ? (int32_t)(mail_stride / 4) : 0, (float4*)out_mem, out_mem_ts,
              (float4*)out_mail, out_mail ? out_mail_ts : nullptr, stamp, stamp_iter, CatchUp{},
              (int32_t)(mail_stride / 4)};
   if (cu) a.cu = *cu;
-  if (bld) a.bld = *bld;
   a.dedup = out_num != nullptr;
-  // L2 warm-up of the tables the root warps probe, each if <= MSPIPE_PF_CAP_MB.  Off by
-  // default: measured slower (wiki 24.8 -> 26.6 us, GDELT 63.7 -> 69.8 us per step)
-  const int64_t cap_b = (int64_t)env_int("MSPIPE_PF_CAP_MB", 0) << 20;
-  auto pf = [&](const void* p, int64_t bytes) {
-    if (p && bytes > 0 && bytes <= cap_b && a.npf < kMaxPf) a.pf[a.npf++] = PfRange{p, bytes};
-  };
-  pf(g.indptr, (g.num_nodes + 1) * (int64_t)sizeof(int64_t));
-  pf(g.ts, g.nnz * (int64_t)sizeof(double));
-  pf(g.nbr, g.nnz * (int64_t)sizeof(int32_t));
-  pf(g.eid, g.nnz * (int64_t)sizeof(int32_t));
-  pf(mem_ts, g.num_nodes * (int64_t)sizeof(double));
-  pf(mem, g.num_nodes * (int64_t)mem_dim * (int64_t)sizeof(float));
   int64_t blocks = (3 * num_events + kPrepWarps - 1) / kPrepWarps;
   // one wave of the two resident blocks per SM; the root warps grid-stride
   const int64_t cap = (int64_t)num_sms() * env_int("MSPIPE_PREP_BPS", 2);
   if (blocks > cap) blocks = cap;
-  static int co0 = -1, co1 = -1;
-  apply_carveout(k_prep<false>, co0);
-  apply_carveout(k_prep<true>, co1);
   if (!a.dedup) return launch_k(k_prep<false>, dim3((unsigned)blocks), dim3(kPrepThreads), 0, s, 1, a);
   blocks += 1;  // block 0: dedup
   if (g.num_nodes <= kDedupSmemNodes && env_int("MSPIPE_PREP_SMEM", 1)) {

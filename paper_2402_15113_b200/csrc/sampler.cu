@@ -21,7 +21,6 @@ __global__ void __launch_bounds__(256) k_sample_recent(
     int32_t F, int32_t* __restrict__ out_nbr, int32_t* __restrict__ out_eid,
     double* __restrict__ out_ts, float* __restrict__ out_dt, int32_t* __restrict__ out_cnt,
     int32_t* __restrict__ out_sub) {
-  pdl_begin();
   const int lane = threadIdx.x & 31;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < R; r += nwarps) {

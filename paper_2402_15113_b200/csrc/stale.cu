@@ -20,7 +20,6 @@ __global__ void __launch_bounds__(kStaleThreads) k_stale_hist(Tcsr g, const int3
                                                               int64_t B, int32_t max_d,
                                                               unsigned long long* __restrict__ hist) {
   extern __shared__ unsigned long long sh[];  // [max_d + 2]
-  pdl_begin();
   for (int q = threadIdx.x; q < max_d + 2; q += blockDim.x) sh[q] = 0ull;
   __syncthreads();
   const int64_t P = 2 * E;
@@ -91,7 +90,6 @@ __global__ void __launch_bounds__(kErrThreads) k_staleness_error(const int32_t* 
                                                                  const float* __restrict__ xb, int64_t stride_b,
                                                                  int32_t M, double* __restrict__ out) {
   __shared__ double part[kErrThreads];
-  pdl_begin();
   const int32_t U = *num;
   double acc = 0.0;
   for (int64_t q = threadIdx.x; q < (int64_t)U * M; q += kErrThreads) {

@@ -51,23 +51,6 @@ class StageConfig:
     mailbox: str = "immediate"  # row F3: "immediate" (G14) | "deferred" (TGL's TGN; needs fetch_mail)
     features: bool = False     # row F2: fetch node / edge features of the sampled subgraphs (bind_features)
     node_dim: int = 0          # |d_v| (GDELT 413); rows padded to a multiple of 4 floats on the device
-    # fused 3xTF32 path without mitigation: the GEMM kernel builds its own operand
-    # (mspipe_gru_build_apply_commit).  Off by default: measured 73 vs 25 us per wiki
-    # step — 6 builder warps per SM cannot keep enough loads in flight to gather the
-    # operand (k_build_x spreads the same gather over ~10^4 warps).  env MSPIPE_GEMM_BUILD=1: A/B
-    gemm_build: bool = dataclasses.field(default_factory=lambda: os.environ.get("MSPIPE_GEMM_BUILD", "0") == "1")
-    # fused path without mitigation: message build inside the prep kernel (mspipe_memory_prep_build).
-    # Off by default: measured slower on the wiki step (30.7 vs 26.0 us; the build waits for the
-    # single dedup block and the longer prep kernel contends with the GEMM).  env MSPIPE_PREP_BUILD=1: A/B
-    prep_build: bool = dataclasses.field(default_factory=lambda: os.environ.get("MSPIPE_PREP_BUILD", "0") == "1")
-    # fused path without mitigation: the message build reads the state tables of the fetched
-    # version directly (mspipe_message_build_tables) on a third stream, right after the dedup
-    # (mspipe_memory_winners), concurrently with the sampler + gather of the same prep, so the
-    # build no longer waits for the gather.  Off by default: measured slower on the wiki
-    # step (28.9 vs 25.2 us; the one-CTA dedup kernel, 6.8 us cold, then heads the build's
-    # chain, and four concurrent kernels contend for the SMs).  env MSPIPE_DIRECT_BUILD=1: A/B
-    direct_build: bool = dataclasses.field(
-        default_factory=lambda: os.environ.get("MSPIPE_DIRECT_BUILD", "0") == "1")
 
     def use_fused(self) -> bool:
         ok = self.precision in (_C.FP32_3XTF32, _C.BF16) and self.fanout <= 31 and self.batch <= 8192
@@ -218,13 +201,8 @@ class MemoryStage(_TimedOps):
                                 mailbox=_C.MAILBOX_DEFERRED if self.deferred else _C.MAILBOX_IMMEDIATE)
         self.upd = _C.alloc_update(cfg.batch, cfg.mem_dim, self.memory.mail_stride, self.device)
         self.fused = cfg.use_fused()
-        self.gemm_build = (self.fused and cfg.gemm_build and not cfg.mitigation and not self.deferred
-                           and cfg.precision == _C.FP32_3XTF32 and not cfg.prep_build)
-        self.direct = (self.fused and cfg.direct_build and not cfg.mitigation and not self.deferred
-                       and not cfg.prep_build and not self.gemm_build)
-        self.bstream = None
         self._dbg_one = torch.zeros(1, device=self.device) if _DEBUG_ONLY else None  # timing diagnostics
-        if self.deferred and not (self.fused and cfg.fetch_mail and not cfg.prep_build):
+        if self.deferred and not (self.fused and cfg.fetch_mail):
             raise ValueError("mailbox='deferred' runs on the fused tensor-core path with fetch_mail=True")
         self.ws_bytes = _C.gru_workspace_size(self.gru, cfg.batch) if self.fused else 0
         self.staged = False
@@ -413,24 +391,6 @@ class MemoryStage(_TimedOps):
         """mspipe_memory_prep (A1+A2+A3[+A4], one launch) then mspipe_message_build (A5) of batch i."""
         cfg = self.cfg
         m = 3 * n * (cfg.fanout + 1)
-        if not cfg.mitigation and cfg.prep_build:
-            # one launch: A1 + A2 + A3 + the A5 message build (mspipe_memory_prep_build)
-            self._ev("prep")
-            sl.version = _C.memory_prep_build(self.memory, self.tcsr, i, x["src"], x["dst"], x["neg"], x["ts"],
-                                              cfg.fanout, samp, sl.dd, sl.mem[:m], sl.mem_ts[:m],
-                                              sl.mail[:m] if sl.mail is not None else None,
-                                              sl.mail_ts[:m] if sl.mail_ts is not None else None, self.gru,
-                                              x["ef"], sl.uts[: 2 * n], sl.umail[: 2 * n], sl.ws)
-            self._ev("prep_end")
-            self._features(sl, samp)
-            self.versions[i] = sl.version
-            if not self.memory.double_buffer:
-                self._fetched = torch.cuda.Event()  # the state tables have been read for batch i
-                self._fetched.record()
-            return
-        if self.direct:
-            self._prep_direct(i, sl, x, n, samp, m)
-            return
         self._ev("prep")
         sl.version = _C.memory_prep(self.memory, self.tcsr, i, x["src"], x["dst"], x["neg"], x["ts"], cfg.fanout,
                                     samp, sl.dd, sl.mem[:m], sl.mem_ts[:m],
@@ -442,8 +402,6 @@ class MemoryStage(_TimedOps):
         if not self.memory.double_buffer:
             self._fetched = torch.cuda.Event()  # the state tables have been read for batch i
             self._fetched.record()
-        if self.gemm_build:  # the commit's GEMM kernel builds the message itself
-            return
         self._ev("build")
         if self.deferred:  # row F3: the message is the stored mail of the snapshot
             _C.message_build_deferred(self.gru, x["ts"], sl.mem, sl.mem_ts, sl.mail, cfg.fanout + 1,
@@ -453,39 +411,6 @@ class MemoryStage(_TimedOps):
                              sl.dd["num"], sl.uts[: 2 * n], sl.umail[: 2 * n], sl.ws,
                              snap_h=sl.h[: 2 * n] if sl.h is not None else None)
         self._ev("build_end")
-
-    def _prep_direct(self, i, sl, x, n, samp, m):
-        """Three launches on two streams: mspipe_memory_winners (A2) then
-        mspipe_message_build_tables (A5, from the tables of the fetched
-        version) on a build stream, while mspipe_memory_prep without its dedup
-        block (A1 + A3) samples and gathers; the build stream joins at the end."""
-        cfg = self.cfg
-        cur = torch.cuda.current_stream()
-        if self.bstream is None or self.bstream.device != cur.device:
-            self.bstream = torch.cuda.Stream(device=cur.device, priority=int(os.environ.get("MSPIPE_BUILD_PRIO", "0")))
-        self.bstream.wait_stream(cur)
-        with torch.cuda.stream(self.bstream):
-            self._ev("dedup")
-            _C.memory_winners(self.memory, i, x["src"], x["dst"], sl.dd)
-            self._ev("dedup_end")
-            self._ev("build")
-            vb = _C.message_build_tables(self.gru, self.memory, i, x["src"], x["dst"], x["ts"], x["ef"],
-                                         sl.dd["winner"][: 2 * n], sl.dd["num"], sl.uts[: 2 * n], sl.umail[: 2 * n],
-                                         sl.ws)
-            self._ev("build_end")
-        self._ev("prep")
-        sl.version = _C.memory_prep(self.memory, self.tcsr, i, x["src"], x["dst"], x["neg"], x["ts"], cfg.fanout,
-                                    samp, None, sl.mem[:m], sl.mem_ts[:m],
-                                    sl.mail[:m] if sl.mail is not None else None,
-                                    sl.mail_ts[:m] if sl.mail_ts is not None else None, None)
-        self._ev("prep_end")
-        assert vb == sl.version, (vb, sl.version)
-        self._features(sl, samp)
-        cur.wait_stream(self.bstream)
-        self.versions[i] = sl.version
-        if not self.memory.double_buffer:
-            self._fetched = torch.cuda.Event()  # the state tables have been read for batch i
-            self._fetched.record()
 
     def _upd(self, i):
         n = self.inputs(i)["src"].numel()
@@ -505,10 +430,6 @@ class MemoryStage(_TimedOps):
         self._ev("update")
         if self.fused:
             upd = self._upd(i)
-            if self.gemm_build:  # the prep left the build to the commit kernel: build here for the plain apply
-                _C.message_build(self.gru, x["ts"], x["ef"], sl.mem, sl.mem_ts, cfg.fanout + 1,
-                                 sl.dd["winner"][: 2 * n], sl.dd["num"], sl.uts[: 2 * n], sl.umail[: 2 * n], sl.ws)
-                upd.update(ts=sl.uts[: 2 * n], mail=sl.umail[: 2 * n])
             _C.gru_apply(self.gru, n, sl.mem, cfg.fanout + 1, upd["winner"], upd["num"], upd["mem"], sl.ws,
                          snap_h=sl.h[: 2 * n] if sl.h is not None else None)
         else:
@@ -539,25 +460,19 @@ class MemoryStage(_TimedOps):
         n = self.inputs(i)["src"].numel()
         upd = self._upd(i)
         self._ev("update")
-        if self.gemm_build:
-            x = self.inputs(i)
-            _C.gru_build_apply_commit(self.gru, self.memory, i, x["ts"], x["ef"], sl.mem, sl.mem_ts, cfg.fanout + 1,
-                                      upd)
-        else:
-            # direct build: h = S.mem[w] is the first M floats of the staged mail row (G14).
-            # e2e: the GEMM also writes the result record's winner ids and U (no copies after it)
-            rec = {}
-            if self.staged:
-                o = self.out_ring[i % self._nout]
-                rec = dict(out_nodes=o[16:16 + 4 * 2 * n].view(torch.int32), out_num=o[:4].view(torch.int32))
-            _C.gru_apply_commit(self.gru, self.memory, i, n, None if self.direct else sl.mem, cfg.fanout + 1, upd,
-                                sl.ws, snap_h=sl.h[: 2 * n] if sl.h is not None else None, **rec)
+        # e2e: the GEMM also writes the result record's winner ids and U (no copies after it)
+        rec = {}
+        if self.staged:
+            o = self.out_ring[i % self._nout]
+            rec = dict(out_nodes=o[16:16 + 4 * 2 * n].view(torch.int32), out_num=o[:4].view(torch.int32))
+        _C.gru_apply_commit(self.gru, self.memory, i, n, sl.mem, cfg.fanout + 1, upd, sl.ws,
+                            snap_h=sl.h[: 2 * n] if sl.h is not None else None, **rec)
         if self.deferred:  # row F3: new mails from the committed memories of both endpoints
             x = self.inputs(i)
             _C.memory_mail_deferred(self.memory, i, x["src"], x["dst"], x["ts"], x["ef"], upd["nodes"], upd["winner"],
                                     upd["num"])
         self._ev("update_end")
-        if self.staged and not self.gemm_build:
+        if self.staged:
             self._pending_out = i  # the GEMM filled the result record
         else:
             self._stash_result(i, upd)

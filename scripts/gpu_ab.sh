@@ -1,6 +1,6 @@
 #!/bin/bash
 # A/B of one knob on the captured step (exp_overlap.py), then quick tests + bench.
-# usage: KNOBS="MSPIPE_DIRECT_BUILD=0,1" CONFIGS="wiki gdelt" bash scripts/gpu_ab.sh
+# usage: KNOBS="MSPIPE_SPLIT_COMMIT=0,1" CONFIGS="wiki gdelt" bash scripts/gpu_ab.sh
 cd "$GRAFT_REPO_ROOT" || exit 1
 mkdir -p gpurun_out
 for c in ${CONFIGS:-wiki}; do

@@ -596,100 +596,6 @@ def test_stream_with_plan_equals_oracle(dev, fused):
     assert rel.max() <= 1e-4
 
 
-@pytest.mark.parametrize("k", [0, 1, 2])
-def test_prep_build_equals_prep_then_build(dev, k):
-    """mspipe_memory_prep_build (message build inside the prep kernel) leaves the
-    same GEMM operand images, commit rows and final state as mspipe_memory_prep +
-    mspipe_message_build, bit for bit."""
-    w = make_workload("lastfm", seed=8, num_events=24_000)
-    cfg = w["cfg"]
-    res = []
-    for pb in (False, True):
-        sc = StageConfig(cfg.num_nodes, cfg.mem_dim, cfg.edge_dim, cfg.time_dim, cfg.fanout, cfg.batch, k,
-                         fetch_mail=True, prep_build=pb, direct_build=False)
-        g = build_tcsr(cfg.num_nodes, w["src"], w["dst"], w["ts"], dev)
-        st = MemoryStage(sc, w["params"], g, dev)
-        assert st.fused
-        t = {kk: _t(w[kk], dev) for kk in ("src", "dst", "ts", "neg", "ef")}
-        st.bind_resident(t["src"], t["dst"], t["ts"], t["neg"], t["ef"])
-        ops = st.step_ops()
-        for o in ops[:-1]:
-            st.run_ops(o)
-        torch.cuda.synchronize()
-        last = max(i for o, i in ops[-1] if o == "commit")
-        sl = st._slot(last)
-        U = int(sl.dd["num"].item())
-        nch = -(-(2 * cfg.mem_dim + cfg.edge_dim + cfg.time_dim + cfg.mem_dim) // 32)
-        mt = -(-U // 128)
-        ws = sl.ws.view(torch.float32)[: mt * nch * 2 * 128 * 32].reshape(-1, 2, 128, 32)  # [block][hi|lo][row][k]
-        ws_rows = ws.cpu().numpy()
-        extra = (sl.uts[:U].cpu().numpy(), sl.umail[:U].cpu().numpy())
-        st.run_ops(ops[-1])
-        torch.cuda.synchronize()
-        _C.check()
-        res.append((ws_rows, U, extra, st.memory.mem.cpu().numpy(), st.memory.mem_ts.cpu().numpy()))
-    (wa, ua, ea, ma, ta), (wb, ub, eb, mb, tb) = res
-    assert ua == ub
-    assert np.array_equal(ea[0], eb[0]) and np.array_equal(ea[1], eb[1])
-    # A images: only rows < U are defined by the build (padding rows are don't-care)
-    for blk in range(wa.shape[0]):
-        mt_i = blk // nch
-        rows = max(0, min(128, ua - 128 * mt_i))
-        assert np.array_equal(wa[blk, :, :rows], wb[blk, :, :rows]), blk
-    assert np.array_equal(ma, mb) and np.array_equal(ta, tb)
-
-
-# ------------------------------------------------------------------ row F2
-@pytest.mark.parametrize("name,k,schedule,E,prec", [("tiny", 0, "exact", 6_000, _C.FP32_3XTF32),
-                                                    ("lastfm", 1, "exact", 24_000, _C.FP32_3XTF32),
-                                                    ("wiki", 2, "grouped", 24_000, _C.FP32_3XTF32),
-                                                    ("wiki", 1, "exact", 24_000, _C.BF16)])
-def test_direct_build_equals_snapshot_build(dev, name, k, schedule, E, prec):
-    """mspipe_memory_winners + mspipe_message_build_tables (the build reads the
-    state tables of the fetched version, concurrently with the dedup-less
-    mspipe_memory_prep) leave the same GEMM operand images, commit rows and
-    final state as mspipe_memory_prep + mspipe_message_build from the snapshot
-    rows, bit for bit; and the direct path equals the oracle (versions, mem_ts
-    bit-exact, memory within 1e-4 row-relative; bf16: 2e-2)."""
-    w = make_workload(name, seed=9, num_events=E)
-    cfg = w["cfg"]
-    res = []
-    for direct in (False, True):
-        sc = StageConfig(cfg.num_nodes, cfg.mem_dim, cfg.edge_dim, cfg.time_dim, cfg.fanout, cfg.batch, k,
-                         schedule=schedule, fetch_mail=True, direct_build=direct, precision=prec)
-        g = build_tcsr(cfg.num_nodes, w["src"], w["dst"], w["ts"], dev)
-        st = MemoryStage(sc, w["params"], g, dev)
-        assert st.fused and st.direct == direct
-        t = {kk: _t(w[kk], dev) for kk in ("src", "dst", "ts", "neg", "ef")}
-        st.bind_resident(t["src"], t["dst"], t["ts"], t["neg"], t["ef"])
-        ops = st.step_ops()
-        for o in ops[:-1]:
-            st.run_ops(o)
-        torch.cuda.synchronize()
-        last = max(i for o, i in ops[-1] if o == "commit")
-        sl = st._slot(last)
-        U = int(sl.dd["num"].item())
-        extra = (sl.uts[:U].cpu().numpy(), sl.umail[:U].cpu().numpy(), sl.dd["nodes"][:U].cpu().numpy())
-        st.run_ops(ops[-1])
-        torch.cuda.synchronize()
-        _C.check()
-        res.append((U, extra, st.memory.mem.cpu().numpy(), st.memory.mem_ts.cpu().numpy(),
-                    st.memory.mail.cpu().numpy(), dict(st.versions)))
-    (ua, ea, ma, ta, la, va), (ub, eb, mb, tb, lb, vb) = res
-    assert ua == ub and va == vb
-    # the last batch's staged commit rows (ts, mail), winners, and the final state, bit for bit
-    assert all(np.array_equal(x, y) for x, y in zip(ea, eb))
-    assert np.array_equal(ma, mb) and np.array_equal(ta, tb) and np.array_equal(la, lb)
-    ref, vers = oracle.run_stream(cfg.num_nodes, w["src"], w["dst"], w["ts"], w["ef"], w["params"], cfg.batch, k,
-                                  schedule, fanout=cfg.fanout)
-    assert [vb[i] for i in range(1, len(vers) + 1)] == vers.tolist()
-    assert np.array_equal(tb, ref["mem_ts"])
-    rel = (np.linalg.norm(mb.astype(np.float64) - ref["mem"], axis=1) /
-           np.maximum(np.linalg.norm(ref["mem"], axis=1), 1e-3))
-    print(f"{name} k={k} {schedule} direct build: row-rel max {rel.max():.3g}")
-    assert rel.max() <= (2e-2 if prec == _C.BF16 else 1e-4)
-
-
 @pytest.mark.parametrize("name,E,fused", [("gdelt", 30_000, True), ("gdelt", 30_000, False), ("tiny", None, True)])
 def test_feature_fetch_equals_oracle(dev, name, E, fused):
     """F2 inside the stage (its own stream, forked after the sampler): node-feature
@@ -878,33 +784,6 @@ def test_bench_configuration_matches_oracle(dev, name, E, gru):
 
 
 
-@pytest.mark.parametrize("name,k,E", [("tiny", 0, None), ("wiki", 1, 60_000), ("lastfm", 2, 60_000)])
-def test_gemm_build_path_equals_oracle(dev, name, k, E):
-    """mspipe_gru_build_apply_commit (operand built inside the GEMM kernel, off by
-    default) over whole streams against the oracle."""
-    w = make_workload(name, seed=13, num_events=E)
-    cfg = w["cfg"]
-    sc = StageConfig(cfg.num_nodes, cfg.mem_dim, cfg.edge_dim, cfg.time_dim, cfg.fanout, cfg.batch, k,
-                     fetch_mail=True, gemm_build=True)
-    g = build_tcsr(cfg.num_nodes, w["src"], w["dst"], w["ts"], dev)
-    st = MemoryStage(sc, w["params"], g, dev)
-    assert st.gemm_build
-    t = {kk: _t(w[kk], dev) for kk in ("src", "dst", "ts", "neg", "ef")}
-    st.bind_resident(t["src"], t["dst"], t["ts"], t["neg"], t["ef"])
-    st.run()
-    torch.cuda.synchronize()
-    _C.check()
-    ref, _ = oracle.run_stream(cfg.num_nodes, w["src"], w["dst"], w["ts"], w["ef"], w["params"], cfg.batch, k)
-    assert np.array_equal(st.memory.mem_ts.cpu().numpy(), ref["mem_ts"])
-    assert np.array_equal(st.memory.mail_ts.cpu().numpy(), ref["mail_ts"])
-    gm, om = st.memory.mem.cpu().numpy().astype(np.float64), ref["mem"].astype(np.float64)
-    rel = np.linalg.norm(gm - om, axis=1) / np.maximum(np.linalg.norm(om, axis=1), 1e-3)
-    assert rel.max() <= 1e-4
-    Dm = cfg.mail_dim  # mail = [s_w | s_o | e]: memory values, so within the fp32 tolerance
-    ok, err = _close(st.memory.mail.cpu().numpy()[:, :Dm], ref["mail"], rtol=1e-4, atol=1e-5)
-    assert ok, err
-
-
 # ------------------------------------------------- sizes and degenerate batches
 def _run_stream(dev, w, B, k, schedule="exact", **kw):
     cfg = w["cfg"]
@@ -962,13 +841,13 @@ def test_degenerate_batches(dev):
         _run_stream(dev, w, B, k)
 
 
-@pytest.mark.parametrize("env", [{"MSPIPE_SPLIT_COMMIT": "0"}, {"MSPIPE_BUILD_ROWS": "1"},
+@pytest.mark.parametrize("env", [{"MSPIPE_SPLIT_COMMIT": "0"},
                                  {"MSPIPE_TC_SPLITS": "2"}, {"MSPIPE_TC_BIG_S2": "0"},
                                  {"MSPIPE_PREP_SMEM": "0", "MSPIPE_PREP_BPS": "4"}])
 def test_switch_variants_equal_oracle(dev, env, monkeypatch):
     """The library's experiment switches (read at every launch) keep the oracle's
     results: the GEMM epilogue writing mem_ts / mail itself (no write-back
-    branch), the row-per-warp message build, S = 2 at wiki size (two K chunks
+    branch), S = 2 at wiki size (two K chunks
     per TMEM buffer), S = 4 at GDELT size, the dedup table in global memory."""
     for kk, v in env.items():
         monkeypatch.setenv(kk, v)
