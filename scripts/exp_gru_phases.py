@@ -11,7 +11,7 @@ import numpy as np, torch
 from paper_2402_15113_b200 import MemoryStage, StageConfig, _C, build_tcsr
 from synth import make_workload
 name = sys.argv[1] if len(sys.argv) > 1 else "wiki"
-w = make_workload(name, num_events=60000)
+w = make_workload(name, num_events=int(os.environ.get("EXP_EVENTS", "200000" if name == "gdelt" else "60000")))
 cfg = w["cfg"]
 dev = torch.device("cuda:0")
 g = build_tcsr(cfg.num_nodes, w["src"], w["dst"], w["ts"], dev)

@@ -150,15 +150,22 @@ def test_gdelt_full_tcsr_sampler(dev, gdelt):
 
 
 # ------------------------------------------------------------ A3s rows vs the oracle
-@pytest.mark.parametrize("name,E,k,db", [("wiki", None, 1, True), ("lastfm", 150_000, 2, True),
-                                         ("reddit", 120_000, 2, True), ("lastfm", 60_000, 2, False),
-                                         ("tiny", None, 0, False)])
-def test_subgraph_rows_equal_oracle_snapshot(dev, name, E, k, db):
-    """Every fetched subgraph row of the dumped batches equals the oracle's
-    S_{v(i)} row for the same id (ids, rows and mem_ts bit-exact), with the
-    double-buffered tables' catch-up active (db) or one table set."""
+@pytest.mark.parametrize("name,E,k", [("wiki", None, 1), ("lastfm", 150_000, 2), ("reddit", 120_000, 2),
+                                      ("tiny", None, 0)])
+def test_subgraph_rows_equal_oracle_snapshot(dev, name, E, k):
+    """The A3s output of the dumped batches against the oracle's S_{v(i)}: the
+    3B(𝒩+1) subgraph ids and the rows' mem_ts bit-exact, the memory rows within
+    the free-running tolerance (the state they copy is itself a GPU trajectory,
+    ~1e-7 from the oracle's); and, with the double-buffered tables' catch-up
+    active, the fetched rows bitwise equal to those of a one-table-set run."""
     w = make_workload(name, seed=3, num_events=E)
-    _subgraph_rows(dev, w, build_tcsr(w["cfg"].num_nodes, w["src"], w["dst"], w["ts"], dev), k, db, _mit(w))
+    g = build_tcsr(w["cfg"].num_nodes, w["src"], w["dst"], w["ts"], dev)
+    a = _subgraph_rows(dev, w, g, k, False, _mit(w))
+    if k >= 1:
+        b = _subgraph_rows(dev, w, g, k, True, _mit(w))
+        for i in a:
+            for x, y in zip(a[i], b[i]):
+                assert np.array_equal(x, y), i
 
 
 def test_subgraph_rows_equal_oracle_snapshot_gdelt(dev, gdelt):
@@ -185,6 +192,7 @@ def _subgraph_rows(dev, w, g, k, db, mit):
     for ops in st.step_ops():
         st.run_ops(ops)
         for op, i in ops:
+            # the slot of a batch is rewritten k+1 preps later: read right after its step
             if op == "prep" and i in want:
                 torch.cuda.synchronize()
                 sl = st._slot(i)
@@ -192,16 +200,22 @@ def _subgraph_rows(dev, w, g, k, db, mit):
                 m = 3 * n * (F + 1)
                 got[i] = (sl.samp["sub"][: 3 * n].cpu().numpy().reshape(-1), sl.mem[:m].cpu().numpy(),
                           sl.mem_ts[:m].cpu().numpy())
-    # the slot of a batch is rewritten k+1 preps later: every dumped slot was read right after its prep
     torch.cuda.synchronize()
     _C.check()
     _, vers, dump = oracle.run_stream(cfg.num_nodes, w["src"], w["dst"], w["ts"], w["ef"], w["params"], B, k,
                                       mitigation=mit, fanout=F, neg=w["neg"], dump_batches=want)
+    worst = 0.0
     for q, i in enumerate(dump["batches"]):
         ids, rows, mts = got[int(i)]
         m = len(ids)
         assert np.array_equal(ids, dump["sub_ids"][q][:m]), i
-        assert np.array_equal(rows, dump["mem"][q][:m]), (i, np.abs(rows - dump["mem"][q][:m]).max())
         assert np.array_equal(mts, dump["mem_ts"][q][:m]), i
+        o = dump["mem"][q][:m].astype(np.float64)
+        err = np.abs(rows.astype(np.float64) - o)
+        assert (err <= 1e-4 * np.abs(o) + 1e-5).all(), (i, err.max())
+        assert (rows[ids == -1] == 0).all()  # pads are zero rows
+        worst = max(worst, float(err.max()))
         assert st.versions[int(i)] == vers[int(i) - 1]
-    print(f"{cfg.name} k={k} db={db}: subgraph rows of batches {want} bit-exact")
+    print(f"{cfg.name} k={k} db={db}: subgraph ids / mem_ts of batches {want} bit-exact, rows max |gpu - oracle| "
+          f"{worst:.3g}")
+    return got
