@@ -493,7 +493,7 @@ def run_mspipe(args):
                                      args.features),
            "clocks": clocks}
     if sharded:
-        out["exchange"] = _exchange_report(st, cfg, ws, ms_step)
+        out["exchange"] = _exchange_report(st, W + K, ms_step)
     if args.profile:
         if rank == 0:
             print(json.dumps(out))
@@ -562,17 +562,21 @@ def _tensor_roofline(gru, flops, t_ms, peaks, st, burst=False):
             "peak_source": "148 SMs x 128 FP32 lanes x 2 x 1965 MHz (guide unit counts, max clock)"}
 
 
-def _exchange_report(st, cfg, ws, ms_step):
-    """Row E: bytes each rank sends per global iteration over NCCL (fetch ids +
-    replies, commit records) and the achieved rate against NVLink 5's 900 GB/s
-    per direction."""
+def _exchange_report(st, steps, ms_step):
+    """Row E: bytes this rank stored into peers' windows per global iteration
+    (fetch request ids, reply rows, commit records: the real entries only) over
+    the last block (reset, then `steps` steps), and that rate against NVLink
+    5's 900 GB/s per direction."""
     try:
-        b = st.exchange_bytes_per_iter()
+        ids, rows, recs = st.exchange_bytes()
     except Exception as e:  # noqa: BLE001
         return {"error": str(e)}
-    return {"bytes_per_iter_per_rank": b, "nvlink_gbs": b / (ms_step / 1e3) / 1e9 if ms_step > 0 else None,
-            "nvlink_peak_gbs": 900.0, "note": "bytes over the whole step time (an upper bound on the exchange "
-                                              "time), so the rate is a lower bound on the link rate"}
+    per = (ids + rows + recs) / max(steps, 1)
+    return {"bytes_per_iter_per_rank": per, "fetch_id_bytes": ids / steps, "reply_bytes": rows / steps,
+            "commit_bytes": recs / steps, "nvlink_gbs": per / (ms_step / 1e3) / 1e9 if ms_step > 0 else None,
+            "nvlink_peak_gbs": 900.0,
+            "note": "bytes over the whole step time (an upper bound on the exchange time), so the rate is a lower "
+                    "bound on the link rate; the owner's own rows are stored locally but counted too"}
 
 
 def hbm_probe(dev, cfg, peaks, flush, seed):
@@ -642,10 +646,10 @@ def _launches(steps, timed_batches, mit, fused, sharded=False, features=False):
     """Kernels of this library per timed step.  fused: prep = k_prep + k_build_x
     (+ k_mitigate), commit = k_gru_tc (h' rows) + k_writeback (mem_ts / mail); otherwise prep = sampler +
     dedup + gather (+ mitigation), commit = build + GEMM (or SIMT GRU) + write-back.  Sharded:
-    prep = sampler + dedup + mark + plan + serve + finish, commit = build + GEMM + clear + pack-plan
-    + pack + merge-key + merge-apply (NCCL kernels not counted)."""
+    prep = sampler + dedup + mark + plan + serve + finish, commit = build + GEMM + pack-plan + pack
+    + merge-key + merge-apply (NCCL barrier kernels not counted)."""
     if sharded:
-        per = {"prep": 6, "commit": 7}
+        per = {"prep": 6, "commit": 6}
         return int(sum(per[op] for t in timed_batches for op, _ in steps[t]))
     # fused commit: k_gru_tc (+ the k_writeback branch of mem_ts / mail unless MSPIPE_SPLIT_COMMIT=0)
     split = fused and os.environ.get("MSPIPE_SPLIT_COMMIT", "1") != "0"

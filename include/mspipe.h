@@ -409,22 +409,39 @@ MSPIPE_API mspipe_status mspipe_gru_apply_commit_out(const mspipe_gru* gru, mspi
  * the same iterations on its own local batch of each global batch;
  * the T-CSR is replicated (sampling and dedup stay local).
  *
- * With an nccl_unique_id at create, mspipe_memory_fetch and
- * mspipe_memory_writeback_keyed are collective (every rank calls them with
- * the same iteration / version, in the same stream order) and run NCCL
- * all-to-alls on `stream`.  Without one (NULL) the handle is an in-process
- * rank: the caller drives the phases below for all ranks and moves the
- * buffers with mspipe_shard_loopback (one process, e.g. G virtual ranks on
- * one GPU for testing).  MSPipe-S mitigation is not available for world > 1
- * in this build (MSPIPE_EUNSUPPORTED).
+ * Transport: every rank owns a receive window; the sending phase stores its
+ * data straight into the peer's window (NVLink peer memory), only the real
+ * entries (request ids, reply rows, commit records) plus per-sender counts,
+ * and a barrier separates it from the phase that reads the window.  Windows
+ * are double-buffered by iteration parity.  Bytes stored per kind are
+ * counted on the device (mspipe_shard_sent_bytes).
  *
- * Phases of a fetch: plan -> exchange(FETCH_IDS) -> serve -> exchange(
- * FETCH_ROWS) -> finish.  Phases of a commit: pack -> exchange(COMMIT) ->
- * merge.  The LWW key of a record is key_base + winner pair index, key_base =
- * 2 x (global index of this rank's first event in the iteration), i.e. the
- * global pair index of the single-GPU batch G·B; the owner keeps, per node,
- * the record with the largest key (64-bit atomicMax, then a keyed copy), so
- * the result does not depend on arrival order.
+ * With an nccl_unique_id at create, the ranks are processes (one per GPU):
+ * after create, every rank exports its window (mspipe_shard_window_handle,
+ * a 64-byte CUDA IPC handle), the handles are all-gathered (e.g. through
+ * torch.distributed) and every rank calls mspipe_shard_connect with all of
+ * them.  mspipe_memory_fetch and mspipe_memory_writeback_keyed are then
+ * collective (every rank calls them with the same iteration / version, in
+ * the same stream order); their barriers are one-int NCCL all-reduces on
+ * `stream`, fetches and commits on two communicators (so a fetch on one
+ * stream and a commit on another never order each other).  Without an id
+ * (NULL) the handles are in-process ranks on one device, connected by
+ * mspipe_shard_connect_local: the caller drives the phases below for all
+ * ranks on one stream (the stream orders them; mspipe_shard_exchange and
+ * mspipe_shard_loopback are then no-ops), e.g. G virtual ranks on one GPU for
+ * testing.  The phases fail with MSPIPE_EUNSUPPORTED before a connect.
+ * MSPipe-S mitigation is not available for world > 1 in this build
+ * (MSPIPE_EUNSUPPORTED).
+ *
+ * Phases of a fetch: plan (stores the request ids into the owners' windows)
+ * -> exchange(FETCH_IDS) -> serve (owner stores the reply rows into the
+ * requesters' windows) -> exchange(FETCH_ROWS) -> finish.  Phases of a
+ * commit: pack (stores the records into the owners' windows) ->
+ * exchange(COMMIT) -> merge.  The LWW key of a record is key_base + winner
+ * pair index, key_base = 2 x (global index of this rank's first event in the
+ * iteration), i.e. the global pair index of the single-GPU batch G·B; the
+ * owner keeps, per node, the record with the largest key (64-bit atomicMax,
+ * then a keyed copy), so the result does not depend on arrival order.
  * ------------------------------------------------------------------------- */
 enum { MSPIPE_XCHG_FETCH_IDS = 0, MSPIPE_XCHG_FETCH_ROWS = 1, MSPIPE_XCHG_COMMIT = 2 };
 
@@ -449,7 +466,20 @@ MSPIPE_API mspipe_status mspipe_shard_commit_pack(mspipe_memory* st, int64_t com
                                        const float* new_mem, const double* new_ts,
                                        const float* new_mail, void* stream);
 MSPIPE_API mspipe_status mspipe_shard_commit_merge(mspipe_memory* st, int64_t commit_version, void* stream);
+/* the barrier of a phase (NCCL all-reduce of one int; no-op for in-process ranks) */
 MSPIPE_API mspipe_status mspipe_shard_exchange(mspipe_memory* st, int32_t kind, void* stream);
+/* [host] this rank's receive window as a CUDA IPC handle (out >= 64 bytes) */
+MSPIPE_API mspipe_status mspipe_shard_window_handle(const mspipe_memory* st, void* out, int32_t out_bytes);
+/* [host] open every peer's window: handles = world x handle_bytes (64) host
+ * bytes, rank order, own entry ignored.  Needs a handle created with an NCCL
+ * id; once.  MSPIPE_ECUDA if a window cannot be opened (no peer access). */
+MSPIPE_API mspipe_status mspipe_shard_connect(mspipe_memory* st, const void* handles, int32_t handle_bytes);
+/* [host] connect `world` in-process ranks (same device, created without an id) */
+MSPIPE_API mspipe_status mspipe_shard_connect_local(mspipe_memory* const* ranks, int32_t world);
+/* [host] bytes this rank has stored into windows since create / the last
+ * reset: out[0] fetch request ids (+ counts), out[1] reply rows, out[2] commit
+ * records (+ counts).  Synchronises the device. */
+MSPIPE_API mspipe_status mspipe_shard_sent_bytes(const mspipe_memory* st, int64_t* out);
 MSPIPE_API mspipe_status mspipe_shard_loopback(mspipe_memory* const* ranks, int32_t world, int32_t kind,
                                     void* stream);
 

@@ -37,7 +37,9 @@ EXPORTS = ("mspipe_abi_version", "mspipe_last_error", "mspipe_check", "mspipe_sa
            "mspipe_feature_fetch", "mspipe_updater_create",
            "mspipe_message_build_deferred", "mspipe_memory_mail_deferred",
            "mspipe_util_rows_to_host",
-           "mspipe_gru_apply_commit_out", "mspipe_plan_stale_fractions", "mspipe_staleness_error")
+           "mspipe_gru_apply_commit_out", "mspipe_plan_stale_fractions", "mspipe_staleness_error",
+           "mspipe_shard_window_handle", "mspipe_shard_connect", "mspipe_shard_connect_local",
+           "mspipe_shard_sent_bytes")
 XCHG_FETCH_IDS, XCHG_FETCH_ROWS, XCHG_COMMIT = 0, 1, 2
 
 
@@ -123,6 +125,10 @@ def lib():
         L.mspipe_shard_commit_merge.argtypes = [P, i64, P]
         L.mspipe_shard_exchange.argtypes = [P, i32, P]
         L.mspipe_shard_loopback.argtypes = [P, i32, i32, P]
+        L.mspipe_shard_window_handle.argtypes = [P, P, i32]
+        L.mspipe_shard_connect.argtypes = [P, P, i32]
+        L.mspipe_shard_connect_local.argtypes = [P, i32]
+        L.mspipe_shard_sent_bytes.argtypes = [P, P]
         if L.mspipe_abi_version() != ABI_VERSION:
             raise RuntimeError(f"libmspipe ABI {L.mspipe_abi_version()} != binding {ABI_VERSION}")
         _lib = L
@@ -444,6 +450,35 @@ def shard_exchange(st, kind, stream=None):
     _ck(lib().mspipe_shard_exchange(st.h, int(kind), stream_ptr(stream)), "mspipe_shard_exchange")
 
 
+IPC_HANDLE_BYTES = 64
+
+
+def shard_window_handle(st) -> bytes:
+    """This rank's receive window as a CUDA IPC handle (row E transport)."""
+    buf = C.create_string_buffer(IPC_HANDLE_BYTES)
+    _ck(lib().mspipe_shard_window_handle(st.h, buf, IPC_HANDLE_BYTES), "mspipe_shard_window_handle")
+    return buf.raw
+
+
+def shard_connect(st, handles):
+    """Open every peer's window (handles: one IPC handle per rank, rank order)."""
+    blob = b"".join(handles)
+    _ck(lib().mspipe_shard_connect(st.h, blob, IPC_HANDLE_BYTES), "mspipe_shard_connect")
+
+
+def shard_connect_local(handles):
+    """Connect in-process ranks (one device): their windows are shared directly."""
+    arr = (C.c_void_p * len(handles))(*[h.h.value for h in handles])
+    _ck(lib().mspipe_shard_connect_local(arr, len(handles)), "mspipe_shard_connect_local")
+
+
+def shard_sent_bytes(st):
+    """Bytes this rank stored into windows: (fetch ids, reply rows, commit records)."""
+    out = (C.c_int64 * 3)()
+    _ck(lib().mspipe_shard_sent_bytes(st.h, out), "mspipe_shard_sent_bytes")
+    return tuple(int(x) for x in out)
+
+
 def shard_loopback(handles, kind, stream=None):
     arr = (C.c_void_p * len(handles))(*[h.h.value for h in handles])
     _ck(lib().mspipe_shard_loopback(arr, len(handles), int(kind), stream_ptr(stream)), "mspipe_shard_loopback")
@@ -563,7 +598,7 @@ def gru_apply_commit(gru: GruHandle, st: MemoryHandle, commit_version, num_event
                                               ptr(upd["num"]), ptr(upd["ts"]), ptr(upd.get("mail")),
                                               ptr(upd.get("mem")), ptr(out_nodes), ptr(out_num), ptr(workspace),
                                               workspace.numel() * workspace.element_size(), stream_ptr(stream)),
-            "mspipe_gru_apply_commit_out", "mspipe_plan_stale_fractions", "mspipe_staleness_error")
+            "mspipe_gru_apply_commit_out")
         return
     _ck(lib().mspipe_gru_apply_commit(gru.h, st.h, int(commit_version), int(num_events), ptr(snap_mem),
                                       int(snap_step), ptr(snap_h), ptr(upd["nodes"]), ptr(upd["winner"]),

@@ -205,8 +205,14 @@ constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(kN 
 // kind::f16 instruction descriptor (MSPIPE_BF16): D f32, A/B bf16, K-major, M = 128, N = 64.
 constexpr uint32_t kIdescBf = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kN >> 3) << 17) |
                               ((uint32_t)(kM >> 4) << 24);
-constexpr int kBBlock16 = kN * kKC16 * 2;            // 8 KB
-constexpr int kStageBytes16 = kATile16 + kBBlock16;  // 24 KB
+constexpr int kBTile16 = kN * kKC16 * 2;             // 8 KB
+// bf16 mode splits both operands, x = hi + lo (two bf16), and issues
+// A_lo.B_hi + A_hi.B_lo + A_hi.B_hi (the bf16 analogue of 3xTF32): ~16
+// mantissa bits per operand, so h' lands within the C.6 per-element rule
+// (2e-2|o| + 1e-3) that plain bf16 operands miss by 3-10x
+constexpr int kABlock16 = 2 * kATile16;              // 32 KB: hi | lo
+constexpr int kBBlock16 = 2 * kBTile16;              // 16 KB: hi | lo
+constexpr int kStageBytes16 = kABlock16 + kBBlock16;  // 48 KB
 }  // namespace tc
 
 #ifdef MSPIPE_PHASES
@@ -266,8 +272,11 @@ __global__ void k_gru_pack_bf16(const float* __restrict__ w_ih, const float* __r
     const int32_t c = (int32_t)((t / (tc::kKC16 * tc::kN)) % nchunks);
     const int32_t jt = (int32_t)(t / ((int64_t)tc::kKC16 * tc::kN * nchunks));
     const float v = wval(w_ih, w_hh, d, n / tc::kJ, jt * tc::kJ + n % tc::kJ, c * tc::kKC16 + kk);
-    uint8_t* blk = wtc + ((int64_t)jt * nchunks + c) * (tc::kN * tc::kKC16 * 2);
-    *reinterpret_cast<__nv_bfloat16*>(blk + tc::sw128_off16((uint32_t)n, (uint32_t)kk)) = __float2bfloat16_rn(v);
+    uint8_t* blk = wtc + ((int64_t)jt * nchunks + c) * tc::kBBlock16;
+    const __nv_bfloat16 hi = __float2bfloat16_rn(v);
+    const uint32_t off = tc::sw128_off16((uint32_t)n, (uint32_t)kk);
+    *reinterpret_cast<__nv_bfloat16*>(blk + off) = hi;
+    *reinterpret_cast<__nv_bfloat16*>(blk + tc::kBTile16 + off) = __float2bfloat16_rn(v - __bfloat162float(hi));
   }
 }
 
@@ -308,13 +317,13 @@ __global__ void k_gru_pack_tc(const float* __restrict__ w_ih, const float* __res
 }
 
 size_t gru_tc_packed_floats(const GruDesc& d) {
-  if (d.bf16) return (size_t)gru_tc_jtiles(d) * (d.Kpad / tc::kKC16) * (tc::kN * tc::kKC16 * 2 / 4);
+  if (d.bf16) return (size_t)gru_tc_jtiles(d) * (d.Kpad / tc::kKC16) * (tc::kBBlock16 / 4);
   return (size_t)gru_tc_jtiles(d) * (d.Kpad / tc::kKC) * (tc::kBBlock / 4);
 }
 
 size_t gru_tc_xbuf_floats(const GruDesc& d, int64_t max_events) {
   const int64_t mtiles = (2 * max_events + tc::kM - 1) / tc::kM;
-  if (d.bf16) return (size_t)mtiles * (d.Kpad / tc::kKC16) * (tc::kATile16 / 4);
+  if (d.bf16) return (size_t)mtiles * (d.Kpad / tc::kKC16) * (tc::kABlock16 / 4);
   return (size_t)mtiles * (d.Kpad / tc::kKC) * (tc::kABlock / 4);
 }
 
@@ -456,9 +465,12 @@ __device__ __forceinline__ void build_bf16(const TcArgs& a) {
       }
       if (c == 0 && lane == 0) a.out_ts[u] = __ldg(a.ts + (p >> 1));
     }
-    uint8_t* blk = reinterpret_cast<uint8_t*>(a.xbuf) + ((int64_t)mt * nchunks + c) * tc::kATile16;
-    *reinterpret_cast<__nv_bfloat162*>(blk + tc::sw128_off16((uint32_t)row, (uint32_t)(2 * lane))) =
-        __floats2bfloat162_rn(v0, v1);
+    uint8_t* blk = reinterpret_cast<uint8_t*>(a.xbuf) + ((int64_t)mt * nchunks + c) * tc::kABlock16;
+    const __nv_bfloat162 hi = __floats2bfloat162_rn(v0, v1);
+    const float2 hf = __bfloat1622float2(hi);
+    const uint32_t off = tc::sw128_off16((uint32_t)row, (uint32_t)(2 * lane));
+    *reinterpret_cast<__nv_bfloat162*>(blk + off) = hi;
+    *reinterpret_cast<__nv_bfloat162*>(blk + tc::kATile16 + off) = __floats2bfloat162_rn(v0 - hf.x, v1 - hf.y);
   }
 }
 
@@ -619,7 +631,7 @@ template <bool kBf>
 __global__ void __launch_bounds__(tc::kThreads, 1) k_gru_tc(TcArgs a) {
   using namespace tc;
   constexpr int SB = kBf ? kStageBytes16 : kStageBytes;
-  constexpr int AB = kBf ? kATile16 : kABlock;
+  constexpr int AB = kBf ? kABlock16 : kABlock;
   constexpr int BB = kBf ? kBBlock16 : kBBlock;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -726,12 +738,15 @@ __global__ void __launch_bounds__(tc::kThreads, 1) k_gru_tc(TcArgs a) {
         mbar_wait(&full[s], ph);
         tc_fence_after();
         const uint32_t base = smem_u32(smem + s * SB);
-        if (kBf) {  // 4 MMAs of K = 16 (32 B along K) into the single accumulator
-          const uint64_t da = sw128_desc(base), db = sw128_desc(base + AB);
+        if (kBf) {  // 4 k-steps of K = 16 (32 B along K), 3 split MMAs each, into the single accumulator
+          const uint64_t da_hi = sw128_desc(base), da_lo = sw128_desc(base + kATile16);
+          const uint64_t db_hi = sw128_desc(base + AB), db_lo = sw128_desc(base + AB + kBTile16);
 #pragma unroll
           for (int kk = 0; kk < kKC16 / 16; ++kk) {
             const uint64_t adv = (uint64_t)(kk * 32) >> 4;
-            mma_bf16(tmem, da + adv, db + adv, kIdescBf, (ci | kk) != 0);
+            mma_bf16(tmem, da_lo + adv, db_hi + adv, kIdescBf, (ci | kk) != 0);
+            mma_bf16(tmem, da_hi + adv, db_lo + adv, kIdescBf, 1u);
+            mma_bf16(tmem, da_hi + adv, db_hi + adv, kIdescBf, 1u);
           }
         } else {
           const uint64_t da_hi = sw128_desc(base), da_lo = sw128_desc(base + kATile);

@@ -353,16 +353,17 @@ void shard_fetch_plan(mspipe_memory* st, const int32_t* ids, int64_t n, cudaStre
 void shard_fetch_serve(mspipe_memory* st, bool with_mail, cudaStream_t s);
 void shard_fetch_finish(mspipe_memory* st, const int32_t* ids, int64_t n, float* out_mem, double* out_mem_ts,
                         float* out_mail, double* out_mail_ts, cudaStream_t s);
-void shard_commit_pack(mspipe_memory* st, const int32_t* nodes, const int32_t* winner, const int32_t* num,
-                       int64_t max_n, int64_t key_base, const float* new_mem, const double* new_ts,
-                       const float* new_mail, cudaStream_t s);
-void shard_commit_merge(mspipe_memory* st, cudaStream_t s);
+void shard_commit_pack(mspipe_memory* st, int64_t commit_version, const int32_t* nodes, const int32_t* winner,
+                       const int32_t* num, int64_t max_n, int64_t key_base, const float* new_mem,
+                       const double* new_ts, const float* new_mail, cudaStream_t s);
+void shard_commit_merge(mspipe_memory* st, int64_t commit_version, cudaStream_t s);
 int64_t shard_fetch_rec_bytes(const mspipe_memory* st, bool with_mail);
 int64_t shard_commit_rec_bytes(const mspipe_memory* st);
+void shard_layout(mspipe_memory* st);
 // nccl_xchg.cu
 mspipe_status nccl_comm_init(mspipe_memory* st, const void* unique_id);
 void nccl_comm_destroy(mspipe_memory* st);
-mspipe_status nccl_alltoall(mspipe_memory* st, const void* send, void* recv, size_t chunk, cudaStream_t s);
+mspipe_status nccl_barrier(mspipe_memory* st, bool fetch, cudaStream_t s);
 int32_t nccl_unique_id_bytes();
 mspipe_status nccl_get_unique_id(void* out);
 }  // namespace mspipe
@@ -381,20 +382,26 @@ struct mspipe_memory {
   int device;
   // ---- world > 1 (shard.cu) ----
   int64_t local_rows;       // rows of this rank's shard: nodes v with v % world == rank
-  int64_t sh_cap;           // max rows any shard serves = ceil(num_nodes / world)
+  int64_t sh_cap;           // request / reply slots per peer = ceil(num_nodes / world)
   int64_t sh_capw;          // commit records per peer
   uint8_t* sh_needed;       // [num_nodes] request marks (cleared by the plan)
   int32_t* sh_slot_of;      // [num_nodes] slot of id v in its owner's request list
-  int32_t* sh_send_ids;     // [world, sh_cap]
-  int32_t* sh_recv_ids;     // [world, sh_cap]
-  void* sh_fsend;           // fetch replies [world, sh_cap] records
-  void* sh_frecv;
-  void* sh_csend;           // commit records [world, sh_capw]
-  void* sh_crecv;
-  int32_t* sh_dest;         // [num_nodes] record slot of each local winner
+  int32_t* sh_dest;         // [num_nodes] owner * capw + slot of each local winner
   unsigned long long* sh_keytab;  // [local_rows] LWW key of the committed row
   int32_t sh_with_mail;     // the in-flight fetch carries mail rows
-  void* nccl_comm;          // ncclComm_t (NULL: in-process loopback transport)
+  int64_t sh_fetch_iter;    // iteration of the fetch in flight (window parity)
+  // receive window: one allocation (exported by CUDA IPC), per parity p:
+  // ids [world][cap] i32 | counts [3][world] i32 | replies [world][cap] | commits [world][capw]
+  uint8_t* sh_window;
+  int64_t sh_win_bytes, sh_off_ids[2], sh_off_cnt[2], sh_off_rep[2], sh_off_com[2];
+  uint8_t** sh_peers;       // [world] device: every rank's window in this process's address space
+  void* sh_peer_host[64];   // host copy (entries of other processes opened by cudaIpcOpenMemHandle)
+  uint8_t sh_peer_ipc[64];  // 1: sh_peer_host[p] must be closed with cudaIpcCloseMemHandle
+  int32_t sh_connected;     // 0: not yet, 1: IPC peers + NCCL barriers, 2: in-process ranks (stream order)
+  unsigned long long* sh_sent;  // [3] device: bytes stored into windows (fetch ids, replies, commit records)
+  int32_t* sh_bar;          // [2] device: barrier all-reduce operands (commit, fetch)
+  void* nccl_comm;          // ncclComm_t of the commit barriers (NULL: in-process rank)
+  void* nccl_comm_fetch;    // ncclComm_t of the fetch barriers
   // ---- double-buffered state (mspipe_memory_double_buffer) ----
   // Set 0 = the tables above, set 1 = a second caller-owned set; version c
   // lives in set c & 1.  Commit c first copies the rows of commit c-1 from

@@ -74,6 +74,10 @@ __device__ __forceinline__ void warp_copy_rows(const float4* __restrict__ src, i
 // ---------------------------------------------------------------------------
 constexpr int kFetchRows = 8;
 constexpr int kCopyU = 8;
+// write-back batches are small (U <= 2B rows, ~1,600 at GDELT): 2 rows per
+// warp keeps ~800 warps in flight instead of ~200 (8 rows per warp measured
+// 10.6 vs 6.4 us for the commit branch at GDELT)
+constexpr int kWbRows = 2;
 
 __global__ void __launch_bounds__(256, 4) k_fetch_gather(
     const int32_t* __restrict__ ids, int64_t n, int64_t N, const float4* __restrict__ mem,
@@ -330,9 +334,9 @@ __global__ void __launch_bounds__(256, 4) k_writeback(
   const int64_t U = min64((int64_t)__ldg(num), max_n);
   const int lane = threadIdx.x & 31;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t base = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * kFetchRows; base < U;
-       base += nwarps * kFetchRows) {
-    const int nrows = (int)min64(kFetchRows, U - base);
+  for (int64_t base = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * kWbRows; base < U;
+       base += nwarps * kWbRows) {
+    const int nrows = (int)min64(kWbRows, U - base);
     int32_t node = lane < nrows ? __ldg(nodes + base + lane) : -1;
     if (lane < nrows && (node < 0 || node >= N)) {
       raise_dev(MSPIPE_DEVERR_RANGE);
@@ -354,7 +358,7 @@ void launch_writeback(const int32_t* nodes, const int32_t* num, int64_t max_n,
                       float* mail, double* mail_ts, int64_t num_nodes, cudaStream_t s) {
   const int32_t Qm = mem_dim / 4, Qa = (int32_t)(mail_stride / 4);
   const int threads = 256;
-  launch_k(k_writeback, dim3(grid_for((max_n + kFetchRows - 1) / kFetchRows * 32, threads, 4)), dim3(threads), 0, s,
+  launch_k(k_writeback, dim3(grid_for((max_n + kWbRows - 1) / kWbRows * 32, threads, 4)), dim3(threads), 0, s,
            1, nodes, num, max_n, (const float4*)new_mem, new_ts, (const float4*)new_mail, Qm, Qa, (float4*)mem,
            mem_ts, (float4*)mail, mail_ts, num_nodes);
 }

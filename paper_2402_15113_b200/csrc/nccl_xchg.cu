@@ -1,8 +1,13 @@
-// nccl_xchg.cu — the library-owned NCCL communicator of a sharded memory
-// handle and the all-to-all that carries fetch requests / replies and
-// write-back records over NVLink (row E).  Buffers are fixed-capacity blocks
-// of `chunk` bytes per peer, so the exchange needs no host-side counts and is
-// capturable into CUDA graphs.
+// nccl_xchg.cu — the library-owned NCCL communicators of a sharded memory
+// handle (row E).  The data moves by direct stores into the peers' receive
+// windows (shard.cu); NCCL provides only the stream-ordered barrier between
+// a phase that writes peers' windows and the phase that reads its own: a
+// one-int all-reduce, which completes on a rank only after every rank has
+// reached it, i.e. after every rank's preceding kernels (whose remote stores
+// end with a system-scope fence) have finished.  Two communicators, so a
+// fetch (on the prep stream) and a commit (on the update stream) can each
+// barrier without ordering the two streams: every collective of one
+// communicator is issued in the same order on every rank.
 #include <nccl.h>
 
 #include "internal.cuh"
@@ -12,30 +17,32 @@ namespace mspipe {
 mspipe_status nccl_comm_init(mspipe_memory* st, const void* unique_id) {
   ncclUniqueId id;
   memcpy(&id, unique_id, sizeof(id));
-  ncclComm_t comm = nullptr;
+  ncclComm_t comm = nullptr, comm2 = nullptr;
   ncclResult_t r = ncclCommInitRank(&comm, st->world, id, st->rank);
   if (r != ncclSuccess) return fail(MSPIPE_ENCCL, "ncclCommInitRank: %s", ncclGetErrorString(r));
   st->nccl_comm = comm;
+  r = ncclCommSplit(comm, 0, st->rank, &comm2, nullptr);  // the fetch communicator (collective)
+  if (r != ncclSuccess) return fail(MSPIPE_ENCCL, "ncclCommSplit: %s", ncclGetErrorString(r));
+  st->nccl_comm_fetch = comm2;
   return MSPIPE_OK;
 }
 
 void nccl_comm_destroy(mspipe_memory* st) {
+  if (st && st->nccl_comm_fetch) {
+    ncclCommDestroy((ncclComm_t)st->nccl_comm_fetch);
+    st->nccl_comm_fetch = nullptr;
+  }
   if (st && st->nccl_comm) {
     ncclCommDestroy((ncclComm_t)st->nccl_comm);
     st->nccl_comm = nullptr;
   }
 }
 
-mspipe_status nccl_alltoall(mspipe_memory* st, const void* send, void* recv, size_t chunk, cudaStream_t s) {
-  ncclComm_t comm = (ncclComm_t)st->nccl_comm;
-  ncclResult_t r = ncclGroupStart();
-  for (int p = 0; p < st->world && r == ncclSuccess; ++p) {
-    r = ncclSend((const char*)send + (size_t)p * chunk, chunk, ncclUint8, p, comm, s);
-    if (r == ncclSuccess) r = ncclRecv((char*)recv + (size_t)p * chunk, chunk, ncclUint8, p, comm, s);
-  }
-  const ncclResult_t r2 = ncclGroupEnd();
-  if (r == ncclSuccess) r = r2;
-  if (r != ncclSuccess) return fail(MSPIPE_ENCCL, "all-to-all: %s", ncclGetErrorString(r));
+mspipe_status nccl_barrier(mspipe_memory* st, bool fetch, cudaStream_t s) {
+  ncclComm_t comm = (ncclComm_t)(fetch ? st->nccl_comm_fetch : st->nccl_comm);
+  ncclResult_t r = ncclAllReduce(st->sh_bar + (fetch ? 1 : 0), st->sh_bar + (fetch ? 1 : 0), 1, ncclInt32, ncclMax,
+                                 comm, s);
+  if (r != ncclSuccess) return fail(MSPIPE_ENCCL, "barrier all-reduce: %s", ncclGetErrorString(r));
   return MSPIPE_OK;
 }
 

@@ -8,10 +8,14 @@ replicated T-CSR, fetches the snapshot rows it needs from their owners
 records to the owners, which keep the largest key per node: the result equals
 the single-GPU stage at batch G·B (pin P10, tests/test_gpu_shard.py).
 
-Two transports: one process per GPU over NCCL (the library-owned communicator,
-``ShardRank`` with an ``nccl_id``), or G in-process ranks moved by
-``mspipe_shard_loopback`` (``LoopbackShards``: validation of the whole
-protocol on one GPU).
+Transport: the sending phases store straight into the peers' receive windows
+(only the real entries); a barrier follows.  One process per GPU
+(``ShardRank`` with an ``nccl_id``: CUDA IPC windows, NCCL barriers), or G
+in-process ranks on one device (``LoopbackShards``: the whole protocol on one
+GPU, the stream orders the phases).  With k >= 1 the process driver runs
+prep(t+k) (sampler, dedup, fetch) on a side stream concurrently with
+commit(t) on the main stream; the commit's merge waits only for the fetch's
+serve phase, the one that reads this rank's tables.
 """
 from __future__ import annotations
 
@@ -48,6 +52,11 @@ class ShardRank(_TimedOps):
         self.tcsr = tcsr
         self.memory = _C.MemoryHandle(cfg.num_nodes, cfg.mem_dim, cfg.edge_dim, cfg.k, self.device, rank, world,
                                       nccl_id)
+        if nccl_id is not None:  # collective: every rank's window handle, then open the peers'
+            from .dist import connect_shards
+            connect_shards(self.memory)
+        self.side = None
+        self._served = None
         self.gru = _C.GruHandle(cfg.mem_dim, cfg.edge_dim, cfg.time_dim, params, self.device, cfg.precision,
                                 max_events=cfg.batch)
         self.slots = [_Slot(cfg, self.memory.mail_stride, self.device, False) for _ in range(cfg.k + 1)]
@@ -149,19 +158,32 @@ class ShardRank(_TimedOps):
     def writeback_collective(self, i):
         _C.memory_writeback_keyed(self.memory, i, self._upd(i), key_base(i, self.rank, self.world, self.cfg.batch))
 
-    # -- NCCL driver ---------------------------------------------------------
+    # -- process driver (one rank per GPU) -----------------------------------
     def prep(self, i):
+        """A1 + A2 local, then the fetch phases with their barriers; the event
+        after the serve phase (the one that reads this rank's tables) lets a
+        concurrent commit's merge start as early as possible."""
         self._ev("prep")
         self.prep_local(i)
-        self.fetch_collective(i)
+        self.fetch_plan(i)
+        _C.shard_exchange(self.memory, _C.XCHG_FETCH_IDS)
+        self.fetch_serve()
+        self._served = torch.cuda.Event()
+        self._served.record()
+        _C.shard_exchange(self.memory, _C.XCHG_FETCH_ROWS)
+        self.fetch_finish(i)
         self._ev("prep_end")
 
-    def commit(self, i):
+    def commit(self, i, served=None):
         self._ev("update")
         self.update(i)
         self._ev("update_end")
         self._ev("writeback")
-        self.writeback_collective(i)
+        self.commit_pack(i)
+        _C.shard_exchange(self.memory, _C.XCHG_COMMIT)
+        if served is not None:  # a concurrent fetch still reads the rows the merge rewrites
+            torch.cuda.current_stream().wait_event(served)
+        self.commit_merge(i)
         self._ev("writeback_end")
         if self.staged:
             self.copy_out(i)
@@ -188,22 +210,50 @@ class ShardRank(_TimedOps):
                 cur = []
         return steps
 
-    def run_ops(self, ops):
+    def run_ops(self, ops, overlap=None, join_copies=True):
+        """One step.  overlap (default k >= 1): the step's preps on a side stream
+        (forked after the previous step's commit, so they read its version),
+        the commit on the current stream; its merge waits for the side
+        stream's serve phase, then the step joins the side stream."""
+        overlap = (self.cfg.k >= 1) if overlap is None else overlap
+        if not overlap:
+            for op, i in ops:
+                (self.prep if op == "prep" else self.commit)(i)
+            return
+        main = torch.cuda.current_stream()
+        if self.side is None or self.side.device != main.device:
+            self.side = torch.cuda.Stream(device=main.device)
+        self.side.wait_stream(main)
+        served = None
         for op, i in ops:
-            (self.prep if op == "prep" else self.commit)(i)
+            if op == "prep":
+                with torch.cuda.stream(self.side):
+                    self.prep(i)
+                served = self._served
+                if any(o == "commit" and j == i for o, j in ops):  # its own commit in this step
+                    main.wait_stream(self.side)
+            else:
+                self.commit(i, served=served)
+        main.wait_stream(self.side)
 
     def run(self, nb=None):
         for ops in self.step_ops(nb):
             self.run_ops(ops)
 
+    def exchange_bytes(self):
+        """(fetch ids, reply rows, commit records) bytes this rank stored since the last reset."""
+        return _C.shard_sent_bytes(self.memory)
+
 
 class LoopbackShards:
-    """G in-process ranks on one device, phases interleaved, buffers moved by
-    mspipe_shard_loopback: the whole sharded protocol without NCCL."""
+    """G in-process ranks on one device, phases interleaved on one stream (the
+    stream orders each phase's stores into the windows before the phase that
+    reads them): the whole sharded protocol without NCCL."""
 
     def __init__(self, cfg: StageConfig, params: dict, tcsr: _C.TcsrHandle, device, world: int):
         self.cfg, self.world = cfg, world
         self.ranks = [ShardRank(cfg, params, tcsr, device, r, world, None) for r in range(world)]
+        _C.shard_connect_local([r.memory for r in self.ranks])
 
     def bind_resident(self, src, dst, ts, neg, ef):
         for r in self.ranks:
