@@ -155,6 +155,8 @@ mspipe_status mspipe_memory_create(mspipe_memory** out, int64_t num_nodes, int32
   st->local_rows = (num_nodes - rank + world - 1) / world;
   cudaError_t e = cudaMalloc(&st->scratch, sizeof(int32_t) * (size_t)num_nodes);
   if (e == cudaSuccess) e = cudaMemset(st->scratch, 0xFF, sizeof(int32_t) * (size_t)num_nodes);
+  if (e == cudaSuccess) e = cudaMalloc(&st->sample_hint, sizeof(int64_t) * (size_t)num_nodes);
+  if (e == cudaSuccess) e = cudaMemset(st->sample_hint, 0, sizeof(int64_t) * (size_t)num_nodes);
   if (e == cudaSuccess && world > 1) {
     st->sh_cap = (num_nodes + world - 1) / world;
     st->sh_capw = st->sh_cap;  // unique nodes per owner never exceed its shard
@@ -286,7 +288,7 @@ mspipe_status mspipe_memory_destroy(mspipe_memory* st) {
   nccl_comm_destroy(st);
   for (int p = 0; p < st->world && p < 64; ++p)
     if (st->sh_peer_ipc[p] && st->sh_peer_host[p]) cudaIpcCloseMemHandle(st->sh_peer_host[p]);
-  void* bufs[] = {st->scratch, st->sh_needed, st->sh_slot_of, st->sh_dest, st->sh_keytab, st->sh_window,
+  void* bufs[] = {st->scratch, st->sample_hint, st->sh_needed, st->sh_slot_of, st->sh_dest, st->sh_keytab, st->sh_window,
                   st->sh_peers, st->sh_sent, st->sh_bar, st->prev_nodes,
                   st->prev_num, st->stamps};
   for (void* b : bufs)
@@ -651,7 +653,8 @@ mspipe_status mspipe_memory_prep(mspipe_memory* st, const mspipe_tcsr* g, int64_
                                 t.mem_ts, st->mem_dim, t.mail, t.mail_ts, st->mail_stride, out_mem,
                                 out_mem_ts, out_mail, out_mail_ts, s,
                                 (st->db && dedup) ? st->stamps + (iteration % (st->k + 1)) * st->num_nodes : nullptr,
-                                (int32_t)iteration, cu ? &cua : nullptr);
+                                (int32_t)iteration, cu ? &cua : nullptr,
+                                env_int("MSPIPE_SAMPLE_HINT", 1) ? st->sample_hint : nullptr);
     if (e != cudaSuccess) return cuda_status(e, "memory_prep: launch");
     if (st->db && dedup) st->stamp_iter[iteration % (st->k + 1)] = iteration;
     if (cu) st->caught_up = c;

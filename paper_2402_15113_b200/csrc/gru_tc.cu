@@ -474,7 +474,8 @@ __device__ __forceinline__ void build_bf16(const TcArgs& a) {
   }
 }
 
-// A5: one warp per (row, chunk).  lane = column inside the chunk.
+// A5: one warp per (row, kBuildChunks chunks).  lane = column inside a chunk.
+constexpr int kBuildChunks = 4;
 __global__ void __launch_bounds__(256) k_build_x(TcArgs a) {
   if (a.d.bf16) {
     build_bf16(a);
@@ -483,45 +484,64 @@ __global__ void __launch_bounds__(256) k_build_x(TcArgs a) {
   const GruDesc& d = a.d;
   const int32_t U = __ldg(a.num_unique);
   const int32_t nchunks = d.Kpad / tc::kKC;
+  const int32_t ngroups = (nchunks + kBuildChunks - 1) / kBuildChunks;
   const int32_t mtiles = (U + tc::kM - 1) / tc::kM;
-  // items < 2^31 (U <= 16384 rows, <= 20 chunks): 32-bit index arithmetic (a
-  // 64-bit division by the runtime chunk count cost ~70 instructions per lane)
-  const uint32_t items = (uint32_t)mtiles * (uint32_t)nchunks * tc::kM;
+  // one warp per (row, group of kBuildChunks K chunks): the row's pair, rows
+  // and Δt are resolved once for 128 columns (the per-item index work was
+  // half of the kernel's issue slots with one chunk per item), kBuildChunks
+  // loads in flight per lane.  items < 2^31: 32-bit index arithmetic.
+  const uint32_t items = (uint32_t)mtiles * (uint32_t)ngroups * tc::kM;
   const int lane = threadIdx.x & 31;
   const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
   const int32_t M = d.M;
   for (uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < items; w += nwarps) {
     const int32_t row = (int32_t)(w % tc::kM);
-    const uint32_t cm = w / tc::kM;
-    const int32_t mt = (int32_t)(cm / (uint32_t)nchunks);
-    const int32_t c = (int32_t)(cm - (uint32_t)mt * (uint32_t)nchunks);
+    const uint32_t gm = w / tc::kM;
+    const int32_t mt = (int32_t)(gm / (uint32_t)ngroups);
+    const int32_t cg = (int32_t)(gm - (uint32_t)mt * (uint32_t)ngroups);
     const int32_t u = mt * tc::kM + row;
-    const int32_t k = c * tc::kKC + lane;
-    float v = 0.f;
+    float v[kBuildChunks];
+#pragma unroll
+    for (int q = 0; q < kBuildChunks; ++q) v[q] = 0.f;
     if (u < U) {
       const int32_t p = __ldg(a.winner + u);
       const int32_t ev = p >> 1, role = p & 1;
-      if (k < M) v = __ldg(a.snap_mem + snap_row(a, ev, role) * M + k);
-      else if (k < 2 * M) v = __ldg(a.snap_mem + snap_row(a, ev, role ^ 1) * M + (k - M));
-      else if (k < d.Dm) v = __ldg(a.ef + (int64_t)ev * d.He + (k - 2 * M));
-      else if (k < d.Dx) {
-        const float dt = (float)(__ldg(a.ts + ev) - __ldg(a.snap_ts + snap_row(a, ev, role)));  // Δt (G4)
-        const int q = k - d.Dm;
-        v = time_cos(fmaf(__ldg(d.time_w + q), dt, __ldg(d.time_b + q)));
-      } else if (k < d.K) {
-        const int q = k - d.Dx;
-        v = a.snap_h ? __ldg(a.snap_h + (role ? a.B + ev : (int64_t)ev) * M + q)
-                     : __ldg(a.snap_mem + snap_row(a, ev, role) * M + q);
+      const float* sw = a.snap_mem + snap_row(a, ev, role) * M;
+      const float* so = a.snap_mem + snap_row(a, ev, role ^ 1) * M;
+      const float* hrow = a.snap_h ? a.snap_h + (role ? a.B + ev : (int64_t)ev) * M : sw;
+      const float* erow = a.ef + (int64_t)ev * d.He;
+      const double t_ev = __ldg(a.ts + ev);
+      const float dt = (float)(t_ev - __ldg(a.snap_ts + snap_row(a, ev, role)));  // Δt (G4)
+#pragma unroll
+      for (int q = 0; q < kBuildChunks; ++q) {  // loads first (all in flight), then the encoding
+        const int32_t k = (cg * kBuildChunks + q) * tc::kKC + lane;
+        if (k < M) v[q] = __ldg(sw + k);
+        else if (k < 2 * M) v[q] = __ldg(so + (k - M));
+        else if (k < d.Dm) v[q] = __ldg(erow + (k - 2 * M));
+        else if (k >= d.Dx && k < d.K) v[q] = __ldg(hrow + (k - d.Dx));
       }
-      if (k < a.mail_stride) a.out_mail[(int64_t)u * a.mail_stride + k] = k < d.Dm ? v : 0.f;
-      if (c == 0 && lane == 0) a.out_ts[u] = __ldg(a.ts + ev);
+#pragma unroll
+      for (int q = 0; q < kBuildChunks; ++q) {
+        const int32_t k = (cg * kBuildChunks + q) * tc::kKC + lane;
+        if (k >= d.Dm && k < d.Dx) {
+          const int qq = k - d.Dm;
+          v[q] = time_cos(fmaf(__ldg(d.time_w + qq), dt, __ldg(d.time_b + qq)));
+        }
+        if (k < a.mail_stride) a.out_mail[(int64_t)u * a.mail_stride + k] = k < d.Dm ? v[q] : 0.f;
+      }
+      if (cg == 0 && lane == 0) a.out_ts[u] = t_ev;
     }
-    const float hi = tc::tf32_rna(v);
-    const float lo = tc::tf32_rna(v - hi);
-    char* blk = reinterpret_cast<char*>(a.xbuf) + ((int64_t)mt * nchunks + c) * tc::kABlock;
     const uint32_t off = tc::sw128_off((uint32_t)row, (uint32_t)lane);
-    *reinterpret_cast<float*>(blk + off) = hi;
-    *reinterpret_cast<float*>(blk + tc::kATile + off) = lo;
+#pragma unroll
+    for (int q = 0; q < kBuildChunks; ++q) {
+      const int32_t c = cg * kBuildChunks + q;
+      if (c >= nchunks) break;
+      const float hi = tc::tf32_rna(v[q]);
+      const float lo = tc::tf32_rna(v[q] - hi);
+      char* blk = reinterpret_cast<char*>(a.xbuf) + ((int64_t)mt * nchunks + c) * tc::kABlock;
+      *reinterpret_cast<float*>(blk + off) = hi;
+      *reinterpret_cast<float*>(blk + tc::kATile + off) = lo;
+    }
   }
 }
 
@@ -1120,7 +1140,8 @@ cudaError_t launch_gru_tc(const GruDesc& d, const float* wtc, float* xbuf, const
   const int64_t max_rows = 2 * num_events;
   const int64_t mtiles = (max_rows + tc::kM - 1) / tc::kM;
   if (parts & kGruBuild) {
-    const int64_t warps = mtiles * (d.Kpad / (d.bf16 ? tc::kKC16 : tc::kKC)) * tc::kM;
+    const int64_t nch = d.Kpad / (d.bf16 ? tc::kKC16 : tc::kKC);
+    const int64_t warps = mtiles * (d.bf16 ? nch : (nch + kBuildChunks - 1) / kBuildChunks) * tc::kM;
     int64_t blocks = (warps * 32 + 255) / 256;
     const int64_t cap = (int64_t)num_sms() * env_int("MSPIPE_BUILD_BPS", 8);
     if (blocks > cap) blocks = cap;

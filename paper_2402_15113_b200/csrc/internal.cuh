@@ -131,9 +131,17 @@ __device__ __forceinline__ int64_t warp_recent_end(const Tcsr& g, int32_t v, dou
 // at most 32 entries (most rows) costs one dependent round less than
 // warp_recent_end followed by the loads; entries below the last window (a long
 // row whose F most recent straddle it) are loaded directly.
+// hint (nullable, [num_nodes]): per node a position near the previous answer
+// (the stage's queries move forward in time, so the next answer is usually a
+// few entries later).  One round of 32 galloping probes around it (offsets
+// +-1, 2, 4, ... 2^15, mostly L2-resident lines the previous batch touched)
+// brackets the answer before the 33-ary search, which then needs one or two
+// rounds instead of log33(row); the result does not depend on the hint (any
+// position is a valid start), and the warp stores its answer back as the next
+// hint (racing stores all write valid positions).
 __device__ __forceinline__ int64_t warp_recent_sample(const Tcsr& g, int32_t v, double tq, int lane, int F,
                                                       int64_t* beg_out, int32_t* nbr_out, int32_t* eid_out,
-                                                      double* ts_out) {
+                                                      double* ts_out, int64_t* hint = nullptr) {
   *nbr_out = -1;
   *eid_out = -1;
   *ts_out = 0.0;
@@ -144,6 +152,24 @@ __device__ __forceinline__ int64_t warp_recent_sample(const Tcsr& g, int32_t v, 
   }
   const int64_t beg = __ldg(g.indptr + v);
   int64_t lo = beg, hi = __ldg(g.indptr + v + 1);
+  if (hint && hi - lo > 32) {
+    int64_t h = __ldcg(hint + v);
+    h = h < lo ? lo : (h > hi ? hi : h);
+    // lanes 0..15 probe h + 2^l - 1, lanes 16..31 probe h - 2^(l-16)
+    const int64_t p = lane < 16 ? h + ((int64_t(1) << lane) - 1) : h - (int64_t(1) << (lane - 16));
+    const bool in = p >= lo && p < hi;
+    const bool below = in && __ldg(g.ts + p) < tq;
+    int64_t lo_c = below ? p + 1 : lo;           // every probe below t_q raises lo
+    int64_t hi_c = (in && !below) ? p : hi;      // every probe at or above t_q lowers hi
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const int64_t a = __shfl_xor_sync(0xffffffffu, lo_c, o), b = __shfl_xor_sync(0xffffffffu, hi_c, o);
+      lo_c = a > lo_c ? a : lo_c;
+      hi_c = b < hi_c ? b : hi_c;
+    }
+    lo = lo_c;
+    hi = hi_c;
+  }
   while (hi - lo > 32) {
     const int64_t span = hi - lo;
     const int64_t p = lo + probe_offset33(lane, span);
@@ -176,6 +202,7 @@ __device__ __forceinline__ int64_t warp_recent_sample(const Tcsr& g, int32_t v, 
       *ts_out = __ldg(g.ts + e);
     }
   }
+  if (hint && lane == 0) hint[v] = end;
   *beg_out = beg;
   return end;
 }
@@ -342,7 +369,7 @@ cudaError_t launch_prep(const Tcsr& g, const int32_t* src, const int32_t* dst, c
                         const float* mem, const double* mem_ts, int32_t mem_dim, const float* mail,
                         const double* mail_ts, int64_t mail_stride, float* out_mem, double* out_mem_ts,
                         float* out_mail, double* out_mail_ts, cudaStream_t s, int32_t* stamp = nullptr,
-                        int32_t stamp_iter = 0, const struct CatchUp* cu = nullptr);
+                        int32_t stamp_iter = 0, const struct CatchUp* cu = nullptr, int64_t* hint = nullptr);
 
 }  // namespace mspipe
 
@@ -379,6 +406,7 @@ struct mspipe_memory {
   int32_t rank, world;
   int64_t committed;
   int32_t* scratch;  // [num_nodes] int32, -1 between calls (self-cleaning)
+  int64_t* sample_hint;  // [num_nodes] search start per node for the fused prep's sampler (any value is valid)
   int device;
   // ---- world > 1 (shard.cu) ----
   int64_t local_rows;       // rows of this rank's shard: nodes v with v % world == rank

@@ -57,6 +57,7 @@ struct PrepArgs {
   CatchUp cu;      // optional (cu.stamp != nullptr): the next commit's catch-up rows
   int32_t Qcu;     // float4 per mail row of the state tables (catch-up)
   int32_t dedup;   // 1: block 0 deduplicates (A2); 0: no dedup block
+  int64_t* hint;   // optional [num_nodes]: per-node search start (warp_recent_sample)
 };
 
 // copy `nrows` table rows (ids held by lanes 0..nrows-1, -1 = zero row) of Q
@@ -139,7 +140,7 @@ __global__ void __launch_bounds__(kPrepThreads, MSPIPE_PREP_MINB) k_prep(PrepArg
     int64_t beg;
     int32_t nbs, eis;
     double tss;
-    const int64_t end = warp_recent_sample(a.g, v, tq, lane, F, &beg, &nbs, &eis, &tss);
+    const int64_t end = warp_recent_sample(a.g, v, tq, lane, F, &beg, &nbs, &eis, &tss, a.hint);
     const int32_t cnt = (int32_t)min64(end - beg, (int64_t)F);
     // A1 outputs; lane s < F = slot s (newest first); lane s in [1, F] also holds subgraph id s
     if (lane < F) {
@@ -183,13 +184,14 @@ cudaError_t launch_prep(const Tcsr& g, const int32_t* src, const int32_t* dst, c
                         const float* mem, const double* mem_ts, int32_t mem_dim, const float* mail,
                         const double* mail_ts, int64_t mail_stride, float* out_mem, double* out_mem_ts,
                         float* out_mail, double* out_mail_ts, cudaStream_t s, int32_t* stamp,
-                        int32_t stamp_iter, const CatchUp* cu) {
+                        int32_t stamp_iter, const CatchUp* cu, int64_t* hint) {
   PrepArgs a{g, src, dst, neg, ts, num_events, fanout, out_nbr, out_eid, out_ts, out_dt, out_cnt, out_sub,
              scratch, out_nodes, out_winner, out_num, (const float4*)mem, mem_ts, mem_dim / 4,
              (const float4*)mail, mail_ts, out_mail ? (int32_t)(mail_stride / 4) : 0, (float4*)out_mem, out_mem_ts,
              (float4*)out_mail, out_mail ? out_mail_ts : nullptr, stamp, stamp_iter, CatchUp{},
              (int32_t)(mail_stride / 4)};
   if (cu) a.cu = *cu;
+  a.hint = hint;
   a.dedup = out_num != nullptr;
   int64_t blocks = (3 * num_events + kPrepWarps - 1) / kPrepWarps;
   // one wave of the two resident blocks per SM; the root warps grid-stride
