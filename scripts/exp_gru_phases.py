@@ -34,18 +34,20 @@ if os.environ.get("EXP_COLD"):  # the recorded step alone (its prep skipped), af
     torch.cuda.synchronize()
     stage_mod._DEBUG_ONLY = ""
 L = ctypes.CDLL(dbg)
-buf = np.zeros((8192, 10), np.uint64)
+buf = np.zeros((8192, 16), np.uint64)
 print("copy rc", L.mspipe_debug_phases(buf.ctypes.data_as(ctypes.c_void_p), 8192))
 U = int(st.upd["num"].item())
 used = buf[:, 9] > 0
 ph = buf[used].astype(np.int64)
 print("U", U, "CTAs recorded", used.sum())
 t0 = ph[:, 9].min()
-names = {9: "entry", 0: "setup", 2: "mma_done", 3: "acc_full", 4: "tmem_sum", 1: "pushed", 5: "sync", 7: "arrived", 6: "cluster1", 8: "end"}
+names = {9: "entry", 0: "setup", 2: "mma_done", 3: "acc_full", 4: "tmem_sum", 1: "pushed", 5: "sync", 7: "arrived", 6: "cluster1", 11: "sum_done", 10: "gates_done", 8: "end"}
 act = ph[:, 3] > 0
+one = act & (ph[:, 8] - ph[:, 9] < np.median(ph[act, 8] - ph[act, 9]) * 1.3)  # CTAs with one tile (the marks are the last tile's)
+print("one-tile CTAs", one.sum())
 print("active CTAs", act.sum())
-for k in [9, 0, 2, 3, 4, 1, 5, 7, 6, 8]:
-    col = ph[act, k] - t0
+for k in [9, 0, 2, 3, 4, 1, 5, 6, 11, 10, 8]:
+    col = ph[one, k] - ph[one, 9]
     print(f"{names[k]:10s} min {col.min()/1e3:8.2f} med {np.median(col)/1e3:8.2f} max {col.max()/1e3:8.2f} us")
 dead = ~act
 if dead.any():

@@ -2,6 +2,8 @@
 # A/B: GEMM K-split at GDELT (prefix T-CSR), sampler hints at GDELT (full T-CSR); then the GPU tests
 cd "$GRAFT_REPO_ROOT" || exit 1
 mkdir -p gpurun_out
+timeout 2400 python -m pytest tests -m gpu -q -s -x > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+tail -5 gpurun_out/pytest_gpu.log
 for S in 1 2 4; do
   MSPIPE_TC_SPLITS=$S timeout 900 python bench.py --tcsr-events 4000000 --no-probe --no-cpu > gpurun_out/ab_splits_$S.json 2> gpurun_out/ab_splits_$S.err
 done
@@ -17,5 +19,8 @@ for f in sorted(glob.glob("gpurun_out/ab_*.json")):
     r = d["roofline"]
     print(f, "%.2f Mev/s" % (d["value"] / 1e6), "%.2f us/step" % (d["ms_per_step"] * 1e3), "alone", {k: round(v * 1e3, 2) for k, v in r.get("dominant_of", {}).items()}, "in_step", {k: round(v * 1e3, 2) for k, v in r.get("in_step_ms", {}).items()})
 PY
-timeout 2400 python -m pytest tests -m gpu -q -s > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
-tail -5 gpurun_out/pytest_gpu.log
+for c in gdelt wiki; do
+  echo "== $c" >> gpurun_out/phases.txt
+  timeout 600 python scripts/exp_gru_phases.py $c >> gpurun_out/phases.txt 2>&1
+done
+cat gpurun_out/phases.txt
