@@ -579,6 +579,11 @@ MSPIPE_API mspipe_status mspipe_util_event_record(void* event, void* stream);
  * Errors: MSPIPE_EINVAL for NULL exec, MSPIPE_ECUDA with the runtime's message
  * (a capture that fails to end is discarded). */
 MSPIPE_API mspipe_status mspipe_util_graph_begin(void* stream);
+/* Utility (e2e inputs): one asynchronous host -> device copy of a batch's
+ * packed input record (`bytes` from pinned host memory at host_src to the
+ * device buffer dst) on `stream`; capturable (a memcpy node of the step
+ * graph).  Errors: MSPIPE_EINVAL (NULL, bytes < 0), MSPIPE_ECUDA. */
+MSPIPE_API mspipe_status mspipe_util_record_to_device(void* dst, const void* host_src, int64_t bytes, void* stream);
 /* Utility (e2e read-back): copy the first *num (device) rows of two device
  * arrays a [.., a_row_bytes] and b [.., b_row_bytes] into host_a / host_b —
  * mapped pinned host memory (cudaHostAlloc; mapped under UVA) written by the

@@ -39,7 +39,7 @@ EXPORTS = ("mspipe_abi_version", "mspipe_last_error", "mspipe_check", "mspipe_sa
            "mspipe_util_rows_to_host",
            "mspipe_gru_apply_commit_out", "mspipe_plan_stale_fractions", "mspipe_staleness_error",
            "mspipe_shard_window_handle", "mspipe_shard_connect", "mspipe_shard_connect_local",
-           "mspipe_shard_sent_bytes")
+           "mspipe_shard_sent_bytes", "mspipe_util_record_to_device")
 XCHG_FETCH_IDS, XCHG_FETCH_ROWS, XCHG_COMMIT = 0, 1, 2
 
 
@@ -129,6 +129,7 @@ def lib():
         L.mspipe_shard_connect.argtypes = [P, P, i32]
         L.mspipe_shard_connect_local.argtypes = [P, i32]
         L.mspipe_shard_sent_bytes.argtypes = [P, P]
+        L.mspipe_util_record_to_device.argtypes = [P, P, i64, P]
         if L.mspipe_abi_version() != ABI_VERSION:
             raise RuntimeError(f"libmspipe ABI {L.mspipe_abi_version()} != binding {ABI_VERSION}")
         _lib = L
@@ -222,6 +223,13 @@ def stale_histogram(g: "TcsrHandle", src, dst, batch, max_d=64, stream=None):
     _ck(lib().mspipe_stale_histogram(C.byref(g.c), ptr(src), ptr(dst), src.numel(), int(batch), int(max_d),
                                      ptr(out), stream_ptr(stream)), "mspipe_stale_histogram")
     return out
+
+
+def record_to_device(dst, host_src, stream=None):
+    """H2D of a pinned host record into a device buffer (mspipe_util_record_to_device)."""
+    n = host_src.numel() * host_src.element_size()
+    _ck(lib().mspipe_util_record_to_device(ptr(dst), C.c_void_p(host_src.data_ptr()), n, stream_ptr(stream)),
+        "mspipe_util_record_to_device")
 
 
 def rows_to_host(num, host_num, a, host_a, b, host_b, max_rows, stream=None):

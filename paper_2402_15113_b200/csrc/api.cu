@@ -1093,6 +1093,13 @@ mspipe_status mspipe_staleness_error(const int32_t* winner, const int32_t* num_u
   return after_launch("staleness_error");
 }
 
+mspipe_status mspipe_util_record_to_device(void* dst, const void* host_src, int64_t bytes, void* stream) {
+  if (!dst || !host_src || bytes < 0) return fail(MSPIPE_EINVAL, "util_record_to_device: NULL or bytes=%lld", (long long)bytes);
+  if (bytes == 0) return MSPIPE_OK;
+  return cuda_status(cudaMemcpyAsync(dst, host_src, (size_t)bytes, cudaMemcpyHostToDevice, (cudaStream_t)stream),
+                     "util_record_to_device");
+}
+
 mspipe_status mspipe_util_rows_to_host(const int32_t* num, int32_t* host_num, const void* a, void* host_a,
                                        int64_t a_row_bytes, const void* b, void* host_b, int64_t b_row_bytes,
                                        int64_t max_rows, void* stream) {

@@ -216,7 +216,7 @@ constexpr int kStageBytes16 = kABlock16 + kBBlock16;  // 48 KB
 }  // namespace tc
 
 #ifdef MSPIPE_PHASES
-__device__ unsigned long long g_phase[8192][10];
+__device__ unsigned long long g_phase[8192][16];
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -942,6 +942,7 @@ __global__ void __launch_bounds__(tc::kThreads, 1) k_gru_tc(TcArgs a) {
             acc[g].z += v.z;
             acc[g].w += v.w;
           }
+        if (it == (int)threadIdx.x) PHASE(11);
         float pr[4], pz[4], pnx[4], pnh[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
@@ -953,6 +954,7 @@ __global__ void __launch_bounds__(tc::kThreads, 1) k_gru_tc(TcArgs a) {
         }
         store_h4(a, u, rownode[mm], j0, gates4(pr, pz, pnx, pnh, hbuf[mm * (kJ / 4) + qq], d.cell));
       }
+      PHASE(10);
       if (a.commit_mem && !a.skip_meta) commit_rows(a, m0, U, rb, rb + R, jt, J, rownode);
       PHASE(8);
     }
@@ -1170,6 +1172,6 @@ cudaError_t launch_gru_tc(const GruDesc& d, const float* wtc, float* xbuf, const
 
 #ifdef MSPIPE_PHASES
 extern "C" __attribute__((visibility("default"))) int mspipe_debug_phases(void* host, int n) {
-  return (int)cudaMemcpyFromSymbol(host, mspipe::g_phase, sizeof(unsigned long long) * 10 * n);
+  return (int)cudaMemcpyFromSymbol(host, mspipe::g_phase, sizeof(unsigned long long) * 16 * n);
 }
 #endif

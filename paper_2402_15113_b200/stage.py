@@ -294,7 +294,7 @@ class MemoryStage(_TimedOps):
 
     def _load(self, i):
         """H2D of batch i's packed record into its ring buffer, on the current stream."""
-        self.inp_ring[(i - 1) % (self.cfg.k + 2)].copy_(self.host_rec[i - 1], non_blocking=True)
+        _C.record_to_device(self.inp_ring[(i - 1) % (self.cfg.k + 2)], self.host_rec[i - 1])
 
     # -- ops ------------------------------------------------------------------
     def _slot(self, i):
