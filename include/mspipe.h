@@ -430,8 +430,21 @@ MSPIPE_API mspipe_status mspipe_gru_apply_commit_out(const mspipe_gru* gru, mspi
  * ranks on one stream (the stream orders them; mspipe_shard_exchange and
  * mspipe_shard_loopback are then no-ops), e.g. G virtual ranks on one GPU for
  * testing.  The phases fail with MSPIPE_EUNSUPPORTED before a connect.
- * MSPipe-S mitigation is not available for world > 1 in this build
- * (MSPIPE_EUNSUPPORTED).
+ *
+ * MSPipe-S with world > 1 (A4): the 2-hop
+ * candidates' mem_ts and the Ω rows belong to other ranks.  After the
+ * subgraph fetch of iteration i (which brought each target's own row and
+ * mem_ts as its root row), mspipe_shard_mitigation_candidates lists, for
+ * every eligible target t (Δ = t* − S.mem_ts[w] > γ, G11), [w, the distinct
+ * ids of sample(x, t*) \ {w} for x in sample(w, t*) \ {w}] into out_ids
+ * [2B, 1 + fanout²] (pads −1; the T-CSR is replicated); a second fetch of
+ * that list (plan -> exchange -> serve -> exchange ->
+ * mspipe_shard_fetch_finish_table) writes those rows into a node-indexed
+ * table [num_nodes, mem_dim] / [num_nodes] of version v(i); mspipe_shard_mitigate
+ * then computes eligibility, Ω and the blend exactly as the single-GPU fetch
+ * does (same outputs as mspipe_mitigation), reading only table rows the list
+ * requested.  memory_fetch with mitigation at world > 1: MSPIPE_EUNSUPPORTED
+ * (use these phases).
  *
  * Phases of a fetch: plan (stores the request ids into the owners' windows)
  * -> exchange(FETCH_IDS) -> serve (owner stores the reply rows into the
@@ -460,6 +473,13 @@ MSPIPE_API mspipe_status mspipe_shard_fetch_serve(mspipe_memory* st, void* strea
 MSPIPE_API mspipe_status mspipe_shard_fetch_finish(mspipe_memory* st, const int32_t* ids, int64_t n,
                                         float* out_mem, double* out_mem_ts, float* out_mail,
                                         double* out_mail_ts, int64_t* out_version, void* stream);
+MSPIPE_API mspipe_status mspipe_shard_mitigation_candidates(mspipe_memory* st, const mspipe_mitigation* mit,
+                                                 const double* root_mem_ts, int64_t root_step,
+                                                 int32_t* out_ids, void* stream);
+MSPIPE_API mspipe_status mspipe_shard_fetch_finish_table(mspipe_memory* st, const int32_t* ids, int64_t n,
+                                              float* table_mem, double* table_mem_ts, void* stream);
+MSPIPE_API mspipe_status mspipe_shard_mitigate(mspipe_memory* st, const mspipe_mitigation* mit,
+                                    const float* table_mem, const double* table_mem_ts, void* stream);
 MSPIPE_API mspipe_status mspipe_shard_commit_pack(mspipe_memory* st, int64_t commit_version,
                                        const int32_t* nodes, const int32_t* winner,
                                        const int32_t* num_unique, int64_t max_n, int64_t key_base,

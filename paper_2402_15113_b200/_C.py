@@ -39,7 +39,8 @@ EXPORTS = ("mspipe_abi_version", "mspipe_last_error", "mspipe_check", "mspipe_sa
            "mspipe_util_rows_to_host",
            "mspipe_gru_apply_commit_out", "mspipe_plan_stale_fractions", "mspipe_staleness_error",
            "mspipe_shard_window_handle", "mspipe_shard_connect", "mspipe_shard_connect_local",
-           "mspipe_shard_sent_bytes", "mspipe_util_record_to_device")
+           "mspipe_shard_sent_bytes", "mspipe_util_record_to_device", "mspipe_shard_mitigation_candidates",
+           "mspipe_shard_fetch_finish_table", "mspipe_shard_mitigate")
 XCHG_FETCH_IDS, XCHG_FETCH_ROWS, XCHG_COMMIT = 0, 1, 2
 
 
@@ -130,6 +131,9 @@ def lib():
         L.mspipe_shard_connect_local.argtypes = [P, i32]
         L.mspipe_shard_sent_bytes.argtypes = [P, P]
         L.mspipe_util_record_to_device.argtypes = [P, P, i64, P]
+        L.mspipe_shard_mitigation_candidates.argtypes = [P, C.POINTER(Mitigation), P, i64, P, P]
+        L.mspipe_shard_fetch_finish_table.argtypes = [P, P, i64, P, P, P]
+        L.mspipe_shard_mitigate.argtypes = [P, C.POINTER(Mitigation), P, P, P]
         if L.mspipe_abi_version() != ABI_VERSION:
             raise RuntimeError(f"libmspipe ABI {L.mspipe_abi_version()} != binding {ABI_VERSION}")
         _lib = L
@@ -485,6 +489,22 @@ def shard_sent_bytes(st):
     out = (C.c_int64 * 3)()
     _ck(lib().mspipe_shard_sent_bytes(st.h, out), "mspipe_shard_sent_bytes")
     return tuple(int(x) for x in out)
+
+
+def shard_mitigation_candidates(st, mit, root_mem_ts, root_step, out_ids, stream=None):
+    """MSPipe-S at world > 1: the ids whose rows the eligible targets' mitigation reads."""
+    _ck(lib().mspipe_shard_mitigation_candidates(st.h, C.byref(mit), ptr(root_mem_ts), int(root_step), ptr(out_ids),
+                                                 stream_ptr(stream)), "mspipe_shard_mitigation_candidates")
+
+
+def shard_fetch_finish_table(st, ids, table_mem, table_mem_ts, stream=None):
+    _ck(lib().mspipe_shard_fetch_finish_table(st.h, ptr(ids), ids.numel(), ptr(table_mem), ptr(table_mem_ts),
+                                              stream_ptr(stream)), "mspipe_shard_fetch_finish_table")
+
+
+def shard_mitigate(st, mit, table_mem, table_mem_ts, stream=None):
+    _ck(lib().mspipe_shard_mitigate(st.h, C.byref(mit), ptr(table_mem), ptr(table_mem_ts), stream_ptr(stream)),
+        "mspipe_shard_mitigate")
 
 
 def shard_loopback(handles, kind, stream=None):

@@ -346,7 +346,7 @@ mspipe_status mspipe_memory_fetch(mspipe_memory* st, int64_t iteration, const in
   if (n > 0 && (!ids || !out_mem || !out_mem_ts)) return fail(MSPIPE_EINVAL, "memory_fetch: null ids/outputs");
   if ((out_mail == nullptr) != (out_mail_ts == nullptr)) return fail(MSPIPE_EINVAL, "memory_fetch: out_mail and out_mail_ts go together");
   if (st->world > 1) {
-    if (mit) return fail(MSPIPE_EUNSUPPORTED, "memory_fetch: mitigation with world > 1 is not in this build");
+    if (mit) return fail(MSPIPE_EUNSUPPORTED, "memory_fetch: world > 1 runs MSPipe-S through the mspipe_shard_mitigation_* phases");
     if (st->sh_connected != 1)
       return fail(MSPIPE_EUNSUPPORTED, "memory_fetch: %s", st->sh_connected == 2 ? "in-process rank: drive the mspipe_shard_* phases" : "not connected (mspipe_shard_connect)");
     cudaStream_t s = (cudaStream_t)stream;
@@ -914,6 +914,45 @@ mspipe_status mspipe_shard_fetch_finish(mspipe_memory* st, const int32_t* ids, i
   if (n > 0) shard_fetch_finish(st, ids, n, out_mem, out_mem_ts, out_mail, out_mail_ts, (cudaStream_t)stream);
   if (out_version) *out_version = st->committed;
   return after_launch("shard_fetch_finish");
+}
+
+mspipe_status mspipe_shard_mitigation_candidates(mspipe_memory* st, const mspipe_mitigation* mit,
+                                                const double* root_mem_ts, int64_t root_step, int32_t* out_ids,
+                                                void* stream) {
+  mspipe_status rc = shard_ok(st, "shard_mitigation_candidates");
+  if (rc != MSPIPE_OK) return rc;
+  if (!mit || !tcsr_ok(mit->g) || mit->num_events < 0 || mit->fanout < 1 || mit->fanout > 16 || root_step < 1 ||
+      (mit->num_events > 0 && (!mit->src || !mit->dst || !mit->ts || !root_mem_ts || !out_ids)))
+    return fail(MSPIPE_EINVAL, "shard_mitigation_candidates: bad arguments");
+  if (mit->num_events == 0) return MSPIPE_OK;
+  shard_mit_candidates(to_tcsr(mit->g), mit->src, mit->dst, mit->ts, mit->num_events, root_mem_ts, root_step,
+                       mit->gamma, mit->fanout, out_ids, (cudaStream_t)stream);
+  return after_launch("shard_mitigation_candidates");
+}
+
+mspipe_status mspipe_shard_fetch_finish_table(mspipe_memory* st, const int32_t* ids, int64_t n, float* table_mem,
+                                              double* table_mem_ts, void* stream) {
+  mspipe_status rc = shard_ok(st, "shard_fetch_finish_table");
+  if (rc != MSPIPE_OK) return rc;
+  if (n < 0 || (n > 0 && (!ids || !table_mem || !table_mem_ts)))
+    return fail(MSPIPE_EINVAL, "shard_fetch_finish_table: null ids/outputs");
+  if (n > 0) shard_fetch_finish_table(st, ids, n, table_mem, table_mem_ts, (cudaStream_t)stream);
+  return after_launch("shard_fetch_finish_table");
+}
+
+mspipe_status mspipe_shard_mitigate(mspipe_memory* st, const mspipe_mitigation* mit, const float* table_mem,
+                                    const double* table_mem_ts, void* stream) {
+  mspipe_status rc = shard_ok(st, "shard_mitigate");
+  if (rc != MSPIPE_OK) return rc;
+  if (!mit || !tcsr_ok(mit->g) || mit->num_events < 0 || !(mit->lambda >= 0.f && mit->lambda <= 1.f) ||
+      mit->n_sim < 0 || mit->n_sim > 16 || mit->fanout < 1 || mit->fanout > 16 ||
+      (mit->num_events > 0 && (!mit->src || !mit->dst || !mit->ts || !mit->out_h || !table_mem || !table_mem_ts)))
+    return fail(MSPIPE_EINVAL, "shard_mitigate: bad arguments");
+  if (mit->num_events == 0) return MSPIPE_OK;
+  launch_mitigate(to_tcsr(mit->g), mit->src, mit->dst, mit->ts, mit->num_events, table_mem, table_mem_ts,
+                  st->mem_dim, mit->lambda, mit->gamma, mit->n_sim, mit->fanout, mit->out_h, mit->out_omega,
+                  mit->out_elig, (cudaStream_t)stream);
+  return after_launch("shard_mitigate");
 }
 
 mspipe_status mspipe_shard_commit_pack(mspipe_memory* st, int64_t commit_version, const int32_t* nodes,

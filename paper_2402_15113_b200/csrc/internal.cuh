@@ -87,6 +87,20 @@ struct Tcsr {
 // (ts is sorted, so the true lanes are a prefix) shrinks the range 33x; a row
 // of L entries costs ceil(log33(L/32)) + 1 dependent rounds instead of log2(L).
 // An id outside [0, N) gives an empty row and raises MSPIPE_DEVERR_RANGE.
+// binary search: first position in row(v) whose ts >= t (A4's per-thread search)
+__device__ __forceinline__ int64_t lower_bound_ts(const Tcsr& g, int32_t v, double t,
+                                                  int64_t* beg_out) {
+  const int64_t beg = __ldg(g.indptr + v);
+  int64_t lo = beg, hi = __ldg(g.indptr + v + 1);
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (__ldg(g.ts + mid) < t) lo = mid + 1;
+    else hi = mid;
+  }
+  *beg_out = beg;
+  return lo;
+}
+
 // ((lane + 1) * span) / 33 without a 64-bit division (~70 instructions on the
 // integer pipe, once per lane per probe round): for products below 2^32 the
 // quotient is umulhi(x, ceil(2^37 / 33)) >> 5, exact for every x < 2^32
@@ -356,6 +370,11 @@ cudaError_t launch_feature_fetch(const int32_t* sub, const int32_t* eid, int64_t
                                  int64_t N, int32_t nstride, const float* efeat, int64_t E, int32_t estride,
                                  float* out_n, float* out_e, cudaStream_t s);
 // stale.cu
+void shard_mit_candidates(const Tcsr& g, const int32_t* src, const int32_t* dst, const double* ts, int64_t B,
+                          const double* root_ts, int64_t root_step, double gamma, int32_t F, int32_t* out_ids,
+                          cudaStream_t s);
+void shard_fetch_finish_table(mspipe_memory* st, const int32_t* ids, int64_t n, float* tab_mem, double* tab_ts,
+                              cudaStream_t s);
 cudaError_t launch_staleness_error(const int32_t* winner, const int32_t* num_unique, int64_t num_events,
                                   const float* rows_a, int64_t stride_a, const float* rows_b, int64_t stride_b,
                                   int32_t mem_dim, double* out, cudaStream_t s);

@@ -133,18 +133,6 @@ struct MitWarpSmem {
   int32_t omega[kMitMaxF];
 };
 
-__device__ __forceinline__ int64_t lower_bound_ts(const Tcsr& g, int32_t v, double t,
-                                                  int64_t* beg_out) {
-  const int64_t beg = __ldg(g.indptr + v);
-  int64_t lo = beg, hi = __ldg(g.indptr + v + 1);
-  while (lo < hi) {
-    const int64_t mid = (lo + hi) >> 1;
-    if (__ldg(g.ts + mid) < t) lo = mid + 1;
-    else hi = mid;
-  }
-  *beg_out = beg;
-  return lo;
-}
 
 __global__ void __launch_bounds__(32 * kMitWarps) k_mitigate(
     Tcsr g, const int32_t* __restrict__ src, const int32_t* __restrict__ dst,

@@ -282,6 +282,83 @@ __global__ void k_shard_merge_apply(const float4* __restrict__ rec, const int32_
   }
 }
 
+// ---- MSPipe-S with sharded memory (A4) ----------------------
+// The mitigation of target w reads S.mem_ts[w], S.mem_ts of its 2-hop
+// candidates and S.mem of the chosen Ω, all owned by other ranks.  After the
+// subgraph fetch (which delivered w's own row and mem_ts as the root row),
+// one warp per target decides eligibility and lists the candidates exactly
+// as k_mitigate enumerates them (the T-CSR is replicated): out_ids[t] =
+// [w, candidates of sample(x, t*) for x in sample(w, t*)] (pads -1), only for
+// eligible targets.  A second fetch of that list fills a node-indexed table
+// from which k_mitigate then runs unchanged.
+__global__ void k_shard_mit_candidates(Tcsr g, const int32_t* __restrict__ src, const int32_t* __restrict__ dst,
+                                       const double* __restrict__ ts, int64_t B, const double* __restrict__ root_ts,
+                                       int64_t root_step, double gamma, int32_t F, int32_t* __restrict__ out_ids) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int32_t L = 1 + F * F;
+  for (int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < 2 * B; t += nwarps) {
+    const int64_t a = t < B ? t : t - B;
+    const int32_t w = t < B ? __ldg(src + a) : __ldg(dst + a);
+    const double tstar = __ldg(ts + a);
+    int32_t* row = out_ids + t * L;
+    const bool wok = w >= 0 && w < g.num_nodes;
+    const bool elig = wok && (tstar - __ldcg(root_ts + t * root_step)) > gamma;  // G11
+    for (int32_t q = lane; q < L; q += 32) row[q] = -1;
+    __syncwarp();
+    if (!elig) continue;
+    if (lane == 0) row[0] = w;
+    int64_t begw;
+    const int64_t endw = lower_bound_ts(g, w, tstar, &begw);
+    const int32_t cntw = (int32_t)min64(endw - begw, (int64_t)F);
+    int32_t x = (lane < cntw) ? __ldg(g.nbr + (endw - 1 - lane)) : -1;
+    if (x == w) x = -1;
+    if (lane < F && x >= 0) {
+      int64_t begx;
+      const int64_t endx = lower_bound_ts(g, x, tstar, &begx);
+      const int32_t cx = (int32_t)min64(endx - begx, (int64_t)F);
+      for (int32_t i = 0; i < cx; ++i) {
+        const int32_t u = __ldg(g.nbr + (endx - 1 - i));
+        row[1 + lane * F + i] = u == w ? -1 : u;
+      }
+    }
+    __syncwarp();
+  }
+}
+
+// rows of a finished fetch written into a node-indexed table (pads skipped;
+// repeated ids write identical rows)
+__global__ void k_shard_finish_table(const int32_t* __restrict__ ids, int64_t n, int64_t N, int32_t G, int64_t cap,
+                                     const int32_t* __restrict__ slot_of, const float4* __restrict__ rep, int32_t Qm,
+                                     int32_t Qa, float4* __restrict__ tab_mem, double* __restrict__ tab_ts) {
+  const int lane = threadIdx.x & 31;
+  const int32_t Qr = Qm + 1 + (Qa > 0 ? Qa + 1 : 0);
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t p = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; p < n; p += nwarps) {
+    const int32_t v = __ldg(ids + p);
+    if (v < 0 || v >= N) continue;
+    const float4* rec = rep + ((int64_t)(v % G) * cap + __ldg(slot_of + v)) * Qr;
+    for (int32_t c = lane; c < Qm; c += 32) tab_mem[(int64_t)v * Qm + c] = __ldcg(rec + c);
+    if (lane == 0) tab_ts[v] = __ldcg(reinterpret_cast<const double2*>(rec) + Qm).x;
+  }
+}
+
+void shard_mit_candidates(const Tcsr& g, const int32_t* src, const int32_t* dst, const double* ts, int64_t B,
+                          const double* root_ts, int64_t root_step, double gamma, int32_t F, int32_t* out_ids,
+                          cudaStream_t s) {
+  k_shard_mit_candidates<<<blocks_for(2 * B * 32, 8), 256, 0, s>>>(g, src, dst, ts, B, root_ts, root_step, gamma,
+                                                                   F, out_ids);
+}
+
+void shard_fetch_finish_table(mspipe_memory* st, const int32_t* ids, int64_t n, float* tab_mem, double* tab_ts,
+                              cudaStream_t s) {
+  const int p = (int)(st->sh_fetch_iter & 1);
+  const int32_t Qm = st->mem_dim / 4, Qa = st->sh_with_mail ? (int32_t)(st->mail_stride / 4) : 0;
+  k_shard_finish_table<<<blocks_for(n * 32, 8), 256, 0, s>>>(
+      ids, n, st->num_nodes, st->world, st->sh_cap, st->sh_slot_of,
+      reinterpret_cast<const float4*>(st->sh_window + st->sh_off_rep[p]), Qm, Qa, (float4*)tab_mem, tab_ts);
+}
+
 // ---- window layout --------------------------------------------------------
 int64_t shard_fetch_rec_bytes(const mspipe_memory* st, bool with_mail) {
   return 16LL * (st->mem_dim / 4 + 1 + (with_mail ? st->mail_stride / 4 + 1 : 0));

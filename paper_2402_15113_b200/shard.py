@@ -45,8 +45,6 @@ class ShardRank(_TimedOps):
 
     def __init__(self, cfg: StageConfig, params: dict, tcsr: _C.TcsrHandle, device, rank: int, world: int,
                  nccl_id: bytes | None = None):
-        if cfg.mitigation:
-            raise NotImplementedError("MSPipe-S mitigation with sharded memory is not in this build")
         self.cfg, self.rank, self.world = cfg, rank, world
         self.device = torch.device(device)
         self.tcsr = tcsr
@@ -57,6 +55,11 @@ class ShardRank(_TimedOps):
             connect_shards(self.memory)
         self.side = None
         self._served = None
+        if cfg.mitigation:  # MSPipe-S (A4): candidate list and a node-indexed table of the fetched rows
+            B, F = cfg.batch, cfg.fanout
+            self.cand = torch.empty((2 * B, 1 + F * F), dtype=torch.int32, device=self.device)
+            self.tab_mem = torch.zeros((cfg.num_nodes, cfg.mem_dim), dtype=torch.float32, device=self.device)
+            self.tab_ts = torch.zeros((cfg.num_nodes,), dtype=torch.float64, device=self.device)
         self.gru = _C.GruHandle(cfg.mem_dim, cfg.edge_dim, cfg.time_dim, params, self.device, cfg.precision,
                                 max_events=cfg.batch)
         self.slots = [_Slot(cfg, self.memory.mail_stride, self.device, False) for _ in range(cfg.k + 1)]
@@ -130,6 +133,29 @@ class ShardRank(_TimedOps):
         ids, mem, mem_ts, mail, mail_ts = self._fetch_out(i)
         self.versions[i] = _C.shard_fetch_finish(self.memory, ids, mem, mem_ts, mail, mail_ts)
 
+    # -- MSPipe-S (A4) with sharded memory: a second fetch of the candidates' rows
+    def _mit(self, i):
+        cfg, sl, x = self.cfg, self._slot(i), self.inputs(i)
+        n = x["src"].numel()
+        m = cfg.mitigation
+        return _C.make_mitigation(self.tcsr, m["lam"], m["gamma"], m["n_sim"], cfg.fanout, x["src"], x["dst"],
+                                  x["ts"], sl.h[: 2 * n], sl.omega[: 2 * n], sl.elig[: 2 * n])
+
+    def mit_plan(self, i):
+        """Candidates of the eligible targets (their roots' mem_ts came with the
+        subgraph fetch), then the fetch plan of that list."""
+        sl = self._slot(i)
+        n = self.inputs(i)["src"].numel()
+        cand = self.cand[: 2 * n]
+        _C.shard_mitigation_candidates(self.memory, self._mit(i), sl.mem_ts, self.cfg.fanout + 1, cand)
+        _C.shard_fetch_plan(self.memory, i, cand.reshape(-1))
+
+    def mit_finish(self, i):
+        """The candidates' rows into the node table, then the blend (k_mitigate)."""
+        n = self.inputs(i)["src"].numel()
+        _C.shard_fetch_finish_table(self.memory, self.cand[: 2 * n].reshape(-1), self.tab_mem, self.tab_ts)
+        _C.shard_mitigate(self.memory, self._mit(i), self.tab_mem, self.tab_ts)
+
     def fetch_collective(self, i):
         """NCCL: plan, all-to-all, serve, all-to-all, finish inside mspipe_memory_fetch."""
         ids, mem, mem_ts, mail, mail_ts = self._fetch_out(i)
@@ -144,10 +170,11 @@ class ShardRank(_TimedOps):
         return upd
 
     def update(self, i):
-        """A5 + A6 for the local winners (rank-local)."""
+        """A5 + A6 for the local winners (rank-local); h = MSPipe-S's blend when mitigating."""
         sl, x = self._slot(i), self.inputs(i)
+        n = x["src"].numel()
         _C.memory_update(self.memory, self.gru, x["src"], x["dst"], x["ts"], x["ef"], sl.mem, sl.mem_ts,
-                         self.cfg.fanout + 1, self._upd(i))
+                         self.cfg.fanout + 1, self._upd(i), snap_h=sl.h[: 2 * n] if sl.h is not None else None)
 
     def commit_pack(self, i):
         _C.shard_commit_pack(self.memory, i, self._upd(i), key_base(i, self.rank, self.world, self.cfg.batch))
@@ -172,6 +199,14 @@ class ShardRank(_TimedOps):
         self._served.record()
         _C.shard_exchange(self.memory, _C.XCHG_FETCH_ROWS)
         self.fetch_finish(i)
+        if self.cfg.mitigation:  # same iteration, same window parity: the barriers above separate the rounds
+            self.mit_plan(i)
+            _C.shard_exchange(self.memory, _C.XCHG_FETCH_IDS)
+            self.fetch_serve()
+            self._served = torch.cuda.Event()
+            self._served.record()
+            _C.shard_exchange(self.memory, _C.XCHG_FETCH_ROWS)
+            self.mit_finish(i)
         self._ev("prep_end")
 
     def commit(self, i, served=None):
@@ -289,6 +324,15 @@ class LoopbackShards:
         self._xchg(_C.XCHG_FETCH_ROWS)
         for r in self.ranks:
             r.fetch_finish(i)
+        if self.cfg.mitigation:
+            for r in self.ranks:
+                r.mit_plan(i)
+            self._xchg(_C.XCHG_FETCH_IDS)
+            for r in self.ranks:
+                r.fetch_serve()
+            self._xchg(_C.XCHG_FETCH_ROWS)
+            for r in self.ranks:
+                r.mit_finish(i)
 
     def commit(self, i):
         for r in self.ranks:
