@@ -41,7 +41,14 @@ constexpr int kBTile = kN * kKC * 4;    // 8 KB
 constexpr int kBBlock = 2 * kBTile;
 constexpr int kStageBytes = kABlock + kBBlock;  // 48 KB
 constexpr int kStages = 3;
-constexpr int kThreads = 128;
+// 8 warps: warp 0 loads, warp 1 issues the MMAs, warps 2..7 prefetch the
+// epilogue's inputs; in the epilogue warps w and w + 4 read the two 32-column
+// halves of the same TMEM lane quarter (w % 4), so the gate math of a tile
+// (expf / tanhf / division chains of 128 rows x 16 units) spreads over 256
+// threads: with 4 warps, one warp per scheduler left every dependent step of
+// those chains exposed (measured: 3.5 of ~15 us per GDELT tile)
+constexpr int kThreads = 256;
+constexpr int kPfThreads = kThreads - 64;  // warps 2..7
 constexpr int kHBufBytes = kM * kJ * 4;   // h rows of the tile's hidden units (prefetched)
 constexpr int kRecvBytes = kM * kN * 4;   // K-split partials received from the cluster (S x 128/S rows)
 constexpr int kSmemBytes =
@@ -731,7 +738,7 @@ __global__ void __launch_bounds__(tc::kThreads, 1) k_gru_tc(TcArgs a) {
   if ((int64_t)blockIdx.y >= tiles) {  // no tile for this cluster (uniform across it)
     if (warp == 0 && lane == 0)
       for (int s = 0; s < pre; ++s) mbar_wait(&full[s], 0u);  // drain the speculative copies
-    if (a.cu.stamp && warp >= 2) catch_up(a, cta_q * 2 + (warp - 2), n_cta * 2, lane);
+    if (a.cu.stamp && warp >= 2) catch_up(a, cta_q * (kPfThreads / 32) + (warp - 2), n_cta * (kPfThreads / 32), lane);
     if (kAsyncPush && S > 1) cluster_wait();
     __syncthreads();
     if (warp == 2) tmem_dealloc(tmem, tcols);
@@ -793,11 +800,11 @@ __global__ void __launch_bounds__(tc::kThreads, 1) k_gru_tc(TcArgs a) {
         // warm the commit epilogue's mail-row slices (staged by k_build_x a step ago) into L2
         const int Q = (int)(a.mail_stride / 4);
         const int cq0 = jt * Q / J, nq = (jt + 1) * Q / J - cq0;
-        for (int mm = rb + (int)threadIdx.x - 64; mm < re; mm += 64)
+        for (int mm = rb + (int)threadIdx.x - 64; mm < re; mm += kPfThreads)
           if (m0 + mm < U && nq > 0)
             l2_prefetch(a.new_mail + ((int64_t)(m0 + mm) * Q + cq0) * 4, (uint32_t)nq * 16u);
       }
-      for (int it = threadIdx.x - 64; it < (re - rb) * (kJ / 4); it += 64) {
+      for (int it = threadIdx.x - 64; it < (re - rb) * (kJ / 4); it += kPfThreads) {
         const int mm = rb + it / (kJ / 4), qq = it % (kJ / 4);
         const int32_t u = m0 + mm, j0 = jt * kJ + qq * 4;
         float4 hv = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -820,8 +827,8 @@ __global__ void __launch_bounds__(tc::kThreads, 1) k_gru_tc(TcArgs a) {
           if (a.res_nodes && jt == 0 && u < U) a.res_nodes[u] = node;
         }
       }
-      for (int i = threadIdx.x - 64; i < kN; i += 64) sbias[i] = __ldg(d.bias + jt * kN + i);
-      if (ti == 0 && a.cu.stamp) catch_up(a, cta_q * 2 + (warp - 2), n_cta * 2, lane);
+      for (int i = threadIdx.x - 64; i < kN; i += kPfThreads) sbias[i] = __ldg(d.bias + jt * kN + i);
+      if (ti == 0 && a.cu.stamp) catch_up(a, cta_q * (kPfThreads / 32) + (warp - 2), n_cta * (kPfThreads / 32), lane);
     }
     __syncwarp();
 
@@ -836,29 +843,27 @@ __global__ void __launch_bounds__(tc::kThreads, 1) k_gru_tc(TcArgs a) {
         for (; pre < nc && pre < kStages; ++pre) load_chunk(ti + 1, (int32_t)(qn / J), (int)(qn % J), pre);
       }
     }
-    const int m = warp * 32 + lane;
-    const uint32_t tbase = tmem + ((uint32_t)(warp * 32) << 16);
-    uint32_t r0[32], r1[32];
+    // thread = (row m of lane quarter warp % 4, column half warp / 4)
+    const int half = warp >> 2;
+    const int m = (warp & 3) * 32 + lane;
+    const uint32_t tbase = tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)(half * 32);
+    uint32_t r0[32];
     MSPIPE_TMEM_LD32(tbase, r0);
-    MSPIPE_TMEM_LD32(tbase + 32, r1);
     tmem_wait_ld();
     for (int bi = 1; bi < (kBf ? 1 : nbuf); ++bi) {
-      uint32_t t0[32], t1[32];
+      uint32_t t0[32];
       MSPIPE_TMEM_LD32(tbase + bi * kN, t0);
-      MSPIPE_TMEM_LD32(tbase + bi * kN + 32, t1);
       tmem_wait_ld();
 #pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        r0[i] = __float_as_uint(__fadd_rn(__uint_as_float(r0[i]), __uint_as_float(t0[i])));
-        r1[i] = __float_as_uint(__fadd_rn(__uint_as_float(r1[i]), __uint_as_float(t1[i])));
-      }
+      for (int i = 0; i < 32; ++i) r0[i] = __float_as_uint(__fadd_rn(__uint_as_float(r0[i]), __uint_as_float(t0[i])));
     }
     PHASE(4);
     const float* bias = sbias;
+    // this thread's half row (8 float4, float4 index half * 8 + c4) goes to
+    // recv[src_rank][m - rb(owner)][16 x float4] of the rank that finalises
+    // row m, float4 index XOR-swizzled by the row so the owner's reads are
+    // conflict-free; S = 1: into this CTA's own buffer
     if (S > 1) {
-      // push this CTA's partial row m into the receive buffer of the rank that
-      // finalises it: recv[src_rank][m - rb(owner)][16 x float4], float4 index
-      // XOR-swizzled by the row so the owner's reads are conflict-free.
       // Fire-and-forget remote stores instead of latency-bound remote loads.
       const int R = kM / S;
       const int owner = m / R, lm = m % R;
@@ -868,51 +873,31 @@ __global__ void __launch_bounds__(tc::kThreads, 1) k_gru_tc(TcArgs a) {
         if (threadIdx.x == 0) mbar_arrive_expect_tx(rfull, (uint32_t)(kM * kN * 4));  // S x R rows x kN floats
         const uint32_t rbar = mapa(smem_u32(rfull), (uint32_t)owner);
 #pragma unroll
-        for (int c4 = 0; c4 < 8; ++c4) {
-          st_async_f4(dst + 16u * (uint32_t)(c4 ^ (lm & 15)), __uint_as_float(r0[4 * c4]),
+        for (int c4 = 0; c4 < 8; ++c4)
+          st_async_f4(dst + 16u * (uint32_t)((half * 8 + c4) ^ (lm & 15)), __uint_as_float(r0[4 * c4]),
                       __uint_as_float(r0[4 * c4 + 1]), __uint_as_float(r0[4 * c4 + 2]), __uint_as_float(r0[4 * c4 + 3]),
                       rbar);
-          st_async_f4(dst + 16u * (uint32_t)((8 + c4) ^ (lm & 15)), __uint_as_float(r1[4 * c4]),
-                      __uint_as_float(r1[4 * c4 + 1]), __uint_as_float(r1[4 * c4 + 2]), __uint_as_float(r1[4 * c4 + 3]),
-                      rbar);
-        }
-      } else
+      } else {
 #pragma unroll
-      for (int c4 = 0; c4 < 8; ++c4) {
-        st_dsmem_f4(dst + 16u * (uint32_t)(c4 ^ (lm & 15)), __uint_as_float(r0[4 * c4]), __uint_as_float(r0[4 * c4 + 1]),
-                    __uint_as_float(r0[4 * c4 + 2]), __uint_as_float(r0[4 * c4 + 3]));
-        st_dsmem_f4(dst + 16u * (uint32_t)((8 + c4) ^ (lm & 15)), __uint_as_float(r1[4 * c4]),
-                    __uint_as_float(r1[4 * c4 + 1]), __uint_as_float(r1[4 * c4 + 2]), __uint_as_float(r1[4 * c4 + 3]));
+        for (int c4 = 0; c4 < 8; ++c4)
+          st_dsmem_f4(dst + 16u * (uint32_t)((half * 8 + c4) ^ (lm & 15)), __uint_as_float(r0[4 * c4]),
+                      __uint_as_float(r0[4 * c4 + 1]), __uint_as_float(r0[4 * c4 + 2]), __uint_as_float(r0[4 * c4 + 3]));
       }
+    } else {
+#pragma unroll
+      for (int c4 = 0; c4 < 8; ++c4)
+        recv[m * (kN / 4) + ((half * 8 + c4) ^ (m & 15))] =
+            make_float4(__uint_as_float(r0[4 * c4]), __uint_as_float(r0[4 * c4 + 1]), __uint_as_float(r0[4 * c4 + 2]),
+                        __uint_as_float(r0[4 * c4 + 3]));
     }
     PHASE(1);
     tc_fence_before();
     __syncthreads();  // hbuf complete; every TMEM read of this tile done (the next tile's MMAs may start)
     PHASE(5);
-    if (S == 1) {
-      const int32_t u = m0 + m;
-      if (u < U) {
-#pragma unroll
-        for (int qq = 0; qq < kJ / 4; ++qq) {
-          const int32_t j0 = jt * kJ + qq * 4;
-          if (j0 >= d.M) break;
-          float pr[4], pz[4], pnx[4], pnh[4];
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const int jj = qq * 4 + e;
-            pr[e] = __uint_as_float(r0[jj]) + bias[jj];
-            pz[e] = __uint_as_float(r0[kJ + jj]) + bias[kJ + jj];
-            pnx[e] = __uint_as_float(r1[jj]) + bias[2 * kJ + jj];
-            pnh[e] = __uint_as_float(r1[kJ + jj]) + bias[3 * kJ + jj];
-          }
-          store_h4(a, u, rownode[m], j0, gates4(pr, pz, pnx, pnh, hbuf[m * (kJ / 4) + qq], d.cell));
-        }
-      }
-      if (a.commit_mem && !a.skip_meta) commit_rows(a, m0, U, 0, kM, jt, J, rownode);
-    } else {
-      if (kAsyncPush) {
+    {
+      if (S > 1 && kAsyncPush) {
         mbar_wait_cluster(rfull, (uint32_t)(ti & 1));  // all S x R partial rows have landed
-      } else {
+      } else if (S > 1) {
 #ifdef MSPIPE_PHASES
         asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
         PHASE(7);
