@@ -435,8 +435,8 @@ MSPIPE_API mspipe_status mspipe_gru_apply_commit_out(const mspipe_gru* gru, mspi
  * candidates' mem_ts and the Ω rows belong to other ranks.  After the
  * subgraph fetch of iteration i (which brought each target's own row and
  * mem_ts as its root row), mspipe_shard_mitigation_candidates lists, for
- * every eligible target t (Δ = t* − S.mem_ts[w] > γ, G11), [w, the distinct
- * ids of sample(x, t*) \ {w} for x in sample(w, t*) \ {w}] into out_ids
+ * every target t, w and, if t is eligible (Δ = t* − S.mem_ts[w] > γ, G11),
+ * the ids of sample(x, t*) \ {w} for x in sample(w, t*) \ {w} into out_ids
  * [2B, 1 + fanout²] (pads −1; the T-CSR is replicated); a second fetch of
  * that list (plan -> exchange -> serve -> exchange ->
  * mspipe_shard_fetch_finish_table) writes those rows into a node-indexed

@@ -1075,9 +1075,10 @@ int gru_tc_splits(int64_t max_rows, const GruDesc& d, bool shared_buffers) {
   // tf32: one TMEM buffer per chunk; bf16: a single accumulator, no minimum
   int64_t s_min = d.bf16 ? 1 : (nchunks + kMaxChunks - 1) / kMaxChunks;
   if (forced > 0) return forced;  // below s_min the chunks share TMEM buffers (TcArgs::cpb)
-  // big batches (GDELT's 2B = 8000): S = 2 with two K chunks per TMEM buffer
-  // (measured 54.5 vs 56.4 us per GDELT step; wiki-sized batches keep S = 4)
-  if (shared_buffers && !d.bf16 && max_rows >= 4096 && env_int("MSPIPE_TC_BIG_S2", 1)) return 2;
+  // big batches (GDELT's 2B = 8000, ~13 M tiles x 7 hidden tiles): S = 1, the
+  // 91 tiles in one wave of CTAs, three K chunks per TMEM buffer (measured with
+  // the 8-warp epilogue: 42.6 / 47.7 / 52.3 us per GDELT step at S = 1 / 2 / 4)
+  if (shared_buffers && !d.bf16 && max_rows >= 4096) return env_int("MSPIPE_TC_BIG_S", 1);
   const int64_t tiles = ((max_rows + tc::kM - 1) / tc::kM) * gru_tc_jtiles(d);
   int64_t s = 1;
   while (s < 8 && tiles * s * 2 <= 2 * (int64_t)num_sms() && s * 2 <= nchunks / 2) s *= 2;

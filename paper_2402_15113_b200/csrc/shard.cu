@@ -288,8 +288,9 @@ __global__ void k_shard_merge_apply(const float4* __restrict__ rec, const int32_
 // subgraph fetch (which delivered w's own row and mem_ts as the root row),
 // one warp per target decides eligibility and lists the candidates exactly
 // as k_mitigate enumerates them (the T-CSR is replicated): out_ids[t] =
-// [w, candidates of sample(x, t*) for x in sample(w, t*)] (pads -1), only for
-// eligible targets.  A second fetch of that list fills a node-indexed table
+// [w, candidates of sample(x, t*) for x in sample(w, t*)] (pads -1; the
+// candidates only for eligible targets, w for every target: k_mitigate reads
+// S.mem_ts[w] and, ineligible, S.mem[w]).  A second fetch of that list fills a node-indexed table
 // from which k_mitigate then runs unchanged.
 __global__ void k_shard_mit_candidates(Tcsr g, const int32_t* __restrict__ src, const int32_t* __restrict__ dst,
                                        const double* __restrict__ ts, int64_t B, const double* __restrict__ root_ts,
@@ -304,10 +305,9 @@ __global__ void k_shard_mit_candidates(Tcsr g, const int32_t* __restrict__ src, 
     int32_t* row = out_ids + t * L;
     const bool wok = w >= 0 && w < g.num_nodes;
     const bool elig = wok && (tstar - __ldcg(root_ts + t * root_step)) > gamma;  // G11
-    for (int32_t q = lane; q < L; q += 32) row[q] = -1;
+    for (int32_t q = lane; q < L; q += 32) row[q] = (q == 0 && wok) ? w : -1;  // k_mitigate reads every w
     __syncwarp();
     if (!elig) continue;
-    if (lane == 0) row[0] = w;
     int64_t begw;
     const int64_t endw = lower_bound_ts(g, w, tstar, &begw);
     const int32_t cntw = (int32_t)min64(endw - begw, (int64_t)F);
