@@ -31,7 +31,7 @@ OPS = {"sample": ["k_sample_recent"], "dedup": ["k_dedup"], "fetch": ["k_fetch_g
 # fused step (StageConfig.use_fused): prep = k_prep, build = k_build_x, update = k_gru_tc with the commit
 OPS_FUSED = {"prep": ["k_prep"], "build": ["k_build_x"], "update": ["k_gru_tc"]}
 SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "B": 1, "KB": 1e3, "MB": 1e6, "GB": 1e9,
-         "nsecond": 1, "usecond": 1e3, "msecond": 1e6, "second": 1e9}
+         "nsecond": 1, "usecond": 1e3, "msecond": 1e6, "second": 1e9, "ns": 1, "us": 1e3, "ms": 1e6}
 
 
 def raw(rep):
