@@ -12,7 +12,7 @@
 //  k_build_x — one warp per (winner row, 32-wide K chunk): gathers the message
 //    x = [s_w | s_o | e | cos(w dt + p) | h] (A5, fused time encoding) from
 //    the snapshot rows, writes the A operand as ready-to-copy SWIZZLE_128B
-//    K-major fp32 images per (128-row tile, chunk), and the mail row and
+//    K-major images (hi | lo) per (128-row tile, chunk), and the mail row and
 //    commit timestamp of the winner (G14).  Thousands of warps hide the
 //    gather latency that a per-CTA producer could not.
 //  k_gru_tc — CTA = 128 rows x 16 hidden units (N = 64 accumulator columns)
@@ -98,13 +98,6 @@ __device__ __forceinline__ void bulk_g2s(void* smem_dst, const void* gsrc, uint3
           smem_u32(smem_dst)),
       "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
-}
-// generic-proxy shared-memory writes made visible to the async proxy (tcgen05.mma operands)
-__device__ __forceinline__ void fence_proxy_async_smem() {
-  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
 }
 __device__ __forceinline__ void tc_fence_before() {
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
@@ -338,7 +331,7 @@ size_t gru_tc_packed_floats(const GruDesc& d) {
 size_t gru_tc_xbuf_floats(const GruDesc& d, int64_t max_events) {
   const int64_t mtiles = (2 * max_events + tc::kM - 1) / tc::kM;
   if (d.bf16) return (size_t)mtiles * (d.Kpad / tc::kKC16) * (tc::kABlock16 / 4);
-  return (size_t)mtiles * (d.Kpad / tc::kKC) * (tc::kATile / 4);
+  return (size_t)mtiles * (d.Kpad / tc::kKC) * (tc::kABlock / 4);
 }
 
 void launch_gru_pack_tc(const float* w_ih, const float* w_hh, const float* b_ih, const float* b_hh,
@@ -550,8 +543,11 @@ __global__ void __launch_bounds__(256) k_build_x(TcArgs a) {
     for (int q = 0; q < kBuildChunks; ++q) {
       const int32_t c = cg * kBuildChunks + q;
       if (c >= nchunks) break;
-      char* blk = reinterpret_cast<char*>(a.xbuf) + ((int64_t)mt * nchunks + c) * tc::kATile;
-      *reinterpret_cast<float*>(blk + off) = v[q];  // fp32: k_gru_tc forms the tf32 hi | lo on chip
+      const float hi = tc::tf32_rna(v[q]);
+      const float lo = tc::tf32_rna(v[q] - hi);
+      char* blk = reinterpret_cast<char*>(a.xbuf) + ((int64_t)mt * nchunks + c) * tc::kABlock;
+      *reinterpret_cast<float*>(blk + off) = hi;
+      *reinterpret_cast<float*>(blk + tc::kATile + off) = lo;
     }
   }
 }
@@ -662,11 +658,7 @@ template <bool kBf>
 __global__ void __launch_bounds__(tc::kThreads, 1) k_gru_tc(TcArgs a) {
   using namespace tc;
   constexpr int SB = kBf ? kStageBytes16 : kStageBytes;
-  // tf32: the A chunk arrives as one fp32 image (kATile) into the stage's hi
-  // slot and warps 2..7 split it on chip into hi | lo (half the bytes of the
-  // materialised hi | lo images through L2); bf16: split images from k_build_x
-  constexpr int AB = kBf ? kABlock16 : kATile;   // bytes of an A chunk in global memory
-  constexpr int AS = kBf ? kABlock16 : kABlock;  // bytes of the A part of a stage
+  constexpr int AB = kBf ? kABlock16 : kABlock;
   constexpr int BB = kBf ? kBBlock16 : kBBlock;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -675,7 +667,6 @@ __global__ void __launch_bounds__(tc::kThreads, 1) k_gru_tc(TcArgs a) {
   uint64_t* acc_full = empty + kStages;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 1);
   uint64_t* rfull = acc_full + 2;  // K-split partials of the tile received (st.async bytes)
-  uint64_t* conv = rfull + 1;      // [kStages] tf32: the stage's A chunk is split into hi | lo
   int32_t* rownode = reinterpret_cast<int32_t*>(smem + kStages * SB + 512);  // [128] node of each row
   float4* hbuf = reinterpret_cast<float4*>(smem + kStages * SB + 1024);  // [128 rows][kJ/4]
   float4* recv2 = reinterpret_cast<float4*>(smem + kStages * SB + 1024 + kHBufBytes);  // [2][kRecvBytes]
@@ -706,7 +697,6 @@ __global__ void __launch_bounds__(tc::kThreads, 1) k_gru_tc(TcArgs a) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
-      mbar_init(&conv[s], kPfThreads / 32);  // one arrive per converter warp
     }
     mbar_init(acc_full, 1);
     mbar_init(rfull, 1);
@@ -730,9 +720,9 @@ __global__ void __launch_bounds__(tc::kThreads, 1) k_gru_tc(TcArgs a) {
     const uint32_t ph = (uint32_t)(g / kStages) & 1u;
     mbar_wait(&empty[s], ph ^ 1u);
     uint8_t* st = smem + s * SB;
-    mbar_arrive_expect_tx(&full[s], AB + BB);
+    mbar_arrive_expect_tx(&full[s], SB);
     bulk_g2s(st, reinterpret_cast<const char*>(a.xbuf) + ((int64_t)mt_l * nchunks + c0 + ci) * AB, AB, &full[s]);
-    bulk_g2s(st + AS, reinterpret_cast<const char*>(a.wtc) + ((int64_t)jt_l * nchunks + c0 + ci) * BB, BB, &full[s]);
+    bulk_g2s(st + AB, reinterpret_cast<const char*>(a.wtc) + ((int64_t)jt_l * nchunks + c0 + ci) * BB, BB, &full[s]);
   };
   // the cluster's first tile (q = blockIdx.y) is issued before U is known: the
   // workspace holds every M tile of the 2B bound, so the reads are in bounds
@@ -772,12 +762,12 @@ __global__ void __launch_bounds__(tc::kThreads, 1) k_gru_tc(TcArgs a) {
         const int64_t g = ti * nc + ci;
         const int s = (int)(g % kStages);
         const uint32_t ph = (uint32_t)(g / kStages) & 1u;
-        mbar_wait(kBf ? &full[s] : &conv[s], ph);
+        mbar_wait(&full[s], ph);
         tc_fence_after();
         const uint32_t base = smem_u32(smem + s * SB);
         if (kBf) {  // 4 k-steps of K = 16 (32 B along K), 3 split MMAs each, into the single accumulator
           const uint64_t da_hi = sw128_desc(base), da_lo = sw128_desc(base + kATile16);
-          const uint64_t db_hi = sw128_desc(base + AS), db_lo = sw128_desc(base + AS + kBTile16);
+          const uint64_t db_hi = sw128_desc(base + AB), db_lo = sw128_desc(base + AB + kBTile16);
 #pragma unroll
           for (int kk = 0; kk < kKC16 / 16; ++kk) {
             const uint64_t adv = (uint64_t)(kk * 32) >> 4;
@@ -838,31 +828,6 @@ __global__ void __launch_bounds__(tc::kThreads, 1) k_gru_tc(TcArgs a) {
         }
       }
       for (int i = threadIdx.x - 64; i < kN; i += kPfThreads) sbias[i] = __ldg(d.bias + jt * kN + i);
-      if (!kBf) {
-        // tf32 operand split of every K chunk of this tile, in ring order:
-        // a_hi = rna_tf32(a), a_lo = rna_tf32(a - a_hi) (the values k_build_x
-        // used to write as two images), hi in place, lo into the lo slot
-        for (int ci = 0; ci < nc; ++ci) {
-          const int64_t g = ti * nc + ci;
-          const int s = (int)(g % kStages);
-          mbar_wait(&full[s], (uint32_t)(g / kStages) & 1u);
-          float4* ahi = reinterpret_cast<float4*>(smem + s * SB);
-          float4* alo = reinterpret_cast<float4*>(smem + s * SB + kATile);
-          for (int q = threadIdx.x - 64; q < kATile / 16; q += kPfThreads) {
-            const float4 v = ahi[q];
-            float4 h, l;
-            h.x = tf32_rna(v.x); l.x = tf32_rna(v.x - h.x);
-            h.y = tf32_rna(v.y); l.y = tf32_rna(v.y - h.y);
-            h.z = tf32_rna(v.z); l.z = tf32_rna(v.z - h.z);
-            h.w = tf32_rna(v.w); l.w = tf32_rna(v.w - h.w);
-            ahi[q] = h;
-            alo[q] = l;
-          }
-          fence_proxy_async_smem();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&conv[s]);
-        }
-      }
       if (ti == 0 && a.cu.stamp) catch_up(a, cta_q * (kPfThreads / 32) + (warp - 2), n_cta * (kPfThreads / 32), lane);
     }
     __syncwarp();

@@ -24,11 +24,14 @@ __host__ __device__ __forceinline__ uint32_t sw128_off(uint32_t row, uint32_t k)
   return row * 128u + ((((k >> 2) ^ (row & 7u)) & 7u) << 4) + (k & 3u) * 4u;
 }
 
-// A operand of GEMM row u, column k = value v: one fp32 image per (128-row
-// tile, 32-wide K chunk); k_gru_tc splits it into tf32 hi | lo on chip
+// A operand of GEMM row u, column k = value v, split hi | lo
 __device__ __forceinline__ void store_a(float* xbuf, int32_t nchunks, int32_t u, int32_t k, float v) {
-  char* blk = reinterpret_cast<char*>(xbuf) + ((int64_t)(u / kM) * nchunks + k / kKC) * kATile;
-  *reinterpret_cast<float*>(blk + sw128_off((uint32_t)(u % kM), (uint32_t)(k % kKC))) = v;
+  const float hi = tf32_rna(v);
+  const float lo = tf32_rna(v - hi);
+  char* blk = reinterpret_cast<char*>(xbuf) + ((int64_t)(u / kM) * nchunks + k / kKC) * kABlock;
+  const uint32_t off = sw128_off((uint32_t)(u % kM), (uint32_t)(k % kKC));
+  *reinterpret_cast<float*>(blk + off) = hi;
+  *reinterpret_cast<float*>(blk + kATile + off) = lo;
 }
 
 // bf16 operands (MSPIPE_BF16): one 128 B swizzle row holds 64 bf16 = one K chunk
