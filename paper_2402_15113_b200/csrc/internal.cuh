@@ -145,17 +145,9 @@ __device__ __forceinline__ int64_t warp_recent_end(const Tcsr& g, int32_t v, dou
 // at most 32 entries (most rows) costs one dependent round less than
 // warp_recent_end followed by the loads; entries below the last window (a long
 // row whose F most recent straddle it) are loaded directly.
-// hint (nullable, [num_nodes]): per node a position near the previous answer
-// (the stage's queries move forward in time, so the next answer is usually a
-// few entries later).  One round of 32 galloping probes around it (offsets
-// +-1, 2, 4, ... 2^15, mostly L2-resident lines the previous batch touched)
-// brackets the answer before the 33-ary search, which then needs one or two
-// rounds instead of log33(row); the result does not depend on the hint (any
-// position is a valid start), and the warp stores its answer back as the next
-// hint (racing stores all write valid positions).
 __device__ __forceinline__ int64_t warp_recent_sample(const Tcsr& g, int32_t v, double tq, int lane, int F,
                                                       int64_t* beg_out, int32_t* nbr_out, int32_t* eid_out,
-                                                      double* ts_out, int64_t* hint = nullptr) {
+                                                      double* ts_out) {
   *nbr_out = -1;
   *eid_out = -1;
   *ts_out = 0.0;
@@ -166,24 +158,6 @@ __device__ __forceinline__ int64_t warp_recent_sample(const Tcsr& g, int32_t v, 
   }
   const int64_t beg = __ldg(g.indptr + v);
   int64_t lo = beg, hi = __ldg(g.indptr + v + 1);
-  if (hint && hi - lo > 32) {
-    int64_t h = __ldcg(hint + v);
-    h = h < lo ? lo : (h > hi ? hi : h);
-    // lanes 0..15 probe h + 2^l - 1, lanes 16..31 probe h - 2^(l-16)
-    const int64_t p = lane < 16 ? h + ((int64_t(1) << lane) - 1) : h - (int64_t(1) << (lane - 16));
-    const bool in = p >= lo && p < hi;
-    const bool below = in && __ldg(g.ts + p) < tq;
-    int64_t lo_c = below ? p + 1 : lo;           // every probe below t_q raises lo
-    int64_t hi_c = (in && !below) ? p : hi;      // every probe at or above t_q lowers hi
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const int64_t a = __shfl_xor_sync(0xffffffffu, lo_c, o), b = __shfl_xor_sync(0xffffffffu, hi_c, o);
-      lo_c = a > lo_c ? a : lo_c;
-      hi_c = b < hi_c ? b : hi_c;
-    }
-    lo = lo_c;
-    hi = hi_c;
-  }
   while (hi - lo > 32) {
     const int64_t span = hi - lo;
     const int64_t p = lo + probe_offset33(lane, span);
@@ -216,7 +190,102 @@ __device__ __forceinline__ int64_t warp_recent_sample(const Tcsr& g, int32_t v, 
       *ts_out = __ldg(g.ts + e);
     }
   }
-  if (hint && lane == 0) hint[v] = end;
+  *beg_out = beg;
+  return end;
+}
+
+// warp_recent_sample with a per-node hint (k_prep; hint[v] = the answer of
+// node v's previous query, stored back by every warp; any value is a valid
+// start, so results never depend on it).  The stage's queries move forward in
+// time and a node's answer moves only when it had events since, so most
+// queries land on or just after the hint.  Round 1 loads, per lane, one entry
+// of the window [w0, w0 + 32), w0 = max(beg, h - F) — the F entries below the
+// hint and 32 - F after it, with their nbr / eid — and one galloping probe at
+// h + 2^l - 1 (lanes 0..15) or h - 2^(l-16) (lanes 16..31).  If the answer
+// falls inside the window (a hit: the common case), the window also holds
+// the F most recent entries and the query costs ONE dependent round instead
+// of the gallop + search + window + tail rounds; otherwise the window and the
+// probes bracket the answer for the 33-ary search, which stops once one
+// final window [lo - F, lo - F + 32) covers both the count and the outputs.
+__device__ __forceinline__ int64_t warp_recent_sample_hinted(const Tcsr& g, int32_t v, double tq, int lane, int F,
+                                                             int64_t* beg_out, int32_t* nbr_out, int32_t* eid_out,
+                                                             double* ts_out, int64_t* hint) {
+  *nbr_out = -1;
+  *eid_out = -1;
+  *ts_out = 0.0;
+  if (v < 0 || v >= g.num_nodes) {
+    if (lane == 0) raise_dev(MSPIPE_DEVERR_RANGE);
+    *beg_out = 0;
+    return 0;
+  }
+  const int64_t beg = __ldg(g.indptr + v), rend = __ldg(g.indptr + v + 1);
+  int64_t h = __ldcg(hint + v);
+  h = h < beg ? beg : (h > rend ? rend : h);
+  int64_t w0 = h - F < beg ? beg : h - F;
+  // round 1: window entry + galloping probe, all independent loads
+  int64_t q = w0 + lane;
+  bool qin = q < rend;
+  double ts_q = qin ? __ldg(g.ts + q) : 0.0;
+  int32_t nb_q = qin ? __ldg(g.nbr + q) : -1;
+  int32_t ei_q = qin ? __ldg(g.eid + q) : -1;
+  const int64_t p = lane < 16 ? h + ((int64_t(1) << lane) - 1) : h - (int64_t(1) << (lane - 16));
+  const bool pin = p >= beg && p < rend;
+  const bool pbelow = pin && __ldg(g.ts + p) < tq;
+  int c = __popc(__ballot_sync(0xffffffffu, qin && ts_q < tq));  // below-t_q entries: a prefix of the window
+  const int nin = (int)min64(32, rend - w0);
+  int64_t end;
+  if (c < nin && (c > 0 || w0 == beg)) {
+    end = w0 + c;  // hit: entry w0 + c is the first at or after t_q, everything before it is below
+  } else if (c == nin && w0 + 32 >= rend) {
+    end = rend;    // the rest of the row is below t_q
+  } else {
+    // miss: bracket with the window (c == 0: the answer is below w0; c == 32: above the window) and the probes
+    int64_t lo = c == 0 ? beg : w0 + 32, hi = c == 0 ? w0 : rend;
+    int64_t lo_c = pbelow ? p + 1 : lo, hi_c = (pin && !pbelow) ? p : hi;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const int64_t a = __shfl_xor_sync(0xffffffffu, lo_c, o), b = __shfl_xor_sync(0xffffffffu, hi_c, o);
+      lo_c = a > lo_c ? a : lo_c;
+      hi_c = b < hi_c ? b : hi_c;
+    }
+    lo = lo_c > lo ? lo_c : lo;
+    hi = hi_c < hi ? hi_c : hi;
+    while (hi - lo > 32 - F) {
+      const int64_t span = hi - lo;
+      const int64_t pp = lo + probe_offset33(lane, span);
+      const bool below = __ldg(g.ts + pp) < tq;
+      const int cc = __popc(__ballot_sync(0xffffffffu, below));
+      const int64_t plast = __shfl_sync(0xffffffffu, pp, cc > 0 ? cc - 1 : 0);
+      const int64_t pfirst = __shfl_sync(0xffffffffu, pp, cc < 32 ? cc : 31);
+      if (cc > 0) lo = plast + 1;
+      if (cc < 32) hi = pfirst;
+    }
+    // final window: the count over [lo, hi) and the F entries below the answer
+    w0 = lo - F < beg ? beg : lo - F;
+    q = w0 + lane;
+    qin = q < rend;
+    ts_q = qin ? __ldg(g.ts + q) : 0.0;
+    nb_q = qin ? __ldg(g.nbr + q) : -1;
+    ei_q = qin ? __ldg(g.eid + q) : -1;
+    end = lo + __popc(__ballot_sync(0xffffffffu, q >= lo && q < hi && ts_q < tq));
+  }
+  const int64_t e = end - 1 - lane;  // this lane's output slot s = lane
+  const int src_lane = (int)(e - w0);
+  const int32_t nb_s = __shfl_sync(0xffffffffu, nb_q, src_lane & 31);
+  const int32_t ei_s = __shfl_sync(0xffffffffu, ei_q, src_lane & 31);
+  const double ts_s = __shfl_sync(0xffffffffu, ts_q, src_lane & 31);
+  if (lane < F && e >= beg) {
+    if (e >= w0) {
+      *nbr_out = nb_s;
+      *eid_out = ei_s;
+      *ts_out = ts_s;
+    } else {  // a hit below a hint that ran ahead (e.g. after an epoch reset)
+      *nbr_out = __ldg(g.nbr + e);
+      *eid_out = __ldg(g.eid + e);
+      *ts_out = __ldg(g.ts + e);
+    }
+  }
+  if (lane == 0) hint[v] = end;
   *beg_out = beg;
   return end;
 }

@@ -140,7 +140,8 @@ __global__ void __launch_bounds__(kPrepThreads, MSPIPE_PREP_MINB) k_prep(PrepArg
     int64_t beg;
     int32_t nbs, eis;
     double tss;
-    const int64_t end = warp_recent_sample(a.g, v, tq, lane, F, &beg, &nbs, &eis, &tss, a.hint);
+    const int64_t end = a.hint ? warp_recent_sample_hinted(a.g, v, tq, lane, F, &beg, &nbs, &eis, &tss, a.hint)
+                               : warp_recent_sample(a.g, v, tq, lane, F, &beg, &nbs, &eis, &tss);
     const int32_t cnt = (int32_t)min64(end - beg, (int64_t)F);
     // A1 outputs; lane s < F = slot s (newest first); lane s in [1, F] also holds subgraph id s
     if (lane < F) {

@@ -199,14 +199,21 @@ def _subgraph_rows(dev, w, g, k, db, mit):
                 n = min(B, len(w["src"]) - (i - 1) * B)
                 m = 3 * n * (F + 1)
                 got[i] = (sl.samp["sub"][: 3 * n].cpu().numpy().reshape(-1), sl.mem[:m].cpu().numpy(),
-                          sl.mem_ts[:m].cpu().numpy())
+                          sl.mem_ts[:m].cpu().numpy(),
+                          {kk: sl.samp[kk][: 3 * n].cpu().numpy() for kk in ("nbr", "eid", "ts", "dt", "cnt")})
     torch.cuda.synchronize()
     _C.check()
     _, vers, dump = oracle.run_stream(cfg.num_nodes, w["src"], w["dst"], w["ts"], w["ef"], w["params"], B, k,
                                       mitigation=mit, fanout=F, neg=w["neg"], dump_batches=want)
     worst = 0.0
+    og = oracle.Graph(cfg.num_nodes, w["src"], w["dst"], w["ts"])
     for q, i in enumerate(dump["batches"]):
-        ids, rows, mts = got[int(i)]
+        ids, rows, mts, samp = got[int(i)]
+        j0, j1 = (int(i) - 1) * B, min(int(i) * B, len(w["src"]))
+        roots = np.concatenate([w["src"][j0:j1], w["dst"][j0:j1], w["neg"][j0:j1]])
+        sref = og.sample(roots, np.concatenate([w["ts"][j0:j1]] * 3), F)  # A1 of the fused prep (hinted search)
+        for kk in ("nbr", "eid", "ts", "dt", "cnt"):
+            assert np.array_equal(samp[kk], sref[kk]), (i, kk)
         m = len(ids)
         assert np.array_equal(ids, dump["sub_ids"][q][:m]), i
         assert np.array_equal(mts, dump["mem_ts"][q][:m]), i
