@@ -164,7 +164,7 @@ def test_subgraph_rows_equal_oracle_snapshot(dev, name, E, k):
     if k >= 1:
         b = _subgraph_rows(dev, w, g, k, True, _mit(w))
         for i in a:
-            for x, y in zip(a[i], b[i]):
+            for x, y in zip(a[i][:3], b[i][:3]):  # ids, rows, mem_ts
                 assert np.array_equal(x, y), i
 
 
