@@ -10,20 +10,22 @@ import numpy as np, torch
 from paper_2402_15113_b200 import MemoryStage, StageConfig, _C, build_tcsr
 from synth import make_workload
 name = sys.argv[1] if len(sys.argv) > 1 else "wiki"
-w = make_workload(name, num_events=60000)
+w = make_workload(name, num_events=int(os.environ.get("EXP_EVENTS", "200000" if name == "gdelt" else "60000")),
+                  tcsr_events=None if not os.environ.get("EXP_FULL") else 10 ** 12)
 cfg = w["cfg"]
 dev = torch.device("cuda:0")
-g = build_tcsr(cfg.num_nodes, w["src"], w["dst"], w["ts"], dev)
+g = build_tcsr(cfg.num_nodes, *w.get("tcsr", (w["src"], w["dst"], w["ts"])), dev)
+w.pop("tcsr", None)
 st = MemoryStage(StageConfig(cfg.num_nodes, 100, cfg.edge_dim, 100, 10, cfg.batch, cfg.staleness_k), w["params"], g, dev)
 t = {k: torch.from_numpy(w[k]).to(dev) for k in ("src", "dst", "ts", "neg", "ef")}
 st.bind_resident(t["src"], t["dst"], t["ts"], t["neg"], t["ef"])
 ops = st.step_ops()
 L = ctypes.CDLL(dbg)
-for i in range(20):
+for i in range(10):
     st.run_ops(ops[i])
 torch.cuda.synchronize()
 L.mspipe_debug_prep_phases(None, 0, 1)
-st.run_ops(ops[20])
+st.run_ops(ops[10])
 torch.cuda.synchronize()
 buf = np.zeros((8192, 6), np.uint64)
 L.mspipe_debug_prep_phases(buf.ctypes.data_as(ctypes.c_void_p), 8192, 0)
