@@ -5,7 +5,7 @@
 // warp-aggregated atomicMax of p into a node table (__match_any_sync groups
 // equal nodes, so a hot node costs one atomic per warp; max is
 // order-independent, hence deterministic).  Phase 2: a pair wins iff
-// table[node_p] == p; a block scan over contiguous chunks compacts the
+// table[node_p] == p; one scan of per-(round, warp) counts compacts the
 // winners in p order.  With kSmem the table lives in shared memory (N <=
 // kDedupSmemNodes); otherwise in a self-cleaning global scratch (phase 3 resets
 // the touched entries to -1).
@@ -21,83 +21,104 @@ __device__ __forceinline__ void block_dedup(const int32_t* __restrict__ src, con
                                             int64_t B, int32_t* __restrict__ gscratch, int32_t* sscratch,
                                             int64_t N, int32_t* __restrict__ out_nodes,
                                             int32_t* __restrict__ out_winner, int32_t* __restrict__ out_num) {
-  __shared__ int32_t warp_tot[32];
+  // Pairs are visited in rounds r: thread tid takes p = r * NT + tid, so every
+  // load is coalesced and a thread's kR node ids stay in registers for both
+  // phases (round 2 kept a contiguous chunk per thread: its phase-2 loads were
+  // strided and sequential, 22 us for GDELT's 8,000 pairs).  p order = (round,
+  // warp, lane) order, so one exclusive scan of the per-(round, warp) winner
+  // counts gives every winner its place in p order.
+  constexpr int kR = 32;  // caller guarantees 2B <= 32 * NT
+  constexpr int kW = NT / 32;
+  __shared__ int32_t cnt_s[kR * kW];
   __shared__ int32_t total_s;
   int32_t* scratch = kSmem ? sscratch : gscratch;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   if (kSmem) {
     for (int64_t i = tid; i < N; i += NT) sscratch[i] = -1;
-    __syncthreads();
   }
   const int64_t P = 2 * B;
-  const int64_t Pr = (P + NT - 1) / NT * NT;
-  for (int64_t p = tid; p < Pr; p += NT) {
-    int32_t node = -1;
-    if (p < P) {
-      node = (p & 1) ? __ldg(dst + (p >> 1)) : __ldg(src + (p >> 1));
-      if (node < 0 || node >= N) {
+  const int R = (int)((P + NT - 1) / NT);
+  int32_t node[kR];
+#pragma unroll
+  for (int r = 0; r < kR; ++r) {
+    const int64_t p = (int64_t)r * NT + tid;
+    int32_t v = -1;
+    if (r < R && p < P) {
+      v = (p & 1) ? __ldg(dst + (p >> 1)) : __ldg(src + (p >> 1));
+      if (v < 0 || v >= N) {
         raise_dev(MSPIPE_DEVERR_RANGE);
-        node = -1;
+        v = -1;
       }
     }
-    const unsigned grp = __match_any_sync(0xffffffffu, node);
-    const int leader = 31 - __clz(grp);  // highest lane = largest p of the group
-    if (node >= 0 && lane == leader) atomicMax(scratch + node, (int32_t)p);
+    node[r] = v;
+  }
+  if (kSmem) __syncthreads();  // the table is cleared
+  // phase 1: warp-aggregated atomicMax of p per node (the highest lane of a
+  // group of equal nodes holds the group's largest p)
+#pragma unroll
+  for (int r = 0; r < kR; ++r) {
+    if (r >= R) break;  // uniform over the block
+    const unsigned grp = __match_any_sync(0xffffffffu, node[r]);
+    const int leader = 31 - __clz(grp);
+    if (node[r] >= 0 && lane == leader) atomicMax(scratch + node[r], (int32_t)((int64_t)r * NT + tid));
   }
   if (!kSmem) __threadfence();
   __syncthreads();
-  const int64_t C = (P + NT - 1) / NT;  // <= 32: caller guarantees 2B <= 32 * NT
-  const int64_t p0 = tid * C;
+  // phase 2: a pair wins iff the table holds its p; per-(round, warp) counts
   uint32_t flags = 0;
-  int32_t cnt = 0;
-  for (int64_t i = 0; i < C; ++i) {
-    const int64_t p = p0 + i;
-    if (p >= P) break;
-    const int32_t node = (p & 1) ? __ldg(dst + (p >> 1)) : __ldg(src + (p >> 1));
-    if (node < 0 || node >= N) continue;
-    const int32_t w = kSmem ? sscratch[node] : __ldcg(gscratch + node);
-    if (w == (int32_t)p) {
-      flags |= 1u << i;
-      ++cnt;
-    }
-  }
-  int32_t incl = cnt;  // block exclusive scan of cnt
 #pragma unroll
-  for (int d = 1; d < 32; d <<= 1) {
-    const int32_t y = __shfl_up_sync(0xffffffffu, incl, d);
-    if (lane >= d) incl += y;
+  for (int r = 0; r < kR; ++r) {
+    if (r >= R) break;
+    const int32_t p = (int32_t)((int64_t)r * NT + tid);
+    const bool win = node[r] >= 0 && (kSmem ? sscratch[node[r]] : __ldcg(gscratch + node[r])) == p;
+    flags |= (win ? 1u : 0u) << r;
+    const unsigned b = __ballot_sync(0xffffffffu, win);
+    if (lane == 0) cnt_s[r * kW + wid] = __popc(b);
   }
-  if (lane == 31) warp_tot[wid] = incl;
   __syncthreads();
-  if (wid == 0) {
-    const int32_t v = lane < NT / 32 ? warp_tot[lane] : 0;
-    int32_t vi = v;
+  if (wid == 0) {  // exclusive scan of the R x kW counts in (round, warp) order
+    const int E = R * kW;
+    const int per = (E + 31) / 32;
+    int32_t sum = 0;
+    for (int j = 0; j < per; ++j) {
+      const int e = lane * per + j;
+      if (e < E) sum += cnt_s[e];
+    }
+    int32_t incl = sum;
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
-      const int32_t y = __shfl_up_sync(0xffffffffu, vi, d);
-      if (lane >= d) vi += y;
+      const int32_t y = __shfl_up_sync(0xffffffffu, incl, d);
+      if (lane >= d) incl += y;
     }
-    warp_tot[lane] = vi - v;  // exclusive prefix of warp totals
-    if (lane == 31) total_s = vi;
+    int32_t run = incl - sum;
+    for (int j = 0; j < per; ++j) {
+      const int e = lane * per + j;
+      if (e < E) {
+        const int32_t c = cnt_s[e];
+        cnt_s[e] = run;
+        run += c;
+      }
+    }
+    if (lane == 31) total_s = incl;
   }
   __syncthreads();
-  int32_t off = warp_tot[wid] + incl - cnt;
-  for (int64_t i = 0; i < C; ++i) {
-    if (flags & (1u << i)) {
-      const int64_t p = p0 + i;
-      out_nodes[off] = (p & 1) ? __ldg(dst + (p >> 1)) : __ldg(src + (p >> 1));
-      out_winner[off] = (int32_t)p;
-      ++off;
+#pragma unroll
+  for (int r = 0; r < kR; ++r) {
+    if (r >= R) break;
+    const bool win = (flags >> r) & 1u;
+    const unsigned b = __ballot_sync(0xffffffffu, win);
+    if (win) {
+      const int32_t off = cnt_s[r * kW + wid] + __popc(b & ((1u << lane) - 1u));
+      out_nodes[off] = node[r];
+      out_winner[off] = (int32_t)((int64_t)r * NT + tid);
     }
   }
   if (!kSmem) {
     __syncthreads();  // all scratch reads are done before the reset
-    for (int64_t i = 0; i < C; ++i) {
-      if (flags & (1u << i)) {
-        const int64_t p = p0 + i;
-        const int32_t node = (p & 1) ? __ldg(dst + (p >> 1)) : __ldg(src + (p >> 1));
-        gscratch[node] = -1;
-      }
+#pragma unroll
+    for (int r = 0; r < kR; ++r) {
+      if (r >= R) break;
+      if ((flags >> r) & 1u) gscratch[node[r]] = -1;
     }
   }
   if (tid == 0) *out_num = total_s;

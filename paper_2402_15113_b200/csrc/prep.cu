@@ -196,7 +196,9 @@ cudaError_t launch_prep(const Tcsr& g, const int32_t* src, const int32_t* dst, c
   a.dedup = out_num != nullptr;
   int64_t blocks = (3 * num_events + kPrepWarps - 1) / kPrepWarps;
   // one wave of the two resident blocks per SM; the root warps grid-stride
-  const int64_t cap = (int64_t)num_sms() * env_int("MSPIPE_PREP_BPS", 2);
+  // (block 0, the dedup, counts against the wave: 297 blocks on 296 slots left
+  // one root block waiting ~13 us for a slot at GDELT)
+  const int64_t cap = (int64_t)num_sms() * env_int("MSPIPE_PREP_BPS", 2) - (a.dedup ? 1 : 0);
   if (blocks > cap) blocks = cap;
   if (!a.dedup) return launch_k(k_prep<false>, dim3((unsigned)blocks), dim3(kPrepThreads), 0, s, 1, a);
   blocks += 1;  // block 0: dedup
