@@ -12,6 +12,10 @@
 #pragma once
 #include "internal.cuh"
 
+#ifndef DEDUP_MARK
+#define DEDUP_MARK(i)  // debug phase marks (prep.cu with MSPIPE_PHASES)
+#endif
+
 namespace mspipe {
 
 constexpr int64_t kDedupSmemNodes = 40960;  // node table in shared memory up to 160 KB
@@ -53,6 +57,7 @@ __device__ __forceinline__ void block_dedup(const int32_t* __restrict__ src, con
     node[r] = v;
   }
   if (kSmem) __syncthreads();  // the table is cleared
+  DEDUP_MARK(3);
   // phase 1: warp-aggregated atomicMax of p per node (the highest lane of a
   // group of equal nodes holds the group's largest p)
 #pragma unroll
@@ -64,6 +69,7 @@ __device__ __forceinline__ void block_dedup(const int32_t* __restrict__ src, con
   }
   if (!kSmem) __threadfence();
   __syncthreads();
+  DEDUP_MARK(4);
   // phase 2: a pair wins iff the table holds its p; per-(round, warp) counts
   uint32_t flags = 0;
 #pragma unroll
@@ -102,6 +108,7 @@ __device__ __forceinline__ void block_dedup(const int32_t* __restrict__ src, con
     if (lane == 31) total_s = incl;
   }
   __syncthreads();
+  DEDUP_MARK(5);
 #pragma unroll
   for (int r = 0; r < kR; ++r) {
     if (r >= R) break;

@@ -10,8 +10,27 @@
 //                   straight into the dense snapshot buffers.
 // Reading the tables here is the "fetch": the stage orders this launch between
 // write-back(i-1-k) and write-back(i-k) (Eq. 2).
-#include "dedup.cuh"
 #include "internal.cuh"
+
+namespace mspipe {
+#ifdef MSPIPE_PHASES
+// debug: per-block phase times of the last k_prep launch (globaltimer ns)
+__device__ unsigned long long g_pphase[8192][6];
+__device__ __forceinline__ void pphase(int i) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  atomicMax(&g_pphase[blockIdx.x][i], t);
+}
+#define PPHASE(i) pphase(i)
+#define DEDUP_MARK(i) \
+  if (threadIdx.x == 0) pphase(i)
+#else
+#define PPHASE(i)
+#endif
+
+}  // namespace mspipe
+
+#include "dedup.cuh"
 
 namespace mspipe {
 
@@ -98,19 +117,6 @@ __device__ __forceinline__ void warp_gather_rows(const float4* __restrict__ tab,
     }
   }
 }
-
-#ifdef MSPIPE_PHASES
-// debug: per-block phase times of the last k_prep launch (globaltimer ns)
-__device__ unsigned long long g_pphase[8192][6];
-__device__ __forceinline__ void pphase(int i) {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  atomicMax(&g_pphase[blockIdx.x][i], t);
-}
-#define PPHASE(i) pphase(i)
-#else
-#define PPHASE(i)
-#endif
 
 template <bool kSmem>
 __global__ void __launch_bounds__(kPrepThreads, MSPIPE_PREP_MINB) k_prep(PrepArgs a) {

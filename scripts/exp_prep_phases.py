@@ -34,7 +34,8 @@ ph = buf[used].astype(np.int64)
 t0 = ph[:, 0].min()
 print("blocks", used.sum())
 names = {0: "entry", 1: "roots/dedup done", 5: "wait start", 2: "flag seen", 3: "build done", 4: "exit"}
-print("block0:", {k: round((ph[0, k] - t0) / 1e3, 2) for k in (0, 2, 1, 4)}, "(0 entry, 2 dedup, 1 stamps, 4 exit)")
+print("block0:", {k: round((ph[0, k] - t0) / 1e3, 2) for k in (0, 3, 4, 5, 2, 1)},
+      "(0 entry, 3 table cleared + ids loaded, 4 atomicMax done, 5 counts scanned, 2 dedup done, 1 stamps)")
 for k in (0, 1, 5, 2, 3, 4):
     col = ph[1:, k]
     col = col[col > 0] - t0
