@@ -482,8 +482,9 @@ def run_mspipe(args):
                              if args.l2 == "flush" else "warm: steps back to back, state tables L2-resident"),
                       "steps_per_graph": gs,
                       "parallelism": ("single" if ws == 1 else
-                                      f"shard{ws}: node-id-sharded memory, NCCL all-to-all fetch + write-back, "
-                                      f"global batch {G * cfg.batch}" if sharded else f"replicas{ws}")},
+                                      f"shard{ws}: node-id-sharded memory, window transport (stores into peers' "
+                                      f"windows + NCCL barriers), global batch {G * cfg.batch}" if sharded
+                                      else f"replicas{ws}")},
            "blocks": {"count": len(blocks), "timed_ms_total": float(sum(b[0] for b in blocks)),
                       "rates": rates, "rule": f"K-step blocks (reset + W warm-up each) until >= {MIN_TIMED_MS} ms; "
                                               "value = the median block"},
@@ -768,9 +769,13 @@ def run_reference(args):
     out = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": K,
            "warmup": W, "ms_per_step": 1e3 * dt / K, "higher_is_better": True, "scaling": "weak",
            "vs_baseline": None, "dtype": "f64-accumulate/f32-state", "data": "synthetic",
-           "config": {"workload": args.config, "batch": cfg.batch, "staleness_k": k, "schedule": args.schedule,
-                      "fanout": cfg.fanout, "mem_dim": cfg.mem_dim, "edge_dim": cfg.edge_dim,
-                      "mitigation": bool(mit), "parallelism": "host cores"},
+           # the same keys as the mspipe arm's config (values of the oracle's run)
+           "config": {"workload": args.config, "events": int(len(w["src"])), "tcsr_events": int(len(w["src"])),
+                      "tcsr_nnz": None, "num_nodes": cfg.num_nodes,
+                      "batch": cfg.batch, "staleness_k": k, "schedule": args.schedule, "fanout": cfg.fanout,
+                      "mem_dim": cfg.mem_dim, "edge_dim": cfg.edge_dim, "time_dim": cfg.time_dim,
+                      "mitigation": bool(mit), "features": False, "fetch_mail": False,
+                      "gru": "f64-oracle", "l2": "host", "steps_per_graph": None, "parallelism": "host cores"},
            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle", "cpu_model": _cpu_model(),
                             "sample": f"batches {W + 1}..{W + K} of the stream (after {W} untimed), full per-batch path"},
            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
