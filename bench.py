@@ -491,7 +491,7 @@ def run_mspipe(args):
            "roofline": roof, "roofline_gather": roof_gather, "roofline_features": roof_features,
            "per_step_graphs": per_step,
            "gpu_launches": _launches(st.step_ops(), timed_batches, bool(mit), getattr(st, "fused", False), sharded,
-                                     args.features, getattr(st, "prep_build", False)),
+                                     args.features),
            "clocks": clocks}
     if sharded:
         out["exchange"] = _exchange_report(st, W + K, ms_step)
@@ -643,9 +643,9 @@ def hbm_probe(dev, cfg, peaks, flush, seed):
     return res
 
 
-def _launches(steps, timed_batches, mit, fused, sharded=False, features=False, prep_build=False):
+def _launches(steps, timed_batches, mit, fused, sharded=False, features=False):
     """Kernels of this library per timed step.  fused: prep = k_prep + k_build_x
-    (+ k_mitigate), or k_prep alone with the build inside it (prep_build), commit = k_gru_tc (h' rows) + k_writeback (mem_ts / mail); otherwise prep = sampler +
+    (+ k_mitigate), commit = k_gru_tc (h' rows) + k_writeback (mem_ts / mail); otherwise prep = sampler +
     dedup + gather (+ mitigation), commit = build + GEMM (or SIMT GRU) + write-back.  Sharded:
     prep = sampler + dedup + mark + plan + serve + finish, commit = build + GEMM + pack-plan + pack
     + merge-key + merge-apply (NCCL barrier kernels not counted)."""
@@ -654,7 +654,7 @@ def _launches(steps, timed_batches, mit, fused, sharded=False, features=False, p
         return int(sum(per[op] for t in timed_batches for op, _ in steps[t]))
     # fused commit: k_gru_tc (+ the k_writeback branch of mem_ts / mail unless MSPIPE_SPLIT_COMMIT=0)
     split = fused and os.environ.get("MSPIPE_SPLIT_COMMIT", "1") != "0"
-    per = {"prep": (1 if prep_build else 2 if fused else 3) + (1 if mit else 0) + (1 if features else 0),
+    per = {"prep": (2 if fused else 3) + (1 if mit else 0) + (1 if features else 0),
            "commit": (2 if split else 1) if fused else 3}
     return int(sum(per[op] for t in timed_batches for op, _ in steps[t]))
 

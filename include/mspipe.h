@@ -360,30 +360,6 @@ MSPIPE_API mspipe_status mspipe_memory_prep(mspipe_memory* st, const mspipe_tcsr
  *     exactly as mspipe_memory_update;
  *   mspipe_gru_apply (A6): out_mem [<=2B, mem_dim] exactly as
  *     mspipe_memory_update. */
-/* A1 + A2 + A3 + A5 in one launch (MSPIPE_FP32_3XTF32, immediate mailbox, no
- * mitigation): mspipe_memory_prep followed by mspipe_message_build of the same
- * batch — the same outputs (out_commit_ts / out_commit_mail = message_build's
- * out_ts / out_mail with the handle's mail_stride; the A-operand images in
- * `workspace`, >= mspipe_gru_workspace_size(gru, num_events) bytes).  Inside
- * the kernel the dedup block publishes the winners and, after their roots,
- * every warp builds (GEMM row, 4 K chunk) items of the message (G1-G4, G14)
- * from the state tables of the version this prep reads: the values
- * message_build computes from the gathered rows, of which they are bit
- * copies.  The dedup outputs are required.  num_events <= the GRU handle's
- * max_events.  Errors as mspipe_memory_prep, plus MSPIPE_EINVAL (NULL GRU /
- * outputs, dims differ, workspace too small) and MSPIPE_EUNSUPPORTED (another
- * precision or the deferred mailbox).  Preps of one handle must not run
- * concurrently (they share the handle's dedup / build scratch). */
-MSPIPE_API mspipe_status mspipe_memory_prep_build(mspipe_memory* st, const mspipe_tcsr* g, int64_t iteration,
-                                       const int32_t* src, const int32_t* dst, const int32_t* neg,
-                                       const double* ts, int64_t num_events, int32_t fanout,
-                                       int32_t* out_nbr, int32_t* out_eid, double* out_ts, float* out_dt,
-                                       int32_t* out_cnt, int32_t* out_sub_ids, int32_t* out_nodes,
-                                       int32_t* out_winner, int32_t* out_num_unique, float* out_mem,
-                                       double* out_mem_ts, float* out_mail, double* out_mail_ts,
-                                       int64_t* out_version, const mspipe_gru* gru, const float* edge_feat,
-                                       double* out_commit_ts, float* out_commit_mail, void* workspace,
-                                       size_t ws_bytes, void* stream);
 MSPIPE_API size_t mspipe_gru_workspace_size(const mspipe_gru* gru, int64_t num_events);
 MSPIPE_API mspipe_status mspipe_message_build(const mspipe_gru* gru, const double* ts, int64_t num_events,
                                    const float* edge_feat, const float* snap_mem,

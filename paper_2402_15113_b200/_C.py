@@ -40,7 +40,7 @@ EXPORTS = ("mspipe_abi_version", "mspipe_last_error", "mspipe_check", "mspipe_sa
            "mspipe_gru_apply_commit_out", "mspipe_plan_stale_fractions", "mspipe_staleness_error",
            "mspipe_shard_window_handle", "mspipe_shard_connect", "mspipe_shard_connect_local",
            "mspipe_shard_sent_bytes", "mspipe_util_record_to_device", "mspipe_shard_mitigation_candidates",
-           "mspipe_shard_fetch_finish_table", "mspipe_shard_mitigate", "mspipe_memory_prep_build")
+           "mspipe_shard_fetch_finish_table", "mspipe_shard_mitigate")
 XCHG_FETCH_IDS, XCHG_FETCH_ROWS, XCHG_COMMIT = 0, 1, 2
 
 
@@ -134,8 +134,6 @@ def lib():
         L.mspipe_shard_mitigation_candidates.argtypes = [P, C.POINTER(Mitigation), P, i64, P, P]
         L.mspipe_shard_fetch_finish_table.argtypes = [P, P, i64, P, P, P]
         L.mspipe_shard_mitigate.argtypes = [P, C.POINTER(Mitigation), P, P, P]
-        L.mspipe_memory_prep_build.argtypes = [P, C.POINTER(Tcsr), i64, P, P, P, P, i64, i32, P, P, P, P, P, P, P, P,
-                                               P, P, P, P, P, C.POINTER(i64), P, P, P, P, P, C.c_size_t, P]
         if L.mspipe_abi_version() != ABI_VERSION:
             raise RuntimeError(f"libmspipe ABI {L.mspipe_abi_version()} != binding {ABI_VERSION}")
         _lib = L
@@ -540,22 +538,6 @@ def memory_dedup(st: MemoryHandle, src, dst, out, stream=None):
 
 
 
-
-
-def memory_prep_build(st: MemoryHandle, g: TcsrHandle, iteration, src, dst, neg, ts, fanout, samp, dd, out_mem,
-                      out_mem_ts, out_mail, out_mail_ts, gru: GruHandle, edge_feat, out_commit_ts, out_commit_mail,
-                      workspace, stream=None) -> int:
-    """A1+A2+A3 and the A5 message build of the same batch in one launch (no mitigation)."""
-    v = i64(-1)
-    _ck(lib().mspipe_memory_prep_build(st.h, C.byref(g.c), int(iteration), ptr(src), ptr(dst), ptr(neg), ptr(ts),
-                                       src.numel(), fanout, ptr(samp["nbr"]), ptr(samp["eid"]), ptr(samp["ts"]),
-                                       ptr(samp["dt"]), ptr(samp["cnt"]), ptr(samp["sub"]), ptr(dd["nodes"]),
-                                       ptr(dd["winner"]), ptr(dd["num"]), ptr(out_mem), ptr(out_mem_ts),
-                                       ptr(out_mail), ptr(out_mail_ts), C.byref(v), gru.h, ptr(edge_feat),
-                                       ptr(out_commit_ts), ptr(out_commit_mail), ptr(workspace),
-                                       workspace.numel() * workspace.element_size(), stream_ptr(stream)),
-        "mspipe_memory_prep_build")
-    return int(v.value)
 
 
 def memory_update(st: MemoryHandle, gru: GruHandle, src, dst, ts, edge_feat, snap_mem, snap_mem_ts, snap_step,

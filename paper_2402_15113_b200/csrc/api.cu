@@ -155,8 +155,6 @@ mspipe_status mspipe_memory_create(mspipe_memory** out, int64_t num_nodes, int32
   st->local_rows = (num_nodes - rank + world - 1) / world;
   cudaError_t e = cudaMalloc(&st->scratch, sizeof(int32_t) * (size_t)num_nodes);
   if (e == cudaSuccess) e = cudaMemset(st->scratch, 0xFF, sizeof(int32_t) * (size_t)num_nodes);
-  if (e == cudaSuccess) e = cudaMalloc(&st->bld_sync, sizeof(int32_t) * 2);
-  if (e == cudaSuccess) e = cudaMemset(st->bld_sync, 0, sizeof(int32_t) * 2);
   if (e == cudaSuccess) e = cudaMalloc(&st->sample_hint, sizeof(int64_t) * (size_t)num_nodes);
   if (e == cudaSuccess) e = cudaMemset(st->sample_hint, 0, sizeof(int64_t) * (size_t)num_nodes);
   if (e == cudaSuccess && world > 1) {
@@ -290,7 +288,7 @@ mspipe_status mspipe_memory_destroy(mspipe_memory* st) {
   nccl_comm_destroy(st);
   for (int p = 0; p < st->world && p < 64; ++p)
     if (st->sh_peer_ipc[p] && st->sh_peer_host[p]) cudaIpcCloseMemHandle(st->sh_peer_host[p]);
-  void* bufs[] = {st->scratch, st->sample_hint, st->bld_sync, st->sh_needed, st->sh_slot_of, st->sh_dest, st->sh_keytab, st->sh_window,
+  void* bufs[] = {st->scratch, st->sample_hint, st->sh_needed, st->sh_slot_of, st->sh_dest, st->sh_keytab, st->sh_window,
                   st->sh_peers, st->sh_sent, st->sh_bar, st->prev_nodes,
                   st->prev_num, st->stamps};
   for (void* b : bufs)
@@ -588,23 +586,6 @@ mspipe_status mspipe_memory_writeback(mspipe_memory* st, int64_t commit_version,
 }
 
 
-// the build arguments of mspipe_memory_prep_build (nullptr: plain prep)
-struct BuildArgs {
-  const mspipe_gru* gru;
-  const float* edge_feat;
-  double* out_ts;
-  float* out_mail;
-  void* workspace;
-};
-
-static mspipe_status prep_impl(mspipe_memory* st, const mspipe_tcsr* g, int64_t iteration, const int32_t* src,
-                               const int32_t* dst, const int32_t* neg, const double* ts, int64_t num_events,
-                               int32_t fanout, int32_t* out_nbr, int32_t* out_eid, double* out_ts, float* out_dt,
-                               int32_t* out_cnt, int32_t* out_sub_ids, int32_t* out_nodes, int32_t* out_winner,
-                               int32_t* out_num_unique, float* out_mem, double* out_mem_ts, float* out_mail,
-                               double* out_mail_ts, const mspipe_mitigation* mit, int64_t* out_version,
-                               void* stream, const BuildArgs* ba);
-
 mspipe_status mspipe_memory_prep(mspipe_memory* st, const mspipe_tcsr* g, int64_t iteration, const int32_t* src,
                                  const int32_t* dst, const int32_t* neg, const double* ts, int64_t num_events,
                                  int32_t fanout, int32_t* out_nbr, int32_t* out_eid, double* out_ts, float* out_dt,
@@ -612,47 +593,6 @@ mspipe_status mspipe_memory_prep(mspipe_memory* st, const mspipe_tcsr* g, int64_
                                  int32_t* out_num_unique, float* out_mem, double* out_mem_ts, float* out_mail,
                                  double* out_mail_ts, const mspipe_mitigation* mit, int64_t* out_version,
                                  void* stream) {
-  return prep_impl(st, g, iteration, src, dst, neg, ts, num_events, fanout, out_nbr, out_eid, out_ts, out_dt, out_cnt,
-                   out_sub_ids, out_nodes, out_winner, out_num_unique, out_mem, out_mem_ts, out_mail, out_mail_ts, mit,
-                   out_version, stream, nullptr);
-}
-
-mspipe_status mspipe_memory_prep_build(mspipe_memory* st, const mspipe_tcsr* g, int64_t iteration,
-                                       const int32_t* src, const int32_t* dst, const int32_t* neg,
-                                       const double* ts, int64_t num_events, int32_t fanout,
-                                       int32_t* out_nbr, int32_t* out_eid, double* out_ts, float* out_dt,
-                                       int32_t* out_cnt, int32_t* out_sub_ids, int32_t* out_nodes,
-                                       int32_t* out_winner, int32_t* out_num_unique, float* out_mem,
-                                       double* out_mem_ts, float* out_mail, double* out_mail_ts,
-                                       int64_t* out_version, const mspipe_gru* gru, const float* edge_feat,
-                                       double* out_commit_ts, float* out_commit_mail, void* workspace,
-                                       size_t ws_bytes, void* stream) {
-  if (!gru) return fail(MSPIPE_EINVAL, "memory_prep_build: NULL GRU handle");
-  if (gru->precision != MSPIPE_FP32_3XTF32 || gru->d.mailbox != MSPIPE_MAILBOX_IMMEDIATE)
-    return fail(MSPIPE_EUNSUPPORTED, "memory_prep_build: only for an immediate-mailbox MSPIPE_FP32_3XTF32 handle");
-  if (!st || gru->d.M != st->mem_dim || gru->d.He != st->edge_dim)
-    return fail(MSPIPE_EINVAL, "memory_prep_build: NULL memory handle or dims differ from the GRU's");
-  if (num_events > gru->max_events)
-    return fail(MSPIPE_EINVAL, "memory_prep_build: num_events=%lld > max_events %lld of the GRU handle",
-                (long long)num_events, (long long)gru->max_events);
-  if (num_events > 0 && (!out_nodes || !out_winner || !out_num_unique || !out_commit_ts || !out_commit_mail ||
-                         (st->edge_dim > 0 && !edge_feat) || !workspace ||
-                         ws_bytes < mspipe_gru_workspace_size(gru, num_events)))
-    return fail(MSPIPE_EINVAL, "memory_prep_build: null dedup / build outputs or edge features, or workspace < %zu bytes",
-                mspipe_gru_workspace_size(gru, num_events));
-  const BuildArgs ba{gru, edge_feat, out_commit_ts, out_commit_mail, workspace};
-  return prep_impl(st, g, iteration, src, dst, neg, ts, num_events, fanout, out_nbr, out_eid, out_ts, out_dt, out_cnt,
-                   out_sub_ids, out_nodes, out_winner, out_num_unique, out_mem, out_mem_ts, out_mail, out_mail_ts,
-                   nullptr, out_version, stream, &ba);
-}
-
-static mspipe_status prep_impl(mspipe_memory* st, const mspipe_tcsr* g, int64_t iteration, const int32_t* src,
-                               const int32_t* dst, const int32_t* neg, const double* ts, int64_t num_events,
-                               int32_t fanout, int32_t* out_nbr, int32_t* out_eid, double* out_ts, float* out_dt,
-                               int32_t* out_cnt, int32_t* out_sub_ids, int32_t* out_nodes, int32_t* out_winner,
-                               int32_t* out_num_unique, float* out_mem, double* out_mem_ts, float* out_mail,
-                               double* out_mail_ts, const mspipe_mitigation* mit, int64_t* out_version,
-                               void* stream, const BuildArgs* ba) {
   if (!st) return fail(MSPIPE_EINVAL, "memory_prep: NULL handle");
   if (st->world > 1) return fail(MSPIPE_EUNSUPPORTED, "memory_prep: fused prep reads local tables; world > 1 uses the sharded fetch");
   if (!tcsr_ok(g) || g->num_nodes != st->num_nodes) return fail(MSPIPE_EINVAL, "memory_prep: bad T-CSR");
@@ -708,23 +648,13 @@ static mspipe_status prep_impl(mspipe_memory* st, const mspipe_tcsr* g, int64_t 
                     (dedup ? (st->stamp_iter[c % (st->k + 1)] == c || c == iteration)
                            : (c != iteration && st->stamp_iter[c % (st->k + 1)] == c));
     const CatchUp cua = cu ? catchup_args(st, c) : CatchUp{};
-    PrepBuild pb{};
-    if (ba) {
-      pb.d = ba->gru->d;
-      pb.xbuf = (float*)ba->workspace;
-      pb.ef = ba->edge_feat;
-      pb.out_ts = ba->out_ts;
-      pb.out_mail = ba->out_mail;
-      pb.mail_stride = st->mail_stride;
-      pb.sync = st->bld_sync;
-    }
     cudaError_t e = launch_prep(to_tcsr(g), src, dst, neg, ts, num_events, fanout, out_nbr, out_eid, out_ts, out_dt,
                                 out_cnt, out_sub_ids, st->scratch, out_nodes, out_winner, out_num_unique, t.mem,
                                 t.mem_ts, st->mem_dim, t.mail, t.mail_ts, st->mail_stride, out_mem,
                                 out_mem_ts, out_mail, out_mail_ts, s,
                                 (st->db && dedup) ? st->stamps + (iteration % (st->k + 1)) * st->num_nodes : nullptr,
                                 (int32_t)iteration, cu ? &cua : nullptr,
-                                env_int("MSPIPE_SAMPLE_HINT", 1) ? st->sample_hint : nullptr, ba ? &pb : nullptr);
+                                env_int("MSPIPE_SAMPLE_HINT", 1) ? st->sample_hint : nullptr);
     if (e != cudaSuccess) return cuda_status(e, "memory_prep: launch");
     if (st->db && dedup) st->stamp_iter[iteration % (st->k + 1)] = iteration;
     if (cu) st->caught_up = c;

@@ -344,17 +344,6 @@ void launch_gru_simt(const GruDesc& d, const int32_t* src, const int32_t* dst, c
                      float* out_mem, double* out_ts, float* out_mail, int64_t mail_stride,
                      cudaStream_t s);
 
-// the message build fused into mspipe_memory_prep_build (prep.cu)
-struct PrepBuild {
-  GruDesc d;
-  float* xbuf;          // GEMM A-operand images (workspace); nullptr: no build
-  const float* ef;      // [B, He] edge features of the batch
-  double* out_ts;       // [U] commit timestamps
-  float* out_mail;      // [U, mail_stride] mail rows
-  int64_t mail_stride;
-  int32_t* sync;        // [2] publish flag, exit count (self-cleaning), library scratch
-};
-
 // gru_tc.cu
 size_t gru_tc_packed_floats(const GruDesc& d);
 size_t gru_tc_xbuf_floats(const GruDesc& d, int64_t max_events);
@@ -468,8 +457,7 @@ cudaError_t launch_prep(const Tcsr& g, const int32_t* src, const int32_t* dst, c
                         const float* mem, const double* mem_ts, int32_t mem_dim, const float* mail,
                         const double* mail_ts, int64_t mail_stride, float* out_mem, double* out_mem_ts,
                         float* out_mail, double* out_mail_ts, cudaStream_t s, int32_t* stamp = nullptr,
-                        int32_t stamp_iter = 0, const struct CatchUp* cu = nullptr, int64_t* hint = nullptr,
-                        const struct PrepBuild* bld = nullptr);
+                        int32_t stamp_iter = 0, const struct CatchUp* cu = nullptr, int64_t* hint = nullptr);
 
 }  // namespace mspipe
 
@@ -507,7 +495,6 @@ struct mspipe_memory {
   int64_t committed;
   int32_t* scratch;  // [num_nodes] int32, -1 between calls (self-cleaning)
   int64_t* sample_hint;  // [num_nodes] search start per node for the fused prep's sampler (any value is valid)
-  int32_t* bld_sync;     // [2] mspipe_memory_prep_build: winners-published flag, exit count (self-cleaning)
   int device;
   // ---- world > 1 (shard.cu) ----
   int64_t local_rows;       // rows of this rank's shard: nodes v with v % world == rank

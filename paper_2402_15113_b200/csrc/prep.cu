@@ -11,7 +11,6 @@
 // Reading the tables here is the "fetch": the stage orders this launch between
 // write-back(i-1-k) and write-back(i-k) (Eq. 2).
 #include "internal.cuh"
-#include "tc_layout.cuh"
 
 namespace mspipe {
 #ifdef MSPIPE_PHASES
@@ -78,84 +77,7 @@ struct PrepArgs {
   int32_t Qcu;     // float4 per mail row of the state tables (catch-up)
   int32_t dedup;   // 1: block 0 deduplicates (A2); 0: no dedup block
   int64_t* hint;   // optional [num_nodes]: per-node search start (warp_recent_sample)
-  PrepBuild bld;   // optional (bld.xbuf != nullptr): the A5 message build of the winners, in this launch
 };
-
-__device__ __forceinline__ int32_t ld_acquire(const int32_t* p) {
-  int32_t v;
-  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release(int32_t* p, int32_t v) {
-  asm volatile("st.release.gpu.global.b32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
-}
-
-// the build's flag is self-cleaning: the last block to leave resets it (every
-// block has passed its wait by then), so graph replays start from 0
-__device__ __forceinline__ void prep_exit(const PrepArgs& a) {
-  if (!a.bld.xbuf) return;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    const int32_t prev = atomicAdd(a.bld.sync + 1, 1);
-    if (prev == (int32_t)gridDim.x - 1) {
-      a.bld.sync[0] = 0;
-      a.bld.sync[1] = 0;
-      __threadfence();
-    }
-  }
-}
-
-// A5 for GEMM row u, K chunks [4 cg, 4 cg + 4) (one warp, lane = column in a
-// chunk): exactly k_build_x's values, read from the state tables of the
-// version this prep fetches (the rows k_build_x would read from the gathered
-// snapshot are bit copies of them), so no warp waits for another's gather —
-// only for block 0's winners.
-constexpr int kPrepBuildChunks = 4;
-__device__ __forceinline__ void build_item(const PrepArgs& a, int32_t u, int32_t cg, int lane) {
-  const PrepBuild& b = a.bld;
-  const GruDesc& d = b.d;
-  const int32_t nchunks = d.Kpad / tc::kKC;
-  const int32_t p = a.out_winner[u];  // written by block 0 of this launch: a plain load after the acquire
-  const int64_t ev = p >> 1;
-  const int role = p & 1;
-  const int32_t w = role ? __ldg(a.dst + ev) : __ldg(a.src + ev);
-  const int32_t o = role ? __ldg(a.src + ev) : __ldg(a.dst + ev);
-  const float* tab = reinterpret_cast<const float*>(a.mem);
-  const float* sw = tab + (int64_t)w * d.M;
-  const float* so = tab + (int64_t)o * d.M;
-  const float* erow = b.ef + ev * d.He;
-  const double t_ev = __ldg(a.ts + ev);
-  const float dt = (float)(t_ev - __ldg(a.mem_ts + w));  // Δt from the snapshot (G4)
-  float v[kPrepBuildChunks];
-#pragma unroll
-  for (int q = 0; q < kPrepBuildChunks; ++q) {
-    const int32_t k = (cg * kPrepBuildChunks + q) * tc::kKC + lane;
-    v[q] = 0.f;
-    if (k < d.M) v[q] = __ldg(sw + k);
-    else if (k < 2 * d.M) v[q] = __ldg(so + (k - d.M));
-    else if (k < d.Dm) v[q] = __ldg(erow + (k - 2 * d.M));
-    else if (k >= d.Dx && k < d.K) v[q] = __ldg(sw + (k - d.Dx));  // h = S.mem[w] (no mitigation)
-  }
-  const uint32_t off = tc::sw128_off((uint32_t)(u % tc::kM), (uint32_t)lane);
-#pragma unroll
-  for (int q = 0; q < kPrepBuildChunks; ++q) {
-    const int32_t c = cg * kPrepBuildChunks + q;
-    if (c >= nchunks) break;
-    const int32_t k = c * tc::kKC + lane;
-    if (k >= d.Dm && k < d.Dx) {
-      const int qq = k - d.Dm;
-      v[q] = time_cos(fmaf(__ldg(d.time_w + qq), dt, __ldg(d.time_b + qq)));
-    }
-    if (k < b.mail_stride) b.out_mail[(int64_t)u * b.mail_stride + k] = k < d.Dm ? v[q] : 0.f;
-    const float hi = tc::tf32_rna(v[q]);
-    const float lo = tc::tf32_rna(v[q] - hi);
-    char* blk = reinterpret_cast<char*>(b.xbuf) + ((int64_t)(u / tc::kM) * nchunks + c) * tc::kABlock;
-    *reinterpret_cast<float*>(blk + off) = hi;
-    *reinterpret_cast<float*>(blk + tc::kATile + off) = lo;
-  }
-  if (cg == 0 && lane == 0) b.out_ts[u] = t_ev;
-}
 
 // copy `nrows` table rows (ids held by lanes 0..nrows-1, -1 = zero row) of Q
 // float4 each into dst rows base..base+nrows-1; kU loads in flight per lane.
@@ -204,19 +126,12 @@ __global__ void __launch_bounds__(kPrepThreads, MSPIPE_PREP_MINB) k_prep(PrepArg
     block_dedup<kPrepThreads, kSmem>(a.src, a.dst, a.B, a.gscratch, sscratch, a.g.num_nodes, a.out_nodes,
                                      a.out_winner, a.out_num);
     if (threadIdx.x == 0) PPHASE(2);
-    if (a.stamp || a.bld.xbuf) {
+    if (a.stamp) {
       __syncthreads();  // out_nodes / out_winner / out_num written by this block
       const int32_t U = *a.out_num;
-      if (a.stamp)
-        for (int32_t u = threadIdx.x; u < U; u += kPrepThreads) a.stamp[a.out_nodes[u]] = a.stamp_iter;
-      if (a.bld.xbuf) {  // publish the winners to the build warps of every block
-        __threadfence();
-        __syncthreads();
-        if (threadIdx.x == 0) st_release(a.bld.sync, 1);
-      }
+      for (int32_t u = threadIdx.x; u < U; u += kPrepThreads) a.stamp[a.out_nodes[u]] = a.stamp_iter;
     }
     if (threadIdx.x == 0) PPHASE(1);
-    prep_exit(a);
     return;
   }
   const int lane = threadIdx.x & 31;
@@ -266,16 +181,6 @@ __global__ void __launch_bounds__(kPrepThreads, MSPIPE_PREP_MINB) k_prep(PrepArg
       if (__ldg(a.cu.stamp + v) != a.cu.iter) catchup_row(a.cu, v, a.Qm, a.Qcu, lane);
     }
   }
-  if (a.bld.xbuf) {
-    // A5 of the winners once block 0 has published them: one warp per (GEMM
-    // row, group of 4 K chunks), over every warp of the grid
-    while (ld_acquire(a.bld.sync) == 0) __nanosleep(64);
-    const int32_t U = *a.out_num;
-    const int32_t ngroups = (a.bld.d.Kpad / tc::kKC + kPrepBuildChunks - 1) / kPrepBuildChunks;
-    for (int64_t it = wid; it < (int64_t)U * ngroups; it += nwarps)
-      build_item(a, (int32_t)(it / ngroups), (int32_t)(it % ngroups), lane);
-  }
-  prep_exit(a);
   if (threadIdx.x == 0) PPHASE(4);
 }
 
@@ -286,7 +191,7 @@ cudaError_t launch_prep(const Tcsr& g, const int32_t* src, const int32_t* dst, c
                         const float* mem, const double* mem_ts, int32_t mem_dim, const float* mail,
                         const double* mail_ts, int64_t mail_stride, float* out_mem, double* out_mem_ts,
                         float* out_mail, double* out_mail_ts, cudaStream_t s, int32_t* stamp,
-                        int32_t stamp_iter, const CatchUp* cu, int64_t* hint, const PrepBuild* bld) {
+                        int32_t stamp_iter, const CatchUp* cu, int64_t* hint) {
   PrepArgs a{g, src, dst, neg, ts, num_events, fanout, out_nbr, out_eid, out_ts, out_dt, out_cnt, out_sub,
              scratch, out_nodes, out_winner, out_num, (const float4*)mem, mem_ts, mem_dim / 4,
              (const float4*)mail, mail_ts, out_mail ? (int32_t)(mail_stride / 4) : 0, (float4*)out_mem, out_mem_ts,
@@ -294,7 +199,6 @@ cudaError_t launch_prep(const Tcsr& g, const int32_t* src, const int32_t* dst, c
              (int32_t)(mail_stride / 4)};
   if (cu) a.cu = *cu;
   a.hint = hint;
-  if (bld) a.bld = *bld;
   a.dedup = out_num != nullptr;
   int64_t blocks = (3 * num_events + kPrepWarps - 1) / kPrepWarps;
   // one wave of the two resident blocks per SM; the root warps grid-stride

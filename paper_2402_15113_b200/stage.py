@@ -51,10 +51,6 @@ class StageConfig:
     mailbox: str = "immediate"  # row F3: "immediate" (G14) | "deferred" (TGL's TGN; needs fetch_mail)
     features: bool = False     # row F2: fetch node / edge features of the sampled subgraphs (bind_features)
     node_dim: int = 0          # |d_v| (GDELT 413); rows padded to a multiple of 4 floats on the device
-    # fused 3xTF32 path, immediate mailbox, no mitigation: the message build runs inside the
-    # prep kernel (mspipe_memory_prep_build) instead of a k_build_x launch after it;
-    # env MSPIPE_PREP_BUILD=0 selects the two-launch form (A/B)
-    prep_build: bool = dataclasses.field(default_factory=lambda: os.environ.get("MSPIPE_PREP_BUILD", "1") == "1")
 
     def use_fused(self) -> bool:
         ok = self.precision in (_C.FP32_3XTF32, _C.BF16) and self.fanout <= 31 and self.batch <= 8192
@@ -205,8 +201,6 @@ class MemoryStage(_TimedOps):
                                 mailbox=_C.MAILBOX_DEFERRED if self.deferred else _C.MAILBOX_IMMEDIATE)
         self.upd = _C.alloc_update(cfg.batch, cfg.mem_dim, self.memory.mail_stride, self.device)
         self.fused = cfg.use_fused()
-        self.prep_build = (self.fused and cfg.prep_build and not cfg.mitigation and cfg.mailbox == "immediate"
-                           and cfg.precision == _C.FP32_3XTF32)
         self._dbg_one = torch.zeros(1, device=self.device) if _DEBUG_ONLY else None  # timing diagnostics
         if self.deferred and not (self.fused and cfg.fetch_mail):
             raise ValueError("mailbox='deferred' runs on the fused tensor-core path with fetch_mail=True")
@@ -397,21 +391,6 @@ class MemoryStage(_TimedOps):
         """mspipe_memory_prep (A1+A2+A3[+A4], one launch) then mspipe_message_build (A5) of batch i."""
         cfg = self.cfg
         m = 3 * n * (cfg.fanout + 1)
-        if self.prep_build:
-            # one launch: A1 + A2 + A3 + the A5 message build (mspipe_memory_prep_build)
-            self._ev("prep")
-            sl.version = _C.memory_prep_build(self.memory, self.tcsr, i, x["src"], x["dst"], x["neg"], x["ts"],
-                                              cfg.fanout, samp, sl.dd, sl.mem[:m], sl.mem_ts[:m],
-                                              sl.mail[:m] if sl.mail is not None else None,
-                                              sl.mail_ts[:m] if sl.mail_ts is not None else None, self.gru,
-                                              x["ef"], sl.uts[: 2 * n], sl.umail[: 2 * n], sl.ws)
-            self._ev("prep_end")
-            self._features(sl, samp)
-            self.versions[i] = sl.version
-            if not self.memory.double_buffer:
-                self._fetched = torch.cuda.Event()  # the state tables have been read for batch i
-                self._fetched.record()
-            return
         self._ev("prep")
         sl.version = _C.memory_prep(self.memory, self.tcsr, i, x["src"], x["dst"], x["neg"], x["ts"], cfg.fanout,
                                     samp, sl.dd, sl.mem[:m], sl.mem_ts[:m],
