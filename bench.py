@@ -488,7 +488,9 @@ def run_mspipe(args):
            "blocks": {"count": len(blocks), "timed_ms_total": float(sum(b[0] for b in blocks)),
                       "rates": rates, "rule": f"K-step blocks (reset + W warm-up each) until >= {MIN_TIMED_MS} ms; "
                                               "value = the median block"},
-           "roofline": roof, "roofline_gather": roof_gather, "roofline_features": roof_features,
+           "roofline": roof, "roofline_gather": roof_gather,
+           "roofline_gemm": rooflines.get("update") if dom != "update" else None,
+           "roofline_features": roof_features,
            "per_step_graphs": per_step,
            "gpu_launches": _launches(st.step_ops(), timed_batches, bool(mit), getattr(st, "fused", False), sharded,
                                      args.features),
