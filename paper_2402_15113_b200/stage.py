@@ -64,7 +64,6 @@ class StageConfig:
 # step (results are meaningless); unset in every real run
 _DEBUG_ONLY = os.environ.get("MSPIPE_DEBUG_ONLY", "")
 _E2E_SKIP = os.environ.get("MSPIPE_E2E_SKIP", "")  # "h2d" | "d2h": drop that copy (e2e timing diagnostics)
-_COMMIT_FIRST = os.environ.get("MSPIPE_COMMIT_FIRST", "0") == "1"  # step order experiment (off)
 
 
 def plan_versions(plan, nb):
@@ -596,10 +595,6 @@ class MemoryStage(_TimedOps):
             self.side = torch.cuda.Stream(device=main.device, priority=int(os.environ.get("MSPIPE_SIDE_PRIO", "0")))
         commits = {i for op, i in ops if op == "commit"}
         db = self.memory.double_buffer
-        if db and _COMMIT_FIRST and not any(op == "prep" and i in commits for op, i in ops):
-            # double-buffered, no prep of this step feeds its commit: enqueue the commit
-            # (GEMM) before the prep, so its CTAs are placed first (A/B switch)
-            ops = [o for o in ops if o[0] == "commit"] + [o for o in ops if o[0] == "prep"]
         forked = joined = False
         for op, i in ops:
             if op == "prep" and _DEBUG_ONLY in ("commit", "none"):  # timing diagnostics only: no prep
