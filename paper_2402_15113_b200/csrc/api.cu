@@ -432,7 +432,8 @@ mspipe_status mspipe_updater_create(mspipe_gru** out, int32_t mem_dim, int32_t e
                       : cudaMalloc(&p->wtc, sizeof(float) * gru_tc_packed_floats(d));
   if (e == cudaSuccess && precision != MSPIPE_FP32_SIMT)
     e = cudaMalloc(&p->xbuf, sizeof(float) * gru_tc_xbuf_floats(d, max_events));
-  if (e == cudaSuccess) e = cudaMalloc(&p->bias, sizeof(float) * (size_t)d.Npad);
+  if (e == cudaSuccess)
+    e = cudaMalloc(&p->bias, sizeof(float) * std::max<size_t>((size_t)d.Npad, gru_tc_bias_floats(d)));
   if (e == cudaSuccess) e = cudaMalloc(&p->time_w, sizeof(float) * (size_t)(time_dim > 0 ? time_dim : 1));
   if (e == cudaSuccess) e = cudaMalloc(&p->time_b, sizeof(float) * (size_t)(time_dim > 0 ? time_dim : 1));
   if (e == cudaSuccess && time_dim > 0) e = cudaMemcpyAsync(p->time_w, time_w, sizeof(float) * time_dim, cudaMemcpyDeviceToDevice, s);

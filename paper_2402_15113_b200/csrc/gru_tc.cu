@@ -35,11 +35,15 @@ namespace mspipe {
 
 namespace tc {
 
-constexpr int kJ = 16;                  // hidden units per tile
-constexpr int kN = 4 * kJ;              // accumulator columns (UMMA N)
-constexpr int kBTile = kN * kKC * 4;    // 8 KB
+// hidden units per tile: 20 divides the paper's memory width (M = 100) into
+// five tiles with no padding (16 needed seven tiles, 112 columns)
+constexpr int kJ = 20;
+constexpr int kN = 4 * kJ;              // accumulator columns (UMMA N = 80: M = 128 needs N % 16 == 0)
+constexpr int kQ = kJ / 4;              // float4 quads of a gate row
+constexpr int kRecvRow = kN / 4 + 1;    // float4 per received row: 21 (odd: conflict-free pushes and reads)
+constexpr int kBTile = kN * kKC * 4;    // 10 KB
 constexpr int kBBlock = 2 * kBTile;
-constexpr int kStageBytes = kABlock + kBBlock;  // 48 KB
+constexpr int kStageBytes = kABlock + kBBlock;  // 52 KB
 constexpr int kStages = 3;
 // 8 warps: warp 0 loads, warp 1 issues the MMAs, warps 2..7 prefetch the
 // epilogue's inputs; in the epilogue warps w and w + 4 read the two 32-column
@@ -50,11 +54,9 @@ constexpr int kStages = 3;
 constexpr int kThreads = 256;
 constexpr int kPfThreads = kThreads - 64;  // warps 2..7
 constexpr int kHBufBytes = kM * kJ * 4;   // h rows of the tile's hidden units (prefetched)
-constexpr int kRecvBytes = kM * kN * 4;   // K-split partials received from the cluster (S x 128/S rows)
+constexpr int kRecvBytes = kM * kRecvRow * 16;  // K-split partials received from the cluster (S x 128/S rows)
 constexpr int kSmemBytes =
     kStages * kStageBytes + 1024 /*align*/ + 1024 /*barriers*/ + kHBufBytes + kRecvBytes + kN * 4 /*biases*/;
-// the persistent k_gru_tc: two receive buffers (tile parity)
-constexpr int kSmemBytesP = kSmemBytes + kRecvBytes;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -141,6 +143,11 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
                    smem_u32(bar))
                : "memory");
 }
+// 32 TMEM lanes x 8 consecutive fp32 columns -> 8 registers per thread.
+#define MSPIPE_TMEM_LD8(taddr, r)                                                                        \
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"                \
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]) \
+               : "r"(taddr))
 // 32 TMEM lanes x 32 consecutive fp32 columns -> 32 registers per thread.
 #define MSPIPE_TMEM_LD32(taddr, r)                                                                          \
   asm volatile(                                                                                             \
@@ -206,20 +213,20 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
   d |= (uint64_t)2u << 61;
   return d;
 }
-// kind::tf32 instruction descriptor: D f32, A/B tf32, K-major, M = 128, N = 64.
+// kind::tf32 instruction descriptor: D f32, A/B tf32, K-major, M = 128, N = kN.
 constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(kN >> 3) << 17) |
                             ((uint32_t)(kM >> 4) << 24);
-// kind::f16 instruction descriptor (MSPIPE_BF16): D f32, A/B bf16, K-major, M = 128, N = 64.
+// kind::f16 instruction descriptor (MSPIPE_BF16): D f32, A/B bf16, K-major, M = 128, N = kN.
 constexpr uint32_t kIdescBf = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kN >> 3) << 17) |
                               ((uint32_t)(kM >> 4) << 24);
-constexpr int kBTile16 = kN * kKC16 * 2;             // 8 KB
+constexpr int kBTile16 = kN * kKC16 * 2;             // 10 KB
 // bf16 mode splits both operands, x = hi + lo (two bf16), and issues
 // A_lo.B_hi + A_hi.B_lo + A_hi.B_hi (the bf16 analogue of 3xTF32): ~16
 // mantissa bits per operand, so h' lands within the C.6 per-element rule
 // (2e-2|o| + 1e-3) that plain bf16 operands miss by 3-10x
 constexpr int kABlock16 = 2 * kATile16;              // 32 KB: hi | lo
-constexpr int kBBlock16 = 2 * kBTile16;              // 16 KB: hi | lo
-constexpr int kStageBytes16 = kABlock16 + kBBlock16;  // 48 KB
+constexpr int kBBlock16 = 2 * kBTile16;              // 20 KB: hi | lo
+constexpr int kStageBytes16 = kABlock16 + kBBlock16;  // 52 KB
 }  // namespace tc
 
 #ifdef MSPIPE_PHASES
@@ -322,6 +329,8 @@ __global__ void k_gru_pack_tc(const float* __restrict__ w_ih, const float* __res
     }
   }
 }
+
+size_t gru_tc_bias_floats(const GruDesc& d) { return (size_t)gru_tc_jtiles(d) * tc::kN; }
 
 size_t gru_tc_packed_floats(const GruDesc& d) {
   if (d.bf16) return (size_t)gru_tc_jtiles(d) * (d.Kpad / tc::kKC16) * (tc::kBBlock16 / 4);
@@ -631,7 +640,7 @@ __device__ __forceinline__ void commit_rows(const TcArgs& a, int32_t m0, int32_t
     }
 }
 
-// kBf: bf16 operands (MSPIPE_BF16): 64-wide K chunks of 24 KB stages, one
+// kBf: bf16 operands (MSPIPE_BF16): 64-wide K chunks of 52 KB stages (hi | lo), one
 // accumulator per CTA for its K range (bf16 tolerance, north star 2e-2); the
 // K split and partial-sum exchange are the tf32 kernel's.
 // Persistent over tiles: grid (S, clusters); cluster c takes tiles
@@ -641,8 +650,8 @@ __device__ __forceinline__ void commit_rows(const TcArgs& a, int32_t m0, int32_t
 // ring (chunk counter continued across tiles, so stage phases carry over) and
 // issues the next tile's first kStages chunks as soon as this tile's MMAs are
 // done, overlapping them with the epilogue; the K-split partials go through
-// two receive buffers (tile parity), so one cluster barrier per tile orders
-// every push after the owner's reads of two tiles before.
+// one receive buffer, so one cluster barrier per tile orders every push after
+// the owner's reads of the tile before.
 #ifndef MSPIPE_MAIL_PF
 #define MSPIPE_MAIL_PF 1
 #endif
@@ -668,10 +677,12 @@ __global__ void __launch_bounds__(tc::kThreads, 1) k_gru_tc(TcArgs a) {
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 1);
   uint64_t* rfull = acc_full + 2;  // K-split partials of the tile received (st.async bytes)
   int32_t* rownode = reinterpret_cast<int32_t*>(smem + kStages * SB + 512);  // [128] node of each row
-  float4* hbuf = reinterpret_cast<float4*>(smem + kStages * SB + 1024);  // [128 rows][kJ/4]
-  float4* recv2 = reinterpret_cast<float4*>(smem + kStages * SB + 1024 + kHBufBytes);  // [2][kRecvBytes]
+  float4* hbuf = reinterpret_cast<float4*>(smem + kStages * SB + 1024);  // [128 rows][kQ]
+  // [S ranks x 128/S rows][kRecvRow float4]: row stride 84 words, so the 8
+  // rows of a quarter-warp's 16-byte accesses fall on 8 distinct bank quads
+  float4* recv = reinterpret_cast<float4*>(smem + kStages * SB + 1024 + kHBufBytes);
   // this tile's gate biases, prefetched during the main loop
-  float* sbias = reinterpret_cast<float*>(smem + kStages * SB + 1024 + kHBufBytes + 2 * kRecvBytes);
+  float* sbias = reinterpret_cast<float*>(smem + kStages * SB + 1024 + kHBufBytes + kRecvBytes);
 
   const GruDesc& d = a.d;
   PHASE(9);
@@ -688,10 +699,11 @@ __global__ void __launch_bounds__(tc::kThreads, 1) k_gru_tc(TcArgs a) {
   const int32_t c0 = split * nchunks / S, c1 = (split + 1) * nchunks / S;
   const int32_t nc = c1 - c0;  // tf32: <= kMaxChunks buffers of cpb chunks
   // tf32: K chunk ci accumulates into TMEM buffer ci / cpb (cpb chunks per
-  // 64-column buffer; 1 unless the K range exceeds kMaxChunks buffers)
+  // kN-column buffer; 1 unless the K range exceeds kMaxChunks buffers)
   const int cpb = a.cpb > 0 ? a.cpb : 1;
   const int nbuf = (nc + cpb - 1) / cpb;
-  const uint32_t tcols = kBf ? 64u : (nbuf <= 2 ? 128u : (nbuf <= 4 ? 256u : 512u));
+  const int need = (kBf ? 1 : nbuf) * kN;  // allocation: a power of two >= 32 columns
+  const uint32_t tcols = need <= 32 ? 32u : need <= 64 ? 64u : need <= 128 ? 128u : need <= 256 ? 256u : 512u;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
@@ -749,7 +761,6 @@ __global__ void __launch_bounds__(tc::kThreads, 1) k_gru_tc(TcArgs a) {
     const int32_t mt = (int32_t)(q / J);
     const int jt = (int)(q % J);
     const int32_t m0 = mt * kM;
-    float4* recv = recv2 + (kAsyncPush ? 0 : (ti & 1)) * (kRecvBytes / 16);
     if (warp == 0 && lane == 0) {
       for (int ci = pre; ci < nc; ++ci) load_chunk(ti, mt, jt, ci);
     } else if (warp == 1 && lane == 0) {
@@ -804,8 +815,8 @@ __global__ void __launch_bounds__(tc::kThreads, 1) k_gru_tc(TcArgs a) {
           if (m0 + mm < U && nq > 0)
             l2_prefetch(a.new_mail + ((int64_t)(m0 + mm) * Q + cq0) * 4, (uint32_t)nq * 16u);
       }
-      for (int it = threadIdx.x - 64; it < (re - rb) * (kJ / 4); it += kPfThreads) {
-        const int mm = rb + it / (kJ / 4), qq = it % (kJ / 4);
+      for (int it = threadIdx.x - 64; it < (re - rb) * kQ; it += kPfThreads) {
+        const int mm = rb + it / kQ, qq = it % kQ;
         const int32_t u = m0 + mm, j0 = jt * kJ + qq * 4;
         float4 hv = make_float4(0.f, 0.f, 0.f, 0.f);
         if (u < U && j0 < d.M) {  // M % 4 == 0: a quad is all valid or all padding
@@ -819,7 +830,7 @@ __global__ void __launch_bounds__(tc::kThreads, 1) k_gru_tc(TcArgs a) {
           }
           hv = __ldg(reinterpret_cast<const float4*>(hrow + j0));
         }
-        hbuf[mm * (kJ / 4) + qq] = hv;
+        hbuf[mm * kQ + qq] = hv;
         if (qq == 0) {
           const int32_t node = (a.commit_mem && u < U) ? __ldg(a.nodes + u) : -1;
           rownode[mm] = node;
@@ -843,50 +854,56 @@ __global__ void __launch_bounds__(tc::kThreads, 1) k_gru_tc(TcArgs a) {
         for (; pre < nc && pre < kStages; ++pre) load_chunk(ti + 1, (int32_t)(qn / J), (int)(qn % J), pre);
       }
     }
-    // thread = (row m of lane quarter warp % 4, column half warp / 4)
+    // thread = (row m of lane quarter warp % 4, column half warp / 4): the
+    // half's kN/2 = 40 columns as five 8-column loads per buffer (column
+    // offsets multiples of 8)
+    constexpr int kHC = kN / 2;
     const int half = warp >> 2;
     const int m = (warp & 3) * 32 + lane;
-    const uint32_t tbase = tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)(half * 32);
-    uint32_t r0[32];
-    MSPIPE_TMEM_LD32(tbase, r0);
+    const uint32_t tbase = tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)(half * kHC);
+    uint32_t r0[kHC];
+#pragma unroll
+    for (int c8 = 0; c8 < kHC / 8; ++c8) MSPIPE_TMEM_LD8(tbase + 8 * c8, (r0 + 8 * c8));
     tmem_wait_ld();
     for (int bi = 1; bi < (kBf ? 1 : nbuf); ++bi) {
-      uint32_t t0[32];
-      MSPIPE_TMEM_LD32(tbase + bi * kN, t0);
+      uint32_t t0[kHC];
+#pragma unroll
+      for (int c8 = 0; c8 < kHC / 8; ++c8) MSPIPE_TMEM_LD8(tbase + bi * kN + 8 * c8, (t0 + 8 * c8));
       tmem_wait_ld();
 #pragma unroll
-      for (int i = 0; i < 32; ++i) r0[i] = __float_as_uint(__fadd_rn(__uint_as_float(r0[i]), __uint_as_float(t0[i])));
+      for (int i = 0; i < kHC; ++i)
+        r0[i] = __float_as_uint(__fadd_rn(__uint_as_float(r0[i]), __uint_as_float(t0[i])));
     }
     PHASE(4);
     const float* bias = sbias;
-    // this thread's half row (8 float4, float4 index half * 8 + c4) goes to
-    // recv[src_rank][m - rb(owner)][16 x float4] of the rank that finalises
-    // row m, float4 index XOR-swizzled by the row so the owner's reads are
-    // conflict-free; S = 1: into this CTA's own buffer
+    // this thread's half row (kHC / 4 = 10 float4, index half * 10 + c4) goes
+    // to recv[src_rank][m - rb(owner)][.] of the rank that finalises row m;
+    // S = 1: into this CTA's own buffer
+    constexpr int kH4 = kHC / 4;
     if (S > 1) {
       // Fire-and-forget remote stores instead of latency-bound remote loads.
       const int R = kM / S;
       const int owner = m / R, lm = m % R;
-      const uint32_t dst = mapa(smem_u32(recv) + (uint32_t)((rank * R + lm) * (kN / 4)) * 16u, (uint32_t)owner);
+      const uint32_t dst = mapa(smem_u32(recv) + (uint32_t)((rank * R + lm) * kRecvRow + half * kH4) * 16u,
+                                (uint32_t)owner);
       if (kAsyncPush) {
         if (ti == 0) cluster_wait();  // every rfull of the cluster is initialised
         if (threadIdx.x == 0) mbar_arrive_expect_tx(rfull, (uint32_t)(kM * kN * 4));  // S x R rows x kN floats
         const uint32_t rbar = mapa(smem_u32(rfull), (uint32_t)owner);
 #pragma unroll
-        for (int c4 = 0; c4 < 8; ++c4)
-          st_async_f4(dst + 16u * (uint32_t)((half * 8 + c4) ^ (lm & 15)), __uint_as_float(r0[4 * c4]),
-                      __uint_as_float(r0[4 * c4 + 1]), __uint_as_float(r0[4 * c4 + 2]), __uint_as_float(r0[4 * c4 + 3]),
-                      rbar);
+        for (int c4 = 0; c4 < kH4; ++c4)
+          st_async_f4(dst + 16u * (uint32_t)c4, __uint_as_float(r0[4 * c4]), __uint_as_float(r0[4 * c4 + 1]),
+                      __uint_as_float(r0[4 * c4 + 2]), __uint_as_float(r0[4 * c4 + 3]), rbar);
       } else {
 #pragma unroll
-        for (int c4 = 0; c4 < 8; ++c4)
-          st_dsmem_f4(dst + 16u * (uint32_t)((half * 8 + c4) ^ (lm & 15)), __uint_as_float(r0[4 * c4]),
-                      __uint_as_float(r0[4 * c4 + 1]), __uint_as_float(r0[4 * c4 + 2]), __uint_as_float(r0[4 * c4 + 3]));
+        for (int c4 = 0; c4 < kH4; ++c4)
+          st_dsmem_f4(dst + 16u * (uint32_t)c4, __uint_as_float(r0[4 * c4]), __uint_as_float(r0[4 * c4 + 1]),
+                      __uint_as_float(r0[4 * c4 + 2]), __uint_as_float(r0[4 * c4 + 3]));
       }
     } else {
 #pragma unroll
-      for (int c4 = 0; c4 < 8; ++c4)
-        recv[m * (kN / 4) + ((half * 8 + c4) ^ (m & 15))] =
+      for (int c4 = 0; c4 < kH4; ++c4)
+        recv[m * kRecvRow + half * kH4 + c4] =
             make_float4(__uint_as_float(r0[4 * c4]), __uint_as_float(r0[4 * c4 + 1]), __uint_as_float(r0[4 * c4 + 2]),
                         __uint_as_float(r0[4 * c4 + 3]));
     }
@@ -909,19 +926,19 @@ __global__ void __launch_bounds__(tc::kThreads, 1) k_gru_tc(TcArgs a) {
       PHASE(6);
       const int R = kM / S;
       const int rb = rank * R;
-      for (int it = threadIdx.x; it < R * (kJ / 4); it += kThreads) {
-        const int lm = it / (kJ / 4), qq = it % (kJ / 4);
+      for (int it = threadIdx.x; it < R * kQ; it += kThreads) {
+        const int lm = it / kQ, qq = it % kQ;
         const int mm = rb + lm;
         const int32_t u = m0 + mm;
         const int32_t j0 = jt * kJ + qq * 4;
         if (u >= U || j0 >= d.M) continue;
         float4 acc[4];
 #pragma unroll
-        for (int g = 0; g < 4; ++g) acc[g] = recv[(0 * R + lm) * (kN / 4) + ((g * (kJ / 4) + qq) ^ (lm & 15))];
+        for (int g = 0; g < 4; ++g) acc[g] = recv[(0 * R + lm) * kRecvRow + g * kQ + qq];
         for (int sr = 1; sr < S; ++sr)  // fixed rank order: deterministic sum
 #pragma unroll
           for (int g = 0; g < 4; ++g) {
-            const float4 v = recv[(sr * R + lm) * (kN / 4) + ((g * (kJ / 4) + qq) ^ (lm & 15))];
+            const float4 v = recv[(sr * R + lm) * kRecvRow + g * kQ + qq];
             acc[g].x += v.x;
             acc[g].y += v.y;
             acc[g].z += v.z;
@@ -937,7 +954,7 @@ __global__ void __launch_bounds__(tc::kThreads, 1) k_gru_tc(TcArgs a) {
           pnx[e] = (&acc[2].x)[e] + bias[2 * kJ + jj];
           pnh[e] = (&acc[3].x)[e] + bias[3 * kJ + jj];
         }
-        store_h4(a, u, rownode[mm], j0, gates4(pr, pz, pnx, pnh, hbuf[mm * (kJ / 4) + qq], d.cell));
+        store_h4(a, u, rownode[mm], j0, gates4(pr, pz, pnx, pnh, hbuf[mm * kQ + qq], d.cell));
       }
       PHASE(10);
       if (a.commit_mem && !a.skip_meta) commit_rows(a, m0, U, rb, rb + R, jt, J, rownode);
@@ -945,7 +962,7 @@ __global__ void __launch_bounds__(tc::kThreads, 1) k_gru_tc(TcArgs a) {
     }
     __syncthreads();  // hbuf / rownode / sbias are rewritten by the next tile's prefetch
     // single receive buffer: every CTA's reads of it precede the next tile's pushes
-    if (kAsyncPush && S > 1 && q + gridDim.y < tiles) cluster_sync_all();
+    if (S > 1 && q + gridDim.y < tiles) cluster_sync_all();
   }
   if (warp == 2) {
     tc_fence_after();
@@ -1037,7 +1054,7 @@ void launch_mail_deferred(const int32_t* src, const int32_t* dst, const double* 
 
 // ---------------------------------------------------------------------------
 
-constexpr int kMaxChunks = 8;  // 8 x 64 TMEM columns = 512 (the whole TMEM of the SM)
+constexpr int kMaxChunks = 512 / tc::kN;  // 6 buffers of 80 TMEM columns (the SM's TMEM: 512)
 
 // co-resident clusters of S CTAs of k_gru_tc (cached per S; env MSPIPE_TC_CLUSTERS overrides)
 static int64_t gru_tc_clusters(int S, bool bf16) {
@@ -1049,7 +1066,7 @@ static int64_t gru_tc_clusters(int S, bool bf16) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)S, 1, 1);
   cfg.blockDim = dim3(tc::kThreads);
-  cfg.dynamicSmemBytes = tc::kSmemBytesP;
+  cfg.dynamicSmemBytes = tc::kSmemBytes;
   cudaLaunchAttribute attr;
   attr.id = cudaLaunchAttributeClusterDimension;
   attr.val.clusterDim.x = (unsigned)S;
@@ -1073,13 +1090,16 @@ int gru_tc_splits(int64_t max_rows, const GruDesc& d, bool shared_buffers) {
   const int forced = env_int("MSPIPE_TC_SPLITS", 0);  // experiments only: read at every launch
   const int nchunks = d.Kpad / (d.bf16 ? tc::kKC16 : tc::kKC);
   // tf32: up to three K chunks share a TMEM buffer (36 MMAs per accumulator:
-  // measured 0.47 of the 1e-4 tolerance at GDELT); bf16: a single accumulator
-  int64_t s_min = d.bf16 ? 1 : (nchunks + 3 * kMaxChunks - 1) / (3 * kMaxChunks);
+  // measured 0.47 of the 1e-4 tolerance at GDELT; four (48 MMAs) exceeded it
+  // on one element); bf16: a single accumulator
+  const int64_t s_min = d.bf16 ? 1 : (nchunks + 3 * kMaxChunks - 1) / (3 * kMaxChunks);
   if (forced > 0) return forced;  // below s_min the chunks share TMEM buffers (TcArgs::cpb)
-  // big batches (GDELT's 2B = 8000, ~13 M tiles x 7 hidden tiles): S = 1, the
-  // 91 tiles in one wave of CTAs, three K chunks per TMEM buffer (measured with
-  // the 8-warp epilogue: 42.6 / 47.7 / 52.3 us per GDELT step at S = 1 / 2 / 4)
-  if (shared_buffers && !d.bf16 && max_rows >= 4096) return env_int("MSPIPE_TC_BIG_S", 1);
+  // big batches (GDELT's 2B = 8000, ~13 M tiles x 5 hidden tiles): S = 2, the
+  // 130 CTAs in one wave, two K chunks per TMEM buffer (measured with the
+  // 20-unit tile: 43.3 vs 44.6 us per GDELT step at S = 2 / 1, and S = 1
+  // needs four chunks per buffer)
+  if (shared_buffers && !d.bf16 && max_rows >= 4096)
+    return (int)std::max<int64_t>(env_int("MSPIPE_TC_BIG_S", 2), s_min);
   const int64_t tiles = ((max_rows + tc::kM - 1) / tc::kM) * gru_tc_jtiles(d);
   int64_t s = 1;
   while (s < 8 && tiles * s * 2 <= 2 * (int64_t)num_sms() && s * 2 <= nchunks / 2) s *= 2;
@@ -1096,9 +1116,9 @@ cudaError_t launch_gru_tc(const GruDesc& d, const float* wtc, float* xbuf, const
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(k_gru_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         tc::kSmemBytesP);
+                                         tc::kSmemBytes);
     if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(k_gru_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::kSmemBytesP);
+      e = cudaFuncSetAttribute(k_gru_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::kSmemBytes);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(k_gru_tc<false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(k_gru_tc<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     if (e != cudaSuccess) return e;
@@ -1149,9 +1169,9 @@ cudaError_t launch_gru_tc(const GruDesc& d, const float* wtc, float* xbuf, const
   const int64_t max_tiles = mtiles * gru_tc_jtiles(d);
   const int64_t nclust = std::min<int64_t>(max_tiles, gru_tc_clusters(S, d.bf16));
   if (d.bf16)
-    return launch_k(k_gru_tc<true>, dim3((unsigned)S, (unsigned)nclust), dim3(tc::kThreads), tc::kSmemBytesP, s,
+    return launch_k(k_gru_tc<true>, dim3((unsigned)S, (unsigned)nclust), dim3(tc::kThreads), tc::kSmemBytes, s,
                     (unsigned)S, a);
-  return launch_k(k_gru_tc<false>, dim3((unsigned)S, (unsigned)nclust), dim3(tc::kThreads), tc::kSmemBytesP, s,
+  return launch_k(k_gru_tc<false>, dim3((unsigned)S, (unsigned)nclust), dim3(tc::kThreads), tc::kSmemBytes, s,
                   (unsigned)S, a);
 }
 

@@ -346,6 +346,7 @@ void launch_gru_simt(const GruDesc& d, const int32_t* src, const int32_t* dst, c
 
 // gru_tc.cu
 size_t gru_tc_packed_floats(const GruDesc& d);
+size_t gru_tc_bias_floats(const GruDesc& d);  // J tiles x 4 gates x kJ
 size_t gru_tc_xbuf_floats(const GruDesc& d, int64_t max_events);
 void launch_gru_pack_tc(const float* w_ih, const float* w_hh, const float* b_ih, const float* b_hh,
                         const GruDesc& d, float* wtc, float* bias, cudaStream_t s);

@@ -842,13 +842,14 @@ def test_degenerate_batches(dev):
 
 
 @pytest.mark.parametrize("env", [{"MSPIPE_SPLIT_COMMIT": "0"}, {"MSPIPE_SAMPLE_HINT": "0"},
-                                 {"MSPIPE_TC_SPLITS": "2"}, {"MSPIPE_TC_BIG_S": "2"}, {"MSPIPE_TC_BIG_S": "4"},
+                                 {"MSPIPE_TC_SPLITS": "1"}, {"MSPIPE_TC_SPLITS": "2"}, {"MSPIPE_TC_BIG_S": "4"},
                                  {"MSPIPE_PREP_SMEM": "0", "MSPIPE_PREP_BPS": "4"}])
 def test_switch_variants_equal_oracle(dev, env, monkeypatch):
     """The library's experiment switches (read at every launch) keep the oracle's
     results: the GEMM epilogue writing mem_ts / mail itself (no write-back
-    branch), the sampler without its per-node search hints, S = 2 at wiki size (two K chunks
-    per TMEM buffer), S = 2 and 4 at GDELT size (default 1), the dedup table in global memory."""
+    branch), the sampler without its per-node search hints, S = 1 and 2 at wiki size (three and
+    two K chunks per TMEM buffer; default 4), S = 4 at GDELT size (default 2), the dedup table
+    in global memory."""
     for kk, v in env.items():
         monkeypatch.setenv(kk, v)
     name = "gdelt" if "MSPIPE_TC_BIG_S" in env else "wiki"
