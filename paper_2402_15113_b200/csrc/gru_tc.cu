@@ -561,6 +561,29 @@ __global__ void __launch_bounds__(256) k_build_x(TcArgs a) {
   }
 }
 
+// Gate nonlinearities.  MSPIPE_FAST_GATES (default): σ(x) = 1 / (1 + e^-x)
+// and tanh(x) = 1 - 2 / (1 + e^2x) from the MUFU exponential (__expf) and
+// reciprocal (rcp.approx, 1 ulp): ~1e-7 absolute on σ and tanh against the
+// 1e-4|o| + 1e-6 rule.  The IEEE division (and __frcp_rn) put a slow-path
+// branch around every reciprocal, which serialised the 12 reciprocals of a
+// 4-unit item: ~2 us of a 12 us GDELT tile (phase marks).
+#ifndef MSPIPE_FAST_GATES
+#define MSPIPE_FAST_GATES 1
+#endif
+__device__ __forceinline__ float rcp_approx(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ float gate_sigmoid(float x) {
+  if (MSPIPE_FAST_GATES) return rcp_approx(1.0f + __expf(-x));
+  return 1.0f / (1.0f + expf(-x));
+}
+__device__ __forceinline__ float gate_tanh(float x) {
+  if (MSPIPE_FAST_GATES) return 1.0f - 2.0f * rcp_approx(1.0f + __expf(2.0f * x));
+  return tanhf(x);
+}
+
 // GRUCell gates (G5): r = σ(.), z = σ(.), n = tanh(x_n + r h_n), h' = (1 - z) n + z h.
 __device__ __forceinline__ float4 gates4(const float* pr, const float* pz, const float* pnx, const float* pnh,
                                          float4 h, int32_t cell) {
@@ -568,14 +591,14 @@ __device__ __forceinline__ float4 gates4(const float* pr, const float* pz, const
   float out[4];
   if (cell == MSPIPE_CELL_RNN) {  // RNNCell (row F3): h' = tanh(W_ih x + b_ih + W_hh h + b_hh)
 #pragma unroll
-    for (int e = 0; e < 4; ++e) out[e] = tanhf(pnx[e] + pnh[e]);
+    for (int e = 0; e < 4; ++e) out[e] = gate_tanh(pnx[e] + pnh[e]);
     return make_float4(out[0], out[1], out[2], out[3]);
   }
 #pragma unroll
   for (int e = 0; e < 4; ++e) {
-    const float r = 1.0f / (1.0f + expf(-pr[e]));
-    const float z = 1.0f / (1.0f + expf(-pz[e]));
-    const float n = tanhf(pnx[e] + r * pnh[e]);
+    const float r = gate_sigmoid(pr[e]);
+    const float z = gate_sigmoid(pz[e]);
+    const float n = gate_tanh(pnx[e] + r * pnh[e]);
     out[e] = (1.0f - z) * n + z * hv[e];
   }
   return make_float4(out[0], out[1], out[2], out[3]);
@@ -662,6 +685,11 @@ constexpr bool kMailPf = MSPIPE_MAIL_PF != 0;
 #define MSPIPE_ASYNC_PUSH 1
 #endif
 constexpr bool kAsyncPush = MSPIPE_ASYNC_PUSH != 0;
+// K-split partials of the CTA's own rows stored locally (not through st.async)
+#ifndef MSPIPE_LOCAL_PUSH
+#define MSPIPE_LOCAL_PUSH 1
+#endif
+constexpr bool kLocalPush = MSPIPE_LOCAL_PUSH != 0;
 
 template <bool kBf>
 __global__ void __launch_bounds__(tc::kThreads, 1) k_gru_tc(TcArgs a) {
@@ -888,7 +916,18 @@ __global__ void __launch_bounds__(tc::kThreads, 1) k_gru_tc(TcArgs a) {
                                 (uint32_t)owner);
       if (kAsyncPush) {
         if (ti == 0) cluster_wait();  // every rfull of the cluster is initialised
-        if (threadIdx.x == 0) mbar_arrive_expect_tx(rfull, (uint32_t)(kM * kN * 4));  // S x R rows x kN floats
+        // the peers' rows: (S - 1) x R rows x kN floats (S x R without kLocalPush)
+        if (threadIdx.x == 0) mbar_arrive_expect_tx(rfull, (uint32_t)((kLocalPush ? S - 1 : S) * R * kN * 4));
+      }
+      if (kLocalPush && owner == rank) {
+        // this CTA's own rows: plain shared stores (the __syncthreads below
+        // orders them before the reduction); only the peers' rows travel
+        float4* own = recv + (rank * R + lm) * kRecvRow + half * kH4;
+#pragma unroll
+        for (int c4 = 0; c4 < kH4; ++c4)
+          own[c4] = make_float4(__uint_as_float(r0[4 * c4]), __uint_as_float(r0[4 * c4 + 1]),
+                                __uint_as_float(r0[4 * c4 + 2]), __uint_as_float(r0[4 * c4 + 3]));
+      } else if (kAsyncPush) {
         const uint32_t rbar = mapa(smem_u32(rfull), (uint32_t)owner);
 #pragma unroll
         for (int c4 = 0; c4 < kH4; ++c4)
@@ -954,7 +993,16 @@ __global__ void __launch_bounds__(tc::kThreads, 1) k_gru_tc(TcArgs a) {
           pnx[e] = (&acc[2].x)[e] + bias[2 * kJ + jj];
           pnh[e] = (&acc[3].x)[e] + bias[3 * kJ + jj];
         }
+#if defined(MSPIPE_PHASES) && defined(MSPIPE_DBG_NOSTORE)  // phase experiments only: the math without the stores
+        {
+          const float4 hv = gates4(pr, pz, pnx, pnh, hbuf[mm * kQ + qq], d.cell);
+          if (hv.x == 12345.f) store_h4(a, u, rownode[mm], j0, hv);
+        }
+#elif defined(MSPIPE_PHASES) && defined(MSPIPE_DBG_NOMATH)  // phase experiments only: the stores without the math
+        store_h4(a, u, rownode[mm], j0, make_float4(pr[0], pz[1], pnx[2], pnh[3]));
+#else
         store_h4(a, u, rownode[mm], j0, gates4(pr, pz, pnx, pnh, hbuf[mm * kQ + qq], d.cell));
+#endif
       }
       PHASE(10);
       if (a.commit_mem && !a.skip_meta) commit_rows(a, m0, U, rb, rb + R, jt, J, rownode);
