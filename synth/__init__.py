@@ -6,4 +6,4 @@ negatives, edge features, GRU weights — and holds none of the method's
 arithmetic (no sampling, dedup, staleness, message, GRU or write-back logic).
 """
 from .events import (CONFIGS, WorkloadConfig, edge_features, gru_params, make_events, make_workload,  # noqa: F401
-                     node_features, rnn_params)
+                     node_features, rnn_params, train_params)

@@ -204,6 +204,23 @@ def gru_params(mem_dim: int, mail_dim: int, time_dim: int, seed: int = 1234):
     return dict(w_ih=w_ih, w_hh=w_hh, b_ih=b_ih, b_hh=b_hh, time_w=time_w, time_b=time_b)
 
 
+def train_params(mem_dim: int, time_dim: int, emb_dim: int = 100, seed: int = 4321):
+    """Row F4 weights (embedding attention + link decoder), U(-1/sqrt(fan_in),
+    1/sqrt(fan_in)) like torch.nn.Linear's default init.  Shapes (reading T3/T4
+    in DESIGN.md): w_q [H, M], w_k / w_v [H, M + d_t], w_o [H, H + M], b_o [H],
+    w_1 [H, 2H], b_1 [H], w_2 [H], b_2 [1].  All f32."""
+    rng = _rng(seed, 9)
+    H, M, Dt = emb_dim, mem_dim, time_dim
+
+    def u(shape, fan_in):
+        a = 1.0 / math.sqrt(fan_in)
+        return rng.uniform(-a, a, size=shape).astype(np.float32)
+
+    return dict(w_q=u((H, M), M), w_k=u((H, M + Dt), M + Dt), w_v=u((H, M + Dt), M + Dt),
+                w_o=u((H, H + M), H + M), b_o=u((H,), H + M), w_1=u((H, 2 * H), 2 * H), b_1=u((H,), 2 * H),
+                w_2=u((H,), H), b_2=u((1,), H))
+
+
 def make_workload(name: str, seed: int = 0, num_events: int | None = None, with_features: bool = True,
                   tcsr_events: int | None = None):
     """The first `num_events` events of the config's stream (default: all) with
