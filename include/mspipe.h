@@ -618,6 +618,59 @@ MSPIPE_API mspipe_status mspipe_util_graph_end(void* stream, void** out_exec);
 MSPIPE_API mspipe_status mspipe_util_graph_launch(void* exec, void* stream);
 MSPIPE_API mspipe_status mspipe_util_graph_destroy(void* exec);
 
+/* ------------------------------------------------------------------------
+ * F4 — the MTGNN training stage of one iteration ("the memory updater
+ * computes the updated memory, the MTGNN layer computes the embeddings, and
+ * the loss and backward steps are performed (including all-reduce)", P:L763;
+ * Eq. 2: h^(i)_v = emb(s~^(i)_v, s~^(i)_u | u ∈ N(v)), "emb (e.g.,
+ * a single layer GAT)").  Readings T1-T7 in DESIGN.md §3:
+ *   s~(v) = h'_v (this batch's GRU output) if v is a winner, else the
+ *   fetched snapshot row (T1); q = W_q s~(r), k_u / v_u = W_k / W_v [s~(u) ‖
+ *   φ(Δt_u)], α = softmax(q·k_u/√H) over the cnt valid neighbours, h_r = W_o
+ *   [Σ α_u v_u ‖ s~(r)] + b_o (T3); logit(a, b) = w_2·relu(W_1 [h_a ‖ h_b] +
+ *   b_1) + b_2 (T4); loss = mean BCE over (src_j, dst_j) = 1 and (src_j,
+ *   neg_j) = 0 (T5); gradients of every learnable tensor, through h' into the
+ *   GRU weights (T2); SGD (T6).  The DP all-reduce of `grads` (T7) is the
+ *   caller's (one flat buffer: one collective).
+ *
+ * mspipe_train_layout: the flat parameter layout, returns the float count;
+ *   offsets[13] (nullable) of [w_q (H,M), w_k (H,M+Dt), w_v (H,M+Dt),
+ *   w_o (H,H+M), b_o (H), w_1 (H,2H), b_1 (H), w_2 (H), b_2 (1), w_ih (3M,Dx),
+ *   w_hh (3M,M), b_ih (3M), b_hh (3M)], row-major, each 16-byte aligned.
+ * mspipe_train_create: params / grads are caller-owned device buffers of
+ *   that many floats (params initialised by the caller; the GRU section is
+ *   the master copy: the updater's tensor-core images are repacked from it at
+ *   create and after every SGD step).  gru: a GRUCell, immediate-mailbox,
+ *   MSPIPE_FP32_3XTF32 handle (else MSPIPE_EUNSUPPORTED).  Allocates the
+ *   step's workspace for max_events events (<= the gru's max_events) and a
+ *   cuBLAS handle; fanout <= 31.
+ * mspipe_gru_save_gates: the GEMM epilogue of `gru` also stores every
+ *   winner's gate pre-activations [r | z | n_x | n_h] (biases included) into
+ *   gates [<=2B, 4M] (device; NULL stops it).  Needed by mspipe_train_step.
+ * mspipe_train_step: batch i after its prep and commit — sub_ids [3B, F+1],
+ *   sub_dt [3B, F], sub_cnt [3B] (the sampler outputs of the 3B roots),
+ *   snap_mem [3B(F+1), M] (the fetched subgraph rows), nodes / num_unique
+ *   (winners), new_mem [<=2B, M] (h' in winner order), workspace (the batch's
+ *   GEMM operand images), gates (saved by its GEMM).  Writes *out_loss
+ *   (device f64), out_logits (nullable, [2B]: positives then negatives) and
+ *   the full gradient into grads (overwritten).  Deterministic.  Errors:
+ *   MSPIPE_EINVAL.
+ * mspipe_train_sgd: params -= lr * grads, then repacks the GRU images. */
+typedef struct mspipe_train mspipe_train;
+MSPIPE_API int64_t mspipe_train_layout(int32_t mem_dim, int32_t edge_dim, int32_t time_dim, int32_t emb_dim,
+                                       int64_t* offsets);
+MSPIPE_API mspipe_status mspipe_train_create(mspipe_train** out, const mspipe_gru* gru, int64_t num_nodes,
+                                             int32_t emb_dim, int32_t fanout, int64_t max_events, float* params,
+                                             float* grads, void* stream);
+MSPIPE_API mspipe_status mspipe_train_destroy(mspipe_train* t);
+MSPIPE_API mspipe_status mspipe_gru_save_gates(mspipe_gru* gru, float* gates);
+MSPIPE_API mspipe_status mspipe_train_step(mspipe_train* t, const mspipe_gru* gru, int64_t num_events,
+                                           const int32_t* sub_ids, const float* sub_dt, const int32_t* sub_cnt,
+                                           const float* snap_mem, const int32_t* nodes, const int32_t* num_unique,
+                                           const float* new_mem, const void* workspace, size_t ws_bytes,
+                                           const float* gates, double* out_loss, float* out_logits, void* stream);
+MSPIPE_API mspipe_status mspipe_train_sgd(mspipe_train* t, mspipe_gru* gru, float lr, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -40,7 +40,8 @@ EXPORTS = ("mspipe_abi_version", "mspipe_last_error", "mspipe_check", "mspipe_sa
            "mspipe_gru_apply_commit_out", "mspipe_plan_stale_fractions", "mspipe_staleness_error",
            "mspipe_shard_window_handle", "mspipe_shard_connect", "mspipe_shard_connect_local",
            "mspipe_shard_sent_bytes", "mspipe_util_record_to_device", "mspipe_shard_mitigation_candidates",
-           "mspipe_shard_fetch_finish_table", "mspipe_shard_mitigate")
+           "mspipe_shard_fetch_finish_table", "mspipe_shard_mitigate", "mspipe_train_layout", "mspipe_train_create",
+           "mspipe_train_destroy", "mspipe_gru_save_gates", "mspipe_train_step", "mspipe_train_sgd")
 XCHG_FETCH_IDS, XCHG_FETCH_ROWS, XCHG_COMMIT = 0, 1, 2
 
 
@@ -134,6 +135,13 @@ def lib():
         L.mspipe_shard_mitigation_candidates.argtypes = [P, C.POINTER(Mitigation), P, i64, P, P]
         L.mspipe_shard_fetch_finish_table.argtypes = [P, P, i64, P, P, P]
         L.mspipe_shard_mitigate.argtypes = [P, C.POINTER(Mitigation), P, P, P]
+        L.mspipe_train_layout.argtypes = [i32, i32, i32, i32, P]
+        L.mspipe_train_layout.restype = i64
+        L.mspipe_train_create.argtypes = [C.POINTER(P), P, i64, i32, i32, i64, P, P, P]
+        L.mspipe_train_destroy.argtypes = [P]
+        L.mspipe_gru_save_gates.argtypes = [P, P]
+        L.mspipe_train_step.argtypes = [P, P, i64, P, P, P, P, P, P, P, P, C.c_size_t, P, P, P, P]
+        L.mspipe_train_sgd.argtypes = [P, P, f32, P]
         if L.mspipe_abi_version() != ABI_VERSION:
             raise RuntimeError(f"libmspipe ABI {L.mspipe_abi_version()} != binding {ABI_VERSION}")
         _lib = L
@@ -657,3 +665,51 @@ def memory_writeback(st: MemoryHandle, commit_version, upd, stream=None):
     _ck(lib().mspipe_memory_writeback(st.h, int(commit_version), ptr(upd["nodes"]), ptr(upd["num"]),
                                       upd["nodes"].numel(), ptr(upd["mem"]), ptr(upd["ts"]), ptr(upd["mail"]),
                                       stream_ptr(stream)), "mspipe_memory_writeback")
+
+
+# ---------------------------------------------------------------- row F4
+TRAIN_TENSORS = ("w_q", "w_k", "w_v", "w_o", "b_o", "w_1", "b_1", "w_2", "b_2", "w_ih", "w_hh", "b_ih", "b_hh")
+
+
+def train_layout(mem_dim, edge_dim, time_dim, emb_dim):
+    """(total floats, {tensor: offset}) of the flat parameter / gradient buffer."""
+    off = (i64 * 13)()
+    n = lib().mspipe_train_layout(int(mem_dim), int(edge_dim), int(time_dim), int(emb_dim), off)
+    if n < 0:
+        raise MspipeError(EINVAL, "mspipe_train_layout", "bad dimensions")
+    return int(n), dict(zip(TRAIN_TENSORS, (int(o) for o in off)))
+
+
+class TrainHandle:
+    """mspipe_train over caller-owned (here: this object's) flat params / grads."""
+
+    def __init__(self, gru: GruHandle, num_nodes, emb_dim, fanout, max_events, params: torch.Tensor,
+                 grads: torch.Tensor, stream=None):
+        if not (params.is_cuda and grads.is_cuda and params.dtype == torch.float32 and grads.dtype == torch.float32):
+            raise ValueError("params / grads: CUDA float32 tensors")
+        self.params, self.grads = params, grads
+        h = C.c_void_p()
+        _ck(lib().mspipe_train_create(C.byref(h), gru.h, int(num_nodes), int(emb_dim), int(fanout), int(max_events),
+                                      ptr(params), ptr(grads), stream_ptr(stream)), "mspipe_train_create")
+        self.h = h
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.mspipe_train_destroy(self.h)
+            self.h = None
+
+
+def gru_save_gates(gru: GruHandle, gates):
+    _ck(lib().mspipe_gru_save_gates(gru.h, ptr(gates)), "mspipe_gru_save_gates")
+
+
+def train_step(tr: TrainHandle, gru: GruHandle, num_events, samp, snap_mem, nodes, num, new_mem, workspace, gates,
+               out_loss, out_logits=None, stream=None):
+    _ck(lib().mspipe_train_step(tr.h, gru.h, int(num_events), ptr(samp["sub"]), ptr(samp["dt"]), ptr(samp["cnt"]),
+                                ptr(snap_mem), ptr(nodes), ptr(num), ptr(new_mem), ptr(workspace),
+                                workspace.numel() * workspace.element_size(), ptr(gates), ptr(out_loss),
+                                ptr(out_logits), stream_ptr(stream)), "mspipe_train_step")
+
+
+def train_sgd(tr: TrainHandle, gru: GruHandle, lr, stream=None):
+    _ck(lib().mspipe_train_sgd(tr.h, gru.h, float(lr), stream_ptr(stream)), "mspipe_train_sgd")

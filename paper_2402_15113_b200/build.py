@@ -11,7 +11,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libmspipe.so")
 SOURCES = ["api.cu", "sampler.cu", "memory.cu", "prep.cu", "gru_simt.cu", "gru_tc.cu", "shard.cu", "nccl_xchg.cu", "planner.cu",
-           "stale.cu", "features.cu"]
+           "stale.cu", "features.cu", "train.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 
@@ -27,9 +27,24 @@ def _nccl_dir():
 
 
 NCCL = _nccl_dir()
+
+
+def _cublas_dir():
+    """cuBLAS as torch loads it (nvidia/cublas): the F4 training stage's plain GEMMs."""
+    import importlib.util
+    spec = importlib.util.find_spec("nvidia")
+    for base in (spec.submodule_search_locations if spec else []):
+        d = os.path.join(base, "cublas")
+        if os.path.exists(os.path.join(d, "lib", "libcublas.so.12")):
+            return d
+    raise RuntimeError("libcublas.so.12 not found (expected site-packages/nvidia/cublas)")
+
+
+CUBLAS = _cublas_dir()
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-rdc=true", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC,-fvisibility=hidden", "--expt-relaxed-constexpr",
-         "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-I", os.path.join(NCCL, "include")]
+         "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-I", os.path.join(NCCL, "include"),
+         "-I", os.path.join(_cublas_dir(), "include")]
 
 
 def _stale() -> bool:
@@ -64,7 +79,9 @@ def build(force: bool = False, verbose: bool = False, extra_flags=(), out: str |
     tmp = lib + f".{os.getpid()}.tmp"
     subprocess.check_call([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-rdc=true", "-shared", "-o", tmp, *objs,
                            "-Xcompiler", "-fPIC", "-L", os.path.join(NCCL, "lib"), "-l:libnccl.so.2",
-                           "-Xlinker", "-rpath=" + os.path.join(NCCL, "lib")])
+                           "-Xlinker", "-rpath=" + os.path.join(NCCL, "lib"),
+                           "-L", os.path.join(CUBLAS, "lib"), "-l:libcublas.so.12",
+                           "-Xlinker", "-rpath=" + os.path.join(CUBLAS, "lib")])
     os.replace(tmp, lib)
     return lib
 

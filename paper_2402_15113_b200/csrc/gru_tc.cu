@@ -1001,6 +1001,14 @@ __global__ void __launch_bounds__(tc::kThreads, 1) k_gru_tc(TcArgs a) {
 #elif defined(MSPIPE_PHASES) && defined(MSPIPE_DBG_NOMATH)  // phase experiments only: the stores without the math
         store_h4(a, u, rownode[mm], j0, make_float4(pr[0], pz[1], pnx[2], pnh[3]));
 #else
+        if (d.gates) {  // row F4: the backward of the gates reads the pre-activations (biases included)
+          float4* gs = reinterpret_cast<float4*>(d.gates + (int64_t)u * 4 * d.M + j0);
+          const int32_t q4 = d.M / 4;
+          gs[0] = make_float4(pr[0], pr[1], pr[2], pr[3]);
+          gs[q4] = make_float4(pz[0], pz[1], pz[2], pz[3]);
+          gs[2 * q4] = make_float4(pnx[0], pnx[1], pnx[2], pnx[3]);
+          gs[3 * q4] = make_float4(pnh[0], pnh[1], pnh[2], pnh[3]);
+        }
         store_h4(a, u, rownode[mm], j0, gates4(pr, pz, pnx, pnh, hbuf[mm * kQ + qq], d.cell));
 #endif
       }

@@ -334,6 +334,7 @@ struct GruDesc {
   int32_t bf16;         // 1: bf16 tensor-core operands (MSPIPE_BF16), Kpad a multiple of 64
   int32_t cell;         // MSPIPE_CELL_GRU | MSPIPE_CELL_RNN (row F3)
   int32_t mailbox;      // MSPIPE_MAILBOX_IMMEDIATE | MSPIPE_MAILBOX_DEFERRED (row F3)
+  float* gates;         // optional sink (row F4, mspipe_gru_save_gates): gate pre-activations [rows, 4M]
 };
 void launch_gru_pack(const float* w_ih, const float* w_hh, const float* b_ih, const float* b_hh,
                      const GruDesc& d, float* wpack, float* bias, cudaStream_t s);

@@ -51,6 +51,7 @@ class StageConfig:
     mailbox: str = "immediate"  # row F3: "immediate" (G14) | "deferred" (TGL's TGN; needs fetch_mail)
     features: bool = False     # row F2: fetch node / edge features of the sampled subgraphs (bind_features)
     node_dim: int = 0          # |d_v| (GDELT 413); rows padded to a multiple of 4 floats on the device
+    train: dict | None = None  # row F4: dict(params=train weights, lr, [group]) — training stage after each commit
 
     def use_fused(self) -> bool:
         ok = self.precision in (_C.FP32_3XTF32, _C.BF16) and self.fanout <= 31 and self.batch <= 8192
@@ -205,6 +206,14 @@ class MemoryStage(_TimedOps):
         if self.deferred and not (self.fused and cfg.fetch_mail):
             raise ValueError("mailbox='deferred' runs on the fused tensor-core path with fetch_mail=True")
         self.ws_bytes = _C.gru_workspace_size(self.gru, cfg.batch) if self.fused else 0
+        self.trainer = None
+        if cfg.train is not None:  # row F4
+            if not self.fused or self.deferred or cfg.cell != "gru" or cfg.precision != _C.FP32_3XTF32:
+                raise ValueError("the training stage runs on the fused 3xTF32 GRUCell path (immediate mailbox)")
+            from .train import TrainStage
+            self.trainer = TrainStage(self.gru, params, cfg.train["params"], cfg.num_nodes, cfg.mem_dim,
+                                      cfg.edge_dim, cfg.time_dim, cfg.fanout, cfg.batch, cfg.train.get("lr", 1e-4),
+                                      self.device, group=cfg.train.get("group"))
         self.staged = False
         self.slots = None
         self.timing = None  # optional dict name -> list of (start, end) events per op
@@ -472,6 +481,10 @@ class MemoryStage(_TimedOps):
             _C.memory_mail_deferred(self.memory, i, x["src"], x["dst"], x["ts"], x["ef"], upd["nodes"], upd["winner"],
                                     upd["num"])
         self._ev("update_end")
+        if self.trainer is not None:  # row F4: embeddings, loss, backward, (all-reduce,) SGD of batch i
+            self._ev("train")
+            self.trainer.step(i, n, sl.samp, sl.mem, upd, sl.ws, sgd=cfg.train.get("sgd", True))
+            self._ev("train_end")
         if self.staged:
             self._pending_out = i  # the GEMM filled the result record
         else:
