@@ -25,6 +25,16 @@ def flat_params(gru_params: dict, train_params: dict, mem_dim, edge_dim, time_di
     return flat, off
 
 
+def allreduce_grads(grads: torch.Tensor, group=None) -> int:
+    """T7: sum the flat gradient buffer over the data-parallel ranks (one
+    collective); returns the world size (the SGD step divides the rate by it)."""
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    if world > 1:
+        dist.all_reduce(grads, group=group)
+    return world
+
+
 class TrainStage:
     """Owns the flat parameter / gradient buffers (device), the gate sink of the
     updater's GEMM and a per-batch loss ring."""
@@ -67,9 +77,5 @@ class TrainStage:
                       self.gates, self.losses[(i - 1) % self.losses.numel():][:1], self.logits[: 2 * num_events])
         if not sgd:
             return
-        world = 1
-        if self.group is not None:
-            import torch.distributed as dist
-            world = dist.get_world_size(self.group)
-            dist.all_reduce(self.grads, group=self.group)  # sum; the lr below takes the mean (T7)
+        world = allreduce_grads(self.grads, self.group) if self.group is not None else 1  # sum; lr / world: mean
         _C.train_sgd(self.h, self.gru, self.lr / world)
