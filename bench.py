@@ -185,6 +185,25 @@ def algorithmic(cfg, stage_cfg, U):
                 update=upd_bytes, update_flops=upd_flops, writeback=wb, features=feats)
 
 
+def train_flops(cfg, H=100):
+    """FLOPs of the row F4 step's contractions (2 m n k each):
+    forward projections / embedding / decoder, their weight and input
+    gradients, the GRU weight gradient over the 2B rows the GEMMs run on."""
+    B, F, M, Dt = cfg.batch, cfg.fanout, cfg.mem_dim, cfg.time_dim
+    Dx = 2 * M + cfg.edge_dim + Dt
+    R, RF, Z = 3 * B, 3 * B * F, M + Dt
+    mnk = [(R, H, M), (RF, 2 * H, Z), (R, H, H + M), (2 * B, H, 2 * H),            # forward
+           (H, 2 * H, 2 * B), (2 * B, 2 * H, H), (H, H + M, R), (R, H + M, H),     # decoder / W_o grads
+           (H, M, R), (R, M, H), (2 * H, Z, RF), (RF, M, 2 * H),                   # attention grads
+           (3 * M, Dx, 2 * B), (2 * M, M, 2 * B), (M, M, 2 * B)]                   # GRU weight grads
+    return float(sum(2 * m * n * k for m, n, k in mnk))
+
+
+def fp32_simt_peak_tflops(sm_mhz):
+    """CUDA-core fp32 peak: 148 SMs x 128 FMA lanes x 2 FLOP x clock (B200_PROFILING.md unit counts)."""
+    return 148 * 128 * 2 * sm_mhz * 1e6 / 1e12
+
+
 def run_mspipe(args):
     import torch
     import torch.distributed as dist
@@ -396,6 +415,53 @@ def run_mspipe(args):
         med = order[len(order) // 2]
         return rates[med], blocks[med][0] / K, rates, blocks[med][1]
 
+    def train_measurement():
+        """Memory stage + training stage (forward, backward, SGD) per step, the
+        same grouped graphs and flush protocol; the train op alone (bracketed,
+        in the two-stream step) against the CUDA-core fp32 peak."""
+        import dataclasses
+
+        from synth import train_params
+        sct = dataclasses.replace(sc, train=dict(params=train_params(cfg.mem_dim, cfg.time_dim, 100), lr=1e-4))
+
+        def mk():
+            stt = MemoryStage(sct, w["params"], g, dev)
+            t = resident
+            stt.bind_resident(t["src"], t["dst"], t["ts"], t["neg"], t["ef"])
+            return stt
+        stt = mk()
+        gr_t, s_t = capture_groups(stt, gs)
+        torch.cuda.synchronize()
+        with ClockSampler(local) as clk_t:
+            ms_t, tb_t, _ = timed_run_groups(stt, gr_t, s_t, W, K, gs)
+        _C.check(s_t)
+        loss = stt.trainer.losses[: min(nb, stt.trainer.losses.numel())]
+        finite = bool(torch.isfinite(loss).all().item())
+        ev_t = sum(min(cfg.batch, E - b * cfg.batch) for b in tb_t)
+        del gr_t, stt
+        sti = mk()
+        gi, si = capture_groups(sti, gs, op="train")
+        _, _, opm = timed_run_groups(sti, gi, si, W, K, gs, op="train")
+        _C.check(si)
+        del gi, sti
+        t_ms = float(np.mean(opm))
+        fl = train_flops(cfg)
+        clk = clk_t.summary()
+        peak = fp32_simt_peak_tflops((clk or {}).get("sm_mhz") or 1965.0)
+        ach = fl / (t_ms / 1e3) / 1e12
+        return {"metric": "memory stage + MTGNN training stage (row F4) events/s", "unit": UNIT,
+                "value": ev_t / (sum(ms_t) / 1e3), "ms_per_step": float(sum(ms_t)) / K,
+                "train_ms_in_step": t_ms, "losses_finite": finite,
+                "roofline": {"kernel": "row F4 step (cuBLAS SGEMM projections / gradients + attention, "
+                                       "decoder, scatter and GRU-backward kernels)",
+                             "bound": "alu", "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
+                             "flops_per_step": fl,
+                             "peak_source": "148 SMs x 128 fp32 lanes x 2 x median SM clock (CUDA cores: the "
+                                            "contractions run as fp32 SGEMM for the 1e-4 parity rule)"},
+                "config": {"emb_dim": 100, "lr": 1e-4, "attention": "single-head, 10 neighbours",
+                           "decoder": "TGN link MLP", "optimizer": "SGD"},
+                "clocks": clk}
+
     # ---- device-resident run (the `value`) ---------------------------------
     blocks, clocks, st = run_blocks(False)
     value, ms_step, rates, timed_batches = block_value(blocks)
@@ -502,6 +568,12 @@ def run_mspipe(args):
             print(json.dumps(out))
         return
     del st
+    # ---- row F4: the same steps with the training stage after every commit ----
+    if ws == 1 and not args.no_train and getattr(sc, "use_fused")() and args.gru == "tc" and not args.features:
+        try:
+            out["train"] = train_measurement()
+        except Exception as ex:  # reported, never hides the headline
+            out["train"] = {"error": f"{type(ex).__name__}: {ex}"}
     # ---- e2e: host buffers through the same C-ABI calls ---------------------
     blocks2, _, st2 = run_blocks(True)
     v2, ms2, _, _ = block_value(blocks2)
@@ -813,6 +885,7 @@ def main():
                     help="events the sampler's T-CSR is built from (default: the whole stream for GDELT, else "
                          "--events)")
     ap.add_argument("--no-probe", action="store_true", help="skip the N = 10^7 HBM probe of the A3/A7 kernels")
+    ap.add_argument("--no-train", action="store_true", help="skip the row F4 (training stage) measurement")
     ap.add_argument("--profile", action="store_true", help="short run for ncu: no flush/e2e/cpu")
     ap.add_argument("--graph-steps", type=int, default=8,
                     help="consecutive steps captured per CUDA graph (1: one graph per step); N = 1 only")

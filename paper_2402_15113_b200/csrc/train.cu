@@ -397,6 +397,7 @@ struct mspipe_train {
   int32_t *key, *val, *skey, *sval;
   void* sort_tmp;
   size_t sort_bytes;
+  void* blas_ws;  // cuBLAS workspace owned here: no allocation inside a CUDA-graph capture
   cublasHandle_t blas;
 };
 
@@ -404,7 +405,7 @@ static void train_free(mspipe_train* t) {
   if (!t) return;
   void* bufs[] = {t->wmap, t->sroot, t->zn, t->q, t->kv, t->alpha, t->zo, t->emb, t->za, t->pre, t->y, t->logit,
                   t->dlogit, t->dpre, t->dza, t->demb, t->dzo, t->dq, t->dkv, t->dzn, t->dhn, t->D, t->xp, t->ones,
-                  t->cs, t->term, t->key, t->val, t->skey, t->sval, t->sort_tmp};
+                  t->cs, t->term, t->key, t->val, t->skey, t->sval, t->sort_tmp, t->blas_ws};
   for (void* b : bufs)
     if (b) cudaFree(b);
   if (t->blas) cublasDestroy(t->blas);
@@ -482,11 +483,15 @@ mspipe_status mspipe_train_create(mspipe_train** out, const mspipe_gru* gru, int
   if (e == cudaSuccess)
     e = cub::DeviceRadixSort::SortPairs(nullptr, t->sort_bytes, t->key, t->skey, t->val, t->sval, (int)slots, 0, 15);
   if (e == cudaSuccess) e = cudaMalloc(&t->sort_tmp, t->sort_bytes);
+  constexpr size_t kBlasWs = 32u << 20;
+  if (e == cudaSuccess) e = cudaMalloc(&t->blas_ws, kBlasWs);
   if (e != cudaSuccess) {
     train_free(t);
     return cuda_status(e, "train_create: allocation");
   }
-  if (cublasCreate(&t->blas) != CUBLAS_STATUS_SUCCESS || cublasSetMathMode(t->blas, CUBLAS_DEFAULT_MATH) != CUBLAS_STATUS_SUCCESS) {
+  if (cublasCreate(&t->blas) != CUBLAS_STATUS_SUCCESS ||
+      cublasSetMathMode(t->blas, CUBLAS_DEFAULT_MATH) != CUBLAS_STATUS_SUCCESS ||
+      cublasSetWorkspace(t->blas, t->blas_ws, kBlasWs) != CUBLAS_STATUS_SUCCESS) {
     t->blas = nullptr;
     train_free(t);
     return fail(MSPIPE_ECUDA, "train_create: cublasCreate failed");
@@ -547,7 +552,10 @@ mspipe_status mspipe_train_step(mspipe_train* t, const mspipe_gru* gru, int64_t 
     return fail(MSPIPE_EINVAL, "train_step: workspace of %zu bytes too small", ws_bytes);
   if (num_events == 0) return MSPIPE_OK;
   cudaStream_t s = (cudaStream_t)stream;
-  if (cublasSetStream(t->blas, s) != CUBLAS_STATUS_SUCCESS) return fail(MSPIPE_ECUDA, "train_step: cublasSetStream");
+  // cublasSetStream resets the workspace to the default pool: re-attach ours
+  if (cublasSetStream(t->blas, s) != CUBLAS_STATUS_SUCCESS ||
+      cublasSetWorkspace(t->blas, t->blas_ws, 32u << 20) != CUBLAS_STATUS_SUCCESS)
+    return fail(MSPIPE_ECUDA, "train_step: cublasSetStream / cublasSetWorkspace");
   const Dims& d = t->d;
   const int64_t B = num_events, R = 3 * B, F = d.F, M = d.M, H = d.H, Z = d.M + d.Dt, B2 = 2 * B;
   const int64_t slots = R * (F + 1);
