@@ -1,0 +1,18 @@
+#!/bin/bash
+# Row F4 on the GPU: its parity tests, then the GDELT and wiki benches with the training measurement
+cd "$GRAFT_REPO_ROOT" || exit 1
+mkdir -p gpurun_out
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build_za.log 2>&1
+timeout 1200 python -m pytest tests/test_gpu_train.py -q -x -s > gpurun_out/pytest_train.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_train.log
+tail -30 gpurun_out/pytest_train.log
+timeout 900 python bench.py --no-probe --no-cpu > gpurun_out/za_bench_gdelt.json 2> gpurun_out/za_bench_gdelt.err
+timeout 600 python bench.py --config wiki --no-probe --no-cpu > gpurun_out/za_bench_wiki.json 2> gpurun_out/za_bench_wiki.err
+python - <<'PY'
+import json
+for f in ("gpurun_out/za_bench_gdelt.json", "gpurun_out/za_bench_wiki.json"):
+    try:
+        d = json.load(open(f))
+    except Exception as e:
+        print(f, "FAILED", e); continue
+    print(f, "%.2f Mev/s" % (d["value"] / 1e6), "%.2f us/step" % (d["ms_per_step"] * 1e3), "train:", json.dumps(d.get("train"))[:600])
+PY
