@@ -53,3 +53,8 @@ dead = ~act
 if dead.any():
     col = ph[dead, 9] - t0
     print(f"dead entry min {col.min()/1e3:8.2f} med {np.median(col)/1e3:8.2f} max {col.max()/1e3:8.2f} us  n={dead.sum()}")
+# kernel-level spread: every CTA's entry and end against the earliest entry
+ent = ph[:, 9] - t0
+end = ph[act, 8] - t0
+print(f"entry spread (all CTAs)  min {ent.min()/1e3:8.2f} med {np.median(ent)/1e3:8.2f} max {ent.max()/1e3:8.2f} us")
+print(f"end   (active CTAs)      min {end.min()/1e3:8.2f} med {np.median(end)/1e3:8.2f} max {end.max()/1e3:8.2f} us")

@@ -16,3 +16,8 @@ for f in ("gpurun_out/za_bench_gdelt.json", "gpurun_out/za_bench_wiki.json"):
         print(f, "FAILED", e); continue
     print(f, "%.2f Mev/s" % (d["value"] / 1e6), "%.2f us/step" % (d["ms_per_step"] * 1e3), "train:", json.dumps(d.get("train"))[:600])
 PY
+# GEMM phases: CTA entry spread vs the kernel duration (serialised step: EXP_COLD runs the commit alone)
+for c in gdelt wiki; do
+  EXP_COLD=1 timeout 600 python scripts/exp_gru_phases.py $c > gpurun_out/za_phases_$c.txt 2>&1
+done
+tail -20 gpurun_out/za_phases_gdelt.txt gpurun_out/za_phases_wiki.txt
