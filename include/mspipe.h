@@ -618,6 +618,46 @@ MSPIPE_API mspipe_status mspipe_util_graph_end(void* stream, void** out_exec);
 MSPIPE_API mspipe_status mspipe_util_graph_launch(void* exec, void* stream);
 MSPIPE_API mspipe_status mspipe_util_graph_destroy(void* exec);
 
+/* Row F3 — the APAN updater ("modified from TGL"; "RNN as the
+ * memory update function while incorporating an attention mechanism ...
+ * asynchronous propagation"; readings F3-4..F3-8 in DESIGN.md).  The GRU
+ * handle is a deferred-mailbox GRUCell MSPIPE_FP32_3XTF32 one (x = [message
+ * (Dm) | cos(ω Δt + ϕ)], so the weights have the TGN shapes).
+ *   Mailbox tables (caller-owned device memory, zeroed by the caller for an
+ *   epoch start): mb [num_nodes, slots, Dm] f32, mb_ts [num_nodes, slots]
+ *   f64, mb_pos / mb_cnt [num_nodes] int32 (next ring slot, filled slots).
+ *   w_q [M, M], w_k [M, Dm] (host or device f32; copied at create).
+ * mspipe_message_build_apan (A5 of APAN, after mspipe_memory_prep of the
+ *   batch): for winner w, q = W_q S.mem[w], k_s = W_k mb[w, s] over its
+ *   filled slots, α = softmax(q·k / √M), x = [Σ α mb[w, s] ‖ cos(ω Δt + ϕ)],
+ *   Δt = t* - S.mem_ts[w], h = S.mem[w] (snap rows in root layout, as
+ *   mspipe_message_build_deferred), into the GEMM operand `workspace`;
+ *   out_ts [<=2B] = t*.  The mailbox is read from the tables: the caller
+ *   orders the call after the previous delivery (k = 0 in the stage).
+ * Then mspipe_gru_apply_commit(new_mail = NULL) commits h' and mem_ts.
+ * mspipe_apan_deliver (after that commit, version commit_version): mail of
+ *   winner w = [mem[w] | mem[o] | e_ev] from the committed tables, time
+ *   t_ev, delivered to w and to the sampled neighbours of w's root row (nbr
+ *   / cnt: the prep's sampler outputs [3B, fanout], [3B]); per node the mail
+ *   with the largest key p (fanout + 1) + s wins (s = 0: itself, 1 + j:
+ *   neighbour j) and fills the node's next ring slot.  world == 1 only. */
+typedef struct mspipe_apan mspipe_apan;
+MSPIPE_API mspipe_status mspipe_apan_create(mspipe_apan** out, int64_t num_nodes, int32_t mem_dim, int32_t edge_dim,
+                                            int32_t slots, int64_t max_events, const float* w_q, const float* w_k,
+                                            float* mb, double* mb_ts, int32_t* mb_pos, int32_t* mb_cnt, void* stream);
+MSPIPE_API mspipe_status mspipe_apan_destroy(mspipe_apan* a);
+MSPIPE_API mspipe_status mspipe_message_build_apan(mspipe_apan* a, const mspipe_gru* gru, const double* ts,
+                                                   int64_t num_events, const float* snap_mem,
+                                                   const double* snap_mem_ts, int64_t snap_step,
+                                                   const int32_t* nodes, const int32_t* winner,
+                                                   const int32_t* num_unique, double* out_ts, void* workspace,
+                                                   size_t ws_bytes, void* stream);
+MSPIPE_API mspipe_status mspipe_apan_deliver(mspipe_apan* a, mspipe_memory* st, int64_t commit_version,
+                                             const int32_t* src, const int32_t* dst, const double* ts,
+                                             const float* edge_feat, int64_t num_events, const int32_t* nodes,
+                                             const int32_t* winner, const int32_t* num_unique, const int32_t* nbr,
+                                             const int32_t* cnt, int32_t fanout, void* stream);
+
 /* ------------------------------------------------------------------------
  * F4 — the MTGNN training stage of one iteration ("the memory updater
  * computes the updated memory, the MTGNN layer computes the embeddings, and

@@ -41,7 +41,8 @@ EXPORTS = ("mspipe_abi_version", "mspipe_last_error", "mspipe_check", "mspipe_sa
            "mspipe_shard_window_handle", "mspipe_shard_connect", "mspipe_shard_connect_local",
            "mspipe_shard_sent_bytes", "mspipe_util_record_to_device", "mspipe_shard_mitigation_candidates",
            "mspipe_shard_fetch_finish_table", "mspipe_shard_mitigate", "mspipe_train_layout", "mspipe_train_create",
-           "mspipe_train_destroy", "mspipe_gru_save_gates", "mspipe_train_step", "mspipe_train_sgd")
+           "mspipe_train_destroy", "mspipe_gru_save_gates", "mspipe_train_step", "mspipe_train_sgd",
+           "mspipe_apan_create", "mspipe_apan_destroy", "mspipe_message_build_apan", "mspipe_apan_deliver")
 XCHG_FETCH_IDS, XCHG_FETCH_ROWS, XCHG_COMMIT = 0, 1, 2
 
 
@@ -142,6 +143,10 @@ def lib():
         L.mspipe_gru_save_gates.argtypes = [P, P]
         L.mspipe_train_step.argtypes = [P, P, i64, P, P, P, P, P, P, P, P, C.c_size_t, P, P, P, P]
         L.mspipe_train_sgd.argtypes = [P, P, f32, P]
+        L.mspipe_apan_create.argtypes = [C.POINTER(P), i64, i32, i32, i32, i64, P, P, P, P, P, P, P]
+        L.mspipe_apan_destroy.argtypes = [P]
+        L.mspipe_message_build_apan.argtypes = [P, P, P, i64, P, P, i64, P, P, P, P, P, C.c_size_t, P]
+        L.mspipe_apan_deliver.argtypes = [P, P, i64, P, P, P, P, i64, P, P, P, P, P, i32, P]
         if L.mspipe_abi_version() != ABI_VERSION:
             raise RuntimeError(f"libmspipe ABI {L.mspipe_abi_version()} != binding {ABI_VERSION}")
         _lib = L
@@ -713,3 +718,47 @@ def train_step(tr: TrainHandle, gru: GruHandle, num_events, samp, snap_mem, node
 
 def train_sgd(tr: TrainHandle, gru: GruHandle, lr, stream=None):
     _ck(lib().mspipe_train_sgd(tr.h, gru.h, float(lr), stream_ptr(stream)), "mspipe_train_sgd")
+
+
+# ---------------------------------------------------------------- row F3, APAN
+class ApanHandle:
+    """mspipe_apan over this object's mailbox tables (ring of `slots` mails per node)."""
+
+    def __init__(self, num_nodes, mem_dim, edge_dim, slots, max_events, w_q, w_k, device, stream=None):
+        Dm = 2 * mem_dim + edge_dim
+        self.slots = slots
+        self.mb = torch.zeros((num_nodes, slots, Dm), dtype=torch.float32, device=device)
+        self.mb_ts = torch.zeros((num_nodes, slots), dtype=torch.float64, device=device)
+        self.mb_pos = torch.zeros((num_nodes,), dtype=torch.int32, device=device)
+        self.mb_cnt = torch.zeros((num_nodes,), dtype=torch.int32, device=device)
+        wq = torch.as_tensor(w_q, dtype=torch.float32).contiguous().to(device)
+        wk = torch.as_tensor(w_k, dtype=torch.float32).contiguous().to(device)
+        h = C.c_void_p()
+        _ck(lib().mspipe_apan_create(C.byref(h), int(num_nodes), int(mem_dim), int(edge_dim), int(slots),
+                                     int(max_events), ptr(wq), ptr(wk), ptr(self.mb), ptr(self.mb_ts),
+                                     ptr(self.mb_pos), ptr(self.mb_cnt), stream_ptr(stream)), "mspipe_apan_create")
+        self.h = h
+
+    def reset(self):
+        for t in (self.mb, self.mb_ts, self.mb_pos, self.mb_cnt):
+            t.zero_()
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.mspipe_apan_destroy(self.h)
+            self.h = None
+
+
+def message_build_apan(ap: ApanHandle, gru: GruHandle, ts, snap_mem, snap_mem_ts, snap_step, nodes, winner, num,
+                       out_ts, workspace, stream=None):
+    _ck(lib().mspipe_message_build_apan(ap.h, gru.h, ptr(ts), ts.numel(), ptr(snap_mem), ptr(snap_mem_ts),
+                                        int(snap_step), ptr(nodes), ptr(winner), ptr(num), ptr(out_ts),
+                                        ptr(workspace), workspace.numel() * workspace.element_size(),
+                                        stream_ptr(stream)), "mspipe_message_build_apan")
+
+
+def apan_deliver(ap: ApanHandle, st: MemoryHandle, commit_version, src, dst, ts, ef, nodes, winner, num, nbr, cnt,
+                 fanout, stream=None):
+    _ck(lib().mspipe_apan_deliver(ap.h, st.h, int(commit_version), ptr(src), ptr(dst), ptr(ts), ptr(ef), src.numel(),
+                                  ptr(nodes), ptr(winner), ptr(num), ptr(nbr), ptr(cnt), int(fanout),
+                                  stream_ptr(stream)), "mspipe_apan_deliver")

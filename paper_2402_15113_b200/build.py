@@ -11,7 +11,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libmspipe.so")
 SOURCES = ["api.cu", "sampler.cu", "memory.cu", "prep.cu", "gru_simt.cu", "gru_tc.cu", "shard.cu", "nccl_xchg.cu", "planner.cu",
-           "stale.cu", "features.cu", "train.cu"]
+           "stale.cu", "features.cu", "train.cu", "apan.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 

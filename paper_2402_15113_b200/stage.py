@@ -48,7 +48,8 @@ class StageConfig:
     double_buffer: bool | None = None  # two table sets (mspipe_memory_double_buffer); default: k >= 1
     plan: tuple | None = None  # schedule "plan": paper staleness k_i per iteration (row F1)
     cell: str = "gru"           # row F3: "gru" (TGN, APAN) | "rnn" (JODIE's RNNCell updater)
-    mailbox: str = "immediate"  # row F3: "immediate" (G14) | "deferred" (TGL's TGN; needs fetch_mail)
+    mailbox: str = "immediate"  # row F3: "immediate" (G14) | "deferred" (TGL's TGN; needs fetch_mail) | "apan"
+    apan: dict | None = None    # row F3, mailbox="apan": dict(w_q [M, M], w_k [M, Dm], slots=10); k = 0
     features: bool = False     # row F2: fetch node / edge features of the sampled subgraphs (bind_features)
     node_dim: int = 0          # |d_v| (GDELT 413); rows padded to a multiple of 4 floats on the device
     train: dict | None = None  # row F4: dict(params=train weights, lr, [group]) — training stage after each commit
@@ -197,12 +198,21 @@ class MemoryStage(_TimedOps):
         self.memory = _C.MemoryHandle(cfg.num_nodes, cfg.mem_dim, cfg.edge_dim, cfg.k, self.device,
                                       double_buffer=cfg.use_double_buffer())
         self.deferred = cfg.mailbox == "deferred"
+        self.apan = None
+        if cfg.mailbox == "apan":  # row F3: APAN (multi-slot mailbox, attention message, propagation)
+            if cfg.k != 0 or cfg.cell != "gru" or cfg.precision != _C.FP32_3XTF32 or cfg.apan is None:
+                raise ValueError("mailbox='apan' runs at k = 0 on the 3xTF32 GRUCell path with cfg.apan weights")
+            self.apan = _C.ApanHandle(cfg.num_nodes, cfg.mem_dim, cfg.edge_dim, cfg.apan.get("slots", 10), cfg.batch,
+                                      cfg.apan["w_q"], cfg.apan["w_k"], self.device)
         self.gru = _C.GruHandle(cfg.mem_dim, cfg.edge_dim, cfg.time_dim, params, self.device, cfg.precision,
                                 max_events=cfg.batch, cell=_C.CELL_RNN if cfg.cell == "rnn" else _C.CELL_GRU,
-                                mailbox=_C.MAILBOX_DEFERRED if self.deferred else _C.MAILBOX_IMMEDIATE)
+                                mailbox=(_C.MAILBOX_DEFERRED if (self.deferred or self.apan is not None)
+                                         else _C.MAILBOX_IMMEDIATE))
         self.upd = _C.alloc_update(cfg.batch, cfg.mem_dim, self.memory.mail_stride, self.device)
         self.fused = cfg.use_fused()
         self._dbg_one = torch.zeros(1, device=self.device) if _DEBUG_ONLY else None  # timing diagnostics
+        if self.apan is not None and not self.fused:
+            raise ValueError("mailbox='apan' runs on the fused tensor-core path")
         if self.deferred and not (self.fused and cfg.fetch_mail):
             raise ValueError("mailbox='deferred' runs on the fused tensor-core path with fetch_mail=True")
         self.ws_bytes = _C.gru_workspace_size(self.gru, cfg.batch) if self.fused else 0
@@ -412,7 +422,10 @@ class MemoryStage(_TimedOps):
             self._fetched = torch.cuda.Event()  # the state tables have been read for batch i
             self._fetched.record()
         self._ev("build")
-        if self.deferred:  # row F3: the message is the stored mail of the snapshot
+        if self.apan is not None:  # row F3 APAN: attention over the node's mailbox slots
+            _C.message_build_apan(self.apan, self.gru, x["ts"], sl.mem, sl.mem_ts, cfg.fanout + 1, sl.dd["nodes"][: 2 * n],
+                                  sl.dd["winner"][: 2 * n], sl.dd["num"], sl.uts[: 2 * n], sl.ws)
+        elif self.deferred:  # row F3: the message is the stored mail of the snapshot
             _C.message_build_deferred(self.gru, x["ts"], sl.mem, sl.mem_ts, sl.mail, cfg.fanout + 1,
                                       sl.dd["winner"][: 2 * n], sl.dd["num"], sl.uts[: 2 * n], sl.ws)
         else:
@@ -428,7 +441,7 @@ class MemoryStage(_TimedOps):
         upd = {k: v[: 2 * n] for k, v in base.items() if k not in ("nodes", "winner", "num")}
         upd.update(nodes=sl.dd["nodes"][: 2 * n], winner=sl.dd["winner"][: 2 * n], num=sl.dd["num"])
         if self.fused:
-            upd.update(ts=sl.uts[: 2 * n], mail=None if self.deferred else sl.umail[: 2 * n])
+            upd.update(ts=sl.uts[: 2 * n], mail=None if (self.deferred or self.apan is not None) else sl.umail[: 2 * n])
         return upd
 
     def update(self, i):
@@ -480,6 +493,10 @@ class MemoryStage(_TimedOps):
             x = self.inputs(i)
             _C.memory_mail_deferred(self.memory, i, x["src"], x["dst"], x["ts"], x["ef"], upd["nodes"], upd["winner"],
                                     upd["num"])
+        if self.apan is not None:  # row F3 APAN: mails from the committed memories, to the node and its neighbours
+            x = self.inputs(i)
+            _C.apan_deliver(self.apan, self.memory, i, x["src"], x["dst"], x["ts"], x["ef"], upd["nodes"], upd["winner"],
+                            upd["num"], sl.samp["nbr"], sl.samp["cnt"], cfg.fanout)
         self._ev("update_end")
         if self.trainer is not None:  # row F4: embeddings, loss, backward, (all-reduce,) SGD of batch i
             self._ev("train")
