@@ -21,3 +21,5 @@ for c in gdelt wiki; do
   EXP_COLD=1 timeout 600 python scripts/exp_gru_phases.py $c > gpurun_out/za_phases_$c.txt 2>&1
 done
 tail -20 gpurun_out/za_phases_gdelt.txt gpurun_out/za_phases_wiki.txt
+timeout 900 python -m pytest tests/test_gpu_apan.py -q -x -s > gpurun_out/pytest_apan.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_apan.log
+tail -15 gpurun_out/pytest_apan.log
