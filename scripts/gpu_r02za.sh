@@ -5,6 +5,8 @@ mkdir -p gpurun_out
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build_za.log 2>&1
 timeout 1200 python -m pytest tests/test_gpu_train.py -q -x -s > gpurun_out/pytest_train.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_train.log
 tail -30 gpurun_out/pytest_train.log
+timeout 900 python -m pytest tests/test_gpu_apan.py -q -x -s > gpurun_out/pytest_apan.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_apan.log
+tail -15 gpurun_out/pytest_apan.log
 timeout 900 python bench.py --no-probe --no-cpu > gpurun_out/za_bench_gdelt.json 2> gpurun_out/za_bench_gdelt.err
 timeout 600 python bench.py --config wiki --no-probe --no-cpu > gpurun_out/za_bench_wiki.json 2> gpurun_out/za_bench_wiki.err
 python - <<'PY'
@@ -21,5 +23,3 @@ for c in gdelt wiki; do
   EXP_COLD=1 timeout 600 python scripts/exp_gru_phases.py $c > gpurun_out/za_phases_$c.txt 2>&1
 done
 tail -20 gpurun_out/za_phases_gdelt.txt gpurun_out/za_phases_wiki.txt
-timeout 900 python -m pytest tests/test_gpu_apan.py -q -x -s > gpurun_out/pytest_apan.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_apan.log
-tail -15 gpurun_out/pytest_apan.log
