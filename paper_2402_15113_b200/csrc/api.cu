@@ -819,21 +819,33 @@ static mspipe_status apply_commit_impl(const mspipe_gru* gru, mspipe_memory* st,
     const bool split = new_mail && gru->d.mailbox == MSPIPE_MAILBOX_IMMEDIATE && env_int("MSPIPE_SPLIT_COMMIT", 1);
     cudaStream_t side = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    // MSPIPE_WB_FIRST=0: the GEMM is enqueued before the write-back branch, so its
+    // one-CTA-per-SM grid is dispatched before the branch's blocks fill the SMs
+    const bool wb_first = env_int("MSPIPE_WB_FIRST", 1) != 0;
+    auto branch = [&]() -> cudaError_t {
+      launch_writeback(nodes, num_unique, max_n, nullptr, new_ts, new_mail, 0, st->mail_stride, t.mem, t.mem_ts,
+                       t.mail, t.mail_ts, st->num_nodes, side);
+      return cudaEventRecord(ev_join, side);
+    };
     if (split) {
       cudaError_t e = aux_stream(st, &side, &ev_fork, &ev_join, 0);
       if (e == cudaSuccess) e = cudaEventRecord(ev_fork, s);
       if (e == cudaSuccess) e = cudaStreamWaitEvent(side, ev_fork, 0);
       if (e != cudaSuccess) return cuda_status(e, "gru_apply_commit: fork");
-      launch_writeback(nodes, num_unique, max_n, nullptr, new_ts, new_mail, 0, st->mail_stride, t.mem, t.mem_ts,
-                       t.mail, t.mail_ts, st->num_nodes, side);
-      e = cudaEventRecord(ev_join, side);
-      if (e != cudaSuccess) return cuda_status(e, "gru_apply_commit: writeback branch");
+      if (wb_first) {
+        e = branch();
+        if (e != cudaSuccess) return cuda_status(e, "gru_apply_commit: writeback branch");
+      }
       c.skip_meta = 1;
     }
     cudaError_t e = launch_gru_tc(gru->d, gru->wtc, (float*)workspace, nullptr, num_events, nullptr, snap_mem, nullptr,
                                   snap_step, snap_h, winner, num_unique, out_mem, nullptr, nullptr, 0,
                                   s, kGruGemm, &c);
     if (e != cudaSuccess) return cuda_status(e, "gru_apply_commit: launch");
+    if (split && !wb_first) {
+      e = branch();
+      if (e != cudaSuccess) return cuda_status(e, "gru_apply_commit: writeback branch");
+    }
     if (split) {
       e = cudaStreamWaitEvent(s, ev_join, 0);
       if (e != cudaSuccess) return cuda_status(e, "gru_apply_commit: join");
