@@ -108,7 +108,8 @@ __global__ void __launch_bounds__(kTrThreads) k_tr_attn_fwd(Dims d, int64_t R, c
                                                             const float* __restrict__ kv,
                                                             const float* __restrict__ sroot, float* alpha,
                                                             float* zo) {
-  const int lane = threadIdx.x & 31;
+  __shared__ float s_al[kTrThreads / 32][32];  // the warp's α (lane = neighbour): no shuffles in ragged loops
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int32_t F = d.F, H = d.H, M = d.M;
   const float scale = rsqrtf((float)H);
   for (int64_t r = gwarp(); r < R; r += nwarps()) {
@@ -129,11 +130,13 @@ __global__ void __launch_bounds__(kTrThreads) k_tr_attn_fwd(Dims d, int64_t R, c
     const float den = warp_sum(e);
     const float a_l = lane < c ? e / den : 0.f;
     if (lane < F) alpha[r * F + lane] = a_l;
+    __syncwarp();
+    s_al[wib][lane] = a_l;
+    __syncwarp();
     float* out = zo + r * (H + M);
     for (int32_t h = lane; h < H; h += 32) {
       float acc = 0.f;
-      for (int32_t u = 0; u < c; ++u)
-        acc += __shfl_sync(0xffffffffu, a_l, u) * __ldg(kv + (r * F + u) * 2 * H + H + h);
+      for (int32_t u = 0; u < c; ++u) acc += s_al[wib][u] * __ldg(kv + (r * F + u) * 2 * H + H + h);
       out[h] = acc;
     }
     if (c == 0)
@@ -224,7 +227,8 @@ __global__ void __launch_bounds__(kTrThreads) k_tr_attn_bwd(Dims d, int64_t R, c
                                                             const float* __restrict__ alpha,
                                                             const float* __restrict__ dzo, float* dq,
                                                             float* dkv) {
-  const int lane = threadIdx.x & 31;
+  __shared__ float s_ds[kTrThreads / 32][32], s_al[kTrThreads / 32][32];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int32_t F = d.F, H = d.H, M = d.M;
   const float scale = rsqrtf((float)H);
   for (int64_t r = gwarp(); r < R; r += nwarps()) {
@@ -240,15 +244,18 @@ __global__ void __launch_bounds__(kTrThreads) k_tr_attn_bwd(Dims d, int64_t R, c
     const float al = lane < F ? __ldg(alpha + r * F + lane) : 0.f;
     const float sdot = warp_sum(lane < c ? al * my_da : 0.f);
     const float ds = lane < c ? al * (my_da - sdot) : 0.f;
+    __syncwarp();
+    s_ds[wib][lane] = ds;
+    s_al[wib][lane] = al;
+    __syncwarp();
     for (int32_t h = lane; h < H; h += 32) {
       float acc = 0.f;
-      for (int32_t u = 0; u < c; ++u)
-        acc += __shfl_sync(0xffffffffu, ds, u) * __ldg(kv + (r * F + u) * 2 * H + h);
+      for (int32_t u = 0; u < c; ++u) acc += s_ds[wib][u] * __ldg(kv + (r * F + u) * 2 * H + h);
       dq[r * H + h] = acc * scale;
     }
     for (int32_t u = 0; u < F; ++u) {
-      const float dsu = __shfl_sync(0xffffffffu, ds, u);
-      const float au = __shfl_sync(0xffffffffu, al, u);
+      const float dsu = s_ds[wib][u];
+      const float au = s_al[wib][u];
       float* o = dkv + (r * F + u) * 2 * H;
       for (int32_t h = lane; h < H; h += 32) {
         o[h] = u < c ? dsu * __ldg(q + r * H + h) * scale : 0.f;
