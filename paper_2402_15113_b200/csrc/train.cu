@@ -265,43 +265,66 @@ __global__ void __launch_bounds__(kTrThreads) k_tr_attn_bwd(Dims d, int64_t R, c
   }
 }
 
-// dh'[u] = Σ over the slots whose node is winner u, in slot order (keys sorted
-// stably); rows u in [U, 2B) are zero (the GEMMs below run over 2B rows)
+// dh'[u] = Σ over the slots whose node is winner u (keys sorted), one block per
+// winner row: thread t takes float4 column group t % 32 (M/4 <= 32 groups) of
+// the slots lo + t/32, lo + t/32 + 8, ... (8 slot lanes: a hot node is referenced
+// by thousands of neighbour slots), then the 8 partials are added in lane order
+// through shared memory — a fixed order, so the sum is deterministic.  Rows u in
+// [U, 2B) are zero (the GEMMs below run over 2B rows).
+constexpr int kSegLanes = kTrThreads / 32;
 __global__ void __launch_bounds__(kTrThreads) k_tr_seg(Dims d, int64_t nslots, int64_t B2,
                                                        const int32_t* __restrict__ num,
                                                        const int32_t* __restrict__ skey,
                                                        const int32_t* __restrict__ sval,
                                                        const float* __restrict__ dzo,
                                                        const float* __restrict__ dzn, float* dhn) {
-  const int lane = threadIdx.x & 31;
+  __shared__ float4 part[kSegLanes][32];
+  __shared__ int64_t range[2];
+  const int g = threadIdx.x & 31, sl = threadIdx.x >> 5;
   const int32_t U = __ldg(num);
-  const int32_t F = d.F, H = d.H, M = d.M;
-  for (int64_t u = gwarp(); u < B2; u += nwarps()) {
-    int64_t lo = 0, hi = 0;
-    if (u < U) {
-      int64_t a = 0, b = nslots;  // lower_bound(u)
-      while (a < b) {
-        const int64_t m = (a + b) >> 1;
-        if (__ldg(skey + m) < u) a = m + 1; else b = m;
+  const int32_t F = d.F, H = d.H, M = d.M, Q = d.M / 4;
+  for (int64_t u = blockIdx.x; u < B2; u += gridDim.x) {
+    if (threadIdx.x < 2) {
+      int64_t lo = 0;
+      if (u < U) {
+        const int64_t key = u + threadIdx.x;  // lower_bound(u) / lower_bound(u + 1)
+        int64_t a = 0, b = nslots;
+        while (a < b) {
+          const int64_t m = (a + b) >> 1;
+          if (__ldg(skey + m) < key) a = m + 1; else b = m;
+        }
+        lo = a;
       }
-      lo = a;
-      b = nslots;  // lower_bound(u + 1)
-      while (a < b) {
-        const int64_t m = (a + b) >> 1;
-        if (__ldg(skey + m) <= u) a = m + 1; else b = m;
-      }
-      hi = a;
+      range[threadIdx.x] = lo;
     }
-    for (int32_t k = lane; k < M; k += 32) {
-      float acc = 0.f;
-      for (int64_t i = lo; i < hi; ++i) {
+    __syncthreads();
+    const int64_t lo = range[0], hi = range[1];
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (g < Q)
+      for (int64_t i = lo + sl; i < hi; i += kSegLanes) {
         const int64_t slot = __ldg(sval + i);
         const int64_t r = slot / (F + 1);
         const int32_t s = (int32_t)(slot % (F + 1));
-        acc += s == 0 ? __ldg(dzo + r * (H + M) + H + k) : __ldg(dzn + (r * F + s - 1) * M + k);
+        const float4 v = s == 0 ? __ldg(reinterpret_cast<const float4*>(dzo + r * (H + M) + H) + g)
+                                : __ldg(reinterpret_cast<const float4*>(dzn + (r * F + s - 1) * M) + g);
+        acc.x += v.x;
+        acc.y += v.y;
+        acc.z += v.z;
+        acc.w += v.w;
       }
-      dhn[u * M + k] = acc;
+    part[sl][g] = acc;
+    __syncthreads();
+    if (sl == 0 && g < Q) {
+      float4 t = part[0][g];
+      for (int q = 1; q < kSegLanes; ++q) {
+        t.x += part[q][g].x;
+        t.y += part[q][g].y;
+        t.z += part[q][g].z;
+        t.w += part[q][g].w;
+      }
+      reinterpret_cast<float4*>(dhn + u * M)[g] = t;
     }
+    __syncthreads();
   }
 }
 
@@ -439,6 +462,7 @@ mspipe_status mspipe_train_create(mspipe_train** out, const mspipe_gru* gru, int
   if (gru->precision != MSPIPE_FP32_3XTF32 || gru->d.cell != MSPIPE_CELL_GRU ||
       gru->d.mailbox != MSPIPE_MAILBOX_IMMEDIATE)
     return fail(MSPIPE_EUNSUPPORTED, "train_create: needs a GRUCell, immediate-mailbox, MSPIPE_FP32_3XTF32 updater");
+  if (gru->d.M > 128) return fail(MSPIPE_EUNSUPPORTED, "train_create: mem_dim <= 128 (one float4 group per lane)");
   if (num_nodes <= 0 || emb_dim <= 0 || fanout < 1 || fanout > 31 || max_events <= 0 ||
       max_events > gru->max_events || 2 * max_events > kNoWinner)
     return fail(MSPIPE_EINVAL, "train_create: num_nodes=%lld emb_dim=%d fanout=%d max_events=%lld",
@@ -612,8 +636,8 @@ mspipe_status mspipe_train_step(mspipe_train* t, const mspipe_gru* gru, int64_t 
   size_t sb = t->sort_bytes;
   cudaError_t e = cub::DeviceRadixSort::SortPairs(t->sort_tmp, sb, t->key, t->skey, t->val, t->sval, (int)slots, 0, 15, s);
   if (e != cudaSuccess) return cuda_status(e, "train_step: sort");
-  k_tr_seg<<<grid_for(B2 * 32, kTrThreads), kTrThreads, 0, s>>>(d, slots, B2, num_unique, t->skey, t->sval, t->dzo,
-                                                               t->dzn, t->dhn);
+  k_tr_seg<<<(unsigned)std::min<int64_t>(B2, (int64_t)num_sms() * 8), kTrThreads, 0, s>>>(
+      d, slots, B2, num_unique, t->skey, t->sval, t->dzo, t->dzn, t->dhn);
   const int32_t nchunks = gru->d.Kpad / tc::kKC;
   k_tr_gru_bwd<<<grid_for(B2 * d.K, 256), 256, 0, s>>>(d, B2, nchunks, num_unique, (const float*)workspace, gates,
                                                       t->dhn, t->D, t->xp);
