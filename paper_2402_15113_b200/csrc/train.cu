@@ -68,7 +68,7 @@ __global__ void k_tr_map(const int32_t* __restrict__ nodes, const int32_t* __res
   for (int64_t u = gthread(); u < U; u += nthreads()) wmap[__ldg(nodes + u)] = set ? (int32_t)u : -1;
 }
 
-// T1 + the attention inputs: per root r (one warp) and slot s in [0, F]:
+// T1 + the attention inputs: one warp per root r and slot s in [0, F]:
 //   s == 0: sroot[r] = s~(root);  s >= 1: zn[r, s-1] = [s~(nbr) ‖ φ(Δt)] or 0;
 //   key[slot] = winner row of the slot's node (kNoWinner if none), val[slot] = slot
 __global__ void __launch_bounds__(kTrThreads) k_tr_gather(
@@ -78,10 +78,11 @@ __global__ void __launch_bounds__(kTrThreads) k_tr_gather(
     float* zn, int32_t* key, int32_t* val) {
   const int lane = threadIdx.x & 31;
   const int32_t F = d.F, M = d.M, Z = d.M + d.Dt;
-  for (int64_t r = gwarp(); r < R; r += nwarps()) {
+  for (int64_t slot = gwarp(); slot < R * (F + 1); slot += nwarps()) {  // one warp per (root, slot)
+    const int64_t r = slot / (F + 1);
+    const int32_t s = (int32_t)(slot % (F + 1));
     const int32_t c = __ldg(cnt + r);
-    for (int32_t s = 0; s <= F; ++s) {
-      const int64_t slot = r * (F + 1) + s;
+    {
       const int32_t id = __ldg(sub + slot);
       const bool valid = id >= 0 && (s == 0 || s - 1 < c);
       const int32_t u = valid ? __ldg(wmap + id) : -1;
@@ -599,7 +600,7 @@ mspipe_status mspipe_train_step(mspipe_train* t, const mspipe_gru* gru, int64_t 
   if (!kv_adj) return fail(MSPIPE_EUNSUPPORTED, "train_step: emb_dim * (mem_dim + time_dim) must be a multiple of 4");
   // forward ------------------------------------------------------------------
   k_tr_map<<<grid_for(B2, 256), 256, 0, s>>>(nodes, num_unique, t->wmap, 1);
-  k_tr_gather<<<grid_for(R * 32, kTrThreads), kTrThreads, 0, s>>>(d, R, sub_ids, sub_dt, sub_cnt, snap_mem, t->wmap,
+  k_tr_gather<<<grid_for(R * (F + 1) * 32, kTrThreads), kTrThreads, 0, s>>>(d, R, sub_ids, sub_dt, sub_cnt, snap_mem, t->wmap,
                                                                  new_mem, gru->time_w, gru->time_b, t->sroot, t->zn,
                                                                  t->key, t->val);
   TR_BLAS(gemm_rm(t->blas, false, true, R, H, M, t->sroot, M, wq, M, 0.f, t->q, H));
