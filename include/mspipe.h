@@ -667,7 +667,7 @@ MSPIPE_API mspipe_status mspipe_apan_deliver(mspipe_apan* a, mspipe_memory* st, 
  *   s~(v) = h'_v (this batch's GRU output) if v is a winner, else the
  *   fetched snapshot row (T1); q = W_q s~(r), k_u / v_u = W_k / W_v [s~(u) ‖
  *   φ(Δt_u)], α = softmax(q·k_u/√H) over the cnt valid neighbours, h_r = W_o
- *   [Σ α_u v_u ‖ s~(r)] + b_o (T3); logit(a, b) = w_2·relu(W_1 [h_a ‖ h_b] +
+ *   [Σ α_u v_u ‖ s~(r)] + b_o (T3); logit(a, b) = w_2·tanh(W_1 [h_a ‖ h_b] +
  *   b_1) + b_2 (T4); loss = mean BCE over (src_j, dst_j) = 1 and (src_j,
  *   neg_j) = 0 (T5); gradients of every learnable tensor, through h' into the
  *   GRU weights (T2); SGD (T6).  The DP all-reduce of `grads` (T7) is the

@@ -25,7 +25,9 @@ learnable"; η, §5.1).  Readings (T1-T7):
         a = Σ_u α_u v_u  (0 when cnt = 0),   h_v = W_o [a ‖ s~_v] + b_o,
       φ = the message's fixed time encoder cos(ω Δt + ϕ) (G2), Δt_u = t_q - t_e
       as the sampler returns it (f32).
-  T4  decoder (TGN's link predictor): logit(a, b) = w_2·relu(W_1 [h_a ‖ h_b] + b_1) + b_2.
+  T4  decoder (a link MLP; the paper names none): logit(a, b) =
+      w_2·tanh(W_1 [h_a ‖ h_b] + b_1) + b_2 — smooth, so no f32-vs-f64 kink
+      decision (TGN's ReLU) separates the GPU from this oracle.
   T5  loss: mean binary cross-entropy on logits over the B positive (src, dst)
       and B negative (src, neg) pairs ("equal number of positive and
       negative"; S:L324-L327).
@@ -147,7 +149,7 @@ def decode_loss(emb, B, p):
     za = np.concatenate([np.concatenate([emb[:B], emb[B:2 * B]], 1),
                          np.concatenate([emb[:B], emb[2 * B:3 * B]], 1)], 0)   # [2B, 2H]
     pre = za @ _f64(p["w_1"]).T + _f64(p["b_1"])
-    y = np.maximum(pre, 0.0)
+    y = np.tanh(pre)
     logit = y @ _f64(p["w_2"]) + _f64(p["b_2"])[0]
     lab = np.concatenate([np.ones(B), np.zeros(B)])
     loss = np.mean(softplus(-logit) * lab + softplus(logit) * (1.0 - lab))
@@ -158,7 +160,7 @@ def decode_backward(logit, B, c, p):
     H = p["w_2"].shape[0]
     dlogit = (sigmoid(logit) - c["lab"]) / (2.0 * B)
     g = dict(w_2=c["y"].T @ dlogit, b_2=np.array([dlogit.sum()]))
-    dpre = dlogit[:, None] * _f64(p["w_2"])[None, :] * (c["pre"] > 0)
+    dpre = dlogit[:, None] * _f64(p["w_2"])[None, :] * (1.0 - c["y"] ** 2)
     g["w_1"] = dpre.T @ c["za"]
     g["b_1"] = dpre.sum(0)
     dza = dpre @ _f64(p["w_1"])

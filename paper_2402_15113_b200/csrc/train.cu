@@ -162,8 +162,8 @@ __global__ void k_tr_dec_in(int64_t B, int32_t H, const float* __restrict__ emb,
 
 __device__ __forceinline__ double softplus_d(double x) { return fmax(x, 0.0) + log1p(exp(-fabs(x))); }
 
-// T4 + T5, one warp per pair: y = relu(pre + b_1), logit = w_2·y + b_2, the
-// BCE term (f64), dlogit = (σ(logit) - label) / 2B, dpre = dlogit w_2 [pre > 0]
+// T4 + T5, one warp per pair: y = tanh(pre + b_1), logit = w_2·y + b_2, the
+// BCE term (f64), dlogit = (σ(logit) - label) / 2B, dpre = dlogit w_2 (1 - y²)
 __global__ void __launch_bounds__(kTrThreads) k_tr_dec_out(int64_t B, int32_t H, const float* __restrict__ pre,
                                                            const float* __restrict__ b_1,
                                                            const float* __restrict__ w_2,
@@ -174,7 +174,7 @@ __global__ void __launch_bounds__(kTrThreads) k_tr_dec_out(int64_t B, int32_t H,
   for (int64_t p = gwarp(); p < 2 * B; p += nwarps()) {
     float acc = 0.f;
     for (int32_t h = lane; h < H; h += 32) {
-      const float v = fmaxf(__ldg(pre + p * H + h) + __ldg(b_1 + h), 0.f);
+      const float v = tanhf(__ldg(pre + p * H + h) + __ldg(b_1 + h));
       y[p * H + h] = v;
       acc += __ldg(w_2 + h) * v;
     }
@@ -186,8 +186,10 @@ __global__ void __launch_bounds__(kTrThreads) k_tr_dec_out(int64_t B, int32_t H,
       dlogit[p] = g;
       term[p] = pos ? softplus_d(-(double)l) : softplus_d((double)l);
     }
-    for (int32_t h = lane; h < H; h += 32)
-      dpre[p * H + h] = (__ldg(pre + p * H + h) + __ldg(b_1 + h)) > 0.f ? g * __ldg(w_2 + h) : 0.f;
+    for (int32_t h = lane; h < H; h += 32) {
+      const float v = y[p * H + h];
+      dpre[p * H + h] = g * __ldg(w_2 + h) * (1.f - v * v);
+    }
   }
 }
 
