@@ -462,6 +462,36 @@ def run_mspipe(args):
                            "decoder": "TGN link MLP", "optimizer": "SGD"},
                 "clocks": clk}
 
+    def apan_measurement():
+        """Row F3, APAN: the stage with the multi-slot mailbox (attention message,
+        GRU GEMM, propagation to sampled neighbours) at k = 0, grouped graphs and
+        the same flush protocol; events/s beside the TGN stage's."""
+        import dataclasses
+
+        rng = np.random.default_rng(args.seed + 77)
+        M, Dm = cfg.mem_dim, cfg.mail_dim
+        ap = dict(w_q=(rng.uniform(-1, 1, (M, M)) / np.sqrt(M)).astype(np.float32),
+                  w_k=(rng.uniform(-1, 1, (M, Dm)) / np.sqrt(Dm)).astype(np.float32), slots=10)
+        sca = dataclasses.replace(sc, k=0, mailbox="apan", apan=ap, mitigation=None, double_buffer=False)
+        sta = MemoryStage(sca, w["params"], g, dev)
+        t = resident
+        sta.bind_resident(t["src"], t["dst"], t["ts"], t["neg"], t["ef"])
+        gr_a, s_a = capture_groups(sta, gs)
+        torch.cuda.synchronize()
+        with ClockSampler(local) as clk_a:
+            ms_a, tb_a, _ = timed_run_groups(sta, gr_a, s_a, W, K, gs)
+        _C.check(s_a)
+        ev_a = sum(min(cfg.batch, E - b * cfg.batch) for b in tb_a)
+        filled = float(sta.apan.mb_cnt.float().mean().item())
+        del gr_a, sta
+        return {"metric": "APAN memory stage (row F3) events/s", "unit": UNIT, "value": ev_a / (sum(ms_a) / 1e3),
+                "ms_per_step": float(sum(ms_a)) / K,
+                "config": {"staleness_k": 0, "slots": 10, "message": "attention over the filled mailbox slots",
+                           "propagation": "node + its sampled neighbours, latest key wins",
+                           "mean_filled_slots_at_end": filled},
+                "note": "the mailbox epoch reset is the caller's (not between timed blocks)",
+                "clocks": clk_a.summary()}
+
     # ---- device-resident run (the `value`) ---------------------------------
     blocks, clocks, st = run_blocks(False)
     value, ms_step, rates, timed_batches = block_value(blocks)
@@ -574,6 +604,11 @@ def run_mspipe(args):
             out["train"] = train_measurement()
         except Exception as ex:  # reported, never hides the headline
             out["train"] = {"error": f"{type(ex).__name__}: {ex}"}
+    if ws == 1 and not args.no_apan and getattr(sc, "use_fused")() and args.gru == "tc" and not args.features:
+        try:
+            out["apan"] = apan_measurement()
+        except Exception as ex:  # reported, never hides the headline
+            out["apan"] = {"error": f"{type(ex).__name__}: {ex}"}
     # ---- e2e: host buffers through the same C-ABI calls ---------------------
     blocks2, _, st2 = run_blocks(True)
     v2, ms2, _, _ = block_value(blocks2)
@@ -886,6 +921,7 @@ def main():
                          "--events)")
     ap.add_argument("--no-probe", action="store_true", help="skip the N = 10^7 HBM probe of the A3/A7 kernels")
     ap.add_argument("--no-train", action="store_true", help="skip the row F4 (training stage) measurement")
+    ap.add_argument("--no-apan", action="store_true", help="skip the row F3 APAN stage measurement")
     ap.add_argument("--profile", action="store_true", help="short run for ncu: no flush/e2e/cpu")
     ap.add_argument("--graph-steps", type=int, default=8,
                     help="consecutive steps captured per CUDA graph (1: one graph per step); N = 1 only")
