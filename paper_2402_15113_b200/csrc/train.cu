@@ -268,43 +268,91 @@ __global__ void __launch_bounds__(kTrThreads) k_tr_attn_bwd(Dims d, int64_t R, c
   }
 }
 
-// dh'[u] = Σ over the slots whose node is winner u (keys sorted), one block per
-// winner row: thread t takes float4 column group t % 32 (M/4 <= 32 groups) of
-// the slots lo + t/32, lo + t/32 + 8, ... (8 slot lanes: a hot node is referenced
-// by thousands of neighbour slots), then the 8 partials are added in lane order
-// through shared memory — a fixed order, so the sum is deterministic.  Rows u in
-// [U, 2B) are zero (the GEMMs below run over 2B rows).
+// dh'[u] = Σ over the slots whose node is winner u (keys sorted).  A hot node
+// is referenced by tens of thousands of neighbour slots, so every winner's
+// segment is cut into pieces of kPiece slots, each summed by one block (8 slot
+// lanes x float4 column groups, the lanes' partials added in lane order), and
+// the pieces of a winner are added in piece order: a fixed order, so the sum
+// is deterministic.  Rows u in [U, 2B) are zero (the GEMMs run over 2B rows).
 constexpr int kSegLanes = kTrThreads / 32;
-__global__ void __launch_bounds__(kTrThreads) k_tr_seg(Dims d, int64_t nslots, int64_t B2,
-                                                       const int32_t* __restrict__ num,
-                                                       const int32_t* __restrict__ skey,
-                                                       const int32_t* __restrict__ sval,
-                                                       const float* __restrict__ dzo,
-                                                       const float* __restrict__ dzn, float* dhn) {
-  __shared__ float4 part[kSegLanes][32];
-  __shared__ int64_t range[2];
-  const int g = threadIdx.x & 31, sl = threadIdx.x >> 5;
+constexpr int64_t kPiece = 512;
+
+// one block: each winner's segment [lo, hi) and the exclusive scan of its piece counts
+__global__ void __launch_bounds__(1024) k_tr_seg_plan(int64_t nslots, int64_t B2, const int32_t* __restrict__ num,
+                                                       const int32_t* __restrict__ skey, int64_t* lo_hi,
+                                                       int64_t* poff) {
+  __shared__ int64_t carry;
+  __shared__ int64_t wsum[32];
   const int32_t U = __ldg(num);
-  const int32_t F = d.F, H = d.H, M = d.M, Q = d.M / 4;
-  for (int64_t u = blockIdx.x; u < B2; u += gridDim.x) {
-    if (threadIdx.x < 2) {
-      int64_t lo = 0;
-      if (u < U) {
-        const int64_t key = u + threadIdx.x;  // lower_bound(u) / lower_bound(u + 1)
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int64_t base = 0; base < B2; base += blockDim.x) {
+    const int64_t u = base + threadIdx.x;
+    int64_t lo = 0, hi = 0;
+    if (u < U) {
+      for (int e = 0; e < 2; ++e) {  // lower_bound(u), lower_bound(u + 1)
         int64_t a = 0, b = nslots;
         while (a < b) {
           const int64_t m = (a + b) >> 1;
-          if (__ldg(skey + m) < key) a = m + 1; else b = m;
+          if (__ldg(skey + m) < u + e) a = m + 1; else b = m;
         }
-        lo = a;
+        (e ? hi : lo) = a;
       }
-      range[threadIdx.x] = lo;
+    }
+    if (u < B2) {
+      lo_hi[2 * u] = lo;
+      lo_hi[2 * u + 1] = hi;
+    }
+    // block-wide exclusive scan of the piece counts
+    int64_t n = (u < B2) ? (hi - lo + kPiece - 1) / kPiece : 0;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    int64_t x = n;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) wsum[w] = x;
+    __syncthreads();
+    if (w == 0) {
+      int64_t v = lane < (int)(blockDim.x >> 5) ? wsum[lane] : 0;
+      for (int o = 1; o < 32; o <<= 1) {
+        const int64_t y = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += y;
+      }
+      wsum[lane] = v;
     }
     __syncthreads();
-    const int64_t lo = range[0], hi = range[1];
+    const int64_t incl = x + (w > 0 ? wsum[w - 1] : 0);
+    if (u < B2) poff[u] = carry + incl - n;
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) carry += incl;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) poff[B2] = carry;
+}
+
+// pass 1: block per piece p (grid-stride over the bound): rows of slots [start, end)
+__global__ void __launch_bounds__(kTrThreads) k_tr_seg_piece(Dims d, int64_t B2, const int64_t* __restrict__ lo_hi,
+                                                             const int64_t* __restrict__ poff,
+                                                             const int32_t* __restrict__ sval,
+                                                             const float* __restrict__ dzo,
+                                                             const float* __restrict__ dzn, float* part) {
+  __shared__ float4 lanes[kSegLanes][32];
+  const int g = threadIdx.x & 31, sl = threadIdx.x >> 5;
+  const int32_t F = d.F, H = d.H, M = d.M, Q = d.M / 4;
+  const int64_t total = poff[B2];
+  for (int64_t p = blockIdx.x; p < total; p += gridDim.x) {
+    int64_t a = 0, b = B2;  // the winner u with poff[u] <= p < poff[u + 1]
+    while (a < b) {
+      const int64_t m = (a + b) >> 1;
+      if (poff[m + 1] <= p) a = m + 1; else b = m;
+    }
+    const int64_t u = a;
+    const int64_t start = lo_hi[2 * u] + (p - poff[u]) * kPiece;
+    const int64_t end = min(start + kPiece, lo_hi[2 * u + 1]);
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
     if (g < Q)
-      for (int64_t i = lo + sl; i < hi; i += kSegLanes) {
+      for (int64_t i = start + sl; i < end; i += kSegLanes) {
         const int64_t slot = __ldg(sval + i);
         const int64_t r = slot / (F + 1);
         const int32_t s = (int32_t)(slot % (F + 1));
@@ -315,19 +363,38 @@ __global__ void __launch_bounds__(kTrThreads) k_tr_seg(Dims d, int64_t nslots, i
         acc.z += v.z;
         acc.w += v.w;
       }
-    part[sl][g] = acc;
+    lanes[sl][g] = acc;
     __syncthreads();
     if (sl == 0 && g < Q) {
-      float4 t = part[0][g];
+      float4 t = lanes[0][g];
       for (int q = 1; q < kSegLanes; ++q) {
-        t.x += part[q][g].x;
-        t.y += part[q][g].y;
-        t.z += part[q][g].z;
-        t.w += part[q][g].w;
+        t.x += lanes[q][g].x;
+        t.y += lanes[q][g].y;
+        t.z += lanes[q][g].z;
+        t.w += lanes[q][g].w;
       }
-      reinterpret_cast<float4*>(dhn + u * M)[g] = t;
+      reinterpret_cast<float4*>(part + p * M)[g] = t;
     }
     __syncthreads();
+  }
+}
+
+// pass 2: thread per (u, float4 group): the winner's pieces in piece order
+__global__ void k_tr_seg_final(int32_t M, int64_t B2, const int64_t* __restrict__ poff,
+                               const float* __restrict__ part, float* dhn) {
+  const int32_t Q = M / 4;
+  for (int64_t t = gthread(); t < B2 * Q; t += nthreads()) {
+    const int64_t u = t / Q;
+    const int32_t g = (int32_t)(t % Q);
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int64_t p = poff[u]; p < poff[u + 1]; ++p) {
+      const float4 v = reinterpret_cast<const float4*>(part + p * M)[g];
+      acc.x += v.x;
+      acc.y += v.y;
+      acc.z += v.z;
+      acc.w += v.w;
+    }
+    reinterpret_cast<float4*>(dhn + u * M)[g] = acc;
   }
 }
 
@@ -428,6 +495,8 @@ struct mspipe_train {
       *dzn, *dhn, *D, *xp, *ones, *cs;
   double* term;
   int32_t *key, *val, *skey, *sval;
+  int64_t *lo_hi, *poff;  // per winner: its sorted segment, exclusive scan of its piece counts
+  float* part;            // piece sums [slots / kPiece + 2B + 1, M]
   void* sort_tmp;
   size_t sort_bytes;
   void* blas_ws;  // cuBLAS workspace owned here: no allocation inside a CUDA-graph capture
@@ -438,7 +507,7 @@ static void train_free(mspipe_train* t) {
   if (!t) return;
   void* bufs[] = {t->wmap, t->sroot, t->zn, t->q, t->kv, t->alpha, t->zo, t->emb, t->za, t->pre, t->y, t->logit,
                   t->dlogit, t->dpre, t->dza, t->demb, t->dzo, t->dq, t->dkv, t->dzn, t->dhn, t->D, t->xp, t->ones,
-                  t->cs, t->term, t->key, t->val, t->skey, t->sval, t->sort_tmp, t->blas_ws};
+                  t->cs, t->term, t->key, t->val, t->skey, t->sval, t->sort_tmp, t->blas_ws, t->lo_hi, t->poff, t->part};
   for (void* b : bufs)
     if (b) cudaFree(b);
   if (t->blas) cublasDestroy(t->blas);
@@ -514,6 +583,9 @@ mspipe_status mspipe_train_create(mspipe_train** out, const mspipe_gru* gru, int
   if (e == cudaSuccess) e = cudaMalloc(&t->val, sizeof(int32_t) * (size_t)slots);
   if (e == cudaSuccess) e = cudaMalloc(&t->skey, sizeof(int32_t) * (size_t)slots);
   if (e == cudaSuccess) e = cudaMalloc(&t->sval, sizeof(int32_t) * (size_t)slots);
+  if (e == cudaSuccess) e = cudaMalloc(&t->lo_hi, sizeof(int64_t) * (size_t)(4 * B));
+  if (e == cudaSuccess) e = cudaMalloc(&t->poff, sizeof(int64_t) * (size_t)(2 * B + 1));
+  af(&t->part, (slots / kPiece + 2 * B + 1) * M);
   if (e == cudaSuccess)
     e = cub::DeviceRadixSort::SortPairs(nullptr, t->sort_bytes, t->key, t->skey, t->val, t->sval, (int)slots, 0, 15);
   if (e == cudaSuccess) e = cudaMalloc(&t->sort_tmp, t->sort_bytes);
@@ -639,8 +711,11 @@ mspipe_status mspipe_train_step(mspipe_train* t, const mspipe_gru* gru, int64_t 
   size_t sb = t->sort_bytes;
   cudaError_t e = cub::DeviceRadixSort::SortPairs(t->sort_tmp, sb, t->key, t->skey, t->val, t->sval, (int)slots, 0, 15, s);
   if (e != cudaSuccess) return cuda_status(e, "train_step: sort");
-  k_tr_seg<<<(unsigned)std::min<int64_t>(B2, (int64_t)num_sms() * 8), kTrThreads, 0, s>>>(
-      d, slots, B2, num_unique, t->skey, t->sval, t->dzo, t->dzn, t->dhn);
+  k_tr_seg_plan<<<1, 1024, 0, s>>>(slots, B2, num_unique, t->skey, t->lo_hi, t->poff);
+  const int64_t max_pieces = slots / kPiece + B2 + 1;
+  k_tr_seg_piece<<<(unsigned)std::min<int64_t>(max_pieces, (int64_t)num_sms() * 8), kTrThreads, 0, s>>>(
+      d, B2, t->lo_hi, t->poff, t->sval, t->dzo, t->dzn, t->part);
+  k_tr_seg_final<<<grid_for(B2 * (M / 4), 256), 256, 0, s>>>((int32_t)M, B2, t->poff, t->part, t->dhn);
   const int32_t nchunks = gru->d.Kpad / tc::kKC;
   k_tr_gru_bwd<<<grid_for(B2 * d.K, 256), 256, 0, s>>>(d, B2, nchunks, num_unique, (const float*)workspace, gates,
                                                       t->dhn, t->D, t->xp);
