@@ -514,7 +514,8 @@ def run_mspipe(args):
     # configuration (two streams), the op's duration while it shares the GPU
     op_mean, op_instr_step, op_in_step = {}, {}, {}
     if ws == 1 and getattr(st, "fused", False) and not args.profile:
-        for op, serial in (("prep", True), ("build", True), ("update", True), ("prep", False), ("update", False)):
+        for op, serial in (("prep", True), ("build", True), ("update", True), ("gemm", True), ("prep", False),
+                           ("update", False), ("gemm", False)):
             sti = make_stage(False)
             gi, si = capture_groups(sti, gs, op=op, serial=serial)
             ms_i, _, opm = timed_run_groups(sti, gi, si, W, K, gs, op=op)
@@ -530,11 +531,14 @@ def run_mspipe(args):
     mean_U = float(np.mean(U_host[timed_batches]))
     alg = algorithmic(cfg, sc, mean_U)
     traffic = _ncu_traffic(args.config)
-    dom = max(op_mean, key=op_mean.get) if op_mean else "update"
+    dom = max((o for o in op_mean if o != "gemm"), key=op_mean.get) if op_mean else "update"
     rooflines = {}
     for op, t_ms in op_mean.items():
-        if op == "update":
+        if op in ("update", "gemm"):
             r = _tensor_roofline(args.gru, alg["update_flops"], t_ms, peaks, st, burst=True)
+            if op == "gemm":
+                r["kernel"] = "k_gru_tc alone (events recorded by the library around the GEMM launch inside " \
+                              "mspipe_gru_apply_commit; the write-back branch excluded)"
         else:
             ach = alg[op] / (t_ms / 1e3) / 1e9
             r = {"kernel": {"prep": "k_prep (A1 sampler + A2 dedup + A3 subgraph gather)",
@@ -548,7 +552,7 @@ def run_mspipe(args):
                                  "from the ops before it); instrumented serial ms/step %.4f" % op_instr_step[op])
         if op in op_in_step:
             r["launch_ms_in_step"] = op_in_step[op]
-        kname = {"prep": "k_prep", "update": "k_gru_tc", "build": "k_build_x"}[op]
+        kname = {"prep": "k_prep", "update": "k_gru_tc", "gemm": "k_gru_tc", "build": "k_build_x"}[op]
         ncu = (traffic or {}).get(kname)
         r["traffic"] = ncu["dram_bytes"] if ncu else None
         if ncu:
@@ -585,7 +589,7 @@ def run_mspipe(args):
                       "rates": rates, "rule": f"K-step blocks (reset + W warm-up each) until >= {MIN_TIMED_MS} ms; "
                                               "value = the median block"},
            "roofline": roof, "roofline_gather": roof_gather,
-           "roofline_gemm": rooflines.get("update") if dom != "update" else None,
+           "roofline_gemm": rooflines.get("gemm") or (rooflines.get("update") if dom != "update" else None),
            "roofline_features": roof_features,
            "per_step_graphs": per_step,
            "gpu_launches": _launches(st.step_ops(), timed_batches, bool(mit), getattr(st, "fused", False), sharded,

@@ -587,6 +587,11 @@ MSPIPE_API mspipe_status mspipe_staleness_error(const int32_t* winner, const int
  * event-record node of the graph and can still be used for elapsed-time
  * measurement of the captured kernels. */
 MSPIPE_API mspipe_status mspipe_util_event_record(void* event, void* stream);
+/* [host] timing: the next mspipe_gru_apply_commit(_out) of this thread records
+ * cudaEvent_t `begin` / `end` (timing events, also as graph nodes) on its
+ * stream right before and right after its GEMM kernel (not the write-back
+ * branch); one-shot.  Both or neither (MSPIPE_EINVAL). */
+MSPIPE_API mspipe_status mspipe_util_kernel_events(void* begin, void* end);
 
 /* Utility (step graphs): the stage of one step is captured once and replayed
  * (the "CUDA graphs instead of a tracing compiler" of DESIGN.md §2).

@@ -42,7 +42,8 @@ EXPORTS = ("mspipe_abi_version", "mspipe_last_error", "mspipe_check", "mspipe_sa
            "mspipe_shard_sent_bytes", "mspipe_util_record_to_device", "mspipe_shard_mitigation_candidates",
            "mspipe_shard_fetch_finish_table", "mspipe_shard_mitigate", "mspipe_train_layout", "mspipe_train_create",
            "mspipe_train_destroy", "mspipe_gru_save_gates", "mspipe_train_step", "mspipe_train_sgd",
-           "mspipe_apan_create", "mspipe_apan_destroy", "mspipe_message_build_apan", "mspipe_apan_deliver")
+           "mspipe_apan_create", "mspipe_apan_destroy", "mspipe_message_build_apan", "mspipe_apan_deliver",
+           "mspipe_util_kernel_events")
 XCHG_FETCH_IDS, XCHG_FETCH_ROWS, XCHG_COMMIT = 0, 1, 2
 
 
@@ -143,6 +144,7 @@ def lib():
         L.mspipe_gru_save_gates.argtypes = [P, P]
         L.mspipe_train_step.argtypes = [P, P, i64, P, P, P, P, P, P, P, P, C.c_size_t, P, P, P, P]
         L.mspipe_train_sgd.argtypes = [P, P, f32, P]
+        L.mspipe_util_kernel_events.argtypes = [P, P]
         L.mspipe_apan_create.argtypes = [C.POINTER(P), i64, i32, i32, i32, i64, P, P, P, P, P, P, P]
         L.mspipe_apan_destroy.argtypes = [P]
         L.mspipe_message_build_apan.argtypes = [P, P, P, i64, P, P, i64, P, P, P, P, P, C.c_size_t, P]
@@ -180,6 +182,13 @@ def check(stream=None):
 
 def last_error() -> str:
     return lib().mspipe_last_error().decode(errors="replace")
+
+
+def kernel_events(begin, end):
+    """The next gru_apply_commit of this thread brackets its GEMM kernel with (begin, end)."""
+    _ck(lib().mspipe_util_kernel_events(C.c_void_p(begin.cuda_event) if begin is not None else None,
+                                        C.c_void_p(end.cuda_event) if end is not None else None),
+        "kernel_events")
 
 
 def event_record(event: torch.cuda.Event, stream=None):

@@ -728,6 +728,10 @@ mspipe_status mspipe_gru_apply(const mspipe_gru* gru, int64_t num_events, const 
   return after_launch("gru_apply");
 }
 
+// one-shot timing pair for the next tensor-core GEMM launch of this thread
+// (mspipe_util_kernel_events): recorded right before / after the kernel
+static thread_local cudaEvent_t g_kev[2] = {nullptr, nullptr};
+
 static mspipe_status apply_commit_impl(const mspipe_gru* gru, mspipe_memory* st, int64_t commit_version,
                                        int64_t num_events, const float* snap_mem, int64_t snap_step,
                                        const float* snap_h, const int32_t* nodes, const int32_t* winner,
@@ -838,10 +842,16 @@ static mspipe_status apply_commit_impl(const mspipe_gru* gru, mspipe_memory* st,
       }
       c.skip_meta = 1;
     }
+    cudaEvent_t kev0 = g_kev[0], kev1 = g_kev[1];
+    g_kev[0] = g_kev[1] = nullptr;
+    if (kev0 && cudaEventRecordWithFlags(kev0, s, cudaEventRecordExternal) != cudaSuccess)
+      return cuda_status(cudaGetLastError(), "gru_apply_commit: timing event");
     cudaError_t e = launch_gru_tc(gru->d, gru->wtc, (float*)workspace, nullptr, num_events, nullptr, snap_mem, nullptr,
                                   snap_step, snap_h, winner, num_unique, out_mem, nullptr, nullptr, 0,
                                   s, kGruGemm, &c);
     if (e != cudaSuccess) return cuda_status(e, "gru_apply_commit: launch");
+    if (kev1 && cudaEventRecordWithFlags(kev1, s, cudaEventRecordExternal) != cudaSuccess)
+      return cuda_status(cudaGetLastError(), "gru_apply_commit: timing event");
     if (split && !wb_first) {
       e = branch();
       if (e != cudaSuccess) return cuda_status(e, "gru_apply_commit: writeback branch");
@@ -1091,6 +1101,13 @@ mspipe_status mspipe_shard_loopback(mspipe_memory* const* ranks, int32_t world, 
     if (!ranks[r] || ranks[r]->world != world || ranks[r]->rank != r || ranks[r]->sh_connected != 2)
       return fail(MSPIPE_EINVAL, "shard_loopback: ranks[%d] is not an in-process rank %d of a world of %d", r, r, world);
   return MSPIPE_OK;  // the data is already in the windows: one stream orders the phases of all ranks
+}
+
+mspipe_status mspipe_util_kernel_events(void* begin, void* end) {
+  if ((begin == nullptr) != (end == nullptr)) return fail(MSPIPE_EINVAL, "util_kernel_events: both or neither");
+  g_kev[0] = (cudaEvent_t)begin;
+  g_kev[1] = (cudaEvent_t)end;
+  return MSPIPE_OK;
 }
 
 mspipe_status mspipe_util_event_record(void* event, void* stream) {

@@ -171,6 +171,15 @@ class _TimedOps:
 
     timing_only = None  # optional set of op names to bracket (the others get no event nodes)
 
+    def _ev_pair(self, name):
+        """Two timing events for the library to record (name, name + '_end')."""
+        if not getattr(self, "_pool", None) or len(self._pool) < 2:
+            return None
+        b, e = self._pool.pop(), self._pool.pop()
+        self.timing.setdefault(name, []).append(b)
+        self.timing.setdefault(name + "_end", []).append(e)
+        return b, e
+
     def _ev(self, name):
         if self.timing is None:
             return None
@@ -487,6 +496,10 @@ class MemoryStage(_TimedOps):
         if self.staged:
             o = self.out_ring[i % self._nout]
             rec = dict(out_nodes=o[16:16 + 4 * 2 * n].view(torch.int32), out_num=o[:4].view(torch.int32))
+        if self.timing is not None and (self.timing_only is None or "gemm" in self.timing_only):
+            pair = self._ev_pair("gemm")  # the GEMM kernel alone, recorded by the library around its launch
+            if pair is not None:
+                _C.kernel_events(*pair)
         _C.gru_apply_commit(self.gru, self.memory, i, n, sl.mem, cfg.fanout + 1, upd, sl.ws,
                             snap_h=sl.h[: 2 * n] if sl.h is not None else None, **rec)
         if self.deferred:  # row F3: new mails from the committed memories of both endpoints
