@@ -646,11 +646,16 @@ MSPIPE_API mspipe_status mspipe_util_graph_destroy(void* exec);
  *   / cnt: the prep's sampler outputs [3B, fanout], [3B]); per node the mail
  *   with the largest key p (fanout + 1) + s wins (s = 0: itself, 1 + j:
  *   neighbour j) and fills the node's next ring slot.  world == 1 only. */
+/* mspipe_apan_refresh_keys: the handle caches k = W_k mail for every ring
+ *   slot (written with the mail at delivery); after the caller writes the
+ *   mailbox tables directly (anything but an all-zero reset), it recomputes
+ *   the cache from them. */
 typedef struct mspipe_apan mspipe_apan;
 MSPIPE_API mspipe_status mspipe_apan_create(mspipe_apan** out, int64_t num_nodes, int32_t mem_dim, int32_t edge_dim,
                                             int32_t slots, int64_t max_events, const float* w_q, const float* w_k,
                                             float* mb, double* mb_ts, int32_t* mb_pos, int32_t* mb_cnt, void* stream);
 MSPIPE_API mspipe_status mspipe_apan_destroy(mspipe_apan* a);
+MSPIPE_API mspipe_status mspipe_apan_refresh_keys(mspipe_apan* a, void* stream);
 MSPIPE_API mspipe_status mspipe_message_build_apan(mspipe_apan* a, const mspipe_gru* gru, const double* ts,
                                                    int64_t num_events, const float* snap_mem,
                                                    const double* snap_mem_ts, int64_t snap_step,

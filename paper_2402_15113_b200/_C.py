@@ -43,7 +43,7 @@ EXPORTS = ("mspipe_abi_version", "mspipe_last_error", "mspipe_check", "mspipe_sa
            "mspipe_shard_fetch_finish_table", "mspipe_shard_mitigate", "mspipe_train_layout", "mspipe_train_create",
            "mspipe_train_destroy", "mspipe_gru_save_gates", "mspipe_train_step", "mspipe_train_sgd",
            "mspipe_apan_create", "mspipe_apan_destroy", "mspipe_message_build_apan", "mspipe_apan_deliver",
-           "mspipe_util_kernel_events")
+           "mspipe_util_kernel_events", "mspipe_apan_refresh_keys")
 XCHG_FETCH_IDS, XCHG_FETCH_ROWS, XCHG_COMMIT = 0, 1, 2
 
 
@@ -147,6 +147,7 @@ def lib():
         L.mspipe_util_kernel_events.argtypes = [P, P]
         L.mspipe_apan_create.argtypes = [C.POINTER(P), i64, i32, i32, i32, i64, P, P, P, P, P, P, P]
         L.mspipe_apan_destroy.argtypes = [P]
+        L.mspipe_apan_refresh_keys.argtypes = [P, P]
         L.mspipe_message_build_apan.argtypes = [P, P, P, i64, P, P, i64, P, P, P, P, P, C.c_size_t, P]
         L.mspipe_apan_deliver.argtypes = [P, P, i64, P, P, P, P, i64, P, P, P, P, P, i32, P]
         if L.mspipe_abi_version() != ABI_VERSION:
@@ -751,6 +752,11 @@ class ApanHandle:
     def reset(self):
         for t in (self.mb, self.mb_ts, self.mb_pos, self.mb_cnt):
             t.zero_()
+        self.refresh_keys()
+
+    def refresh_keys(self, stream=None):
+        """Recompute the cached keys after writing the mailbox tables directly."""
+        _ck(lib().mspipe_apan_refresh_keys(self.h, stream_ptr(stream)), "mspipe_apan_refresh_keys")
 
     def __del__(self):
         if getattr(self, "h", None) and _lib is not None:

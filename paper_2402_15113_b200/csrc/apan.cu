@@ -9,8 +9,11 @@
 //   (k_gru_tc, deferred-mailbox handle: the commit writes h' and mem_ts);
 //   after the commit, w's mail [h'_w ‖ h'_o ‖ e] is delivered to w and to its
 //   sampled neighbours, the latest key p (F + 1) + s winning per node.
-// The two projections are plain GEMMs (cuBLAS SGEMM, fp32); gathers, the
-// per-winner softmax + operand build, and the delivery are kernels here.
+// The projections are plain GEMMs (cuBLAS SGEMM, fp32): q of the winners per
+// batch, and k = W_k mail ONCE per delivered mail (a key ring beside the mail
+// ring: a mail is read by up to S_mb later updates, its key never changes);
+// the per-winner softmax + operand build (mails read straight from the ring)
+// and the delivery are kernels here.
 #include <cublas_v2.h>
 
 #include "internal.cuh"
@@ -26,26 +29,15 @@ __device__ __forceinline__ int64_t nw() { return ((int64_t)gridDim.x * blockDim.
 // row of winner pair p in the prep's root layout (snapshot rows: times `step`)
 __device__ __forceinline__ int64_t root_row(int32_t p, int64_t B) { return (p & 1) ? B + (p >> 1) : (p >> 1); }
 
-// G[u*S + s] = mail slot s of winner u's node (0 beyond its filled count); Sw[u] = S.mem[w]
-__global__ void k_apan_gather(int64_t B, int32_t M, int32_t Dm, int32_t S, const int32_t* __restrict__ num,
-                              const int32_t* __restrict__ nodes, const int32_t* __restrict__ winner,
-                              const float* __restrict__ snap_mem, int64_t step, const float* __restrict__ mb,
-                              const int32_t* __restrict__ mb_cnt, float* G, float* Sw) {
+// Sw[u] = S.mem[w] (the query input and the GRU hidden input of winner u)
+__global__ void k_apan_gather(int64_t B, int32_t M, const int32_t* __restrict__ num,
+                              const int32_t* __restrict__ winner, const float* __restrict__ snap_mem, int64_t step,
+                              float* Sw) {
   const int lane = threadIdx.x & 31;
   const int32_t U = __ldg(num);
-  for (int64_t w = gw(); w < 2 * B * (S + 1); w += nw()) {
-    const int64_t u = w / (S + 1);
-    const int32_t s = (int32_t)(w % (S + 1));
-    if (s == S) {  // the hidden input row
-      const float* row = snap_mem + root_row(u < U ? __ldg(winner + u) : 0, B) * step * M;
-      for (int32_t k = lane; k < M; k += 32) Sw[u * M + k] = u < U ? __ldg(row + k) : 0.f;
-      continue;
-    }
-    const int32_t v = u < U ? __ldg(nodes + u) : -1;
-    const bool ok = v >= 0 && s < __ldg(mb_cnt + v);
-    const float* src = mb + ((int64_t)(ok ? v : 0) * S + s) * Dm;
-    float* dst = G + (u * S + s) * Dm;
-    for (int32_t k = lane; k < Dm; k += 32) dst[k] = ok ? __ldg(src + k) : 0.f;
+  for (int64_t u = gw(); u < 2 * B; u += nw()) {
+    const float* row = snap_mem + root_row(u < U ? __ldg(winner + u) : 0, B) * step * M;
+    for (int32_t k = lane; k < M; k += 32) Sw[u * M + k] = u < U ? __ldg(row + k) : 0.f;
   }
 }
 
@@ -57,9 +49,9 @@ __global__ void __launch_bounds__(256) k_apan_build(GruDesc d, int64_t B, int32_
                                                     const int32_t* __restrict__ winner,
                                                     const double* __restrict__ ts,
                                                     const double* __restrict__ snap_ts, int64_t step,
-                                                    const int32_t* __restrict__ mb_cnt, const float* __restrict__ G,
-                                                    const float* __restrict__ Sw, const float* __restrict__ Q,
-                                                    const float* __restrict__ Kp, float* xbuf, double* out_ts) {
+                                                    const int32_t* __restrict__ mb_cnt, const float* __restrict__ mb,
+                                                    const float* __restrict__ kb, const float* __restrict__ Sw,
+                                                    const float* __restrict__ Q, float* xbuf, double* out_ts) {
   __shared__ float sal[8][32];  // the warp's α (lane = slot)
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int32_t U = __ldg(num);
@@ -77,7 +69,7 @@ __global__ void __launch_bounds__(256) k_apan_build(GruDesc d, int64_t B, int32_
     if (lane < c) {
       float acc = 0.f;
       const float* q = Q + u * M;
-      const float* kr = Kp + (u * S + lane) * M;
+      const float* kr = kb + ((int64_t)v * S + lane) * M;  // k_s = W_k mail_s, cached at delivery
       for (int32_t k = 0; k < M; ++k) acc += __ldg(q + k) * __ldg(kr + k);
       e = acc * scale;
     }
@@ -96,7 +88,7 @@ __global__ void __launch_bounds__(256) k_apan_build(GruDesc d, int64_t B, int32_
     for (int32_t k = lane; k < d.Kpad; k += 32) {
       float val = 0.f;
       if (k < d.Dm) {
-        for (int32_t s = 0; s < c; ++s) val += sal[wib][s] * __ldg(G + (u * S + s) * d.Dm + k);
+        for (int32_t s = 0; s < c; ++s) val += sal[wib][s] * __ldg(mb + ((int64_t)v * S + s) * d.Dm + k);
       } else if (k < d.Dx) {
         const int32_t q = k - d.Dm;
         val = time_cos(fmaf(__ldg(d.time_w + q), dt, __ldg(d.time_b + q)));
@@ -130,12 +122,12 @@ __global__ void k_apan_mail(int64_t B, int32_t M, int32_t He, const int32_t* __r
 // F3-8, candidate (u, s): target = winner u's node (s = 0) or its root's
 // neighbour s - 1; key = p (F + 1) + s.  pass 0: atomicMax into best[v];
 // pass 1: the candidate holding best[v] writes its mail into v's next slot
-__global__ void k_apan_deliver(int64_t B, int32_t F, int32_t S, int32_t Dm, int pass,
+__global__ void k_apan_deliver(int64_t B, int32_t F, int32_t S, int32_t Dm, int32_t M, int pass,
                                const int32_t* __restrict__ num, const int32_t* __restrict__ nodes,
                                const int32_t* __restrict__ winner, const int32_t* __restrict__ nbr,
                                const int32_t* __restrict__ cnt, const double* __restrict__ ts,
-                               const float* __restrict__ mails, int32_t* best, float* mb, double* mb_ts,
-                               int32_t* mb_pos, int32_t* mb_cnt) {
+                               const float* __restrict__ mails, const float* __restrict__ keys, int32_t* best,
+                               float* mb, float* kb, double* mb_ts, int32_t* mb_pos, int32_t* mb_cnt) {
   const int lane = threadIdx.x & 31;
   const int32_t U = __ldg(num);
   for (int64_t w = gw(); w < (int64_t)U * (F + 1); w += nw()) {
@@ -166,6 +158,8 @@ __global__ void k_apan_deliver(int64_t B, int32_t F, int32_t S, int32_t Dm, int 
     if (!win) continue;
     float* out = mb + ((int64_t)v * S + pos) * Dm;
     for (int32_t k = lane; k < Dm; k += 32) out[k] = __ldg(mails + u * Dm + k);
+    float* ko = kb + ((int64_t)v * S + pos) * M;
+    for (int32_t k = lane; k < M; k += 32) ko[k] = __ldg(keys + u * M + k);
   }
 }
 
@@ -192,7 +186,8 @@ struct mspipe_apan {
   float *mb;         // caller-owned mailbox tables
   double* mb_ts;
   int32_t *mb_pos, *mb_cnt;
-  float *G, *Sw, *Q, *Kp, *mails;
+  float* kb;  // key ring [N, S, M]: k = W_k mail, computed once when the mail is delivered
+  float *Sw, *Q, *mails, *keys;
   int32_t* best;
   void* blas_ws;
   cublasHandle_t blas;
@@ -200,7 +195,7 @@ struct mspipe_apan {
 
 static void apan_free(mspipe_apan* a) {
   if (!a) return;
-  void* bufs[] = {a->w_q, a->w_k, a->G, a->Sw, a->Q, a->Kp, a->mails, a->best, a->blas_ws};
+  void* bufs[] = {a->w_q, a->w_k, a->kb, a->Sw, a->Q, a->mails, a->keys, a->best, a->blas_ws};
   for (void* b : bufs)
     if (b) cudaFree(b);
   if (a->blas) cublasDestroy(a->blas);
@@ -231,10 +226,10 @@ mspipe_status mspipe_apan_create(mspipe_apan** out, int64_t num_nodes, int32_t m
   const int64_t R = 2 * max_events;
   cudaError_t e = cudaMalloc(&a->w_q, sizeof(float) * (size_t)mem_dim * mem_dim);
   if (e == cudaSuccess) e = cudaMalloc(&a->w_k, sizeof(float) * (size_t)mem_dim * a->Dm);
-  if (e == cudaSuccess) e = cudaMalloc(&a->G, sizeof(float) * (size_t)(R * slots * a->Dm));
+  if (e == cudaSuccess) e = cudaMalloc(&a->kb, sizeof(float) * (size_t)(num_nodes * slots * mem_dim));
+  if (e == cudaSuccess) e = cudaMalloc(&a->keys, sizeof(float) * (size_t)(R * mem_dim));
   if (e == cudaSuccess) e = cudaMalloc(&a->Sw, sizeof(float) * (size_t)(R * mem_dim));
   if (e == cudaSuccess) e = cudaMalloc(&a->Q, sizeof(float) * (size_t)(R * mem_dim));
-  if (e == cudaSuccess) e = cudaMalloc(&a->Kp, sizeof(float) * (size_t)(R * slots * mem_dim));
   if (e == cudaSuccess) e = cudaMalloc(&a->mails, sizeof(float) * (size_t)(R * a->Dm));
   if (e == cudaSuccess) e = cudaMalloc(&a->best, sizeof(int32_t) * (size_t)num_nodes);
   constexpr size_t kWs = 16u << 20;
@@ -245,6 +240,7 @@ mspipe_status mspipe_apan_create(mspipe_apan** out, int64_t num_nodes, int32_t m
   if (e == cudaSuccess)
     e = cudaMemcpyAsync(a->w_k, w_k, sizeof(float) * (size_t)mem_dim * a->Dm, cudaMemcpyDefault, s);
   if (e == cudaSuccess) e = cudaMemsetAsync(a->best, 0xff, sizeof(int32_t) * (size_t)num_nodes, s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(a->kb, 0, sizeof(float) * (size_t)(num_nodes * slots * mem_dim), s);
   if (e != cudaSuccess) {
     apan_free(a);
     return cuda_status(e, "apan_create");
@@ -284,16 +280,14 @@ mspipe_status mspipe_message_build_apan(mspipe_apan* a, const mspipe_gru* gru, c
     return fail(MSPIPE_EINVAL, "message_build_apan: workspace too small");
   cudaStream_t s = (cudaStream_t)stream;
   const int64_t B = num_events, R = 2 * B;
-  k_apan_gather<<<blocks_for(R * (a->S + 1)), 256, 0, s>>>(B, a->M, a->Dm, a->S, num_unique, nodes, winner, snap_mem,
-                                                           snap_step, a->mb, a->mb_cnt, a->G, a->Sw);
+  k_apan_gather<<<blocks_for(R), 256, 0, s>>>(B, a->M, num_unique, winner, snap_mem, snap_step, a->Sw);
   if (cublasSetStream(a->blas, s) != CUBLAS_STATUS_SUCCESS ||
       cublasSetWorkspace(a->blas, a->blas_ws, 16u << 20) != CUBLAS_STATUS_SUCCESS ||
-      gemm_nt(a->blas, R, a->M, a->M, a->Sw, a->w_q, a->Q) != CUBLAS_STATUS_SUCCESS ||
-      gemm_nt(a->blas, R * a->S, a->M, a->Dm, a->G, a->w_k, a->Kp) != CUBLAS_STATUS_SUCCESS)
+      gemm_nt(a->blas, R, a->M, a->M, a->Sw, a->w_q, a->Q) != CUBLAS_STATUS_SUCCESS)
     return fail(MSPIPE_ECUDA, "message_build_apan: cuBLAS");
   const int64_t rows = (R + tc::kM - 1) / tc::kM * tc::kM;
   k_apan_build<<<blocks_for(rows), 256, 0, s>>>(gru->d, B, a->S, num_unique, nodes, winner, ts, snap_mem_ts, snap_step,
-                                                a->mb_cnt, a->G, a->Sw, a->Q, a->Kp, (float*)workspace, out_ts);
+                                                a->mb_cnt, a->mb, a->kb, a->Sw, a->Q, (float*)workspace, out_ts);
   return cuda_status(cudaGetLastError(), "message_build_apan: launch");
 }
 
@@ -317,9 +311,25 @@ mspipe_status mspipe_apan_deliver(mspipe_apan* a, mspipe_memory* st, int64_t com
   const int64_t B = num_events, R = 2 * B;
   k_apan_mail<<<blocks_for(R), 256, 0, s>>>(B, a->M, a->He, num_unique, nodes, winner, src, dst, edge_feat, mem,
                                             a->mails);
+  // the key of every new mail, once (rows >= U: stale but never delivered)
+  if (cublasSetStream(a->blas, s) != CUBLAS_STATUS_SUCCESS ||
+      cublasSetWorkspace(a->blas, a->blas_ws, 16u << 20) != CUBLAS_STATUS_SUCCESS ||
+      gemm_nt(a->blas, R, a->M, a->Dm, a->mails, a->w_k, a->keys) != CUBLAS_STATUS_SUCCESS)
+    return fail(MSPIPE_ECUDA, "apan_deliver: cuBLAS");
   for (int pass = 0; pass < 2; ++pass)
-    k_apan_deliver<<<blocks_for(R * (fanout + 1)), 256, 0, s>>>(B, fanout, a->S, a->Dm, pass, num_unique, nodes,
-                                                                 winner, nbr, cnt, ts, a->mails, a->best, a->mb,
-                                                                 a->mb_ts, a->mb_pos, a->mb_cnt);
+    k_apan_deliver<<<blocks_for(R * (fanout + 1)), 256, 0, s>>>(B, fanout, a->S, a->Dm, a->M, pass, num_unique,
+                                                                 nodes, winner, nbr, cnt, ts, a->mails, a->keys,
+                                                                 a->best, a->mb, a->kb, a->mb_ts, a->mb_pos,
+                                                                 a->mb_cnt);
   return cuda_status(cudaGetLastError(), "apan_deliver: launch");
+}
+
+mspipe_status mspipe_apan_refresh_keys(mspipe_apan* a, void* stream) {
+  if (!a) return fail(MSPIPE_EINVAL, "apan_refresh_keys: NULL handle");
+  cudaStream_t s = (cudaStream_t)stream;
+  if (cublasSetStream(a->blas, s) != CUBLAS_STATUS_SUCCESS ||
+      cublasSetWorkspace(a->blas, a->blas_ws, 16u << 20) != CUBLAS_STATUS_SUCCESS ||
+      gemm_nt(a->blas, a->num_nodes * a->S, a->M, a->Dm, a->mb, a->w_k, a->kb) != CUBLAS_STATUS_SUCCESS)
+    return fail(MSPIPE_ECUDA, "apan_refresh_keys: cuBLAS");
+  return MSPIPE_OK;
 }

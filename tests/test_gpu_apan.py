@@ -66,6 +66,7 @@ def test_apan_teacher_forced(dev, name, i, E):
     st.memory.mem_ts.copy_(_t(state["mem_ts"], dev))
     for k in ("mb", "mb_ts", "mb_pos", "mb_cnt"):
         getattr(st.apan, k).copy_(_t(box[k], dev))
+    st.apan.refresh_keys()
     x = {k: _t(v[j0:j1], dev) for k, v in dict(src=src, dst=dst, ts=ts, neg=neg).items()}
     x["ef"] = _t(ef, dev)
     st.bind_resident(x["src"], x["dst"], x["ts"], x["neg"], x["ef"])
