@@ -128,14 +128,15 @@ def test_sgd_updates_params_and_the_updater(dev):
     assert np.all(np.abs(got - o["mem"]) <= 1e-4 * np.abs(o["mem"]) + 1e-6)
 
 
-@pytest.mark.parametrize("name,k,nb,lr", [("tiny", 0, 12, 1e-2), ("tiny", 1, 12, 1e-2), ("wiki", 1, 8, 1e-3)])
-def test_training_trajectory_matches_oracle(dev, name, k, nb, lr):
+@pytest.mark.parametrize("name,k,nb,lr,tail", [("tiny", 0, 12, 1e-2, 0), ("tiny", 1, 12, 1e-2, 0),
+                                               ("wiki", 1, 8, 1e-3, 0), ("tiny", 2, 7, 1e-2, 123)])
+def test_training_trajectory_matches_oracle(dev, name, k, nb, lr, tail):
     """Stage + training over nb batches with SGD (weights change every step,
     memory committed from the updated GRU): per-batch losses, final memory and
     final parameters against the oracle run in the same order (exact schedule:
     batch i reads S_{max(0, i-1-k)} and the weights after SGD of batch i-1)."""
     cfg = CONFIGS[name]
-    E = nb * cfg.batch
+    E = nb * cfg.batch - tail  # tail > 0: a ragged last batch
     src, dst, ts, neg = make_events(cfg, 0, E)
     ef = edge_features(0, 0, E, cfg.edge_dim)
     M, F, B = cfg.mem_dim, cfg.fanout, cfg.batch
@@ -154,7 +155,7 @@ def test_training_trajectory_matches_oracle(dev, name, k, nb, lr):
     gru, prm = dict(gp), dict(tp)
     losses = []
     for i in range(1, nb + 1):
-        b = slice((i - 1) * B, i * B)
+        b = slice((i - 1) * B, min(i * B, E))
         snap = states[max(0, i - 1 - k)]
         out = ot.train_step(cfg.num_nodes, src[b], dst[b], neg[b], ts[b], ef[b], snap["mem"], snap["mem_ts"], graph,
                             gru, prm, fanout=F)
@@ -195,3 +196,29 @@ def test_train_abi_errors(dev):
     with pytest.raises(_C.MspipeError) as e:
         _C.TrainHandle(tc, cfg.num_nodes, 100, 40, 200, p, gr)  # fanout > 31
     assert e.value.status == _C.EINVAL
+
+
+def test_train_single_event_batch(dev):
+    """Degenerate batch: one event (2 winners, 3 roots) on a fresh stage."""
+    cfg = CONFIGS["tiny"]
+    src, dst, ts, neg = make_events(cfg, 0, 50)
+    M = cfg.mem_dim
+    gp = gru_params(M, cfg.mail_dim, cfg.time_dim)
+    tp = train_params(M, cfg.time_dim, 100)
+    ef = edge_features(0, 0, 50, cfg.edge_dim)
+    g = build_tcsr(cfg.num_nodes, src, dst, ts, dev)
+    st = MemoryStage(StageConfig(cfg.num_nodes, M, cfg.edge_dim, cfg.time_dim, cfg.fanout, 1, 0, fused=True,
+                                 train=dict(params=tp, lr=0.0, sgd=False)), gp, g, dev)
+    j = 40
+    x = {k: _t(v[j:j + 1], dev) for k, v in dict(src=src, dst=dst, ts=ts, neg=neg, ef=ef).items()}
+    st.bind_resident(x["src"], x["dst"], x["ts"], x["neg"], x["ef"])
+    st.prep(1)
+    st.commit(1)
+    torch.cuda.synchronize()
+    _C.check()
+    zero = oracle.new_state(cfg.num_nodes, M, cfg.edge_dim)
+    ref = ot.train_step(cfg.num_nodes, src[j:j + 1], dst[j:j + 1], neg[j:j + 1], ts[j:j + 1], ef[j:j + 1], zero["mem"],
+                        zero["mem_ts"], oracle.Graph(cfg.num_nodes, src, dst, ts), gp, tp, fanout=cfg.fanout)
+    assert abs(float(st.trainer.losses[0].item()) - ref["loss"]) <= TOL * ref["loss"]
+    for k in _C.TRAIN_TENSORS:
+        assert _worst(st.trainer.tensor(k, "grads").cpu().numpy(), ref["grads"][k]) <= TOL, k
