@@ -464,15 +464,15 @@ def run_mspipe(args):
 
     def apan_measurement():
         """Row F3, APAN: the stage with the multi-slot mailbox (attention message,
-        GRU GEMM, propagation to sampled neighbours) at k = 0, grouped graphs and
-        the same flush protocol; events/s beside the TGN stage's."""
+        GRU GEMM, propagation to sampled neighbours) at the config's staleness k,
+        grouped graphs and the same flush protocol; events/s beside the TGN stage's."""
         import dataclasses
 
         rng = np.random.default_rng(args.seed + 77)
         M, Dm = cfg.mem_dim, cfg.mail_dim
         ap = dict(w_q=(rng.uniform(-1, 1, (M, M)) / np.sqrt(M)).astype(np.float32),
                   w_k=(rng.uniform(-1, 1, (M, Dm)) / np.sqrt(Dm)).astype(np.float32), slots=10)
-        sca = dataclasses.replace(sc, k=0, mailbox="apan", apan=ap, mitigation=None, double_buffer=False)
+        sca = dataclasses.replace(sc, mailbox="apan", apan=ap, mitigation=None, double_buffer=False)
         sta = MemoryStage(sca, w["params"], g, dev)
         t = resident
         sta.bind_resident(t["src"], t["dst"], t["ts"], t["neg"], t["ef"])
@@ -486,7 +486,8 @@ def run_mspipe(args):
         del gr_a, sta
         return {"metric": "APAN memory stage (row F3) events/s", "unit": UNIT, "value": ev_a / (sum(ms_a) / 1e3),
                 "ms_per_step": float(sum(ms_a)) / K,
-                "config": {"staleness_k": 0, "slots": 10, "message": "attention over the filled mailbox slots",
+                "config": {"staleness_k": sca.k, "slots": 10, "message": "attention over the filled mailbox slots",
+                           "tables": "one set (the commit waits for the fetch and the APAN build of the later batch)",
                            "propagation": "node + its sampled neighbours, latest key wins",
                            "mean_filled_slots_at_end": filled},
                 "note": "the mailbox epoch reset is the caller's (not between timed blocks)",

@@ -59,9 +59,11 @@ def attention_message(mem_w, mb_w, cnt_w, w_q, w_k):
     return np.einsum("us,usd->ud", a, np.asarray(mb_w, np.float64)), a
 
 
-def step(num_nodes, src, dst, ts, ef, state, box, graph: Graph, gru, apan, fanout=10, snapshot=None):
-    """One APAN iteration on the snapshot (state, box) (k = 0: the state after
-    the previous iteration).  Returns the new (state, box) and the winners' h'."""
+def step(num_nodes, src, dst, ts, ef, state, box, graph: Graph, gru, apan, fanout=10, latest=None, latest_box=None):
+    """One APAN iteration: the message and the GRU read the snapshot (state, box)
+    = version v(i) (Eq. 2); the commit and the deliveries apply to
+    the latest version (latest, latest_box; default: the snapshot, k = 0).
+    Returns the new (state, box) and the winners' h'."""
     src, dst = np.asarray(src, np.int32), np.asarray(dst, np.int32)
     ts = np.asarray(ts, np.float64)
     B = len(src)
@@ -73,7 +75,7 @@ def step(num_nodes, src, dst, ts, ef, state, box, graph: Graph, gru, apan, fanou
     dt = (ts[ev] - mem_ts[nodes]).astype(np.float32)
     x = np.concatenate([msg, time_encode(dt, gru["time_w"], gru["time_b"])], 1)
     hn, _ = gru_forward(x, np.asarray(mem[nodes], np.float64), gru)          # F3-5
-    new = {k: v.copy() for k, v in state.items()}
+    new = {k: v.copy() for k, v in (state if latest is None else latest).items()}
     new["mem"][nodes] = hn.astype(np.float32)                                 # F3-6
     new["mem_ts"][nodes] = ts[ev]
     other = np.where(role == 1, src[ev], dst[ev])
@@ -88,7 +90,7 @@ def step(num_nodes, src, dst, ts, ef, state, box, graph: Graph, gru, apan, fanou
             key = int(winner[u]) * (fanout + 1) + s
             if v not in best or key > best[v][0]:
                 best[v] = (key, u)
-    nb = {k: v.copy() for k, v in box.items()}
+    nb = {k: v.copy() for k, v in (box if latest_box is None else latest_box).items()}
     S = box["mb"].shape[1]
     for v, (key, u) in best.items():
         pos = nb["mb_pos"][v]
@@ -99,8 +101,9 @@ def step(num_nodes, src, dst, ts, ef, state, box, graph: Graph, gru, apan, fanou
     return new, nb, dict(nodes=nodes, winner=winner, h_new=hn, mails=mails, targets=best)
 
 
-def run_stream(num_nodes, src, dst, ts, ef, gru, apan, batch, fanout=10, max_batches=-1, slots=SLOTS):
-    """k = 0 over the stream (the T-CSR of the whole stream; A1's strict ts < t)."""
+def run_stream(num_nodes, src, dst, ts, ef, gru, apan, batch, fanout=10, max_batches=-1, slots=SLOTS, k=0):
+    """Over the stream (the T-CSR of the whole stream; A1's strict ts < t) under
+    the exact staleness schedule: batch i reads version v(i) = max(0, i-1-k)."""
     import oracle
     src, dst, ts = np.asarray(src, np.int32), np.asarray(dst, np.int32), np.asarray(ts, np.float64)
     M = np.asarray(gru["w_hh"]).shape[1]
@@ -111,7 +114,11 @@ def run_stream(num_nodes, src, dst, ts, ef, gru, apan, batch, fanout=10, max_bat
     nb = -(-len(src) // batch)
     if max_batches >= 0:
         nb = min(nb, max_batches)
-    for i in range(nb):
-        b = slice(i * batch, min((i + 1) * batch, len(src)))
-        state, box, _ = step(num_nodes, src[b], dst[b], ts[b], ef[b], state, box, graph, gru, apan, fanout)
+    hist = [(state, box)]  # version v = after batch v
+    for i in range(1, nb + 1):
+        b = slice((i - 1) * batch, min(i * batch, len(src)))
+        snap_s, snap_b = hist[max(0, i - 1 - k)]
+        state, box, _ = step(num_nodes, src[b], dst[b], ts[b], ef[b], snap_s, snap_b, graph, gru, apan, fanout,
+                             latest=hist[-1][0], latest_box=hist[-1][1])
+        hist.append((state, box))
     return state, box

@@ -59,6 +59,8 @@ class StageConfig:
         return ok if self.fused is None else (self.fused and ok)
 
     def use_double_buffer(self) -> bool:
+        if self.mailbox == "apan":  # one table set: the commit waits for the fetch and the APAN build
+            return False
         return self.k >= 1 if self.double_buffer is None else bool(self.double_buffer)
 
 
@@ -209,8 +211,8 @@ class MemoryStage(_TimedOps):
         self.deferred = cfg.mailbox == "deferred"
         self.apan = None
         if cfg.mailbox == "apan":  # row F3: APAN (multi-slot mailbox, attention message, propagation)
-            if cfg.k != 0 or cfg.cell != "gru" or cfg.precision != _C.FP32_3XTF32 or cfg.apan is None:
-                raise ValueError("mailbox='apan' runs at k = 0 on the 3xTF32 GRUCell path with cfg.apan weights")
+            if cfg.cell != "gru" or cfg.precision != _C.FP32_3XTF32 or cfg.apan is None or cfg.schedule != "exact":
+                raise ValueError("mailbox='apan' runs on the 3xTF32 GRUCell path, exact schedule, with cfg.apan weights")
             self.apan = _C.ApanHandle(cfg.num_nodes, cfg.mem_dim, cfg.edge_dim, cfg.apan.get("slots", 10), cfg.batch,
                                       cfg.apan["w_q"], cfg.apan["w_k"], self.device)
         self.gru = _C.GruHandle(cfg.mem_dim, cfg.edge_dim, cfg.time_dim, params, self.device, cfg.precision,
@@ -427,7 +429,7 @@ class MemoryStage(_TimedOps):
         self._ev("prep_end")
         self._features(sl, samp)
         self.versions[i] = sl.version
-        if not self.memory.double_buffer:
+        if not self.memory.double_buffer and self.apan is None:
             self._fetched = torch.cuda.Event()  # the state tables have been read for batch i
             self._fetched.record()
         self._ev("build")
@@ -442,6 +444,9 @@ class MemoryStage(_TimedOps):
                              sl.dd["num"], sl.uts[: 2 * n], sl.umail[: 2 * n], sl.ws,
                              snap_h=sl.h[: 2 * n] if sl.h is not None else None)
         self._ev("build_end")
+        if self.apan is not None:  # the APAN build read the mailbox rings: commits of later batches wait for it
+            self._fetched = torch.cuda.Event()
+            self._fetched.record()
 
     def _upd(self, i):
         n = self.inputs(i)["src"].numel()

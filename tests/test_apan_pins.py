@@ -104,3 +104,39 @@ def test_ring_keeps_the_last_slots_mails():
     for j in range(n_b - S, n_b):
         assert box["mb_ts"][0, j % S] == ts[j]
         assert box["mb"][0, j % S, -1] == ef[j, 0]
+
+
+def test_staleness_zero_equals_sequential_and_k_reads_old_versions():
+    """run_stream(k=0) = stepping the latest version; with k = 2 the third batch's
+    message reads version 0 (zeros: empty boxes, zero memory), so its h' equals
+    the GRU of [0 | cos(w t + p)] with h = 0."""
+    rng = np.random.default_rng(9)
+    N, M, He, Dt, B = 12, 4, 2, 3, 5
+    E = 4 * B
+    src = rng.integers(0, N, E).astype(np.int32)
+    dst = ((src + 1 + rng.integers(0, N - 1, E)) % N).astype(np.int32)
+    ts = np.cumsum(rng.uniform(0.5, 1.5, E))
+    ef = rng.uniform(-1, 1, (E, He)).astype(np.float32)
+    g = gru_params(M, 2 * M + He, Dt, seed=3)
+    w = _w(M, 2 * M + He, 4)
+    s0, b0 = apan.run_stream(N, src, dst, ts, ef, g, w, B, fanout=3, k=0)
+    graph = oracle.Graph(N, src, dst, ts)
+    st, bx = oracle.new_state(N, M, He), apan.new_mailbox(N, M, He)
+    for i in range(4):
+        b = slice(i * B, (i + 1) * B)
+        st, bx, _ = apan.step(N, src[b], dst[b], ts[b], ef[b], st, bx, graph, g, w, fanout=3)
+    assert np.array_equal(s0["mem"], st["mem"]) and np.array_equal(b0["mb"], bx["mb"])
+    # k = 2: batch 3 reads version 0
+    hist = [(oracle.new_state(N, M, He), apan.new_mailbox(N, M, He))]
+    for i in range(1, 4):
+        b = slice((i - 1) * B, i * B)
+        snap = hist[max(0, i - 1 - 2)]
+        ns, nb, info = apan.step(N, src[b], dst[b], ts[b], ef[b], snap[0], snap[1], graph, g, w, fanout=3,
+                                 latest=hist[-1][0], latest_box=hist[-1][1])
+        hist.append((ns, nb))
+    ev = info["winner"] >> 1
+    from oracle.train import gru_forward, time_encode
+    x = np.concatenate([np.zeros((len(ev), 2 * M + He)),
+                        time_encode((ts[2 * B:3 * B][ev]).astype(np.float32), g["time_w"], g["time_b"])], 1)
+    want, _ = gru_forward(x, np.zeros((len(ev), M)), g)
+    assert np.allclose(info["h_new"], want, rtol=0, atol=1e-15)

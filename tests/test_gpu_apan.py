@@ -33,8 +33,8 @@ def _weights(M, Dm, seed=21):
                 w_k=rng.uniform(-1, 1, (M, Dm)).astype(np.float32) / np.sqrt(Dm))
 
 
-def _stage(dev, cfg, gp, ap, src, dst, ts, neg, ef):
-    sc = StageConfig(cfg.num_nodes, cfg.mem_dim, cfg.edge_dim, cfg.time_dim, cfg.fanout, cfg.batch, 0, fused=True,
+def _stage(dev, cfg, gp, ap, src, dst, ts, neg, ef, k=0):
+    sc = StageConfig(cfg.num_nodes, cfg.mem_dim, cfg.edge_dim, cfg.time_dim, cfg.fanout, cfg.batch, k, fused=True,
                      mailbox="apan", apan=dict(ap, slots=oa.SLOTS))
     g = build_tcsr(cfg.num_nodes, src, dst, ts, dev)
     st = MemoryStage(sc, gp, g, dev)
@@ -90,20 +90,24 @@ def _compare(st, new, nb, tol=1e-4):
     print(f"memory {dm:.1e}, mailbox rows {db:.1e}")
 
 
-@pytest.mark.parametrize("name,nb_", [("tiny", 50), ("wiki", 15)])
-def test_apan_stream_free_running(dev, name, nb_):
+@pytest.mark.parametrize("name,nb_,k", [("tiny", 50, 0), ("wiki", 15, 0), ("tiny", 30, 1), ("tiny", 30, 3),
+                                        ("wiki", 12, 2)])
+def test_apan_stream_free_running(dev, name, nb_, k):
+    """Free-running under the exact staleness schedule (k >= 1: two streams, one
+    table set; the commit waits for the fetch and the APAN build of the later batch)."""
     cfg = CONFIGS[name]
     E = nb_ * cfg.batch
     src, dst, ts, neg = make_events(cfg, 0, E)
     ef = edge_features(0, 0, E, cfg.edge_dim)
     gp = gru_params(cfg.mem_dim, cfg.mail_dim, cfg.time_dim)
     ap = _weights(cfg.mem_dim, cfg.mail_dim)
-    st, _ = _stage(dev, cfg, gp, ap, src, dst, ts, neg, ef)
-    t = {k: _t(v, dev) for k, v in dict(src=src, dst=dst, ts=ts, neg=neg, ef=ef).items()}
+    st, _ = _stage(dev, cfg, gp, ap, src, dst, ts, neg, ef, k=k)
+    t = {kk: _t(v, dev) for kk, v in dict(src=src, dst=dst, ts=ts, neg=neg, ef=ef).items()}
     st.bind_resident(t["src"], t["dst"], t["ts"], t["neg"], t["ef"])
     st.run()
     torch.cuda.synchronize()
     _C.check()
-    new, nb = oa.run_stream(cfg.num_nodes, src, dst, ts, ef, gp, ap, cfg.batch, fanout=cfg.fanout)
+    assert [st.versions[i] for i in range(1, nb_ + 1)] == [max(0, i - 1 - k) for i in range(1, nb_ + 1)]
+    new, nb = oa.run_stream(cfg.num_nodes, src, dst, ts, ef, gp, ap, cfg.batch, fanout=cfg.fanout, k=k)
     _compare(st, new, nb, tol=1e-3)
     assert int(st.apan.mb_cnt.max().item()) == oa.SLOTS  # some rings wrapped
