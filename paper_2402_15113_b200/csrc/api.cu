@@ -1195,7 +1195,9 @@ mspipe_status mspipe_util_graph_end(void* stream, void** out_exec) {
     return cuda_status(e, "util_graph_end: end capture");
   }
   cudaGraphExec_t x = nullptr;
-  e = cudaGraphInstantiate(&x, g, 0);
+  // MSPIPE_GRAPH_PRIO=1: kernel nodes keep the priority of the stream they were
+  // captured on (the prep's side stream vs the commit's), an A/B knob
+  e = cudaGraphInstantiate(&x, g, env_int("MSPIPE_GRAPH_PRIO", 0) ? cudaGraphInstantiateFlagUseNodePriority : 0);
   cudaGraphDestroy(g);
   if (e != cudaSuccess) return cuda_status(e, "util_graph_end: instantiate");
   *out_exec = (void*)x;
