@@ -9,8 +9,12 @@
 //   T4 TGN link decoder;  T5 mean BCE on logits;  T6 SGD;  T7 DP mean.
 //
 // The contractions (projections, their weight and input gradients, the
-// GRU weight gradient) are plain fp32 GEMMs: cuBLAS SGEMM (default math: no
-// TF32), row-major through the transposed-operand identity.  The gathers, the
+// GRU weight gradient) are plain GEMMs on cuBLAS, row-major through the
+// transposed-operand identity: the three over the 3B·𝒩 neighbour slots (the
+// K|V projection, its weight gradient and its input gradient: ~85 % of the
+// step's FLOPs) in 3xTF32 on the tensor cores (operands split into tf32
+// hi | lo by their producers, three TF32 GEMMs accumulated in fp32: fp32
+// accuracy), the small rest in SGEMM (default math: no TF32).  The gathers, the
 // per-root attention (≤ 𝒩 = 10 neighbours, one warp per root), the decoder's
 // nonlinearity and loss, the deterministic scatter of the node gradients into
 // the winners' h' rows (stable radix sort of (winner, slot) pairs, then one
@@ -75,7 +79,7 @@ __global__ void __launch_bounds__(kTrThreads) k_tr_gather(
     Dims d, int64_t R, const int32_t* __restrict__ sub, const float* __restrict__ sdt,
     const int32_t* __restrict__ cnt, const float* __restrict__ snap, const int32_t* __restrict__ wmap,
     const float* __restrict__ hn, const float* __restrict__ tw, const float* __restrict__ tb, float* sroot,
-    float* zn, int32_t* key, int32_t* val) {
+    float* zn, float* zn_lo, int32_t* key, int32_t* val) {
   const int lane = threadIdx.x & 31;
   const int32_t F = d.F, M = d.M, Z = d.M + d.Dt;
   for (int64_t slot = gwarp(); slot < R * (F + 1); slot += nwarps()) {  // one warp per (root, slot)
@@ -91,12 +95,20 @@ __global__ void __launch_bounds__(kTrThreads) k_tr_gather(
         val[slot] = (int32_t)slot;
       }
       const float* row = u >= 0 ? hn + (int64_t)u * M : snap + slot * M;
-      float* out = s == 0 ? sroot + r * M : zn + (r * F + s - 1) * Z;
-      for (int32_t k = lane; k < M; k += 32) out[k] = valid ? __ldg(row + k) : 0.f;
-      if (s > 0) {
+      if (s == 0) {
+        float* out = sroot + r * M;
+        for (int32_t k = lane; k < M; k += 32) out[k] = valid ? __ldg(row + k) : 0.f;
+      } else {  // neighbour rows feed the 3xTF32 projections: tf32 hi | lo images
+        float* out = zn + (r * F + s - 1) * Z;
+        float* olo = zn_lo + (r * F + s - 1) * Z;
         const float dt = __ldg(sdt + r * F + s - 1);
-        for (int32_t q = lane; q < d.Dt; q += 32)
-          out[M + q] = valid ? time_cos(fmaf(__ldg(tw + q), dt, __ldg(tb + q))) : 0.f;
+        for (int32_t k = lane; k < Z; k += 32) {
+          const float v = !valid ? 0.f
+                          : k < M ? __ldg(row + k) : time_cos(fmaf(__ldg(tw + k - M), dt, __ldg(tb + k - M)));
+          const float hi = tc::tf32_rna(v);
+          out[k] = hi;
+          olo[k] = tc::tf32_rna(v - hi);
+        }
       }
     }
   }
@@ -229,7 +241,7 @@ __global__ void __launch_bounds__(kTrThreads) k_tr_attn_bwd(Dims d, int64_t R, c
                                                             const float* __restrict__ kv,
                                                             const float* __restrict__ alpha,
                                                             const float* __restrict__ dzo, float* dq,
-                                                            float* dkv) {
+                                                            float* dkv, float* dkv_lo) {
   __shared__ float s_ds[kTrThreads / 32][32], s_al[kTrThreads / 32][32];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int32_t F = d.F, H = d.H, M = d.M;
@@ -260,9 +272,15 @@ __global__ void __launch_bounds__(kTrThreads) k_tr_attn_bwd(Dims d, int64_t R, c
       const float dsu = s_ds[wib][u];
       const float au = s_al[wib][u];
       float* o = dkv + (r * F + u) * 2 * H;
+      float* ol = dkv_lo + (r * F + u) * 2 * H;
       for (int32_t h = lane; h < H; h += 32) {
-        o[h] = u < c ? dsu * __ldg(q + r * H + h) * scale : 0.f;
-        o[H + h] = u < c ? au * __ldg(da + h) : 0.f;
+        const float dk = u < c ? dsu * __ldg(q + r * H + h) * scale : 0.f;
+        const float dv = u < c ? au * __ldg(da + h) : 0.f;
+        const float kh = tc::tf32_rna(dk), vh = tc::tf32_rna(dv);
+        o[h] = kh;
+        o[H + h] = vh;
+        ol[h] = tc::tf32_rna(dk - kh);
+        ol[H + h] = tc::tf32_rna(dv - vh);
       }
     }
   }
@@ -458,6 +476,34 @@ __global__ void k_tr_fill(int64_t n, float v, float* p) {
   for (int64_t t = gthread(); t < n; t += nthreads()) p[t] = v;
 }
 
+__global__ void k_tr_split(int64_t n, const float* __restrict__ x, float* hi, float* lo) {
+  for (int64_t t = gthread(); t < n; t += nthreads()) {
+    const float v = x[t];
+    const float h = tc::tf32_rna(v);
+    hi[t] = h;
+    lo[t] = tc::tf32_rna(v - h);
+  }
+}
+
+// row-major C = op(A) op(B) on the tensor cores in 3xTF32 (A = A_hi + A_lo, B = B_hi + B_lo,
+// every part tf32-representable, so each product is exact and the sums are fp32):
+//   C = A_lo B_hi + A_hi B_lo + A_hi B_hi   (the dropped A_lo B_lo ~ 2^-22 relative)
+cublasStatus_t gemm_tf32(cublasHandle_t h, bool ta, bool tb, int64_t m, int64_t n, int64_t k, const float* A,
+                         int64_t lda, const float* B, int64_t ldb, float beta, float* C, int64_t ldc) {
+  const float one = 1.f;
+  return cublasGemmEx(h, tb ? CUBLAS_OP_T : CUBLAS_OP_N, ta ? CUBLAS_OP_T : CUBLAS_OP_N, (int)n, (int)m, (int)k, &one,
+                      B, CUDA_R_32F, (int)ldb, A, CUDA_R_32F, (int)lda, &beta, C, CUDA_R_32F, (int)ldc,
+                      CUBLAS_COMPUTE_32F_FAST_TF32, CUBLAS_GEMM_DEFAULT);
+}
+cublasStatus_t gemm3(cublasHandle_t h, bool ta, bool tb, int64_t m, int64_t n, int64_t k, const float* Ahi,
+                     const float* Alo, int64_t lda, const float* Bhi, const float* Blo, int64_t ldb, float* C,
+                     int64_t ldc) {
+  cublasStatus_t st = gemm_tf32(h, ta, tb, m, n, k, Alo, lda, Bhi, ldb, 0.f, C, ldc);
+  if (st == CUBLAS_STATUS_SUCCESS) st = gemm_tf32(h, ta, tb, m, n, k, Ahi, lda, Blo, ldb, 1.f, C, ldc);
+  if (st == CUBLAS_STATUS_SUCCESS) st = gemm_tf32(h, ta, tb, m, n, k, Ahi, lda, Bhi, ldb, 1.f, C, ldc);
+  return st;
+}
+
 // row-major C[m, n] = alpha op(A)[m, k] op(B)[k, n] + beta C (column-major cuBLAS on the transposes)
 cublasStatus_t gemm_rm(cublasHandle_t h, bool ta, bool tb, int64_t m, int64_t n, int64_t k, const float* A,
                        int64_t lda, const float* B, int64_t ldb, float beta, float* C, int64_t ldc) {
@@ -493,6 +539,7 @@ struct mspipe_train {
   int32_t* wmap;
   float *sroot, *zn, *q, *kv, *alpha, *zo, *emb, *za, *pre, *y, *logit, *dlogit, *dpre, *dza, *demb, *dzo, *dq, *dkv,
       *dzn, *dhn, *D, *xp, *ones, *cs;
+  float *zn_lo, *dkv_lo, *wkv_hi, *wkv_lo;  // 3xTF32 parts (zn / dkv hold the hi parts)
   double* term;
   int32_t *key, *val, *skey, *sval;
   int64_t *lo_hi, *poff;  // per winner: its sorted segment, exclusive scan of its piece counts
@@ -507,7 +554,8 @@ static void train_free(mspipe_train* t) {
   if (!t) return;
   void* bufs[] = {t->wmap, t->sroot, t->zn, t->q, t->kv, t->alpha, t->zo, t->emb, t->za, t->pre, t->y, t->logit,
                   t->dlogit, t->dpre, t->dza, t->demb, t->dzo, t->dq, t->dkv, t->dzn, t->dhn, t->D, t->xp, t->ones,
-                  t->cs, t->term, t->key, t->val, t->skey, t->sval, t->sort_tmp, t->blas_ws, t->lo_hi, t->poff, t->part};
+                  t->cs, t->term, t->key, t->val, t->skey, t->sval, t->sort_tmp, t->blas_ws, t->lo_hi, t->poff, t->part,
+                  t->zn_lo, t->dkv_lo, t->wkv_hi, t->wkv_lo};
   for (void* b : bufs)
     if (b) cudaFree(b);
   if (t->blas) cublasDestroy(t->blas);
@@ -573,6 +621,10 @@ mspipe_status mspipe_train_create(mspipe_train** out, const mspipe_gru* gru, int
   af(&t->dq, R * H);
   af(&t->dkv, R * F * 2 * H);
   af(&t->dzn, R * F * M);
+  af(&t->zn_lo, R * F * Z);
+  af(&t->dkv_lo, R * F * 2 * H);
+  af(&t->wkv_hi, 2 * H * Z);
+  af(&t->wkv_lo, 2 * H * Z);
   af(&t->dhn, 2 * B * M);
   af(&t->D, 2 * B * 4 * M);
   af(&t->xp, 2 * B * g.K);
@@ -675,10 +727,11 @@ mspipe_status mspipe_train_step(mspipe_train* t, const mspipe_gru* gru, int64_t 
   // forward ------------------------------------------------------------------
   k_tr_map<<<grid_for(B2, 256), 256, 0, s>>>(nodes, num_unique, t->wmap, 1);
   k_tr_gather<<<grid_for(R * (F + 1) * 32, kTrThreads), kTrThreads, 0, s>>>(d, R, sub_ids, sub_dt, sub_cnt, snap_mem, t->wmap,
-                                                                 new_mem, gru->time_w, gru->time_b, t->sroot, t->zn,
+                                                                 new_mem, gru->time_w, gru->time_b, t->sroot, t->zn, t->zn_lo,
                                                                  t->key, t->val);
   TR_BLAS(gemm_rm(t->blas, false, true, R, H, M, t->sroot, M, wq, M, 0.f, t->q, H));
-  TR_BLAS(gemm_rm(t->blas, false, true, R * F, 2 * H, Z, t->zn, Z, wkv, Z, 0.f, t->kv, 2 * H));
+  k_tr_split<<<grid_for(2 * H * Z, 256), 256, 0, s>>>(2 * H * Z, wkv, t->wkv_hi, t->wkv_lo);
+  TR_BLAS(gemm3(t->blas, false, true, R * F, 2 * H, Z, t->zn, t->zn_lo, Z, t->wkv_hi, t->wkv_lo, Z, t->kv, 2 * H));
   k_tr_attn_fwd<<<grid_for(R * 32, kTrThreads), kTrThreads, 0, s>>>(d, R, sub_cnt, t->q, t->kv, t->sroot, t->alpha,
                                                                    t->zo);
   TR_BLAS(gemm_rm(t->blas, false, true, R, H, H + M, t->zo, H + M, wo, H + M, 0.f, t->emb, H));
@@ -702,11 +755,12 @@ mspipe_status mspipe_train_step(mspipe_train* t, const mspipe_gru* gru, int64_t 
   TR_BLAS(colsum(t->blas, R, H, t->demb, H, t->ones, G + t->off[P_BO]));
   TR_BLAS(gemm_rm(t->blas, false, false, R, H + M, H, t->demb, H, wo, H + M, 0.f, t->dzo, H + M));
   k_tr_attn_bwd<<<grid_for(R * 32, kTrThreads), kTrThreads, 0, s>>>(d, R, sub_cnt, t->q, t->kv, t->alpha, t->dzo,
-                                                                   t->dq, t->dkv);
+                                                                   t->dq, t->dkv, t->dkv_lo);
   TR_BLAS(gemm_rm(t->blas, true, false, H, M, R, t->dq, H, t->sroot, M, 0.f, G + t->off[P_WQ], M));
   TR_BLAS(gemm_rm(t->blas, false, false, R, M, H, t->dq, H, wq, M, 1.f, t->dzo + H, H + M));  // ds~(root) += W_q^T dq
-  TR_BLAS(gemm_rm(t->blas, true, false, 2 * H, Z, R * F, t->dkv, 2 * H, t->zn, Z, 0.f, G + t->off[P_WK], Z));
-  TR_BLAS(gemm_rm(t->blas, false, false, R * F, M, 2 * H, t->dkv, 2 * H, wkv, Z, 0.f, t->dzn, M));
+  TR_BLAS(gemm3(t->blas, true, false, 2 * H, Z, R * F, t->dkv, t->dkv_lo, 2 * H, t->zn, t->zn_lo, Z,
+                G + t->off[P_WK], Z));
+  TR_BLAS(gemm3(t->blas, false, false, R * F, M, 2 * H, t->dkv, t->dkv_lo, 2 * H, t->wkv_hi, t->wkv_lo, Z, t->dzn, M));
   // T2: node gradients into the winners' h' rows, deterministic order
   size_t sb = t->sort_bytes;
   cudaError_t e = cub::DeviceRadixSort::SortPairs(t->sort_tmp, sb, t->key, t->skey, t->val, t->sval, (int)slots, 0, 15, s);
