@@ -504,6 +504,39 @@ cublasStatus_t gemm3(cublasHandle_t h, bool ta, bool tb, int64_t m, int64_t n, i
   return st;
 }
 
+// long-K weight gradient C[m, n] = A^T B (A [K, m], B [K, n] row-major) in 3xTF32: the
+// tensor core's fp32 accumulation truncates, so K is cut into chunks of kChunkK rows
+// (64 MMA k-steps each), one strided-batched GEMM per term writes the chunk partials,
+// and the partials are added on the CUDA cores in chunk order (deterministic)
+constexpr int64_t kChunkK = 512;
+cublasStatus_t gemm3_tn_chunked(cublasHandle_t h, int64_t m, int64_t n, int64_t K, const float* Ahi,
+                                const float* Alo, int64_t lda, const float* Bhi, const float* Blo, int64_t ldb,
+                                float* part, int64_t nparts) {
+  const float one = 1.f, zero = 0.f;
+  const float* As[3] = {Alo, Ahi, Ahi};
+  const float* Bs[3] = {Bhi, Blo, Bhi};
+  for (int t = 0; t < 3; ++t) {
+    cublasStatus_t st = cublasGemmStridedBatchedEx(
+        h, CUBLAS_OP_N, CUBLAS_OP_T, (int)n, (int)m, (int)kChunkK, &one, Bs[t], CUDA_R_32F, (int)ldb, kChunkK * ldb,
+        As[t], CUDA_R_32F, (int)lda, kChunkK * lda, t ? &one : &zero, part, CUDA_R_32F, (int)n, m * n, (int)nparts,
+        CUBLAS_COMPUTE_32F_FAST_TF32, CUBLAS_GEMM_DEFAULT);
+    if (st != CUBLAS_STATUS_SUCCESS) return st;
+  }
+  (void)K;
+  return CUBLAS_STATUS_SUCCESS;
+}
+
+// out[i] = Σ_p part[p][i] in p order (+ tail[i] when given: the last, partial chunk)
+__global__ void k_tr_sum_parts(int64_t n, int64_t nparts, const float* __restrict__ part,
+                               const float* __restrict__ tail, float* out) {
+  for (int64_t i = gthread(); i < n; i += nthreads()) {
+    float acc = 0.f;
+    for (int64_t p = 0; p < nparts; ++p) acc += part[p * n + i];
+    if (tail) acc += tail[i];
+    out[i] = acc;
+  }
+}
+
 // row-major C[m, n] = alpha op(A)[m, k] op(B)[k, n] + beta C (column-major cuBLAS on the transposes)
 cublasStatus_t gemm_rm(cublasHandle_t h, bool ta, bool tb, int64_t m, int64_t n, int64_t k, const float* A,
                        int64_t lda, const float* B, int64_t ldb, float beta, float* C, int64_t ldc) {
@@ -540,6 +573,7 @@ struct mspipe_train {
   float *sroot, *zn, *q, *kv, *alpha, *zo, *emb, *za, *pre, *y, *logit, *dlogit, *dpre, *dza, *demb, *dzo, *dq, *dkv,
       *dzn, *dhn, *D, *xp, *ones, *cs;
   float *zn_lo, *dkv_lo, *wkv_hi, *wkv_lo;  // 3xTF32 parts (zn / dkv hold the hi parts)
+  float* wpart;                             // chunk partials of dW_k | dW_v [RF / kChunkK + 1, 2H, Z]
   double* term;
   int32_t *key, *val, *skey, *sval;
   int64_t *lo_hi, *poff;  // per winner: its sorted segment, exclusive scan of its piece counts
@@ -555,7 +589,7 @@ static void train_free(mspipe_train* t) {
   void* bufs[] = {t->wmap, t->sroot, t->zn, t->q, t->kv, t->alpha, t->zo, t->emb, t->za, t->pre, t->y, t->logit,
                   t->dlogit, t->dpre, t->dza, t->demb, t->dzo, t->dq, t->dkv, t->dzn, t->dhn, t->D, t->xp, t->ones,
                   t->cs, t->term, t->key, t->val, t->skey, t->sval, t->sort_tmp, t->blas_ws, t->lo_hi, t->poff, t->part,
-                  t->zn_lo, t->dkv_lo, t->wkv_hi, t->wkv_lo};
+                  t->zn_lo, t->dkv_lo, t->wkv_hi, t->wkv_lo, t->wpart};
   for (void* b : bufs)
     if (b) cudaFree(b);
   if (t->blas) cublasDestroy(t->blas);
@@ -625,6 +659,7 @@ mspipe_status mspipe_train_create(mspipe_train** out, const mspipe_gru* gru, int
   af(&t->dkv_lo, R * F * 2 * H);
   af(&t->wkv_hi, 2 * H * Z);
   af(&t->wkv_lo, 2 * H * Z);
+  af(&t->wpart, (R * F / kChunkK + 1) * 2 * H * Z);
   af(&t->dhn, 2 * B * M);
   af(&t->D, 2 * B * 4 * M);
   af(&t->xp, 2 * B * g.K);
@@ -758,8 +793,19 @@ mspipe_status mspipe_train_step(mspipe_train* t, const mspipe_gru* gru, int64_t 
                                                                    t->dq, t->dkv, t->dkv_lo);
   TR_BLAS(gemm_rm(t->blas, true, false, H, M, R, t->dq, H, t->sroot, M, 0.f, G + t->off[P_WQ], M));
   TR_BLAS(gemm_rm(t->blas, false, false, R, M, H, t->dq, H, wq, M, 1.f, t->dzo + H, H + M));  // ds~(root) += W_q^T dq
-  TR_BLAS(gemm3(t->blas, true, false, 2 * H, Z, R * F, t->dkv, t->dkv_lo, 2 * H, t->zn, t->zn_lo, Z,
-                G + t->off[P_WK], Z));
+  {  // dW_k | dW_v = dKV^T Z over the 3B·𝒩 slots: chunked 3xTF32, partials added in order
+    const int64_t RF = R * F, full = RF / kChunkK, rem = RF - full * kChunkK;
+    if (full > 0)
+      TR_BLAS(gemm3_tn_chunked(t->blas, 2 * H, Z, RF, t->dkv, t->dkv_lo, 2 * H, t->zn, t->zn_lo, Z, t->wpart, full));
+    float* tail = nullptr;
+    if (rem > 0) {
+      tail = t->wpart + full * 2 * H * Z;
+      TR_BLAS(gemm3(t->blas, true, false, 2 * H, Z, rem, t->dkv + full * kChunkK * 2 * H,
+                    t->dkv_lo + full * kChunkK * 2 * H, 2 * H, t->zn + full * kChunkK * Z, t->zn_lo + full * kChunkK * Z,
+                    Z, tail, Z));
+    }
+    k_tr_sum_parts<<<grid_for(2 * H * Z, 256), 256, 0, s>>>(2 * H * Z, full, t->wpart, tail, G + t->off[P_WK]);
+  }
   TR_BLAS(gemm3(t->blas, false, false, R * F, M, 2 * H, t->dkv, t->dkv_lo, 2 * H, t->wkv_hi, t->wkv_lo, Z, t->dzn, M));
   // T2: node gradients into the winners' h' rows, deterministic order
   size_t sb = t->sort_bytes;
