@@ -491,7 +491,11 @@ __device__ __forceinline__ void build_bf16(const TcArgs& a) {
 }
 
 // A5: one warp per (row, kBuildChunks chunks).  lane = column inside a chunk.
+// kBuildChunks = 4 (default) or 20 (MSPIPE_BUILD_ROW=1: one warp per whole row
+// for Kpad <= 640, the row's metadata resolved once, 20 loads in flight per lane)
 constexpr int kBuildChunks = 4;
+constexpr int kBuildRowChunks = 20;
+template <int kBuildChunks>
 __global__ void __launch_bounds__(256) k_build_x(TcArgs a) {
   if (a.d.bf16) {
     build_bf16(a);
@@ -1210,7 +1214,9 @@ cudaError_t launch_gru_tc(const GruDesc& d, const float* wtc, float* xbuf, const
     int64_t blocks = (warps * 32 + 255) / 256;
     const int64_t cap = (int64_t)num_sms() * env_int("MSPIPE_BUILD_BPS", 8);
     if (blocks > cap) blocks = cap;
-    cudaError_t e = launch_k(k_build_x, dim3((unsigned)blocks), dim3(256), 0, s, 1, a);
+    const bool row = !d.bf16 && env_int("MSPIPE_BUILD_ROW", 0) && d.Kpad / tc::kKC <= kBuildRowChunks;
+    cudaError_t e = row ? launch_k(k_build_x<kBuildRowChunks>, dim3((unsigned)blocks), dim3(256), 0, s, 1, a)
+                        : launch_k(k_build_x<kBuildChunks>, dim3((unsigned)blocks), dim3(256), 0, s, 1, a);
     if (e != cudaSuccess) return e;
   }
   if (!(parts & kGruGemm)) return cudaSuccess;
