@@ -77,13 +77,14 @@ struct PrepArgs {
   int32_t Qcu;     // float4 per mail row of the state tables (catch-up)
   int32_t dedup;   // 1: block 0 deduplicates (A2); 0: no dedup block
   int64_t* hint;   // optional [num_nodes]: per-node search start (warp_recent_sample)
+  int32_t stream_nbr;  // 1: neighbour rows stored evict-first (read only by a later training stage)
 };
 
 // copy `nrows` table rows (ids held by lanes 0..nrows-1, -1 = zero row) of Q
 // float4 each into dst rows base..base+nrows-1; kU loads in flight per lane.
 __device__ __forceinline__ void warp_gather_rows(const float4* __restrict__ tab, int32_t Q, int32_t my_id,
                                                  int nrows, float4* __restrict__ dst, int64_t dst_row0,
-                                                 int lane) {
+                                                 int lane, int stream_tail = 0) {
   // kU float4 loads in flight per lane before their stores: the whole subgraph
   // (11 rows x 25 float4 for M = 100) in one dependent round instead of three
 #ifndef MSPIPE_PREP_KU
@@ -113,7 +114,12 @@ __device__ __forceinline__ void warp_gather_rows(const float4* __restrict__ tab,
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
       const int idx = base + u * 32 + lane;
-      if (idx < total) dst[dst_row0 * Q + idx] = v[u];
+      if (idx < total) {
+        // rows >= 1 (the neighbours) with stream_tail: st.global.cs (evict-first), so the
+        // 3B·𝒩 rows nobody reads in this step do not push the root rows and tables out of L2
+        if (stream_tail && idx >= Q) __stcs(dst + dst_row0 * Q + idx, v[u]);
+        else dst[dst_row0 * Q + idx] = v[u];
+      }
     }
   }
 }
@@ -169,7 +175,7 @@ __global__ void __launch_bounds__(kPrepThreads, MSPIPE_PREP_MINB) k_prep(PrepArg
       a.out_mem_ts[r * F1 + lane] = gid >= 0 ? __ldg(a.mem_ts + gid) : 0.0;
       if (a.out_mail_ts) a.out_mail_ts[r * F1 + lane] = gid >= 0 ? __ldg(a.mail_ts + gid) : 0.0;
     }
-    warp_gather_rows(a.mem, a.Qm, gid, F1, a.out_mem, r * F1, lane);
+    warp_gather_rows(a.mem, a.Qm, gid, F1, a.out_mem, r * F1, lane, a.stream_nbr);
     if (a.Qa > 0) warp_gather_rows(a.mail, a.Qa, gid, F1, a.out_mail, r * F1, lane);
   }
   if (lane == 0) PPHASE(1);
@@ -199,6 +205,7 @@ cudaError_t launch_prep(const Tcsr& g, const int32_t* src, const int32_t* dst, c
              (int32_t)(mail_stride / 4)};
   if (cu) a.cu = *cu;
   a.hint = hint;
+  a.stream_nbr = env_int("MSPIPE_PREP_STCS", 0);
   a.dedup = out_num != nullptr;
   int64_t blocks = (3 * num_events + kPrepWarps - 1) / kPrepWarps;
   // one wave of the two resident blocks per SM; the root warps grid-stride
