@@ -56,7 +56,15 @@ class TrainStage:
         self.logits = torch.zeros((2 * batch,), dtype=torch.float32, device=device)
 
     def close(self):
-        _C.gru_save_gates(self.gru, None)
+        """Detach the gate sink from the updater (its GEMM stops writing self.gates)."""
+        if getattr(self, "gru", None) is not None and getattr(self.gru, "h", None):
+            _C.gru_save_gates(self.gru, None)
+
+    def __del__(self):  # self.gru outlives this object (it holds the reference)
+        try:
+            self.close()
+        except Exception:
+            pass
 
     def shape(self, name):
         M, He, Dt, H = self.dims
