@@ -78,7 +78,17 @@ struct Tcsr {
   const int32_t* nbr;
   const int32_t* eid;
   const double* ts;
+  int32_t stream;  // 1: the sampler's probes of nbr / eid / ts load evict-first (MSPIPE_TCSR_LDCS, A/B)
 };
+
+// T-CSR entry loads of the sampler: read-only path, or cache-streaming (evict-first)
+__device__ __forceinline__ double tcsr_ts(const Tcsr& g, int64_t i) { return g.stream ? __ldcs(g.ts + i) : __ldg(g.ts + i); }
+__device__ __forceinline__ int32_t tcsr_nbr(const Tcsr& g, int64_t i) {
+  return g.stream ? __ldcs(g.nbr + i) : __ldg(g.nbr + i);
+}
+__device__ __forceinline__ int32_t tcsr_eid(const Tcsr& g, int64_t i) {
+  return g.stream ? __ldcs(g.eid + i) : __ldg(g.eid + i);
+}
 
 // A1 core, executed by a whole warp for one root v at query time tq: returns
 // `end`, the first row position with ts >= tq (the entries [beg, end) are the
@@ -94,7 +104,7 @@ __device__ __forceinline__ int64_t lower_bound_ts(const Tcsr& g, int32_t v, doub
   int64_t lo = beg, hi = __ldg(g.indptr + v + 1);
   while (lo < hi) {
     const int64_t mid = (lo + hi) >> 1;
-    if (__ldg(g.ts + mid) < t) lo = mid + 1;
+    if (tcsr_ts(g, mid) < t) lo = mid + 1;
     else hi = mid;
   }
   *beg_out = beg;
@@ -126,7 +136,7 @@ __device__ __forceinline__ int64_t warp_recent_end(const Tcsr& g, int32_t v, dou
   while (hi - lo > 32) {
     const int64_t span = hi - lo;
     const int64_t p = lo + probe_offset33(lane, span);  // strictly inside [lo, hi)
-    const bool below = __ldg(g.ts + p) < tq;
+    const bool below = tcsr_ts(g, p) < tq;
     const int c = __popc(__ballot_sync(0xffffffffu, below));
     const int64_t plast = __shfl_sync(0xffffffffu, p, c > 0 ? c - 1 : 0);
     const int64_t pfirst = __shfl_sync(0xffffffffu, p, c < 32 ? c : 31);
@@ -134,7 +144,7 @@ __device__ __forceinline__ int64_t warp_recent_end(const Tcsr& g, int32_t v, dou
     if (c < 32) hi = pfirst;
   }
   const int64_t q = lo + lane;
-  const bool below = q < hi && __ldg(g.ts + q) < tq;
+  const bool below = q < hi && tcsr_ts(g, q) < tq;
   *beg_out = beg;
   return lo + __popc(__ballot_sync(0xffffffffu, below));
 }
@@ -161,7 +171,7 @@ __device__ __forceinline__ int64_t warp_recent_sample(const Tcsr& g, int32_t v, 
   while (hi - lo > 32) {
     const int64_t span = hi - lo;
     const int64_t p = lo + probe_offset33(lane, span);
-    const bool below = __ldg(g.ts + p) < tq;
+    const bool below = tcsr_ts(g, p) < tq;
     const int c = __popc(__ballot_sync(0xffffffffu, below));
     const int64_t plast = __shfl_sync(0xffffffffu, p, c > 0 ? c - 1 : 0);
     const int64_t pfirst = __shfl_sync(0xffffffffu, p, c < 32 ? c : 31);
@@ -170,9 +180,9 @@ __device__ __forceinline__ int64_t warp_recent_sample(const Tcsr& g, int32_t v, 
   }
   const int64_t q = lo + lane;
   const bool in = q < hi;
-  const double tq_q = in ? __ldg(g.ts + q) : 0.0;
-  const int32_t nb_q = in ? __ldg(g.nbr + q) : -1;
-  const int32_t ei_q = in ? __ldg(g.eid + q) : -1;
+  const double tq_q = in ? tcsr_ts(g, q) : 0.0;
+  const int32_t nb_q = in ? tcsr_nbr(g, q) : -1;
+  const int32_t ei_q = in ? tcsr_eid(g, q) : -1;
   const int64_t end = lo + __popc(__ballot_sync(0xffffffffu, in && tq_q < tq));
   const int64_t e = end - 1 - lane;  // this lane's output slot s = lane
   const int src_lane = (int)(e - lo);
@@ -185,9 +195,9 @@ __device__ __forceinline__ int64_t warp_recent_sample(const Tcsr& g, int32_t v, 
       *eid_out = ei_s;
       *ts_out = ts_s;
     } else {
-      *nbr_out = __ldg(g.nbr + e);
-      *eid_out = __ldg(g.eid + e);
-      *ts_out = __ldg(g.ts + e);
+      *nbr_out = tcsr_nbr(g, e);
+      *eid_out = tcsr_eid(g, e);
+      *ts_out = tcsr_ts(g, e);
     }
   }
   *beg_out = beg;
@@ -225,12 +235,12 @@ __device__ __forceinline__ int64_t warp_recent_sample_hinted(const Tcsr& g, int3
   // round 1: window entry + galloping probe, all independent loads
   int64_t q = w0 + lane;
   bool qin = q < rend;
-  double ts_q = qin ? __ldg(g.ts + q) : 0.0;
-  int32_t nb_q = qin ? __ldg(g.nbr + q) : -1;
-  int32_t ei_q = qin ? __ldg(g.eid + q) : -1;
+  double ts_q = qin ? tcsr_ts(g, q) : 0.0;
+  int32_t nb_q = qin ? tcsr_nbr(g, q) : -1;
+  int32_t ei_q = qin ? tcsr_eid(g, q) : -1;
   const int64_t p = lane < 16 ? h + ((int64_t(1) << lane) - 1) : h - (int64_t(1) << (lane - 16));
   const bool pin = p >= beg && p < rend;
-  const bool pbelow = pin && __ldg(g.ts + p) < tq;
+  const bool pbelow = pin && tcsr_ts(g, p) < tq;
   int c = __popc(__ballot_sync(0xffffffffu, qin && ts_q < tq));  // below-t_q entries: a prefix of the window
   const int nin = (int)min64(32, rend - w0);
   int64_t end;
@@ -253,7 +263,7 @@ __device__ __forceinline__ int64_t warp_recent_sample_hinted(const Tcsr& g, int3
     while (hi - lo > 32 - F) {
       const int64_t span = hi - lo;
       const int64_t pp = lo + probe_offset33(lane, span);
-      const bool below = __ldg(g.ts + pp) < tq;
+      const bool below = tcsr_ts(g, pp) < tq;
       const int cc = __popc(__ballot_sync(0xffffffffu, below));
       const int64_t plast = __shfl_sync(0xffffffffu, pp, cc > 0 ? cc - 1 : 0);
       const int64_t pfirst = __shfl_sync(0xffffffffu, pp, cc < 32 ? cc : 31);
@@ -264,9 +274,9 @@ __device__ __forceinline__ int64_t warp_recent_sample_hinted(const Tcsr& g, int3
     w0 = lo - F < beg ? beg : lo - F;
     q = w0 + lane;
     qin = q < rend;
-    ts_q = qin ? __ldg(g.ts + q) : 0.0;
-    nb_q = qin ? __ldg(g.nbr + q) : -1;
-    ei_q = qin ? __ldg(g.eid + q) : -1;
+    ts_q = qin ? tcsr_ts(g, q) : 0.0;
+    nb_q = qin ? tcsr_nbr(g, q) : -1;
+    ei_q = qin ? tcsr_eid(g, q) : -1;
     end = lo + __popc(__ballot_sync(0xffffffffu, q >= lo && q < hi && ts_q < tq));
   }
   const int64_t e = end - 1 - lane;  // this lane's output slot s = lane
@@ -280,9 +290,9 @@ __device__ __forceinline__ int64_t warp_recent_sample_hinted(const Tcsr& g, int3
       *eid_out = ei_s;
       *ts_out = ts_s;
     } else {  // a hit below a hint that ran ahead (e.g. after an epoch reset)
-      *nbr_out = __ldg(g.nbr + e);
-      *eid_out = __ldg(g.eid + e);
-      *ts_out = __ldg(g.ts + e);
+      *nbr_out = tcsr_nbr(g, e);
+      *eid_out = tcsr_eid(g, e);
+      *ts_out = tcsr_ts(g, e);
     }
   }
   if (lane == 0) hint[v] = end;
@@ -291,7 +301,7 @@ __device__ __forceinline__ int64_t warp_recent_sample_hinted(const Tcsr& g, int3
 }
 
 inline Tcsr to_tcsr(const mspipe_tcsr* g) {
-  return Tcsr{g->num_nodes, g->nnz, g->indptr, g->nbr, g->eid, g->ts};
+  return Tcsr{g->num_nodes, g->nnz, g->indptr, g->nbr, g->eid, g->ts, env_int("MSPIPE_TCSR_LDCS", 0)};
 }
 
 // ---- kernels' host-side launchers (one .cu each) -------------------------
