@@ -300,8 +300,14 @@ __device__ __forceinline__ int64_t warp_recent_sample_hinted(const Tcsr& g, int3
   return end;
 }
 
+// The sampler's probes of a T-CSR much larger than L2 (GDELT: 382M entries, 6 GB)
+// load evict-first: the probed sectors are rarely reused and pushed the state
+// tables and GEMM operands out of L2 (r02zl: 97.2 vs 96.0 M events/s); a small
+// T-CSR keeps the read-only path (wiki: neutral).  MSPIPE_TCSR_LDCS=0/1 forces it.
 inline Tcsr to_tcsr(const mspipe_tcsr* g) {
-  return Tcsr{g->num_nodes, g->nnz, g->indptr, g->nbr, g->eid, g->ts, env_int("MSPIPE_TCSR_LDCS", 0)};
+  const int forced = env_int("MSPIPE_TCSR_LDCS", -1);
+  const int stream = forced >= 0 ? forced : (g->nnz * 16 > (int64_t)(256ll << 20) ? 1 : 0);
+  return Tcsr{g->num_nodes, g->nnz, g->indptr, g->nbr, g->eid, g->ts, stream};
 }
 
 // ---- kernels' host-side launchers (one .cu each) -------------------------
