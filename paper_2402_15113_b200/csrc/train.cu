@@ -295,10 +295,22 @@ __global__ void __launch_bounds__(kTrThreads) k_tr_attn_bwd(Dims d, int64_t R, c
 constexpr int kSegLanes = kTrThreads / 32;
 constexpr int64_t kPiece = 512;
 
-// one block: each winner's segment [lo, hi) and the exclusive scan of its piece counts
-__global__ void __launch_bounds__(1024) k_tr_seg_plan(int64_t nslots, int64_t B2, const int32_t* __restrict__ num,
-                                                       const int32_t* __restrict__ skey, int64_t* lo_hi,
-                                                       int64_t* poff) {
+// segment bounds of every winner from the sorted keys in one parallel pass:
+// position i starts a run when key[i] != key[i - 1] (lo of key[i], hi of key[i - 1]);
+// winners without slots keep lo = hi = 0 (lo_hi zeroed first)
+__global__ void k_tr_seg_bounds(int64_t nslots, const int32_t* __restrict__ skey, int64_t* lo_hi) {
+  for (int64_t i = gthread(); i <= nslots; i += nthreads()) {
+    const int32_t k = i < nslots ? __ldg(skey + i) : kNoWinner;
+    const int32_t kp = i > 0 ? __ldg(skey + i - 1) : -1;
+    if (k == kp) continue;
+    if (kp >= 0 && kp != kNoWinner) lo_hi[2 * kp + 1] = i;
+    if (k != kNoWinner) lo_hi[2 * k] = i;
+  }
+}
+
+// one block: the exclusive scan of the winners' piece counts
+__global__ void __launch_bounds__(1024) k_tr_seg_plan(int64_t B2, const int32_t* __restrict__ num,
+                                                       const int64_t* __restrict__ lo_hi, int64_t* poff) {
   __shared__ int64_t carry;
   __shared__ int64_t wsum[32];
   const int32_t U = __ldg(num);
@@ -306,23 +318,8 @@ __global__ void __launch_bounds__(1024) k_tr_seg_plan(int64_t nslots, int64_t B2
   __syncthreads();
   for (int64_t base = 0; base < B2; base += blockDim.x) {
     const int64_t u = base + threadIdx.x;
-    int64_t lo = 0, hi = 0;
-    if (u < U) {
-      for (int e = 0; e < 2; ++e) {  // lower_bound(u), lower_bound(u + 1)
-        int64_t a = 0, b = nslots;
-        while (a < b) {
-          const int64_t m = (a + b) >> 1;
-          if (__ldg(skey + m) < u + e) a = m + 1; else b = m;
-        }
-        (e ? hi : lo) = a;
-      }
-    }
-    if (u < B2) {
-      lo_hi[2 * u] = lo;
-      lo_hi[2 * u + 1] = hi;
-    }
-    // block-wide exclusive scan of the piece counts
-    int64_t n = (u < B2) ? (hi - lo + kPiece - 1) / kPiece : 0;
+    int64_t n = 0;
+    if (u < U) n = (lo_hi[2 * u + 1] - lo_hi[2 * u] + kPiece - 1) / kPiece;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     int64_t x = n;
     for (int o = 1; o < 32; o <<= 1) {
@@ -811,7 +808,10 @@ mspipe_status mspipe_train_step(mspipe_train* t, const mspipe_gru* gru, int64_t 
   size_t sb = t->sort_bytes;
   cudaError_t e = cub::DeviceRadixSort::SortPairs(t->sort_tmp, sb, t->key, t->skey, t->val, t->sval, (int)slots, 0, 15, s);
   if (e != cudaSuccess) return cuda_status(e, "train_step: sort");
-  k_tr_seg_plan<<<1, 1024, 0, s>>>(slots, B2, num_unique, t->skey, t->lo_hi, t->poff);
+  e = cudaMemsetAsync(t->lo_hi, 0, sizeof(int64_t) * (size_t)(2 * B2), s);
+  if (e != cudaSuccess) return cuda_status(e, "train_step: segment bounds");
+  k_tr_seg_bounds<<<grid_for(slots + 1, 256), 256, 0, s>>>(slots, t->skey, t->lo_hi);
+  k_tr_seg_plan<<<1, 1024, 0, s>>>(B2, num_unique, t->lo_hi, t->poff);
   const int64_t max_pieces = slots / kPiece + B2 + 1;
   k_tr_seg_piece<<<(unsigned)std::min<int64_t>(max_pieces, (int64_t)num_sms() * 8), kTrThreads, 0, s>>>(
       d, B2, t->lo_hi, t->poff, t->sval, t->dzo, t->dzn, t->part);
