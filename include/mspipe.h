@@ -703,8 +703,8 @@ MSPIPE_API mspipe_status mspipe_apan_deliver(mspipe_apan* a, mspipe_memory* st, 
  *   (winners), new_mem [<=2B, M] (h' in winner order), workspace (the batch's
  *   GEMM operand images), gates (saved by its GEMM).  Writes *out_loss
  *   (device f64), out_logits (nullable, [2B]: positives then negatives) and
- *   the full gradient into grads (overwritten).  Deterministic.  Errors:
- *   MSPIPE_EINVAL.
+ *   the full gradient into grads (overwritten).  Deterministic.  An empty
+ *   batch (num_events == 0) enqueues nothing.  Errors: MSPIPE_EINVAL.
  * mspipe_train_sgd: params -= lr * grads, then repacks the GRU images. */
 typedef struct mspipe_train mspipe_train;
 MSPIPE_API int64_t mspipe_train_layout(int32_t mem_dim, int32_t edge_dim, int32_t time_dim, int32_t emb_dim,
