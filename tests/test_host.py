@@ -121,3 +121,19 @@ def test_gamma_helper_matches_oracle(name):
     cfg = CONFIGS[name]
     src, dst, ts, _ = make_events(cfg, 0, 100_000)
     assert gamma_quantile(cfg.num_nodes, src, dst, ts, 0.99) == oracle.gamma(cfg.num_nodes, src, dst, ts, 0.99)
+
+
+def test_header_is_plain_c(tmp_path):
+    """include/mspipe.h is a C ABI: it compiles as strict C11 (gcc -pedantic) and as C++17."""
+    import shutil
+    import subprocess
+    if shutil.which("gcc") is None:
+        import pytest
+        pytest.skip("no gcc")
+    inc = os.path.join(ROOT, "include")
+    src = tmp_path / "h.c"
+    src.write_text('#include "mspipe.h"\nint main(void) { return mspipe_abi_version() == MSPIPE_ABI_VERSION ? 0 : 1; }\n')
+    subprocess.run(["gcc", "-std=c11", "-Wall", "-Wextra", "-pedantic", "-Werror", "-I", inc, "-c", str(src), "-o",
+                    str(tmp_path / "h.o")], check=True)
+    subprocess.run(["g++", "-std=c++17", "-Wall", "-Werror", "-I", inc, "-x", "c++", "-c", str(src), "-o",
+                    str(tmp_path / "h2.o")], check=True)
