@@ -422,35 +422,22 @@ __device__ __forceinline__ float x_elem(const float* xbuf, int32_t nchunks, int6
 
 // GRU backward of the gates (chain rule of torch.nn.GRUCell, G5) per (u, j):
 //   D[u] = [d pre_r | d pre_z | d pre_n(x) | d (W_hn h + b_hn)], and X plain [2B, K]
-// the A image's own tf32 parts of X[u, k] (hi, lo): the 3xTF32 weight-gradient GEMMs use them as they are
-__device__ __forceinline__ float2 x_parts(const float* xbuf, int32_t nchunks, int64_t u, int32_t k) {
-  const char* blk = reinterpret_cast<const char*>(xbuf) + ((u / tc::kM) * nchunks + k / tc::kKC) * tc::kABlock;
-  const uint32_t off = tc::sw128_off((uint32_t)(u % tc::kM), (uint32_t)(k % tc::kKC));
-  return make_float2(__ldg(reinterpret_cast<const float*>(blk + off)),
-                     __ldg(reinterpret_cast<const float*>(blk + tc::kATile + off)));
-}
-
 __global__ void k_tr_gru_bwd(Dims d, int64_t B2, int32_t nchunks, const int32_t* __restrict__ num,
                              const float* __restrict__ xbuf, const float* __restrict__ gates,
-                             const float* __restrict__ dhn, float* D, float* D_hi, float* D_lo, float* xp,
-                             float* xp_lo) {
+                             const float* __restrict__ dhn, float* D, float* xp) {
   const int32_t U = __ldg(num);
   const int32_t M = d.M, K = d.K;
   for (int64_t t = gthread(); t < B2 * K; t += nthreads()) {
     const int64_t u = t / K;
     const int32_t k = (int32_t)(t % K);
-    const float2 x = u < U ? x_parts(xbuf, nchunks, u, k) : make_float2(0.f, 0.f);
-    xp[t] = x.x;  // hi
-    xp_lo[t] = x.y;
+    xp[t] = u < U ? x_elem(xbuf, nchunks, u, k) : 0.f;
   }
   for (int64_t t = gthread(); t < B2 * M; t += nthreads()) {
     const int64_t u = t / M;
     const int32_t j = (int32_t)(t % M);
     float* o = D + u * 4 * M;
-    float* oh = D_hi + u * 4 * M;
-    float* ol = D_lo + u * 4 * M;
     if (u >= U) {
-      for (int g = 0; g < 4; ++g) o[g * M + j] = oh[g * M + j] = ol[g * M + j] = 0.f;
+      o[j] = o[M + j] = o[2 * M + j] = o[3 * M + j] = 0.f;
       continue;
     }
     const float* g = gates + u * 4 * M;
@@ -463,14 +450,10 @@ __global__ void k_tr_gru_bwd(Dims d, int64_t B2, int32_t nchunks, const int32_t*
     const float dn = dh * (1.f - z);
     const float dz = dh * (h - n);
     const float dan = dn * (1.f - n * n);
-    const float v[4] = {dan * ghn * r * (1.f - r), dz * z * (1.f - z), dan, dan * r};
-#pragma unroll
-    for (int g = 0; g < 4; ++g) {
-      const float hi = tc::tf32_rna(v[g]);
-      o[g * M + j] = v[g];
-      oh[g * M + j] = hi;
-      ol[g * M + j] = tc::tf32_rna(v[g] - hi);
-    }
+    o[j] = dan * ghn * r * (1.f - r);
+    o[M + j] = dz * z * (1.f - z);
+    o[2 * M + j] = dan;
+    o[3 * M + j] = dan * r;
   }
 }
 
@@ -545,7 +528,6 @@ __global__ void k_tr_sum_parts(int64_t n, int64_t nparts, const float* __restric
                                const float* __restrict__ tail, float* out) {
   for (int64_t i = gthread(); i < n; i += nthreads()) {
     float acc = 0.f;
-#pragma unroll 8
     for (int64_t p = 0; p < nparts; ++p) acc += part[p * n + i];
     if (tail) acc += tail[i];
     out[i] = acc;
@@ -588,8 +570,7 @@ struct mspipe_train {
   float *sroot, *zn, *q, *kv, *alpha, *zo, *emb, *za, *pre, *y, *logit, *dlogit, *dpre, *dza, *demb, *dzo, *dq, *dkv,
       *dzn, *dhn, *D, *xp, *ones, *cs;
   float *zn_lo, *dkv_lo, *wkv_hi, *wkv_lo;  // 3xTF32 parts (zn / dkv hold the hi parts)
-  float* wpart;                             // chunk partials of dW_k | dW_v [RF / kChunkK + 1, 2H, Z] (and the GRU's)
-  float *D_hi, *D_lo, *xp_lo;               // tf32 parts for the GRU weight gradients
+  float* wpart;                             // chunk partials of dW_k | dW_v [RF / kChunkK + 1, 2H, Z]
   double* term;
   int32_t *key, *val, *skey, *sval;
   int64_t *lo_hi, *poff;  // per winner: its sorted segment, exclusive scan of its piece counts
@@ -605,7 +586,7 @@ static void train_free(mspipe_train* t) {
   void* bufs[] = {t->wmap, t->sroot, t->zn, t->q, t->kv, t->alpha, t->zo, t->emb, t->za, t->pre, t->y, t->logit,
                   t->dlogit, t->dpre, t->dza, t->demb, t->dzo, t->dq, t->dkv, t->dzn, t->dhn, t->D, t->xp, t->ones,
                   t->cs, t->term, t->key, t->val, t->skey, t->sval, t->sort_tmp, t->blas_ws, t->lo_hi, t->poff, t->part,
-                  t->zn_lo, t->dkv_lo, t->wkv_hi, t->wkv_lo, t->wpart, t->D_hi, t->D_lo, t->xp_lo};
+                  t->zn_lo, t->dkv_lo, t->wkv_hi, t->wkv_lo, t->wpart};
   for (void* b : bufs)
     if (b) cudaFree(b);
   if (t->blas) cublasDestroy(t->blas);
@@ -675,10 +656,7 @@ mspipe_status mspipe_train_create(mspipe_train** out, const mspipe_gru* gru, int
   af(&t->dkv_lo, R * F * 2 * H);
   af(&t->wkv_hi, 2 * H * Z);
   af(&t->wkv_lo, 2 * H * Z);
-  af(&t->wpart, std::max<int64_t>((R * F / kChunkK + 1) * 2 * H * Z, (2 * B / kChunkK + 1) * 3 * M * g.Dx));
-  af(&t->D_hi, 2 * B * 4 * M);
-  af(&t->D_lo, 2 * B * 4 * M);
-  af(&t->xp_lo, 2 * B * g.K);
+  af(&t->wpart, (R * F / kChunkK + 1) * 2 * H * Z);
   af(&t->dhn, 2 * B * M);
   af(&t->D, 2 * B * 4 * M);
   af(&t->xp, 2 * B * g.K);
@@ -840,29 +818,12 @@ mspipe_status mspipe_train_step(mspipe_train* t, const mspipe_gru* gru, int64_t 
   k_tr_seg_final<<<grid_for(B2 * (M / 4), 256), 256, 0, s>>>((int32_t)M, B2, t->poff, t->part, t->dhn);
   const int32_t nchunks = gru->d.Kpad / tc::kKC;
   k_tr_gru_bwd<<<grid_for(B2 * d.K, 256), 256, 0, s>>>(d, B2, nchunks, num_unique, (const float*)workspace, gates,
-                                                      t->dhn, t->D, t->D_hi, t->D_lo, t->xp, t->xp_lo);
+                                                      t->dhn, t->D, t->xp);
   const int64_t K = d.K, Dx = d.Dx;
-  // GRU weight gradients over the 2B rows: chunked 3xTF32 (as dW_k | dW_v)
-  auto wgrad = [&](int64_t m, int64_t n, int64_t dcol, int64_t xcol, float* out) -> cublasStatus_t {
-    const int64_t full = B2 / kChunkK, rem = B2 - full * kChunkK;
-    cublasStatus_t st = CUBLAS_STATUS_SUCCESS;
-    if (full > 0)
-      st = gemm3_tn_chunked(t->blas, m, n, B2, t->D_hi + dcol, t->D_lo + dcol, 4 * M, t->xp + xcol, t->xp_lo + xcol,
-                            K, t->wpart, full);
-    float* tail = nullptr;
-    if (st == CUBLAS_STATUS_SUCCESS && rem > 0) {
-      tail = t->wpart + full * m * n;
-      st = gemm3(t->blas, true, false, m, n, rem, t->D_hi + full * kChunkK * 4 * M + dcol,
-                 t->D_lo + full * kChunkK * 4 * M + dcol, 4 * M, t->xp + full * kChunkK * K + xcol,
-                 t->xp_lo + full * kChunkK * K + xcol, K, tail, n);
-    }
-    if (st == CUBLAS_STATUS_SUCCESS)
-      k_tr_sum_parts<<<grid_for(m * n, 256), 256, 0, s>>>(m * n, full, t->wpart, tail, out);
-    return st;
-  };
-  TR_BLAS(wgrad(3 * M, Dx, 0, 0, G + t->off[P_WIH]));
-  TR_BLAS(wgrad(2 * M, M, 0, Dx, G + t->off[P_WHH]));
-  TR_BLAS(wgrad(M, M, 3 * M, Dx, G + t->off[P_WHH] + 2 * M * M));
+  TR_BLAS(gemm_rm(t->blas, true, false, 3 * M, Dx, B2, t->D, 4 * M, t->xp, K, 0.f, G + t->off[P_WIH], Dx));
+  TR_BLAS(gemm_rm(t->blas, true, false, 2 * M, M, B2, t->D, 4 * M, t->xp + Dx, K, 0.f, G + t->off[P_WHH], M));
+  TR_BLAS(gemm_rm(t->blas, true, false, M, M, B2, t->D + 3 * M, 4 * M, t->xp + Dx, K, 0.f,
+                  G + t->off[P_WHH] + 2 * M * M, M));
   TR_BLAS(colsum(t->blas, B2, 4 * M, t->D, 4 * M, t->ones, t->cs));
   k_tr_gru_bias<<<grid_for(3 * M, 256), 256, 0, s>>>((int32_t)M, t->cs, G + t->off[P_BIH], G + t->off[P_BHH]);
   k_tr_map<<<grid_for(B2, 256), 256, 0, s>>>(nodes, num_unique, t->wmap, 0);
