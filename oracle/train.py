@@ -183,15 +183,24 @@ def build_message(src, dst, ts, ef, mem, mem_ts, winner, gru):
     return x, _f64(mem[w])
 
 
-def train_step(num_nodes, src, dst, neg, ts, ef, mem, mem_ts, graph: Graph, gru: dict, prm: dict, fanout=10):
+def train_step(num_nodes, src, dst, neg, ts, ef, mem, mem_ts, graph: Graph, gru: dict, prm: dict, fanout=10,
+               mitigation=None):
     """Forward and backward of one iteration on the snapshot tables (mem,
     mem_ts) = S_{v(i)}.  Returns loss, logits, emb, every gradient (fp64),
-    and the winners' (nodes, h') that the stage commits."""
+    and the winners' (nodes, h') that the stage commits.  mitigation
+    (dict(lam, gamma, n_sim)): the GRU's hidden input is MSPipe-S's blended
+    row (A4, G13), taken from this oracle's own A4."""
     src, dst, neg = (np.asarray(a, np.int32) for a in (src, dst, neg))
     ts = np.asarray(ts, np.float64)
     B = len(src)
     nodes, winner = dedup(num_nodes, src, dst)                   # A2
     x, h = build_message(src, dst, ts, ef, mem, mem_ts, winner, gru)
+    if mitigation is not None:                                   # A4: h = ŝ of each winner
+        from . import memory_update
+        mu = memory_update(num_nodes, src, dst, ts, ef, gru, mem, mem_ts, mitigation=mitigation, graph=graph,
+                           fanout=fanout)
+        assert np.array_equal(mu["nodes"], nodes)
+        h = np.asarray(mu["h"], np.float64)
     hn, gc = gru_forward(x, h, gru)                              # A6: s~^(i) of the winners
     roots = np.concatenate([src, dst, neg])
     qts = np.concatenate([ts, ts, ts])

@@ -222,3 +222,41 @@ def test_train_single_event_batch(dev):
     assert abs(float(st.trainer.losses[0].item()) - ref["loss"]) <= TOL * ref["loss"]
     for k in _C.TRAIN_TENSORS:
         assert _worst(st.trainer.tensor(k, "grads").cpu().numpy(), ref["grads"][k]) <= TOL, k
+
+
+def test_train_step_with_mitigation(dev):
+    """MSPipe-S (A4) feeding the training stage: the GRU's hidden input is the
+    blended row, so its backward (dW_hh, via h read from the GEMM operand) must
+    follow the oracle run with the same mitigation (Reddit shape)."""
+    from paper_2402_15113_b200 import gamma_quantile
+    cfg = CONFIGS["reddit"]
+    E, i = 60_000, 80
+    src, dst, ts, neg = make_events(cfg, 0, E)
+    B, F, M = cfg.batch, cfg.fanout, cfg.mem_dim
+    j0, j1 = (i - 1) * B, i * B
+    ef = edge_features(0, j0, B, cfg.edge_dim)
+    gp = gru_params(M, cfg.mail_dim, cfg.time_dim)
+    tp = train_params(M, cfg.time_dim, 100)
+    mem, mem_ts = _random_state(cfg.num_nodes, M, src, dst, ts, j0, 7)
+    mit = dict(lam=cfg.lam, gamma=gamma_quantile(cfg.num_nodes, src, dst, ts, cfg.quantile_p) * 0.05, n_sim=cfg.n_sim)
+    g = build_tcsr(cfg.num_nodes, src, dst, ts, dev)
+    st = MemoryStage(StageConfig(cfg.num_nodes, M, cfg.edge_dim, cfg.time_dim, F, B, 0, fused=True, mitigation=mit,
+                                 train=dict(params=tp, lr=0.0, sgd=False)), gp, g, dev)
+    st.memory.mem.copy_(_t(mem, dev))
+    st.memory.mem_ts.copy_(_t(mem_ts, dev))
+    x = {k: _t(v[j0:j1], dev) for k, v in dict(src=src, dst=dst, ts=ts, neg=neg).items()}
+    x["ef"] = _t(ef, dev)
+    st.bind_resident(x["src"], x["dst"], x["ts"], x["neg"], x["ef"])
+    st.prep(1)
+    st.commit(1)
+    torch.cuda.synchronize()
+    _C.check()
+    graph = oracle.Graph(cfg.num_nodes, src, dst, ts)
+    ref = ot.train_step(cfg.num_nodes, src[j0:j1], dst[j0:j1], neg[j0:j1], ts[j0:j1], ef, mem, mem_ts, graph, gp, tp,
+                        fanout=F, mitigation=mit)
+    plain = ot.train_step(cfg.num_nodes, src[j0:j1], dst[j0:j1], neg[j0:j1], ts[j0:j1], ef, mem, mem_ts, graph, gp,
+                          tp, fanout=F)
+    assert np.abs(ref["grads"]["w_hh"] - plain["grads"]["w_hh"]).max() > 0  # the blend is on the path
+    assert abs(float(st.trainer.losses[0].item()) - ref["loss"]) <= TOL * ref["loss"]
+    for k in _C.TRAIN_TENSORS:
+        assert _worst(st.trainer.tensor(k, "grads").cpu().numpy(), ref["grads"][k]) <= TOL, k
