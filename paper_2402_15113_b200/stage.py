@@ -213,6 +213,8 @@ class MemoryStage(_TimedOps):
         if cfg.mailbox == "apan":  # row F3: APAN (multi-slot mailbox, attention message, propagation)
             if cfg.cell != "gru" or cfg.precision != _C.FP32_3XTF32 or cfg.apan is None or cfg.schedule != "exact":
                 raise ValueError("mailbox='apan' runs on the 3xTF32 GRUCell path, exact schedule, with cfg.apan weights")
+            if cfg.mitigation:
+                raise ValueError("mailbox='apan' with MSPipe-S is not built (the APAN build takes h = S.mem[w])")
             self.apan = _C.ApanHandle(cfg.num_nodes, cfg.mem_dim, cfg.edge_dim, cfg.apan.get("slots", 10), cfg.batch,
                                       cfg.apan["w_q"], cfg.apan["w_k"], self.device)
         self.gru = _C.GruHandle(cfg.mem_dim, cfg.edge_dim, cfg.time_dim, params, self.device, cfg.precision,
