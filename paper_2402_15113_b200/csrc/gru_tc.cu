@@ -9,16 +9,16 @@
 //   D += A_hi.B_hi + A_hi.B_lo + A_lo.B_hi      (dropped A_lo.B_lo ~ 2^-22).
 //
 // Two kernels:
-//  k_build_x — one warp per (winner row, 32-wide K chunk): gathers the message
+//  k_build_x — one warp per (winner row, 4 x 32-wide K chunks): gathers the message
 //    x = [s_w | s_o | e | cos(w dt + p) | h] (A5, fused time encoding) from
 //    the snapshot rows, writes the A operand as ready-to-copy SWIZZLE_128B
 //    K-major images (hi | lo) per (128-row tile, chunk), and the mail row and
 //    commit timestamp of the winner (G14).  Thousands of warps hide the
 //    gather latency that a per-CTA producer could not.
-//  k_gru_tc — CTA = 128 rows x 16 hidden units (N = 64 accumulator columns)
+//  k_gru_tc — CTA = 128 rows x 20 hidden units (N = 80 accumulator columns)
 //    x a K range.  One thread streams (A, B) chunk images with cp.async.bulk
-//    (TMA engine, mbarrier complete_tx) through a 4-stage ring, one thread
-//    issues 12 MMAs per chunk, all 4 warps read TMEM in the epilogue.  U ~ 10^3
+//    (TMA engine, mbarrier complete_tx) through a 3-stage ring, one thread
+//    issues 12 MMAs per chunk, all 8 warps read TMEM in the epilogue.  U ~ 10^3
 //    rows is only a handful of M tiles, so K is split S ways over a cluster
 //    (1,1,S); the S partial tiles are summed through distributed shared memory
 //    in fixed rank order (deterministic) and each rank applies the gates to
@@ -48,7 +48,7 @@ constexpr int kStages = 3;
 // 8 warps: warp 0 loads, warp 1 issues the MMAs, warps 2..7 prefetch the
 // epilogue's inputs; in the epilogue warps w and w + 4 read the two 32-column
 // halves of the same TMEM lane quarter (w % 4), so the gate math of a tile
-// (expf / tanhf / division chains of 128 rows x 16 units) spreads over 256
+// (expf / tanhf / division chains of 128 rows x 20 units) spreads over 256
 // threads: with 4 warps, one warp per scheduler left every dependent step of
 // those chains exposed (measured: 3.5 of ~15 us per GDELT tile)
 constexpr int kThreads = 256;
