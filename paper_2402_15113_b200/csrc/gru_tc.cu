@@ -1215,8 +1215,14 @@ cudaError_t launch_gru_tc(const GruDesc& d, const float* wtc, float* xbuf, const
     const int64_t cap = (int64_t)num_sms() * env_int("MSPIPE_BUILD_BPS", 8);
     if (blocks > cap) blocks = cap;
     const bool row = !d.bf16 && env_int("MSPIPE_BUILD_ROW", 0) && d.Kpad / tc::kKC <= kBuildRowChunks;
-    cudaError_t e = row ? launch_k(k_build_x<kBuildRowChunks>, dim3((unsigned)blocks), dim3(256), 0, s, 1, a)
-                        : launch_k(k_build_x<kBuildChunks>, dim3((unsigned)blocks), dim3(256), 0, s, 1, a);
+    const bool two = !d.bf16 && !row && env_int("MSPIPE_BUILD_CHUNKS", kBuildChunks) == 2;  // A/B: 2 chunks per item
+    if (two) {
+      const int64_t w2 = mtiles * ((nch + 1) / 2) * tc::kM;
+      blocks = std::min<int64_t>((w2 * 32 + 255) / 256, cap);
+    }
+    cudaError_t e = row   ? launch_k(k_build_x<kBuildRowChunks>, dim3((unsigned)blocks), dim3(256), 0, s, 1, a)
+                    : two ? launch_k(k_build_x<2>, dim3((unsigned)blocks), dim3(256), 0, s, 1, a)
+                          : launch_k(k_build_x<kBuildChunks>, dim3((unsigned)blocks), dim3(256), 0, s, 1, a);
     if (e != cudaSuccess) return e;
   }
   if (!(parts & kGruGemm)) return cudaSuccess;
