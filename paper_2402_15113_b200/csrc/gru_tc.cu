@@ -1215,7 +1215,10 @@ cudaError_t launch_gru_tc(const GruDesc& d, const float* wtc, float* xbuf, const
     const int64_t cap = (int64_t)num_sms() * env_int("MSPIPE_BUILD_BPS", 8);
     if (blocks > cap) blocks = cap;
     const bool row = !d.bf16 && env_int("MSPIPE_BUILD_ROW", 0) && d.Kpad / tc::kKC <= kBuildRowChunks;
-    const bool two = !d.bf16 && !row && env_int("MSPIPE_BUILD_CHUNKS", kBuildChunks) == 2;  // A/B: 2 chunks per item
+    // items of 2 K chunks for small batches (more warps hide the gather latency: wiki 37.1 vs
+    // 36.7 M events/s), 4 for large (GDELT 98.1 vs 96.4 M, r02zs); MSPIPE_BUILD_CHUNKS forces it
+    const int bc = env_int("MSPIPE_BUILD_CHUNKS", max_rows <= 2048 ? 2 : kBuildChunks);
+    const bool two = !d.bf16 && !row && bc == 2;
     if (two) {
       const int64_t w2 = mtiles * ((nch + 1) / 2) * tc::kM;
       blocks = std::min<int64_t>((w2 * 32 + 255) / 256, cap);
