@@ -268,6 +268,13 @@ def rows_to_host(num, host_num, a, host_a, b, host_b, max_rows, stream=None):
                                        stream_ptr(stream)), "mspipe_util_rows_to_host")
 
 
+_capture_seq = 0  # bumped at every capture start: events of another capture must not be waited on
+
+
+def capture_seq():
+    return _capture_seq
+
+
 class StepGraph:
     """One captured step (mspipe_util_graph_*).  Capture must not allocate: the
     stage's buffers are preallocated, and an allocation during capture raises."""
@@ -276,6 +283,8 @@ class StepGraph:
         self.exec = C.c_void_p()
 
     def capture(self, fn, stream):
+        global _capture_seq
+        _capture_seq += 1
         # a handle freed by the cyclic GC mid-capture would cudaFree inside it
         # and invalidate the capture: collect first, and keep the GC off meanwhile
         gc.collect()
@@ -290,6 +299,7 @@ class StepGraph:
                 finally:
                     _ck(lib().mspipe_util_graph_end(stream_ptr(stream), C.byref(self.exec)), "util_graph_end")
         finally:
+            _capture_seq += 1  # events recorded inside this capture stay inside it
             if was_enabled:
                 gc.enable()
         after = torch.cuda.memory_stats(stream.device).get("allocation.all.allocated", 0)

@@ -248,7 +248,7 @@ class MemoryStage(_TimedOps):
         self.res = dict(src=src, dst=dst, ts=ts, neg=neg, ef=ef)
         self.staged = False
         self.slots = [_Slot(self.cfg, self.memory.mail_stride, self.device, False, self.ws_bytes)
-                      for _ in range(self.cfg.k + 1)]
+                      for _ in range(self._nslots())]
 
     def bind_host(self, src, dst, ts, neg, ef):
         """e2e path: the stream in pinned host memory, one packed record per
@@ -273,7 +273,7 @@ class MemoryStage(_TimedOps):
                 view[: j1 - j0].copy_(torch.as_tensor(arrays[name][j0:j1]))
         self.host_rec = host
         self.staged = True
-        self.slots = [_Slot(cfg, self.memory.mail_stride, dev, False, self.ws_bytes) for _ in range(cfg.k + 1)]
+        self.slots = [_Slot(cfg, self.memory.mail_stride, dev, False, self.ws_bytes) for _ in range(self._nslots())]
         self.inp_ring = [torch.empty(rec_bytes, dtype=torch.uint8, device=dev) for _ in range(cfg.k + 2)]
         # result records: [num (16 B) | nodes 2B x 4 | h' 2B x M x 4]; the GEMM writes h' in place
         M = cfg.mem_dim
@@ -329,8 +329,13 @@ class MemoryStage(_TimedOps):
         _C.record_to_device(self.inp_ring[(i - 1) % (self.cfg.k + 2)], self.host_rec[i - 1])
 
     # -- ops ------------------------------------------------------------------
+    def _nslots(self):
+        """k + 1 snapshot slots in flight; with the training stage one more,
+        so prep(t+k+1) need not wait for train(t), which still reads slot t."""
+        return self.cfg.k + 1 + (1 if self.trainer is not None and self.cfg.k >= 1 else 0)
+
     def _slot(self, i):
-        return self.slots[(i - 1) % (self.cfg.k + 1)]
+        return self.slots[(i - 1) % len(self.slots)]
 
     def prep(self, i):
         """A1 sampler, A2 dedup, A3 fetch (+A4 mitigation) of batch i into its slot."""
@@ -519,6 +524,11 @@ class MemoryStage(_TimedOps):
                             upd["num"], sl.samp["nbr"], sl.samp["cnt"], cfg.fanout)
         self._ev("update_end")
         if self.trainer is not None:  # row F4: embeddings, loss, backward, (all-reduce,) SGD of batch i
+            # the next step's preps fork from here, not after the training step: MSPipe's
+            # fetch of later batches overlaps the training stage (Fig. pipeline (c))
+            ev = torch.cuda.Event()
+            ev.record()
+            self._after_commit = (ev, _C.capture_seq())
             self._ev("train")
             self.trainer.step(i, n, sl.samp, sl.mem, upd, sl.ws, sgd=cfg.train.get("sgd", True))
             self._ev("train_end")
@@ -653,7 +663,11 @@ class MemoryStage(_TimedOps):
                 # every prep goes to the side stream, in order (preps of one handle
                 # share its scratch); a commit of this group waits for its own prep
                 if not forked:
-                    self.side.wait_stream(main)
+                    ac = getattr(self, "_after_commit", None)
+                    if ac is not None and ac[1] == _C.capture_seq() and len(self.slots) > self.cfg.k + 1:
+                        self.side.wait_event(ac[0])  # the previous commit, not its training step
+                    else:
+                        self.side.wait_stream(main)
                     forked = True
                 with torch.cuda.stream(self.side):
                     self.prep(i)
