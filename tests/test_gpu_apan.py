@@ -91,7 +91,7 @@ def _compare(st, new, nb, tol=1e-4):
 
 
 @pytest.mark.parametrize("name,nb_,k", [("tiny", 50, 0), ("wiki", 15, 0), ("tiny", 30, 1), ("tiny", 30, 3),
-                                        ("wiki", 12, 2)])
+                                        ("wiki", 12, 2), ("gdelt", 6, 3)])
 def test_apan_stream_free_running(dev, name, nb_, k):
     """Free-running under the exact staleness schedule (k >= 1: two streams, one
     table set; the commit waits for the fetch and the APAN build of the later batch)."""
@@ -110,4 +110,5 @@ def test_apan_stream_free_running(dev, name, nb_, k):
     assert [st.versions[i] for i in range(1, nb_ + 1)] == [max(0, i - 1 - k) for i in range(1, nb_ + 1)]
     new, nb = oa.run_stream(cfg.num_nodes, src, dst, ts, ef, gp, ap, cfg.batch, fanout=cfg.fanout, k=k)
     _compare(st, new, nb, tol=1e-3)
-    assert int(st.apan.mb_cnt.max().item()) == oa.SLOTS  # some rings wrapped
+    if nb_ >= 12:
+        assert int(st.apan.mb_cnt.max().item()) == oa.SLOTS  # some rings wrapped

@@ -129,7 +129,8 @@ def test_sgd_updates_params_and_the_updater(dev):
 
 
 @pytest.mark.parametrize("name,k,nb,lr,tail", [("tiny", 0, 12, 1e-2, 0), ("tiny", 1, 12, 1e-2, 0),
-                                               ("wiki", 1, 8, 1e-3, 0), ("tiny", 2, 7, 1e-2, 123)])
+                                               ("wiki", 1, 8, 1e-3, 0), ("tiny", 2, 7, 1e-2, 123),
+                                               ("gdelt", 3, 5, 1e-3, 0)])
 def test_training_trajectory_matches_oracle(dev, name, k, nb, lr, tail):
     """Stage + training over nb batches with SGD (weights change every step,
     memory committed from the updated GRU): per-batch losses, final memory and
