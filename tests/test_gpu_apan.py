@@ -90,9 +90,11 @@ def _compare(st, new, nb, tol=1e-4):
     print(f"memory {dm:.1e}, mailbox rows {db:.1e}")
 
 
-@pytest.mark.parametrize("name,nb_,k", [("tiny", 50, 0), ("wiki", 15, 0), ("tiny", 30, 1), ("tiny", 30, 3),
-                                        ("wiki", 12, 2), ("gdelt", 6, 3)])
-def test_apan_stream_free_running(dev, name, nb_, k):
+@pytest.mark.parametrize("name,nb_,k,staged", [("tiny", 50, 0, False), ("wiki", 15, 0, False), ("tiny", 30, 1, False),
+                                               ("tiny", 30, 3, False), ("wiki", 12, 2, False), ("gdelt", 6, 3, False),
+                                               ("reddit", 10, 1, False), ("lastfm", 10, 1, False),
+                                               ("wiki", 10, 1, True)])
+def test_apan_stream_free_running(dev, name, nb_, k, staged):
     """Free-running under the exact staleness schedule (k >= 1: two streams, one
     table set; the commit waits for the fetch and the APAN build of the later batch)."""
     cfg = CONFIGS[name]
@@ -102,8 +104,11 @@ def test_apan_stream_free_running(dev, name, nb_, k):
     gp = gru_params(cfg.mem_dim, cfg.mail_dim, cfg.time_dim)
     ap = _weights(cfg.mem_dim, cfg.mail_dim)
     st, _ = _stage(dev, cfg, gp, ap, src, dst, ts, neg, ef, k=k)
-    t = {kk: _t(v, dev) for kk, v in dict(src=src, dst=dst, ts=ts, neg=neg, ef=ef).items()}
-    st.bind_resident(t["src"], t["dst"], t["ts"], t["neg"], t["ef"])
+    if staged:  # e2e: pinned host records
+        st.bind_host(src, dst, ts, neg, ef)
+    else:
+        t = {kk: _t(v, dev) for kk, v in dict(src=src, dst=dst, ts=ts, neg=neg, ef=ef).items()}
+        st.bind_resident(t["src"], t["dst"], t["ts"], t["neg"], t["ef"])
     st.run()
     torch.cuda.synchronize()
     _C.check()

@@ -128,10 +128,10 @@ def test_sgd_updates_params_and_the_updater(dev):
     assert np.all(np.abs(got - o["mem"]) <= 1e-4 * np.abs(o["mem"]) + 1e-6)
 
 
-@pytest.mark.parametrize("name,k,nb,lr,tail", [("tiny", 0, 12, 1e-2, 0), ("tiny", 1, 12, 1e-2, 0),
-                                               ("wiki", 1, 8, 1e-3, 0), ("tiny", 2, 7, 1e-2, 123),
-                                               ("gdelt", 3, 5, 1e-3, 0)])
-def test_training_trajectory_matches_oracle(dev, name, k, nb, lr, tail):
+@pytest.mark.parametrize("name,k,nb,lr,tail,staged", [("tiny", 0, 12, 1e-2, 0, False), ("tiny", 1, 12, 1e-2, 0, False),
+                                                      ("wiki", 1, 8, 1e-3, 0, False), ("tiny", 2, 7, 1e-2, 123, False),
+                                                      ("gdelt", 3, 5, 1e-3, 0, False), ("wiki", 1, 6, 1e-3, 0, True)])
+def test_training_trajectory_matches_oracle(dev, name, k, nb, lr, tail, staged):
     """Stage + training over nb batches with SGD (weights change every step,
     memory committed from the updated GRU): per-batch losses, final memory and
     final parameters against the oracle run in the same order (exact schedule:
@@ -146,8 +146,11 @@ def test_training_trajectory_matches_oracle(dev, name, k, nb, lr, tail):
     g = build_tcsr(cfg.num_nodes, src, dst, ts, dev)
     sc = StageConfig(cfg.num_nodes, M, cfg.edge_dim, cfg.time_dim, F, B, k, fused=True, train=dict(params=tp, lr=lr))
     st = MemoryStage(sc, gp, g, dev)
-    t = {kk: _t(v, dev) for kk, v in dict(src=src, dst=dst, ts=ts, neg=neg, ef=ef).items()}
-    st.bind_resident(t["src"], t["dst"], t["ts"], t["neg"], t["ef"])
+    if staged:  # e2e: inputs from pinned host records, results read back (the bench's e2e path)
+        st.bind_host(src, dst, ts, neg, ef)
+    else:
+        t = {kk: _t(v, dev) for kk, v in dict(src=src, dst=dst, ts=ts, neg=neg, ef=ef).items()}
+        st.bind_resident(t["src"], t["dst"], t["ts"], t["neg"], t["ef"])
     st.run()
     torch.cuda.synchronize()
     _C.check()
