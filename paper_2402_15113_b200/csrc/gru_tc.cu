@@ -695,8 +695,17 @@ constexpr bool kAsyncPush = MSPIPE_ASYNC_PUSH != 0;
 #endif
 constexpr bool kLocalPush = MSPIPE_LOCAL_PUSH != 0;
 
+// __launch_bounds__ without a min-blocks clause: ptxas then keeps k_gru_tc at 167
+// registers (213 with ", 1"), so a 256-thread k_build_x block (40 registers) of the
+// next batch fits beside the GEMM CTA in the SM's 64K-register file (the GEMM's
+// shared memory leaves room for it: k_build_x uses none).  -DMSPIPE_GEMM_MINB1: the old bound.
+#ifdef MSPIPE_GEMM_MINB1
+#define MSPIPE_GEMM_BOUNDS __launch_bounds__(tc::kThreads, 1)
+#else
+#define MSPIPE_GEMM_BOUNDS __launch_bounds__(tc::kThreads)
+#endif
 template <bool kBf>
-__global__ void __launch_bounds__(tc::kThreads, 1) k_gru_tc(TcArgs a) {
+__global__ void MSPIPE_GEMM_BOUNDS k_gru_tc(TcArgs a) {
   using namespace tc;
   constexpr int SB = kBf ? kStageBytes16 : kStageBytes;
   constexpr int AB = kBf ? kABlock16 : kABlock;
