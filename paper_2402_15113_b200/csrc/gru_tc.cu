@@ -698,9 +698,10 @@ constexpr bool kLocalPush = MSPIPE_LOCAL_PUSH != 0;
 // __launch_bounds__ without a min-blocks clause: ptxas then keeps k_gru_tc at 167
 // registers (213 with ", 1"), so a 256-thread k_build_x block (40 registers) of the
 // next batch fits beside the GEMM CTA in the SM's 64K-register file (the GEMM's
-// shared memory leaves room for it: k_build_x uses none).  -DMSPIPE_GEMM_MINB1: the old bound.
-#ifdef MSPIPE_GEMM_MINB1
-#define MSPIPE_GEMM_BOUNDS __launch_bounds__(tc::kThreads, 1)
+// shared memory leaves room for it: k_build_x uses none).  -DMSPIPE_GEMM_MINB=n: a
+// min-blocks bound of n (1: the old 213 registers; 2: 128 registers, small spills).
+#ifdef MSPIPE_GEMM_MINB
+#define MSPIPE_GEMM_BOUNDS __launch_bounds__(tc::kThreads, MSPIPE_GEMM_MINB)
 #else
 #define MSPIPE_GEMM_BOUNDS __launch_bounds__(tc::kThreads)
 #endif
