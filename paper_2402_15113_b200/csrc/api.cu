@@ -825,7 +825,10 @@ static mspipe_status apply_commit_impl(const mspipe_gru* gru, mspipe_memory* st,
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     // MSPIPE_WB_FIRST=0: the GEMM is enqueued before the write-back branch, so its
     // one-CTA-per-SM grid is dispatched before the branch's blocks fill the SMs
-    const bool wb_first = env_int("MSPIPE_WB_FIRST", 1) != 0;
+    // large batches: the write-back branch first (GDELT 100.5 vs 95.7 M events/s); small:
+    // the GEMM first, its 167-register CTAs leave room for the branch's blocks (wiki 36.9
+    // vs 36.0 M; r02zz6).  MSPIPE_WB_FIRST=0/1 forces it.
+    const bool wb_first = env_int("MSPIPE_WB_FIRST", max_n > 2048 ? 1 : 0) != 0;
     auto branch = [&]() -> cudaError_t {
       launch_writeback(nodes, num_unique, max_n, nullptr, new_ts, new_mail, 0, st->mail_stride, t.mem, t.mem_ts,
                        t.mail, t.mail_ts, st->num_nodes, side);

@@ -844,7 +844,7 @@ def test_degenerate_batches(dev):
 @pytest.mark.parametrize("env", [{"MSPIPE_SPLIT_COMMIT": "0"}, {"MSPIPE_SAMPLE_HINT": "0"},
                                  {"MSPIPE_TC_SPLITS": "1"}, {"MSPIPE_TC_SPLITS": "2"}, {"MSPIPE_TC_BIG_S": "4"},
                                  {"MSPIPE_PREP_SMEM": "0", "MSPIPE_PREP_BPS": "4"}, {"MSPIPE_BUILD_ROW": "1"}, {"MSPIPE_BUILD_CHUNKS": "2"}, {"MSPIPE_BUILD_CHUNKS": "4"},
-                                 {"MSPIPE_WB_FIRST": "0"}, {"MSPIPE_GRAPH_PRIO": "1"}, {"MSPIPE_PREP_STCS": "1"},
+                                 {"MSPIPE_WB_FIRST": "0"}, {"MSPIPE_WB_FIRST": "1"}, {"MSPIPE_GRAPH_PRIO": "1"}, {"MSPIPE_PREP_STCS": "1"},
                                  {"MSPIPE_TCSR_LDCS": "1"}, {"MSPIPE_TCSR_LDCS": "0", "MSPIPE_PREP_STCS": "0"}])
 def test_switch_variants_equal_oracle(dev, env, monkeypatch):
     """The library's experiment switches (read at every launch) keep the oracle's
